@@ -1,0 +1,119 @@
+/*
+ * ctm.h — C ABI of libctm: collapsed Taylor mode PDE operators of tanh MLPs on
+ * NVIDIA B200 (sm_100a).  arXiv 2505.13644 ("collapsed Taylor mode AD").
+ *
+ * The library computes, for a batch of N points x_n in R^D and an MLP
+ * f: R^D -> R (tanh on the hidden layers, affine output), the linear
+ * PDE operators of the paper by COLLAPSED Taylor mode (Eq. 7,
+ * `eq:faa-di-bruno-expanded`): every layer propagates the primal
+ * x_0, the first-order coefficients {x_{1,r}} (K=2) or {x_{1,j},x_{2,j},x_{3,j}}
+ * (K=4) and ONE summed top coefficient, so sum_r d^K f[v_r] is never
+ * materialised per direction.
+ *
+ * Conventions (all calls):
+ *  - Tensor pointers are DEVICE pointers on the handle's device, fp32,
+ *    row-major, contiguous, 16-byte aligned (else CTM_ESHAPE).
+ *  - Operator calls are ASYNCHRONOUS on `stream` (a cudaStream_t, NULL = the
+ *    legacy default stream); the caller synchronises. Inputs must stay valid
+ *    until the work on `stream` completes.
+ *  - A handle is not re-entrant: concurrent calls on one handle are undefined
+ *    (one handle per stream/thread). The handle owns a grow-only workspace.
+ *  - Errors are status codes; nothing is thrown or aborted. Arguments are
+ *    validated before any launch. N == 0 is a no-op returning CTM_OK.
+ *    ctm_last_error() gives a thread-local detail message.
+ *  - Results are bitwise deterministic run to run, and independent of how a
+ *    batch is split into calls (no reduction depends on N or on a point's
+ *    position; random directions are keyed on the global point index).
+ *  - Arithmetic: fp32 storage; the layer contractions run on tcgen05 tensor
+ *    cores as 3xTF32 (hi*hi + hi*lo + lo*hi, fp32 accumulation); the Taylor
+ *    rules run in fp32.  Accuracy target: |op - op_fp64| <= 1e-4 * sum_r
+ *    |c_r f_{K,r}|.
+ */
+#ifndef CTM_H
+#define CTM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ctm_mlp *ctm_mlp_t; /* opaque; owns device copies of the weights */
+
+typedef enum {
+    CTM_OK = 0,
+    CTM_EINVAL = 1,       /* NULL required pointer, negative size, bad enum      */
+    CTM_ESHAPE = 2,       /* width/D mismatch, misaligned pointer               */
+    CTM_ENOMEM = 3,       /* device allocation failed                           */
+    CTM_ECUDA = 4,        /* a CUDA runtime/driver call or a launch failed       */
+    CTM_EUNSUPPORTED = 5  /* slot count over the cap, non-scalar output, ...     */
+} ctm_status;
+
+typedef enum { CTM_RADEMACHER = 0, CTM_GAUSSIAN = 1 } ctm_dist;
+
+/* Load an MLP with n_layers affine layers (n_layers >= 2): tanh after layers
+ * 1..n_layers-1, affine output.
+ *   widths [n_layers+1] (HOST): widths[0] = D >= 1, widths[n_layers] = 1.
+ *   W [n_layers] (HOST array of DEVICE pointers): W_l is [w_l, w_{l-1}] (nn.Linear).
+ *   b [n_layers] (HOST array of DEVICE pointers): b_l is [w_l].
+ * The weights are copied (pre-split into tf32 hi/lo pairs, padded); the call
+ * synchronises the device before returning, so W and b may be freed after.
+ * Errors: CTM_EINVAL (NULL, n_layers < 2, width < 1), CTM_EUNSUPPORTED
+ * (widths[n_layers] != 1, hidden width > 8192), CTM_ECUDA, CTM_ENOMEM. */
+ctm_status ctm_load_mlp(int32_t n_layers, const int32_t *widths, const float *const *W,
+                        const float *const *b, int32_t device, ctm_mlp_t *out);
+
+/* Free a handle (NULL-safe). Synchronises the handle's device. */
+ctm_status ctm_free_mlp(ctm_mlp_t mlp);
+
+/* Exact Laplacian, Eq. 8 exact case: op[n] = sum_d <d^2 f(x_n), e_d^{(x)2}>.
+ *   X [N, D]; op_out [N]; f_out [N] or NULL (f(x_n)).
+ * Slots per point P = D + 2 (CTM_EUNSUPPORTED if P > 256). */
+ctm_status ctm_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
+                         void *stream);
+
+/* Weighted Laplacian, Eq. 10 exact case:
+ * op[n] = <d^2 f(x_n), sigma sigma^T> = sum_r <d^2 f, s_r^{(x)2}>,
+ *   sigma [D, R] (columns s_r; constant across points), R >= 1,
+ *   R + 2 <= 256. */
+ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma,
+                                  int32_t R, float *op_out, float *f_out, void *stream);
+
+/* Randomized (Hutchinson) Laplacian, Eq. 8/10 stochastic cases:
+ * op[n] = (1/S) sum_s <d^2 f(x_n), (sigma v_{n,s})^{(x)2}>, directions i.i.d. per
+ * point.
+ *   V [N, S, Rv] explicit directions, or NULL to generate Rademacher directions
+ *     in-kernel: v_{n,s,d} = sign from splitmix64(seed, ((point_offset+n)*S+s)*Rv+d)
+ *     (top bit set -> -1), SURVEY §8(c) O5. dist must be CTM_RADEMACHER when V
+ *     is NULL (Gaussian directions are passed explicitly).
+ *   point_offset: global index of X[0] (shard-invariant generation), >= 0.
+ *   sigma [D, Rv] or NULL (then Rv must equal D). 1 <= S, S + 2 <= 256. */
+ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S,
+                                    const float *V, ctm_dist dist, uint64_t seed,
+                                    int64_t point_offset, const float *sigma, int32_t Rv,
+                                    float *op_out, float *f_out, void *stream);
+
+/* Exact biharmonic, Eq. 12 exact case, by collapsed 4th-order Taylor
+ * mode through the interpolation family of Eq. `ttc_for_biharm_final`
+ * (gamma of Fig. 3): J = D(3D-1)/2 jets collapsed into
+ * ONE weighted top slot (P = 3J + 2 <= 256, i.e. D <= 7). */
+ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
+                          void *stream);
+
+/* Static message for a status. */
+const char *ctm_status_str(ctm_status s);
+
+/* Thread-local detail of the last error on this thread ("" if none). */
+const char *ctm_last_error(void);
+
+/* Introspection for tests/bench (HOST-side, no device work):
+ * number of kernel launches the last operator call on this handle issued,
+ * and the slot plan of the last call: P (slots per point), points per tile,
+ * MMA N of the hidden-layer GEMMs. */
+ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t *launches, int32_t *slots_per_point,
+                         int32_t *points_per_tile, int32_t *mma_n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTM_H */

@@ -1,0 +1,186 @@
+"""paper_2505_13644_b200 — collapsed Taylor mode PDE operators on B200 (arXiv 2505.13644).
+
+A thin ctypes binding of ``libctm.so`` (C ABI: ``include/ctm.h``). Argument
+marshalling only: every step of the hot path runs in the library's sm_100a
+kernels. PyTorch provides device memory and streams. There is no CPU fallback:
+if the CUDA library is missing or a call fails, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libctm.so")
+
+CTM_RADEMACHER, CTM_GAUSSIAN = 0, 1
+_STATUS = {0: "CTM_OK", 1: "CTM_EINVAL", 2: "CTM_ESHAPE", 3: "CTM_ENOMEM", 4: "CTM_ECUDA", 5: "CTM_EUNSUPPORTED"}
+
+# The C ABI (include/ctm.h): name -> (restype, argtypes)
+_VP, _I32, _I64, _U64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+ABI = {
+    "ctm_load_mlp": (ctypes.c_int, [_I32, _VP, _VP, _VP, _I32, ctypes.POINTER(_VP)]),
+    "ctm_free_mlp": (ctypes.c_int, [_VP]),
+    "ctm_laplacian": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_weighted_laplacian": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
+    "ctm_randomized_laplacian": (
+        ctypes.c_int,
+        [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _I32, _VP, _VP, _VP],
+    ),
+    "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+    "ctm_last_error": (ctypes.c_char_p, []),
+    "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
+                                     ctypes.POINTER(_I32)]),
+}
+
+_lib = None
+
+
+class CTMError(RuntimeError):
+    pass
+
+
+def lib() -> ctypes.CDLL:
+    """Load libctm.so (built in-tree by ``paper_2505_13644_b200.build``). Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CTMError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2505_13644_b200.build` "
+                "(there is no fallback path)"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in ABI.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        detail = lib().ctm_last_error().decode()
+        raise CTMError(f"{what} -> {_STATUS.get(status, status)}: {detail}")
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream], device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def _dev_f32(t: torch.Tensor, device, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    t = t.to(device=device, dtype=torch.float32).contiguous()
+    if t.data_ptr() % 16:
+        t = t.clone()
+    return t
+
+
+class MLP:
+    """A tanh MLP f: R^D -> R loaded into libctm (weights copied to the device).
+
+    params: sequence of (W_l [w_l, w_{l-1}], b_l [w_l]) as in ``torch.nn.Linear``;
+    tanh after every layer but the last.
+    """
+
+    def __init__(self, params: Sequence, device: int | str | torch.device | None = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        Ws = [_dev_f32(W, self.device, "W") for W, _ in params]
+        bs = [_dev_f32(b, self.device, "b").reshape(-1) for _, b in params]
+        widths = [Ws[0].shape[1]] + [W.shape[0] for W in Ws]
+        self.widths = widths
+        self.D = widths[0]
+        w_arr = (_I32 * len(widths))(*widths)
+        W_arr = (_VP * len(Ws))(*[W.data_ptr() for W in Ws])
+        b_arr = (_VP * len(bs))(*[b.data_ptr() for b in bs])
+        h = _VP()
+        _check(
+            lib().ctm_load_mlp(len(Ws), w_arr, W_arr, b_arr, self.device.index, ctypes.byref(h)), "ctm_load_mlp"
+        )
+        self._h = h
+
+    # ------------------------------------------------------------------ helpers
+    def _io(self, X, out, f_out, want_f):
+        X = _dev_f32(X, self.device, "X")
+        if X.dim() != 2 or X.shape[1] != self.D:
+            raise CTMError(f"X must be [N, {self.D}]")
+        N = X.shape[0]
+        if out is None:
+            out = torch.empty(N, device=self.device, dtype=torch.float32)
+        if f_out is None and want_f:
+            f_out = torch.empty(N, device=self.device, dtype=torch.float32)
+        return X, N, out, f_out
+
+    @staticmethod
+    def _p(t):
+        return None if t is None else t.data_ptr()
+
+    # ------------------------------------------------------------------ operators
+    def laplacian(self, X, out=None, f_out=None, want_f=True, stream=None):
+        """Exact Laplacian (Eq. 8). Returns (op [N], f [N] or None)."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        _check(lib().ctm_laplacian(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
+                                   _stream_ptr(stream, self.device)), "ctm_laplacian")
+        return out, f_out
+
+    def weighted_laplacian(self, X, sigma, out=None, f_out=None, want_f=True, stream=None):
+        """<d^2 f, sigma sigma^T> (Eq. 10), sigma [D, R]."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        sigma = _dev_f32(sigma, self.device, "sigma")
+        _check(lib().ctm_weighted_laplacian(self._h, X.data_ptr(), N, sigma.data_ptr(), sigma.shape[1],
+                                            out.data_ptr(), self._p(f_out), _stream_ptr(stream, self.device)),
+               "ctm_weighted_laplacian")
+        return out, f_out
+
+    def randomized_laplacian(self, X, S=None, V=None, seed=0, point_offset=0, sigma=None, dist="rademacher",
+                             out=None, f_out=None, want_f=True, stream=None):
+        """(1/S) sum_s <d^2 f, (sigma v_s)^2> (Eq. 8/10 stochastic). V [N, S, Rv] or generated."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        if V is not None:
+            V = _dev_f32(V, self.device, "V")
+            S, Rv = V.shape[1], V.shape[2]
+        if sigma is not None:
+            sigma = _dev_f32(sigma, self.device, "sigma")
+            Rv_s = sigma.shape[1]
+            Rv = Rv if V is not None else Rv_s
+        elif V is None:
+            Rv = self.D
+        if S is None:
+            raise CTMError("S is required when V is not given")
+        d = {"rademacher": CTM_RADEMACHER, "gaussian": CTM_GAUSSIAN}[dist]
+        _check(lib().ctm_randomized_laplacian(self._h, X.data_ptr(), N, int(S), self._p(V), d, int(seed) & (2**64 - 1),
+                                              int(point_offset), self._p(sigma), int(Rv), out.data_ptr(),
+                                              self._p(f_out), _stream_ptr(stream, self.device)),
+               "ctm_randomized_laplacian")
+        return out, f_out
+
+    def biharmonic(self, X, out=None, f_out=None, want_f=True, stream=None):
+        """Exact biharmonic (Eq. 12) via the interpolation family, one collapsed slot."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        _check(lib().ctm_biharmonic(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
+                                    _stream_ptr(stream, self.device)), "ctm_biharmonic")
+        return out, f_out
+
+    def last_plan(self) -> dict:
+        a, b, c, d = _I32(), _I32(), _I32(), _I32()
+        _check(lib().ctm_last_plan(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
+               "ctm_last_plan")
+        return {"launches": a.value, "slots_per_point": b.value, "points_per_tile": c.value, "mma_n": d.value}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ctm_free_mlp(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,603 @@
+// ctm.cu — libctm: the C ABI of include/ctm.h (collapsed Taylor mode on B200).
+//
+// Launch sequence of one operator call:
+//   [prep]  per-call direction matrix (weighted / randomized with sigma only)
+//   seed    layer 1: z0 = W1 x0 + b1, first-order coefficients, tanh Taylor rule  -> block B1
+//   layer   l = 2..L-1: fused tcgen05 3xTF32 GEMM + tanh Taylor epilogue            -> block B_l
+//           (the last hidden layer reduces straight against the output weights)
+//   final   op = c * (w_L . sum h_K), f = w_L . h0 + b_L
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ctm.h"
+#include "jet_layer.cuh"
+#include "seed.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ctm_status fail(ctm_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define CTM_CUDA(call)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? CTM_ENOMEM : CTM_ECUDA,                   \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D fp32 tensor map: inner dim `cols` (contiguous), outer `rows`; box {kBK, box_rows}; SWIZZLE_64B.
+bool make_map(CUtensorMap* m, const float* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)ctm::kBK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct ctm_mlp {
+  int device = 0;
+  int L = 0;                  // affine layers
+  std::vector<int> widths;    // L + 1
+  std::vector<int> wpad;      // hidden widths padded to 128 (index = layer)
+  // layer 1
+  float* W1T = nullptr;       // [D, wpad[1]]
+  float* b1 = nullptr;        // [wpad[1]]
+  // hidden GEMM layers l = 2..L-1 (index l-2)
+  std::vector<float*> Whi, Wlo, bias;
+  std::vector<CUtensorMap> mapA_hi, mapA_lo;
+  // output layer
+  float* w_out = nullptr;     // [wpad[L-1]]
+  float b_out = 0.f;
+  // fixed direction sets
+  float* U_lap = nullptr;     // [D, ld1]: z1 for e_d
+  float* c_lap = nullptr;     // [ld1]
+  float* U_bih = nullptr;     // [J, ld1]
+  float* c_bih = nullptr;     // [ld1]
+  float* w_bih = nullptr;     // [J] jet weights
+  int J_bih = 0;
+  // per-call scratch
+  float* U_call = nullptr;
+  float* c_call = nullptr;
+  size_t U_call_elems = 0;
+  // workspace: two ping-pong blocks (hi, lo)
+  float* blk[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  size_t blk_elems = 0;
+  float* partial = nullptr;
+  size_t partial_elems = 0;
+  // last plan
+  int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
+};
+
+namespace {
+
+ctm_status free_all(ctm_mlp* h) {
+  DeviceGuard g(h->device);
+  auto F = [](float*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  F(h->W1T); F(h->b1); F(h->w_out);
+  for (auto& p : h->Whi) F(p);
+  for (auto& p : h->Wlo) F(p);
+  for (auto& p : h->bias) F(p);
+  F(h->U_lap); F(h->c_lap); F(h->U_bih); F(h->c_bih); F(h->w_bih);
+  F(h->U_call); F(h->c_call);
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
+  F(h->partial);
+  return CTM_OK;
+}
+
+ctm_status ensure(float*& p, size_t& have, size_t need) {
+  if (need <= have && p) return CTM_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  have = 0;
+  CTM_CUDA(cudaMalloc(&p, std::max<size_t>(need, 1) * sizeof(float)));
+  have = need;
+  return CTM_OK;
+}
+
+ctm_status ensure_workspace(ctm_mlp* h, int64_t rows) {
+  int ldmax = 0;
+  for (int l = 1; l < h->L; ++l) ldmax = std::max(ldmax, h->wpad[l]);
+  const size_t need = (size_t)rows * ldmax;
+  if (need > h->blk_elems || !h->blk[0][0]) {
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) {
+        if (h->blk[i][j]) cudaFree(h->blk[i][j]);
+        h->blk[i][j] = nullptr;
+      }
+    h->blk_elems = 0;
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) CTM_CUDA(cudaMalloc(&h->blk[i][j], std::max<size_t>(need, 1) * sizeof(float)));
+    h->blk_elems = need;
+  }
+  return CTM_OK;
+}
+
+// The biharmonic direction family of Eq. `ttc_for_biharm_final` with the
+// gamma of Fig. 3 (g40 = 13/192, g31 = -1/3, g22 = 5/8), rescaled so the
+// directions are small integers:
+//   A: e_d           weight 4^4 (2D g40 + 2 g31 + g22)/24 = (13D - 4)/9
+//   B: 3 e_a + e_b   weight 2 g31 / 24               = -1/36      (a != b, a-major)
+//   C: e_a + e_b     weight 2^4 * 2 g22 / 24         = 5/6        (a < b,  a-major)
+void biharmonic_family(int D, std::vector<float>& dirs, std::vector<float>& w) {
+  const double g40 = 13.0 / 192.0, g31 = -1.0 / 3.0, g22 = 5.0 / 8.0;
+  const double wA = 256.0 * (2.0 * D * g40 + 2.0 * g31 + g22) / 24.0;
+  const double wB = 2.0 * g31 / 24.0;
+  const double wC = 16.0 * 2.0 * g22 / 24.0;
+  dirs.clear();
+  w.clear();
+  auto push = [&](int a, float va, int b, float vb, double wt) {
+    std::vector<float> v(D, 0.f);
+    v[a] += va;
+    if (b >= 0) v[b] += vb;
+    dirs.insert(dirs.end(), v.begin(), v.end());
+    w.push_back((float)wt);
+  };
+  for (int d = 0; d < D; ++d) push(d, 1.f, -1, 0.f, wA);
+  for (int a = 0; a < D; ++a)
+    for (int b = 0; b < D; ++b)
+      if (a != b) push(a, 3.f, b, 1.f, wB);
+  for (int a = 0; a < D; ++a)
+    for (int b = a + 1; b < D; ++b) push(a, 1.f, b, 1.f, wC);
+}
+
+bool g_smem_attr_set[2] = {false, false};
+
+template <int KORD>
+ctm_status set_layer_attr() {
+  if (!g_smem_attr_set[KORD == 4]) {
+    CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ctm::kLayerSmem));
+    g_smem_attr_set[KORD == 4] = true;
+  }
+  return CTM_OK;
+}
+
+struct Plan {
+  int P = 0, ppt = 0, nmma = 0;
+};
+
+Plan make_plan(int P) {
+  Plan pl;
+  pl.P = P;
+  int k = 1;
+  while (round_up((k + 1) * P, 16) <= ctm::kMaxN && k + 1 <= ctm::kMaxPtsPerTile) ++k;
+  pl.ppt = k;
+  pl.nmma = round_up(k * P, 16);
+  return pl;
+}
+
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH };
+
+struct CallArgs {
+  Op op;
+  const float* X;
+  int64_t N;
+  const float* sigma;
+  int R;
+  int S;
+  const float* V;
+  uint64_t seed;
+  int64_t point_offset;
+  int Rv;
+  float* op_out;
+  float* f_out;
+  cudaStream_t stream;
+};
+
+ctm_status run(ctm_mlp* h, const CallArgs& a) {
+  const int D = h->widths[0];
+  const int ld1 = h->wpad[1];
+  const int KORD = (a.op == OP_BIH) ? 4 : 2;
+  int P = 0;
+  switch (a.op) {
+    case OP_LAP: P = D + 2; break;
+    case OP_WLAP: P = a.R + 2; break;
+    case OP_RLAP: P = a.S + 2; break;
+    case OP_BIH: P = 3 * h->J_bih + 2; break;
+  }
+  if (P > ctm::kMaxN)
+    return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
+  const Plan pl = make_plan(P);
+  h->last_P = pl.P;
+  h->last_ppt = pl.ppt;
+  h->last_nmma = pl.nmma;
+  h->last_launches = 0;
+  if (a.N == 0) return CTM_OK;
+
+  DeviceGuard g(h->device);
+  cudaStream_t st = a.stream;
+  int launches = 0;
+  const int64_t rows = a.N * (int64_t)P;
+  if (rows > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "N * slots exceeds 2^31 rows");
+  ctm_status s = ensure_workspace(h, rows);
+  if (s != CTM_OK) return s;
+
+  // ---- per-call direction preparation
+  ctm::SeedParams sp{};
+  sp.X = a.X;
+  sp.D = D;
+  sp.n_points = a.N;
+  sp.W1T = h->W1T;
+  sp.b1 = h->b1;
+  sp.ld = ld1;
+  sp.P = P;
+  sp.out_hi = h->blk[0][0];
+  sp.out_lo = h->blk[0][1];
+  float scale = 1.f;
+  if (a.op == OP_LAP) {
+    sp.UT = h->U_lap;
+    sp.csum = h->c_lap;
+    sp.R = D;
+  } else if (a.op == OP_BIH) {
+    sp.UT = h->U_bih;
+    sp.csum = h->c_bih;
+    sp.R = h->J_bih;
+  } else if (a.op == OP_WLAP) {
+    s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
+    if (s != CTM_OK) return s;
+    if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
+    ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call, h->c_call);
+    ++launches;
+    sp.UT = h->U_call;
+    sp.csum = h->c_call;
+    sp.R = a.R;
+  } else {  // randomized
+    sp.random = 1;
+    sp.S = a.S;
+    sp.Rv = a.Rv;
+    sp.V = a.V;
+    sp.seed = a.seed;
+    sp.point_offset = a.point_offset;
+    if (a.sigma) {
+      s = ensure(h->U_call, h->U_call_elems, (size_t)a.Rv * ld1);
+      if (s != CTM_OK) return s;
+      ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.Rv, h->U_call, nullptr);
+      ++launches;
+      sp.AT = h->U_call;
+    } else {
+      sp.AT = h->W1T;  // v in R^D directly: A = W1
+    }
+    scale = 1.f / (float)a.S;
+  }
+
+  // ---- layer 1
+  {
+    const int mchunks = (ld1 + ctm::kSeedThreads - 1) / ctm::kSeedThreads;
+    const int64_t blocks = a.N * mchunks;
+    if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+    if (KORD == 2)
+      ctm::seed_layer_kernel<2><<<(unsigned)blocks, ctm::kSeedThreads, 0, st>>>(sp);
+    else
+      ctm::seed_layer_kernel<4><<<(unsigned)blocks, ctm::kSeedThreads, 0, st>>>(sp);
+    ++launches;
+  }
+
+  // ---- hidden layers 2..L-1
+  int cur = 0;
+  const int L = h->L;
+  if (L == 2) {
+    const int threads = 256, ppb = threads / 32;
+    ctm::readout_block_kernel<<<(unsigned)((a.N + ppb - 1) / ppb), threads, 0, st>>>(
+        h->blk[0][0], h->blk[0][1], ld1, P, h->widths[1], h->w_out, h->b_out, scale, a.N, a.op_out, a.f_out);
+    ++launches;
+  } else {
+    const int64_t n_tiles = (a.N + pl.ppt - 1) / pl.ppt;
+    for (int l = 2; l <= L - 1; ++l) {
+      const int i = l - 2;
+      const int kpad = h->wpad[l - 1];
+      const int mpad = h->wpad[l];
+      const int m_tiles = mpad / ctm::kBM;
+      const bool last = (l == L - 1);
+      CUtensorMap mb_hi, mb_lo;
+      if (!make_map(&mb_hi, h->blk[cur][0], (uint64_t)kpad, (uint64_t)rows, (uint32_t)pl.nmma) ||
+          !make_map(&mb_lo, h->blk[cur][1], (uint64_t)kpad, (uint64_t)rows, (uint32_t)pl.nmma))
+        return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
+      ctm::LayerParams lp{};
+      lp.bias = h->bias[i];
+      lp.out_hi = h->blk[cur ^ 1][0];
+      lp.out_lo = h->blk[cur ^ 1][1];
+      lp.ldo = mpad;
+      lp.m_tiles = m_tiles;
+      lp.n_points = a.N;
+      lp.P = P;
+      lp.pts_per_tile = pl.ppt;
+      lp.n_mma = pl.nmma;
+      lp.k_iters = kpad / ctm::kBK;
+      lp.jet_w = h->w_bih;
+      lp.J = h->J_bih;
+      if (last) {
+        s = ensure(h->partial, h->partial_elems, (size_t)a.N * m_tiles * 2);
+        if (s != CTM_OK) return s;
+        lp.readout = 1;
+        lp.w_out = h->w_out;
+        lp.partial = h->partial;
+      }
+      const int64_t grid = n_tiles * m_tiles;
+      if (grid > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+      if (KORD == 2) {
+        s = set_layer_attr<2>();
+        if (s != CTM_OK) return s;
+        ctm::jet_layer_kernel<2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
+            h->mapA_hi[i], h->mapA_lo[i], mb_hi, mb_lo, lp);
+      } else {
+        s = set_layer_attr<4>();
+        if (s != CTM_OK) return s;
+        ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
+            h->mapA_hi[i], h->mapA_lo[i], mb_hi, mb_lo, lp);
+      }
+      ++launches;
+      if (last) {
+        ctm::finalize_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, st>>>(h->partial, m_tiles, a.N, h->b_out,
+                                                                           scale, a.op_out, a.f_out);
+        ++launches;
+      }
+      cur ^= 1;
+    }
+  }
+  CTM_CUDA(cudaGetLastError());
+  h->last_launches = launches;
+  return CTM_OK;
+}
+
+ctm_status check_common(ctm_mlp* h, const float* X, int64_t N, float* op_out, float* f_out) {
+  if (!h) return fail(CTM_EINVAL, "NULL handle");
+  if (N < 0) return fail(CTM_EINVAL, "N < 0");
+  if (N > 0 && (!X || !op_out)) return fail(CTM_EINVAL, "NULL X or op_out");
+  if ((X && !aligned16(X)) || (op_out && !aligned16(op_out)) || (f_out && !aligned16(f_out)))
+    return fail(CTM_ESHAPE, "pointers must be 16-byte aligned");
+  return CTM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ctm_status_str(ctm_status s) {
+  switch (s) {
+    case CTM_OK: return "CTM_OK";
+    case CTM_EINVAL: return "CTM_EINVAL";
+    case CTM_ESHAPE: return "CTM_ESHAPE";
+    case CTM_ENOMEM: return "CTM_ENOMEM";
+    case CTM_ECUDA: return "CTM_ECUDA";
+    case CTM_EUNSUPPORTED: return "CTM_EUNSUPPORTED";
+  }
+  return "CTM_UNKNOWN";
+}
+
+const char* ctm_last_error(void) { return g_last_error.c_str(); }
+
+ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* const* W, const float* const* b,
+                        int32_t device, ctm_mlp_t* out) {
+  g_last_error.clear();
+  if (!out) return fail(CTM_EINVAL, "NULL out");
+  *out = nullptr;
+  if (n_layers < 2 || !widths || !W || !b) return fail(CTM_EINVAL, "need n_layers >= 2 and non-NULL widths/W/b");
+  for (int l = 0; l <= n_layers; ++l)
+    if (widths[l] < 1) return fail(CTM_EINVAL, "width < 1");
+  if (widths[n_layers] != 1) return fail(CTM_EUNSUPPORTED, "only scalar-output MLPs (widths[L] == 1)");
+  if (widths[0] > 256) return fail(CTM_EUNSUPPORTED, "input dimension D > 256");
+  for (int l = 1; l < n_layers; ++l)
+    if (widths[l] > 8192) return fail(CTM_EUNSUPPORTED, "hidden width > 8192");
+  for (int l = 0; l < n_layers; ++l)
+    if (!W[l] || !b[l] || !aligned16(W[l]) || !aligned16(b[l]))
+      return fail(W[l] && b[l] ? CTM_ESHAPE : CTM_EINVAL, "weights must be non-NULL and 16-byte aligned");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(CTM_ECUDA, "no such CUDA device");
+  if (!get_encode()) return fail(CTM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+
+  ctm_mlp* h = new ctm_mlp();
+  h->device = device;
+  h->L = n_layers;
+  h->widths.assign(widths, widths + n_layers + 1);
+  h->wpad.assign(n_layers + 1, 0);
+  for (int l = 1; l < n_layers; ++l) h->wpad[l] = round_up(widths[l], ctm::kBM);
+  DeviceGuard g(device);
+  const int D = widths[0], ld1 = h->wpad[1];
+  auto bail = [&](ctm_status s) {
+    free_all(h);
+    delete h;
+    return s;
+  };
+#define LOAD_CUDA(call)                                                                       \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      fail(e_ == cudaErrorMemoryAllocation ? CTM_ENOMEM : CTM_ECUDA,                          \
+           std::string(#call) + ": " + cudaGetErrorString(e_));                               \
+      return bail(e_ == cudaErrorMemoryAllocation ? CTM_ENOMEM : CTM_ECUDA);                  \
+    }                                                                                         \
+  } while (0)
+
+  // layer 1: transposed copy
+  LOAD_CUDA(cudaMalloc(&h->W1T, sizeof(float) * (size_t)D * ld1));
+  LOAD_CUDA(cudaMalloc(&h->b1, sizeof(float) * ld1));
+  {
+    const int64_t n = (int64_t)D * ld1;
+    ctm::transpose_w1_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[0], b[0], widths[1], D, ld1, h->W1T, h->b1);
+  }
+  // hidden GEMM layers
+  for (int l = 2; l <= n_layers - 1; ++l) {
+    const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
+    float *whi, *wlo, *bp;
+    LOAD_CUDA(cudaMalloc(&whi, sizeof(float) * (size_t)mpad * kpad));
+    h->Whi.push_back(whi);
+    LOAD_CUDA(cudaMalloc(&wlo, sizeof(float) * (size_t)mpad * kpad));
+    h->Wlo.push_back(wlo);
+    LOAD_CUDA(cudaMalloc(&bp, sizeof(float) * mpad));
+    h->bias.push_back(bp);
+    const int64_t n = (int64_t)mpad * kpad;
+    ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[l - 1], b[l - 1], widths[l], widths[l - 1],
+                                                                      mpad, kpad, whi, wlo, bp);
+    CUtensorMap mh, ml;
+    if (!make_map(&mh, whi, kpad, mpad, ctm::kBM) || !make_map(&ml, wlo, kpad, mpad, ctm::kBM)) {
+      fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for weights");
+      return bail(CTM_ECUDA);
+    }
+    h->mapA_hi.push_back(mh);
+    h->mapA_lo.push_back(ml);
+  }
+  // output layer
+  {
+    const int wl = widths[n_layers - 1], lpad = h->wpad[n_layers - 1];
+    LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * lpad));
+    ctm::pad_vector_kernel<<<(lpad + 255) / 256, 256>>>(W[n_layers - 1], wl, lpad, h->w_out);
+    LOAD_CUDA(cudaMemcpy(&h->b_out, b[n_layers - 1], sizeof(float), cudaMemcpyDeviceToHost));
+  }
+  // fixed direction sets: Laplacian (e_d) and, for D <= 7, the biharmonic family
+  {
+    std::vector<float> eye((size_t)D * D, 0.f);
+    for (int d = 0; d < D; ++d) eye[(size_t)d * D + d] = 1.f;
+    float* dd;
+    LOAD_CUDA(cudaMalloc(&dd, sizeof(float) * eye.size()));
+    LOAD_CUDA(cudaMemcpy(dd, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
+    LOAD_CUDA(cudaMalloc(&h->U_lap, sizeof(float) * (size_t)D * ld1));
+    LOAD_CUDA(cudaMalloc(&h->c_lap, sizeof(float) * ld1));
+    ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128>>>(h->W1T, D, ld1, dd, D, nullptr, 2, h->U_lap, h->c_lap);
+    LOAD_CUDA(cudaDeviceSynchronize());
+    cudaFree(dd);
+    if (3 * (D * (3 * D - 1) / 2) + 2 <= ctm::kMaxN) {
+      std::vector<float> dirs, w;
+      biharmonic_family(D, dirs, w);
+      h->J_bih = (int)w.size();
+      float* dv;
+      LOAD_CUDA(cudaMalloc(&dv, sizeof(float) * dirs.size()));
+      LOAD_CUDA(cudaMemcpy(dv, dirs.data(), sizeof(float) * dirs.size(), cudaMemcpyHostToDevice));
+      LOAD_CUDA(cudaMalloc(&h->w_bih, sizeof(float) * w.size()));
+      LOAD_CUDA(cudaMemcpy(h->w_bih, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice));
+      LOAD_CUDA(cudaMalloc(&h->U_bih, sizeof(float) * (size_t)h->J_bih * ld1));
+      LOAD_CUDA(cudaMalloc(&h->c_bih, sizeof(float) * ld1));
+      ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128>>>(h->W1T, D, ld1, dv, h->J_bih, h->w_bih, 4, h->U_bih,
+                                                              h->c_bih);
+      LOAD_CUDA(cudaDeviceSynchronize());
+      cudaFree(dv);
+    }
+  }
+  LOAD_CUDA(cudaGetLastError());
+  LOAD_CUDA(cudaDeviceSynchronize());
+#undef LOAD_CUDA
+  *out = h;
+  return CTM_OK;
+}
+
+ctm_status ctm_free_mlp(ctm_mlp_t mlp) {
+  if (!mlp) return CTM_OK;
+  {
+    DeviceGuard g(mlp->device);
+    cudaDeviceSynchronize();
+  }
+  free_all(mlp);
+  delete mlp;
+  return CTM_OK;
+}
+
+ctm_status ctm_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  CallArgs a{OP_LAP, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, const float* sigma, int32_t R,
+                                  float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (R < 1 || !sigma) return fail(CTM_EINVAL, "need sigma and R >= 1");
+  if (!aligned16(sigma)) return fail(CTM_ESHAPE, "sigma must be 16-byte aligned");
+  CallArgs a{OP_WLAP, X, N, sigma, R, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, int32_t S, const float* V,
+                                    ctm_dist dist, uint64_t seed, int64_t point_offset, const float* sigma,
+                                    int32_t Rv, float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (S < 1 || Rv < 1 || point_offset < 0) return fail(CTM_EINVAL, "need S >= 1, Rv >= 1, point_offset >= 0");
+  if (dist != CTM_RADEMACHER && dist != CTM_GAUSSIAN) return fail(CTM_EINVAL, "bad dist");
+  if (!V && dist != CTM_RADEMACHER)
+    return fail(CTM_EUNSUPPORTED, "in-kernel generation is Rademacher only; pass Gaussian directions as V");
+  if (!sigma && Rv != mlp->widths[0]) return fail(CTM_ESHAPE, "Rv must equal D when sigma is NULL");
+  if ((V && !aligned16(V)) || (sigma && !aligned16(sigma))) return fail(CTM_ESHAPE, "V/sigma must be 16-byte aligned");
+  if (Rv > ctm::kSeedChunk) return fail(CTM_EUNSUPPORTED, "Rv too large");
+  CallArgs a{OP_RLAP, X, N, sigma, 0, S, V, seed, point_offset, Rv, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (mlp->J_bih == 0)
+    return fail(CTM_EUNSUPPORTED, "biharmonic needs 3J+2 <= 256 slots, i.e. D <= 7");
+  CallArgs a{OP_BIH, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t* launches, int32_t* slots_per_point, int32_t* points_per_tile,
+                         int32_t* mma_n) {
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (launches) *launches = mlp->last_launches;
+  if (slots_per_point) *slots_per_point = mlp->last_P;
+  if (points_per_tile) *points_per_tile = mlp->last_ppt;
+  if (mma_n) *mma_n = mlp->last_nmma;
+  return CTM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,259 @@
+// jet_layer.cuh — one hidden layer of collapsed Taylor mode, fused:
+//
+//   Z^T[feature, slot] = W_l[feature, :] . B_{l-1}[slot, :]      (3xTF32, tcgen05, TMEM accumulator)
+//   B_l[slot, feature] = Taylor rule of tanh applied per point    (epilogue, registers)
+//
+// Swap-AB mapping: the MMA's M = 128 output features (one TMEM lane
+// each), N = the slots of `pts_per_tile` points (one TMEM column each). Each epilogue
+// thread owns one feature across all slots of a point, so the collapse
+// sum_r (...) over directions is a sequential in-register sum inside one thread:
+// X1 never round-trips HBM between the GEMM and the nonlinearity.
+//
+// K=2 epilogue (Eq. 1 P:327 + Eq. 7, Eq. D4):
+//   h0 = tanh z0, h1_r = s' z1_r, sum h2 = s' sum z2 + s'' sum_r z1_r^2
+// K=4 epilogue (cheat-sheet rows for k<=4, collapsed by Eq. 7):
+//   h1 = s'z1, h2 = s''z1^2 + s'z2, h3 = s'''z1^3 + 3s''z1z2 + s'z3,
+//   sum_w h4 = sum_j w_j (s''''z1^4 + 6s'''z1^2z2 + 4s''z1z3 + 3s''z2^2) + s' sum_w z4
+//
+// Layout in HBM: block B_l is [N*P rows, ld] fp32, row = n*P + slot,
+// stored as a tf32 pair (hi = rna_tf32(v), lo = v - hi) so that hi*hi + hi*lo + lo*hi
+// on the tensor cores reproduces fp32-accurate products.
+#pragma once
+#include "ptx.cuh"
+
+namespace ctm {
+
+constexpr int kBM = 128;                         // features per tile = TMEM lanes
+constexpr int kBK = 16;                          // fp32 K per stage: 64-byte rows, SWIZZLE_64B
+constexpr int kStages = 4;
+constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
+constexpr int kATileBytes = kBM * kBK * 4;       // 8 KB
+constexpr int kBTileBytes = kMaxN * kBK * 4;     // 16 KB
+constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
+constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
+constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
+constexpr int kLayerThreads = 192;               // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
+                           4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxJets * 4;
+constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
+constexpr uint32_t kSw64 = 4;                    // descriptor layout code for SWIZZLE_64B
+
+struct LayerParams {
+  const float* bias;      // [Mpad]
+  float* out_hi;          // [rows, ldo]
+  float* out_lo;
+  int ldo;
+  int m_tiles;
+  int64_t n_points;
+  int P;                  // slots per point
+  int pts_per_tile;
+  int n_mma;              // MMA N, multiple of 16, <= 256
+  int k_iters;            // Kpad / kBK
+  const float* jet_w;     // K=4: weights of the J jets in the collapsed slot
+  int J;
+  int readout;            // last hidden layer: reduce against w_out instead of storing
+  const float* w_out;     // [Mpad] output-layer weights (zero padded)
+  float* partial;         // [n_points, m_tiles, 2]
+};
+
+__device__ __forceinline__ void store_pair(float* hi, float* lo, size_t idx, float v) {
+  const float h = ptx::tf32_rna(v);
+  hi[idx] = h;
+  lo[idx] = v - h;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int KORD>
+__global__ void __launch_bounds__(kLayerThreads, 1)
+    jet_layer_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
+                     const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
+                     const LayerParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tmem_full_bar = empty_bar + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full_bar + 1);
+  float* red = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [4][kMaxPtsPerTile][2]
+  float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_tile = blockIdx.x % p.m_tiles;
+  const int n_tile = blockIdx.x / p.m_tiles;
+  const int64_t row0 = (int64_t)n_tile * p.pts_per_tile * p.P;  // first slot row of the tile
+  const uint32_t b_bytes = (uint32_t)p.n_mma * kBK * 4;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA_hi);
+    ptx::tma_prefetch_desc(&tmA_lo);
+    ptx::tma_prefetch_desc(&tmB_hi);
+    ptx::tma_prefetch_desc(&tmB_lo);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    ptx::mbar_init(tmem_full_bar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (KORD == 4)
+    for (int j = threadIdx.x; j < p.J; j += blockDim.x) jw[j] = p.jet_w[j];
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const int m0 = m_tile * kBM;
+      for (int kb = 0; kb < p.k_iters; ++kb) {
+        const int s = kb % kStages;
+        const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+        ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
+        uint8_t* st = smem + s * kStageBytes;
+        ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * kATileBytes + 2u * b_bytes);
+        const int k0 = kb * kBK;
+        ptx::tma_load_2d(st, &tmA_hi, &full_bar[s], k0, m0);
+        ptx::tma_load_2d(st + kATileBytes, &tmA_lo, &full_bar[s], k0, m0);
+        ptx::tma_load_2d(st + 2 * kATileBytes, &tmB_hi, &full_bar[s], k0, (int32_t)row0);
+        ptx::tma_load_2d(st + 2 * kATileBytes + kBTileBytes, &tmB_lo, &full_bar[s], k0, (int32_t)row0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_tf32(kBM, (uint32_t)p.n_mma);
+      for (int kb = 0; kb < p.k_iters; ++kb) {
+        const int s = kb % kStages;
+        const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+        ptx::mbar_wait(&full_bar[s], ph);
+        ptx::tc_fence_after();
+        const uint32_t a_hi = ptx::smem_u32(smem + s * kStageBytes);
+        const uint32_t a_lo = a_hi + kATileBytes;
+        const uint32_t b_hi = a_hi + 2 * kATileBytes;
+        const uint32_t b_lo = b_hi + kBTileBytes;
+#pragma unroll
+        for (int ks = 0; ks < kBK / 8; ++ks) {  // tf32 MMA K = 8 (32 bytes)
+          const uint32_t off = ks * 32;
+          const uint64_t dah = ptx::smem_desc_kmajor(a_hi + off, 512, kSw64);
+          const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, 512, kSw64);
+          const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, 512, kSw64);
+          const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, 512, kSw64);
+          ptx::mma_tf32(tmem_base, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
+          ptx::mma_tf32(tmem_base, dah, dbl, idesc, 1u);               // hi * lo
+          ptx::mma_tf32(tmem_base, dah, dbh, idesc, 1u);               // hi * hi
+        }
+        ptx::mma_commit(&empty_bar[s]);  // stage free once these MMAs retire
+      }
+      ptx::mma_commit(tmem_full_bar);    // accumulator complete
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;                      // TMEM lane quadrant of this warp
+    const int m_local = q * 32 + lane;
+    const int m = m_tile * kBM + m_local;
+    const float bias = p.bias[m];
+    const float wo = p.readout ? p.w_out[m] : 0.f;
+    const int64_t pts_left = p.n_points - (int64_t)n_tile * p.pts_per_tile;
+    const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
+    const int ncols = npts * p.P;
+    ptx::mbar_wait(tmem_full_bar, 0);
+    ptx::tc_fence_after();
+    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
+
+    int slot = 0, pt = 0;
+    float d1 = 0.f, d2 = 0.f, d3 = 0.f, d4 = 0.f, acc = 0.f;  // acc: sum over directions
+    float z1 = 0.f, z2 = 0.f;                                // K=4 jet state
+    int jj = 0;
+    for (int c0 = 0; c0 < ncols; c0 += 16) {
+      float v[16];
+      ptx::tmem_ld16(taddr + (uint32_t)c0, v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = c0 + i;
+        if (c >= ncols) break;
+        const size_t oidx = (size_t)(row0 + c) * p.ldo + m;
+        float z = v[i];
+        if (slot == 0) {
+          z += bias;  // the bias enters the primal only (affine rule)
+          const float t = tanhf(z);
+          d1 = 1.f - t * t;          // tanh'
+          d2 = -2.f * t * d1;        // tanh''
+          if (KORD == 4) {
+            d3 = d1 * (6.f * t * t - 2.f);        // tanh'''
+            d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
+          }
+          acc = 0.f;
+          jj = 0;
+          if (p.readout) {
+            const float s = warp_sum(wo * t);
+            if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 0] = s;
+          } else {
+            store_pair(p.out_hi, p.out_lo, oidx, t);
+          }
+        } else if (slot == p.P - 1) {
+          const float top = d1 * z + (KORD == 2 ? d2 * acc : acc);  // <dh, sum z_K> + collapsed rest
+          if (p.readout) {
+            const float s = warp_sum(wo * top);
+            if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 1] = s;
+          } else {
+            store_pair(p.out_hi, p.out_lo, oidx, top);
+          }
+        } else {
+          float h;
+          if (KORD == 2) {
+            h = d1 * z;          // h_{1,r} = tanh' z_{1,r}
+            acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
+          } else {
+            const int which = (slot - 1) % 3;  // 0: z1, 1: z2, 2: z3 of jet jj
+            if (which == 0) {
+              z1 = z;
+              h = d1 * z1;
+            } else if (which == 1) {
+              z2 = z;
+              h = d2 * z1 * z1 + d1 * z2;
+            } else {
+              const float z3 = z;
+              h = d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3;
+              const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 +
+                               3.f * d2 * z2 * z2;
+              acc = fmaf(jw[jj], nl, acc);
+              ++jj;
+            }
+          }
+          if (!p.readout) store_pair(p.out_hi, p.out_lo, oidx, h);
+        }
+        if (++slot == p.P) {
+          slot = 0;
+          ++pt;
+        }
+      }
+    }
+    if (p.readout) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps only
+      for (int j = threadIdx.x - 64; j < npts * 2; j += 128) {
+        const int pj = j >> 1, comp = j & 1;
+        const float s = red[(0 * kMaxPtsPerTile + pj) * 2 + comp] + red[(1 * kMaxPtsPerTile + pj) * 2 + comp] +
+                        red[(2 * kMaxPtsPerTile + pj) * 2 + comp] + red[(3 * kMaxPtsPerTile + pj) * 2 + comp];
+        const int64_t n = (int64_t)n_tile * p.pts_per_tile + pj;
+        p.partial[(n * p.m_tiles + m_tile) * 2 + comp] = s;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace ctm

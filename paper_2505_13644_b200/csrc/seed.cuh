@@ -1,0 +1,233 @@
+// seed.cuh — layer 1 of the collapsed jet (steps a1 + a2 + a3 of SURVEY §8(a)),
+// the per-call direction preparation, and the readout (a5).
+//
+// Layer 1 is tiny in K (K = D) and needs no tensor cores: z0 = W1 x0 + b1 is a
+// D-term dot product per feature; for FIXED direction sets the first-order
+// coefficients z_{1,r} = (W1 V)[:, r] are the same for every point and are
+// precomputed once (U^T [R, ld]); for RANDOM directions z_{1,s} = A v_{n,s} with
+// A = W1 (or W1 sigma) and v_{n,s} generated in-kernel (Rademacher, splitmix64)
+// or read from V. The kernel is bound by the HBM write of the layer-1 block.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace ctm {
+
+constexpr int kSeedThreads = 256;
+constexpr int kSeedChunk = 4096;  // floats of directions staged in smem per pass
+
+// splitmix64 finaliser of seed + (idx+1) * golden gamma
+__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t idx) {
+  uint64_t z = seed + (idx + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct SeedParams {
+  const float* X;        // [N, D]
+  int D;
+  int64_t n_points;
+  const float* W1T;      // [D, ld]   (W1 transposed, zero padded columns)
+  const float* b1;       // [ld]
+  int ld;                // padded width of layer 1 (= output ld)
+  int P;
+  // FIXED directions: z1_r = UT[r, m], csum[m] = sum_r z1^2 (K=2) or sum_j w_j z1^4 (K=4)
+  const float* UT;       // [R, ld]
+  const float* csum;     // [ld]
+  int R;                 // K=2: number of directions; K=4: number of jets J
+  // RANDOM directions (K=2 only): z1_s = sum_r AT[r, m] v[n, s, r]
+  int random;
+  const float* AT;       // [Rv, ld]
+  int Rv;
+  int S;
+  const float* V;        // [N, S, Rv] or nullptr => Rademacher(seed, point_offset + n)
+  uint64_t seed;
+  int64_t point_offset;
+  float* out_hi;         // [N*P, ld]
+  float* out_lo;
+};
+
+__device__ __forceinline__ void seed_store(float* hi, float* lo, size_t idx, float v) {
+  const float h = ptx::tf32_rna(v);
+  hi[idx] = h;
+  lo[idx] = v - h;
+}
+
+// grid: one block per (point, 256-feature chunk); one thread per feature.
+template <int KORD>
+__global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedParams p) {
+  __shared__ float xs[256];
+  __shared__ float vs[kSeedChunk];
+  const int mchunks = (p.ld + kSeedThreads - 1) / kSeedThreads;
+  const int64_t n = blockIdx.x / mchunks;
+  const int m = (blockIdx.x % mchunks) * kSeedThreads + threadIdx.x;
+  for (int d = threadIdx.x; d < p.D; d += blockDim.x) xs[d] = p.X[n * p.D + d];
+  __syncthreads();
+  const bool active = m < p.ld;
+  const size_t row0 = (size_t)n * p.P;
+  float t = 0.f, d1 = 0.f, d2 = 0.f;
+  if (active) {
+    float z0 = p.b1[m];
+    for (int d = 0; d < p.D; ++d) z0 = fmaf(p.W1T[(size_t)d * p.ld + m], xs[d], z0);
+    t = tanhf(z0);
+    d1 = 1.f - t * t;    // tanh'
+    d2 = -2.f * t * d1;  // tanh''
+    seed_store(p.out_hi, p.out_lo, row0 * p.ld + m, t);
+  }
+  if (!p.random) {
+    if (!active) return;
+    if (KORD == 2) {
+      for (int r = 0; r < p.R; ++r)
+        seed_store(p.out_hi, p.out_lo, (row0 + 1 + r) * p.ld + m, d1 * p.UT[(size_t)r * p.ld + m]);
+      // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
+      seed_store(p.out_hi, p.out_lo, (row0 + 1 + p.R) * p.ld + m, d2 * p.csum[m]);
+    } else {
+      const float d3 = d1 * (6.f * t * t - 2.f), d4 = 8.f * t * d1 * (2.f - 3.f * t * t);
+      for (int j = 0; j < p.R; ++j) {
+        const float z1 = p.UT[(size_t)j * p.ld + m];
+        const size_t r = row0 + 1 + 3 * j;
+        seed_store(p.out_hi, p.out_lo, r * p.ld + m, d1 * z1);                  // h1
+        seed_store(p.out_hi, p.out_lo, (r + 1) * p.ld + m, d2 * z1 * z1);       // h2 (z2 = 0)
+        seed_store(p.out_hi, p.out_lo, (r + 2) * p.ld + m, d3 * z1 * z1 * z1);  // h3 (z2 = z3 = 0)
+      }
+      // sum_w h4 = tanh'''' * sum_j w_j z1_j^4   (z2 = z3 = z4 = 0)
+      seed_store(p.out_hi, p.out_lo, (row0 + 1 + 3 * p.R) * p.ld + m, d4 * p.csum[m]);
+    }
+    return;
+  }
+  // randomized (K=2): per-point directions, staged in smem a chunk at a time
+  const int per_chunk = kSeedChunk / p.Rv;
+  float sumsq = 0.f;
+  for (int s0 = 0; s0 < p.S; s0 += per_chunk) {
+    const int ns = (p.S - s0 < per_chunk) ? (p.S - s0) : per_chunk;
+    __syncthreads();
+    for (int e = threadIdx.x; e < ns * p.Rv; e += blockDim.x) {
+      const int s = s0 + e / p.Rv, r = e % p.Rv;
+      float v;
+      if (p.V) {
+        v = p.V[((size_t)n * p.S + s) * p.Rv + r];
+      } else {
+        const uint64_t idx =
+            ((uint64_t)(p.point_offset + n) * (uint64_t)p.S + (uint64_t)s) * (uint64_t)p.Rv + (uint64_t)r;
+        v = (splitmix64(p.seed, idx) >> 63) ? -1.f : 1.f;
+      }
+      vs[e] = v;
+    }
+    __syncthreads();
+    if (active) {
+      for (int s = 0; s < ns; ++s) {
+        float z1 = 0.f;
+        for (int r = 0; r < p.Rv; ++r) z1 = fmaf(p.AT[(size_t)r * p.ld + m], vs[s * p.Rv + r], z1);
+        seed_store(p.out_hi, p.out_lo, (row0 + 1 + s0 + s) * p.ld + m, d1 * z1);
+        sumsq = fmaf(z1, z1, sumsq);
+      }
+    }
+  }
+  if (active) seed_store(p.out_hi, p.out_lo, (row0 + 1 + p.S) * p.ld + m, d2 * sumsq);
+}
+
+// UT[r, m] = sum_d W1T[d, m] dirs[r, d]; csum[m] = sum_r w_r UT[r, m]^pow (pow 2 or 4).
+// dirs is [R, D] (device), w is [R] or nullptr (all ones). One thread per feature.
+__global__ void prep_directions_kernel(const float* __restrict__ W1T, int D, int ld, const float* __restrict__ dirs,
+                                       int R, const float* __restrict__ w, int pow, float* __restrict__ UT,
+                                       float* __restrict__ csum) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= ld) return;
+  float cs = 0.f;
+  for (int r = 0; r < R; ++r) {
+    float u = 0.f;
+    for (int d = 0; d < D; ++d) u = fmaf(W1T[(size_t)d * ld + m], dirs[(size_t)r * D + d], u);
+    UT[(size_t)r * ld + m] = u;
+    const float u2 = u * u;
+    cs = fmaf(w ? w[r] : 1.f, pow == 2 ? u2 : u2 * u2, cs);
+  }
+  if (csum) csum[m] = cs;
+}
+
+// AT[r, m] = sum_d W1T[d, m] sigma[d, r]  (sigma [D, R] row-major)
+__global__ void prep_sigma_kernel(const float* __restrict__ W1T, int D, int ld, const float* __restrict__ sigma,
+                                  int R, float* __restrict__ AT, float* __restrict__ csum) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= ld) return;
+  float cs = 0.f;
+  for (int r = 0; r < R; ++r) {
+    float u = 0.f;
+    for (int d = 0; d < D; ++d) u = fmaf(W1T[(size_t)d * ld + m], sigma[(size_t)d * R + r], u);
+    AT[(size_t)r * ld + m] = u;
+    cs = fmaf(u, u, cs);
+  }
+  if (csum) csum[m] = cs;
+}
+
+// op[n] = scale * sum_t partial[n, t, 1];  f[n] = b_out + sum_t partial[n, t, 0]   (fixed order)
+__global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, int64_t N, float b_out, float scale,
+                                float* __restrict__ op, float* __restrict__ f) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s0 = 0.f, s1 = 0.f;
+  for (int t = 0; t < m_tiles; ++t) {
+    s0 += partial[(n * m_tiles + t) * 2 + 0];
+    s1 += partial[(n * m_tiles + t) * 2 + 1];
+  }
+  op[n] = scale * s1;
+  if (f) f[n] = b_out + s0;
+}
+
+// Readout straight from a layer block (nets with a single hidden layer):
+// one warp per point, lanes over features.
+__global__ void readout_block_kernel(const float* __restrict__ hi, const float* __restrict__ lo, int ld, int P,
+                                     int width, const float* __restrict__ w_out, float b_out, float scale,
+                                     int64_t N, float* __restrict__ op, float* __restrict__ f) {
+  const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  const size_t r0 = (size_t)n * P * ld, rt = ((size_t)n * P + P - 1) * ld;
+  float s0 = 0.f, s1 = 0.f;
+  for (int m = lane; m < width; m += 32) {
+    s0 = fmaf(w_out[m], hi[r0 + m] + lo[r0 + m], s0);
+    s1 = fmaf(w_out[m], hi[rt + m] + lo[rt + m], s1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if (lane == 0) {
+    op[n] = scale * s1;
+    if (f) f[n] = b_out + s0;
+  }
+}
+
+// Split W [rows, cols] (row-major, device) into padded tf32 pairs [Mpad, Kpad];
+// bias into [Mpad]. Padding is zero.
+__global__ void split_weights_kernel(const float* __restrict__ W, const float* __restrict__ b, int rows, int cols,
+                                     int Mpad, int Kpad, float* __restrict__ Whi, float* __restrict__ Wlo,
+                                     float* __restrict__ bpad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)Mpad * Kpad) return;
+  const int r = (int)(i / Kpad), c = (int)(i % Kpad);
+  const float v = (r < rows && c < cols) ? W[(size_t)r * cols + c] : 0.f;
+  const float h = ptx::tf32_rna(v);
+  Whi[i] = h;
+  Wlo[i] = v - h;
+  if (c == 0) bpad[r] = (r < rows) ? b[r] : 0.f;
+}
+
+// W1T [D, ld] = W1^T zero padded; b1 [ld]
+__global__ void transpose_w1_kernel(const float* __restrict__ W1, const float* __restrict__ b1, int w1, int D, int ld,
+                                    float* __restrict__ W1T, float* __restrict__ b1p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)D * ld) return;
+  const int d = (int)(i / ld), m = (int)(i % ld);
+  W1T[i] = (m < w1) ? W1[(size_t)m * D + d] : 0.f;
+  if (d == 0) b1p[m] = (m < w1) ? b1[m] : 0.f;
+}
+
+__global__ void pad_vector_kernel(const float* __restrict__ src, int n, int npad, float* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < npad) dst[i] = (i < n) ? src[i] : 0.f;
+}
+
+}  // namespace ctm

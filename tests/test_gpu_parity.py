@@ -1,0 +1,240 @@
+"""GPU parity: libctm (sm_100a, through the C ABI) vs the fp64 oracle, element by
+element on identical seeded inputs (the fp32 values handed to the GPU, upcast).
+
+Metric (north_star): per point
+    |op_gpu - op_oracle| / sum_r |c_r f_{K,r}|  <= 1e-4
+with the normaliser from the oracle's vanilla route (O1).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gaussian_directions, mlp_params, points, sigma as make_sigma, widths_for
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+C1_WIDTHS = widths_for(50)  # 50 -> 768 -> 768 -> 512 -> 512 -> 1
+C4_WIDTHS = widths_for(5)
+
+
+@pytest.fixture(scope="module")
+def ctm():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2505_13644_b200 as ctm
+
+    ctm.lib()
+    return ctm
+
+
+_cache = {}
+
+
+def nets(widths, seed=0):
+    key = (tuple(widths), seed)
+    if key not in _cache:
+        params = mlp_params(widths, seed)
+        _cache[key] = (params, O.Net([W.astype(np.float64) for W, _ in params],
+                                     [b.astype(np.float64) for _, b in params], "tanh"))
+    return _cache[key]
+
+
+def gpu_mlp(ctm, params):
+    return ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0)
+
+
+ERRORS = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dump_errors():
+    yield
+    import json
+    import os
+
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if ERRORS and os.path.isdir(out):
+        with open(os.path.join(out, "parity_errors.json"), "w") as fh:
+            json.dump(ERRORS, fh, indent=1, sort_keys=True)
+
+
+def check(got, want, norm, fgot=None, fwant=None, tol=TOL):
+    got = got.double().cpu().numpy() if isinstance(got, torch.Tensor) else got
+    err = np.abs(got - want) / norm
+    ERRORS[os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0] + f"#{len(ERRORS)}"] = {
+        "max_norm_err": float(err.max()), "n": int(err.size), "max_abs_op": float(np.abs(want).max())}
+    assert np.all(np.isfinite(got))
+    assert err.max() <= tol, f"max normalised error {err.max():.3e} at point {err.argmax()}"
+    if fgot is not None:
+        fgot = fgot.double().cpu().numpy()
+        ferr = np.abs(fgot - fwant) / np.maximum(1.0, np.abs(fwant))
+        assert ferr.max() <= 1e-5, f"f error {ferr.max():.3e}"
+    return err.max()
+
+
+# ------------------------------------------------------------------ exact Laplacian
+@pytest.mark.parametrize("widths,N", [
+    ([2, 2, 1], 3),                 # single hidden layer (readout straight from the block)
+    ([5, 16, 16, 1], 8),            # BASELINE config C0 shape
+    ([50, 128, 96, 1], 37),         # ragged tail, padded widths
+    (C1_WIDTHS, 203),               # C1 net: 51 tiles of 4 points, ragged last tile
+])
+def test_laplacian_parity(ctm, widths, N):
+    params, onet = nets(widths)
+    X = points(N, widths[0])
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.laplacian(torch.from_numpy(X).cuda())
+    torch.cuda.synchronize()
+    want, fwant, norm = O.laplacian(onet, X.astype(np.float64), O.O1)
+    check(op, want, norm, f, fwant)
+
+
+def test_golden_g1_net(ctm):
+    # W1 = [[.5,-.25],[.3,.8]], b1 = [.1,-.2], w2 = [1.5,-.7], b2 = .05
+    params = [(np.array([[0.5, -0.25], [0.3, 0.8]], np.float32), np.array([0.1, -0.2], np.float32)),
+              (np.array([[1.5, -0.7]], np.float32), np.array([0.05], np.float32))]
+    onet = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params])
+    X = np.array([[0.2, -0.4]], np.float32)
+    sig = np.array([[1.0, 0.5], [0.0, 2.0]], np.float32)
+    mlp = gpu_mlp(ctm, params)
+    Xc = torch.from_numpy(X).cuda()
+    want, fw, norm = O.laplacian(onet, X.astype(np.float64))
+    op, f = mlp.laplacian(Xc)
+    check(op, want, norm, f, fw)
+    want, _, norm = O.weighted_laplacian(onet, X.astype(np.float64), sig.astype(np.float64))
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
+    want, _, norm = O.biharmonic(onet, X.astype(np.float64))
+    check(mlp.biharmonic(Xc)[0], want, norm)
+
+
+# ------------------------------------------------------------------ weighted
+@pytest.mark.parametrize("kind,R", [("dense", 50), ("diag", 50), ("rect", 20)])
+def test_weighted_parity(ctm, kind, R):
+    params, onet = nets(C1_WIDTHS)
+    N = 29
+    X = points(N, 50)
+    sig = make_sigma(50, R, kind=kind)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.weighted_laplacian(torch.from_numpy(X).cuda(), torch.from_numpy(sig).cuda())
+    want, fwant, norm = O.weighted_laplacian(onet, X.astype(np.float64), sig.astype(np.float64))
+    check(op, want, norm, f, fwant)
+
+
+def test_weighted_identity_is_laplacian_bitwise(ctm):
+    params, _ = nets([5, 16, 16, 1])
+    X = torch.from_numpy(points(40, 5)).cuda()
+    mlp = gpu_mlp(ctm, params)
+    a = mlp.laplacian(X)[0].clone()
+    b = mlp.weighted_laplacian(X, torch.eye(5).cuda())[0]
+    # same code path up to U = W1 I computed once at load vs per call: equal to rounding
+    np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-6, atol=1e-6)
+
+
+# ------------------------------------------------------------------ randomized
+@pytest.mark.parametrize("S", [8, 32, 128])
+def test_randomized_rademacher_generated(ctm, S):
+    params, onet = nets(C1_WIDTHS)
+    N, seed, off = 19, 1234, 77
+    X = points(N, 50)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.randomized_laplacian(torch.from_numpy(X).cuda(), S=S, seed=seed, point_offset=off)
+    V = O.rademacher(seed, off, N, S, 50)  # the oracle's own generator, same counter scheme
+    want, fwant, norm = O.randomized_laplacian(onet, X.astype(np.float64), V)
+    check(op, want, norm, f, fwant)
+
+
+def test_randomized_gaussian_explicit_with_sigma(ctm):
+    params, onet = nets(C1_WIDTHS)
+    N, S, Rv = 13, 16, 12
+    X = points(N, 50)
+    V = gaussian_directions(N, S, Rv)
+    sig = make_sigma(50, Rv, kind="rect")
+    mlp = gpu_mlp(ctm, params)
+    op, _ = mlp.randomized_laplacian(torch.from_numpy(X).cuda(), V=torch.from_numpy(V).cuda(),
+                                     sigma=torch.from_numpy(sig).cuda(), dist="gaussian")
+    want, _, norm = O.randomized_laplacian(onet, X.astype(np.float64), V.astype(np.float64), sig.astype(np.float64))
+    check(op, want, norm)
+
+
+def test_randomized_rademacher_generated_with_sigma(ctm):
+    params, onet = nets(C1_WIDTHS)
+    N, S, Rv = 11, 8, 30
+    X = points(N, 50)
+    sig = make_sigma(50, Rv, kind="rect")
+    mlp = gpu_mlp(ctm, params)
+    op, _ = mlp.randomized_laplacian(torch.from_numpy(X).cuda(), S=S, seed=5, sigma=torch.from_numpy(sig).cuda())
+    V = O.rademacher(5, 0, N, S, Rv)
+    want, _, norm = O.randomized_laplacian(onet, X.astype(np.float64), V, sig.astype(np.float64))
+    check(op, want, norm)
+
+
+# ------------------------------------------------------------------ biharmonic
+@pytest.mark.parametrize("widths,N", [
+    ([3, 24, 24, 1], 9),
+    (C4_WIDTHS, 21),                # BASELINE config C4: D=5, 768-768-512-512-1
+    ([7, 64, 64, 1], 5),            # D = 7: J = 70, P = 212 (the slot cap)
+])
+def test_biharmonic_parity(ctm, widths, N):
+    params, onet = nets(widths)
+    X = points(N, widths[0])
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.biharmonic(torch.from_numpy(X).cuda())
+    want, fwant, norm = O.biharmonic(onet, X.astype(np.float64), O.O1)
+    check(op, want, norm, f, fwant)
+
+
+# ------------------------------------------------------------------ invariants & edges
+def test_shard_invariance_bitwise(ctm):
+    """Splitting a batch into calls (as ranks do) must not change a single bit."""
+    params, _ = nets(C1_WIDTHS)
+    X = torch.from_numpy(points(100, 50)).cuda()
+    mlp = gpu_mlp(ctm, params)
+    full = mlp.laplacian(X)[0].clone()
+    parts = torch.cat([mlp.laplacian(X[:37])[0].clone(), mlp.laplacian(X[37:])[0].clone()])
+    assert torch.equal(full, parts)
+    rfull = mlp.randomized_laplacian(X, S=8, seed=9)[0].clone()
+    rparts = torch.cat([mlp.randomized_laplacian(X[:61], S=8, seed=9, point_offset=0)[0].clone(),
+                        mlp.randomized_laplacian(X[61:], S=8, seed=9, point_offset=61)[0].clone()])
+    assert torch.equal(rfull, rparts)
+    again = mlp.laplacian(X)[0]
+    assert torch.equal(full, again)  # run-to-run determinism
+
+
+def test_empty_batch_is_noop(ctm):
+    params, _ = nets([5, 16, 16, 1])
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.laplacian(torch.empty(0, 5).cuda())
+    assert op.numel() == 0
+
+
+def test_errors_are_status_codes(ctm):
+    params, _ = nets([8, 16, 1])
+    mlp = gpu_mlp(ctm, params)
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        mlp.biharmonic(torch.zeros(2, 8).cuda())  # D = 8 > 7: 3J + 2 > 256
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        mlp.randomized_laplacian(torch.zeros(2, 8).cuda(), S=255)
+    X = torch.zeros(9, 8).cuda()
+    out = torch.empty(5, device="cuda")
+    with pytest.raises(ctm.CTMError, match="ESHAPE"):
+        ctm.lib()  # misaligned output pointer
+        st = ctm.lib().ctm_laplacian(mlp._h, X.data_ptr(), 2, out.data_ptr() + 4, None, None)
+        ctm._check(st, "ctm_laplacian")
+
+
+# ------------------------------------------------------------------ full size (bench config)
+def test_c1_full_batch_sampled(ctm):
+    """BASELINE C1 at N = 16384 in the bench's launch configuration; the oracle
+    checks every 512th point (32 points, including tile-boundary positions)."""
+    params, onet = nets(C1_WIDTHS)
+    N = 16384
+    X = points(N, 50)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.laplacian(torch.from_numpy(X).cuda())
+    idx = np.arange(0, N, 512) + (np.arange(32) % 4)
+    want, fwant, norm = O.laplacian(onet, X[idx].astype(np.float64), O.O1)
+    check(op.cpu()[idx], want, norm, f.cpu()[idx], fwant)
