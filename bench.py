@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py — collapsed-Taylor Laplacian throughput on B200 (BASELINE.json metric).
+
+One step = one full pass of the hot path (seed + layer 1,
+the three fused tcgen05 layers, readout) over one batch of synthetic points:
+config C1 = exact Laplacian of the tanh MLP 50-768-768-512-512-1 on
+N = 16384 points per GPU (weak scaling: every rank processes its own batch;
+points shard with no collective in the step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0. Timing: W untimed warm-up steps; then K steps,
+each bracketed by CUDA events on the launch stream, with an L2 flush (256 MiB
+write) between steps outside the events; barrier + synchronize around the timed
+loop; the max over ranks. `roofline` comes from per-kernel events recorded by
+the library on the same stream during the timed steps (ctm_profile_*).
+`--impl reference` times the fp64 CPU oracle (oracle/, test infrastructure) on
+bounded samples of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "collapsed-Taylor Laplacian points/s, D=50 MLP, 1/2/4/8 B200; % TC peak"
+PAPER_PTS_PER_S = 1.0 / 0.33e-3  # 0.33 ms/datum marginal, RTX 6000, PyTorch (context only)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=16384, help="points per GPU")
+    ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic"], default="laplacian")
+    ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from synth import widths_for
+
+    D = 5 if args.op == "biharmonic" else 50
+    names = {
+        "laplacian": "C1 exact Laplacian",
+        "weighted": "C2 weighted Laplacian (dense full-rank sigma, R=50)",
+        "randomized": f"C3 randomized Laplacian (Rademacher, S={args.S}, generated in-kernel)",
+        "biharmonic": "C4 exact biharmonic (interpolation family, J=35)",
+    }
+    w = widths_for(D)
+    return D, w, f"{names[args.op]}, tanh MLP {'-'.join(map(str, w[:-1]))}-1, N={args.n} points per GPU"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0])]
+        mx = [num(r[1]) for r in self.rows if num(r[1])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
+    """Time the fp64 oracle (vanilla Taylor route O1, as it stands) on a bounded
+    sample of the workload; returns (points/s, points, seconds, threads)."""
+    import oracle as O
+    from synth import mlp_params, points, sigma as make_sigma
+
+    params = mlp_params(widths, 0)
+    net = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params])
+    sig = make_sigma(D, D, kind="dense").astype(np.float64)
+
+    def run(X):
+        if op == "laplacian":
+            O.laplacian(net, X, O.O1)
+        elif op == "weighted":
+            O.weighted_laplacian(net, X, sig, O.O1)
+        elif op == "randomized":
+            O.randomized_laplacian(net, X, O.rademacher(2, 0, X.shape[0], S, D), route=O.O1)
+        else:
+            O.biharmonic(net, X, O.O1)
+
+    nthr = O.num_threads()
+    Xall = points(4096, D, seed_pts).astype(np.float64)
+    m = max(nthr, 8)
+    t0 = time.perf_counter()
+    run(Xall[:m])
+    dt = time.perf_counter() - t0
+    rate = m / dt
+    M = int(min(4096, max(m, rate * budget_s)))
+    t0 = time.perf_counter()
+    run(Xall[:M])
+    dt = time.perf_counter() - t0
+    return M / dt, M, dt, nthr
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    D, widths, wl = workload(args)
+    per_step = []
+    total_pts = 0
+    nthr = None
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        rate, M, dt, nthr = oracle_rate(D, widths, args.op, args.S, budget)
+        if i >= args.warmup:
+            per_step.append(dt)
+            total_pts += M
+    value = total_pts / sum(per_step)
+    sample = f"{total_pts // args.steps} points per step of the {wl.split(',')[0]} workload (fp64 oracle, vanilla Taylor route O1)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(per_step) / len(per_step),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl, "parallelism": "host cores (OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": nthr, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_13644_b200 as ctm
+    from synth import mlp_params, points, sigma as make_sigma
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    D, widths, wl = workload(args)
+    N = args.n
+    params = mlp_params(widths, 0)
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=local)
+    # each rank: its own contiguous slice of the global point set (global index rank*N ...)
+    X_host = points(N * world, D, 1)[rank * N:(rank + 1) * N]
+    X = torch.from_numpy(X_host).to(dev)
+    sig = torch.from_numpy(make_sigma(D, D, kind="dense")).to(dev)
+    op_out = torch.empty(N, device=dev)
+    f_out = torch.empty(N, device=dev)
+
+    def step(Xd):
+        if args.op == "laplacian":
+            mlp.laplacian(Xd, out=op_out, f_out=f_out)
+        elif args.op == "weighted":
+            mlp.weighted_laplacian(Xd, sig, out=op_out, f_out=f_out)
+        elif args.op == "randomized":
+            mlp.randomized_laplacian(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out)
+        else:
+            mlp.biharmonic(Xd, out=op_out, f_out=f_out)
+
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step(X)
+    torch.cuda.synchronize()
+    plan = mlp.last_plan()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    # ---------------- device-resident timed loop
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    mlp.profile(True)
+    for a, b in evs:
+        flush_buf.zero_()
+        a.record()
+        step(X)
+        b.record()
+    torch.cuda.synchronize()
+    barrier()
+    prof = mlp.profile_read()
+    mlp.profile(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = max_over_ranks(sum(step_ms))
+
+    # ---------------- end to end: pinned host X -> device, operator, result -> pinned host
+    Xh = torch.from_numpy(X_host.copy()).pin_memory()
+    oh = torch.empty(N, dtype=torch.float32).pin_memory()
+    fh = torch.empty(N, dtype=torch.float32).pin_memory()
+    Xd = torch.empty_like(X)
+    for _ in range(2):
+        Xd.copy_(Xh, non_blocking=True)
+        step(Xd)
+        oh.copy_(op_out, non_blocking=True)
+        fh.copy_(f_out, non_blocking=True)
+    torch.cuda.synchronize()
+    evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for a, b in evs2:
+        flush_buf.zero_()
+        a.record()
+        Xd.copy_(Xh, non_blocking=True)
+        step(Xd)
+        oh.copy_(op_out, non_blocking=True)
+        fh.copy_(f_out, non_blocking=True)
+        b.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs2))
+    clk = clocks.stop()
+
+    # sanity: the e2e result equals the device-resident one bit for bit
+    assert torch.equal(oh, op_out.cpu()), "e2e result differs from the device-resident run"
+
+    value = N * world * args.steps / (total_ms / 1e3)
+    e2e_value = N * world * args.steps / (e2e_ms / 1e3)
+
+    # roofline of the dominant kernel (the fused tcgen05 layer kernel)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh_:
+            peaks = json.load(fh_)
+        peak_src = "measured"
+    except OSError:
+        peak_src = "fallback"
+    bf16_sust = peaks.get("bf16_tflops_sustained", 1400.0)
+    tf32_peak = 0.5 * bf16_sust            # nominal tf32 : bf16 = 1 : 2 (B200_PROFILING.md)
+    useful_peak = tf32_peak / 3.0          # 3xTF32: three tensor products per useful product
+    lay = prof["layer"]
+    achieved = lay["work"] / (lay["ms"] / 1e3) / 1e12 if lay["ms"] > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "layer_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh_:
+            tj = json.load(fh_)
+        traffic = tj.get(args.op, {}).get("dram_bytes_per_launch")
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
+        "frac": (achieved / useful_peak) if achieved else None, "traffic": traffic,
+        "kernel": "jet_layer_kernel (layers 2-4: tcgen05 3xTF32 GEMM + tanh Taylor epilogue)",
+        "peak_basis": (f"{peak_src} bf16 sustained {bf16_sust} TF/s x 0.5 (tf32) / 3 (3xTF32 split) = "
+                       "useful fp32-accurate FLOP/s ceiling"),
+        "tensor_pipe_frac": (3.0 * achieved / tf32_peak) if achieved else None,
+        "layer_ms_share": lay["ms"] / sum(step_ms) if sum(step_ms) > 0 else None,
+        "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
+        "launches_per_step": {k: v["launches"] / args.steps for k, v in prof.items()},
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, M, dt, nthr = oracle_rate(D, widths, args.op, args.S, budget_s=12.0)
+        cpu = {"value": rate, "unit": "points/s", "cores": nthr, "kind": "oracle",
+               "sample": f"{M} points of the same workload ({dt:.1f} s, fp64 vanilla-Taylor route O1, OpenMP)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": value / PAPER_PTS_PER_S,
+            "vs_baseline_ref": "paper P:1205 collapsed Taylor 0.33 ms/datum marginal on RTX 6000 (context)",
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl, "op": args.op, "N_per_gpu": N, "D": D, "widths": widths,
+                       "slots_per_point": plan["slots_per_point"], "points_per_tile": plan["points_per_tile"],
+                       "mma_n": plan["mma_n"], "parallelism": f"dp{world} (points sharded, no collective in step)",
+                       "l2": "flushed between timed steps (256 MiB write, outside the step events); "
+                             "step working set > 10 GB >> L2"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": N * D * 4,
+                    "d2h_bytes_per_step": 2 * N * 4},
+            "clocks": clk,
+            "gpu_launches": plan["launches"] * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    mlp.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,6 +113,25 @@ const char *ctm_last_error(void);
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t *launches, int32_t *slots_per_point,
                          int32_t *points_per_tile, int32_t *mma_n);
 
+/* Per-kernel timing (measurement support for bench.py; off by default).
+ * When enabled, every launch of an operator call is bracketed by CUDA events
+ * recorded on the call's stream. ctm_profile_read synchronises those events
+ * and returns, per kernel kind, the summed device time (ms), the number of
+ * launches, and the algorithmic work those launches did (FLOP for
+ * CTM_KIND_LAYER = 2 * N * P * w_in * w_out useful products; bytes written
+ * for CTM_KIND_SEED = N * P * w_1 * 8), then clears the accumulators.
+ * arrays: ms[CTM_KIND_COUNT], launches[CTM_KIND_COUNT], work[CTM_KIND_COUNT]. */
+typedef enum {
+    CTM_KIND_PREP = 0,    /* per-call direction matrices (W1 sigma)            */
+    CTM_KIND_SEED = 1,    /* layer 1: seed + affine + tanh rule                 */
+    CTM_KIND_LAYER = 2,   /* hidden layers: tcgen05 GEMM + Taylor epilogue      */
+    CTM_KIND_FINAL = 3,   /* readout / finalize                                 */
+    CTM_KIND_COUNT = 4
+} ctm_kernel_kind;
+
+ctm_status ctm_profile_enable(ctm_mlp_t mlp, int32_t enable);
+ctm_status ctm_profile_read(ctm_mlp_t mlp, double *ms, int64_t *launches, double *work);
+
 #ifdef __cplusplus
 }
 #endif

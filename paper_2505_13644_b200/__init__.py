@@ -35,7 +35,10 @@ ABI = {
     "ctm_last_error": (ctypes.c_char_p, []),
     "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                                      ctypes.POINTER(_I32)]),
+    "ctm_profile_enable": (ctypes.c_int, [_VP, _I32]),
+    "ctm_profile_read": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
 }
+KINDS = ("prep", "seed", "layer", "final")
 
 _lib = None
 
@@ -173,6 +176,20 @@ class MLP:
         _check(lib().ctm_last_plan(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
                "ctm_last_plan")
         return {"launches": a.value, "slots_per_point": b.value, "points_per_tile": c.value, "mma_n": d.value}
+
+    def profile(self, enable: bool = True):
+        """Bracket every launch with CUDA events on its stream (see ctm_profile_read)."""
+        _check(lib().ctm_profile_enable(self._h, int(enable)), "ctm_profile_enable")
+
+    def profile_read(self) -> dict:
+        """{kind: {"ms", "launches", "work"}} summed since the last read; clears."""
+        import numpy as np
+
+        ms = np.zeros(len(KINDS))
+        n = np.zeros(len(KINDS), dtype=np.int64)
+        w = np.zeros(len(KINDS))
+        _check(lib().ctm_profile_read(self._h, ms.ctypes.data, n.ctypes.data, w.ctypes.data), "ctm_profile_read")
+        return {k: {"ms": float(ms[i]), "launches": int(n[i]), "work": float(w[i])} for i, k in enumerate(KINDS)}
 
     def close(self):
         if getattr(self, "_h", None):

@@ -115,6 +115,15 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
+  // profiling (events around launches)
+  bool profiling = false;
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+    double work;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
 };
 
 namespace {
@@ -134,6 +143,13 @@ ctm_status free_all(ctm_mlp* h) {
   for (int i = 0; i < 2; ++i)
     for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
   F(h->partial);
+  for (auto& r : h->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  h->recs.clear();
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  h->event_pool.clear();
   return CTM_OK;
 }
 
@@ -192,6 +208,39 @@ void biharmonic_family(int D, std::vector<float>& dirs, std::vector<float>& w) {
   for (int a = 0; a < D; ++a)
     for (int b = a + 1; b < D; ++b) push(a, 1.f, b, 1.f, wC);
 }
+
+cudaEvent_t take_event(ctm_mlp* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one launch with events when profiling is on.
+struct ProfScope {
+  ctm_mlp* h;
+  int kind;
+  double work;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(ctm_mlp* h_, int kind_, double work_, cudaStream_t st_) : h(h_), kind(kind_), work(work_), st(st_) {
+    if (h->profiling) {
+      a = take_event(h);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (h->profiling) {
+      cudaEvent_t b = take_event(h);
+      cudaEventRecord(b, st);
+      h->recs.push_back({kind, a, b, work});
+    }
+  }
+};
 
 bool g_smem_attr_set[2] = {false, false};
 
@@ -289,7 +338,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
     if (s != CTM_OK) return s;
     if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
-    ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call, h->c_call);
+    {
+      ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
+      ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call, h->c_call);
+    }
     ++launches;
     sp.UT = h->U_call;
     sp.csum = h->c_call;
@@ -304,7 +356,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     if (a.sigma) {
       s = ensure(h->U_call, h->U_call_elems, (size_t)a.Rv * ld1);
       if (s != CTM_OK) return s;
-      ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.Rv, h->U_call, nullptr);
+      {
+        ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
+        ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.Rv, h->U_call, nullptr);
+      }
       ++launches;
       sp.AT = h->U_call;
     } else {
@@ -318,6 +373,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     const int mchunks = (ld1 + ctm::kSeedThreads - 1) / ctm::kSeedThreads;
     const int64_t blocks = a.N * mchunks;
     if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+    ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 8.0, st);
     if (KORD == 2)
       ctm::seed_layer_kernel<2><<<(unsigned)blocks, ctm::kSeedThreads, 0, st>>>(sp);
     else
@@ -330,6 +386,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int L = h->L;
   if (L == 2) {
     const int threads = 256, ppb = threads / 32;
+    ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((a.N + ppb - 1) / ppb), threads, 0, st>>>(
         h->blk[0][0], h->blk[0][1], ld1, P, h->widths[1], h->w_out, h->b_out, scale, a.N, a.op_out, a.f_out);
     ++launches;
@@ -370,16 +427,19 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       if (KORD == 2) {
         s = set_layer_attr<2>();
         if (s != CTM_OK) return s;
+        ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * h->widths[l - 1] * h->widths[l], st);
         ctm::jet_layer_kernel<2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
             h->mapA_hi[i], h->mapA_lo[i], mb_hi, mb_lo, lp);
       } else {
         s = set_layer_attr<4>();
         if (s != CTM_OK) return s;
+        ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * h->widths[l - 1] * h->widths[l], st);
         ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
             h->mapA_hi[i], h->mapA_lo[i], mb_hi, mb_lo, lp);
       }
       ++launches;
       if (last) {
+        ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
         ctm::finalize_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, st>>>(h->partial, m_tiles, a.N, h->b_out,
                                                                            scale, a.op_out, a.f_out);
         ++launches;
@@ -588,6 +648,41 @@ ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, float* op_ou
     return fail(CTM_EUNSUPPORTED, "biharmonic needs 3J+2 <= 256 slots, i.e. D <= 7");
   CallArgs a{OP_BIH, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
+}
+
+ctm_status ctm_profile_enable(ctm_mlp_t mlp, int32_t enable) {
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  DeviceGuard g(mlp->device);
+  for (auto& r : mlp->recs) {
+    cudaEventSynchronize(r.b);
+    mlp->event_pool.push_back(r.a);
+    mlp->event_pool.push_back(r.b);
+  }
+  mlp->recs.clear();
+  mlp->profiling = enable != 0;
+  return CTM_OK;
+}
+
+ctm_status ctm_profile_read(ctm_mlp_t mlp, double* ms, int64_t* launches, double* work) {
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  DeviceGuard g(mlp->device);
+  for (int k = 0; k < CTM_KIND_COUNT; ++k) {
+    if (ms) ms[k] = 0.0;
+    if (launches) launches[k] = 0;
+    if (work) work[k] = 0.0;
+  }
+  for (auto& r : mlp->recs) {
+    CTM_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CTM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (ms) ms[r.kind] += t;
+    if (launches) launches[r.kind] += 1;
+    if (work) work[r.kind] += r.work;
+    mlp->event_pool.push_back(r.a);
+    mlp->event_pool.push_back(r.b);
+  }
+  mlp->recs.clear();
+  return CTM_OK;
 }
 
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t* launches, int32_t* slots_per_point, int32_t* points_per_tile,
