@@ -41,13 +41,15 @@ PAPER_PTS_PER_S = 1.0 / 0.33e-3  # 0.33 ms/datum marginal, RTX 6000, PyT
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
     ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic"], default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: total CPU seconds spread over the warm-up + timed steps")
     return ap.parse_args()
 
 
@@ -157,7 +159,7 @@ def reference_arm(args, rank):
     per_step = []
     total_pts = 0
     nthr = None
-    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    budget = max(1.0, args.ref_budget_s / max(1, args.steps + args.warmup))
     for i in range(args.warmup + args.steps):
         rate, M, dt, nthr = oracle_rate(D, widths, args.op, args.S, budget)
         if i >= args.warmup:

@@ -85,6 +85,7 @@ struct DeviceGuard {
 
 struct ctm_mlp {
   int device = 0;
+  int sm_count = 148;
   int L = 0;                  // affine layers
   std::vector<int> widths;    // L + 1
   std::vector<int> wpad;      // hidden widths padded to 128 (index = layer)
@@ -422,7 +423,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
         lp.w_out = h->w_out;
         lp.partial = h->partial;
       }
-      const int64_t grid = n_tiles * m_tiles;
+      const int64_t grid = std::min<int64_t>(n_tiles * m_tiles, h->sm_count);  // persistent
       if (grid > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
       if (KORD == 2) {
         s = set_layer_attr<2>();
@@ -501,6 +502,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
 
   ctm_mlp* h = new ctm_mlp();
   h->device = device;
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
   h->L = n_layers;
   h->widths.assign(widths, widths + n_layers + 1);
   h->wpad.assign(n_layers + 1, 0);

@@ -68,6 +68,14 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// Persistent: one CTA per SM loops over tiles (tile = m_tile + m_tiles * n_tile, so CTAs
+// running side by side share the B tile of a point group through L2). Warp roles:
+//   warp 0   TMA producer: streams A (W hi/lo) and B (block hi/lo) k-blocks into a
+//            kStages-deep smem ring, continuously across tiles;
+//   warp 1   MMA issuer (one thread): 3 tf32 MMAs per 8-K step into one of two TMEM
+//            accumulators (double buffer), commit -> tmem_full[buf];
+//   warps 2-5 epilogue: TMEM -> registers, Taylor rule, stores; arrive tmem_empty[buf]
+//            so the MMA of tile t+1 overlaps the epilogue of tile t.
 template <int KORD>
 __global__ void __launch_bounds__(kLayerThreads, 1)
     jet_layer_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
@@ -77,16 +85,16 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tmem_full_bar = empty_bar + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full_bar + 1);
+  uint64_t* tmem_full_bar = empty_bar + kStages;   // [2]
+  uint64_t* tmem_empty_bar = tmem_full_bar + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
   float* red = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [4][kMaxPtsPerTile][2]
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x % p.m_tiles;
-  const int n_tile = blockIdx.x / p.m_tiles;
-  const int64_t row0 = (int64_t)n_tile * p.pts_per_tile * p.P;  // first slot row of the tile
+  const int64_t n_tiles = (p.n_points + p.pts_per_tile - 1) / p.pts_per_tile;
+  const int64_t total_tiles = n_tiles * p.m_tiles;
   const uint32_t b_bytes = (uint32_t)p.n_mma * kBK * 4;
 
   if (warp == 0 && lane == 0) {
@@ -98,7 +106,10 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
-    ptx::mbar_init(tmem_full_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tmem_full_bar[b], 1);
+      ptx::mbar_init(&tmem_empty_bar[b], 4);  // one arrive per epilogue warp
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
@@ -112,139 +123,166 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const int m0 = m_tile * kBM;
-      for (int kb = 0; kb < p.k_iters; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
-        ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
-        uint8_t* st = smem + s * kStageBytes;
-        ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * kATileBytes + 2u * b_bytes);
-        const int k0 = kb * kBK;
-        ptx::tma_load_2d(st, &tmA_hi, &full_bar[s], k0, m0);
-        ptx::tma_load_2d(st + kATileBytes, &tmA_lo, &full_bar[s], k0, m0);
-        ptx::tma_load_2d(st + 2 * kATileBytes, &tmB_hi, &full_bar[s], k0, (int32_t)row0);
-        ptx::tma_load_2d(st + 2 * kATileBytes + kBTileBytes, &tmB_lo, &full_bar[s], k0, (int32_t)row0);
+      uint32_t it = 0;  // global k-block counter across tiles
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int m0 = (int)(tile % p.m_tiles) * kBM;
+        const int32_t row0 = (int32_t)((tile / p.m_tiles) * p.pts_per_tile * p.P);
+        for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
+          const uint32_t s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1u;
+          ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* st = smem + s * kStageBytes;
+          ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * kATileBytes + 2u * b_bytes);
+          const int k0 = kb * kBK;
+          ptx::tma_load_2d(st, &tmA_hi, &full_bar[s], k0, m0);
+          ptx::tma_load_2d(st + kATileBytes, &tmA_lo, &full_bar[s], k0, m0);
+          ptx::tma_load_2d(st + 2 * kATileBytes, &tmB_hi, &full_bar[s], k0, row0);
+          ptx::tma_load_2d(st + 2 * kATileBytes + kBTileBytes, &tmB_lo, &full_bar[s], k0, row0);
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
       const uint32_t idesc = ptx::idesc_tf32(kBM, (uint32_t)p.n_mma);
-      for (int kb = 0; kb < p.k_iters; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
-        ptx::mbar_wait(&full_bar[s], ph);
+      uint32_t it = 0, local = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
+        const uint32_t buf = local & 1u;
+        const uint32_t use = local >> 1;  // how many times this buffer was used before
+        ptx::mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
         ptx::tc_fence_after();
-        const uint32_t a_hi = ptx::smem_u32(smem + s * kStageBytes);
-        const uint32_t a_lo = a_hi + kATileBytes;
-        const uint32_t b_hi = a_hi + 2 * kATileBytes;
-        const uint32_t b_lo = b_hi + kBTileBytes;
+        const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
+        for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
+          const uint32_t s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1u;
+          ptx::mbar_wait(&full_bar[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t a_hi = ptx::smem_u32(smem + s * kStageBytes);
+          const uint32_t a_lo = a_hi + kATileBytes;
+          const uint32_t b_hi = a_hi + 2 * kATileBytes;
+          const uint32_t b_lo = b_hi + kBTileBytes;
 #pragma unroll
-        for (int ks = 0; ks < kBK / 8; ++ks) {  // tf32 MMA K = 8 (32 bytes)
-          const uint32_t off = ks * 32;
-          const uint64_t dah = ptx::smem_desc_kmajor(a_hi + off, 512, kSw64);
-          const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, 512, kSw64);
-          const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, 512, kSw64);
-          const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, 512, kSw64);
-          ptx::mma_tf32(tmem_base, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
-          ptx::mma_tf32(tmem_base, dah, dbl, idesc, 1u);               // hi * lo
-          ptx::mma_tf32(tmem_base, dah, dbh, idesc, 1u);               // hi * hi
+          for (int ks = 0; ks < kBK / 8; ++ks) {  // tf32 MMA K = 8 (32 bytes)
+            const uint32_t off = ks * 32;
+            const uint64_t dah = ptx::smem_desc_kmajor(a_hi + off, 512, kSw64);
+            const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, 512, kSw64);
+            const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, 512, kSw64);
+            const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, 512, kSw64);
+            ptx::mma_tf32(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
+            ptx::mma_tf32(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
+            ptx::mma_tf32(d_tmem, dah, dbh, idesc, 1u);               // hi * hi
+          }
+          ptx::mma_commit(&empty_bar[s]);  // stage free once these MMAs retire
         }
-        ptx::mma_commit(&empty_bar[s]);  // stage free once these MMAs retire
+        ptx::mma_commit(&tmem_full_bar[buf]);  // accumulator complete
       }
-      ptx::mma_commit(tmem_full_bar);    // accumulator complete
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
-    const int q = warp & 3;                      // TMEM lane quadrant of this warp
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
     const int m_local = q * 32 + lane;
-    const int m = m_tile * kBM + m_local;
-    const float bias = p.bias[m];
-    const float wo = p.readout ? p.w_out[m] : 0.f;
-    const int64_t pts_left = p.n_points - (int64_t)n_tile * p.pts_per_tile;
-    const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
-    const int ncols = npts * p.P;
-    ptx::mbar_wait(tmem_full_bar, 0);
-    ptx::tc_fence_after();
-    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
+    uint32_t local = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
+      const uint32_t buf = local & 1u;
+      const uint32_t use = local >> 1;
+      const int m_tile = (int)(tile % p.m_tiles);
+      const int64_t n_tile = tile / p.m_tiles;
+      const int64_t row0 = n_tile * p.pts_per_tile * p.P;
+      const int m = m_tile * kBM + m_local;
+      const float bias = p.bias[m];
+      const float wo = p.readout ? p.w_out[m] : 0.f;
+      const int64_t pts_left = p.n_points - n_tile * p.pts_per_tile;
+      const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
+      const int ncols = npts * p.P;
+      ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
+      ptx::tc_fence_after();
+      const uint32_t taddr = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
 
-    int slot = 0, pt = 0;
-    float d1 = 0.f, d2 = 0.f, d3 = 0.f, d4 = 0.f, acc = 0.f;  // acc: sum over directions
-    float z1 = 0.f, z2 = 0.f;                                // K=4 jet state
-    int jj = 0;
-    for (int c0 = 0; c0 < ncols; c0 += 16) {
-      float v[16];
-      ptx::tmem_ld16(taddr + (uint32_t)c0, v);
-      ptx::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = c0 + i;
-        if (c >= ncols) break;
-        const size_t oidx = (size_t)(row0 + c) * p.ldo + m;
-        float z = v[i];
-        if (slot == 0) {
-          z += bias;  // the bias enters the primal only (affine rule)
-          const float t = tanhf(z);
-          d1 = 1.f - t * t;          // tanh'
-          d2 = -2.f * t * d1;        // tanh''
-          if (KORD == 4) {
-            d3 = d1 * (6.f * t * t - 2.f);        // tanh'''
-            d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
-          }
-          acc = 0.f;
-          jj = 0;
-          if (p.readout) {
-            const float s = warp_sum(wo * t);
-            if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 0] = s;
-          } else {
-            store_pair(p.out_hi, p.out_lo, oidx, t);
-          }
-        } else if (slot == p.P - 1) {
-          const float top = d1 * z + (KORD == 2 ? d2 * acc : acc);  // <dh, sum z_K> + collapsed rest
-          if (p.readout) {
-            const float s = warp_sum(wo * top);
-            if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 1] = s;
-          } else {
-            store_pair(p.out_hi, p.out_lo, oidx, top);
-          }
-        } else {
-          float h;
-          if (KORD == 2) {
-            h = d1 * z;          // h_{1,r} = tanh' z_{1,r}
-            acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
-          } else {
-            const int which = (slot - 1) % 3;  // 0: z1, 1: z2, 2: z3 of jet jj
-            if (which == 0) {
-              z1 = z;
-              h = d1 * z1;
-            } else if (which == 1) {
-              z2 = z;
-              h = d2 * z1 * z1 + d1 * z2;
-            } else {
-              const float z3 = z;
-              h = d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3;
-              const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 +
-                               3.f * d2 * z2 * z2;
-              acc = fmaf(jw[jj], nl, acc);
-              ++jj;
-            }
-          }
-          if (!p.readout) store_pair(p.out_hi, p.out_lo, oidx, h);
+      int slot = 0, pt = 0;
+      float d1 = 0.f, d2 = 0.f, d3 = 0.f, d4 = 0.f, acc = 0.f;  // acc: sum over directions
+      float z1 = 0.f, z2 = 0.f;                                // K=4 jet state
+      int jj = 0;
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        float v[16];
+        ptx::tmem_ld16(taddr + (uint32_t)c0, v);
+        ptx::tmem_ld_wait();
+        if (c0 + 16 >= ncols) {
+          // the whole accumulator of this tile is read: hand the buffer back to the MMA
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tmem_empty_bar[buf]);
         }
-        if (++slot == p.P) {
-          slot = 0;
-          ++pt;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = c0 + i;
+          if (c >= ncols) break;
+          const size_t oidx = (size_t)(row0 + c) * p.ldo + m;
+          float z = v[i];
+          if (slot == 0) {
+            z += bias;  // the bias enters the primal only (affine rule)
+            const float t = tanhf(z);
+            d1 = 1.f - t * t;    // tanh'
+            d2 = -2.f * t * d1;  // tanh''
+            if (KORD == 4) {
+              d3 = d1 * (6.f * t * t - 2.f);            // tanh'''
+              d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
+            }
+            acc = 0.f;
+            jj = 0;
+            if (p.readout) {
+              const float s = warp_sum(wo * t);
+              if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 0] = s;
+            } else {
+              store_pair(p.out_hi, p.out_lo, oidx, t);
+            }
+          } else if (slot == p.P - 1) {
+            const float top = d1 * z + (KORD == 2 ? d2 * acc : acc);  // <dh, sum z_K> + collapsed rest
+            if (p.readout) {
+              const float s = warp_sum(wo * top);
+              if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 1] = s;
+            } else {
+              store_pair(p.out_hi, p.out_lo, oidx, top);
+            }
+          } else {
+            float h;
+            if (KORD == 2) {
+              h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
+              acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
+            } else {
+              const int which = (slot - 1) % 3;  // 0: z1, 1: z2, 2: z3 of jet jj
+              if (which == 0) {
+                z1 = z;
+                h = d1 * z1;
+              } else if (which == 1) {
+                z2 = z;
+                h = d2 * z1 * z1 + d1 * z2;
+              } else {
+                const float z3 = z;
+                h = d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3;
+                const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 +
+                                 3.f * d2 * z2 * z2;
+                acc = fmaf(jw[jj], nl, acc);
+                ++jj;
+              }
+            }
+            if (!p.readout) store_pair(p.out_hi, p.out_lo, oidx, h);
+          }
+          if (++slot == p.P) {
+            slot = 0;
+            ++pt;
+          }
         }
       }
-    }
-    if (p.readout) {
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps only
-      for (int j = threadIdx.x - 64; j < npts * 2; j += 128) {
-        const int pj = j >> 1, comp = j & 1;
-        const float s = red[(0 * kMaxPtsPerTile + pj) * 2 + comp] + red[(1 * kMaxPtsPerTile + pj) * 2 + comp] +
-                        red[(2 * kMaxPtsPerTile + pj) * 2 + comp] + red[(3 * kMaxPtsPerTile + pj) * 2 + comp];
-        const int64_t n = (int64_t)n_tile * p.pts_per_tile + pj;
-        p.partial[(n * p.m_tiles + m_tile) * 2 + comp] = s;
+      if (p.readout) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps only
+        for (int j = threadIdx.x - 64; j < npts * 2; j += 128) {
+          const int pj = j >> 1, comp = j & 1;
+          const float s = red[(0 * kMaxPtsPerTile + pj) * 2 + comp] + red[(1 * kMaxPtsPerTile + pj) * 2 + comp] +
+                          red[(2 * kMaxPtsPerTile + pj) * 2 + comp] + red[(3 * kMaxPtsPerTile + pj) * 2 + comp];
+          const int64_t n = n_tile * p.pts_per_tile + pj;
+          p.partial[(n * p.m_tiles + m_tile) * 2 + comp] = s;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // red[] is reused by the next tile
       }
     }
   }
