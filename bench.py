@@ -300,8 +300,8 @@ def main():
     except OSError:
         peak_src = "fallback"
     bf16_sust = peaks.get("bf16_tflops_sustained", 1400.0)
-    tf32_peak = 0.5 * bf16_sust            # nominal tf32 : bf16 = 1 : 2 (B200_PROFILING.md)
-    useful_peak = tf32_peak / 3.0          # 3xTF32: three tensor products per useful product
+    tensor_peak = bf16_sust                # the layer MMAs are kind::f16 with bf16 operands
+    useful_peak = tensor_peak / 3.0        # 3xBF16: three tensor products per useful product
     lay = prof["layer"]
     achieved = lay["work"] / (lay["ms"] / 1e3) / 1e12 if lay["ms"] > 0 else None
     traffic = None
@@ -313,10 +313,10 @@ def main():
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
         "frac": (achieved / useful_peak) if achieved else None, "traffic": traffic,
-        "kernel": "jet_layer_kernel (layers 2-4: tcgen05 3xTF32 GEMM + tanh Taylor epilogue)",
-        "peak_basis": (f"{peak_src} bf16 sustained {bf16_sust} TF/s x 0.5 (tf32) / 3 (3xTF32 split) = "
-                       "useful fp32-accurate FLOP/s ceiling"),
-        "tensor_pipe_frac": (3.0 * achieved / tf32_peak) if achieved else None,
+        "kernel": "jet_layer_kernel (layers 2-4: tcgen05 3xBF16 GEMM + tanh Taylor epilogue)",
+        "peak_basis": (f"{peak_src} bf16 sustained {bf16_sust} TF/s / 3 (3xBF16 split: three bf16 tensor "
+                       "products per useful fp32-accurate product)"),
+        "tensor_pipe_frac": (3.0 * achieved / tensor_peak) if achieved else None,
         "layer_ms_share": lay["ms"] / sum(step_ms) if sum(step_ms) > 0 else None,
         "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
         "launches_per_step": {k: v["launches"] / args.steps for k, v in prof.items()},
@@ -335,7 +335,7 @@ def main():
             "scaling": "weak",
             "vs_baseline": value / PAPER_PTS_PER_S,
             "vs_baseline_ref": "paper P:1205 collapsed Taylor 0.33 ms/datum marginal on RTX 6000 (context)",
-            "dtype": "f32", "data": "synthetic",
+            "dtype": "f32 (3xbf16 tensor products, fp32 accumulate)", "data": "synthetic",
             "config": {"workload": wl, "op": args.op, "N_per_gpu": N, "D": D, "widths": widths,
                        "slots_per_point": plan["slots_per_point"], "points_per_tile": plan["points_per_tile"],
                        "mma_n": plan["mma_n"], "parallelism": f"dp{world} (points sharded, no collective in step)",

@@ -24,8 +24,8 @@
  *  - Results are bitwise deterministic run to run, and independent of how a
  *    batch is split into calls (no reduction depends on N or on a point's
  *    position; random directions are keyed on the global point index).
- *  - Arithmetic: fp32 storage; the layer contractions run on tcgen05 tensor
- *    cores as 3xTF32 (hi*hi + hi*lo + lo*hi, fp32 accumulation); the Taylor
+ *  - Arithmetic: fp32 values; the layer contractions run on tcgen05 tensor
+ *    cores on bf16 pairs as 3xBF16 (hi*hi + hi*lo + lo*hi, fp32 accumulation); the Taylor
  *    rules run in fp32.  Accuracy target: |op - op_fp64| <= 1e-4 * sum_r
  *    |c_r f_{K,r}|.
  */
@@ -56,7 +56,7 @@ typedef enum { CTM_RADEMACHER = 0, CTM_GAUSSIAN = 1 } ctm_dist;
  *   widths [n_layers+1] (HOST): widths[0] = D >= 1, widths[n_layers] = 1.
  *   W [n_layers] (HOST array of DEVICE pointers): W_l is [w_l, w_{l-1}] (nn.Linear).
  *   b [n_layers] (HOST array of DEVICE pointers): b_l is [w_l].
- * The weights are copied (pre-split into tf32 hi/lo pairs, padded); the call
+ * The weights are copied (pre-split into bf16 hi/lo pairs, padded); the call
  * synchronises the device before returning, so W and b may be freed after.
  * Errors: CTM_EINVAL (NULL, n_layers < 2, width < 1), CTM_EUNSUPPORTED
  * (widths[n_layers] != 1, hidden width > 8192), CTM_ECUDA, CTM_ENOMEM. */
@@ -119,7 +119,7 @@ ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t *launches, int32_t *slots_per_po
  * and returns, per kernel kind, the summed device time (ms), the number of
  * launches, and the algorithmic work those launches did (FLOP for
  * CTM_KIND_LAYER = 2 * N * P * w_in * w_out useful products; bytes written
- * for CTM_KIND_SEED = N * P * w_1 * 8), then clears the accumulators.
+ * for CTM_KIND_SEED = N * P * w_1 * 4, a bf16 pair), then clears the accumulators.
  * arrays: ms[CTM_KIND_COUNT], launches[CTM_KIND_COUNT], work[CTM_KIND_COUNT]. */
 typedef enum {
     CTM_KIND_PREP = 0,    /* per-call direction matrices (W1 sigma)            */

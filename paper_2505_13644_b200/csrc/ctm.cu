@@ -53,15 +53,16 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 2D fp32 tensor map: inner dim `cols` (contiguous), outer `rows`; box {kBK, box_rows}; SWIZZLE_64B.
-bool make_map(CUtensorMap* m, const float* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+// 2D bf16 tensor map: inner dim `cols` (contiguous), outer `rows`; box {kBK, box_rows}
+// (64-byte rows); SWIZZLE_64B, matching the UMMA descriptors of jet_layer.cuh.
+bool make_map(CUtensorMap* m, const uint16_t* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * sizeof(float)};
+  cuuint64_t strides[1] = {cols * sizeof(uint16_t)};
   cuuint32_t box[2] = {(cuuint32_t)ctm::kBK, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -93,7 +94,8 @@ struct ctm_mlp {
   float* W1T = nullptr;       // [D, wpad[1]]
   float* b1 = nullptr;        // [wpad[1]]
   // hidden GEMM layers l = 2..L-1 (index l-2)
-  std::vector<float*> Whi, Wlo, bias;
+  std::vector<uint16_t*> Whi, Wlo;       // bf16 pairs [Mpad, Kpad]
+  std::vector<float*> bias;
   std::vector<CUtensorMap> mapA_hi, mapA_lo;
   // output layer
   float* w_out = nullptr;     // [wpad[L-1]]
@@ -109,8 +111,8 @@ struct ctm_mlp {
   float* U_call = nullptr;
   float* c_call = nullptr;
   size_t U_call_elems = 0;
-  // workspace: two ping-pong blocks (hi, lo)
-  float* blk[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  // workspace: two ping-pong blocks (bf16 hi, lo)
+  uint16_t* blk[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   size_t blk_elems = 0;
   float* partial = nullptr;
   size_t partial_elems = 0;
@@ -131,7 +133,7 @@ namespace {
 
 ctm_status free_all(ctm_mlp* h) {
   DeviceGuard g(h->device);
-  auto F = [](float*& p) {
+  auto F = [](auto*& p) {
     if (p) cudaFree(p);
     p = nullptr;
   };
@@ -176,7 +178,7 @@ ctm_status ensure_workspace(ctm_mlp* h, int64_t rows) {
       }
     h->blk_elems = 0;
     for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j) CTM_CUDA(cudaMalloc(&h->blk[i][j], std::max<size_t>(need, 1) * sizeof(float)));
+      for (int j = 0; j < 2; ++j) CTM_CUDA(cudaMalloc(&h->blk[i][j], std::max<size_t>(need, 1) * sizeof(uint16_t)));
     h->blk_elems = need;
   }
   return CTM_OK;
@@ -374,7 +376,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     const int mchunks = (ld1 + ctm::kSeedThreads - 1) / ctm::kSeedThreads;
     const int64_t blocks = a.N * mchunks;
     if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
-    ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 8.0, st);
+    ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
     if (KORD == 2)
       ctm::seed_layer_kernel<2><<<(unsigned)blocks, ctm::kSeedThreads, 0, st>>>(sp);
     else
@@ -534,10 +536,11 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
   // hidden GEMM layers
   for (int l = 2; l <= n_layers - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
-    float *whi, *wlo, *bp;
-    LOAD_CUDA(cudaMalloc(&whi, sizeof(float) * (size_t)mpad * kpad));
+    uint16_t *whi, *wlo;
+    float* bp;
+    LOAD_CUDA(cudaMalloc(&whi, sizeof(uint16_t) * (size_t)mpad * kpad));
     h->Whi.push_back(whi);
-    LOAD_CUDA(cudaMalloc(&wlo, sizeof(float) * (size_t)mpad * kpad));
+    LOAD_CUDA(cudaMalloc(&wlo, sizeof(uint16_t) * (size_t)mpad * kpad));
     h->Wlo.push_back(wlo);
     LOAD_CUDA(cudaMalloc(&bp, sizeof(float) * mpad));
     h->bias.push_back(bp);

@@ -15,24 +15,24 @@
 //   h1 = s'z1, h2 = s''z1^2 + s'z2, h3 = s'''z1^3 + 3s''z1z2 + s'z3,
 //   sum_w h4 = sum_j w_j (s''''z1^4 + 6s'''z1^2z2 + 4s''z1z3 + 3s''z2^2) + s' sum_w z4
 //
-// Layout in HBM: block B_l is [N*P rows, ld] fp32, row = n*P + slot,
-// stored as a tf32 pair (hi = rna_tf32(v), lo = v - hi) so that hi*hi + hi*lo + lo*hi
-// on the tensor cores reproduces fp32-accurate products.
+// Layout in HBM: block B_l is [N*P rows, ld], row = n*P + slot, stored as
+// a bf16 pair (hi = rn_bf16(v), lo = rn_bf16(v - hi)); the tensor cores form
+// hi*hi + hi*lo + lo*hi (kind::f16, fp32 accumulation) -- "3xBF16", DESIGN.md §5.
 #pragma once
 #include "ptx.cuh"
 
 namespace ctm {
 
 constexpr int kBM = 128;                         // features per tile = TMEM lanes
-constexpr int kBK = 16;                          // fp32 K per stage: 64-byte rows, SWIZZLE_64B
+constexpr int kBK = 32;                          // bf16 K per stage: 64-byte rows, SWIZZLE_64B
 constexpr int kStages = 4;
 constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
-constexpr int kATileBytes = kBM * kBK * 4;       // 8 KB
-constexpr int kBTileBytes = kMaxN * kBK * 4;     // 16 KB
+constexpr int kATileBytes = kBM * kBK * 2;       // 8 KB
+constexpr int kBTileBytes = kMaxN * kBK * 2;     // 16 KB
 constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
-constexpr int kLayerThreads = 192;               // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                            4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxJets * 4;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
@@ -40,8 +40,8 @@ constexpr uint32_t kSw64 = 4;                    // descriptor layout code for S
 
 struct LayerParams {
   const float* bias;      // [Mpad]
-  float* out_hi;          // [rows, ldo]
-  float* out_lo;
+  uint16_t* out_hi;       // [rows, ldo] bf16 pair
+  uint16_t* out_lo;
   int ldo;
   int m_tiles;
   int64_t n_points;
@@ -56,10 +56,11 @@ struct LayerParams {
   float* partial;         // [n_points, m_tiles, 2]
 };
 
-__device__ __forceinline__ void store_pair(float* hi, float* lo, size_t idx, float v) {
-  const float h = ptx::tf32_rna(v);
+__device__ __forceinline__ void store_pair(uint16_t* hi, uint16_t* lo, size_t idx, float v) {
+  uint16_t h, l;
+  ptx::bf16_split(v, h, l);
   hi[idx] = h;
-  lo[idx] = v - h;
+  lo[idx] = l;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -68,13 +69,95 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// One point of one tile, for the feature owned by this thread: TMEM columns
+// [tcol, tcol + P) hold z for slots 0..P-1. Writes the P output slots (bf16 pairs) or,
+// on the readout layer, returns w_out*h0 and w_out*(top) for the reduction.
+template <int KORD>
+__device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
+                                               float wo, const float* jw, float& fpart, float& opart) {
+  const int P = p.P;
+  const int ld = p.ldo;
+  uint16_t* ph = p.out_hi + (size_t)row * ld + m;
+  uint16_t* pl = p.out_lo + (size_t)row * ld + m;
+  // ---- slot 0: the primal; the bias enters here only (affine rule)
+  const float z0 = ptx::tmem_ld1(tcol) + bias;
+  ptx::tmem_ld_wait();
+  const float t = tanhf(z0);
+  const float d1 = 1.f - t * t;   // tanh'
+  const float d2 = -2.f * t * d1;  // tanh''
+  float d3 = 0.f, d4 = 0.f;
+  if (KORD == 4) {
+    d3 = d1 * (6.f * t * t - 2.f);            // tanh'''
+    d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
+  }
+  fpart = wo * t;
+  if (!p.readout) store_pair(ph, pl, 0, t);
+  ph += ld;
+  pl += ld;
+  // ---- slots 1..P-2: first-order coefficients (K=2) or jets (z1, z2, z3) (K=4)
+  float acc = 0.f;            // the collapsed sum over directions
+  float z1 = 0.f, z2 = 0.f;   // K=4 jet state
+  int which = 0, jj = 0;
+  auto middle = [&](float z) {
+    float h;
+    if (KORD == 2) {
+      h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
+      acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
+    } else {
+      if (which == 0) {
+        z1 = z;
+        h = d1 * z1;
+      } else if (which == 1) {
+        z2 = z;
+        h = d2 * z1 * z1 + d1 * z2;
+      } else {
+        const float z3 = z;
+        h = d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3;
+        const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 + 3.f * d2 * z2 * z2;
+        acc = fmaf(jw[jj], nl, acc);
+        ++jj;
+      }
+      which = (which == 2) ? 0 : which + 1;
+    }
+    if (!p.readout) store_pair(ph, pl, 0, h);
+    ph += ld;
+    pl += ld;
+  };
+  const int nmid = P - 2;
+  int s = 0;
+  for (; s + 16 <= nmid; s += 16) {
+    float v[16];
+    ptx::tmem_ld16(tcol + 1u + (uint32_t)s, v);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) middle(v[i]);
+  }
+  const int rem = nmid - s;  // 0..15, warp-uniform
+  if (rem > 0) {
+    float v[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i)
+      if (i < rem) v[i] = ptx::tmem_ld1(tcol + 1u + (uint32_t)(s + i));
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 15; ++i)
+      if (i < rem) middle(v[i]);
+  }
+  // ---- slot P-1: the collapsed top, <dh, sum z_K> + the collapsed non-linear terms (Eq. 7)
+  const float zt = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
+  ptx::tmem_ld_wait();
+  const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
+  opart = wo * top;
+  if (!p.readout) store_pair(ph, pl, 0, top);
+}
+
 // Persistent: one CTA per SM loops over tiles (tile = m_tile + m_tiles * n_tile, so CTAs
 // running side by side share the B tile of a point group through L2). Warp roles:
 //   warp 0   TMA producer: streams A (W hi/lo) and B (block hi/lo) k-blocks into a
 //            kStages-deep smem ring, continuously across tiles;
-//   warp 1   MMA issuer (one thread): 3 tf32 MMAs per 8-K step into one of two TMEM
+//   warp 1   MMA issuer (one thread): 3 bf16 MMAs per 16-K step into one of two TMEM
 //            accumulators (double buffer), commit -> tmem_full[buf];
-//   warps 2-5 epilogue: TMEM -> registers, Taylor rule, stores; arrive tmem_empty[buf]
+//   warps 2-9 epilogue: TMEM -> registers, Taylor rule, stores; arrive tmem_empty[buf]
 //            so the MMA of tile t+1 overlaps the epilogue of tile t.
 template <int KORD>
 __global__ void __launch_bounds__(kLayerThreads, 1)
@@ -95,7 +178,7 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n_points + p.pts_per_tile - 1) / p.pts_per_tile;
   const int64_t total_tiles = n_tiles * p.m_tiles;
-  const uint32_t b_bytes = (uint32_t)p.n_mma * kBK * 4;
+  const uint32_t b_bytes = (uint32_t)p.n_mma * kBK * 2;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA_hi);
@@ -108,7 +191,7 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tmem_full_bar[b], 1);
-      ptx::mbar_init(&tmem_empty_bar[b], 4);  // one arrive per epilogue warp
+      ptx::mbar_init(&tmem_empty_bar[b], 8);  // one arrive per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -144,7 +227,7 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_tf32(kBM, (uint32_t)p.n_mma);
+      const uint32_t idesc = ptx::idesc_bf16(kBM, (uint32_t)p.n_mma);
       uint32_t it = 0, local = 0;
       for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
         const uint32_t buf = local & 1u;
@@ -162,15 +245,15 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
           const uint32_t b_hi = a_hi + 2 * kATileBytes;
           const uint32_t b_lo = b_hi + kBTileBytes;
 #pragma unroll
-          for (int ks = 0; ks < kBK / 8; ++ks) {  // tf32 MMA K = 8 (32 bytes)
+          for (int ks = 0; ks < kBK / 16; ++ks) {  // bf16 MMA K = 16 (32 bytes)
             const uint32_t off = ks * 32;
             const uint64_t dah = ptx::smem_desc_kmajor(a_hi + off, 512, kSw64);
             const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, 512, kSw64);
             const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, 512, kSw64);
             const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, 512, kSw64);
-            ptx::mma_tf32(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
-            ptx::mma_tf32(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
-            ptx::mma_tf32(d_tmem, dah, dbh, idesc, 1u);               // hi * hi
+            ptx::mma_bf16(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
+            ptx::mma_bf16(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
+            ptx::mma_bf16(d_tmem, dah, dbh, idesc, 1u);               // hi * hi
           }
           ptx::mma_commit(&empty_bar[s]);  // stage free once these MMAs retire
         }
@@ -178,8 +261,13 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
-    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    // ------------------------------------------------------------ epilogue (warps 2..9)
+    // Two warps per TMEM lane quadrant (a warp may only touch lanes 32*(warp%4)..+31);
+    // group g = 0/1 takes the even/odd points of the tile. Each thread owns one output
+    // feature and walks the P slots of its points in order, so the collapse
+    // sum_r (...) is a sequential in-register sum.
+    const int q = warp & 3;
+    const int g = (warp - 2) >> 2;
     const int m_local = q * 32 + lane;
     uint32_t local = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
@@ -193,96 +281,35 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
       const float wo = p.readout ? p.w_out[m] : 0.f;
       const int64_t pts_left = p.n_points - n_tile * p.pts_per_tile;
       const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
-      const int ncols = npts * p.P;
       ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
       ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
-
-      int slot = 0, pt = 0;
-      float d1 = 0.f, d2 = 0.f, d3 = 0.f, d4 = 0.f, acc = 0.f;  // acc: sum over directions
-      float z1 = 0.f, z2 = 0.f;                                // K=4 jet state
-      int jj = 0;
-      for (int c0 = 0; c0 < ncols; c0 += 16) {
-        float v[16];
-        ptx::tmem_ld16(taddr + (uint32_t)c0, v);
-        ptx::tmem_ld_wait();
-        if (c0 + 16 >= ncols) {
-          // the whole accumulator of this tile is read: hand the buffer back to the MMA
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tmem_empty_bar[buf]);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int c = c0 + i;
-          if (c >= ncols) break;
-          const size_t oidx = (size_t)(row0 + c) * p.ldo + m;
-          float z = v[i];
-          if (slot == 0) {
-            z += bias;  // the bias enters the primal only (affine rule)
-            const float t = tanhf(z);
-            d1 = 1.f - t * t;    // tanh'
-            d2 = -2.f * t * d1;  // tanh''
-            if (KORD == 4) {
-              d3 = d1 * (6.f * t * t - 2.f);            // tanh'''
-              d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
-            }
-            acc = 0.f;
-            jj = 0;
-            if (p.readout) {
-              const float s = warp_sum(wo * t);
-              if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 0] = s;
-            } else {
-              store_pair(p.out_hi, p.out_lo, oidx, t);
-            }
-          } else if (slot == p.P - 1) {
-            const float top = d1 * z + (KORD == 2 ? d2 * acc : acc);  // <dh, sum z_K> + collapsed rest
-            if (p.readout) {
-              const float s = warp_sum(wo * top);
-              if (lane == 0) red[(q * kMaxPtsPerTile + pt) * 2 + 1] = s;
-            } else {
-              store_pair(p.out_hi, p.out_lo, oidx, top);
-            }
-          } else {
-            float h;
-            if (KORD == 2) {
-              h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
-              acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
-            } else {
-              const int which = (slot - 1) % 3;  // 0: z1, 1: z2, 2: z3 of jet jj
-              if (which == 0) {
-                z1 = z;
-                h = d1 * z1;
-              } else if (which == 1) {
-                z2 = z;
-                h = d2 * z1 * z1 + d1 * z2;
-              } else {
-                const float z3 = z;
-                h = d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3;
-                const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 +
-                                 3.f * d2 * z2 * z2;
-                acc = fmaf(jw[jj], nl, acc);
-                ++jj;
-              }
-            }
-            if (!p.readout) store_pair(p.out_hi, p.out_lo, oidx, h);
-          }
-          if (++slot == p.P) {
-            slot = 0;
-            ++pt;
+      const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
+      for (int pt = g; pt < npts; pt += 2) {
+        float fpart, opart;
+        epilogue_point<KORD>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, fpart, opart);
+        if (p.readout) {
+          fpart = warp_sum(fpart);
+          opart = warp_sum(opart);
+          if (lane == 0) {
+            red[(q * kMaxPtsPerTile + pt) * 2 + 0] = fpart;
+            red[(q * kMaxPtsPerTile + pt) * 2 + 1] = opart;
           }
         }
       }
+      // every epilogue warp releases the accumulator buffer once per tile
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tmem_empty_bar[buf]);
       if (p.readout) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps only
-        for (int j = threadIdx.x - 64; j < npts * 2; j += 128) {
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps only
+        for (int j = threadIdx.x - 64; j < npts * 2; j += 256) {
           const int pj = j >> 1, comp = j & 1;
           const float s = red[(0 * kMaxPtsPerTile + pj) * 2 + comp] + red[(1 * kMaxPtsPerTile + pj) * 2 + comp] +
                           red[(2 * kMaxPtsPerTile + pj) * 2 + comp] + red[(3 * kMaxPtsPerTile + pj) * 2 + comp];
           const int64_t n = n_tile * p.pts_per_tile + pj;
           p.partial[(n * p.m_tiles + m_tile) * 2 + comp] = s;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // red[] is reused by the next tile
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // red[] is reused by the next tile
       }
     }
   }

@@ -45,14 +45,15 @@ struct SeedParams {
   const float* V;        // [N, S, Rv] or nullptr => Rademacher(seed, point_offset + n)
   uint64_t seed;
   int64_t point_offset;
-  float* out_hi;         // [N*P, ld]
-  float* out_lo;
+  uint16_t* out_hi;      // [N*P, ld] bf16 pair
+  uint16_t* out_lo;
 };
 
-__device__ __forceinline__ void seed_store(float* hi, float* lo, size_t idx, float v) {
-  const float h = ptx::tf32_rna(v);
+__device__ __forceinline__ void seed_store(uint16_t* hi, uint16_t* lo, size_t idx, float v) {
+  uint16_t h, l;
+  ptx::bf16_split(v, h, l);
   hi[idx] = h;
-  lo[idx] = v - h;
+  lo[idx] = l;
 }
 
 // grid: one block per (point, 256-feature chunk); one thread per feature.
@@ -177,7 +178,7 @@ __global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, 
 
 // Readout straight from a layer block (nets with a single hidden layer):
 // one warp per point, lanes over features.
-__global__ void readout_block_kernel(const float* __restrict__ hi, const float* __restrict__ lo, int ld, int P,
+__global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo, int ld, int P,
                                      int width, const float* __restrict__ w_out, float b_out, float scale,
                                      int64_t N, float* __restrict__ op, float* __restrict__ f) {
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -186,8 +187,8 @@ __global__ void readout_block_kernel(const float* __restrict__ hi, const float* 
   const size_t r0 = (size_t)n * P * ld, rt = ((size_t)n * P + P - 1) * ld;
   float s0 = 0.f, s1 = 0.f;
   for (int m = lane; m < width; m += 32) {
-    s0 = fmaf(w_out[m], hi[r0 + m] + lo[r0 + m], s0);
-    s1 = fmaf(w_out[m], hi[rt + m] + lo[rt + m], s1);
+    s0 = fmaf(w_out[m], ptx::bf16_val(hi[r0 + m]) + ptx::bf16_val(lo[r0 + m]), s0);
+    s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -200,18 +201,16 @@ __global__ void readout_block_kernel(const float* __restrict__ hi, const float* 
   }
 }
 
-// Split W [rows, cols] (row-major, device) into padded tf32 pairs [Mpad, Kpad];
+// Split W [rows, cols] (row-major, device) into padded bf16 pairs [Mpad, Kpad];
 // bias into [Mpad]. Padding is zero.
 __global__ void split_weights_kernel(const float* __restrict__ W, const float* __restrict__ b, int rows, int cols,
-                                     int Mpad, int Kpad, float* __restrict__ Whi, float* __restrict__ Wlo,
+                                     int Mpad, int Kpad, uint16_t* __restrict__ Whi, uint16_t* __restrict__ Wlo,
                                      float* __restrict__ bpad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)Mpad * Kpad) return;
   const int r = (int)(i / Kpad), c = (int)(i % Kpad);
   const float v = (r < rows && c < cols) ? W[(size_t)r * cols + c] : 0.f;
-  const float h = ptx::tf32_rna(v);
-  Whi[i] = h;
-  Wlo[i] = v - h;
+  ptx::bf16_split(v, Whi[i], Wlo[i]);
   if (c == 0) bpad[r] = (r < rows) ? b[r] : 0.f;
 }
 
