@@ -93,6 +93,11 @@ struct ctm_mlp {
   // layer 1
   float* W1T = nullptr;       // [D, wpad[1]]
   float* b1 = nullptr;        // [wpad[1]]
+  // layer 1 as a tensor-core layer (randomized directions): bf16 pairs [wpad[1], k1pad]
+  int k1pad = 0;
+  uint16_t* W1hi = nullptr;
+  uint16_t* W1lo = nullptr;
+  CUtensorMap mapA1_hi, mapA1_lo;
   // hidden GEMM layers l = 2..L-1 (index l-2)
   std::vector<uint16_t*> Whi, Wlo;       // bf16 pairs [Mpad, Kpad]
   std::vector<float*> bias;
@@ -137,7 +142,7 @@ ctm_status free_all(ctm_mlp* h) {
     if (p) cudaFree(p);
     p = nullptr;
   };
-  F(h->W1T); F(h->b1); F(h->w_out);
+  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1hi); F(h->W1lo);
   for (auto& p : h->Whi) F(p);
   for (auto& p : h->Wlo) F(p);
   for (auto& p : h->bias) F(p);
@@ -167,7 +172,7 @@ ctm_status ensure(float*& p, size_t& have, size_t need) {
 }
 
 ctm_status ensure_workspace(ctm_mlp* h, int64_t rows) {
-  int ldmax = 0;
+  int ldmax = h->k1pad;
   for (int l = 1; l < h->L; ++l) ldmax = std::max(ldmax, h->wpad[l]);
   const size_t need = (size_t)rows * ldmax;
   if (need > h->blk_elems || !h->blk[0][0]) {
@@ -317,138 +322,152 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   ctm_status s = ensure_workspace(h, rows);
   if (s != CTM_OK) return s;
 
-  // ---- per-call direction preparation
-  ctm::SeedParams sp{};
-  sp.X = a.X;
-  sp.D = D;
-  sp.n_points = a.N;
-  sp.W1T = h->W1T;
-  sp.b1 = h->b1;
-  sp.ld = ld1;
-  sp.P = P;
-  sp.out_hi = h->blk[0][0];
-  sp.out_lo = h->blk[0][1];
+  // ---- layer 1 (the seed of the collapsed jet)
   float scale = 1.f;
-  if (a.op == OP_LAP) {
-    sp.UT = h->U_lap;
-    sp.csum = h->c_lap;
-    sp.R = D;
-  } else if (a.op == OP_BIH) {
-    sp.UT = h->U_bih;
-    sp.csum = h->c_bih;
-    sp.R = h->J_bih;
-  } else if (a.op == OP_WLAP) {
-    s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
-    if (s != CTM_OK) return s;
-    if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
+  int cur;  // workspace block holding the next GEMM layer's input
+  struct GemmLayer {
+    const CUtensorMap* a_hi;
+    const CUtensorMap* a_lo;
+    const float* bias;
+    int kpad, mpad, w_in, w_out;
+  };
+  std::vector<GemmLayer> layers;
+  if (a.op == OP_RLAP) {
+    // per-point directions: write the input block [x0; u_1..u_S; 0] and run layer 1 as a
+    // tensor-core layer like the others
+    ctm::SeedRandomParams rp{};
+    rp.X = a.X;
+    rp.D = D;
+    rp.ldk = h->k1pad;
+    rp.S = a.S;
+    rp.Rv = a.Rv;
+    rp.V = a.V;
+    rp.sigma = a.sigma;
+    rp.seed = a.seed;
+    rp.point_offset = a.point_offset;
+    rp.out_hi = h->blk[1][0];
+    rp.out_lo = h->blk[1][1];
     {
-      ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
-      ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call, h->c_call);
+      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->k1pad * 4.0, st);
+      ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
     }
     ++launches;
-    sp.UT = h->U_call;
-    sp.csum = h->c_call;
-    sp.R = a.R;
-  } else {  // randomized
-    sp.random = 1;
-    sp.S = a.S;
-    sp.Rv = a.Rv;
-    sp.V = a.V;
-    sp.seed = a.seed;
-    sp.point_offset = a.point_offset;
-    if (a.sigma) {
-      s = ensure(h->U_call, h->U_call_elems, (size_t)a.Rv * ld1);
+    cur = 1;
+    scale = 1.f / (float)a.S;
+    layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
+  } else {
+    ctm::SeedParams sp{};
+    sp.X = a.X;
+    sp.D = D;
+    sp.n_points = a.N;
+    sp.W1T = h->W1T;
+    sp.b1 = h->b1;
+    sp.ld = ld1;
+    sp.P = P;
+    sp.out_hi = h->blk[0][0];
+    sp.out_lo = h->blk[0][1];
+    if (a.op == OP_LAP) {
+      sp.UT = h->U_lap;
+      sp.csum = h->c_lap;
+      sp.R = D;
+    } else if (a.op == OP_BIH) {
+      sp.UT = h->U_bih;
+      sp.csum = h->c_bih;
+      sp.R = h->J_bih;
+    } else {  // weighted: U = W1 sigma for this call
+      s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
       if (s != CTM_OK) return s;
+      if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
       {
         ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
-        ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.Rv, h->U_call, nullptr);
+        ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call,
+                                                                  h->c_call);
       }
       ++launches;
-      sp.AT = h->U_call;
-    } else {
-      sp.AT = h->W1T;  // v in R^D directly: A = W1
+      sp.UT = h->U_call;
+      sp.csum = h->c_call;
+      sp.R = a.R;
     }
-    scale = 1.f / (float)a.S;
-  }
-
-  // ---- layer 1
-  {
-    const int mchunks = (ld1 + ctm::kSeedThreads - 1) / ctm::kSeedThreads;
+    const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
+    const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
     const int64_t blocks = a.N * mchunks;
     if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
-    ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
-    if (KORD == 2)
-      ctm::seed_layer_kernel<2><<<(unsigned)blocks, ctm::kSeedThreads, 0, st>>>(sp);
-    else
-      ctm::seed_layer_kernel<4><<<(unsigned)blocks, ctm::kSeedThreads, 0, st>>>(sp);
+    {
+      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
+      if (KORD == 2)
+        ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      else
+        ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
+    }
     ++launches;
+    cur = 0;
+  }
+  for (int l = 2; l <= h->L - 1; ++l) {
+    const int i = l - 2;
+    layers.push_back({&h->mapA_hi[i], &h->mapA_lo[i], h->bias[i], h->wpad[l - 1], h->wpad[l], h->widths[l - 1],
+                      h->widths[l]});
   }
 
-  // ---- hidden layers 2..L-1
-  int cur = 0;
-  const int L = h->L;
-  if (L == 2) {
+  // ---- hidden layers on the tensor cores; the last one reduces against w_out
+  if (layers.empty()) {  // fixed directions and a single hidden layer: read the seed block
     const int threads = 256, ppb = threads / 32;
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((a.N + ppb - 1) / ppb), threads, 0, st>>>(
         h->blk[0][0], h->blk[0][1], ld1, P, h->widths[1], h->w_out, h->b_out, scale, a.N, a.op_out, a.f_out);
     ++launches;
-  } else {
-    const int64_t n_tiles = (a.N + pl.ppt - 1) / pl.ppt;
-    for (int l = 2; l <= L - 1; ++l) {
-      const int i = l - 2;
-      const int kpad = h->wpad[l - 1];
-      const int mpad = h->wpad[l];
-      const int m_tiles = mpad / ctm::kBM;
-      const bool last = (l == L - 1);
-      CUtensorMap mb_hi, mb_lo;
-      if (!make_map(&mb_hi, h->blk[cur][0], (uint64_t)kpad, (uint64_t)rows, (uint32_t)pl.nmma) ||
-          !make_map(&mb_lo, h->blk[cur][1], (uint64_t)kpad, (uint64_t)rows, (uint32_t)pl.nmma))
-        return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
-      ctm::LayerParams lp{};
-      lp.bias = h->bias[i];
-      lp.out_hi = h->blk[cur ^ 1][0];
-      lp.out_lo = h->blk[cur ^ 1][1];
-      lp.ldo = mpad;
-      lp.m_tiles = m_tiles;
-      lp.n_points = a.N;
-      lp.P = P;
-      lp.pts_per_tile = pl.ppt;
-      lp.n_mma = pl.nmma;
-      lp.k_iters = kpad / ctm::kBK;
-      lp.jet_w = h->w_bih;
-      lp.J = h->J_bih;
-      if (last) {
-        s = ensure(h->partial, h->partial_elems, (size_t)a.N * m_tiles * 2);
-        if (s != CTM_OK) return s;
-        lp.readout = 1;
-        lp.w_out = h->w_out;
-        lp.partial = h->partial;
-      }
-      const int64_t grid = std::min<int64_t>(n_tiles * m_tiles, h->sm_count);  // persistent
-      if (grid > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+  }
+  const int64_t n_tiles = (a.N + pl.ppt - 1) / pl.ppt;
+  for (size_t li = 0; li < layers.size(); ++li) {
+    const GemmLayer& gl = layers[li];
+    const int m_tiles = gl.mpad / ctm::kBM;
+    const bool last = (li + 1 == layers.size());
+    CUtensorMap mb_hi, mb_lo;
+    if (!make_map(&mb_hi, h->blk[cur][0], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma) ||
+        !make_map(&mb_lo, h->blk[cur][1], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma))
+      return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
+    ctm::LayerParams lp{};
+    lp.bias = gl.bias;
+    lp.out_hi = h->blk[cur ^ 1][0];
+    lp.out_lo = h->blk[cur ^ 1][1];
+    lp.ldo = gl.mpad;
+    lp.m_tiles = m_tiles;
+    lp.n_points = a.N;
+    lp.P = P;
+    lp.pts_per_tile = pl.ppt;
+    lp.n_mma = pl.nmma;
+    lp.k_iters = gl.kpad / ctm::kBK;
+    lp.jet_w = h->w_bih;
+    lp.J = h->J_bih;
+    if (last) {
+      s = ensure(h->partial, h->partial_elems, (size_t)a.N * m_tiles * 2);
+      if (s != CTM_OK) return s;
+      lp.readout = 1;
+      lp.w_out = h->w_out;
+      lp.partial = h->partial;
+    }
+    const int64_t grid = std::min<int64_t>(n_tiles * m_tiles, h->sm_count);  // persistent
+    {
+      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * gl.w_in * gl.w_out, st);
       if (KORD == 2) {
         s = set_layer_attr<2>();
         if (s != CTM_OK) return s;
-        ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * h->widths[l - 1] * h->widths[l], st);
-        ctm::jet_layer_kernel<2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
-            h->mapA_hi[i], h->mapA_lo[i], mb_hi, mb_lo, lp);
+        ctm::jet_layer_kernel<2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
+                                                                                              mb_hi, mb_lo, lp);
       } else {
         s = set_layer_attr<4>();
         if (s != CTM_OK) return s;
-        ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * h->widths[l - 1] * h->widths[l], st);
-        ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
-            h->mapA_hi[i], h->mapA_lo[i], mb_hi, mb_lo, lp);
+        ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
+                                                                                              mb_hi, mb_lo, lp);
       }
-      ++launches;
-      if (last) {
-        ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
-        ctm::finalize_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, st>>>(h->partial, m_tiles, a.N, h->b_out,
-                                                                           scale, a.op_out, a.f_out);
-        ++launches;
-      }
-      cur ^= 1;
     }
+    ++launches;
+    if (last) {
+      ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
+      ctm::finalize_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, st>>>(h->partial, m_tiles, a.N, h->b_out, scale,
+                                                                         a.op_out, a.f_out);
+      ++launches;
+    }
+    cur ^= 1;
   }
   CTM_CUDA(cudaGetLastError());
   h->last_launches = launches;
@@ -532,6 +551,20 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
   {
     const int64_t n = (int64_t)D * ld1;
     ctm::transpose_w1_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[0], b[0], widths[1], D, ld1, h->W1T, h->b1);
+  }
+  // layer 1 as a tensor-core layer (used by the randomized operator)
+  {
+    h->k1pad = round_up(D, ctm::kBK);
+    LOAD_CUDA(cudaMalloc(&h->W1hi, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
+    LOAD_CUDA(cudaMalloc(&h->W1lo, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
+    const int64_t n = (int64_t)ld1 * h->k1pad;
+    ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[0], b[0], widths[1], D, ld1, h->k1pad,
+                                                                      h->W1hi, h->W1lo, h->b1);
+    if (!make_map(&h->mapA1_hi, h->W1hi, h->k1pad, ld1, ctm::kBM) ||
+        !make_map(&h->mapA1_lo, h->W1lo, h->k1pad, ld1, ctm::kBM)) {
+      fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W1");
+      return bail(CTM_ECUDA);
+    }
   }
   // hidden GEMM layers
   for (int l = 2; l <= n_layers - 1; ++l) {
@@ -640,7 +673,7 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, in
     return fail(CTM_EUNSUPPORTED, "in-kernel generation is Rademacher only; pass Gaussian directions as V");
   if (!sigma && Rv != mlp->widths[0]) return fail(CTM_ESHAPE, "Rv must equal D when sigma is NULL");
   if ((V && !aligned16(V)) || (sigma && !aligned16(sigma))) return fail(CTM_ESHAPE, "V/sigma must be 16-byte aligned");
-  if (Rv > ctm::kSeedChunk) return fail(CTM_EUNSUPPORTED, "Rv too large");
+  if (Rv > 256) return fail(CTM_EUNSUPPORTED, "Rv > 256");
   CallArgs a{OP_RLAP, X, N, sigma, 0, S, V, seed, point_offset, Rv, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }

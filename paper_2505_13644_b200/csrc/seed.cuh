@@ -1,12 +1,13 @@
 // seed.cuh — layer 1 of the collapsed jet (steps a1 + a2 + a3 of SURVEY §8(a)),
 // the per-call direction preparation, and the readout (a5).
 //
-// Layer 1 is tiny in K (K = D) and needs no tensor cores: z0 = W1 x0 + b1 is a
-// D-term dot product per feature; for FIXED direction sets the first-order
-// coefficients z_{1,r} = (W1 V)[:, r] are the same for every point and are
-// precomputed once (U^T [R, ld]); for RANDOM directions z_{1,s} = A v_{n,s} with
-// A = W1 (or W1 sigma) and v_{n,s} generated in-kernel (Rademacher, splitmix64)
-// or read from V. The kernel is bound by the HBM write of the layer-1 block.
+// FIXED direction sets: layer 1 needs no tensor cores: z0 = W1 x0 + b1 is a D-term dot
+// product per feature and the first-order coefficients z_{1,r} = (W1 V)[:, r] are the
+// same for every point, precomputed once (U^T [R, ld]). The kernel is bound by the HBM
+// write of the layer-1 block.
+// RANDOM directions: the per-point directions make layer 1 a real contraction
+// [N(S+2), D] x [D, w1]; seed_random_kernel only writes the input block and layer 1
+// runs on the tensor cores (jet_layer.cuh).
 #pragma once
 #include <cstdint>
 
@@ -37,70 +38,120 @@ struct SeedParams {
   const float* UT;       // [R, ld]
   const float* csum;     // [ld]
   int R;                 // K=2: number of directions; K=4: number of jets J
-  // RANDOM directions (K=2 only): z1_s = sum_r AT[r, m] v[n, s, r]
-  int random;
-  const float* AT;       // [Rv, ld]
-  int Rv;
-  int S;
-  const float* V;        // [N, S, Rv] or nullptr => Rademacher(seed, point_offset + n)
-  uint64_t seed;
-  int64_t point_offset;
   uint16_t* out_hi;      // [N*P, ld] bf16 pair
   uint16_t* out_lo;
 };
 
-__device__ __forceinline__ void seed_store(uint16_t* hi, uint16_t* lo, size_t idx, float v) {
-  uint16_t h, l;
-  ptx::bf16_split(v, h, l);
-  hi[idx] = h;
-  lo[idx] = l;
+// four adjacent features -> one 8-byte store into each of the hi and lo planes
+__device__ __forceinline__ void seed_store4(uint16_t* hi, uint16_t* lo, size_t idx, float a, float b, float c,
+                                           float d) {
+  uint16_t h[4], l[4];
+  ptx::bf16_split(a, h[0], l[0]);
+  ptx::bf16_split(b, h[1], l[1]);
+  ptx::bf16_split(c, h[2], l[2]);
+  ptx::bf16_split(d, h[3], l[3]);
+  *reinterpret_cast<uint2*>(hi + idx) = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+  *reinterpret_cast<uint2*>(lo + idx) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
 }
 
-// grid: one block per (point, 256-feature chunk); one thread per feature.
+// Fixed direction sets (K=2: e_d or sigma columns; K=4: the biharmonic family).
+// grid: one block per (point, 4*blockDim-feature chunk); each thread owns 4 adjacent
+// features, so loads are float4 and the bf16-pair stores are 8 bytes wide.
 template <int KORD>
 __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedParams p) {
   __shared__ float xs[256];
-  __shared__ float vs[kSeedChunk];
-  const int mchunks = (p.ld + kSeedThreads - 1) / kSeedThreads;
+  const int feats = 4 * blockDim.x;
+  const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
-  const int m = (blockIdx.x % mchunks) * kSeedThreads + threadIdx.x;
+  const int m = (blockIdx.x % mchunks) * feats + 4 * threadIdx.x;
   for (int d = threadIdx.x; d < p.D; d += blockDim.x) xs[d] = p.X[n * p.D + d];
   __syncthreads();
-  const bool active = m < p.ld;
+  if (m >= p.ld) return;  // ld is a multiple of 128: a thread's 4 features are all in or all out
   const size_t row0 = (size_t)n * p.P;
-  float t = 0.f, d1 = 0.f, d2 = 0.f;
-  if (active) {
-    float z0 = p.b1[m];
-    for (int d = 0; d < p.D; ++d) z0 = fmaf(p.W1T[(size_t)d * p.ld + m], xs[d], z0);
-    t = tanhf(z0);
-    d1 = 1.f - t * t;    // tanh'
-    d2 = -2.f * t * d1;  // tanh''
-    seed_store(p.out_hi, p.out_lo, row0 * p.ld + m, t);
+  float4 z0 = *reinterpret_cast<const float4*>(p.b1 + m);
+  for (int d = 0; d < p.D; ++d) {
+    const float4 w = *reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m);
+    z0.x = fmaf(w.x, xs[d], z0.x);
+    z0.y = fmaf(w.y, xs[d], z0.y);
+    z0.z = fmaf(w.z, xs[d], z0.z);
+    z0.w = fmaf(w.w, xs[d], z0.w);
   }
-  if (!p.random) {
-    if (!active) return;
-    if (KORD == 2) {
-      for (int r = 0; r < p.R; ++r)
-        seed_store(p.out_hi, p.out_lo, (row0 + 1 + r) * p.ld + m, d1 * p.UT[(size_t)r * p.ld + m]);
-      // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
-      seed_store(p.out_hi, p.out_lo, (row0 + 1 + p.R) * p.ld + m, d2 * p.csum[m]);
-    } else {
-      const float d3 = d1 * (6.f * t * t - 2.f), d4 = 8.f * t * d1 * (2.f - 3.f * t * t);
-      for (int j = 0; j < p.R; ++j) {
-        const float z1 = p.UT[(size_t)j * p.ld + m];
-        const size_t r = row0 + 1 + 3 * j;
-        seed_store(p.out_hi, p.out_lo, r * p.ld + m, d1 * z1);                  // h1
-        seed_store(p.out_hi, p.out_lo, (r + 1) * p.ld + m, d2 * z1 * z1);       // h2 (z2 = 0)
-        seed_store(p.out_hi, p.out_lo, (r + 2) * p.ld + m, d3 * z1 * z1 * z1);  // h3 (z2 = z3 = 0)
-      }
-      // sum_w h4 = tanh'''' * sum_j w_j z1_j^4   (z2 = z3 = z4 = 0)
-      seed_store(p.out_hi, p.out_lo, (row0 + 1 + 3 * p.R) * p.ld + m, d4 * p.csum[m]);
+  float t[4] = {tanhf(z0.x), tanhf(z0.y), tanhf(z0.z), tanhf(z0.w)};
+  float d1[4], d2[4], d3[4], d4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d1[i] = 1.f - t[i] * t[i];    // tanh'
+    d2[i] = -2.f * t[i] * d1[i];  // tanh''
+    d3[i] = d1[i] * (6.f * t[i] * t[i] - 2.f);            // tanh'''
+    d4[i] = 8.f * t[i] * d1[i] * (2.f - 3.f * t[i] * t[i]);  // tanh''''
+  }
+  seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+  const float4 cs = *reinterpret_cast<const float4*>(p.csum + m);
+  if (KORD == 2) {
+    for (int r = 0; r < p.R; ++r) {
+      const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m);
+      seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
+                  d1[3] * u.w);
     }
-    return;
+    // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
+    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + p.R) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
+                d2[3] * cs.w);
+  } else {
+    for (int j = 0; j < p.R; ++j) {
+      const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)j * p.ld + m);
+      const float z[4] = {u.x, u.y, u.z, u.w};
+      float h1[4], h2[4], h3[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        h1[i] = d1[i] * z[i];                       // h1
+        h2[i] = d2[i] * z[i] * z[i];                // h2 (z2 = 0)
+        h3[i] = d3[i] * z[i] * z[i] * z[i];         // h3 (z2 = z3 = 0)
+      }
+      const size_t r = row0 + 1 + 3 * j;
+      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+      seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+      seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+    }
+    // sum_w h4 = tanh'''' * sum_j w_j z1_j^4   (z2 = z3 = z4 = 0)
+    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + 3 * p.R) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
+                d4[3] * cs.w);
   }
-  // randomized (K=2): per-point directions, staged in smem a chunk at a time
+}
+
+// Randomized directions: the layer-1 INPUT block of the collapsed jet,
+// rows [x0; u_1 .. u_S; 0] per point (Eq. 8/10 stochastic seeds),
+// u_s = v_s or sigma v_s, stored as bf16 pairs [N*(S+2), ldk] (ldk = D padded to 32,
+// zero padded). Layer 1 then runs on the tensor cores like every other layer.
+// grid: one block per point.
+struct SeedRandomParams {
+  const float* X;        // [N, D]
+  int D;
+  int ldk;               // padded row length (multiple of 32)
+  int S;
+  int Rv;
+  const float* V;        // [N, S, Rv] or nullptr => Rademacher(seed, point_offset + n)
+  const float* sigma;    // [D, Rv] or nullptr (then Rv == D)
+  uint64_t seed;
+  int64_t point_offset;
+  uint16_t* out_hi;
+  uint16_t* out_lo;
+};
+
+__global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
+  __shared__ float vs[kSeedChunk];
+  const int64_t n = blockIdx.x;
+  const int P = p.S + 2;
+  const size_t row0 = (size_t)n * P;
+  const int q4 = p.ldk / 4;  // 4-column groups per row
+  // primal row and the zero top row
+  for (int c4 = threadIdx.x; c4 < q4; c4 += blockDim.x) {
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = (4 * c4 + i < p.D) ? p.X[n * p.D + 4 * c4 + i] : 0.f;
+    seed_store4(p.out_hi, p.out_lo, row0 * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
+    seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+  }
   const int per_chunk = kSeedChunk / p.Rv;
-  float sumsq = 0.f;
   for (int s0 = 0; s0 < p.S; s0 += per_chunk) {
     const int ns = (p.S - s0 < per_chunk) ? (p.S - s0) : per_chunk;
     __syncthreads();
@@ -117,16 +168,25 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
       vs[e] = v;
     }
     __syncthreads();
-    if (active) {
-      for (int s = 0; s < ns; ++s) {
-        float z1 = 0.f;
-        for (int r = 0; r < p.Rv; ++r) z1 = fmaf(p.AT[(size_t)r * p.ld + m], vs[s * p.Rv + r], z1);
-        seed_store(p.out_hi, p.out_lo, (row0 + 1 + s0 + s) * p.ld + m, d1 * z1);
-        sumsq = fmaf(z1, z1, sumsq);
+    for (int e = threadIdx.x; e < ns * q4; e += blockDim.x) {
+      const int s = e / q4, c4 = e % q4;
+      float u[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int d = 4 * c4 + i;
+        float val = 0.f;
+        if (d < p.D) {
+          if (p.sigma) {
+            for (int r = 0; r < p.Rv; ++r) val = fmaf(p.sigma[(size_t)d * p.Rv + r], vs[s * p.Rv + r], val);
+          } else {
+            val = vs[s * p.Rv + d];
+          }
+        }
+        u[i] = val;
       }
+      seed_store4(p.out_hi, p.out_lo, (row0 + 1 + s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
     }
   }
-  if (active) seed_store(p.out_hi, p.out_lo, (row0 + 1 + p.S) * p.ld + m, d2 * sumsq);
 }
 
 // UT[r, m] = sum_d W1T[d, m] dirs[r, d]; csum[m] = sum_r w_r UT[r, m]^pow (pow 2 or 4).
