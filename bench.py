@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
-    ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic"], default="laplacian")
+    ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard"],
+                    default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
@@ -59,6 +60,7 @@ def workload(args):
     D = 5 if args.op == "biharmonic" else 50
     names = {
         "laplacian": "C1 exact Laplacian",
+        "standard": "C1 exact Laplacian by STANDARD Taylor mode (1+2D vectors; the paper's baseline)",
         "weighted": "C2 weighted Laplacian (dense full-rank sigma, R=50)",
         "randomized": f"C3 randomized Laplacian (Rademacher, S={args.S}, generated in-kernel)",
         "biharmonic": "C4 exact biharmonic (interpolation family, J=35)",
@@ -129,7 +131,7 @@ def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
     sig = make_sigma(D, D, kind="dense").astype(np.float64)
 
     def run(X):
-        if op == "laplacian":
+        if op in ("laplacian", "standard"):
             O.laplacian(net, X, O.O1)
         elif op == "weighted":
             O.weighted_laplacian(net, X, sig, O.O1)
@@ -213,6 +215,8 @@ def main():
     def step(Xd):
         if args.op == "laplacian":
             mlp.laplacian(Xd, out=op_out, f_out=f_out)
+        elif args.op == "standard":
+            mlp.laplacian_standard(Xd, out=op_out, f_out=f_out)
         elif args.op == "weighted":
             mlp.weighted_laplacian(Xd, sig, out=op_out, f_out=f_out)
         elif args.op == "randomized":

@@ -72,6 +72,15 @@ ctm_status ctm_free_mlp(ctm_mlp_t mlp);
 ctm_status ctm_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                          void *stream);
 
+/* Exact Laplacian by STANDARD (vanilla) Taylor mode, P:560-564 and Eq. D3:
+ * the same value as ctm_laplacian, but every layer propagates 1 + 2D vectors
+ * (x0, and per direction x_{1,d}, x_{2,d}); the top coefficients are sliced and
+ * summed only at the output. The paper's baseline, exposed to measure the
+ * collapsed/standard ratio of Table `tab:benchmark-ratios` on B200.
+ * P = 1 + 2D <= 256 (D <= 127), else CTM_EUNSUPPORTED. */
+ctm_status ctm_laplacian_standard(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
+                                  void *stream);
+
 /* Weighted Laplacian, Eq. 10 exact case:
  * op[n] = <d^2 f(x_n), sigma sigma^T> = sum_r <d^2 f, s_r^{(x)2}>,
  *   sigma [D, R] (columns s_r; constant across points), R >= 1,

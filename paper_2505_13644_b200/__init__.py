@@ -25,6 +25,7 @@ ABI = {
     "ctm_load_mlp": (ctypes.c_int, [_I32, _VP, _VP, _VP, _I32, ctypes.POINTER(_VP)]),
     "ctm_free_mlp": (ctypes.c_int, [_VP]),
     "ctm_laplacian": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_laplacian_standard": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_weighted_laplacian": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
     "ctm_randomized_laplacian": (
         ctypes.c_int,
@@ -131,6 +132,14 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_laplacian(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                    _stream_ptr(stream, self.device)), "ctm_laplacian")
+        return out, f_out
+
+    def laplacian_standard(self, X, out=None, f_out=None, want_f=True, stream=None):
+        """Exact Laplacian by STANDARD Taylor mode (1 + 2D vectors per layer): the
+        paper's baseline, same value as ``laplacian``."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        _check(lib().ctm_laplacian_standard(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
+                                            _stream_ptr(stream, self.device)), "ctm_laplacian_standard")
         return out, f_out
 
     def weighted_laplacian(self, X, sigma, out=None, f_out=None, want_f=True, stream=None):

@@ -123,6 +123,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
+  bool smem_attr_set[5] = {false, false, false, false, false};
   // profiling (events around launches)
   bool profiling = false;
   struct Rec {
@@ -250,14 +251,13 @@ struct ProfScope {
   }
 };
 
-bool g_smem_attr_set[2] = {false, false};
-
+// cudaFuncSetAttribute is per device: tracked per handle (a handle lives on one device)
 template <int KORD>
-ctm_status set_layer_attr() {
-  if (!g_smem_attr_set[KORD == 4]) {
+ctm_status set_layer_attr(ctm_mlp* h) {
+  if (!h->smem_attr_set[KORD]) {
     CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctm::kLayerSmem));
-    g_smem_attr_set[KORD == 4] = true;
+    h->smem_attr_set[KORD] = true;
   }
   return CTM_OK;
 }
@@ -276,7 +276,7 @@ Plan make_plan(int P) {
   return pl;
 }
 
-enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH };
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD };
 
 struct CallArgs {
   Op op;
@@ -297,13 +297,14 @@ struct CallArgs {
 ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int D = h->widths[0];
   const int ld1 = h->wpad[1];
-  const int KORD = (a.op == OP_BIH) ? 4 : 2;
+  const int KORD = (a.op == OP_BIH) ? 4 : (a.op == OP_LAP_STD) ? ctm::kStd2 : 2;
   int P = 0;
   switch (a.op) {
     case OP_LAP: P = D + 2; break;
     case OP_WLAP: P = a.R + 2; break;
     case OP_RLAP: P = a.S + 2; break;
     case OP_BIH: P = 3 * h->J_bih + 2; break;
+    case OP_LAP_STD: P = 1 + 2 * D; break;
   }
   if (P > ctm::kMaxN)
     return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
@@ -366,7 +367,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     sp.P = P;
     sp.out_hi = h->blk[0][0];
     sp.out_lo = h->blk[0][1];
-    if (a.op == OP_LAP) {
+    if (a.op == OP_LAP || a.op == OP_LAP_STD) {
       sp.UT = h->U_lap;
       sp.csum = h->c_lap;
       sp.R = D;
@@ -396,8 +397,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
       if (KORD == 2)
         ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
-      else
+      else if (KORD == 4)
         ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      else
+        ctm::seed_layer_kernel<ctm::kStd2><<<(unsigned)blocks, threads, 0, st>>>(sp);
     }
     ++launches;
     cur = 0;
@@ -413,7 +416,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     const int threads = 256, ppb = threads / 32;
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((a.N + ppb - 1) / ppb), threads, 0, st>>>(
-        h->blk[0][0], h->blk[0][1], ld1, P, h->widths[1], h->w_out, h->b_out, scale, a.N, a.op_out, a.f_out);
+        h->blk[0][0], h->blk[0][1], ld1, P, h->widths[1], h->w_out, h->b_out, scale, a.N, a.op_out, a.f_out, a.op == OP_LAP_STD);
     ++launches;
   }
   const int64_t n_tiles = (a.N + pl.ppt - 1) / pl.ppt;
@@ -449,15 +452,20 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     {
       ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * gl.w_in * gl.w_out, st);
       if (KORD == 2) {
-        s = set_layer_attr<2>();
+        s = set_layer_attr<2>(h);
         if (s != CTM_OK) return s;
         ctm::jet_layer_kernel<2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
                                                                                               mb_hi, mb_lo, lp);
-      } else {
-        s = set_layer_attr<4>();
+      } else if (KORD == 4) {
+        s = set_layer_attr<4>(h);
         if (s != CTM_OK) return s;
         ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
                                                                                               mb_hi, mb_lo, lp);
+      } else {
+        s = set_layer_attr<ctm::kStd2>(h);
+        if (s != CTM_OK) return s;
+        ctm::jet_layer_kernel<ctm::kStd2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
+            *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp);
       }
     }
     ++launches;
@@ -647,6 +655,15 @@ ctm_status ctm_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out
   ctm_status s = check_common(mlp, X, N, op_out, f_out);
   if (s != CTM_OK) return s;
   CallArgs a{OP_LAP, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_laplacian_standard(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out, float* f_out,
+                                  void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  CallArgs a{OP_LAP_STD, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
 

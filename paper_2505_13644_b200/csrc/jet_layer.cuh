@@ -37,6 +37,10 @@ constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barrie
                            4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxJets * 4;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
 constexpr uint32_t kSw64 = 4;                    // descriptor layout code for SWIZZLE_64B
+// Epilogue modes (template parameter KORD): 2 = K=2 collapsed, 4 = K=4 collapsed (weighted
+// top), kStd2 = K=2 STANDARD Taylor mode (1 + 2R slots, the per-direction top
+// coefficients are propagated and only summed at the output) -- the paper's baseline.
+constexpr int kStd2 = 3;
 
 struct LayerParams {
   const float* bias;      // [Mpad]
@@ -94,8 +98,9 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   if (!p.readout) store_pair(ph, pl, 0, t);
   ph += ld;
   pl += ld;
-  // ---- slots 1..P-2: first-order coefficients (K=2) or jets (z1, z2, z3) (K=4)
-  float acc = 0.f;            // the collapsed sum over directions
+  // ---- slots 1..P-2: first-order coefficients (K=2) or jets (z1, z2, z3) (K=4);
+  //      standard mode (kStd2): slots 1..P-1 are the pairs (z1_r, z2_r), no collapse
+  float acc = 0.f;            // the collapsed sum over directions (standard: sum_r h2_r at readout)
   float z1 = 0.f, z2 = 0.f;   // K=4 jet state
   int which = 0, jj = 0;
   auto middle = [&](float z) {
@@ -103,6 +108,15 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     if (KORD == 2) {
       h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
       acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
+    } else if (KORD == kStd2) {
+      if (which == 0) {
+        z1 = z;
+        h = d1 * z1;                    // h_{1,r}
+      } else {
+        h = fmaf(d2 * z1, z1, d1 * z);  // h_{2,r} = tanh'' z1^2 + tanh' z2 (Eq. 1, per direction)
+        acc += h;
+      }
+      which ^= 1;
     } else {
       if (which == 0) {
         z1 = z;
@@ -123,7 +137,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     ph += ld;
     pl += ld;
   };
-  const int nmid = P - 2;
+  const int nmid = (KORD == kStd2) ? P - 1 : P - 2;
   int s = 0;
   for (; s + 16 <= nmid; s += 16) {
     float v[16];
@@ -142,6 +156,10 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
 #pragma unroll
     for (int i = 0; i < 15; ++i)
       if (i < rem) middle(v[i]);
+  }
+  if (KORD == kStd2) {  // standard mode: the top coefficients are sliced and summed only here
+    opart = wo * acc;
+    return;
   }
   // ---- slot P-1: the collapsed top, <dh, sum z_K> + the collapsed non-linear terms (Eq. 7)
   const float zt = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));

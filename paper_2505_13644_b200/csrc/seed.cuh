@@ -87,7 +87,16 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
   }
   seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
   const float4 cs = *reinterpret_cast<const float4*>(p.csum + m);
-  if (KORD == 2) {
+  if (KORD == kStd2) {
+    // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
+    for (int r = 0; r < p.R; ++r) {
+      const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m);
+      const size_t rr = row0 + 1 + 2 * r;
+      seed_store4(p.out_hi, p.out_lo, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+      seed_store4(p.out_hi, p.out_lo, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
+                  d2[2] * u.z * u.z, d2[3] * u.w * u.w);
+    }
+  } else if (KORD == 2) {
     for (int r = 0; r < p.R; ++r) {
       const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m);
       seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
@@ -238,9 +247,10 @@ __global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, 
 
 // Readout straight from a layer block (nets with a single hidden layer):
 // one warp per point, lanes over features.
+// standard != 0: the op is sum_r w_out . h2_r over rows 2, 4, .., P-1 (standard mode)
 __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo, int ld, int P,
                                      int width, const float* __restrict__ w_out, float b_out, float scale,
-                                     int64_t N, float* __restrict__ op, float* __restrict__ f) {
+                                     int64_t N, float* __restrict__ op, float* __restrict__ f, int standard) {
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
@@ -248,7 +258,14 @@ __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint
   float s0 = 0.f, s1 = 0.f;
   for (int m = lane; m < width; m += 32) {
     s0 = fmaf(w_out[m], ptx::bf16_val(hi[r0 + m]) + ptx::bf16_val(lo[r0 + m]), s0);
-    s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
+    if (!standard) {
+      s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
+    } else {
+      for (int r = 2; r < P; r += 2) {
+        const size_t ri = ((size_t)n * P + r) * ld;
+        s1 = fmaf(w_out[m], ptx::bf16_val(hi[ri + m]) + ptx::bf16_val(lo[ri + m]), s1);
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

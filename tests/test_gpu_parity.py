@@ -93,6 +93,18 @@ def test_laplacian_parity(ctm, widths, N):
     check(op, want, norm, f, fwant)
 
 
+@pytest.mark.parametrize("widths,N", [([2, 2, 1], 3), ([5, 16, 16, 1], 8), (C1_WIDTHS, 61)])
+def test_laplacian_standard_mode_parity(ctm, widths, N):
+    """NEXT-1: standard (uncollapsed) Taylor mode gives the same operator (Eq. 7 is exact)."""
+    params, onet = nets(widths)
+    X = points(N, widths[0])
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.laplacian_standard(torch.from_numpy(X).cuda())
+    assert mlp.last_plan()["slots_per_point"] == 1 + 2 * widths[0]
+    want, fwant, norm = O.laplacian(onet, X.astype(np.float64), O.O1)
+    check(op, want, norm, f, fwant)
+
+
 def test_golden_g1_net(ctm):
     # SURVEY §8(c) G1: W1 = [[.5,-.25],[.3,.8]], b1 = [.1,-.2], w2 = [1.5,-.7], b2 = .05
     params = [(np.array([[0.5, -0.25], [0.3, 0.8]], np.float32), np.array([0.1, -0.2], np.float32)),
