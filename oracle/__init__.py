@@ -64,6 +64,7 @@ def lib():
         _lib.ctmo_weighted_laplacian.argtypes = [P(_Net), vp, i64, vp, i32, i32, vp, vp, vp]
         _lib.ctmo_randomized_laplacian.argtypes = [P(_Net), vp, i64, vp, i32, vp, i32, i32, vp, vp, vp]
         _lib.ctmo_forward.argtypes = [P(_Net), vp, i64, vp]
+        _lib.ctmo_stochastic_biharmonic.argtypes = [P(_Net), vp, i64, vp, i32, i32, vp, vp, vp]
         _lib.ctmo_act_derivs.argtypes = [i32, d, vp]
         _lib.ctmo_act_derivs.restype = None
         _lib.ctmo_gamma.argtypes = [i32, i32, i32, i32, P(ctypes.c_int64), P(ctypes.c_int64)]
@@ -151,6 +152,12 @@ def randomized_laplacian(net: Net, X, V, sigma=None, route=O1):
 def biharmonic(net: Net, X, route=O1):
     """Exact biharmonic (Eq. 12) via the interpolation family (O1/O3) or T4 (O2)."""
     return _call(lib().ctmo_biharmonic, net, X, route=route)
+
+
+def stochastic_biharmonic(net: Net, X, V, route=O1):
+    """1/(3S) sum_s <d^4 f, v_s^4> with V [N, S, D] (Eq. 12 stochastic, unbiased scale, Q1)."""
+    V = _f64(V)
+    return _call(lib().ctmo_stochastic_biharmonic, net, X, _ptr(V), V.shape[1], route=route)
 
 
 def forward(net: Net, X) -> np.ndarray:

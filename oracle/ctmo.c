@@ -391,9 +391,11 @@ static void route_o3(const ctmo_net *net, const dirset_t *ds, const double *X, i
  * K=2 needs orders 1-2; K=4 orders 1-4 (D^4 entries per unit). */
 static int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; return r; }
 
-/* C2 [D*D] coefficient matrix (K=2) or, for K=4, biharmonic flag (C is
- * e_a (x) e_a (x) e_b (x) e_b summed). Returns <d^K f, C> per point. */
+/* C2 [D*D] coefficient matrix (K=2). For K=4: if dirs4 is NULL, C is the biharmonic
+ * tensor sum_{a,b} e_a (x) e_a (x) e_b (x) e_b; otherwise C = c4 sum_s v_s^{(x)4} with the
+ * per-point directions dirs4 [N, S4, D]. Returns <d^K f, C> per point. */
 static void route_o2(const ctmo_net *net, int K, const double *C2, int C2_per_point,
+                     const double *dirs4, int S4, double c4,
                      const double *X, int64_t N, double *op, double *f)
 {
     const int D = net->widths[0], L = net->L, wm = max_width(net);
@@ -488,10 +490,19 @@ static void route_o2(const ctmo_net *net, int K, const double *C2, int C2_per_po
                 const double *C = C2_per_point ? C2 + (size_t)n * D * D : C2;
                 for (int a = 0; a < D; ++a)
                     for (int b = 0; b < D; ++b) val += H[a * D + b] * C[a * D + b];
-            } else {
+            } else if (!dirs4) {
                 const double *T4 = A + toff[4];
                 for (int a = 0; a < D; ++a)
                     for (int b = 0; b < D; ++b) val += T4[I4(a, a, b, b)];
+            } else {
+                const double *T4 = A + toff[4];
+                for (int s = 0; s < S4; ++s) {
+                    const double *v = dirs4 + ((size_t)n * S4 + s) * D;
+                    for (int a = 0; a < D; ++a)
+                        for (int b = 0; b < D; ++b)
+                            for (int c = 0; c < D; ++c)
+                                for (int e = 0; e < D; ++e) val += c4 * T4[I4(a, b, c, e)] * v[a] * v[b] * v[c] * v[e];
+                }
             }
             op[n] = val;
             if (f) f[n] = a0[0];
@@ -523,7 +534,7 @@ int ctmo_laplacian(const ctmo_net *net, const double *X, int64_t N, int32_t rout
     if (route == CTMO_O2) {
         double *C = calloc((size_t)D * D, sizeof(double));
         for (int a = 0; a < D; ++a) C[a * D + a] = 1.0; /* <d^2 f, I_D> */
-        route_o2(net, 2, C, 0, X, N, op, f);
+        route_o2(net, 2, C, 0, NULL, 0, 0.0, X, N, op, f);
         free(C);
         fill_nan(norm, N);
         return 0;
@@ -553,7 +564,7 @@ int ctmo_weighted_laplacian(const ctmo_net *net, const double *X, int64_t N,
         for (int a = 0; a < D; ++a)
             for (int b = 0; b < D; ++b)
                 for (int r = 0; r < R; ++r) C[a * D + b] += sigma[a * R + r] * sigma[b * R + r];
-        route_o2(net, 2, C, 0, X, N, op, f);
+        route_o2(net, 2, C, 0, NULL, 0, 0.0, X, N, op, f);
         free(C);
         fill_nan(norm, N);
         return 0;
@@ -603,7 +614,7 @@ int ctmo_randomized_laplacian(const ctmo_net *net, const double *X, int64_t N,
                 for (int a = 0; a < D; ++a)
                     for (int b = 0; b < D; ++b) C[(size_t)n * D * D + a * D + b] += u[a] * u[b] / S;
             }
-        route_o2(net, 2, C, 1, X, N, op, f);
+        route_o2(net, 2, C, 1, NULL, 0, 0.0, X, N, op, f);
         free(C);
         fill_nan(norm, N);
     } else {
@@ -716,7 +727,7 @@ int ctmo_biharmonic(const ctmo_net *net, const double *X, int64_t N, int32_t rou
     init_partitions();
     const int D = net->widths[0];
     if (route == CTMO_O2) {
-        route_o2(net, 4, NULL, 0, X, N, op, f);
+        route_o2(net, 4, NULL, 0, NULL, 0, 0.0, X, N, op, f);
         fill_nan(norm, N);
         return 0;
     }
@@ -737,6 +748,29 @@ int ctmo_biharmonic(const ctmo_net *net, const double *X, int64_t N, int32_t rou
     else rc = 1;
     free(dirs); free(coef); free(group);
     return rc;
+}
+
+/* Stochastic biharmonic, Eq. 12 stochastic case: the paper prints the
+ * scale D/S; with standard normal v, Isserlis' theorem gives
+ * E <d^4 f, v^{(x)4}> = 3 Laplacian^2 f, so the unbiased scale is 1/(3S)
+ * (reading Q1). One 4-jet per sample (x1 = v_s, x2 = x3 = x4 = 0),
+ * collapsed over the S samples (1 + 3S + 1 vectors). */
+int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, const double *V, int32_t S,
+                               int32_t route, double *op, double *f, double *norm)
+{
+    if (check_net(net) || N < 0 || S < 1 || (N > 0 && (!X || !op || !V))) return 1;
+    init_partitions();
+    const double c = 1.0 / (3.0 * S);
+    if (route == CTMO_O2) {
+        route_o2(net, 4, NULL, 0, V, S, c, X, N, op, f);
+        fill_nan(norm, N);
+        return 0;
+    }
+    dirset_t ds = {4, S, 1, V, 1, NULL, &c};
+    if (route == CTMO_O1) route_o1(net, &ds, X, N, op, f, norm);
+    else if (route == CTMO_O3) { route_o3(net, &ds, X, N, op, f); fill_nan(norm, N); }
+    else return 1;
+    return 0;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -71,6 +71,12 @@ int ctmo_randomized_laplacian(const ctmo_net *net, const double *X, int64_t N,
 int ctmo_biharmonic(const ctmo_net *net, const double *X, int64_t N, int32_t route,
                     double *op, double *f, double *norm);
 
+/* Stochastic biharmonic, Eq. 12 stochastic case, with the unbiased scale
+ * 1/(3S) for standard normal directions (the printed D/S is read as garbled, DESIGN.md
+ * Q1): op = 1/(3S) sum_s <d^4 f, v_s^{(x)4}>, V [N, S, D] the drawn directions. */
+int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, const double *V, int32_t S,
+                               int32_t route, double *op, double *f, double *norm);
+
 /* sigma^(k)(z), k = 0..4, of the activation (d must hold 5 doubles). */
 void ctmo_act_derivs(int32_t act, double z, double *d);
 

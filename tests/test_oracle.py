@@ -404,3 +404,39 @@ def test_rademacher_estimator_unbiased_and_variance():
     se = math.sqrt(var_theory / T)
     assert abs(est.mean() - exact) < 4 * se
     assert abs(est.var() / var_theory - 1) < 0.15
+
+
+# --------------------------------------------------------------------------
+# Stochastic biharmonic (Eq. 12 stochastic case, unbiased 1/(3S) scale: reading Q1)
+# --------------------------------------------------------------------------
+def test_stochastic_biharmonic_routes_agree():
+    D = 4
+    net = _mid_net(D, 111)
+    X = _pts(3, D, seed=112)
+    V = np.random.default_rng(113).standard_normal((3, 5, D))
+    o1, _, norm = O.stochastic_biharmonic(net, X, V, O.O1)
+    assert rel_err(O.stochastic_biharmonic(net, X, V, O.O3)[0], o1, norm) < 1e-12
+    assert rel_err(O.stochastic_biharmonic(net, X, V, O.O2)[0], o1, norm) < 1e-11
+
+
+@pytest.mark.parametrize("route", ROUTES)
+def test_stochastic_biharmonic_norm4_closed_form(route):
+    # f = ||x||^4: d^4/dt^4 ||x + t v||^4 = 24 ||v||^4, so the estimator is 8/S sum_s ||v_s||^4
+    D = 3
+    net = _norm4_net(D)
+    X = _pts(2, D)
+    V = np.random.default_rng(121).standard_normal((2, 6, D))
+    want = 8.0 / 6 * np.sum(np.sum(V**2, axis=2) ** 2, axis=1)
+    np.testing.assert_allclose(O.stochastic_biharmonic(net, X, V, route)[0], want, rtol=1e-12)
+
+
+def test_stochastic_biharmonic_unbiased_for_gaussian():
+    # E <d^4 f, v^4> = 3 Laplacian^2 f for v ~ N(0, I) (Isserlis); mean within 4 SE
+    D = 3
+    net = _mid_net(D, 131)
+    x = _pts(1, D, seed=132)
+    exact = O.biharmonic(net, x, O.O2)[0][0]
+    T = 20000
+    V = np.random.default_rng(133).standard_normal((T, 1, D))
+    est = O.stochastic_biharmonic(net, np.repeat(x, T, axis=0), V, O.O3)[0]
+    assert abs(est.mean() - exact) < 4 * est.std() / math.sqrt(T)
