@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
-    ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard"],
+    ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard",
+                                   "stochastic_biharmonic"],
                     default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -57,13 +58,14 @@ def parse():
 def workload(args):
     from synth import widths_for
 
-    D = 5 if args.op == "biharmonic" else 50
+    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic") else 50
     names = {
         "laplacian": "C1 exact Laplacian",
         "standard": "C1 exact Laplacian by STANDARD Taylor mode (1+2D vectors; the paper's baseline)",
         "weighted": "C2 weighted Laplacian (dense full-rank sigma, R=50)",
         "randomized": f"C3 randomized Laplacian (Rademacher, S={args.S}, generated in-kernel)",
         "biharmonic": "C4 exact biharmonic (interpolation family, J=35)",
+        "stochastic_biharmonic": f"stochastic biharmonic (Gaussian, S={args.S}, generated in-kernel)",
     }
     w = widths_for(D)
     return D, w, f"{names[args.op]}, tanh MLP {'-'.join(map(str, w[:-1]))}-1, N={args.n} points per GPU"
@@ -137,6 +139,9 @@ def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
             O.weighted_laplacian(net, X, sig, O.O1)
         elif op == "randomized":
             O.randomized_laplacian(net, X, O.rademacher(2, 0, X.shape[0], S, D), route=O.O1)
+        elif op == "stochastic_biharmonic":
+            V = np.random.default_rng(2).standard_normal((X.shape[0], S, D))
+            O.stochastic_biharmonic(net, X, V, O.O1)
         else:
             O.biharmonic(net, X, O.O1)
 
@@ -221,6 +226,8 @@ def main():
             mlp.weighted_laplacian(Xd, sig, out=op_out, f_out=f_out)
         elif args.op == "randomized":
             mlp.randomized_laplacian(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out)
+        elif args.op == "stochastic_biharmonic":
+            mlp.stochastic_biharmonic(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out)
         else:
             mlp.biharmonic(Xd, out=op_out, f_out=f_out)
 

@@ -91,10 +91,10 @@ ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, cons
 /* Randomized (Hutchinson) Laplacian, Eq. 8/10 stochastic cases:
  * op[n] = (1/S) sum_s <d^2 f(x_n), (sigma v_{n,s})^{(x)2}>, directions i.i.d. per
  * point.
- *   V [N, S, Rv] explicit directions, or NULL to generate Rademacher directions
- *     in-kernel: v_{n,s,d} = sign from splitmix64(seed, ((point_offset+n)*S+s)*Rv+d)
- *     (top bit set -> -1), SURVEY §8(c) O5. dist must be CTM_RADEMACHER when V
- *     is NULL (Gaussian directions are passed explicitly).
+ *   V [N, S, Rv] explicit directions, or NULL to generate them in-kernel from the
+ *     counter i = ((point_offset+n)*S+s)*Rv+d: CTM_RADEMACHER = sign of splitmix64(seed, i)
+ *     (top bit set -> -1); CTM_GAUSSIAN = Box-Muller on splitmix64
+ *     counters 2i, 2i+1 (parity tests pass Gaussian V explicitly).
  *   point_offset: global index of X[0] (shard-invariant generation), >= 0.
  *   sigma [D, Rv] or NULL (then Rv must equal D). 1 <= S, S + 2 <= 256. */
 ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S,
@@ -108,6 +108,17 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, in
  * ONE weighted top slot (P = 3J + 2 <= 256, i.e. D <= 7). */
 ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                           void *stream);
+
+/* Stochastic biharmonic, Eq. 12 stochastic case, collapsed over S samples
+ * (1 + 3S + 1 vectors): op[n] = 1/(3S) sum_s <d^4 f(x_n), v_{n,s}^{(x)4}> with
+ * standard normal v (the printed scale D/S is read as garbled: Isserlis gives
+ * E<d^4 f, v^4> = 3 Laplacian^2 f, Q1).
+ *   V [N, S, D] explicit directions, or NULL: generated in-kernel (Box-Muller on the
+ *   splitmix64 counters 2i, 2i+1 of i = ((point_offset+n)*S+s)*D+d).
+ *   dist must be CTM_GAUSSIAN. P = 3S + 2 <= 256 (S <= 84). */
+ctm_status ctm_stochastic_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S, const float *V,
+                                     ctm_dist dist, uint64_t seed, int64_t point_offset, float *op_out,
+                                     float *f_out, void *stream);
 
 /* Static message for a status. */
 const char *ctm_status_str(ctm_status s);

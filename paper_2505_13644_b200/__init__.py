@@ -32,6 +32,8 @@ ABI = {
         [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _I32, _VP, _VP, _VP],
     ),
     "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
+                                                 _VP]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "ctm_last_error": (ctypes.c_char_p, []),
     "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
@@ -178,6 +180,21 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_biharmonic(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                     _stream_ptr(stream, self.device)), "ctm_biharmonic")
+        return out, f_out
+
+    def stochastic_biharmonic(self, X, S=None, V=None, seed=0, point_offset=0, out=None, f_out=None, want_f=True,
+                              stream=None):
+        """1/(3S) sum_s <d^4 f, v_s^4>, v_s ~ N(0, I) (Eq. 12 stochastic; V [N, S, D] or generated)."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        if V is not None:
+            V = _dev_f32(V, self.device, "V")
+            S = V.shape[1]
+        if S is None:
+            raise CTMError("S is required when V is not given")
+        _check(lib().ctm_stochastic_biharmonic(self._h, X.data_ptr(), N, int(S), self._p(V), CTM_GAUSSIAN,
+                                               int(seed) & (2**64 - 1), int(point_offset), out.data_ptr(),
+                                               self._p(f_out), _stream_ptr(stream, self.device)),
+               "ctm_stochastic_biharmonic")
         return out, f_out
 
     def last_plan(self) -> dict:

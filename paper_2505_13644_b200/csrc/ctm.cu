@@ -111,6 +111,7 @@ struct ctm_mlp {
   float* U_bih = nullptr;     // [J, ld1]
   float* c_bih = nullptr;     // [ld1]
   float* w_bih = nullptr;     // [J] jet weights
+  float* w_ones = nullptr;    // [kMaxJets] unit weights (stochastic biharmonic: plain sum over samples)
   int J_bih = 0;
   // per-call scratch
   float* U_call = nullptr;
@@ -147,7 +148,7 @@ ctm_status free_all(ctm_mlp* h) {
   for (auto& p : h->Whi) F(p);
   for (auto& p : h->Wlo) F(p);
   for (auto& p : h->bias) F(p);
-  F(h->U_lap); F(h->c_lap); F(h->U_bih); F(h->c_bih); F(h->w_bih);
+  F(h->U_lap); F(h->c_lap); F(h->w_ones); F(h->U_bih); F(h->c_bih); F(h->w_bih);
   F(h->U_call); F(h->c_call);
   for (int i = 0; i < 2; ++i)
     for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
@@ -276,7 +277,7 @@ Plan make_plan(int P) {
   return pl;
 }
 
-enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD };
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH };
 
 struct CallArgs {
   Op op;
@@ -289,6 +290,7 @@ struct CallArgs {
   uint64_t seed;
   int64_t point_offset;
   int Rv;
+  int gaussian;
   float* op_out;
   float* f_out;
   cudaStream_t stream;
@@ -297,7 +299,7 @@ struct CallArgs {
 ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int D = h->widths[0];
   const int ld1 = h->wpad[1];
-  const int KORD = (a.op == OP_BIH) ? 4 : (a.op == OP_LAP_STD) ? ctm::kStd2 : 2;
+  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH) ? 4 : (a.op == OP_LAP_STD) ? ctm::kStd2 : 2;
   int P = 0;
   switch (a.op) {
     case OP_LAP: P = D + 2; break;
@@ -305,6 +307,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     case OP_RLAP: P = a.S + 2; break;
     case OP_BIH: P = 3 * h->J_bih + 2; break;
     case OP_LAP_STD: P = 1 + 2 * D; break;
+    case OP_SBIH: P = 3 * a.S + 2; break;
   }
   if (P > ctm::kMaxN)
     return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
@@ -333,7 +336,33 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     int kpad, mpad, w_in, w_out;
   };
   std::vector<GemmLayer> layers;
-  if (a.op == OP_RLAP) {
+  if (a.op == OP_SBIH) {
+    // stochastic biharmonic: layer 1 in fp32 with the per-point Gaussian directions
+    if ((int64_t)a.S * D > 12288) return fail(CTM_EUNSUPPORTED, "S * D > 12288 for the stochastic biharmonic");
+    ctm::SeedStochParams bp{};
+    bp.X = a.X;
+    bp.D = D;
+    bp.W1T = h->W1T;
+    bp.b1 = h->b1;
+    bp.ld = ld1;
+    bp.S = a.S;
+    bp.V = a.V;
+    bp.seed = a.seed;
+    bp.point_offset = a.point_offset;
+    bp.out_hi = h->blk[0][0];
+    bp.out_lo = h->blk[0][1];
+    const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
+    const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
+    const int64_t blocks = a.N * mchunks;
+    if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+    {
+      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
+      ctm::seed_stoch_biharmonic_kernel<<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
+    }
+    ++launches;
+    cur = 0;
+    scale = 1.f / (3.f * (float)a.S);  // Eq. 12 stochastic with the unbiased scale (reading Q1)
+  } else if (a.op == OP_RLAP) {
     // per-point directions: write the input block [x0; u_1..u_S; 0] and run layer 1 as a
     // tensor-core layer like the others
     ctm::SeedRandomParams rp{};
@@ -346,6 +375,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.sigma = a.sigma;
     rp.seed = a.seed;
     rp.point_offset = a.point_offset;
+    rp.gaussian = a.gaussian;
     rp.out_hi = h->blk[1][0];
     rp.out_lo = h->blk[1][1];
     {
@@ -354,7 +384,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     }
     ++launches;
     cur = 1;
-    scale = 1.f / (float)a.S;
+    scale = 1.f / (float)a.S;  // Eq. 8/10 stochastic
     layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
   } else {
     ctm::SeedParams sp{};
@@ -439,8 +469,8 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     lp.pts_per_tile = pl.ppt;
     lp.n_mma = pl.nmma;
     lp.k_iters = gl.kpad / ctm::kBK;
-    lp.jet_w = h->w_bih;
-    lp.J = h->J_bih;
+    lp.jet_w = (a.op == OP_SBIH) ? h->w_ones : h->w_bih;
+    lp.J = (a.op == OP_SBIH) ? a.S : h->J_bih;
     if (last) {
       s = ensure(h->partial, h->partial_elems, (size_t)a.N * m_tiles * 2);
       if (s != CTM_OK) return s;
@@ -632,6 +662,11 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
       cudaFree(dv);
     }
   }
+  {
+    std::vector<float> ones(ctm::kMaxJets, 1.f);
+    LOAD_CUDA(cudaMalloc(&h->w_ones, sizeof(float) * ones.size()));
+    LOAD_CUDA(cudaMemcpy(h->w_ones, ones.data(), sizeof(float) * ones.size(), cudaMemcpyHostToDevice));
+  }
   LOAD_CUDA(cudaGetLastError());
   LOAD_CUDA(cudaDeviceSynchronize());
 #undef LOAD_CUDA
@@ -654,7 +689,7 @@ ctm_status ctm_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out
   g_last_error.clear();
   ctm_status s = check_common(mlp, X, N, op_out, f_out);
   if (s != CTM_OK) return s;
-  CallArgs a{OP_LAP, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  CallArgs a{OP_LAP, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
 
@@ -663,7 +698,7 @@ ctm_status ctm_laplacian_standard(ctm_mlp_t mlp, const float* X, int64_t N, floa
   g_last_error.clear();
   ctm_status s = check_common(mlp, X, N, op_out, f_out);
   if (s != CTM_OK) return s;
-  CallArgs a{OP_LAP_STD, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  CallArgs a{OP_LAP_STD, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
 
@@ -674,7 +709,7 @@ ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, cons
   if (s != CTM_OK) return s;
   if (R < 1 || !sigma) return fail(CTM_EINVAL, "need sigma and R >= 1");
   if (!aligned16(sigma)) return fail(CTM_ESHAPE, "sigma must be 16-byte aligned");
-  CallArgs a{OP_WLAP, X, N, sigma, R, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  CallArgs a{OP_WLAP, X, N, sigma, R, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
 
@@ -686,12 +721,11 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, in
   if (s != CTM_OK) return s;
   if (S < 1 || Rv < 1 || point_offset < 0) return fail(CTM_EINVAL, "need S >= 1, Rv >= 1, point_offset >= 0");
   if (dist != CTM_RADEMACHER && dist != CTM_GAUSSIAN) return fail(CTM_EINVAL, "bad dist");
-  if (!V && dist != CTM_RADEMACHER)
-    return fail(CTM_EUNSUPPORTED, "in-kernel generation is Rademacher only; pass Gaussian directions as V");
   if (!sigma && Rv != mlp->widths[0]) return fail(CTM_ESHAPE, "Rv must equal D when sigma is NULL");
   if ((V && !aligned16(V)) || (sigma && !aligned16(sigma))) return fail(CTM_ESHAPE, "V/sigma must be 16-byte aligned");
   if (Rv > 256) return fail(CTM_EUNSUPPORTED, "Rv > 256");
-  CallArgs a{OP_RLAP, X, N, sigma, 0, S, V, seed, point_offset, Rv, op_out, f_out, (cudaStream_t)stream};
+  CallArgs a{OP_RLAP, X, N, sigma, 0, S, V, seed, point_offset, Rv, dist == CTM_GAUSSIAN, op_out, f_out,
+             (cudaStream_t)stream};
   return run(mlp, a);
 }
 
@@ -701,7 +735,7 @@ ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, float* op_ou
   if (s != CTM_OK) return s;
   if (mlp->J_bih == 0)
     return fail(CTM_EUNSUPPORTED, "biharmonic needs 3J+2 <= 256 slots, i.e. D <= 7");
-  CallArgs a{OP_BIH, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  CallArgs a{OP_BIH, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
 
@@ -738,6 +772,22 @@ ctm_status ctm_profile_read(ctm_mlp_t mlp, double* ms, int64_t* launches, double
   }
   mlp->recs.clear();
   return CTM_OK;
+}
+
+ctm_status ctm_stochastic_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, int32_t S, const float* V,
+                                     ctm_dist dist, uint64_t seed, int64_t point_offset, float* op_out, float* f_out,
+                                     void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (S < 1 || point_offset < 0) return fail(CTM_EINVAL, "need S >= 1 and point_offset >= 0");
+  if (dist != CTM_GAUSSIAN)
+    return fail(CTM_EINVAL, "the stochastic biharmonic needs standard normal directions (CTM_GAUSSIAN)");
+  if (V && !aligned16(V)) return fail(CTM_ESHAPE, "V must be 16-byte aligned");
+  if (mlp->widths[0] > 256) return fail(CTM_EUNSUPPORTED, "D > 256");
+  CallArgs a{OP_SBIH, X, N, nullptr, 0, S, V, seed, point_offset, mlp->widths[0], 1, op_out, f_out,
+             (cudaStream_t)stream};
+  return run(mlp, a);
 }
 
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t* launches, int32_t* slots_per_point, int32_t* points_per_tile,

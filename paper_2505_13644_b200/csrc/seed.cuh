@@ -127,6 +127,94 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
   }
 }
 
+// Stochastic biharmonic (Eq. 12 stochastic), layer 1 in fp32 on the CUDA
+// cores: per point, S standard normal directions v_s (explicit or generated), and for
+// each feature z1_s = W1 v_s; writes h1, h2, h3 per sample (x2 = x3 = 0) and the
+// collapsed top sum_s h4_s = tanh'''' sum_s z1_s^4. K = D is tiny for this operator and
+// the 4th powers would amplify a bf16-pair rounding of W1 and v 4x.
+// grid: one block per (point, 4*blockDim-feature chunk); dynamic smem: S*D floats.
+struct SeedStochParams {
+  const float* X;        // [N, D]
+  int D;
+  const float* W1T;      // [D, ld]
+  const float* b1;       // [ld]
+  int ld;
+  int S;
+  const float* V;        // [N, S, D] or nullptr => generated standard normal
+  uint64_t seed;
+  int64_t point_offset;
+  uint16_t* out_hi;      // [N*(3S+2), ld]
+  uint16_t* out_lo;
+};
+
+__device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx);
+
+__global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(const SeedStochParams p) {
+  extern __shared__ float vsh[];  // [S, D]
+  __shared__ float xs[256];
+  const int feats = 4 * blockDim.x;
+  const int mchunks = (p.ld + feats - 1) / feats;
+  const int64_t n = blockIdx.x / mchunks;
+  const int m = (blockIdx.x % mchunks) * feats + 4 * threadIdx.x;
+  for (int d = threadIdx.x; d < p.D; d += blockDim.x) xs[d] = p.X[n * p.D + d];
+  for (int e = threadIdx.x; e < p.S * p.D; e += blockDim.x) {
+    if (p.V) {
+      vsh[e] = p.V[(size_t)n * p.S * p.D + e];
+    } else {
+      const uint64_t idx = (uint64_t)(p.point_offset + n) * (uint64_t)p.S * (uint64_t)p.D + (uint64_t)e;
+      vsh[e] = gaussian_draw(p.seed, idx);  // e = s * D + d
+    }
+  }
+  __syncthreads();
+  if (m >= p.ld) return;
+  const int P = 3 * p.S + 2;
+  const size_t row0 = (size_t)n * P;
+  float4 z0 = *reinterpret_cast<const float4*>(p.b1 + m);
+  for (int d = 0; d < p.D; ++d) {
+    const float4 w = *reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m);
+    z0.x = fmaf(w.x, xs[d], z0.x);
+    z0.y = fmaf(w.y, xs[d], z0.y);
+    z0.z = fmaf(w.z, xs[d], z0.z);
+    z0.w = fmaf(w.w, xs[d], z0.w);
+  }
+  const float t[4] = {tanhf(z0.x), tanhf(z0.y), tanhf(z0.z), tanhf(z0.w)};
+  float d1[4], d2[4], d3[4], d4[4], acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d1[i] = 1.f - t[i] * t[i];
+    d2[i] = -2.f * t[i] * d1[i];
+    d3[i] = d1[i] * (6.f * t[i] * t[i] - 2.f);
+    d4[i] = 8.f * t[i] * d1[i] * (2.f - 3.f * t[i] * t[i]);
+  }
+  seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+  for (int s = 0; s < p.S; ++s) {
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int d = 0; d < p.D; ++d) {
+      const float4 w = *reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m);
+      const float v = vsh[s * p.D + d];
+      z[0] = fmaf(w.x, v, z[0]);
+      z[1] = fmaf(w.y, v, z[1]);
+      z[2] = fmaf(w.z, v, z[2]);
+      z[3] = fmaf(w.w, v, z[3]);
+    }
+    float h1[4], h2[4], h3[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float z2 = z[i] * z[i];
+      h1[i] = d1[i] * z[i];
+      h2[i] = d2[i] * z2;
+      h3[i] = d3[i] * z2 * z[i];
+      acc[i] = fmaf(z2, z2, acc[i]);
+    }
+    const size_t r = row0 + 1 + 3 * (size_t)s;
+    seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+    seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+    seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+  }
+  seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
+              d4[3] * acc[3]);
+}
+
 // Randomized directions: the layer-1 INPUT block of the collapsed jet,
 // rows [x0; u_1 .. u_S; 0] per point (Eq. 8/10 stochastic seeds),
 // u_s = v_s or sigma v_s, stored as bf16 pairs [N*(S+2), ldk] (ldk = D padded to 32,
@@ -142,9 +230,19 @@ struct SeedRandomParams {
   const float* sigma;    // [D, Rv] or nullptr (then Rv == D)
   uint64_t seed;
   int64_t point_offset;
+  int gaussian;          // generated directions: 0 Rademacher, 1 standard normal
   uint16_t* out_hi;
   uint16_t* out_lo;
 };
+
+// Standard normal draw for counter idx: Box-Muller on two splitmix64 outputs
+// (counters 2 idx and 2 idx + 1), u1 in (0, 1], u2 in [0, 1), 24-bit uniforms.
+__device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx) {
+  const uint64_t a = splitmix64(seed, 2ull * idx), b = splitmix64(seed, 2ull * idx + 1ull);
+  const float u1 = ((float)(a >> 40) + 0.5f) * 5.9604644775390625e-8f;  // 2^-24
+  const float u2 = (float)(b >> 40) * 5.9604644775390625e-8f;
+  return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+}
 
 __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
   __shared__ float vs[kSeedChunk];
@@ -172,7 +270,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
       } else {
         const uint64_t idx =
             ((uint64_t)(p.point_offset + n) * (uint64_t)p.S + (uint64_t)s) * (uint64_t)p.Rv + (uint64_t)r;
-        v = (splitmix64(p.seed, idx) >> 63) ? -1.f : 1.f;
+        v = p.gaussian ? gaussian_draw(p.seed, idx) : ((splitmix64(p.seed, idx) >> 63) ? -1.f : 1.f);
       }
       vs[e] = v;
     }

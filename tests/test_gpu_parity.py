@@ -199,6 +199,35 @@ def test_biharmonic_parity(ctm, widths, N):
     check(op, want, norm, f, fwant)
 
 
+# ------------------------------------------------------------------ stochastic biharmonic (NEXT-2)
+@pytest.mark.parametrize("widths,N,S", [([3, 24, 24, 1], 7, 5), (C4_WIDTHS, 13, 16), (C4_WIDTHS, 3, 84)])
+def test_stochastic_biharmonic_parity(ctm, widths, N, S):
+    params, onet = nets(widths)
+    X = points(N, widths[0])
+    V = gaussian_directions(N, S, widths[0])
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.stochastic_biharmonic(torch.from_numpy(X).cuda(), V=torch.from_numpy(V).cuda())
+    assert mlp.last_plan()["slots_per_point"] == 3 * S + 2
+    want, fwant, norm = O.stochastic_biharmonic(onet, X.astype(np.float64), V.astype(np.float64), O.O1)
+    check(op, want, norm, f, fwant)
+
+
+def test_generated_gaussian_directions_are_unbiased(ctm):
+    """In-kernel Box-Muller draws (bench path): the randomized Laplacian and the stochastic
+    biharmonic averaged over many seeds match the exact operators within 4 standard errors."""
+    params, onet = nets([4, 16, 16, 1])
+    x = np.repeat(points(1, 4), 512, axis=0)
+    Xc = torch.from_numpy(x).cuda()
+    mlp = gpu_mlp(ctm, params)
+    lap = O.laplacian(onet, x[:1].astype(np.float64))[0][0]
+    bih = O.biharmonic(onet, x[:1].astype(np.float64))[0][0]
+    # one draw set per "point" (the 512 copies get different counters): 512 x S samples
+    est_l = mlp.randomized_laplacian(Xc, S=4, seed=11, dist="gaussian")[0].double().cpu().numpy()
+    est_b = mlp.stochastic_biharmonic(Xc, S=4, seed=12)[0].double().cpu().numpy()
+    for est, exact in ((est_l, lap), (est_b, bih)):
+        assert abs(est.mean() - exact) < 4 * est.std() / np.sqrt(est.size) + 1e-6 * abs(exact)
+
+
 # ------------------------------------------------------------------ invariants & edges
 def test_shard_invariance_bitwise(ctm):
     """Splitting a batch into calls (as ranks do) must not change a single bit."""
