@@ -44,5 +44,9 @@ for S in (8, 128):
     run(f"C3 randomized S={S}", 50, lambda m, X, S=S: m.randomized_laplacian(X, S=S, seed=2),
         lambda n, X, V=V: O.randomized_laplacian(n, X, V))
 run("C4 biharmonic", 5, lambda m, X: m.biharmonic(X), lambda n, X: O.biharmonic(n, X))
+run("C1 standard Taylor mode", 50, lambda m, X: m.laplacian_standard(X), lambda n, X: O.laplacian(n, X))
+Vg = np.random.default_rng(7).standard_normal((N, 16, 5)).astype(np.float32)
+run("stochastic biharmonic S=16", 5, lambda m, X: m.stochastic_biharmonic(X, V=torch.from_numpy(Vg).cuda()),
+    lambda n, X: O.stochastic_biharmonic(n, X, Vg.astype(np.float64)))
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(res, open(os.path.join(ROOT, "gpurun_out", "parity_sweep.json"), "w"), indent=1)
