@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -117,9 +118,9 @@ struct ctm_mlp {
   float* U_call = nullptr;
   float* c_call = nullptr;
   size_t U_call_elems = 0;
-  // workspace: two ping-pong blocks (bf16 hi, lo)
-  uint16_t* blk[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  size_t blk_elems = 0;
+  // workspace (bf16 hi, lo planes): see ensure_workspace
+  uint16_t* blk[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  size_t blk_elems[4] = {0, 0, 0, 0};
   float* partial = nullptr;
   size_t partial_elems = 0;
   // last plan
@@ -150,7 +151,7 @@ ctm_status free_all(ctm_mlp* h) {
   for (auto& p : h->bias) F(p);
   F(h->U_lap); F(h->c_lap); F(h->w_ones); F(h->U_bih); F(h->c_bih); F(h->w_bih);
   F(h->U_call); F(h->c_call);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
   F(h->partial);
   for (auto& r : h->recs) {
@@ -173,23 +174,28 @@ ctm_status ensure(float*& p, size_t& have, size_t need) {
   return CTM_OK;
 }
 
-ctm_status ensure_workspace(ctm_mlp* h, int64_t rows) {
-  int ldmax = h->k1pad;
-  for (int l = 1; l < h->L; ++l) ldmax = std::max(ldmax, h->wpad[l]);
-  const size_t need = (size_t)rows * ldmax;
-  if (need > h->blk_elems || !h->blk[0][0]) {
-    for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j) {
-        if (h->blk[i][j]) cudaFree(h->blk[i][j]);
-        h->blk[i][j] = nullptr;
-      }
-    h->blk_elems = 0;
-    for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j) CTM_CUDA(cudaMalloc(&h->blk[i][j], std::max<size_t>(need, 1) * sizeof(uint16_t)));
-    h->blk_elems = need;
+// blk[0], blk[1]: layer ping-pong blocks [rows, ldmax]; blk[2] (and blk[3] if nseed > 1):
+// layer-1 blocks (seed output or random input block) [rows, max(ld1, k1pad)].
+ctm_status ensure_workspace(ctm_mlp* h, int64_t rows, int nseed) {
+  int ldmax = 0;
+  for (int l = 2; l < h->L; ++l) ldmax = std::max(ldmax, h->wpad[l]);
+  const int ld_seed = std::max(h->wpad[1], h->k1pad);
+  const size_t need[4] = {(size_t)rows * ldmax, (size_t)rows * ldmax, (size_t)rows * ld_seed,
+                          nseed > 1 ? (size_t)rows * ld_seed : 0};
+  for (int i = 0; i < 4; ++i) {
+    if (need[i] <= h->blk_elems[i] && (h->blk[i][0] || need[i] == 0)) continue;
+    for (int j = 0; j < 2; ++j) {
+      if (h->blk[i][j]) cudaFree(h->blk[i][j]);
+      h->blk[i][j] = nullptr;
+    }
+    h->blk_elems[i] = 0;
+    for (int j = 0; j < 2; ++j)
+      CTM_CUDA(cudaMalloc(&h->blk[i][j], std::max<size_t>(need[i], 1) * sizeof(uint16_t)));
+    h->blk_elems[i] = need[i];
   }
   return CTM_OK;
 }
+
 
 // The biharmonic direction family of Eq. `ttc_for_biharm_final` with the
 // gamma of Fig. 3 (g40 = 13/192, g31 = -1/3, g22 = 5/8), rescaled so the
@@ -296,175 +302,98 @@ struct CallArgs {
   cudaStream_t stream;
 };
 
-ctm_status run(ctm_mlp* h, const CallArgs& a) {
-  const int D = h->widths[0];
-  const int ld1 = h->wpad[1];
-  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH) ? 4 : (a.op == OP_LAP_STD) ? ctm::kStd2 : 2;
-  int P = 0;
-  switch (a.op) {
-    case OP_LAP: P = D + 2; break;
-    case OP_WLAP: P = a.R + 2; break;
-    case OP_RLAP: P = a.S + 2; break;
-    case OP_BIH: P = 3 * h->J_bih + 2; break;
-    case OP_LAP_STD: P = 1 + 2 * D; break;
-    case OP_SBIH: P = 3 * a.S + 2; break;
-  }
-  if (P > ctm::kMaxN)
-    return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
-  const Plan pl = make_plan(P);
-  h->last_P = pl.P;
-  h->last_ppt = pl.ppt;
-  h->last_nmma = pl.nmma;
-  h->last_launches = 0;
-  if (a.N == 0) return CTM_OK;
+struct GemmLayer {
+  const CUtensorMap* a_hi;
+  const CUtensorMap* a_lo;
+  const float* bias;
+  int kpad, mpad, w_in, w_out;
+};
 
-  DeviceGuard g(h->device);
-  cudaStream_t st = a.stream;
-  int launches = 0;
-  const int64_t rows = a.N * (int64_t)P;
-  if (rows > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "N * slots exceeds 2^31 rows");
-  ctm_status s = ensure_workspace(h, rows);
-  if (s != CTM_OK) return s;
-
-  // ---- layer 1 (the seed of the collapsed jet)
-  float scale = 1.f;
-  int cur;  // workspace block holding the next GEMM layer's input
-  struct GemmLayer {
-    const CUtensorMap* a_hi;
-    const CUtensorMap* a_lo;
-    const float* bias;
-    int kpad, mpad, w_in, w_out;
-  };
-  std::vector<GemmLayer> layers;
+// Layer 1 for fixed direction sets (and the stochastic biharmonic) for points
+// [p0, p0 + n): writes the layer-1 output block into buf.
+ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p0, int64_t n, uint16_t* const* buf,
+                       const float* UT, const float* csum, int R, cudaStream_t st, int& launches) {
+  const int D = h->widths[0], ld1 = h->wpad[1];
+  const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
+  const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
+  const int64_t blocks = n * mchunks;
+  if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+  ProfScope ps(h, CTM_KIND_SEED, (double)n * P * h->widths[1] * 4.0, st);
   if (a.op == OP_SBIH) {
-    // stochastic biharmonic: layer 1 in fp32 with the per-point Gaussian directions
-    if ((int64_t)a.S * D > 12288) return fail(CTM_EUNSUPPORTED, "S * D > 12288 for the stochastic biharmonic");
     ctm::SeedStochParams bp{};
-    bp.X = a.X;
+    bp.X = a.X + p0 * D;
     bp.D = D;
     bp.W1T = h->W1T;
     bp.b1 = h->b1;
     bp.ld = ld1;
     bp.S = a.S;
-    bp.V = a.V;
+    bp.V = a.V ? a.V + p0 * a.S * D : nullptr;
     bp.seed = a.seed;
-    bp.point_offset = a.point_offset;
-    bp.out_hi = h->blk[0][0];
-    bp.out_lo = h->blk[0][1];
-    const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
-    const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
-    const int64_t blocks = a.N * mchunks;
-    if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
-    {
-      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
-      ctm::seed_stoch_biharmonic_kernel<<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
-    }
-    ++launches;
-    cur = 0;
-    scale = 1.f / (3.f * (float)a.S);  // Eq. 12 stochastic with the unbiased scale (reading Q1)
-  } else if (a.op == OP_RLAP) {
-    // per-point directions: write the input block [x0; u_1..u_S; 0] and run layer 1 as a
-    // tensor-core layer like the others
-    ctm::SeedRandomParams rp{};
-    rp.X = a.X;
-    rp.D = D;
-    rp.ldk = h->k1pad;
-    rp.S = a.S;
-    rp.Rv = a.Rv;
-    rp.V = a.V;
-    rp.sigma = a.sigma;
-    rp.seed = a.seed;
-    rp.point_offset = a.point_offset;
-    rp.gaussian = a.gaussian;
-    rp.out_hi = h->blk[1][0];
-    rp.out_lo = h->blk[1][1];
-    {
-      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->k1pad * 4.0, st);
-      ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
-    }
-    ++launches;
-    cur = 1;
-    scale = 1.f / (float)a.S;  // Eq. 8/10 stochastic
-    layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
+    bp.point_offset = a.point_offset + p0;
+    bp.out_hi = buf[0];
+    bp.out_lo = buf[1];
+    ctm::seed_stoch_biharmonic_kernel<<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
   } else {
     ctm::SeedParams sp{};
-    sp.X = a.X;
+    sp.X = a.X + p0 * D;
     sp.D = D;
-    sp.n_points = a.N;
+    sp.n_points = n;
     sp.W1T = h->W1T;
     sp.b1 = h->b1;
     sp.ld = ld1;
     sp.P = P;
-    sp.out_hi = h->blk[0][0];
-    sp.out_lo = h->blk[0][1];
-    if (a.op == OP_LAP || a.op == OP_LAP_STD) {
-      sp.UT = h->U_lap;
-      sp.csum = h->c_lap;
-      sp.R = D;
-    } else if (a.op == OP_BIH) {
-      sp.UT = h->U_bih;
-      sp.csum = h->c_bih;
-      sp.R = h->J_bih;
-    } else {  // weighted: U = W1 sigma for this call
-      s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
-      if (s != CTM_OK) return s;
-      if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
-      {
-        ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
-        ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call,
-                                                                  h->c_call);
-      }
-      ++launches;
-      sp.UT = h->U_call;
-      sp.csum = h->c_call;
-      sp.R = a.R;
-    }
-    const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
-    const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
-    const int64_t blocks = a.N * mchunks;
-    if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
-    {
-      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->widths[1] * 4.0, st);
-      if (KORD == 2)
-        ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
-      else if (KORD == 4)
-        ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
-      else
-        ctm::seed_layer_kernel<ctm::kStd2><<<(unsigned)blocks, threads, 0, st>>>(sp);
-    }
-    ++launches;
-    cur = 0;
+    sp.UT = UT;
+    sp.csum = csum;
+    sp.R = R;
+    sp.out_hi = buf[0];
+    sp.out_lo = buf[1];
+    if (KORD == 2)
+      ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
+    else if (KORD == 4)
+      ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
+    else
+      ctm::seed_layer_kernel<ctm::kStd2><<<(unsigned)blocks, threads, 0, st>>>(sp);
   }
-  for (int l = 2; l <= h->L - 1; ++l) {
-    const int i = l - 2;
-    layers.push_back({&h->mapA_hi[i], &h->mapA_lo[i], h->bias[i], h->wpad[l - 1], h->wpad[l], h->widths[l - 1],
-                      h->widths[l]});
-  }
+  ++launches;
+  return CTM_OK;
+}
 
-  // ---- hidden layers on the tensor cores; the last one reduces against w_out
-  if (layers.empty()) {  // fixed directions and a single hidden layer: read the seed block
+// The tensor-core layers for points [p0, p0 + n), whose first GEMM reads `in`;
+// ping-pongs through blk[0] / blk[1] and ends in the readout of op/f. `after_first`
+// (optional) is recorded on st once the first GEMM (the reader of `in`) is enqueued.
+ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, const std::vector<GemmLayer>& layers,
+                         int64_t p0, int64_t n, uint16_t* const* in, float scale, cudaStream_t st,
+                         cudaEvent_t after_first, int& launches) {
+  const int P = pl.P;
+  const int64_t rows = n * (int64_t)P;
+  if (layers.empty()) {  // a single hidden layer: read the layer-1 block
     const int threads = 256, ppb = threads / 32;
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
-    ctm::readout_block_kernel<<<(unsigned)((a.N + ppb - 1) / ppb), threads, 0, st>>>(
-        h->blk[0][0], h->blk[0][1], ld1, P, h->widths[1], h->w_out, h->b_out, scale, a.N, a.op_out, a.f_out, a.op == OP_LAP_STD);
+    ctm::readout_block_kernel<<<(unsigned)((n + ppb - 1) / ppb), threads, 0, st>>>(
+        in[0], in[1], h->wpad[1], P, h->widths[1], h->w_out, h->b_out, scale, n, a.op_out + p0,
+        a.f_out ? a.f_out + p0 : nullptr, a.op == OP_LAP_STD);
     ++launches;
+    if (after_first) CTM_CUDA(cudaEventRecord(after_first, st));
+    return CTM_OK;
   }
-  const int64_t n_tiles = (a.N + pl.ppt - 1) / pl.ppt;
+  const int64_t n_tiles = (n + pl.ppt - 1) / pl.ppt;
+  uint16_t* const* src = in;
+  int dst = 0;
   for (size_t li = 0; li < layers.size(); ++li) {
     const GemmLayer& gl = layers[li];
     const int m_tiles = gl.mpad / ctm::kBM;
     const bool last = (li + 1 == layers.size());
     CUtensorMap mb_hi, mb_lo;
-    if (!make_map(&mb_hi, h->blk[cur][0], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma) ||
-        !make_map(&mb_lo, h->blk[cur][1], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma))
+    if (!make_map(&mb_hi, src[0], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma) ||
+        !make_map(&mb_lo, src[1], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma))
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
     ctm::LayerParams lp{};
     lp.bias = gl.bias;
-    lp.out_hi = h->blk[cur ^ 1][0];
-    lp.out_lo = h->blk[cur ^ 1][1];
+    lp.out_hi = h->blk[dst][0];
+    lp.out_lo = h->blk[dst][1];
     lp.ldo = gl.mpad;
     lp.m_tiles = m_tiles;
-    lp.n_points = a.N;
+    lp.n_points = n;
     lp.P = P;
     lp.pts_per_tile = pl.ppt;
     lp.n_mma = pl.nmma;
@@ -472,7 +401,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     lp.jet_w = (a.op == OP_SBIH) ? h->w_ones : h->w_bih;
     lp.J = (a.op == OP_SBIH) ? a.S : h->J_bih;
     if (last) {
-      s = ensure(h->partial, h->partial_elems, (size_t)a.N * m_tiles * 2);
+      ctm_status s = ensure(h->partial, h->partial_elems, (size_t)n * m_tiles * 2);
       if (s != CTM_OK) return s;
       lp.readout = 1;
       lp.w_out = h->w_out;
@@ -480,7 +409,8 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     }
     const int64_t grid = std::min<int64_t>(n_tiles * m_tiles, h->sm_count);  // persistent
     {
-      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * a.N * P * gl.w_in * gl.w_out, st);
+      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * n * P * gl.w_in * gl.w_out, st);
+      ctm_status s;
       if (KORD == 2) {
         s = set_layer_attr<2>(h);
         if (s != CTM_OK) return s;
@@ -499,13 +429,114 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       }
     }
     ++launches;
+    if (li == 0 && after_first) CTM_CUDA(cudaEventRecord(after_first, st));
     if (last) {
       ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
-      ctm::finalize_kernel<<<(unsigned)((a.N + 255) / 256), 256, 0, st>>>(h->partial, m_tiles, a.N, h->b_out, scale,
-                                                                         a.op_out, a.f_out);
+      ctm::finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+          h->partial, m_tiles, n, h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr);
       ++launches;
     }
-    cur ^= 1;
+    src = h->blk[dst];
+    dst ^= 1;
+  }
+  return CTM_OK;
+}
+
+ctm_status run(ctm_mlp* h, const CallArgs& a) {
+  const int D = h->widths[0];
+  const int ld1 = h->wpad[1];
+  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH) ? 4 : (a.op == OP_LAP_STD) ? ctm::kStd2 : 2;
+  int P = 0;
+  switch (a.op) {
+    case OP_LAP: P = D + 2; break;
+    case OP_WLAP: P = a.R + 2; break;
+    case OP_RLAP: P = a.S + 2; break;
+    case OP_BIH: P = 3 * h->J_bih + 2; break;
+    case OP_LAP_STD: P = 1 + 2 * D; break;
+    case OP_SBIH: P = 3 * a.S + 2; break;
+  }
+  if (P > ctm::kMaxN)
+    return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
+  if (a.op == OP_SBIH && (int64_t)a.S * D > 12288)
+    return fail(CTM_EUNSUPPORTED, "S * D > 12288 for the stochastic biharmonic");
+  const Plan pl = make_plan(P);
+  h->last_P = pl.P;
+  h->last_ppt = pl.ppt;
+  h->last_nmma = pl.nmma;
+  h->last_launches = 0;
+  if (a.N == 0) return CTM_OK;
+  if (a.N * (int64_t)P > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "N * slots exceeds 2^31 rows");
+
+  DeviceGuard g(h->device);
+  cudaStream_t st = a.stream;
+  int launches = 0;
+  ctm_status s;
+
+  // GEMM layers: layer 1 for per-point K=2 directions, then the hidden layers 2..L-1
+  std::vector<GemmLayer> layers;
+  if (a.op == OP_RLAP) layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
+  for (int l = 2; l <= h->L - 1; ++l)
+    layers.push_back({&h->mapA_hi[l - 2], &h->mapA_lo[l - 2], h->bias[l - 2], h->wpad[l - 1], h->wpad[l],
+                      h->widths[l - 1], h->widths[l]});
+
+  if (a.op == OP_RLAP) {
+    // per-point K=2 directions: the input block [x0; u_1..u_S; 0], then layer 1 on the
+    // tensor cores like every other layer
+    s = ensure_workspace(h, a.N * (int64_t)P, 1);
+    if (s != CTM_OK) return s;
+    ctm::SeedRandomParams rp{};
+    rp.X = a.X;
+    rp.D = D;
+    rp.ldk = h->k1pad;
+    rp.S = a.S;
+    rp.Rv = a.Rv;
+    rp.V = a.V;
+    rp.sigma = a.sigma;
+    rp.seed = a.seed;
+    rp.point_offset = a.point_offset;
+    rp.gaussian = a.gaussian;
+    rp.out_hi = h->blk[2][0];
+    rp.out_lo = h->blk[2][1];
+    {
+      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->k1pad * 4.0, st);
+      ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
+    }
+    ++launches;
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, h->blk[2], 1.f / (float)a.S, st, nullptr, launches);
+    if (s != CTM_OK) return s;
+  } else {
+    // fixed direction sets (or the K=4 stochastic seed): U and the per-feature constant
+    const float* UT = h->U_lap;
+    const float* csum = h->c_lap;
+    int R = D;
+    if (a.op == OP_BIH) {
+      UT = h->U_bih;
+      csum = h->c_bih;
+      R = h->J_bih;
+    } else if (a.op == OP_WLAP) {  // U = W1 sigma for this call
+      s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
+      if (s != CTM_OK) return s;
+      if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
+      {
+        ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
+        ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call,
+                                                                  h->c_call);
+      }
+      ++launches;
+      UT = h->U_call;
+      csum = h->c_call;
+      R = a.R;
+    }
+    const float scale = (a.op == OP_SBIH) ? 1.f / (3.f * (float)a.S) : 1.f;  // Eq. 12 stochastic: 1/(3S), Q1
+    // Sequential: running the HBM-write-bound seed of one chunk beside the power-capped
+    // tensor-core layers of another was measured slower (2.58-2.65 M vs 2.68 M points/s at
+    // C1): the two compete for the 1 kW budget rather than for SMs.
+    s = ensure_workspace(h, a.N * (int64_t)P, 1);
+    if (s != CTM_OK) return s;
+    s = launch_seed(h, a, KORD, P, 0, a.N, h->blk[2], UT, csum, R, st, launches);
+    if (s != CTM_OK) return s;
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, h->blk[2], scale, st, nullptr, launches);
+    if (s != CTM_OK) return s;
   }
   CTM_CUDA(cudaGetLastError());
   h->last_launches = launches;

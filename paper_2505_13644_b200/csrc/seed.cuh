@@ -68,9 +68,9 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
   __syncthreads();
   if (m >= p.ld) return;  // ld is a multiple of 128: a thread's 4 features are all in or all out
   const size_t row0 = (size_t)n * p.P;
-  float4 z0 = *reinterpret_cast<const float4*>(p.b1 + m);
+  float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
   for (int d = 0; d < p.D; ++d) {
-    const float4 w = *reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m);
+    const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
     z0.x = fmaf(w.x, xs[d], z0.x);
     z0.y = fmaf(w.y, xs[d], z0.y);
     z0.z = fmaf(w.z, xs[d], z0.z);
@@ -86,19 +86,32 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
     d4[i] = 8.f * t[i] * d1[i] * (2.f - 3.f * t[i] * t[i]);  // tanh''''
   }
   seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
-  const float4 cs = *reinterpret_cast<const float4*>(p.csum + m);
+  const float4 cs = __ldg(reinterpret_cast<const float4*>(p.csum + m));
   if (KORD == kStd2) {
     // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
+#pragma unroll 4
     for (int r = 0; r < p.R; ++r) {
-      const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m);
+      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m));
       const size_t rr = row0 + 1 + 2 * r;
       seed_store4(p.out_hi, p.out_lo, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
       seed_store4(p.out_hi, p.out_lo, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
     }
   } else if (KORD == 2) {
-    for (int r = 0; r < p.R; ++r) {
-      const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m);
+    // batches of 4 rows: the 4 loads of U are in flight together (latency, not bandwidth,
+    // bounded this loop when each load fed its stores one at a time)
+    int r = 0;
+    for (; r + 4 <= p.R; r += 4) {
+      float4 u[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)(r + i) * p.ld + m));
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
+                    d1[2] * u[i].z, d1[3] * u[i].w);
+    }
+    for (; r < p.R; ++r) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m));
       seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
                   d1[3] * u.w);
     }
@@ -107,7 +120,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
                 d2[3] * cs.w);
   } else {
     for (int j = 0; j < p.R; ++j) {
-      const float4 u = *reinterpret_cast<const float4*>(p.UT + (size_t)j * p.ld + m);
+      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)j * p.ld + m));
       const float z[4] = {u.x, u.y, u.z, u.w};
       float h1[4], h2[4], h3[4];
 #pragma unroll
@@ -169,9 +182,9 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   if (m >= p.ld) return;
   const int P = 3 * p.S + 2;
   const size_t row0 = (size_t)n * P;
-  float4 z0 = *reinterpret_cast<const float4*>(p.b1 + m);
+  float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
   for (int d = 0; d < p.D; ++d) {
-    const float4 w = *reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m);
+    const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
     z0.x = fmaf(w.x, xs[d], z0.x);
     z0.y = fmaf(w.y, xs[d], z0.y);
     z0.z = fmaf(w.z, xs[d], z0.z);
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   for (int s = 0; s < p.S; ++s) {
     float z[4] = {0.f, 0.f, 0.f, 0.f};
     for (int d = 0; d < p.D; ++d) {
-      const float4 w = *reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m);
+      const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
       const float v = vsh[s * p.D + d];
       z[0] = fmaf(w.x, v, z[0]);
       z[1] = fmaf(w.y, v, z[1]);

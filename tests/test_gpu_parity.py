@@ -245,6 +245,24 @@ def test_shard_invariance_bitwise(ctm):
     assert torch.equal(full, again)  # run-to-run determinism
 
 
+@pytest.mark.parametrize("op", ["laplacian", "biharmonic", "stochastic_biharmonic", "laplacian_standard"])
+def test_split_batches_are_bitwise_equal(ctm, op):
+    """One call over 5001 points equals two calls over its halves bit for bit, for every
+    kernel family (fixed K=2, K=4, per-point K=4 directions, standard mode)."""
+    D = 5 if "biharmonic" in op else 50
+    params, _ = nets(widths_for(D))
+    N = 5001
+    X = torch.from_numpy(points(N, D)).cuda()
+    mlp = gpu_mlp(ctm, params)
+    kw = {"S": 6, "seed": 3} if op == "stochastic_biharmonic" else {}
+    fn = getattr(mlp, op)
+    full = fn(X, **kw)[0].clone()
+    kw2 = dict(kw, point_offset=2500) if kw else {}
+    parts = torch.cat([fn(X[:2500], **kw)[0].clone(), fn(X[2500:], **kw2)[0].clone()])
+    torch.cuda.synchronize()
+    assert torch.equal(full, parts)
+
+
 def test_empty_batch_is_noop(ctm):
     params, _ = nets([5, 16, 16, 1])
     mlp = gpu_mlp(ctm, params)
