@@ -384,8 +384,8 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     const int m_tiles = gl.mpad / ctm::kBM;
     const bool last = (li + 1 == layers.size());
     CUtensorMap mb_hi, mb_lo;
-    if (!make_map(&mb_hi, src[0], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma) ||
-        !make_map(&mb_lo, src[1], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma))
+    if (!make_map(&mb_hi, src[0], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma / 2) ||
+        !make_map(&mb_lo, src[1], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma / 2))  // a CTA stages half of B
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
     ctm::LayerParams lp{};
     lp.bias = gl.bias;
@@ -407,7 +407,8 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       lp.w_out = h->w_out;
       lp.partial = h->partial;
     }
-    const int64_t grid = std::min<int64_t>(n_tiles * m_tiles, h->sm_count);  // persistent
+    // persistent CTA pairs: an even grid, at most one CTA per SM
+    const int64_t grid = 2 * std::min<int64_t>(n_tiles * (m_tiles / 2), h->sm_count / 2);
     {
       ProfScope ps(h, CTM_KIND_LAYER, 2.0 * n * P * gl.w_in * gl.w_out, st);
       ctm_status s;
@@ -596,7 +597,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
   h->L = n_layers;
   h->widths.assign(widths, widths + n_layers + 1);
   h->wpad.assign(n_layers + 1, 0);
-  for (int l = 1; l < n_layers; ++l) h->wpad[l] = round_up(widths[l], ctm::kBM);
+  for (int l = 1; l < n_layers; ++l) h->wpad[l] = round_up(widths[l], 2 * ctm::kBM);  // CTA-pair M tile
   DeviceGuard g(device);
   const int D = widths[0], ld1 = h->wpad[1];
   auto bail = [&](ctm_status s) {

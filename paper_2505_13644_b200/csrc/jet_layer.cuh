@@ -23,7 +23,7 @@
 
 namespace ctm {
 
-constexpr int kBM = 128;                         // features per tile = TMEM lanes
+constexpr int kBM = 128;                         // features per CTA = TMEM lanes (a CTA pair spans 256)
 constexpr int kBK = 32;                          // bf16 K per stage: 64-byte rows, SWIZZLE_64B
 constexpr int kStages = 4;
 constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
@@ -169,16 +169,21 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   if (!p.readout) store_pair(ph, pl, 0, top);
 }
 
-// Persistent: one CTA per SM loops over tiles (tile = m_tile + m_tiles * n_tile, so CTAs
-// running side by side share the B tile of a point group through L2). Warp roles:
-//   warp 0   TMA producer: streams A (W hi/lo) and B (block hi/lo) k-blocks into a
-//            kStages-deep smem ring, continuously across tiles;
-//   warp 1   MMA issuer (one thread): 3 bf16 MMAs per 16-K step into one of two TMEM
-//            accumulators (double buffer), commit -> tmem_full[buf];
-//   warps 2-9 epilogue: TMEM -> registers, Taylor rule, stores; arrive tmem_empty[buf]
-//            so the MMA of tile t+1 overlaps the epilogue of tile t.
+// Persistent CTA PAIRS (cluster of 2, cta_group::2): each pair owns an M = 256 feature tile
+// (CTA rank r holds features m0 + 128 r .. +127 of A = W and, in its TMEM, the matching
+// accumulator lanes) and the N slots of pts_per_tile points (CTA rank r holds B rows
+// r*N/2 .. +N/2-1). The pair's leader issues tcgen05.mma.cta_group::2; the tensor cores
+// of both SMs read the two B halves from both CTAs' smem, so each SM stages half of B
+// (less L2 -> SM traffic and fewer smem operand reads per useful FLOP than one CTA per tile).
+// Pairs loop over tiles (tile = m_pair + m_pairs * n_tile). Warp roles, in BOTH CTAs:
+//   warp 0   TMA producer: its A half and B half of each k-block into a kStages-deep
+//            ring; the transaction bytes of both CTAs are counted on the LEADER's full_bar;
+//   warp 1   leader only: MMA issuer (one thread), 3 bf16 MMAs per 16-K step into one of
+//            two TMEM accumulators; commits multicast to both CTAs (empty_bar, tmem_full);
+//   warps 2-9 epilogue on this CTA's 128 accumulator lanes; releases a buffer with a
+//            remote arrive on the leader's tmem_empty (8 warps x 2 CTAs).
 template <int KORD>
-__global__ void __launch_bounds__(kLayerThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     jet_layer_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                      const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
                      const LayerParams p) {
@@ -187,16 +192,21 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tmem_full_bar = empty_bar + kStages;   // [2]
-  uint64_t* tmem_empty_bar = tmem_full_bar + 2;    // [2]
+  uint64_t* tmem_empty_bar = tmem_full_bar + 2;    // [2] (used in the leader)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
   float* red = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [4][kMaxPtsPerTile][2]
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int m_pairs = p.m_tiles >> 1;
   const int64_t n_tiles = (p.n_points + p.pts_per_tile - 1) / p.pts_per_tile;
-  const int64_t total_tiles = n_tiles * p.m_tiles;
-  const uint32_t b_bytes = (uint32_t)p.n_mma * kBK * 2;
+  const int64_t total_tiles = n_tiles * m_pairs;
+  const int half_n = p.n_mma >> 1;
+  const uint32_t b_bytes = (uint32_t)half_n * kBK * 2;  // this CTA's B half of one plane
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA_hi);
@@ -209,47 +219,47 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tmem_full_bar[b], 1);
-      ptx::mbar_init(&tmem_empty_bar[b], 8);  // one arrive per epilogue warp
+      ptx::mbar_init(&tmem_empty_bar[b], 16);  // 8 epilogue warps in each CTA of the pair
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
   if (KORD == 4)
     for (int j = threadIdx.x; j < p.J; j += blockDim.x) jw[j] = p.jet_w[j];
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // barrier inits and TMEM allocation visible to the pair
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
-      uint32_t it = 0;  // global k-block counter across tiles
-      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int m0 = (int)(tile % p.m_tiles) * kBM;
-        const int32_t row0 = (int32_t)((tile / p.m_tiles) * p.pts_per_tile * p.P);
+      uint32_t it = 0;
+      for (int64_t tile = pair; tile < total_tiles; tile += npairs) {
+        const int m0 = (int)(tile % m_pairs) * (2 * kBM) + (int)rank * kBM;
+        const int32_t row0 = (int32_t)((tile / m_pairs) * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
         for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
           const uint32_t s = it % kStages;
           const uint32_t ph = (it / kStages) & 1u;
           ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
           uint8_t* st = smem + s * kStageBytes;
-          ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * kATileBytes + 2u * b_bytes);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * (2u * kATileBytes + 2u * b_bytes));
           const int k0 = kb * kBK;
-          ptx::tma_load_2d(st, &tmA_hi, &full_bar[s], k0, m0);
-          ptx::tma_load_2d(st + kATileBytes, &tmA_lo, &full_bar[s], k0, m0);
-          ptx::tma_load_2d(st + 2 * kATileBytes, &tmB_hi, &full_bar[s], k0, row0);
-          ptx::tma_load_2d(st + 2 * kATileBytes + kBTileBytes, &tmB_lo, &full_bar[s], k0, row0);
+          ptx::tma_load_2d_pair(st, &tmA_hi, &full_bar[s], k0, m0);
+          ptx::tma_load_2d_pair(st + kATileBytes, &tmA_lo, &full_bar[s], k0, m0);
+          ptx::tma_load_2d_pair(st + 2 * kATileBytes, &tmB_hi, &full_bar[s], k0, row0);
+          ptx::tma_load_2d_pair(st + 2 * kATileBytes + kBTileBytes, &tmB_lo, &full_bar[s], k0, row0);
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_bf16(kBM, (uint32_t)p.n_mma);
+    // ------------------------------------------------------------ MMA issuer (leader, one thread)
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
       uint32_t it = 0, local = 0;
-      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
+      for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++local) {
         const uint32_t buf = local & 1u;
-        const uint32_t use = local >> 1;  // how many times this buffer was used before
+        const uint32_t use = local >> 1;
         ptx::mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
@@ -269,30 +279,26 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
             const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, 512, kSw64);
             const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, 512, kSw64);
             const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, 512, kSw64);
-            ptx::mma_bf16(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
-            ptx::mma_bf16(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
-            ptx::mma_bf16(d_tmem, dah, dbh, idesc, 1u);               // hi * hi
+            ptx::mma_bf16_pair(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
+            ptx::mma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
+            ptx::mma_bf16_pair(d_tmem, dah, dbh, idesc, 1u);               // hi * hi
           }
-          ptx::mma_commit(&empty_bar[s]);  // stage free once these MMAs retire
+          ptx::mma_commit_pair(&empty_bar[s]);  // both CTAs' stage s is free once these retire
         }
-        ptx::mma_commit(&tmem_full_bar[buf]);  // accumulator complete
+        ptx::mma_commit_pair(&tmem_full_bar[buf]);  // both CTAs' accumulator halves complete
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..9)
-    // Two warps per TMEM lane quadrant (a warp may only touch lanes 32*(warp%4)..+31);
-    // group g = 0/1 takes the even/odd points of the tile. Each thread owns one output
-    // feature and walks the P slots of its points in order, so the collapse
-    // sum_r (...) is a sequential in-register sum.
+    // ------------------------------------------------------------ epilogue (warps 2..9, both CTAs)
     const int q = warp & 3;
     const int g = (warp - 2) >> 2;
     const int m_local = q * 32 + lane;
     uint32_t local = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
+    for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++local) {
       const uint32_t buf = local & 1u;
       const uint32_t use = local >> 1;
-      const int m_tile = (int)(tile % p.m_tiles);
-      const int64_t n_tile = tile / p.m_tiles;
+      const int m_tile = (int)(tile % m_pairs) * 2 + (int)rank;  // 128-feature tile of this CTA
+      const int64_t n_tile = tile / m_pairs;
       const int64_t row0 = n_tile * p.pts_per_tile * p.P;
       const int m = m_tile * kBM + m_local;
       const float bias = p.bias[m];
@@ -314,10 +320,10 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
           }
         }
       }
-      // every epilogue warp releases the accumulator buffer once per tile
+      // every epilogue warp of both CTAs releases the buffer once per tile (leader's barrier)
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tmem_empty_bar[buf]);
+      if (lane == 0) ptx::mbar_arrive_remote(&tmem_empty_bar[buf], 0);
       if (p.readout) {
         asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps only
         for (int j = threadIdx.x - 64; j < npts * 2; j += 256) {
@@ -332,10 +338,10 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // no CTA of the pair touches TMEM or the peer's barriers any more
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<kTmemCols>(tmem_base);
+    ptx::tmem_dealloc_pair<kTmemCols>(tmem_base);
   }
 }
 
