@@ -25,10 +25,10 @@ namespace ctm {
 
 constexpr int kBM = 128;                         // features per CTA = TMEM lanes (a CTA pair spans 256)
 constexpr int kBK = 32;                          // bf16 K per stage: 64-byte rows, SWIZZLE_64B
-constexpr int kStages = 4;
+constexpr int kStages = 6;
 constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
 constexpr int kATileBytes = kBM * kBK * 2;       // 8 KB
-constexpr int kBTileBytes = kMaxN * kBK * 2;     // 16 KB
+constexpr int kBTileBytes = (kMaxN / 2) * kBK * 2;  // 8 KB: a CTA of the pair stages half of B
 constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
