@@ -34,7 +34,7 @@ constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
 constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
-                           4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxJets * 4;
+                           4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxJets * 4 + 2 * kBM * 4 /*xacc*/;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
 constexpr uint32_t kSw64 = 4;                    // descriptor layout code for SWIZZLE_64B
 // Epilogue modes (template parameter KORD): 2 = K=2 collapsed, 4 = K=4 collapsed (weighted
@@ -74,15 +74,21 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // One point of one tile, for the feature owned by this thread: TMEM columns
-// [tcol, tcol + P) hold z for slots 0..P-1. Writes the P output slots (bf16 pairs) or,
-// on the readout layer, returns w_out*h0 and w_out*(top) for the reduction.
+// [tcol, tcol + P) hold z for slots 0..P-1. Writes the output slots (bf16 pairs) or, on
+// the readout layer, returns w_out*h0 and w_out*(top) for the reduction.
+// part 0: the whole point. A tile holding a single point (P > 128) is split between the
+// two epilogue warp groups at a jet boundary `split`: part 1 = the primal and middle slots
+// [1, split), part 2 = middle slots [split, ..) and the top; the partial collapsed sum of
+// part 1 reaches part 2 through xacc (this thread's slot) and the named barrier bar_id.
 template <int KORD>
 __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
-                                               float wo, const float* jw, float& fpart, float& opart) {
+                                               float wo, const float* jw, int part, int split, float* xacc,
+                                               int bar_id, float& fpart, float& opart) {
   const int P = p.P;
   const int ld = p.ldo;
-  uint16_t* ph = p.out_hi + (size_t)row * ld + m;
-  uint16_t* pl = p.out_lo + (size_t)row * ld + m;
+  const int nmid = (KORD == kStd2) ? P - 1 : P - 2;  // middle slots are 1 .. nmid
+  const int mb = (part == 2) ? split : 1;
+  const int me = (part == 1) ? split : nmid + 1;
   // ---- slot 0: the primal; the bias enters here only (affine rule)
   const float z0 = ptx::tmem_ld1(tcol) + bias;
   ptx::tmem_ld_wait();
@@ -94,15 +100,16 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     d3 = d1 * (6.f * t * t - 2.f);            // tanh'''
     d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
   }
-  fpart = wo * t;
-  if (!p.readout) store_pair(ph, pl, 0, t);
-  ph += ld;
-  pl += ld;
-  // ---- slots 1..P-2: first-order coefficients (K=2) or jets (z1, z2, z3) (K=4);
-  //      standard mode (kStd2): slots 1..P-1 are the pairs (z1_r, z2_r), no collapse
+  fpart = (part == 2) ? 0.f : wo * t;
+  opart = 0.f;
+  if (!p.readout && part != 2) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
+  uint16_t* ph = p.out_hi + (size_t)(row + mb) * ld + m;
+  uint16_t* pl = p.out_lo + (size_t)(row + mb) * ld + m;
+  // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
+  //      standard-mode pairs (z1_r, z2_r) with no collapse
   float acc = 0.f;            // the collapsed sum over directions (standard: sum_r h2_r at readout)
   float z1 = 0.f, z2 = 0.f;   // K=4 jet state
-  int which = 0, jj = 0;
+  int which = 0, jj = (KORD == 4) ? (mb - 1) / 3 : 0;
   auto middle = [&](float z) {
     float h;
     if (KORD == 2) {
@@ -137,25 +144,34 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     ph += ld;
     pl += ld;
   };
-  const int nmid = (KORD == kStd2) ? P - 1 : P - 2;
+  const int cnt = me - mb;
   int s = 0;
-  for (; s + 16 <= nmid; s += 16) {
+  for (; s + 16 <= cnt; s += 16) {
     float v[16];
-    ptx::tmem_ld16(tcol + 1u + (uint32_t)s, v);
+    ptx::tmem_ld16(tcol + (uint32_t)(mb + s), v);
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < 16; ++i) middle(v[i]);
   }
-  const int rem = nmid - s;  // 0..15, warp-uniform
+  const int rem = cnt - s;  // 0..15, warp-uniform
   if (rem > 0) {
     float v[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i)
-      if (i < rem) v[i] = ptx::tmem_ld1(tcol + 1u + (uint32_t)(s + i));
+      if (i < rem) v[i] = ptx::tmem_ld1(tcol + (uint32_t)(mb + s + i));
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < 15; ++i)
       if (i < rem) middle(v[i]);
+  }
+  if (part == 1) {  // hand the partial collapsed sum to part 2
+    *xacc = acc;
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    return;
+  }
+  if (part == 2) {
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    acc += *xacc;
   }
   if (KORD == kStd2) {  // standard mode: the top coefficients are sliced and summed only here
     opart = wo * acc;
@@ -196,6 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
   float* red = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [4][kMaxPtsPerTile][2]
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
+  float* xacc = jw + kMaxJets;                                                 // [2][128] split-point partials
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -292,6 +309,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     // ------------------------------------------------------------ epilogue (warps 2..9, both CTAs)
     const int q = warp & 3;
     const int g = (warp - 2) >> 2;
+    // split of a single point's middle slots between the groups, at a unit boundary
+    const int unit = (KORD == 4) ? 3 : (KORD == kStd2) ? 2 : 1;
+    const int nunits = ((KORD == kStd2) ? p.P - 1 : p.P - 2) / unit;
+    const int split = 1 + (nunits / 2) * unit;
     const int m_local = q * 32 + lane;
     uint32_t local = 0;
     for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++local) {
@@ -308,15 +329,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
-      for (int pt = g; pt < npts; pt += 2) {
+      if (p.pts_per_tile == 1) {
+        // one point per tile: both warp groups share it (split at a jet / pair boundary)
         float fpart, opart;
-        epilogue_point<KORD>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, fpart, opart);
+        epilogue_point<KORD>(p, tbase, row0, m, bias, wo, jw, g + 1, split, xacc + (local & 1u) * kBM + m_local,
+                             2 + q, fpart, opart);
         if (p.readout) {
-          fpart = warp_sum(fpart);
-          opart = warp_sum(opart);
-          if (lane == 0) {
-            red[(q * kMaxPtsPerTile + pt) * 2 + 0] = fpart;
-            red[(q * kMaxPtsPerTile + pt) * 2 + 1] = opart;
+          const float v = warp_sum(g == 0 ? fpart : opart);
+          if (lane == 0) red[(q * kMaxPtsPerTile + 0) * 2 + g] = v;
+        }
+      } else {
+        for (int pt = g; pt < npts; pt += 2) {
+          float fpart, opart;
+          epilogue_point<KORD>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, 0, 0,
+                               nullptr, 0, fpart, opart);
+          if (p.readout) {
+            fpart = warp_sum(fpart);
+            opart = warp_sum(opart);
+            if (lane == 0) {
+              red[(q * kMaxPtsPerTile + pt) * 2 + 0] = fpart;
+              red[(q * kMaxPtsPerTile + pt) * 2 + 1] = opart;
+            }
           }
         }
       }
