@@ -185,13 +185,31 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   if (!p.readout) store_pair(ph, pl, 0, top);
 }
 
+// The k-th tile of CTA pair `pair`. With at least one point group per pair, a pair runs
+// all feature tiles of a point group back to back (n-tile pair + (k / m_pairs) * npairs,
+// feature pair k % m_pairs), so the group's B operand is re-read from L2 while resident;
+// small batches spread the tiles (tile pair + k * npairs) to keep every pair busy.
+// Returns false past the pair's last tile.
+__device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_pairs, int64_t n_tiles, int64_t& n,
+                                        int& m) {
+  if (n_tiles >= npairs) {
+    n = pair + (k / m_pairs) * npairs;
+    m = (int)(k % m_pairs);
+    return n < n_tiles;
+  }
+  const int64_t tile = pair + k * npairs;
+  n = tile / m_pairs;
+  m = (int)(tile % m_pairs);
+  return n < n_tiles;
+}
+
 // Persistent CTA PAIRS (cluster of 2, cta_group::2): each pair owns an M = 256 feature tile
 // (CTA rank r holds features m0 + 128 r .. +127 of A = W and, in its TMEM, the matching
 // accumulator lanes) and the N slots of pts_per_tile points (CTA rank r holds B rows
 // r*N/2 .. +N/2-1). The pair's leader issues tcgen05.mma.cta_group::2; the tensor cores
 // of both SMs read the two B halves from both CTAs' smem, so each SM stages half of B
 // (less L2 -> SM traffic and fewer smem operand reads per useful FLOP than one CTA per tile).
-// Pairs loop over tiles (tile = m_pair + m_pairs * n_tile). Warp roles, in BOTH CTAs:
+// Pairs loop over tiles in the order of tile_of(). Warp roles, in BOTH CTAs:
 //   warp 0   TMA producer: its A half and B half of each k-block into a kStages-deep
 //            ring; the transaction bytes of both CTAs are counted on the LEADER's full_bar;
 //   warp 1   leader only: MMA issuer (one thread), 3 bf16 MMAs per 16-K step into one of
@@ -221,7 +239,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
   const int npairs = gridDim.x >> 1;
   const int m_pairs = p.m_tiles >> 1;
   const int64_t n_tiles = (p.n_points + p.pts_per_tile - 1) / p.pts_per_tile;
-  const int64_t total_tiles = n_tiles * m_pairs;
   const int half_n = p.n_mma >> 1;
   const uint32_t b_bytes = (uint32_t)half_n * kBK * 2;  // this CTA's B half of one plane
 
@@ -252,9 +269,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       uint32_t it = 0;
-      for (int64_t tile = pair; tile < total_tiles; tile += npairs) {
-        const int m0 = (int)(tile % m_pairs) * (2 * kBM) + (int)rank * kBM;
-        const int32_t row0 = (int32_t)((tile / m_pairs) * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
+      int64_t nt;
+      int mp;
+      for (int64_t k = 0; tile_of(k, pair, npairs, m_pairs, n_tiles, nt, mp); ++k) {
+        const int m0 = mp * (2 * kBM) + (int)rank * kBM;
+        const int32_t row0 = (int32_t)(nt * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
         for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
           const uint32_t s = it % kStages;
           const uint32_t ph = (it / kStages) & 1u;
@@ -274,7 +293,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     if (rank == 0 && lane == 0) {
       const uint32_t idesc = ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
       uint32_t it = 0, local = 0;
-      for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++local) {
+      int64_t nt;
+      int mp;
+      for (; tile_of(local, pair, npairs, m_pairs, n_tiles, nt, mp); ++local) {
         const uint32_t buf = local & 1u;
         const uint32_t use = local >> 1;
         ptx::mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
@@ -315,11 +336,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     const int split = 1 + (nunits / 2) * unit;
     const int m_local = q * 32 + lane;
     uint32_t local = 0;
-    for (int64_t tile = pair; tile < total_tiles; tile += npairs, ++local) {
+    int64_t n_tile;
+    int mp;
+    for (; tile_of(local, pair, npairs, m_pairs, n_tiles, n_tile, mp); ++local) {
       const uint32_t buf = local & 1u;
       const uint32_t use = local >> 1;
-      const int m_tile = (int)(tile % m_pairs) * 2 + (int)rank;  // 128-feature tile of this CTA
-      const int64_t n_tile = tile / m_pairs;
+      const int m_tile = mp * 2 + (int)rank;  // 128-feature tile of this CTA
       const int64_t row0 = n_tile * p.pts_per_tile * p.P;
       const int m = m_tile * kBM + m_local;
       const float bias = p.bias[m];
