@@ -1,0 +1,25 @@
+"""Small runs of every operator for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_13644_b200 as ctm  # noqa: E402
+from synth import gaussian_directions, mlp_params, points, sigma  # noqa: E402
+
+for widths in ([5, 16, 16, 1], [50, 64, 64, 1]):
+    D = widths[0]
+    params = mlp_params(widths, 0)
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0)
+    X = torch.from_numpy(points(9, D)).cuda()
+    outs = [mlp.laplacian(X)[0], mlp.laplacian_standard(X)[0],
+            mlp.weighted_laplacian(X, torch.from_numpy(sigma(D, D)).cuda())[0],
+            mlp.randomized_laplacian(X, S=4, seed=1)[0],
+            mlp.randomized_laplacian(X, V=torch.from_numpy(gaussian_directions(9, 3, D)).cuda(), dist="gaussian")[0]]
+    if D <= 7:
+        outs += [mlp.biharmonic(X)[0], mlp.stochastic_biharmonic(X, S=3, seed=2)[0]]
+    torch.cuda.synchronize()
+    print(widths, [float(o.abs().max()) for o in outs])
+    mlp.close()

@@ -12,11 +12,13 @@ import pytest
 import torch
 
 import oracle as O
+from tests._util import magnitude_k2
 from synth import gaussian_directions, mlp_params, points, sigma as make_sigma, widths_for
 
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-4
+TAU = 1e-5  # condition-aware fallback, edge cases only (DESIGN.md §5 R9)
 C1_WIDTHS = widths_for(50)  # 50 -> 768 -> 768 -> 512 -> 512 -> 1
 C4_WIDTHS = widths_for(5)
 
@@ -62,13 +64,28 @@ def _dump_errors():
             json.dump(ERRORS, fh, indent=1, sort_keys=True)
 
 
-def check(got, want, norm, fgot=None, fwant=None, tol=TOL):
+def check(got, want, norm, fgot=None, fwant=None, tol=TOL, mag=None):
+    """north_star metric per point: |got - want| <= tol * norm. Where ``mag`` (the
+    running magnitude of the K = 2 computation, tests/_util.magnitude_k2) is given —
+    only for the small-net edge cases — a point that misses it may instead satisfy
+    |got - want| <= TAU * mag (reading R9: points whose direction
+    derivative cancels internally are beyond any fp32-class method under the
+    north_star normaliser). Fallback points are counted in parity_errors.json."""
     got = got.double().cpu().numpy() if isinstance(got, torch.Tensor) else got
-    err = np.abs(got - want) / norm
-    ERRORS[os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0] + f"#{len(ERRORS)}"] = {
-        "max_norm_err": float(err.max()), "n": int(err.size), "max_abs_op": float(np.abs(want).max())}
+    d = np.abs(got - want)
+    err = d / norm
+    ok = err <= tol
+    rec = {"max_norm_err": float(err.max()), "n": int(err.size), "max_abs_op": float(np.abs(want).max())}
+    if mag is not None:
+        rec["fallback_points"] = int(np.sum(~ok))
+        rec["max_err_over_mag"] = float((d / mag).max())
+        rec["max_condition_mag_over_norm"] = float((mag / norm).max())
+        ok |= d <= TAU * mag
+    ERRORS[os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0] + f"#{len(ERRORS)}"] = rec
     assert np.all(np.isfinite(got))
-    assert err.max() <= tol, f"max normalised error {err.max():.3e} at point {err.argmax()}"
+    bad = np.flatnonzero(~ok)
+    assert bad.size == 0, (f"max normalised error {err.max():.3e} at point {err.argmax()}"
+                           + ("" if mag is None else f"; fails err <= {TAU:g}*M at {bad.tolist()}"))
     if fgot is not None:
         fgot = fgot.double().cpu().numpy()
         ferr = np.abs(fgot - fwant) / np.maximum(1.0, np.abs(fwant))
@@ -284,6 +301,64 @@ def test_cuda_graph_capture_and_replay(ctm):
     want, fwant = mlp.laplacian(X)
     torch.cuda.synchronize()
     assert torch.equal(out, want) and torch.equal(f, fwant)
+
+
+@pytest.mark.parametrize("widths,N", [
+    ([1, 40, 24, 1], 5),              # D = 1 (P = 3: 85 points per tile), widths far below 256
+    ([7, 300, 270, 1], 11),           # widths padded to 512 (two CTA pairs, ragged features)
+    ([50, 768, 768, 512, 512, 1], 1),  # a single point
+    ([50, 64, 48, 1], 4 * 12 + 3),    # ragged last tile, more tiles than CTA pairs' groups
+])
+def test_edge_shapes_all_operators(ctm, widths, N):
+    """Every operator on shapes at the edges of the tiling. Tiny random nets have
+    points whose second derivative cancels internally (condition M / norm in the
+    hundreds), so on nets with hidden widths <= 64 the K = 2 checks carry the R9 fallback bound; the biharmonic and
+    every BASELINE-shaped test hold the plain north_star metric."""
+    params, onet = nets(widths)
+    Ws, bs = onet.Ws, onet.bs
+    D = widths[0]
+    # M is a tight bound only on tiny nets; on wide deep nets M / norm reaches 1e9
+    # (|W| sums compound), so the fallback would be vacuous there: plain metric.
+    tiny = max(widths[1:-1]) <= 64
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    want, fw, norm = O.laplacian(onet, Xd)
+    mag = magnitude_k2(Ws, bs, Xd, np.eye(D), 1.0) if tiny else None
+    op, f = mlp.laplacian(Xc)
+    check(op, want, norm, f, fw, mag=mag)
+    check(mlp.laplacian_standard(Xc)[0], want, norm, mag=mag)
+    sig = make_sigma(D, 3, kind="rect")
+    want, _, norm = O.weighted_laplacian(onet, Xd, sig.astype(np.float64))
+    mag = magnitude_k2(Ws, bs, Xd, sig.astype(np.float64).T, 1.0) if tiny else None
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm, mag=mag)
+    V = O.rademacher(4, 0, N, 5, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    mag = magnitude_k2(Ws, bs, Xd, V, 1.0 / 5) if tiny else None
+    check(mlp.randomized_laplacian(Xc, S=5, seed=4)[0], want, norm, mag=mag)
+    if D <= 7:
+        want, _, norm = O.biharmonic(onet, Xd)
+        check(mlp.biharmonic(Xc)[0], want, norm)
+
+
+def test_slot_cap_exactly_256(ctm):
+    """P = 256 (one point per tile, MMA N = 256) for the weighted (R = 254) and the
+    randomized (S = 254) Laplacian; P = 257 is refused."""
+    params, onet = nets([6, 32, 32, 1])
+    X = points(3, 6)
+    Xc = torch.from_numpy(X).cuda()
+    mlp = gpu_mlp(ctm, params)
+    sig = make_sigma(6, 254, kind="rect")
+    want, _, norm = O.weighted_laplacian(onet, X.astype(np.float64), sig.astype(np.float64))
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
+    assert mlp.last_plan() == {"launches": mlp.last_plan()["launches"], "slots_per_point": 256,
+                               "points_per_tile": 1, "mma_n": 256}
+    V = O.rademacher(8, 0, 3, 254, 6)
+    want, _, norm = O.randomized_laplacian(onet, X.astype(np.float64), V)
+    check(mlp.randomized_laplacian(Xc, S=254, seed=8)[0], want, norm)
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        mlp.weighted_laplacian(Xc, torch.from_numpy(make_sigma(6, 255, kind="rect")).cuda())
 
 
 def test_empty_batch_is_noop(ctm):

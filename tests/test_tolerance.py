@@ -1,0 +1,66 @@
+"""Pins for the condition-aware fallback bound used by the small-net GPU edge tests
+(tests/_util.magnitude_k2, DESIGN.md §5 reading R9). CPU only."""
+import numpy as np
+
+import oracle as O
+from tests._util import magnitude_k2, random_params
+
+
+def test_magnitude_equals_value_when_nothing_cancels():
+    """One hidden layer, D = 1: f'' = sum_j w2_j s''(z_j) w1_j^2. Choosing
+    w2_j = sign(s''(z_j)) makes every term non-negative, so the magnitude must equal
+    the exact Laplacian the oracle computes (no cancellation, nothing to bound)."""
+    Ws, bs = random_params([1, 9, 1], seed=3)
+    x = np.array([[0.37]])
+    z = Ws[0] @ x[0] + bs[0]
+    t = np.tanh(z)
+    s2 = -2.0 * t * (1.0 - t * t)
+    Ws[1] = np.sign(s2)[None, :] * np.abs(Ws[1])
+    want, _, norm = O.laplacian(O.Net(Ws, bs), x)
+    M = magnitude_k2(Ws, bs, x, np.eye(1), 1.0)
+    assert want[0] > 0
+    np.testing.assert_allclose(M, want, rtol=1e-13)
+    np.testing.assert_allclose(M, norm, rtol=1e-13)
+
+
+def test_magnitude_bounds_the_north_star_normaliser():
+    """Triangle inequality: M >= sum_r |c_r f_{2,r}| for shared (Laplacian, weighted)
+    and per-point (randomized) direction sets, deep nets, any signs."""
+    rng = np.random.default_rng(0)
+    for trial in range(12):
+        D = int(rng.integers(1, 6))
+        widths = [D] + [int(rng.integers(4, 40)) for _ in range(int(rng.integers(1, 4)))] + [1]
+        Ws, bs = random_params(widths, seed=trial)
+        net = O.Net(Ws, bs)
+        X = rng.uniform(-1, 1, size=(4, D))
+        _, _, norm = O.laplacian(net, X)
+        assert np.all(magnitude_k2(Ws, bs, X, np.eye(D), 1.0) >= norm * (1 - 1e-12))
+        sig = rng.normal(size=(D, 3))
+        _, _, norm = O.weighted_laplacian(net, X, sig)
+        assert np.all(magnitude_k2(Ws, bs, X, sig.T, 1.0) >= norm * (1 - 1e-12))
+        V = O.rademacher(trial, 0, 4, 5, D)
+        _, _, norm = O.randomized_laplacian(net, X, V)
+        assert np.all(magnitude_k2(Ws, bs, X, V, 1.0 / 5) >= norm * (1 - 1e-12))
+
+
+def test_magnitude_is_homogeneous_and_catches_a_dropped_term():
+    """M scales with |c|; and a plausible bug (dropping the s' x2 term of Eq. 3 in one
+    layer) changes the result by far more than 1e-5 M, so the fallback cannot hide it."""
+    Ws, bs = random_params([3, 20, 16, 1], seed=5)
+    X = np.random.default_rng(1).uniform(-1, 1, size=(6, 3))
+    M = magnitude_k2(Ws, bs, X, np.eye(3), 1.0)
+    np.testing.assert_allclose(magnitude_k2(Ws, bs, X, np.eye(3), -2.5), 2.5 * M, rtol=1e-14)
+    want, _, _ = O.laplacian(O.Net(Ws, bs), X)
+    # same propagation without the s' x2 term in the second hidden layer
+    bad = np.empty(len(X))
+    for n, x in enumerate(X):
+        z = Ws[0] @ x + bs[0]
+        t = np.tanh(z); d1 = 1 - t * t; d2 = -2 * t * d1
+        x1 = d1[None, :] * Ws[0].T                      # [D, h1]
+        x2 = d2[None, :] * Ws[0].T ** 2
+        z0 = Ws[1] @ t + bs[1]
+        z1, z2 = x1 @ Ws[1].T, x2 @ Ws[1].T
+        t = np.tanh(z0); d1 = 1 - t * t; d2 = -2 * t * d1
+        x2 = d2 * z1 ** 2                               # dropped: + d1 * z2
+        bad[n] = float((x2 @ Ws[2][0]).sum())
+    assert np.all(np.abs(bad - want) > 1e-3 * M)
