@@ -65,6 +65,7 @@ def lib():
         _lib.ctmo_randomized_laplacian.argtypes = [P(_Net), vp, i64, vp, i32, vp, i32, i32, vp, vp, vp]
         _lib.ctmo_forward.argtypes = [P(_Net), vp, i64, vp]
         _lib.ctmo_stochastic_biharmonic.argtypes = [P(_Net), vp, i64, vp, i32, i32, vp, vp, vp]
+        _lib.ctmo_biharmonic_nested.argtypes = [P(_Net), vp, i64, vp, vp, vp]
         _lib.ctmo_act_derivs.argtypes = [i32, d, vp]
         _lib.ctmo_act_derivs.restype = None
         _lib.ctmo_gamma.argtypes = [i32, i32, i32, i32, P(ctypes.c_int64), P(ctypes.c_int64)]
@@ -158,6 +159,16 @@ def stochastic_biharmonic(net: Net, X, V, route=O1):
     """1/(3S) sum_s <d^4 f, v_s^4> with V [N, S, D] (Eq. 12 stochastic, unbiased scale, Q1)."""
     V = _f64(V)
     return _call(lib().ctmo_stochastic_biharmonic, net, X, _ptr(V), V.shape[1], route=route)
+
+
+def biharmonic_nested(net: Net, X):
+    """Laplacian^2 f by nested collapsed Laplacians. Returns (op, f, lap)."""
+    X = _f64(X)
+    N = X.shape[0]
+    op, f, lap = np.empty(N), np.empty(N), np.empty(N)
+    if lib().ctmo_biharmonic_nested(net.cref(), _ptr(X), N, _ptr(op), _ptr(f), _ptr(lap)) != 0:
+        raise ValueError("oracle call failed")
+    return op, f, lap
 
 
 def forward(net: Net, X) -> np.ndarray:

@@ -774,6 +774,121 @@ int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, 
 }
 
 /* ------------------------------------------------------------------------ */
+/* Nested collapsed Laplacians: Laplacian^2 f = Laplacian (Laplacian f)      */
+/* ("we simply nest the Laplacian implementations":   */
+/* "nesting Taylor mode Laplacians ... while also allowing to apply our      */
+/* collapsing technique").                                                   */
+/*                                                                           */
+/* The INNER computation is the collapsed Laplacian of Eq. 8/Eq. 7 (K = 2,   */
+/* directions e_d): per unit (h0, h1_1..h1_D, sum h2) with                   */
+/*   h0 = s(z0), h1_d = s'(z0) z1_d, sum h2 = s'(z0) sum z2 + s''(z0) sum_d z1_d^2 */
+/* (Eq. 1, Eq. 7). The OUTER computation applies collapsed   */
+/* Taylor mode again (K = 2, directions e_1..e_D) to every quantity of the   */
+/* inner one: each becomes an outer 2-jet (value, first coefficients along   */
+/* e_1..e_D, one collapsed second coefficient), and the inner rule is        */
+/* evaluated in 2-jet arithmetic. Linear layers act on every component, the  */
+/* bias on the (inner value, outer value) component only.            */
+/* ------------------------------------------------------------------------ */
+
+/* An outer jet is D + 2 doubles: [value, c_1 .. c_D, collapsed second]. */
+/* g = phi(a) for phi with derivatives (p0, p1, p2) at a[0]:
+ *   value p0, c_e = p1 a_e, second = p1 a_2 + p2 sum_e a_e^2  (Eq. 1/7, K = 2) */
+static void jet_apply(int D, double p0, double p1, double p2, const double *a, double *g)
+{
+    double sq = 0.0;
+    for (int e = 1; e <= D; ++e) { g[e] = p1 * a[e]; sq += a[e] * a[e]; }
+    g[D + 1] = p1 * a[D + 1] + p2 * sq;
+    g[0] = p0;
+}
+
+/* g = a * b (Leibniz; the collapsed second coefficient of a product of two
+ * 2-jets along e is a b_2 + a_2 b + 2 sum_e a_e b_e) */
+static void jet_mul(int D, const double *a, const double *b, double *g)
+{
+    double cross = 0.0;
+    for (int e = 1; e <= D; ++e) cross += a[e] * b[e];
+    const double v = a[0] * b[0];
+    const double s2 = a[0] * b[D + 1] + a[D + 1] * b[0] + 2.0 * cross;
+    for (int e = 1; e <= D; ++e) g[e] = a[0] * b[e] + a[e] * b[0];
+    g[0] = v;
+    g[D + 1] = s2;
+}
+
+int ctmo_biharmonic_nested(const ctmo_net *net, const double *X, int64_t N, double *op, double *f,
+                           double *lap)
+{
+    if (check_net(net) || N < 0 || (N > 0 && (!X || !op))) return 1;
+    const int D = net->widths[0];
+    const int J = D + 2;           /* components of one outer jet */
+    const int C = D + 2;           /* inner components: h0, h1_1..h1_D, sum h2 */
+    const int U = C * J;           /* doubles per unit */
+    const int wmax = max_width(net);
+#pragma omp parallel
+    {
+        double *H = malloc(sizeof(double) * (size_t)wmax * U);
+        double *Z = malloc(sizeof(double) * (size_t)wmax * U);
+        double *t0 = malloc(sizeof(double) * J), *t1 = malloc(sizeof(double) * J);
+        double *s0 = malloc(sizeof(double) * J), *s1 = malloc(sizeof(double) * J), *s2 = malloc(sizeof(double) * J);
+        double *acc = malloc(sizeof(double) * J);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t n = 0; n < N; ++n) {
+            /* input: x as an inner jet (x, e_d, 0); each inner quantity as an outer jet:
+             * x_i -> (x_i, e_i, 0); the constants (e_d)_i and 0 -> (const, 0, 0) */
+            memset(H, 0, sizeof(double) * (size_t)D * U);
+            for (int i = 0; i < D; ++i) {
+                double *u = H + (size_t)i * U;
+                u[0 * J + 0] = X[n * D + i];
+                u[0 * J + 1 + i] = 1.0;
+                u[(1 + i) * J + 0] = 1.0;
+            }
+            for (int l = 0; l < net->L; ++l) {
+                const int in = net->widths[l], out = net->widths[l + 1];
+                const double *W = layer_W(net, l), *b = layer_b(net, l);
+                for (int i = 0; i < out; ++i) {
+                    double *z = Z + (size_t)i * U;
+                    for (int k = 0; k < U; ++k) {
+                        double a = 0.0;
+                        for (int j = 0; j < in; ++j) a += W[(size_t)i * in + j] * H[(size_t)j * U + k];
+                        z[k] = a;
+                    }
+                    z[0] += b[i];
+                }
+                if (l == net->L - 1) break;
+                for (int i = 0; i < out; ++i) {
+                    const double *z = Z + (size_t)i * U;
+                    double *h = H + (size_t)i * U;
+                    double d[5];
+                    ctmo_act_derivs(net->act, z[0], d);
+                    /* s(z0), s'(z0), s''(z0) as outer jets */
+                    jet_apply(D, d[0], d[1], d[2], z, s0);
+                    jet_apply(D, d[1], d[2], d[3], z, s1);
+                    jet_apply(D, d[2], d[3], d[4], z, s2);
+                    /* sum h2 = s'(z0) * sum z2 + s''(z0) * sum_d z1_d * z1_d */
+                    memset(acc, 0, sizeof(double) * J);
+                    for (int dd = 0; dd < D; ++dd) {
+                        jet_mul(D, z + (1 + dd) * J, z + (1 + dd) * J, t0);
+                        for (int k = 0; k < J; ++k) acc[k] += t0[k];
+                    }
+                    jet_mul(D, s2, acc, t0);
+                    jet_mul(D, s1, z + (D + 1) * J, t1);
+                    for (int k = 0; k < J; ++k) h[(D + 1) * J + k] = t0[k] + t1[k];
+                    /* h1_d = s'(z0) * z1_d */
+                    for (int dd = 0; dd < D; ++dd) jet_mul(D, s1, z + (1 + dd) * J, h + (1 + dd) * J);
+                    /* h0 = s(z0) */
+                    memcpy(h, s0, sizeof(double) * J);
+                }
+            }
+            /* scalar output: outer second coefficient of the inner collapsed top */
+            op[n] = Z[(D + 1) * J + (D + 1)];
+            if (f) f[n] = Z[0];
+            if (lap) lap[n] = Z[(D + 1) * J + 0];
+        }
+        free(H); free(Z); free(t0); free(t1); free(s0); free(s1); free(s2); free(acc);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Counter-based Rademacher directions: splitmix64         */
 /* finaliser of seed + (idx + 1) * 0x9E3779B97F4A7C15; sign = top bit.        */
 /* ------------------------------------------------------------------------ */

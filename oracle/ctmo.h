@@ -77,6 +77,14 @@ int ctmo_biharmonic(const ctmo_net *net, const double *X, int64_t N, int32_t rou
 int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, const double *V, int32_t S,
                                int32_t route, double *op, double *f, double *norm);
 
+/* Biharmonic by NESTED collapsed Laplacians:
+ * Laplacian^2 f = Laplacian(Laplacian f), the inner Laplacian in collapsed Taylor mode
+ * (Eq. 7/8) evaluated in the 2-jet arithmetic of an outer collapsed Laplacian.
+ * op[N] = Laplacian^2 f, f[N] (may be NULL), lap[N] = Laplacian f (may be NULL).
+ * No normaliser: parity uses the O1 biharmonic's (same operator). */
+int ctmo_biharmonic_nested(const ctmo_net *net, const double *X, int64_t N, double *op, double *f,
+                           double *lap);
+
 /* sigma^(k)(z), k = 0..4, of the activation (d must hold 5 doubles). */
 void ctmo_act_derivs(int32_t act, double z, double *d);
 

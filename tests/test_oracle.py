@@ -440,3 +440,73 @@ def test_stochastic_biharmonic_unbiased_for_gaussian():
     V = np.random.default_rng(133).standard_normal((T, 1, D))
     est = O.stochastic_biharmonic(net, np.repeat(x, T, axis=0), V, O.O3)[0]
     assert abs(est.mean() - exact) < 4 * est.std() / math.sqrt(T)
+
+
+# --------------------------------------------------------------------------
+# Nested collapsed Laplacians: Laplacian(Laplacian f)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("D", [1, 2, 3, 5])
+def test_nested_biharmonic_norm4_and_x1sq_x2sq(D):
+    net = _norm4_net(D)
+    X = _pts(3, D)
+    op, f, lap = O.biharmonic_nested(net, X)
+    r2 = np.sum(X**2, axis=1)
+    np.testing.assert_allclose(op, 8 * D * (D + 2), rtol=1e-12)
+    np.testing.assert_allclose(lap, 4 * (D + 2) * r2, rtol=1e-13)
+    np.testing.assert_allclose(f, r2**2, rtol=1e-14)
+    W1 = np.array([[1.0, 1.0], [1.0, -1.0], [1.0, 0.0], [0.0, 1.0]])
+    net = O.Net([W1, np.eye(4), np.array([[1.0, 1.0, -2.0, -2.0]]) / 12.0],
+                [np.zeros(4), np.zeros(4), np.zeros(1)], "square")
+    np.testing.assert_allclose(O.biharmonic_nested(net, _pts(4, 2))[0], 8.0, rtol=1e-12)
+
+
+def test_nested_biharmonic_sum_of_sines_and_linear_net():
+    rng = np.random.default_rng(9)
+    D = 4
+    bvec, phi, a = rng.uniform(0.5, 2, D), rng.uniform(-1, 1, D), rng.uniform(-1, 1, D)
+    net = O.Net([np.diag(bvec), a[None, :]], [phi, np.array([0.3])], "sin")
+    X = _pts(5, D)
+    s = np.sin(X * bvec + phi)
+    op, _, lap = O.biharmonic_nested(net, X)
+    np.testing.assert_allclose(op, (s * a * bvec**4).sum(1), rtol=1e-11)
+    np.testing.assert_allclose(lap, -(s * a * bvec**2).sum(1), rtol=1e-12)
+    Ws, bs = random_params([4, 7, 5, 1], 1)
+    assert np.max(np.abs(O.biharmonic_nested(O.Net(Ws, bs, "identity"), X)[0])) < 1e-13
+
+
+def test_nested_biharmonic_one_hidden_layer_tanh_closed_form():
+    D, H = 5, 7
+    Ws, bs = random_params([D, H, 1], 11, scale=2.0)
+    X = _pts(4, D)
+    W1, c = Ws[0], Ws[1][0]
+    t4 = _tanh_derivs_autograd(X @ W1.T + bs[0], 4)
+    np.testing.assert_allclose(O.biharmonic_nested(O.Net(Ws, bs), X)[0], (t4 * c * np.sum(W1**2, 1) ** 2).sum(1),
+                               rtol=1e-11)
+
+
+def test_nested_biharmonic_vs_tensor_route_interpolation_and_autograd():
+    """Three independent derivations of the same number: the explicit 4th-derivative
+    tensor (O2), the interpolation family (O1), and torch's nested autograd Laplacian."""
+    for D, seed in ((3, 31), (5, 7), (1, 51)):
+        Ws, bs = random_params([D, 10, 8, 6, 1], seed, scale=1.5)
+        net = O.Net(Ws, bs, "tanh")
+        X = _pts(3, D, seed=seed + 1)
+        op, f, lap = O.biharmonic_nested(net, X)
+        want, _, norm = O.biharmonic(net, X, O.O1)
+        assert np.max(np.abs(op - want) / norm) < 1e-12
+        if D <= 3:
+            np.testing.assert_allclose(op, O.biharmonic(net, X, O.O2)[0], rtol=1e-11)
+        np.testing.assert_allclose(lap, O.laplacian(net, X)[0], rtol=1e-12)
+        np.testing.assert_allclose(f, O.forward(net, X), rtol=1e-14)
+    D = 3
+    Ws, bs = random_params([D, 10, 8, 1], 31, scale=1.5)
+    tf = _torch_f(Ws, bs)
+    x = torch.tensor(_pts(1, D, seed=32)[0], requires_grad=True)
+
+    def lap(g, y):
+        (gr,) = torch.autograd.grad(g(y), y, create_graph=True)
+        return sum(torch.autograd.grad(gr[i], y, create_graph=True)[0][i] for i in range(D))
+
+    want = lap(lambda y: lap(tf, y), x).item()
+    got = O.biharmonic_nested(O.Net(Ws, bs), x.detach().numpy()[None])[0][0]
+    assert abs(got - want) < 1e-10 * max(1.0, abs(want))
