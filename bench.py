@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
     ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard",
-                                   "stochastic_biharmonic"],
+                                   "stochastic_biharmonic", "biharmonic_nested"],
                     default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -58,13 +58,14 @@ def parse():
 def workload(args):
     from synth import widths_for
 
-    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic") else 50
+    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic", "biharmonic_nested") else 50
     names = {
         "laplacian": "C1 exact Laplacian",
         "standard": "C1 exact Laplacian by STANDARD Taylor mode (1+2D vectors; the paper's baseline)",
         "weighted": "C2 weighted Laplacian (dense full-rank sigma, R=50)",
         "randomized": f"C3 randomized Laplacian (Rademacher, S={args.S}, generated in-kernel)",
         "biharmonic": "C4 exact biharmonic (interpolation family, J=35)",
+        "biharmonic_nested": "C4 exact biharmonic by nested collapsed Laplacians (P:4073; 27 vectors)",
         "stochastic_biharmonic": f"stochastic biharmonic (Gaussian, S={args.S}, generated in-kernel)",
     }
     w = widths_for(D)
@@ -142,6 +143,8 @@ def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
         elif op == "stochastic_biharmonic":
             V = np.random.default_rng(2).standard_normal((X.shape[0], S, D))
             O.stochastic_biharmonic(net, X, V, O.O1)
+        elif op == "biharmonic_nested":
+            O.biharmonic_nested(net, X)
         else:
             O.biharmonic(net, X, O.O1)
 
@@ -228,6 +231,8 @@ def main():
             mlp.randomized_laplacian(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out)
         elif args.op == "stochastic_biharmonic":
             mlp.stochastic_biharmonic(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out)
+        elif args.op == "biharmonic_nested":
+            mlp.biharmonic_nested(Xd, out=op_out, f_out=f_out)
         else:
             mlp.biharmonic(Xd, out=op_out, f_out=f_out)
 

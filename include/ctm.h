@@ -109,6 +109,17 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, in
 ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                           void *stream);
 
+/* Exact biharmonic by NESTED collapsed Laplacians, Laplacian(Laplacian f) (P:1192,
+ * "the most efficient way to compute biharmonics is by nesting
+ * Laplacians ... while also allowing to apply our collapsing technique"). The slots of
+ * the nest that are equal by symmetry of mixed partials are propagated once: per point
+ * z, the gradient (D), the Hessian upper triangle (D(D+1)/2), the gradient of the
+ * Laplacian (D) and the biharmonic (1): P = 2 + 2D + D(D+1)/2 <= 256, i.e. D <= 20
+ * (27 vectors at D = 5 vs 107 for ctm_biharmonic). Same arguments, layout, ownership and
+ * errors as ctm_biharmonic; CTM_EUNSUPPORTED for D > 20. */
+ctm_status ctm_biharmonic_nested(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
+                                 void *stream);
+
 /* Stochastic biharmonic, Eq. 12 stochastic case, collapsed over S samples
  * (1 + 3S + 1 vectors): op[n] = 1/(3S) sum_s <d^4 f(x_n), v_{n,s}^{(x)4}> with
  * standard normal v (the printed scale D/S is read as garbled: Isserlis gives

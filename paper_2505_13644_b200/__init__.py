@@ -32,6 +32,7 @@ ABI = {
         [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _I32, _VP, _VP, _VP],
     ),
     "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_biharmonic_nested": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
                                                  _VP]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
@@ -180,6 +181,13 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_biharmonic(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                     _stream_ptr(stream, self.device)), "ctm_biharmonic")
+        return out, f_out
+
+    def biharmonic_nested(self, X, out=None, f_out=None, want_f=True, stream=None):
+        """Exact biharmonic (Eq. 12) by nested collapsed Laplacians, 2 + 2D + D(D+1)/2 slots."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        _check(lib().ctm_biharmonic_nested(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
+                                           _stream_ptr(stream, self.device)), "ctm_biharmonic_nested")
         return out, f_out
 
     def stochastic_biharmonic(self, X, S=None, V=None, seed=0, point_offset=0, out=None, f_out=None, want_f=True,

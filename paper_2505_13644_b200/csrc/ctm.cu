@@ -125,7 +125,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
-  bool smem_attr_set[5] = {false, false, false, false, false};
+  bool smem_attr_set[6] = {false, false, false, false, false, false};
   // profiling (events around launches)
   bool profiling = false;
   struct Rec {
@@ -283,7 +283,7 @@ Plan make_plan(int P) {
   return pl;
 }
 
-enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH };
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST };
 
 struct CallArgs {
   Op op;
@@ -351,6 +351,8 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
       ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
     else if (KORD == 4)
       ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
+    else if (KORD == ctm::kNest)
+      ctm::seed_layer_kernel<ctm::kNest><<<(unsigned)blocks, threads, 0, st>>>(sp);
     else
       ctm::seed_layer_kernel<ctm::kStd2><<<(unsigned)blocks, threads, 0, st>>>(sp);
   }
@@ -399,7 +401,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     lp.n_mma = pl.nmma;
     lp.k_iters = gl.kpad / ctm::kBK;
     lp.jet_w = (a.op == OP_SBIH) ? h->w_ones : h->w_bih;
-    lp.J = (a.op == OP_SBIH) ? a.S : h->J_bih;
+    lp.J = (a.op == OP_SBIH) ? a.S : (a.op == OP_BIH_NEST) ? h->widths[0] : h->J_bih;
     if (last) {
       ctm_status s = ensure(h->partial, h->partial_elems, (size_t)n * m_tiles * 2);
       if (s != CTM_OK) return s;
@@ -422,6 +424,11 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
         if (s != CTM_OK) return s;
         ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
                                                                                               mb_hi, mb_lo, lp);
+      } else if (KORD == ctm::kNest) {
+        s = set_layer_attr<ctm::kNest>(h);
+        if (s != CTM_OK) return s;
+        ctm::jet_layer_kernel<ctm::kNest><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
+            *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp);
       } else {
         s = set_layer_attr<ctm::kStd2>(h);
         if (s != CTM_OK) return s;
@@ -446,7 +453,10 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
 ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int D = h->widths[0];
   const int ld1 = h->wpad[1];
-  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH) ? 4 : (a.op == OP_LAP_STD) ? ctm::kStd2 : 2;
+  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH) ? 4
+                   : (a.op == OP_LAP_STD)                ? ctm::kStd2
+                   : (a.op == OP_BIH_NEST)               ? ctm::kNest
+                                                         : 2;
   int P = 0;
   switch (a.op) {
     case OP_LAP: P = D + 2; break;
@@ -455,6 +465,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     case OP_BIH: P = 3 * h->J_bih + 2; break;
     case OP_LAP_STD: P = 1 + 2 * D; break;
     case OP_SBIH: P = 3 * a.S + 2; break;
+    case OP_BIH_NEST: P = 2 + 2 * D + D * (D + 1) / 2; break;
   }
   if (P > ctm::kMaxN)
     return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
@@ -768,6 +779,17 @@ ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, float* op_ou
   if (mlp->J_bih == 0)
     return fail(CTM_EUNSUPPORTED, "biharmonic needs 3J+2 <= 256 slots, i.e. D <= 7");
   CallArgs a{OP_BIH, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_biharmonic_nested(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out, float* f_out,
+                                 void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (mlp->widths[0] > ctm::kNestMaxD)
+    return fail(CTM_EUNSUPPORTED, "nested biharmonic needs 2 + 2D + D(D+1)/2 <= 256 slots, i.e. D <= 20");
+  CallArgs a{OP_BIH_NEST, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
 

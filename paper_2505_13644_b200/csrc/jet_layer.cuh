@@ -41,6 +41,12 @@ constexpr uint32_t kSw64 = 4;                    // descriptor layout code for S
 // top), kStd2 = K=2 STANDARD Taylor mode (1 + 2R slots, the per-direction top
 // coefficients are propagated and only summed at the output) -- the paper's baseline.
 constexpr int kStd2 = 3;
+// kNest: the biharmonic by NESTED collapsed Laplacians, with the slots
+// of the nest that are equal by symmetry of partial derivatives stored once: per point
+// [z | g_a = d_a z (D) | H_ab = d_a d_b z, a <= b packed row-major (D(D+1)/2) |
+//  L_a = d_a Lap z (D) | Q = Lap^2 z], P = 2 + 2D + D(D+1)/2 (27 at D = 5, 252 at D = 20).
+constexpr int kNest = 5;
+constexpr int kNestMaxD = 20;
 
 struct LayerParams {
   const float* bias;      // [Mpad]
@@ -54,7 +60,7 @@ struct LayerParams {
   int n_mma;              // MMA N, multiple of 16, <= 256
   int k_iters;            // Kpad / kBK
   const float* jet_w;     // K=4: weights of the J jets in the collapsed slot
-  int J;
+  int J;                  // K=4: jets; kNest: D
   int readout;            // last hidden layer: reduce against w_out instead of storing
   const float* w_out;     // [Mpad] output-layer weights (zero padded)
   float* partial;         // [n_points, m_tiles, 2]
@@ -183,6 +189,181 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
   opart = wo * top;
   if (!p.readout) store_pair(ph, pl, 0, top);
+}
+
+// Nested-Laplacian biharmonic epilogue (kNest) for one point, the whole point in this
+// thread (no split). With s = tanh and the slots of the layout above (multivariate chain
+// rule for h = s(z)):
+//   h_a   = s' g_a
+//   H'_ab = s'' g_a g_b + s' H_ab
+//   L'_a  = s''' g_a |g|^2 + 2 s'' (H g)_a + s'' g_a tr H + s' L_a
+//   Q'    = s'''' |g|^4 + 2 s''' |g|^2 tr H + 4 s''' g^T H g + 2 s'' |H|_F^2 + s'' (tr H)^2
+//           + 4 s'' g^T L + s' Q
+// (D = 1 gives the K=4 Faa di Bruno row of the cheat sheet.) Register
+// arrays are sized kNestMaxD and indexed with compile-time indices under runtime guards.
+__device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
+                                                float wo, float& fpart, float& opart) {
+  const int D = p.J;
+  const int ld = p.ldo;
+  const float z0 = ptx::tmem_ld1(tcol) + bias;
+  float g[kNestMaxD];
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a) g[a] = (a < D) ? ptx::tmem_ld1(tcol + 1u + (uint32_t)a) : 0.f;
+  ptx::tmem_ld_wait();
+  const float t = tanhf(z0);
+  const float d1 = 1.f - t * t;
+  const float d2 = -2.f * t * d1;
+  const float d3 = d1 * (6.f * t * t - 2.f);
+  const float d4 = 8.f * t * d1 * (2.f - 3.f * t * t);
+  const bool store = !p.readout;
+  fpart = wo * t;
+  if (store) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
+  float gg = 0.f;
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a)
+    if (a < D) {
+      gg = fmaf(g[a], g[a], gg);
+      if (store) store_pair(p.out_hi, p.out_lo, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
+    }
+  // Hessian slots, one packed row at a time
+  float hg[kNestMaxD];
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a) hg[a] = 0.f;
+  float trH = 0.f, HF = 0.f;
+  int slot = 1 + D;
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a) {
+    if (a < D) {
+      float hr[kNestMaxD];
+#pragma unroll
+      for (int b = a; b < kNestMaxD; ++b) hr[b] = (b < D) ? ptx::tmem_ld1(tcol + (uint32_t)(slot + b - a)) : 0.f;
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int b = a; b < kNestMaxD; ++b)
+        if (b < D) {
+          const float h = hr[b];
+          if (store)
+            store_pair(p.out_hi, p.out_lo, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
+          if (b == a) {
+            trH += h;
+            HF = fmaf(h, h, HF);
+            hg[a] = fmaf(h, g[a], hg[a]);
+          } else {
+            HF = fmaf(2.f * h, h, HF);
+            hg[a] = fmaf(h, g[b], hg[a]);
+            hg[b] = fmaf(h, g[a], hg[b]);
+          }
+        }
+      slot += D - a;
+    }
+  }
+  // gradient-of-Laplacian slots and the top
+  float Lv[kNestMaxD];
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a) Lv[a] = (a < D) ? ptx::tmem_ld1(tcol + (uint32_t)(slot + a)) : 0.f;
+  const float zq = ptx::tmem_ld1(tcol + (uint32_t)(slot + D));
+  ptx::tmem_ld_wait();
+  float gL = 0.f, gHg = 0.f;
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a)
+    if (a < D) {
+      gL = fmaf(g[a], Lv[a], gL);
+      gHg = fmaf(g[a], hg[a], gHg);
+      if (store) {
+        const float v = d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * Lv[a];
+        store_pair(p.out_hi, p.out_lo, (size_t)(row + slot + a) * ld + m, v);
+      }
+    }
+  const float q = d4 * gg * gg + 2.f * d3 * gg * trH + 4.f * d3 * gHg + 2.f * d2 * HF + d2 * trH * trH +
+                  4.f * d2 * gL + d1 * zq;
+  opart = wo * q;
+  if (store) store_pair(p.out_hi, p.out_lo, (size_t)(row + slot + D) * ld + m, q);
+}
+
+// The same rule with D known at compile time (D <= 8, P <= 54): the point's P columns
+// are read with one burst of x16/x8/x4/x2/x1 loads and a single wait, and every slot
+// index is a constant, so the whole point lives in registers.
+template <int D>
+__device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t tcol, int64_t row, int m,
+                                                  float bias, float wo, float& fpart, float& opart) {
+  constexpr int T = D * (D + 1) / 2;
+  constexpr int P = 2 + 2 * D + T;
+  constexpr int oH = 1 + D, oL = 1 + D + T;
+  float v[P];
+  ptx::tmem_ld_cols<P>(tcol, v);
+  ptx::tmem_ld_wait();
+  const int ld = p.ldo;
+  const float t = tanhf(v[0] + bias);
+  const float d1 = 1.f - t * t;
+  const float d2 = -2.f * t * d1;
+  const float d3 = d1 * (6.f * t * t - 2.f);
+  const float d4 = 8.f * t * d1 * (2.f - 3.f * t * t);
+  const float* g = v + 1;
+  float gg = 0.f, trH = 0.f, HF = 0.f, gL = 0.f, gHg = 0.f;
+  float hg[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    gg = fmaf(g[a], g[a], gg);
+    gL = fmaf(g[a], v[oL + a], gL);
+    hg[a] = 0.f;
+  }
+  {
+    int k = oH;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = a; b < D; ++b, ++k) {
+        const float h = v[k];
+        if (b == a) {
+          trH += h;
+          HF = fmaf(h, h, HF);
+          hg[a] = fmaf(h, g[a], hg[a]);
+        } else {
+          HF = fmaf(2.f * h, h, HF);
+          hg[a] = fmaf(h, g[b], hg[a]);
+          hg[b] = fmaf(h, g[a], hg[b]);
+        }
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) gHg = fmaf(g[a], hg[a], gHg);
+  const float q = d4 * gg * gg + 2.f * d3 * gg * trH + 4.f * d3 * gHg + 2.f * d2 * HF + d2 * trH * trH +
+                  4.f * d2 * gL + d1 * v[P - 1];
+  fpart = wo * t;
+  opart = wo * q;
+  if (p.readout) return;
+  uint16_t* ph = p.out_hi + (size_t)row * ld + m;
+  uint16_t* pl = p.out_lo + (size_t)row * ld + m;
+  store_pair(ph, pl, 0, t);
+#pragma unroll
+  for (int a = 0; a < D; ++a) store_pair(ph, pl, (size_t)(1 + a) * ld, d1 * g[a]);
+  {
+    int k = oH;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = a; b < D; ++b, ++k) store_pair(ph, pl, (size_t)k * ld, fmaf(d2 * g[a], g[b], d1 * v[k]));
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    store_pair(ph, pl, (size_t)(oL + a) * ld,
+               d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * v[oL + a]);
+  store_pair(ph, pl, (size_t)(P - 1) * ld, q);
+}
+
+__device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32_t tcol, int64_t row, int m,
+                                                    float bias, float wo, float& fpart, float& opart) {
+  switch (p.J) {
+    case 1: epilogue_nested_d<1>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 2: epilogue_nested_d<2>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 3: epilogue_nested_d<3>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 4: epilogue_nested_d<4>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 5: epilogue_nested_d<5>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 6: epilogue_nested_d<6>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 7: epilogue_nested_d<7>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 8: epilogue_nested_d<8>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    default: epilogue_nested(p, tcol, row, m, bias, wo, fpart, opart);
+  }
 }
 
 // The k-th tile of CTA pair `pair`. With at least one point group per pair, a pair runs
@@ -351,7 +532,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
-      if (p.pts_per_tile == 1) {
+      if (KORD == kNest) {
+        // nested biharmonic: a point is never split; with one point per tile (D >= 14)
+        // only warp group 0 works on it
+        for (int pt = g; pt < npts; pt += 2) {
+          float fpart, opart;
+          epilogue_nested_any(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, fpart,
+                              opart);
+          if (p.readout) {
+            fpart = warp_sum(fpart);
+            opart = warp_sum(opart);
+            if (lane == 0) {
+              red[(q * kMaxPtsPerTile + pt) * 2 + 0] = fpart;
+              red[(q * kMaxPtsPerTile + pt) * 2 + 1] = opart;
+            }
+          }
+        }
+      } else if (p.pts_per_tile == 1) {
         // one point per tile: both warp groups share it (split at a jet / pair boundary)
         float fpart, opart;
         epilogue_point<KORD>(p, tbase, row0, m, bias, wo, jw, g + 1, split, xacc + (local & 1u) * kBM + m_local,

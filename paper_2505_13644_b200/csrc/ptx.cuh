@@ -152,6 +152,42 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
   return __uint_as_float(r);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+}
+// N consecutive columns into v[0..N), composed at compile time from x16/x8/x4/x2/x1
+// loads (no column past N is touched). Needs tmem_ld_wait() before v is read.
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+  if constexpr (N >= 16) {
+    tmem_ld16(taddr, v);
+    tmem_ld_cols<N - 16>(taddr + 16u, v + 16);
+  } else if constexpr (N >= 8) {
+    tmem_ld8(taddr, v);
+    tmem_ld_cols<N - 8>(taddr + 8u, v + 8);
+  } else if constexpr (N >= 4) {
+    tmem_ld4(taddr, v);
+    tmem_ld_cols<N - 4>(taddr + 4u, v + 4);
+  } else if constexpr (N >= 2) {
+    tmem_ld2(taddr, v);
+    tmem_ld_cols<N - 2>(taddr + 2u, v + 2);
+  } else if constexpr (N == 1) {
+    v[0] = tmem_ld1(taddr);
+  }
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"), K-major operand:

@@ -118,6 +118,30 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
     // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
     seed_store4(p.out_hi, p.out_lo, (row0 + 1 + p.R) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
                 d2[3] * cs.w);
+  } else if (KORD == kNest) {
+    // nested biharmonic, layer 1: g_a = W1[:, a] = UT[a] and H = L = Q = 0 at the input,
+    // so h_a = s' g_a, H'_ab = s'' g_a g_b, L'_a = s''' g_a |g|^2, Q' = s'''' |g|^4 (the
+    // epilogue rule of jet_layer.cuh with H = L = Q = 0); |g|^2 = csum.
+    size_t r = row0 + 1;
+    for (int a = 0; a < p.R; ++a, ++r) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)a * p.ld + m));
+      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+    }
+    for (int a = 0; a < p.R; ++a) {
+      const float4 ua = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)a * p.ld + m));
+      for (int b = a; b < p.R; ++b, ++r) {
+        const float4 ub = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)b * p.ld + m));
+        seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d2[0] * ua.x * ub.x, d2[1] * ua.y * ub.y,
+                    d2[2] * ua.z * ub.z, d2[3] * ua.w * ub.w);
+      }
+    }
+    for (int a = 0; a < p.R; ++a, ++r) {
+      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)a * p.ld + m));
+      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
+                  d3[3] * u.w * cs.w);
+    }
+    seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
+                d4[3] * cs.w * cs.w);
   } else {
     for (int j = 0; j < p.R; ++j) {
       const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)j * p.ld + m));

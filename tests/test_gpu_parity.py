@@ -216,6 +216,46 @@ def test_biharmonic_parity(ctm, widths, N):
     check(op, want, norm, f, fwant)
 
 
+# ------------------------------------------------------------------ nested-Laplacian biharmonic (NEXT-2)
+@pytest.mark.parametrize("widths,N", [
+    ([1, 40, 24, 1], 13),           # D = 1: P = 5, the K=4 Faa di Bruno row
+    ([5, 12, 1], 4),                # one hidden layer: the layer-1 block is read out directly
+    ([5, 16, 16, 1], 8),            # BASELINE C0 shape
+    (C4_WIDTHS, 37),                # BASELINE C4: P = 27 (vs 107 by interpolation), 9 points per tile
+    ([13, 96, 80, 1], 7),           # P = 119: two points per tile
+    ([14, 64, 64, 1], 3),           # P = 135: one point per tile
+    ([20, 128, 64, 1], 3),          # P = 252: the slot cap, D beyond the interpolation route's 7
+])
+def test_biharmonic_nested_parity(ctm, widths, N):
+    """GPU nested route vs the oracle's nested route (value) with the north_star
+    normaliser of the O1 interpolation route (same operator, Eq. 12)."""
+    params, onet = nets(widths)
+    D = widths[0]
+    X = points(N, D)
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.biharmonic_nested(torch.from_numpy(X).cuda())
+    P = 2 + 2 * D + D * (D + 1) // 2
+    assert mlp.last_plan()["slots_per_point"] == P
+    want, fwant, _ = O.biharmonic_nested(onet, Xd)
+    ref, _, norm = O.biharmonic(onet, Xd, O.O1)
+    assert np.max(np.abs(want - ref) / norm) < 1e-11  # the two oracle routes agree
+    check(op, want, norm, f, fwant)
+
+
+def test_biharmonic_nested_matches_interpolation_route_and_refuses_d21(ctm):
+    params, onet = nets(C4_WIDTHS)
+    X = torch.from_numpy(points(64, 5)).cuda()
+    mlp = gpu_mlp(ctm, params)
+    a = mlp.biharmonic_nested(X)[0].double().cpu().numpy()
+    b = mlp.biharmonic(X)[0].double().cpu().numpy()
+    _, _, norm = O.biharmonic(onet, X.cpu().double().numpy(), O.O1)
+    assert np.max(np.abs(a - b) / norm) < 2 * TOL
+    params, _ = nets([21, 16, 1])
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        gpu_mlp(ctm, params).biharmonic_nested(torch.zeros(2, 21).cuda())
+
+
 # ------------------------------------------------------------------ stochastic biharmonic (NEXT-2)
 @pytest.mark.parametrize("widths,N,S", [([3, 24, 24, 1], 7, 5), (C4_WIDTHS, 13, 16), (C4_WIDTHS, 3, 84)])
 def test_stochastic_biharmonic_parity(ctm, widths, N, S):
