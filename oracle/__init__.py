@@ -65,6 +65,7 @@ def lib():
         _lib.ctmo_randomized_laplacian.argtypes = [P(_Net), vp, i64, vp, i32, vp, i32, i32, vp, vp, vp]
         _lib.ctmo_forward.argtypes = [P(_Net), vp, i64, vp]
         _lib.ctmo_stochastic_biharmonic.argtypes = [P(_Net), vp, i64, vp, i32, i32, vp, vp, vp]
+        _lib.ctmo_directional_sum.argtypes = [P(_Net), vp, i64, i32, i32, vp, i32, vp, i32, vp, vp, vp]
         _lib.ctmo_biharmonic_nested.argtypes = [P(_Net), vp, i64, vp, vp, vp]
         _lib.ctmo_act_derivs.argtypes = [i32, d, vp]
         _lib.ctmo_act_derivs.restype = None
@@ -159,6 +160,21 @@ def stochastic_biharmonic(net: Net, X, V, route=O1):
     """1/(3S) sum_s <d^4 f, v_s^4> with V [N, S, D] (Eq. 12 stochastic, unbiased scale, Q1)."""
     V = _f64(V)
     return _call(lib().ctmo_stochastic_biharmonic, net, X, _ptr(V), V.shape[1], route=route)
+
+
+def directional_sum(net: Net, X, K: int, dirs, w, route=O1):
+    """sum_j w_j <d^K f, u_j^K> (K = 2 or 4); dirs [J, D] shared or [N, J, D] per point."""
+    dirs, w = _f64(dirs), _f64(w).reshape(-1)
+    per_point = dirs.ndim == 3
+    return _call(lib().ctmo_directional_sum, net, X, int(K), int(w.size), _ptr(dirs), int(per_point), _ptr(w),
+                 route=route)
+
+
+def weighted_laplacian_pointwise(net: Net, X, sigma_x, route=O1):
+    """<d^2 f(x_n), sigma(x_n) sigma(x_n)^T> with sigma_x [N, D, R] (Eq. 10, sigma depending on x)."""
+    sigma_x = _f64(sigma_x)
+    U = np.ascontiguousarray(np.transpose(sigma_x, (0, 2, 1)))  # [N, R, D]: the columns s_r(x_n)
+    return directional_sum(net, X, 2, U, np.ones(U.shape[1]), route)
 
 
 def biharmonic_nested(net: Net, X):

@@ -392,10 +392,11 @@ static void route_o3(const ctmo_net *net, const dirset_t *ds, const double *X, i
 static int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; return r; }
 
 /* C2 [D*D] coefficient matrix (K=2). For K=4: if dirs4 is NULL, C is the biharmonic
- * tensor sum_{a,b} e_a (x) e_a (x) e_b (x) e_b; otherwise C = c4 sum_s v_s^{(x)4} with the
- * per-point directions dirs4 [N, S4, D]. Returns <d^K f, C> per point. */
+ * tensor sum_{a,b} e_a (x) e_a (x) e_b (x) e_b; otherwise C = sum_s c_s v_s^{(x)4} with
+ * c_s = w4[s] (or c4 when w4 is NULL) and the directions dirs4 [N, S4, D] per point
+ * (d4_per_point) or [S4, D] shared. Returns <d^K f, C> per point. */
 static void route_o2(const ctmo_net *net, int K, const double *C2, int C2_per_point,
-                     const double *dirs4, int S4, double c4,
+                     const double *dirs4, int S4, double c4, const double *w4, int d4_per_point,
                      const double *X, int64_t N, double *op, double *f)
 {
     const int D = net->widths[0], L = net->L, wm = max_width(net);
@@ -497,11 +498,12 @@ static void route_o2(const ctmo_net *net, int K, const double *C2, int C2_per_po
             } else {
                 const double *T4 = A + toff[4];
                 for (int s = 0; s < S4; ++s) {
-                    const double *v = dirs4 + ((size_t)n * S4 + s) * D;
+                    const double *v = dirs4 + ((size_t)(d4_per_point ? n * S4 : 0) + s) * D;
+                    const double cs = w4 ? w4[s] : c4;
                     for (int a = 0; a < D; ++a)
                         for (int b = 0; b < D; ++b)
                             for (int c = 0; c < D; ++c)
-                                for (int e = 0; e < D; ++e) val += c4 * T4[I4(a, b, c, e)] * v[a] * v[b] * v[c] * v[e];
+                                for (int e = 0; e < D; ++e) val += cs * T4[I4(a, b, c, e)] * v[a] * v[b] * v[c] * v[e];
                 }
             }
             op[n] = val;
@@ -534,7 +536,7 @@ int ctmo_laplacian(const ctmo_net *net, const double *X, int64_t N, int32_t rout
     if (route == CTMO_O2) {
         double *C = calloc((size_t)D * D, sizeof(double));
         for (int a = 0; a < D; ++a) C[a * D + a] = 1.0; /* <d^2 f, I_D> */
-        route_o2(net, 2, C, 0, NULL, 0, 0.0, X, N, op, f);
+        route_o2(net, 2, C, 0, NULL, 0, 0.0, NULL, 0, X, N, op, f);
         free(C);
         fill_nan(norm, N);
         return 0;
@@ -564,7 +566,7 @@ int ctmo_weighted_laplacian(const ctmo_net *net, const double *X, int64_t N,
         for (int a = 0; a < D; ++a)
             for (int b = 0; b < D; ++b)
                 for (int r = 0; r < R; ++r) C[a * D + b] += sigma[a * R + r] * sigma[b * R + r];
-        route_o2(net, 2, C, 0, NULL, 0, 0.0, X, N, op, f);
+        route_o2(net, 2, C, 0, NULL, 0, 0.0, NULL, 0, X, N, op, f);
         free(C);
         fill_nan(norm, N);
         return 0;
@@ -614,7 +616,7 @@ int ctmo_randomized_laplacian(const ctmo_net *net, const double *X, int64_t N,
                 for (int a = 0; a < D; ++a)
                     for (int b = 0; b < D; ++b) C[(size_t)n * D * D + a * D + b] += u[a] * u[b] / S;
             }
-        route_o2(net, 2, C, 1, NULL, 0, 0.0, X, N, op, f);
+        route_o2(net, 2, C, 1, NULL, 0, 0.0, NULL, 0, X, N, op, f);
         free(C);
         fill_nan(norm, N);
     } else {
@@ -727,7 +729,7 @@ int ctmo_biharmonic(const ctmo_net *net, const double *X, int64_t N, int32_t rou
     init_partitions();
     const int D = net->widths[0];
     if (route == CTMO_O2) {
-        route_o2(net, 4, NULL, 0, NULL, 0, 0.0, X, N, op, f);
+        route_o2(net, 4, NULL, 0, NULL, 0, 0.0, NULL, 0, X, N, op, f);
         fill_nan(norm, N);
         return 0;
     }
@@ -762,7 +764,7 @@ int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, 
     init_partitions();
     const double c = 1.0 / (3.0 * S);
     if (route == CTMO_O2) {
-        route_o2(net, 4, NULL, 0, V, S, c, X, N, op, f);
+        route_o2(net, 4, NULL, 0, V, S, c, NULL, 1, X, N, op, f);
         fill_nan(norm, N);
         return 0;
     }
@@ -771,6 +773,59 @@ int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, 
     else if (route == CTMO_O3) { route_o3(net, &ds, X, N, op, f); fill_nan(norm, N); }
     else return 1;
     return 0;
+}
+
+/* General linear operator of degree K as a weighted sum of K-th directional
+ * derivatives (Eq. 5 `eq:sum-k-directional` P:548-558 with coefficients; the form Eq. 15
+ * `eq:ttc-general` P:824-839 reduces any <d^K f, C> to, with the gamma_{i,j}/K! of
+ * Eq. F1 as weights):  op = sum_j w_j <d^K f(x0), u_j^{(x)K}>,  K in {2, 4}.
+ * dirs [J, D] shared, or [N, J, D] per point (per_point != 0); w [J].
+ * O1: one K-jet per direction; O3: collapsed, one summed top coefficient per group of
+ * equal weights (Eq. 7); O2: the explicit tensor contracted with sum_j w_j u_j^{(x)K}. */
+int ctmo_directional_sum(const ctmo_net *net, const double *X, int64_t N, int32_t K, int32_t J,
+                         const double *dirs, int32_t per_point, const double *w, int32_t route,
+                         double *op, double *f, double *norm)
+{
+    if (check_net(net) || N < 0 || J < 1 || !dirs || !w || (K != 2 && K != 4) ||
+        (N > 0 && (!X || !op)))
+        return 1;
+    init_partitions();
+    const int D = net->widths[0];
+    if (route == CTMO_O2) {
+        if (K == 2) {
+            const int64_t nC = per_point ? (N > 0 ? N : 1) : 1;
+            double *C = calloc((size_t)nC * D * D, sizeof(double));
+            for (int64_t n = 0; n < nC; ++n)
+                for (int j = 0; j < J; ++j) {
+                    const double *u = dirs + ((size_t)n * J + j) * D;
+                    for (int a = 0; a < D; ++a)
+                        for (int b = 0; b < D; ++b) C[(size_t)n * D * D + a * D + b] += w[j] * u[a] * u[b];
+                }
+            route_o2(net, 2, C, per_point != 0, NULL, 0, 0.0, NULL, 0, X, N, op, f);
+            free(C);
+        } else {
+            route_o2(net, 4, NULL, 0, dirs, J, 0.0, w, per_point != 0, X, N, op, f);
+        }
+        fill_nan(norm, N);
+        return 0;
+    }
+    /* groups of equal weight (first-occurrence order) */
+    int *group = malloc(sizeof(int) * J);
+    double *gcoef = malloc(sizeof(double) * J);
+    int G = 0;
+    for (int j = 0; j < J; ++j) {
+        int g = 0;
+        while (g < G && gcoef[g] != w[j]) ++g;
+        if (g == G) gcoef[G++] = w[j];
+        group[j] = g;
+    }
+    dirset_t ds = {K, J, G, dirs, per_point != 0, group, gcoef};
+    int rc = 0;
+    if (route == CTMO_O1) route_o1(net, &ds, X, N, op, f, norm);
+    else if (route == CTMO_O3) { route_o3(net, &ds, X, N, op, f); fill_nan(norm, N); }
+    else rc = 1;
+    free(group); free(gcoef);
+    return rc;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -77,6 +77,13 @@ int ctmo_biharmonic(const ctmo_net *net, const double *X, int64_t N, int32_t rou
 int ctmo_stochastic_biharmonic(const ctmo_net *net, const double *X, int64_t N, const double *V, int32_t S,
                                int32_t route, double *op, double *f, double *norm);
 
+/* Weighted sum of K-th directional derivatives, K in {2, 4} (Eq. 5 with weights; the
+ * reduction target of the general approach Eq. 13-15):
+ * op = sum_j w[j] <d^K f(x0), u_j^{(x)K}>, dirs [J, D] shared or [N, J, D] per point. */
+int ctmo_directional_sum(const ctmo_net *net, const double *X, int64_t N, int32_t K, int32_t J,
+                         const double *dirs, int32_t per_point, const double *w, int32_t route,
+                         double *op, double *f, double *norm);
+
 /* Biharmonic by NESTED collapsed Laplacians:
  * Laplacian^2 f = Laplacian(Laplacian f), the inner Laplacian in collapsed Taylor mode
  * (Eq. 7/8) evaluated in the 2-jet arithmetic of an outer collapsed Laplacian.

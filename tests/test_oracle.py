@@ -510,3 +510,79 @@ def test_nested_biharmonic_vs_tensor_route_interpolation_and_autograd():
     want = lap(lambda y: lap(tf, y), x).item()
     got = O.biharmonic_nested(O.Net(Ws, bs), x.detach().numpy()[None])[0][0]
     assert abs(got - want) < 1e-10 * max(1.0, abs(want))
+
+
+# --------------------------------------------------------------------------
+# Weighted directional sums (Eq. 5 with weights; Eq. 13-15 general approach)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("K", [2, 4])
+@pytest.mark.parametrize("per_point", [False, True])
+def test_directional_sum_routes_agree(K, per_point):
+    D, J, N = 3, 5, 4
+    net = _mid_net(D, 61)
+    rng = np.random.default_rng(62)
+    X = _pts(N, D, seed=63)
+    dirs = rng.standard_normal((N, J, D) if per_point else (J, D))
+    w = rng.uniform(-1, 1, J)
+    w[1] = w[0]  # a group of two equal weights for the collapsed route
+    o1, f1, norm = O.directional_sum(net, X, K, dirs, w, O.O1)
+    o2, f2, _ = O.directional_sum(net, X, K, dirs, w, O.O2)
+    o3, _, _ = O.directional_sum(net, X, K, dirs, w, O.O3)
+    assert np.max(np.abs(o1 - o3) / norm) < 1e-12
+    assert np.max(np.abs(o1 - o2) / norm) < 1e-11
+    np.testing.assert_allclose(f1, O.forward(net, X), rtol=1e-14)
+
+
+def test_directional_sum_reduces_to_the_named_operators():
+    D = 4
+    net = _mid_net(D, 64)
+    X = _pts(3, D, seed=65)
+    np.testing.assert_allclose(O.directional_sum(net, X, 2, np.eye(D), np.ones(D))[0], O.laplacian(net, X)[0],
+                               rtol=1e-13)
+    dirs, coef = O.biharmonic_set(D)
+    np.testing.assert_allclose(O.directional_sum(net, X, 4, dirs, coef)[0], O.biharmonic(net, X)[0], rtol=1e-12)
+    sig = np.random.default_rng(66).standard_normal((D, 3))
+    sx = np.broadcast_to(sig, (3, D, 3))
+    np.testing.assert_allclose(O.weighted_laplacian_pointwise(net, X, sx)[0], O.weighted_laplacian(net, X, sig)[0],
+                               rtol=1e-13)
+
+
+def test_directional_sum_closed_forms():
+    # quadratic net: <d^2 f, u^2> = u^T H u;  ||x||^4: <d^4 f, u^4> = 24 |u|^4
+    D, H = 5, 6
+    Ws, bs = random_params([D, H, 1], 3, scale=2.0)
+    net = O.Net(Ws, bs, "square")
+    Hess = 2 * (Ws[0].T * Ws[1][0]) @ Ws[0]
+    rng = np.random.default_rng(67)
+    X = _pts(4, D)
+    dirs, w = rng.standard_normal((3, D)), np.array([0.5, -2.0, 1.25])
+    np.testing.assert_allclose(O.directional_sum(net, X, 2, dirs, w)[0], np.einsum("j,ja,ab,jb->", w, dirs, Hess, dirs),
+                               rtol=1e-12)
+    sx = rng.standard_normal((4, D, 2))  # sigma(x_n): a different sigma per point
+    np.testing.assert_allclose(O.weighted_laplacian_pointwise(net, X, sx)[0],
+                               np.einsum("ab,nar,nbr->n", Hess, sx, sx), rtol=1e-12)
+    net4 = _norm4_net(D)
+    np.testing.assert_allclose(O.directional_sum(net4, X, 4, dirs, w)[0], 24 * np.sum(w * np.sum(dirs**2, 1) ** 2),
+                               rtol=1e-12)
+
+
+@pytest.mark.parametrize("i", [(3, 1), (2, 2)])
+def test_interpolation_family_eq15_recovers_mixed_partials(i):
+    """Eq. 15 with I = 2, v_1 = e_1, v_2 = e_2: the family j in N^2, |j| = 4, directions
+    j_1 e_1 + j_2 e_2, weights gamma_{i,j} / 4!, gives d_1^{i_1} d_2^{i_2} f, checked against
+    torch fp64 autograd on a tanh net (gamma pinned by Fig. 3 separately)."""
+    D = 2
+    Ws, bs = random_params([D, 9, 7, 1], 71, scale=1.5)
+    net = O.Net(Ws, bs, "tanh")
+    x = _pts(1, D, seed=72)[0]
+    fam = [(j1, 4 - j1) for j1 in range(5)]
+    dirs = np.array([[j1, j2] for j1, j2 in fam], dtype=float)
+    w = np.array([float(O.gamma(i, j)) / 24.0 for j in fam])
+    got = O.directional_sum(net, x[None], 4, dirs, w)[0][0]
+    tf = _torch_f(Ws, bs)
+    xt = torch.tensor(x, requires_grad=True)
+    g = tf(xt)
+    for ax in [0] * i[0] + [1] * i[1]:
+        (gr,) = torch.autograd.grad(g, xt, create_graph=True)
+        g = gr[ax]
+    assert abs(got - g.item()) < 1e-10 * max(1.0, abs(g.item()))
