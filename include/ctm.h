@@ -109,6 +109,30 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, in
 ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                           void *stream);
 
+/* Weighted Laplacian with a point-dependent sigma (Eq. 10; "sigma can depend on x0",
+ * P:686): op[n] = <d^2 f(x_n), sigma(x_n) sigma(x_n)^T> = sum_r <d^2 f(x_n), s_r(x_n)^2>.
+ *   sigma_x [N, D, R] device, fp32: sigma(x_n) row-major [D, R] for each point (the
+ *   caller evaluates sigma at its points). P = R + 2 <= 256. Layer 1 runs on the tensor
+ *   cores as for ctm_randomized_laplacian with explicit V. Errors: CTM_EINVAL (NULL
+ *   sigma_x, R < 1), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (R > 254, D > 256). */
+ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma_x,
+                                            int32_t R, float *op_out, float *f_out, void *stream);
+
+/* General linear operator of degree K as a weighted sum of K-th directional derivatives
+ * (Eq. 5 `eq:sum-k-directional` P:548-558 with coefficients; the general approach of
+ * Eq. 13-15, reduces <d^K f, C> to this form with the weights gamma_{i,j}/K!
+ * of Eq. F1 and directions sum_i v_{d_i} [j]_i):
+ *   op[n] = sum_j weights[j] <d^K f(x_n), u_j^{(x)K}>,   K in {2, 4},
+ * collapsed: one summed, weighted top coefficient (Eq. 7).
+ *   dirs [J, D] (per_point = 0: the same directions for every point; U = W1 u_j is
+ *   computed once per call) or [N, J, D] (per_point = 1); weights [J]; device, fp32.
+ *   P = J + 2 (K = 2) or 3J + 2 (K = 4) <= 256; per-point K = 4 also needs J*D <= 12288.
+ * Errors: CTM_EINVAL (NULL dirs/weights, J < 1), CTM_ESHAPE (misaligned),
+ * CTM_EUNSUPPORTED (K not 2 or 4, slot cap, D > 256). */
+ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float *X, int64_t N, int32_t K, int32_t J,
+                               const float *dirs, int32_t per_point, const float *weights, float *op_out,
+                               float *f_out, void *stream);
+
 /* Exact biharmonic by NESTED collapsed Laplacians, Laplacian(Laplacian f) (P:1192,
  * "the most efficient way to compute biharmonics is by nesting
  * Laplacians ... while also allowing to apply our collapsing technique"). The slots of

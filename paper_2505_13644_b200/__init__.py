@@ -33,6 +33,8 @@ ABI = {
     ),
     "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_biharmonic_nested": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_weighted_laplacian_pointwise": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
+    "ctm_directional_sum": (ctypes.c_int, [_VP, _VP, _I64, _I32, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
                                                  _VP]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
@@ -181,6 +183,32 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_biharmonic(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                     _stream_ptr(stream, self.device)), "ctm_biharmonic")
+        return out, f_out
+
+    def weighted_laplacian_pointwise(self, X, sigma_x, out=None, f_out=None, want_f=True, stream=None):
+        """<d^2 f(x_n), sigma(x_n) sigma(x_n)^T> with sigma_x [N, D, R] (Eq. 10, sigma depending on x)."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        sigma_x = _dev_f32(sigma_x, self.device, "sigma_x")
+        if sigma_x.dim() != 3 or sigma_x.shape[0] != N:
+            raise CTMError("sigma_x must be [N, D, R]")
+        _check(lib().ctm_weighted_laplacian_pointwise(self._h, X.data_ptr(), N, sigma_x.data_ptr(),
+                                                      int(sigma_x.shape[2]), out.data_ptr(), self._p(f_out),
+                                                      _stream_ptr(stream, self.device)),
+               "ctm_weighted_laplacian_pointwise")
+        return out, f_out
+
+    def directional_sum(self, X, K, dirs, weights, out=None, f_out=None, want_f=True, stream=None):
+        """sum_j w_j <d^K f, u_j^K>, K in {2, 4}; dirs [J, D] shared or [N, J, D] per point (Eq. 5, Eq. 13-15)."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        dirs = _dev_f32(dirs, self.device, "dirs")
+        weights = _dev_f32(weights, self.device, "weights")
+        per_point = dirs.dim() == 3
+        J = int(weights.numel())
+        if dirs.shape[-2] != J or (per_point and dirs.shape[0] != N):
+            raise CTMError("dirs must be [J, D] or [N, J, D] with J = len(weights)")
+        _check(lib().ctm_directional_sum(self._h, X.data_ptr(), N, int(K), J, dirs.data_ptr(), int(per_point),
+                                         weights.data_ptr(), out.data_ptr(), self._p(f_out),
+                                         _stream_ptr(stream, self.device)), "ctm_directional_sum")
         return out, f_out
 
     def biharmonic_nested(self, X, out=None, f_out=None, want_f=True, stream=None):

@@ -117,7 +117,7 @@ struct ctm_mlp {
   // per-call scratch
   float* U_call = nullptr;
   float* c_call = nullptr;
-  size_t U_call_elems = 0;
+  size_t U_call_elems = 0, c_call_elems = 0;
   // workspace (bf16 hi, lo planes): see ensure_workspace
   uint16_t* blk[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   size_t blk_elems[4] = {0, 0, 0, 0};
@@ -283,7 +283,7 @@ Plan make_plan(int P) {
   return pl;
 }
 
-enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST };
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST, OP_DSUM, OP_WLAP_X };
 
 struct CallArgs {
   Op op;
@@ -300,7 +300,21 @@ struct CallArgs {
   float* op_out;
   float* f_out;
   cudaStream_t stream;
+  // OP_DSUM: sum_j w_j <d^K f, u_j^K>; dirs [J, D] (shared) or [N, J, D] (per point)
+  int K = 0;
+  int J = 0;
+  const float* dirs = nullptr;
+  int per_point = 0;
+  const float* weights = nullptr;
+  int v_trans = 0;  // OP_WLAP_X: V = sigma(x) stored [N, D, R]
 };
+
+// per-point K=2 directions: the input block [x0; u; 0] and layer 1 on the tensor cores
+bool random_k2(const CallArgs& a) {
+  return a.op == OP_RLAP || a.op == OP_WLAP_X || (a.op == OP_DSUM && a.per_point && a.K == 2);
+}
+// per-point K=4 directions: layer 1 in fp32 on the CUDA cores (seed_stoch_biharmonic_kernel)
+bool stoch_k4(const CallArgs& a) { return a.op == OP_SBIH || (a.op == OP_DSUM && a.per_point && a.K == 4); }
 
 struct GemmLayer {
   const CUtensorMap* a_hi;
@@ -319,7 +333,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
   const int64_t blocks = n * mchunks;
   if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
   ProfScope ps(h, CTM_KIND_SEED, (double)n * P * h->widths[1] * 4.0, st);
-  if (a.op == OP_SBIH) {
+  if (stoch_k4(a)) {
     ctm::SeedStochParams bp{};
     bp.X = a.X + p0 * D;
     bp.D = D;
@@ -328,6 +342,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
     bp.ld = ld1;
     bp.S = a.S;
     bp.V = a.V ? a.V + p0 * a.S * D : nullptr;
+    bp.w = (a.op == OP_DSUM) ? a.weights : nullptr;
     bp.seed = a.seed;
     bp.point_offset = a.point_offset + p0;
     bp.out_hi = buf[0];
@@ -400,8 +415,13 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     lp.pts_per_tile = pl.ppt;
     lp.n_mma = pl.nmma;
     lp.k_iters = gl.kpad / ctm::kBK;
-    lp.jet_w = (a.op == OP_SBIH) ? h->w_ones : h->w_bih;
-    lp.J = (a.op == OP_SBIH) ? a.S : (a.op == OP_BIH_NEST) ? h->widths[0] : h->J_bih;
+    switch (a.op) {
+      case OP_SBIH: lp.jet_w = h->w_ones; lp.J = a.S; break;
+      case OP_BIH: lp.jet_w = h->w_bih; lp.J = h->J_bih; break;
+      case OP_BIH_NEST: lp.J = h->widths[0]; break;
+      case OP_DSUM: lp.jet_w = a.weights; lp.J = a.J; lp.weighted = (a.K == 2); break;
+      default: break;
+    }
     if (last) {
       ctm_status s = ensure(h->partial, h->partial_elems, (size_t)n * m_tiles * 2);
       if (s != CTM_OK) return s;
@@ -453,10 +473,10 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
 ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int D = h->widths[0];
   const int ld1 = h->wpad[1];
-  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH) ? 4
-                   : (a.op == OP_LAP_STD)                ? ctm::kStd2
-                   : (a.op == OP_BIH_NEST)               ? ctm::kNest
-                                                         : 2;
+  const int KORD = (a.op == OP_BIH || a.op == OP_SBIH || (a.op == OP_DSUM && a.K == 4)) ? 4
+                   : (a.op == OP_LAP_STD)                                             ? ctm::kStd2
+                   : (a.op == OP_BIH_NEST)                                            ? ctm::kNest
+                                                                                      : 2;
   int P = 0;
   switch (a.op) {
     case OP_LAP: P = D + 2; break;
@@ -466,11 +486,13 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     case OP_LAP_STD: P = 1 + 2 * D; break;
     case OP_SBIH: P = 3 * a.S + 2; break;
     case OP_BIH_NEST: P = 2 + 2 * D + D * (D + 1) / 2; break;
+    case OP_DSUM: P = (a.K == 4 ? 3 : 1) * a.J + 2; break;
+    case OP_WLAP_X: P = a.S + 2; break;
   }
   if (P > ctm::kMaxN)
     return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
-  if (a.op == OP_SBIH && (int64_t)a.S * D > 12288)
-    return fail(CTM_EUNSUPPORTED, "S * D > 12288 for the stochastic biharmonic");
+  if (stoch_k4(a) && (int64_t)a.S * D > 12288)
+    return fail(CTM_EUNSUPPORTED, "S * D > 12288 for per-point K=4 directions");
   const Plan pl = make_plan(P);
   h->last_P = pl.P;
   h->last_ppt = pl.ppt;
@@ -486,12 +508,12 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
 
   // GEMM layers: layer 1 for per-point K=2 directions, then the hidden layers 2..L-1
   std::vector<GemmLayer> layers;
-  if (a.op == OP_RLAP) layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
+  if (random_k2(a)) layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
   for (int l = 2; l <= h->L - 1; ++l)
     layers.push_back({&h->mapA_hi[l - 2], &h->mapA_lo[l - 2], h->bias[l - 2], h->wpad[l - 1], h->wpad[l],
                       h->widths[l - 1], h->widths[l]});
 
-  if (a.op == OP_RLAP) {
+  if (random_k2(a)) {
     // per-point K=2 directions: the input block [x0; u_1..u_S; 0], then layer 1 on the
     // tensor cores like every other layer
     s = ensure_workspace(h, a.N * (int64_t)P, 1);
@@ -507,6 +529,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.seed = a.seed;
     rp.point_offset = a.point_offset;
     rp.gaussian = a.gaussian;
+    rp.v_trans = a.v_trans;
     rp.out_hi = h->blk[2][0];
     rp.out_lo = h->blk[2][1];
     {
@@ -514,7 +537,8 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
     }
     ++launches;
-    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, h->blk[2], 1.f / (float)a.S, st, nullptr, launches);
+    const float scale = (a.op == OP_RLAP) ? 1.f / (float)a.S : 1.f;  // Eq. 8/10 stochastic: the mean
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, h->blk[2], scale, st, nullptr, launches);
     if (s != CTM_OK) return s;
   } else {
     // fixed direction sets (or the K=4 stochastic seed): U and the per-feature constant
@@ -525,10 +549,25 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       UT = h->U_bih;
       csum = h->c_bih;
       R = h->J_bih;
+    } else if (a.op == OP_DSUM && !a.per_point) {  // U = W1 u_j, c = sum_j w_j (W1 u_j)^K for this call
+      s = ensure(h->U_call, h->U_call_elems, (size_t)a.J * ld1);
+      if (s != CTM_OK) return s;
+      s = ensure(h->c_call, h->c_call_elems, (size_t)ld1);
+      if (s != CTM_OK) return s;
+      {
+        ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
+        ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.dirs, a.J, a.weights, a.K,
+                                                                       h->U_call, h->c_call);
+      }
+      ++launches;
+      UT = h->U_call;
+      csum = h->c_call;
+      R = a.J;
     } else if (a.op == OP_WLAP) {  // U = W1 sigma for this call
       s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
       if (s != CTM_OK) return s;
-      if (!h->c_call) CTM_CUDA(cudaMalloc(&h->c_call, sizeof(float) * 8192));
+      s = ensure(h->c_call, h->c_call_elems, (size_t)ld1);
+      if (s != CTM_OK) return s;
       {
         ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
         ctm::prep_sigma_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, a.sigma, a.R, h->U_call,
@@ -790,6 +829,38 @@ ctm_status ctm_biharmonic_nested(ctm_mlp_t mlp, const float* X, int64_t N, float
   if (mlp->widths[0] > ctm::kNestMaxD)
     return fail(CTM_EUNSUPPORTED, "nested biharmonic needs 2 + 2D + D(D+1)/2 <= 256 slots, i.e. D <= 20");
   CallArgs a{OP_BIH_NEST, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float* X, int64_t N, int32_t K, int32_t J, const float* dirs,
+                               int32_t per_point, const float* weights, float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (K != 2 && K != 4) return fail(CTM_EUNSUPPORTED, "K must be 2 or 4");
+  if (J < 1 || !dirs || !weights) return fail(CTM_EINVAL, "need J >= 1, dirs and weights");
+  if (!aligned16(dirs) || !aligned16(weights)) return fail(CTM_ESHAPE, "dirs/weights must be 16-byte aligned");
+  if (mlp->widths[0] > 256) return fail(CTM_EUNSUPPORTED, "D > 256");
+  CallArgs a{OP_DSUM, X, N, nullptr, 0, per_point ? J : 0, per_point ? dirs : nullptr, 0, 0, mlp->widths[0], 0,
+             op_out, f_out, (cudaStream_t)stream};
+  a.K = K;
+  a.J = J;
+  a.dirs = dirs;
+  a.per_point = per_point != 0;
+  a.weights = weights;
+  return run(mlp, a);
+}
+
+ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64_t N, const float* sigma_x, int32_t R,
+                                            float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (R < 1 || !sigma_x) return fail(CTM_EINVAL, "need sigma_x and R >= 1");
+  if (!aligned16(sigma_x)) return fail(CTM_ESHAPE, "sigma_x must be 16-byte aligned");
+  if (mlp->widths[0] > 256) return fail(CTM_EUNSUPPORTED, "D > 256");
+  CallArgs a{OP_WLAP_X, X, N, nullptr, 0, R, sigma_x, 0, 0, mlp->widths[0], 0, op_out, f_out, (cudaStream_t)stream};
+  a.v_trans = 1;
   return run(mlp, a);
 }
 

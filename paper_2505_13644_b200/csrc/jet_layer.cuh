@@ -32,9 +32,10 @@ constexpr int kBTileBytes = (kMaxN / 2) * kBK * 2;  // 8 KB: a CTA of the pair s
 constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
+constexpr int kMaxW = 256;                       // per-direction weights in smem (K=2: R+2 <= 256)
 constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
-                           4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxJets * 4 + 2 * kBM * 4 /*xacc*/;
+                           4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxW * 4 + 2 * kBM * 4 /*xacc*/;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
 constexpr uint32_t kSw64 = 4;                    // descriptor layout code for SWIZZLE_64B
 // Epilogue modes (template parameter KORD): 2 = K=2 collapsed, 4 = K=4 collapsed (weighted
@@ -59,8 +60,9 @@ struct LayerParams {
   int pts_per_tile;
   int n_mma;              // MMA N, multiple of 16, <= 256
   int k_iters;            // Kpad / kBK
-  const float* jet_w;     // K=4: weights of the J jets in the collapsed slot
-  int J;                  // K=4: jets; kNest: D
+  const float* jet_w;     // K=4: weights of the J jets in the collapsed slot; K=2 if weighted
+  int J;                  // K=4: jets; kNest: D; K=2 weighted: directions
+  int weighted;           // K=2: collapse sum_r w_r z_{1,r}^2 (directional sums, Eq. 5 with weights)
   int readout;            // last hidden layer: reduce against w_out instead of storing
   const float* w_out;     // [Mpad] output-layer weights (zero padded)
   float* partial;         // [n_points, m_tiles, 2]
@@ -115,12 +117,16 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   //      standard-mode pairs (z1_r, z2_r) with no collapse
   float acc = 0.f;            // the collapsed sum over directions (standard: sum_r h2_r at readout)
   float z1 = 0.f, z2 = 0.f;   // K=4 jet state
-  int which = 0, jj = (KORD == 4) ? (mb - 1) / 3 : 0;
+  int which = 0, jj = (KORD == 4) ? (mb - 1) / 3 : mb - 1;
+  const bool wsum = (KORD == 2) && p.weighted;
   auto middle = [&](float z) {
     float h;
     if (KORD == 2) {
       h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
-      acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
+      if (wsum)
+        acc = fmaf(jw[jj++] * z, z, acc);  // sum_r w_r z_{1,r}^2
+      else
+        acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
     } else if (KORD == kStd2) {
       if (which == 0) {
         z1 = z;
@@ -411,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
   float* red = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [4][kMaxPtsPerTile][2]
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
-  float* xacc = jw + kMaxJets;                                                 // [2][128] split-point partials
+  float* xacc = jw + kMaxW;                                                 // [2][128] split-point partials
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -439,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
-  if (KORD == 4)
+  if (KORD == 4 || p.weighted)
     for (int j = threadIdx.x; j < p.J; j += blockDim.x) jw[j] = p.jet_w[j];
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barrier inits and TMEM allocation visible to the pair

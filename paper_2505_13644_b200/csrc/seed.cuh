@@ -178,6 +178,7 @@ struct SeedStochParams {
   int ld;
   int S;
   const float* V;        // [N, S, D] or nullptr => generated standard normal
+  const float* w;        // [S] weights of the collapsed sum, or nullptr (all 1)
   uint64_t seed;
   int64_t point_offset;
   uint16_t* out_hi;      // [N*(3S+2), ld]
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
       h1[i] = d1[i] * z[i];
       h2[i] = d2[i] * z2;
       h3[i] = d3[i] * z2 * z[i];
-      acc[i] = fmaf(z2, z2, acc[i]);
+      acc[i] = fmaf(p.w ? p.w[s] * z2 : z2, z2, acc[i]);
     }
     const size_t r = row0 + 1 + 3 * (size_t)s;
     seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
@@ -263,7 +264,8 @@ struct SeedRandomParams {
   int ldk;               // padded row length (multiple of 32)
   int S;
   int Rv;
-  const float* V;        // [N, S, Rv] or nullptr => Rademacher(seed, point_offset + n)
+  const float* V;        // [N, S, Rv] (or [N, Rv, S] if v_trans) or nullptr => generated
+  int v_trans;           // V stored [N, Rv, S]: sigma(x_n) [D, R] per point
   const float* sigma;    // [D, Rv] or nullptr (then Rv == D)
   uint64_t seed;
   int64_t point_offset;
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
       const int s = s0 + e / p.Rv, r = e % p.Rv;
       float v;
       if (p.V) {
-        v = p.V[((size_t)n * p.S + s) * p.Rv + r];
+        v = p.v_trans ? p.V[((size_t)n * p.Rv + r) * p.S + s] : p.V[((size_t)n * p.S + s) * p.Rv + r];
       } else {
         const uint64_t idx =
             ((uint64_t)(p.point_offset + n) * (uint64_t)p.S + (uint64_t)s) * (uint64_t)p.Rv + (uint64_t)r;

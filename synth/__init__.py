@@ -72,3 +72,19 @@ def sylvester_hadamard(order: int) -> np.ndarray:
         H = np.block([[H, H], [H, -H]])
     assert H.shape[0] == order
     return H
+
+
+def sigma_field(X: np.ndarray, R: int, seed: int = 4) -> np.ndarray:
+    """A smooth point-dependent weighting sigma(x) [N, D, R] ("sigma can depend on
+    x0"): sigma(x)[d, r] = A[d, r] (1 + 0.5 sin(x_d + phi_r)), A Gaussian / sqrt(R)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    N, D = X.shape
+    A = rng.standard_normal((D, R)) / np.sqrt(R)
+    phi = rng.uniform(-np.pi, np.pi, size=R)
+    return (A[None] * (1.0 + 0.5 * np.sin(X.astype(np.float64)[:, :, None] + phi[None, None, :]))).astype(np.float32)
+
+
+def signed_weights(J: int, seed: int = 5) -> np.ndarray:
+    """Direction weights for general directional sums: U(-1, 1), both signs."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.uniform(-1.0, 1.0, size=J).astype(np.float32)

@@ -13,7 +13,8 @@ import torch
 
 import oracle as O
 from tests._util import magnitude_k2
-from synth import gaussian_directions, mlp_params, points, sigma as make_sigma, widths_for
+from synth import (gaussian_directions, mlp_params, points, sigma as make_sigma, sigma_field, signed_weights,
+                   widths_for)
 
 pytestmark = pytest.mark.gpu
 
@@ -214,6 +215,73 @@ def test_biharmonic_parity(ctm, widths, N):
     op, f = mlp.biharmonic(torch.from_numpy(X).cuda())
     want, fwant, norm = O.biharmonic(onet, X.astype(np.float64), O.O1)
     check(op, want, norm, f, fwant)
+
+
+# ------------------------------------------------------------------ sigma(x) and general directional sums (NEXT-4)
+@pytest.mark.parametrize("widths,N,R", [([6, 32, 32, 1], 9, 3), (C1_WIDTHS, 37, 50)])
+def test_weighted_laplacian_pointwise_parity(ctm, widths, N, R):
+    """Eq. 10 with sigma depending on x: sigma_x [N, D, R] per point."""
+    params, onet = nets(widths)
+    X = points(N, widths[0])
+    sx = sigma_field(X, R)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.weighted_laplacian_pointwise(torch.from_numpy(X).cuda(), torch.from_numpy(sx).cuda())
+    want, fwant, norm = O.weighted_laplacian_pointwise(onet, X.astype(np.float64), sx.astype(np.float64))
+    check(op, want, norm, f, fwant)
+
+
+def test_weighted_laplacian_pointwise_constant_sigma_matches_weighted(ctm):
+    params, onet = nets([8, 64, 48, 1])
+    X = points(21, 8)
+    sig = make_sigma(8, 5, kind="rect")
+    mlp = gpu_mlp(ctm, params)
+    Xc = torch.from_numpy(X).cuda()
+    a = mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(np.broadcast_to(sig, (21, 8, 5)).copy()).cuda())[0]
+    b = mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0]
+    _, _, norm = O.weighted_laplacian(onet, X.astype(np.float64), sig.astype(np.float64))
+    check(a, b.double().cpu().numpy(), norm, tol=2 * TOL)
+
+
+@pytest.mark.parametrize("K", [2, 4])
+@pytest.mark.parametrize("per_point", [False, True])
+@pytest.mark.parametrize("widths,N,J", [([4, 48, 40, 1], 11, 6), (C4_WIDTHS, 19, 12)])
+def test_directional_sum_parity(ctm, K, per_point, widths, N, J):
+    """sum_j w_j <d^K f, u_j^K> with signed weights (Eq. 5 with coefficients)."""
+    params, onet = nets(widths)
+    D = widths[0]
+    X = points(N, D)
+    dirs = gaussian_directions(N, J, D, seed=6) if per_point else gaussian_directions(1, J, D, seed=6)[0]
+    w = signed_weights(J)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.directional_sum(torch.from_numpy(X).cuda(), K, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())
+    want, fwant, norm = O.directional_sum(onet, X.astype(np.float64), K, dirs.astype(np.float64), w.astype(np.float64))
+    check(op, want, norm, f, fwant)
+    P = (J if K == 2 else 3 * J) + 2
+    assert mlp.last_plan()["slots_per_point"] == P
+
+
+def test_directional_sum_eq15_family_mixed_partial(ctm):
+    """A user-supplied interpolation family (Eq. 15, I = 2, i = (3, 1)): directions
+    j_1 e_1 + j_2 e_2 for |j| = 4 with weights gamma_{i,j}/4! give d_1^3 d_2 f."""
+    params, onet = nets([2, 64, 48, 1])
+    X = points(17, 2)
+    fam = [(j1, 4 - j1) for j1 in range(5)]
+    dirs = np.array(fam, dtype=np.float32)
+    w = np.array([float(O.gamma((3, 1), j)) / 24.0 for j in fam], dtype=np.float32)
+    mlp = gpu_mlp(ctm, params)
+    op, _ = mlp.directional_sum(torch.from_numpy(X).cuda(), 4, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())
+    want, _, norm = O.directional_sum(onet, X.astype(np.float64), 4, dirs.astype(np.float64), w.astype(np.float64))
+    check(op, want, norm)
+
+
+def test_directional_sum_errors(ctm):
+    params, _ = nets([4, 16, 1])
+    mlp = gpu_mlp(ctm, params)
+    X = torch.zeros(3, 4).cuda()
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        mlp.directional_sum(X, 3, torch.ones(2, 4), torch.ones(2))
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        mlp.directional_sum(X, 4, torch.ones(85, 4), torch.ones(85))  # 3J + 2 > 256
 
 
 # ------------------------------------------------------------------ nested-Laplacian biharmonic (NEXT-2)
