@@ -109,6 +109,14 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, in
 ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                           void *stream);
 
+/* Hidden-layer activation of a loaded MLP (default CTM_ACT_TANH, the paper's).
+ * Every operator applies the Taylor rules of the selected s with its derivatives
+ * s', s'', s''', s'''' (sin: cos, -sin, -cos, sin; square z^2: 2z, 2, 0, 0; identity:
+ * 1, 0, 0, 0). Host-side setting, takes effect for the next call. CTM_EINVAL for an
+ * unknown code or a NULL handle. */
+typedef enum { CTM_ACT_TANH = 0, CTM_ACT_IDENTITY = 1, CTM_ACT_SQUARE = 2, CTM_ACT_SIN = 3 } ctm_activation;
+ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
+
 /* Weighted Laplacian with a point-dependent sigma (Eq. 10; "sigma can depend on x0",
  * P:686): op[n] = <d^2 f(x_n), sigma(x_n) sigma(x_n)^T> = sum_r <d^2 f(x_n), s_r(x_n)^2>.
  *   sigma_x [N, D, R] device, fp32: sigma(x_n) row-major [D, R] for each point (the

@@ -37,6 +37,7 @@ ABI = {
     "ctm_directional_sum": (ctypes.c_int, [_VP, _VP, _I64, _I32, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
                                                  _VP]),
+    "ctm_set_activation": (ctypes.c_int, [_VP, ctypes.c_int]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "ctm_last_error": (ctypes.c_char_p, []),
     "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
@@ -90,14 +91,18 @@ def _dev_f32(t: torch.Tensor, device, name: str) -> torch.Tensor:
     return t
 
 
+ACTIVATIONS = {"tanh": 0, "identity": 1, "square": 2, "sin": 3}  # ctm_activation
+
+
 class MLP:
-    """A tanh MLP f: R^D -> R loaded into libctm (weights copied to the device).
+    """An MLP f: R^D -> R loaded into libctm (weights copied to the device).
 
     params: sequence of (W_l [w_l, w_{l-1}], b_l [w_l]) as in ``torch.nn.Linear``;
-    tanh after every layer but the last.
+    the activation (tanh by default; or sin, identity, square) after every layer
+    but the last.
     """
 
-    def __init__(self, params: Sequence, device: int | str | torch.device | None = None):
+    def __init__(self, params: Sequence, device: int | str | torch.device | None = None, act: str = "tanh"):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
@@ -114,6 +119,10 @@ class MLP:
             lib().ctm_load_mlp(len(Ws), w_arr, W_arr, b_arr, self.device.index, ctypes.byref(h)), "ctm_load_mlp"
         )
         self._h = h
+        if act not in ACTIVATIONS:
+            raise CTMError(f"unknown activation {act!r}")
+        _check(lib().ctm_set_activation(self._h, ACTIVATIONS[act]), "ctm_set_activation")
+        self.act = act
 
     # ------------------------------------------------------------------ helpers
     def _io(self, X, out, f_out, want_f):

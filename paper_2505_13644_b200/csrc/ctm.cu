@@ -87,6 +87,7 @@ struct DeviceGuard {
 
 struct ctm_mlp {
   int device = 0;
+  int act = ctm::kActTanh;    // hidden-layer activation (ctm_set_activation)
   int sm_count = 148;
   int L = 0;                  // affine layers
   std::vector<int> widths;    // L + 1
@@ -347,6 +348,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
     bp.point_offset = a.point_offset + p0;
     bp.out_hi = buf[0];
     bp.out_lo = buf[1];
+    bp.act = h->act;
     ctm::seed_stoch_biharmonic_kernel<<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
   } else {
     ctm::SeedParams sp{};
@@ -362,6 +364,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
     sp.R = R;
     sp.out_hi = buf[0];
     sp.out_lo = buf[1];
+    sp.act = h->act;
     if (KORD == 2)
       ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
     else if (KORD == 4)
@@ -406,6 +409,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
     ctm::LayerParams lp{};
     lp.bias = gl.bias;
+    lp.act = h->act;
     lp.out_hi = h->blk[dst][0];
     lp.out_lo = h->blk[dst][1];
     lp.ldo = gl.mpad;
@@ -862,6 +866,18 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64
   CallArgs a{OP_WLAP_X, X, N, nullptr, 0, R, sigma_x, 0, 0, mlp->widths[0], 0, op_out, f_out, (cudaStream_t)stream};
   a.v_trans = 1;
   return run(mlp, a);
+}
+
+ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (act != CTM_ACT_TANH && act != CTM_ACT_IDENTITY && act != CTM_ACT_SQUARE && act != CTM_ACT_SIN)
+    return fail(CTM_EINVAL, "unknown activation");
+  static_assert(CTM_ACT_TANH == ctm::kActTanh && CTM_ACT_IDENTITY == ctm::kActIdentity &&
+                    CTM_ACT_SQUARE == ctm::kActSquare && CTM_ACT_SIN == ctm::kActSin,
+                "ABI activation codes");
+  mlp->act = (int)act;
+  return CTM_OK;
 }
 
 ctm_status ctm_profile_enable(ctm_mlp_t mlp, int32_t enable) {

@@ -49,6 +49,35 @@ constexpr int kStd2 = 3;
 constexpr int kNest = 5;
 constexpr int kNestMaxD = 20;
 
+// Hidden-layer activation s and its derivatives s', s'', s''', s'''' at z (the Taylor
+// rules only ever need these five numbers). tanh is the paper's; sin, identity
+// and square extend the path and turn closed forms into GPU tests.
+enum : int { kActTanh = 0, kActIdentity = 1, kActSquare = 2, kActSin = 3 };
+struct ActD {
+  float d0, d1, d2, d3, d4;
+};
+__device__ __forceinline__ ActD act_derivs(int act, float z) {
+  ActD r;
+  if (act == kActTanh) {
+    const float t = tanhf(z);
+    const float s = 1.f - t * t;          // tanh'
+    r.d0 = t;
+    r.d1 = s;
+    r.d2 = -2.f * t * s;                  // tanh''
+    r.d3 = s * (6.f * t * t - 2.f);       // tanh'''
+    r.d4 = 8.f * t * s * (2.f - 3.f * t * t);  // tanh''''
+  } else if (act == kActSin) {
+    float sn, cs;
+    sincosf(z, &sn, &cs);
+    r.d0 = sn; r.d1 = cs; r.d2 = -sn; r.d3 = -cs; r.d4 = sn;
+  } else if (act == kActSquare) {
+    r.d0 = z * z; r.d1 = 2.f * z; r.d2 = 2.f; r.d3 = 0.f; r.d4 = 0.f;
+  } else {
+    r.d0 = z; r.d1 = 1.f; r.d2 = 0.f; r.d3 = 0.f; r.d4 = 0.f;
+  }
+  return r;
+}
+
 struct LayerParams {
   const float* bias;      // [Mpad]
   uint16_t* out_hi;       // [rows, ldo] bf16 pair
@@ -63,6 +92,7 @@ struct LayerParams {
   const float* jet_w;     // K=4: weights of the J jets in the collapsed slot; K=2 if weighted
   int J;                  // K=4: jets; kNest: D; K=2 weighted: directions
   int weighted;           // K=2: collapse sum_r w_r z_{1,r}^2 (directional sums, Eq. 5 with weights)
+  int act;                // kAct*
   int readout;            // last hidden layer: reduce against w_out instead of storing
   const float* w_out;     // [Mpad] output-layer weights (zero padded)
   float* partial;         // [n_points, m_tiles, 2]
@@ -100,14 +130,8 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   // ---- slot 0: the primal; the bias enters here only (affine rule)
   const float z0 = ptx::tmem_ld1(tcol) + bias;
   ptx::tmem_ld_wait();
-  const float t = tanhf(z0);
-  const float d1 = 1.f - t * t;   // tanh'
-  const float d2 = -2.f * t * d1;  // tanh''
-  float d3 = 0.f, d4 = 0.f;
-  if (KORD == 4) {
-    d3 = d1 * (6.f * t * t - 2.f);            // tanh'''
-    d4 = 8.f * t * d1 * (2.f - 3.f * t * t);  // tanh''''
-  }
+  const ActD A = act_derivs(p.act, z0);
+  const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   fpart = (part == 2) ? 0.f : wo * t;
   opart = 0.f;
   if (!p.readout && part != 2) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
@@ -216,11 +240,8 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a) g[a] = (a < D) ? ptx::tmem_ld1(tcol + 1u + (uint32_t)a) : 0.f;
   ptx::tmem_ld_wait();
-  const float t = tanhf(z0);
-  const float d1 = 1.f - t * t;
-  const float d2 = -2.f * t * d1;
-  const float d3 = d1 * (6.f * t * t - 2.f);
-  const float d4 = 8.f * t * d1 * (2.f - 3.f * t * t);
+  const ActD A = act_derivs(p.act, z0);
+  const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   const bool store = !p.readout;
   fpart = wo * t;
   if (store) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
@@ -299,11 +320,8 @@ __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t
   ptx::tmem_ld_cols<P>(tcol, v);
   ptx::tmem_ld_wait();
   const int ld = p.ldo;
-  const float t = tanhf(v[0] + bias);
-  const float d1 = 1.f - t * t;
-  const float d2 = -2.f * t * d1;
-  const float d3 = d1 * (6.f * t * t - 2.f);
-  const float d4 = 8.f * t * d1 * (2.f - 3.f * t * t);
+  const ActD A = act_derivs(p.act, v[0] + bias);
+  const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   const float* g = v + 1;
   float gg = 0.f, trH = 0.f, HF = 0.f, gL = 0.f, gHg = 0.f;
   float hg[D];

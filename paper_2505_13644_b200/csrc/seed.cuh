@@ -40,6 +40,7 @@ struct SeedParams {
   int R;                 // K=2: number of directions; K=4: number of jets J
   uint16_t* out_hi;      // [N*P, ld] bf16 pair
   uint16_t* out_lo;
+  int act;               // kAct*
 };
 
 // four adjacent features -> one 8-byte store into each of the hi and lo planes
@@ -76,14 +77,12 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
     z0.z = fmaf(w.z, xs[d], z0.z);
     z0.w = fmaf(w.w, xs[d], z0.w);
   }
-  float t[4] = {tanhf(z0.x), tanhf(z0.y), tanhf(z0.z), tanhf(z0.w)};
-  float d1[4], d2[4], d3[4], d4[4];
+  const float zz[4] = {z0.x, z0.y, z0.z, z0.w};
+  float t[4], d1[4], d2[4], d3[4], d4[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    d1[i] = 1.f - t[i] * t[i];    // tanh'
-    d2[i] = -2.f * t[i] * d1[i];  // tanh''
-    d3[i] = d1[i] * (6.f * t[i] * t[i] - 2.f);            // tanh'''
-    d4[i] = 8.f * t[i] * d1[i] * (2.f - 3.f * t[i] * t[i]);  // tanh''''
+    const ActD A = act_derivs(p.act, zz[i]);  // s, s', s'', s''', s''''
+    t[i] = A.d0; d1[i] = A.d1; d2[i] = A.d2; d3[i] = A.d3; d4[i] = A.d4;
   }
   seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
   const float4 cs = __ldg(reinterpret_cast<const float4*>(p.csum + m));
@@ -183,6 +182,7 @@ struct SeedStochParams {
   int64_t point_offset;
   uint16_t* out_hi;      // [N*(3S+2), ld]
   uint16_t* out_lo;
+  int act;
 };
 
 __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx);
@@ -215,14 +215,12 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
     z0.z = fmaf(w.z, xs[d], z0.z);
     z0.w = fmaf(w.w, xs[d], z0.w);
   }
-  const float t[4] = {tanhf(z0.x), tanhf(z0.y), tanhf(z0.z), tanhf(z0.w)};
-  float d1[4], d2[4], d3[4], d4[4], acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const float zz[4] = {z0.x, z0.y, z0.z, z0.w};
+  float t[4], d1[4], d2[4], d3[4], d4[4], acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    d1[i] = 1.f - t[i] * t[i];
-    d2[i] = -2.f * t[i] * d1[i];
-    d3[i] = d1[i] * (6.f * t[i] * t[i] - 2.f);
-    d4[i] = 8.f * t[i] * d1[i] * (2.f - 3.f * t[i] * t[i]);
+    const ActD A = act_derivs(p.act, zz[i]);
+    t[i] = A.d0; d1[i] = A.d1; d2[i] = A.d2; d3[i] = A.d3; d4[i] = A.d4;
   }
   seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
   for (int s = 0; s < p.S; ++s) {

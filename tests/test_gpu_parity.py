@@ -284,6 +284,64 @@ def test_directional_sum_errors(ctm):
         mlp.directional_sum(X, 4, torch.ones(85, 4), torch.ones(85))  # 3J + 2 > 256
 
 
+# ------------------------------------------------------------------ other activations (NEXT-4)
+def test_square_net_closed_forms_on_gpu(ctm):
+    """square(1^T square(x)) = ||x||^4 (oracle test fixture, now through the GPU):
+    Laplacian 4(D+2)||x||^2, biharmonic 8D(D+2) by both routes, <d^4 f, u^4> = 24|u|^4."""
+    D = 5
+    params = [(np.eye(D, dtype=np.float32), np.zeros(D, np.float32)), (np.ones((1, D), np.float32), np.zeros(1, np.float32)),
+              (np.ones((1, 1), np.float32), np.zeros(1, np.float32))]
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act="square")
+    X = points(23, D)
+    Xc = torch.from_numpy(X).cuda()
+    r2 = np.sum(X.astype(np.float64) ** 2, 1)
+    op, f = mlp.laplacian(Xc)
+    np.testing.assert_allclose(op.double().cpu().numpy(), 4 * (D + 2) * r2, rtol=2e-5)
+    np.testing.assert_allclose(f.double().cpu().numpy(), r2**2, rtol=2e-5)
+    np.testing.assert_allclose(mlp.laplacian_standard(Xc)[0].double().cpu().numpy(), 4 * (D + 2) * r2, rtol=2e-5)
+    for got in (mlp.biharmonic(Xc)[0], mlp.biharmonic_nested(Xc)[0]):
+        np.testing.assert_allclose(got.double().cpu().numpy(), 8 * D * (D + 2), rtol=2e-5)
+    dirs = gaussian_directions(1, 4, D, seed=9)[0]
+    w = signed_weights(4)
+    got = mlp.directional_sum(Xc, 4, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())[0]
+    want = 24 * np.sum(w.astype(np.float64) * np.sum(dirs.astype(np.float64) ** 2, 1) ** 2)
+    np.testing.assert_allclose(got.double().cpu().numpy(), want, rtol=2e-5, atol=1e-5 * abs(want))
+
+
+@pytest.mark.parametrize("widths,N", [([5, 40, 32, 1], 13), (C1_WIDTHS, 9)])
+def test_sin_activation_parity_all_operators(ctm, widths, N):
+    params, _ = nets(widths)
+    onet = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params], "sin")
+    D = widths[0]
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act="sin")
+    want, fw, norm = O.laplacian(onet, Xd)
+    op, f = mlp.laplacian(Xc)
+    check(op, want, norm, f, fw)
+    sig = make_sigma(D, 3, kind="rect")
+    want, _, norm = O.weighted_laplacian(onet, Xd, sig.astype(np.float64))
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
+    V = O.rademacher(4, 0, N, 5, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    check(mlp.randomized_laplacian(Xc, S=5, seed=4)[0], want, norm)
+    if D <= 7:
+        want, _, norm = O.biharmonic(onet, Xd)
+        check(mlp.biharmonic(Xc)[0], want, norm)
+        check(mlp.biharmonic_nested(Xc)[0], want, norm)
+
+
+def test_identity_activation_gives_zero_operators(ctm):
+    params, _ = nets([4, 32, 24, 1])
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act="identity")
+    Xc = torch.from_numpy(points(7, 4)).cuda()
+    for op in (mlp.laplacian(Xc)[0], mlp.biharmonic(Xc)[0], mlp.biharmonic_nested(Xc)[0]):
+        assert torch.all(op == 0)
+    with pytest.raises(ctm.CTMError):
+        ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act="relu")
+
+
 # ------------------------------------------------------------------ nested-Laplacian biharmonic (NEXT-2)
 @pytest.mark.parametrize("widths,N", [
     ([1, 40, 24, 1], 13),           # D = 1: P = 5, the K=4 Faa di Bruno row
