@@ -163,6 +163,31 @@ ctm_status ctm_stochastic_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, i
                                      ctm_dist dist, uint64_t seed, int64_t point_offset, float *op_out,
                                      float *f_out, void *stream);
 
+/* ---- Differentiable path (PINN training) ----------------
+ * ctm_grad_enable(mlp, 1) makes every later K=2 operator call on this handle
+ * (ctm_laplacian, ctm_weighted_laplacian, ctm_randomized_laplacian,
+ * ctm_weighted_laplacian_pointwise, ctm_directional_sum with K = 2) record a tape of
+ * what its adjoint needs, in library-owned device memory: the layer-1 input block and
+ * every hidden layer's output block (bf16 pairs) and pre-activations (fp32), about
+ * 8 * N * P * sum_l w_l bytes (C1, N = 16384: ~20 GB). Other operators clear the tape.
+ * ctm_grad_enable(mlp, 0) stops recording (memory is kept until ctm_free_mlp).
+ * Errors: CTM_EINVAL (NULL), CTM_ECUDA / CTM_ENOMEM (setup). */
+ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable);
+
+/* Gradients of  L = sum_n gop[n] * op[n] + gf[n] * f[n]  with respect to every weight and
+ * bias, for the LAST recorded call (its X, directions and N):
+ *   gop [N] device (required), gf [N] device or NULL (= 0);
+ *   dW, db: HOST arrays of L device pointers, dW[l] [w_{l+1}, w_l] row-major (nn.Linear
+ *   layout, as passed to ctm_load_mlp), db[l] [w_{l+1}]; fp32, caller-owned;
+ *   accumulate != 0 adds into dW/db, else overwrites.
+ * The adjoint runs the transposed Taylor rules layer by layer (jet_layer_kernel<kBwd2>:
+ * tcgen05 GEMM with A = W^T fused with the transposed rule) and dW_l = Z_bar_l^T B_{l-1}
+ * as 3xBF16 GEMMs; deterministic. Asynchronous on `stream` (order it after the forward).
+ * Errors: CTM_EUNSUPPORTED (no recorded differentiable call), CTM_EINVAL (NULL
+ * pointers), CTM_ESHAPE (misaligned gop/gf), CTM_ECUDA. */
+ctm_status ctm_backward(ctm_mlp_t mlp, const float *gop, const float *gf, float *const *dW, float *const *db,
+                        int32_t accumulate, void *stream);
+
 /* Static message for a status. */
 const char *ctm_status_str(ctm_status s);
 

@@ -38,6 +38,8 @@ ABI = {
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
                                                  _VP]),
     "ctm_set_activation": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "ctm_grad_enable": (ctypes.c_int, [_VP, _I32]),
+    "ctm_backward": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "ctm_last_error": (ctypes.c_char_p, []),
     "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
@@ -241,6 +243,28 @@ class MLP:
                                                self._p(f_out), _stream_ptr(stream, self.device)),
                "ctm_stochastic_biharmonic")
         return out, f_out
+
+    # ------------------------------------------------------------------ differentiable path
+    def grad_enable(self, enable: bool = True):
+        """Record a tape on later K=2 operator calls so that ``backward`` can run (NEXT-3)."""
+        _check(lib().ctm_grad_enable(self._h, int(bool(enable))), "ctm_grad_enable")
+
+    def backward(self, gop, gf=None, grads=None, accumulate=False, stream=None):
+        """Gradients of sum_n gop[n] op[n] + gf[n] f[n] for the last recorded call.
+
+        Returns [(dW_l, db_l)] in nn.Linear layout (fp32, on the device); pass ``grads``
+        (same structure) to write into existing tensors, with ``accumulate`` to add."""
+        gop = _dev_f32(gop, self.device, "gop").reshape(-1)
+        gf = None if gf is None else _dev_f32(gf, self.device, "gf").reshape(-1)
+        if grads is None:
+            grads = [(torch.empty(self.widths[l + 1], self.widths[l], device=self.device),
+                      torch.empty(self.widths[l + 1], device=self.device)) for l in range(len(self.widths) - 1)]
+        L = len(grads)
+        dW = (_VP * L)(*[g[0].data_ptr() for g in grads])
+        db = (_VP * L)(*[g[1].data_ptr() for g in grads])
+        _check(lib().ctm_backward(self._h, gop.data_ptr(), self._p(gf), dW, db, int(bool(accumulate)),
+                                  _stream_ptr(stream, self.device)), "ctm_backward")
+        return grads
 
     def last_plan(self) -> dict:
         a, b, c, d = _I32(), _I32(), _I32(), _I32()

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libctm.so")
 SOURCES = ["ctm.cu"]
-HEADERS = ["ptx.cuh", "jet_layer.cuh", "seed.cuh"]
+HEADERS = ["ptx.cuh", "jet_layer.cuh", "seed.cuh", "backward.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -19,6 +19,7 @@ FLAGS = [
     "-Xptxas", "-v",
     f"-I{os.path.join(ROOT, 'include')}",
 ]
+LIBS = ["-lcublas"]  # the weight-gradient GEMMs of the differentiable path (plain long-K GEMMs)
 
 
 def stale() -> bool:
@@ -33,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+    cmd = [NVCC, *FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1,0 +1,131 @@
+// backward.cuh — the differentiable path: the adjoint of the collapsed
+// K=2 forward for PINN training, L = sum_n gop[n] op[n] + gf[n] f[n].
+//
+//   top_bwd_kernel     readout + last hidden rule, transposed: Z_bar_{L-1} (bf16 pairs),
+//                      per-group partials of dW_L (f = w_L . h0 + b_L, op = c w_L . top)
+//   colsum_kernel      deterministic two-stage column sums (db_l from the slot-0 rows of
+//                      Z_bar_l, dW_L, db_L): group partials, then reduce_groups_kernel
+//   crop_kernel        padded fp32 [rows, ld] -> caller's [rows, cols] (= or +=)
+//
+// The hidden layers' adjoints run in jet_layer_kernel<kBwd2> (jet_layer.cuh) and the
+// weight gradients dW_l = Z_bar_l^T B_{l-1} are plain long-K GEMMs (ctm.cu).
+#pragma once
+#include <cstdint>
+
+#include "jet_layer.cuh"
+
+namespace ctm {
+
+struct TopBwdParams {
+  const float* Z;       // [N*P, ldz] pre-activations of the last hidden layer
+  int ldz;
+  int P;
+  int64_t N;
+  int width;            // padded width (threads cover [0, width))
+  const float* w_out;   // [width]
+  float c;              // op scale (1, or 1/S)
+  const float* gop;     // [N]
+  const float* gf;      // [N] or nullptr
+  const float* jw;      // K=2 weights [P-2] or nullptr
+  int act;
+  uint16_t* out_hi;     // Z_bar [N*P, ldo]
+  uint16_t* out_lo;
+  int ldo;
+  float* dw_part;       // [G, width] partials of dW_L
+  int G;
+};
+
+// grid (width / 128, G); a thread owns one feature and the points n = g, g + G, ...
+__global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.y;
+  if (m >= p.width) return;
+  const float wl = p.w_out[m];
+  const size_t ldz = (size_t)p.ldz, ldo = (size_t)p.ldo;
+  float dwp = 0.f;
+  for (int64_t n = g; n < p.N; n += p.G) {
+    const size_t row = (size_t)n * p.P;
+    const float* zr = p.Z + row * ldz + m;
+    const float z0 = zr[0], zt = zr[(size_t)(p.P - 1) * ldz];
+    const ActD A = act_derivs(p.act, z0);
+    const float go = p.gop[n], gfn = p.gf ? p.gf[n] : 0.f;
+    const float tb = p.c * go * wl;  // adjoint of the collapsed top h_top
+    const float hb0 = gfn * wl;      // adjoint of h0
+    float szz = 0.f;
+    for (int r = 0; r < p.P - 2; ++r) {
+      const float z1 = zr[(size_t)(1 + r) * ldz];
+      const float w = p.jw ? p.jw[r] : 1.f;
+      szz = fmaf(w * z1, z1, szz);
+      store_pair(p.out_hi, p.out_lo, (row + 1 + r) * ldo + m, 2.f * A.d2 * w * z1 * tb);
+    }
+    store_pair(p.out_hi, p.out_lo, (row + p.P - 1) * ldo + m, A.d1 * tb);
+    store_pair(p.out_hi, p.out_lo, row * ldo + m, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb);
+    const float top = A.d1 * zt + A.d2 * szz;
+    dwp += gfn * A.d0 + p.c * go * top;
+  }
+  p.dw_part[(size_t)g * p.width + m] = dwp;
+}
+
+// part[g, m] = sum over rows r = g, g + G, ... < nrows of src[row0 + r * stride, m]
+// (bf16 pair if lo != nullptr, else fp32 `srcf`); grid (ceil(ncols / 128), G)
+__global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo,
+                                                     const float* __restrict__ srcf, int64_t nrows, int64_t stride,
+                                                     int ld, int ncols, int G, float* __restrict__ part) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.y;
+  if (m >= ncols) return;
+  float acc = 0.f;
+  for (int64_t r = g; r < nrows; r += G) {
+    const size_t i = (size_t)(r * stride) * ld + m;
+    acc += srcf ? srcf[i] : ptx::bf16_val(hi[i]) + ptx::bf16_val(lo[i]);
+  }
+  part[(size_t)g * ncols + m] = acc;
+}
+
+// out[m] (=|+=) sum_g part[g, m], g = 0..G-1 in order, for m < ncols
+__global__ void reduce_groups_kernel(const float* __restrict__ part, int G, int ncols, float* __restrict__ out,
+                                     int accumulate) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= ncols) return;
+  float s = 0.f;
+  for (int g = 0; g < G; ++g) s += part[(size_t)g * ncols + m];
+  out[m] = accumulate ? out[m] + s : s;
+}
+
+// out[0] (=|+=) sum_n v[n] (one block, fixed order: strided partials then a tree)
+__global__ void __launch_bounds__(256) vector_sum_kernel(const float* __restrict__ v, int64_t N, float* __restrict__ out,
+                                                         int accumulate) {
+  __shared__ float red[256];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = accumulate ? out[0] + red[0] : red[0];
+}
+
+// dst[i, j] (=|+=) src[i * lds + j] for i < rows, j < cols
+__global__ void crop_kernel(const float* __restrict__ src, int lds, int rows, int cols, float* __restrict__ dst,
+                            int accumulate) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (int64_t)rows * cols) return;
+  const int i = (int)(k / cols), j = (int)(k % cols);
+  const float v = src[(size_t)i * lds + j];
+  dst[k] = accumulate ? dst[k] + v : v;
+}
+
+// bf16 pair transpose: out[c, r] = in[r, c] for the [rows, cols] planes (W^T for kBwd2)
+__global__ void transpose_pair_kernel(const uint16_t* __restrict__ in_hi, const uint16_t* __restrict__ in_lo,
+                                      int rows, int cols, uint16_t* __restrict__ out_hi,
+                                      uint16_t* __restrict__ out_lo) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (int64_t)rows * cols) return;
+  const int r = (int)(k / cols), c = (int)(k % cols);
+  out_hi[(size_t)c * rows + r] = in_hi[k];
+  out_lo[(size_t)c * rows + r] = in_lo[k];
+}
+
+}  // namespace ctm

@@ -6,6 +6,7 @@
 //   layer   l = 2..L-1: fused tcgen05 3xTF32 GEMM + tanh Taylor epilogue            -> block B_l
 //           (the last hidden layer reduces straight against the output weights)
 //   final   op = c * (w_L . sum h_K), f = w_L . h0 + b_L
+#include <cublas_v2.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -18,6 +19,7 @@
 #include <vector>
 
 #include "../../include/ctm.h"
+#include "backward.cuh"
 #include "jet_layer.cuh"
 #include "seed.cuh"
 
@@ -126,7 +128,32 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
-  bool smem_attr_set[6] = {false, false, false, false, false, false};
+  bool smem_attr_set[7] = {false, false, false, false, false, false, false};
+  // differentiable path (ctm_grad_enable / ctm_backward)
+  bool grad = false;
+  std::vector<uint16_t*> WThi, WTlo;        // W_l^T bf16 pairs [wpad[l-1], wpad[l]], l = 2..L-1
+  std::vector<CUtensorMap> mapAT_hi, mapAT_lo;
+  float* eye = nullptr;                     // [256, 256] identity: fixed direction sets as shared V
+  cublasHandle_t cublas = nullptr;
+  struct Tape {
+    bool valid = false;
+    int64_t N = 0;
+    int P = 0, ppt = 0, nmma = 0;
+    float scale = 1.f;
+    int weighted = 0, J = 0;
+    float* weights = nullptr;
+    size_t weights_elems = 0;
+    std::vector<uint16_t*> Bhi, Blo;        // B_l, l = 0 .. L-1 (B_0 = layer-1 input block)
+    std::vector<size_t> B_elems;
+    std::vector<float*> Z;                  // Z_l, l = 1 .. L-1 (fp32 pre-activations)
+    std::vector<size_t> Z_elems;
+    uint16_t* Zb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    size_t Zb_elems[2] = {0, 0};
+    float* part = nullptr;
+    size_t part_elems = 0;
+    float* dWpad = nullptr;
+    size_t dWpad_elems = 0;
+  } tape;
   // profiling (events around launches)
   bool profiling = false;
   struct Rec {
@@ -155,6 +182,17 @@ ctm_status free_all(ctm_mlp* h) {
   for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
   F(h->partial);
+  for (auto& p : h->WThi) F(p);
+  for (auto& p : h->WTlo) F(p);
+  F(h->eye);
+  F(h->tape.weights); F(h->tape.part); F(h->tape.dWpad);
+  for (auto& p : h->tape.Bhi) F(p);
+  for (auto& p : h->tape.Blo) F(p);
+  for (auto& p : h->tape.Z) F(p);
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) F(h->tape.Zb[i][j]);
+  if (h->cublas) cublasDestroy(h->cublas);
+  h->cublas = nullptr;
   for (auto& r : h->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -171,6 +209,18 @@ ctm_status ensure(float*& p, size_t& have, size_t need) {
   p = nullptr;
   have = 0;
   CTM_CUDA(cudaMalloc(&p, std::max<size_t>(need, 1) * sizeof(float)));
+  have = need;
+  return CTM_OK;
+}
+
+ctm_status ensure_pair(uint16_t*& hi, uint16_t*& lo, size_t& have, size_t need) {
+  if (need <= have && hi) return CTM_OK;
+  if (hi) cudaFree(hi);
+  if (lo) cudaFree(lo);
+  hi = lo = nullptr;
+  have = 0;
+  CTM_CUDA(cudaMalloc(&hi, std::max<size_t>(need, 1) * sizeof(uint16_t)));
+  CTM_CUDA(cudaMalloc(&lo, std::max<size_t>(need, 1) * sizeof(uint16_t)));
   have = need;
   return CTM_OK;
 }
@@ -324,10 +374,17 @@ struct GemmLayer {
   int kpad, mpad, w_in, w_out;
 };
 
+// grad mode: where a layer writes its output block and its pre-activations
+struct LayerIO {
+  uint16_t* out[2];
+  float* z;
+};
+
 // Layer 1 for fixed direction sets (and the stochastic biharmonic) for points
 // [p0, p0 + n): writes the layer-1 output block into buf.
 ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p0, int64_t n, uint16_t* const* buf,
-                       const float* UT, const float* csum, int R, cudaStream_t st, int& launches) {
+                       const float* UT, const float* csum, int R, cudaStream_t st, int& launches,
+                       float* z_out = nullptr) {
   const int D = h->widths[0], ld1 = h->wpad[1];
   const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
   const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
@@ -365,6 +422,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
     sp.out_hi = buf[0];
     sp.out_lo = buf[1];
     sp.act = h->act;
+    sp.z_out = z_out;
     if (KORD == 2)
       ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
     else if (KORD == 4)
@@ -383,7 +441,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
 // (optional) is recorded on st once the first GEMM (the reader of `in`) is enqueued.
 ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, const std::vector<GemmLayer>& layers,
                          int64_t p0, int64_t n, uint16_t* const* in, float scale, cudaStream_t st,
-                         cudaEvent_t after_first, int& launches) {
+                         cudaEvent_t after_first, int& launches, const std::vector<LayerIO>* io = nullptr) {
   const int P = pl.P;
   const int64_t rows = n * (int64_t)P;
   if (layers.empty()) {  // a single hidden layer: read the layer-1 block
@@ -410,9 +468,11 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     ctm::LayerParams lp{};
     lp.bias = gl.bias;
     lp.act = h->act;
-    lp.out_hi = h->blk[dst][0];
-    lp.out_lo = h->blk[dst][1];
+    lp.out_hi = io ? (*io)[li].out[0] : h->blk[dst][0];
+    lp.out_lo = io ? (*io)[li].out[1] : h->blk[dst][1];
     lp.ldo = gl.mpad;
+    lp.z_out = io ? (*io)[li].z : nullptr;
+    lp.ldz = gl.mpad;
     lp.m_tiles = m_tiles;
     lp.n_points = n;
     lp.P = P;
@@ -468,8 +528,35 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
           h->partial, m_tiles, n, h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr);
       ++launches;
     }
-    src = h->blk[dst];
+    src = io ? (*io)[li].out : h->blk[dst];
     dst ^= 1;
+  }
+  return CTM_OK;
+}
+
+// the K=2 operators have a backward (ctm_backward)
+bool differentiable(const CallArgs& a) {
+  return a.op == OP_LAP || a.op == OP_WLAP || a.op == OP_RLAP || a.op == OP_WLAP_X || (a.op == OP_DSUM && a.K == 2);
+}
+
+// grad mode: per-layer tape buffers for `rows` slot rows
+ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
+  auto& T = h->tape;
+  const int L = h->L;
+  T.Bhi.resize(L, nullptr);
+  T.Blo.resize(L, nullptr);
+  T.B_elems.resize(L, 0);
+  T.Z.resize(L, nullptr);
+  T.Z_elems.resize(L, 0);
+  ctm_status s = ensure_pair(T.Bhi[0], T.Blo[0], T.B_elems[0], (size_t)rows * h->k1pad);
+  if (s != CTM_OK) return s;
+  for (int l = 1; l <= std::max(1, L - 2); ++l) {
+    s = ensure_pair(T.Bhi[l], T.Blo[l], T.B_elems[l], (size_t)rows * h->wpad[l]);
+    if (s != CTM_OK) return s;
+  }
+  for (int l = 1; l <= L - 1; ++l) {
+    s = ensure(T.Z[l], T.Z_elems[l], (size_t)rows * h->wpad[l]);
+    if (s != CTM_OK) return s;
   }
   return CTM_OK;
 }
@@ -509,6 +596,20 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   cudaStream_t st = a.stream;
   int launches = 0;
   ctm_status s;
+  // grad mode: record the tape of this call (differentiable operators only)
+  const bool grad = h->grad && differentiable(a);
+  h->tape.valid = false;
+  std::vector<LayerIO> io;
+  if (grad) {
+    s = prepare_tape(h, a.N * (int64_t)P);
+    if (s != CTM_OK) return s;
+    const int first = random_k2(a) ? 1 : 2;
+    for (int l = first; l <= h->L - 1; ++l)
+      io.push_back({{l < h->L - 1 ? h->tape.Bhi[l] : nullptr, l < h->L - 1 ? h->tape.Blo[l] : nullptr},
+                    h->tape.Z[l]});
+  }
+  uint16_t* const tapeB0[2] = {grad ? h->tape.Bhi[0] : nullptr, grad ? h->tape.Blo[0] : nullptr};
+  uint16_t* const tapeB1[2] = {grad ? h->tape.Bhi[1] : nullptr, grad ? h->tape.Blo[1] : nullptr};
 
   // GEMM layers: layer 1 for per-point K=2 directions, then the hidden layers 2..L-1
   std::vector<GemmLayer> layers;
@@ -534,15 +635,16 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.point_offset = a.point_offset;
     rp.gaussian = a.gaussian;
     rp.v_trans = a.v_trans;
-    rp.out_hi = h->blk[2][0];
-    rp.out_lo = h->blk[2][1];
+    rp.out_hi = grad ? tapeB0[0] : h->blk[2][0];
+    rp.out_lo = grad ? tapeB0[1] : h->blk[2][1];
     {
       ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->k1pad * 4.0, st);
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
     }
     ++launches;
     const float scale = (a.op == OP_RLAP) ? 1.f / (float)a.S : 1.f;  // Eq. 8/10 stochastic: the mean
-    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, h->blk[2], scale, st, nullptr, launches);
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB0 : h->blk[2], scale, st, nullptr, launches,
+                      grad ? &io : nullptr);
     if (s != CTM_OK) return s;
   } else {
     // fixed direction sets (or the K=4 stochastic seed): U and the per-feature constant
@@ -588,13 +690,187 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     // C1): the two compete for the 1 kW budget rather than for SMs.
     s = ensure_workspace(h, a.N * (int64_t)P, 1);
     if (s != CTM_OK) return s;
-    s = launch_seed(h, a, KORD, P, 0, a.N, h->blk[2], UT, csum, R, st, launches);
+    if (grad) {
+      // the layer-1 input block B_0 = [x0; u_r; 0] for dW_1 (directions shared by all points)
+      ctm::SeedRandomParams rp{};
+      rp.X = a.X;
+      rp.D = D;
+      rp.ldk = h->k1pad;
+      rp.v_shared = 1;
+      if (a.op == OP_LAP) {
+        rp.S = D, rp.Rv = D, rp.V = h->eye, rp.ldv = 256;
+      } else if (a.op == OP_WLAP) {
+        rp.S = a.R, rp.Rv = a.R, rp.V = h->eye, rp.ldv = 256, rp.sigma = a.sigma;
+      } else {
+        rp.S = a.J, rp.Rv = D, rp.V = a.dirs, rp.ldv = D;
+      }
+      rp.out_hi = tapeB0[0];
+      rp.out_lo = tapeB0[1];
+      ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
+      ++launches;
+    }
+    s = launch_seed(h, a, KORD, P, 0, a.N, grad ? tapeB1 : h->blk[2], UT, csum, R, st, launches,
+                    grad ? h->tape.Z[1] : nullptr);
     if (s != CTM_OK) return s;
-    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, h->blk[2], scale, st, nullptr, launches);
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB1 : h->blk[2], scale, st, nullptr, launches,
+                      grad ? &io : nullptr);
     if (s != CTM_OK) return s;
+  }
+  if (grad) {
+    auto& T = h->tape;
+    T.N = a.N;
+    T.P = P;
+    T.ppt = pl.ppt;
+    T.nmma = pl.nmma;
+    T.scale = (a.op == OP_RLAP) ? 1.f / (float)a.S : 1.f;
+    T.weighted = (a.op == OP_DSUM);
+    T.J = (a.op == OP_DSUM) ? a.J : 0;
+    if (T.weighted) {  // the caller's weights may not outlive the call
+      s = ensure(T.weights, T.weights_elems, (size_t)a.J);
+      if (s != CTM_OK) return s;
+      CTM_CUDA(cudaMemcpyAsync(T.weights, a.weights, sizeof(float) * a.J, cudaMemcpyDeviceToDevice, st));
+    }
+    T.valid = true;
   }
   CTM_CUDA(cudaGetLastError());
   h->last_launches = launches;
+  return CTM_OK;
+}
+
+// dW_pad[Mout, Kin] = Zb^T B over `rows` slot rows, 3xBF16: hi*hi + lo*hi + hi*lo with fp32
+// accumulation (a plain long-K GEMM: cuBLAS). B [rows, Kin], Zb [rows, Mout], both bf16
+// pairs, row-major (= column-major [K, rows], [M, rows]); the result is column-major
+// [Kin, Mout] = row-major [Mout, Kin].
+ctm_status weight_grad_gemm(ctm_mlp* h, const uint16_t* Bhi, const uint16_t* Blo, int Kin, const uint16_t* Zhi,
+                            const uint16_t* Zlo, int Mout, int64_t rows, float* C, cudaStream_t st) {
+  if (cublasSetStream(h->cublas, st) != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasSetStream");
+  const float one = 1.f, zero = 0.f;
+  const uint16_t* As[3] = {Bhi, Blo, Bhi};
+  const uint16_t* Bs[3] = {Zhi, Zhi, Zlo};
+  for (int i = 0; i < 3; ++i) {
+    cublasStatus_t cs = cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, Kin, Mout, (int)rows, &one, As[i],
+                                     CUDA_R_16BF, Kin, Bs[i], CUDA_R_16BF, Mout, i == 0 ? &zero : &one, C, CUDA_R_32F,
+                                     Kin, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (cs != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasGemmEx failed (" + std::to_string((int)cs) + ")");
+  }
+  return CTM_OK;
+}
+
+// out[m] (=|+=) sum_n Zb[n * P + 0, m] for m < ncols (the bias gradient: bias on slot 0 only)
+ctm_status bias_grad(ctm_mlp* h, const uint16_t* Zhi, const uint16_t* Zlo, int ld, int ncols, float* out, int acc,
+                     cudaStream_t st) {
+  const int G = 128;
+  ctm_status s = ensure(h->tape.part, h->tape.part_elems, (size_t)G * std::max(ncols, 1));
+  if (s != CTM_OK) return s;
+  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Zhi, Zlo, nullptr, h->tape.N, h->tape.P, ld, ncols,
+                                                                   G, h->tape.part);
+  ctm::reduce_groups_kernel<<<(ncols + 127) / 128, 128, 0, st>>>(h->tape.part, G, ncols, out, acc);
+  return CTM_OK;
+}
+
+ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const* dW, float* const* db, int acc,
+                    cudaStream_t st) {
+  auto& T = h->tape;
+  const int L = h->L, P = T.P;
+  const int64_t N = T.N, rows = N * (int64_t)P;
+  int ldmax = 0;
+  for (int l = 1; l <= L - 1; ++l) ldmax = std::max(ldmax, h->wpad[l]);
+  ctm_status s;
+  for (int i = 0; i < 2; ++i) {
+    s = ensure_pair(T.Zb[i][0], T.Zb[i][1], T.Zb_elems[i], (size_t)rows * ldmax);
+    if (s != CTM_OK) return s;
+  }
+  size_t dwmax = (size_t)h->wpad[1] * h->k1pad;
+  for (int l = 2; l <= L - 1; ++l) dwmax = std::max(dwmax, (size_t)h->wpad[l] * h->wpad[l - 1]);
+  s = ensure(T.dWpad, T.dWpad_elems, dwmax);
+  if (s != CTM_OK) return s;
+  const float* jw = T.weighted ? T.weights : nullptr;
+  // ---- readout and the last hidden rule, transposed
+  {
+    const int G = 128, w = h->wpad[L - 1];
+    s = ensure(T.part, T.part_elems, (size_t)G * w);
+    if (s != CTM_OK) return s;
+    ctm::TopBwdParams tp{};
+    tp.Z = T.Z[L - 1];
+    tp.ldz = w;
+    tp.P = P;
+    tp.N = N;
+    tp.width = w;
+    tp.w_out = h->w_out;
+    tp.c = T.scale;
+    tp.gop = gop;
+    tp.gf = gf;
+    tp.jw = jw;
+    tp.act = h->act;
+    tp.out_hi = T.Zb[0][0];
+    tp.out_lo = T.Zb[0][1];
+    tp.ldo = w;
+    tp.dw_part = T.part;
+    tp.G = G;
+    ctm::top_bwd_kernel<<<dim3(w / 128, G), 128, 0, st>>>(tp);
+    ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 127) / 128, 128, 0, st>>>(T.part, G, w, dW[L - 1], acc);
+    if (gf)
+      ctm::vector_sum_kernel<<<1, 256, 0, st>>>(gf, N, db[L - 1], acc);
+    else if (!acc)
+      CTM_CUDA(cudaMemsetAsync(db[L - 1], 0, sizeof(float), st));
+  }
+  // ---- hidden layers L-1 .. 2: weight gradients, then the adjoint of the previous layer
+  int cur = 0;
+  for (int l = L - 1; l >= 2; --l) {
+    const int Mout = h->wpad[l], Kin = h->wpad[l - 1];
+    s = weight_grad_gemm(h, T.Bhi[l - 1], T.Blo[l - 1], Kin, T.Zb[cur][0], T.Zb[cur][1], Mout, rows, T.dWpad, st);
+    if (s != CTM_OK) return s;
+    {
+      const int64_t n = (int64_t)h->widths[l] * h->widths[l - 1];
+      ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, Kin, h->widths[l], h->widths[l - 1],
+                                                                    dW[l - 1], acc);
+    }
+    s = bias_grad(h, T.Zb[cur][0], T.Zb[cur][1], Mout, h->widths[l], db[l - 1], acc, st);
+    if (s != CTM_OK) return s;
+    // Z_bar_{l-1} = rule^T( (Z_bar_l W_l)^T ) on the tensor cores (jet_layer_kernel<kBwd2>)
+    CUtensorMap mb_hi, mb_lo;
+    if (!make_map(&mb_hi, T.Zb[cur][0], (uint64_t)Mout, (uint64_t)rows, (uint32_t)T.nmma / 2) ||
+        !make_map(&mb_lo, T.Zb[cur][1], (uint64_t)Mout, (uint64_t)rows, (uint32_t)T.nmma / 2))
+      return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the adjoint block");
+    ctm::LayerParams lp{};
+    lp.bias = nullptr;
+    lp.act = h->act;
+    lp.out_hi = T.Zb[cur ^ 1][0];
+    lp.out_lo = T.Zb[cur ^ 1][1];
+    lp.ldo = Kin;
+    lp.m_tiles = Kin / ctm::kBM;
+    lp.n_points = N;
+    lp.P = P;
+    lp.pts_per_tile = T.ppt;
+    lp.n_mma = T.nmma;
+    lp.k_iters = Mout / ctm::kBK;
+    lp.jet_w = jw;
+    lp.J = T.J;
+    lp.weighted = T.weighted;
+    lp.z_in = T.Z[l - 1];
+    lp.ldzi = Kin;
+    const int64_t n_tiles = (N + T.ppt - 1) / T.ppt;
+    const int64_t grid = 2 * std::min<int64_t>(n_tiles * (lp.m_tiles / 2), h->sm_count / 2);
+    s = set_layer_attr<ctm::kBwd2>(h);
+    if (s != CTM_OK) return s;
+    {
+      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * N * P * h->widths[l - 1] * h->widths[l], st);
+      ctm::jet_layer_kernel<ctm::kBwd2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
+          h->mapAT_hi[l - 2], h->mapAT_lo[l - 2], mb_hi, mb_lo, lp);
+    }
+    cur ^= 1;
+  }
+  // ---- layer 1: dW_1 = Z_bar_1^T B_0 (B_0 = [x0; u_r; 0]), db_1
+  s = weight_grad_gemm(h, T.Bhi[0], T.Blo[0], h->k1pad, T.Zb[cur][0], T.Zb[cur][1], h->wpad[1], rows, T.dWpad, st);
+  if (s != CTM_OK) return s;
+  {
+    const int64_t n = (int64_t)h->widths[1] * h->widths[0];
+    ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, h->k1pad, h->widths[1], h->widths[0], dW[0],
+                                                                  acc);
+  }
+  s = bias_grad(h, T.Zb[cur][0], T.Zb[cur][1], h->wpad[1], h->widths[1], db[0], acc, st);
+  if (s != CTM_OK) return s;
+  CTM_CUDA(cudaGetLastError());
   return CTM_OK;
 }
 
@@ -878,6 +1154,67 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act) {
                 "ABI activation codes");
   mlp->act = (int)act;
   return CTM_OK;
+}
+
+ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  DeviceGuard g(mlp->device);
+  mlp->tape.valid = false;
+  mlp->grad = enable != 0;
+  if (!mlp->grad || mlp->cublas) return CTM_OK;
+  // W_l^T as bf16 pairs (the A operand of the adjoint GEMMs), from the split weights
+  for (int l = 2; l <= mlp->L - 1; ++l) {
+    const int mpad = mlp->wpad[l], kpad = mlp->wpad[l - 1];
+    uint16_t *thi = nullptr, *tlo = nullptr;
+    CTM_CUDA(cudaMalloc(&thi, sizeof(uint16_t) * (size_t)mpad * kpad));
+    mlp->WThi.push_back(thi);
+    CTM_CUDA(cudaMalloc(&tlo, sizeof(uint16_t) * (size_t)mpad * kpad));
+    mlp->WTlo.push_back(tlo);
+    const int64_t n = (int64_t)mpad * kpad;
+    ctm::transpose_pair_kernel<<<(unsigned)((n + 255) / 256), 256>>>(mlp->Whi[l - 2], mlp->Wlo[l - 2], mpad, kpad, thi,
+                                                                     tlo);
+    CUtensorMap mh, ml;
+    if (!make_map(&mh, thi, mpad, kpad, ctm::kBM) || !make_map(&ml, tlo, mpad, kpad, ctm::kBM))
+      return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W^T");
+    mlp->mapAT_hi.push_back(mh);
+    mlp->mapAT_lo.push_back(ml);
+  }
+  {
+    std::vector<float> eye(256 * 256, 0.f);
+    for (int i = 0; i < 256; ++i) eye[i * 257] = 1.f;
+    CTM_CUDA(cudaMalloc(&mlp->eye, sizeof(float) * eye.size()));
+    CTM_CUDA(cudaMemcpy(mlp->eye, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
+  }
+  if (cublasCreate(&mlp->cublas) != CUBLAS_STATUS_SUCCESS) {
+    mlp->cublas = nullptr;
+    return fail(CTM_ECUDA, "cublasCreate failed");
+  }
+  CTM_CUDA(cudaDeviceSynchronize());
+  return CTM_OK;
+}
+
+ctm_status ctm_backward(ctm_mlp_t mlp, const float* gop, const float* gf, float* const* dW, float* const* db,
+                        int32_t accumulate, void* stream) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (!mlp->grad || !mlp->tape.valid)
+    return fail(CTM_EUNSUPPORTED, "no differentiable call recorded (ctm_grad_enable, then a K=2 operator call)");
+  if (!dW || !db) return fail(CTM_EINVAL, "NULL gradient arrays");
+  for (int l = 0; l < mlp->L; ++l)
+    if (!dW[l] || !db[l]) return fail(CTM_EINVAL, "NULL gradient pointer");
+  if (mlp->tape.N > 0 && !gop) return fail(CTM_EINVAL, "NULL gop");
+  if ((gop && !aligned16(gop)) || (gf && !aligned16(gf))) return fail(CTM_ESHAPE, "gop/gf must be 16-byte aligned");
+  DeviceGuard g(mlp->device);
+  if (mlp->tape.N == 0) {
+    if (!accumulate)
+      for (int l = 0; l < mlp->L; ++l) {
+        CTM_CUDA(cudaMemsetAsync(dW[l], 0, sizeof(float) * mlp->widths[l] * mlp->widths[l + 1], (cudaStream_t)stream));
+        CTM_CUDA(cudaMemsetAsync(db[l], 0, sizeof(float) * mlp->widths[l + 1], (cudaStream_t)stream));
+      }
+    return CTM_OK;
+  }
+  return backward(mlp, gop, gf, dW, db, accumulate != 0, (cudaStream_t)stream);
 }
 
 ctm_status ctm_profile_enable(ctm_mlp_t mlp, int32_t enable) {

@@ -48,6 +48,10 @@ constexpr int kStd2 = 3;
 //  L_a = d_a Lap z (D) | Q = Lap^2 z], P = 2 + 2D + D(D+1)/2 (27 at D = 5, 252 at D = 20).
 constexpr int kNest = 5;
 constexpr int kNestMaxD = 20;
+// kBwd2: the backward of the K=2 collapsed rule (differentiable path): the
+// mainloop computes B_bar^T = W^T Z_bar^T (A = W^T), the epilogue applies the transposed
+// Taylor rule with the saved pre-activations (epilogue_bwd2).
+constexpr int kBwd2 = 6;
 
 // Hidden-layer activation s and its derivatives s', s'', s''', s'''' at z (the Taylor
 // rules only ever need these five numbers). tanh is the paper's; sin, identity
@@ -93,6 +97,10 @@ struct LayerParams {
   int J;                  // K=4: jets; kNest: D; K=2 weighted: directions
   int weighted;           // K=2: collapse sum_r w_r z_{1,r}^2 (directional sums, Eq. 5 with weights)
   int act;                // kAct*
+  float* z_out;           // forward, grad mode: the pre-activations z of every slot (fp32) or nullptr
+  int ldz;
+  const float* z_in;      // kBwd2: this layer's saved pre-activations (fp32)
+  int ldzi;
   int readout;            // last hidden layer: reduce against w_out instead of storing
   const float* w_out;     // [Mpad] output-layer weights (zero padded)
   float* partial;         // [n_points, m_tiles, 2]
@@ -135,6 +143,8 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   fpart = (part == 2) ? 0.f : wo * t;
   opart = 0.f;
   if (!p.readout && part != 2) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
+  float* zp = p.z_out ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
+  if (zp && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
   uint16_t* ph = p.out_hi + (size_t)(row + mb) * ld + m;
   uint16_t* pl = p.out_lo + (size_t)(row + mb) * ld + m;
   // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
@@ -179,6 +189,10 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     if (!p.readout) store_pair(ph, pl, 0, h);
     ph += ld;
     pl += ld;
+    if (zp) {
+      *zp = z;
+      zp += p.ldz;
+    }
   };
   const int cnt = me - mb;
   int s = 0;
@@ -217,6 +231,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float zt = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
   ptx::tmem_ld_wait();
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
+  if (zp) *zp = zt;
   opart = wo * top;
   if (!p.readout) store_pair(ph, pl, 0, top);
 }
@@ -390,6 +405,71 @@ __device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32
   }
 }
 
+// Backward of the K=2 collapsed tanh rule (kBwd2), for one point and the feature owned
+// by this thread. The accumulator holds the adjoints of the layer's OUTPUT slots,
+// (h0b, h1b_r, tb) = B_bar[slot] = (Z_bar_next W)[slot], computed by the mainloop with
+// A = W^T; the saved pre-activations z (p.z_in, fp32) give the forward rule
+//   h0 = s(z0), h1_r = s'(z0) z1_r, top = s'(z0) zt + s''(z0) sum_r w_r z1_r^2
+// whose transpose is
+//   zt_bar  = s' tb
+//   z1_bar_r = s' h1b_r + 2 s'' w_r z1_r tb
+//   z0_bar  = s' h0b + s'' sum_r z1_r h1b_r + (s'' zt + s''' sum_r w_r z1_r^2) tb
+// (w_r = 1 unless p.weighted). Writes Z_bar of this layer as bf16 pairs.
+__device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tcol, int64_t row, int m,
+                                              const float* jw) {
+  const int P = p.P;
+  const int ld = p.ldo;
+  const size_t ldz = (size_t)p.ldzi;
+  const float* zr = p.z_in + (size_t)row * ldz + m;
+  const float hb0 = ptx::tmem_ld1(tcol);
+  const float tb = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
+  const float z0 = zr[0];
+  const float zt = zr[(size_t)(P - 1) * ldz];
+  ptx::tmem_ld_wait();
+  const ActD A = act_derivs(p.act, z0);
+  const float two_s2_tb = 2.f * A.d2 * tb;
+  const bool wsum = p.weighted;
+  float szh = 0.f, szz = 0.f;
+  uint16_t* ph = p.out_hi + (size_t)(row + 1) * ld + m;
+  uint16_t* pl = p.out_lo + (size_t)(row + 1) * ld + m;
+  const int nmid = P - 2;
+  int s = 0;
+  auto one = [&](float hb, float z1, int r) {
+    const float w = wsum ? jw[r] : 1.f;
+    szh = fmaf(z1, hb, szh);
+    szz = fmaf(w * z1, z1, szz);
+    store_pair(ph, pl, 0, fmaf(A.d1, hb, w * two_s2_tb * z1));
+    ph += ld;
+    pl += ld;
+  };
+  for (; s + 16 <= nmid; s += 16) {
+    float v[16], z[16];
+    ptx::tmem_ld16(tcol + (uint32_t)(1 + s), v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = zr[(size_t)(1 + s + i) * ldz];
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) one(v[i], z[i], s + i);
+  }
+  const int rem = nmid - s;
+  if (rem > 0) {
+    float v[15], z[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i)
+      if (i < rem) {
+        v[i] = ptx::tmem_ld1(tcol + (uint32_t)(1 + s + i));
+        z[i] = zr[(size_t)(1 + s + i) * ldz];
+      }
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 15; ++i)
+      if (i < rem) one(v[i], z[i], s + i);
+  }
+  store_pair(ph, pl, 0, A.d1 * tb);  // slot P-1
+  const float z0b = A.d1 * hb0 + A.d2 * szh + (A.d2 * zt + A.d3 * szz) * tb;
+  store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, z0b);
+}
+
 // The k-th tile of CTA pair `pair`. With at least one point group per pair, a pair runs
 // all feature tiles of a point group back to back (n-tile pair + (k / m_pairs) * npairs,
 // feature pair k % m_pairs), so the group's B operand is re-read from L2 while resident;
@@ -549,14 +629,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       const int m_tile = mp * 2 + (int)rank;  // 128-feature tile of this CTA
       const int64_t row0 = n_tile * p.pts_per_tile * p.P;
       const int m = m_tile * kBM + m_local;
-      const float bias = p.bias[m];
+      const float bias = p.bias ? p.bias[m] : 0.f;
       const float wo = p.readout ? p.w_out[m] : 0.f;
       const int64_t pts_left = p.n_points - n_tile * p.pts_per_tile;
       const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
       ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
-      if (KORD == kNest) {
+      if (KORD == kBwd2) {
+        for (int pt = g; pt < npts; pt += 2)
+          epilogue_bwd2(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);
+      } else if (KORD == kNest) {
         // nested biharmonic: a point is never split; with one point per tile (D >= 14)
         // only warp group 0 works on it
         for (int pt = g; pt < npts; pt += 2) {

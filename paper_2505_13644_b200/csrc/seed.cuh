@@ -41,6 +41,7 @@ struct SeedParams {
   uint16_t* out_hi;      // [N*P, ld] bf16 pair
   uint16_t* out_lo;
   int act;               // kAct*
+  float* z_out;          // K=2, grad mode: pre-activations [N*P, ld] (z0, W1 u_r, 0) or nullptr
 };
 
 // four adjacent features -> one 8-byte store into each of the hi and lo planes
@@ -97,6 +98,13 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
     }
   } else if (KORD == 2) {
+    if (p.z_out) {  // grad mode: the layer-1 pre-activations for the backward pass
+      *reinterpret_cast<float4*>(p.z_out + row0 * p.ld + m) = z0;
+      for (int r = 0; r < p.R; ++r)
+        *reinterpret_cast<float4*>(p.z_out + (row0 + 1 + r) * p.ld + m) =
+            __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m));
+      *reinterpret_cast<float4*>(p.z_out + (row0 + 1 + p.R) * p.ld + m) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     // batches of 4 rows: the 4 loads of U are in flight together (latency, not bandwidth,
     // bounded this loop when each load fed its stores one at a time)
     int r = 0;
@@ -264,6 +272,8 @@ struct SeedRandomParams {
   int Rv;
   const float* V;        // [N, S, Rv] (or [N, Rv, S] if v_trans) or nullptr => generated
   int v_trans;           // V stored [N, Rv, S]: sigma(x_n) [D, R] per point
+  int v_shared;          // V [S, ldv]: the same directions for every point (grad mode, fixed sets)
+  int ldv;
   const float* sigma;    // [D, Rv] or nullptr (then Rv == D)
   uint64_t seed;
   int64_t point_offset;
@@ -303,7 +313,9 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
       const int s = s0 + e / p.Rv, r = e % p.Rv;
       float v;
       if (p.V) {
-        v = p.v_trans ? p.V[((size_t)n * p.Rv + r) * p.S + s] : p.V[((size_t)n * p.S + s) * p.Rv + r];
+        v = p.v_shared ? p.V[(size_t)s * p.ldv + r]
+            : p.v_trans ? p.V[((size_t)n * p.Rv + r) * p.S + s]
+                        : p.V[((size_t)n * p.S + s) * p.Rv + r];
       } else {
         const uint64_t idx =
             ((uint64_t)(p.point_offset + n) * (uint64_t)p.S + (uint64_t)s) * (uint64_t)p.Rv + (uint64_t)r;

@@ -1,0 +1,149 @@
+"""GPU parity of the differentiable path (NEXT-3): ctm_backward vs the fp64 reverse-mode
+oracle (oracle/grad.py) on identical seeded inputs.
+
+Metric (reading R10): per parameter tensor,
+    max_i |g_gpu,i - g_oracle,i| / max_i |g_oracle,i|  <= GTOL
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle import grad as OG
+from synth import gaussian_directions, mlp_params, points, sigma as make_sigma, sigma_field, signed_weights, widths_for
+
+pytestmark = pytest.mark.gpu
+
+GTOL = 1e-4
+ERRS = {}
+
+
+@pytest.fixture(scope="module")
+def ctm():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2505_13644_b200 as ctm
+
+    ctm.lib()
+    return ctm
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dump():
+    yield
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if ERRS and os.path.isdir(out):
+        with open(os.path.join(out, "grad_errors.json"), "w") as fh:
+            json.dump(ERRS, fh, indent=1, sort_keys=True)
+
+
+def _mlp(ctm, params, act="tanh"):
+    m = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act=act)
+    m.grad_enable()
+    return m
+
+
+def _check_grads(name, grads, dW, db, tol=GTOL):
+    rec = {}
+    for l, ((gW, gb), rW, rb) in enumerate(zip(grads, dW, db)):
+        for tag, g, r in (("W", gW, rW), ("b", gb, rb)):
+            g = g.double().cpu().numpy()
+            assert np.all(np.isfinite(g))
+            scale = np.max(np.abs(r))
+            err = np.max(np.abs(g - r)) / scale if scale > 0 else np.max(np.abs(g))
+            rec[f"{tag}{l}"] = float(err)
+    ERRS[name] = rec
+    worst = max(rec.values())
+    assert worst <= tol, f"{name}: {rec}"
+
+
+def _gs(N, seed=7):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.standard_normal(N).astype(np.float32), rng.standard_normal(N).astype(np.float32)
+
+
+@pytest.mark.parametrize("widths,N", [([3, 16, 12, 1], 9), ([5, 16, 16, 1], 16), ([4, 40, 48, 36, 1], 7),
+                                      ([6, 24, 1], 5), (widths_for(50), 6)])
+def test_laplacian_gradients(ctm, widths, N):
+    params = mlp_params(widths, 0)
+    D = widths[0]
+    X = points(N, D)
+    gop, gf = _gs(N)
+    mlp = _mlp(ctm, params)
+    op, f = mlp.laplacian(torch.from_numpy(X).cuda())
+    grads = mlp.backward(torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda())
+    Ws = [W.astype(np.float64) for W, _ in params]
+    bs = [b.astype(np.float64) for _, b in params]
+    _, _, dW, db = OG.k2_grad(Ws, bs, X.astype(np.float64), np.eye(D), np.ones(D), gop, gf)
+    _check_grads(f"laplacian{widths}", grads, dW, db)
+
+
+def test_weighted_randomized_pointwise_and_directional_gradients(ctm):
+    widths = [5, 48, 40, 1]
+    params = mlp_params(widths, 0)
+    Ws = [W.astype(np.float64) for W, _ in params]
+    bs = [b.astype(np.float64) for _, b in params]
+    D, N = 5, 11
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    gop, gf = _gs(N)
+    g_op, g_f = torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda()
+    mlp = _mlp(ctm, params)
+    # weighted (sigma rect R = 3)
+    sig = make_sigma(D, 3, kind="rect")
+    mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())
+    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, sig.astype(np.float64).T, np.ones(3), gop, gf)
+    _check_grads("weighted", mlp.backward(g_op, g_f), dW, db)
+    # randomized (Rademacher generated in-kernel, S = 6): op carries 1/S
+    mlp.randomized_laplacian(Xc, S=6, seed=3)
+    V = O.rademacher(3, 0, N, 6, D)
+    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, V, np.full(6, 1 / 6), gop, gf)
+    _check_grads("randomized", mlp.backward(g_op, g_f), dW, db)
+    # sigma(x)
+    sx = sigma_field(X, 4)
+    mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())
+    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, np.transpose(sx.astype(np.float64), (0, 2, 1)), np.ones(4), gop, gf)
+    _check_grads("pointwise", mlp.backward(g_op, g_f), dW, db)
+    # directional sums K = 2 with signed weights, shared and per point
+    w = signed_weights(4)
+    for per_point in (False, True):
+        dirs = gaussian_directions(N, 4, D, seed=8) if per_point else gaussian_directions(1, 4, D, seed=8)[0]
+        mlp.directional_sum(Xc, 2, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())
+        _, _, dW, db = OG.k2_grad(Ws, bs, Xd, dirs.astype(np.float64), w.astype(np.float64), gop, gf)
+        _check_grads(f"directional_pp{int(per_point)}", mlp.backward(g_op, g_f), dW, db)
+
+
+def test_sin_activation_gradients(ctm):
+    widths = [4, 32, 24, 1]
+    params = mlp_params(widths, 0)
+    X = points(8, 4)
+    gop, gf = _gs(8)
+    mlp = _mlp(ctm, params, act="sin")
+    mlp.laplacian(torch.from_numpy(X).cuda())
+    grads = mlp.backward(torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda())
+    _, _, dW, db = OG.k2_grad([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params],
+                              X.astype(np.float64), np.eye(4), np.ones(4), gop, gf, act="sin")
+    _check_grads("sin", grads, dW, db)
+
+
+def test_backward_is_deterministic_accumulates_and_needs_a_tape(ctm):
+    params = mlp_params([5, 64, 48, 1], 0)
+    X = torch.from_numpy(points(33, 5)).cuda()
+    gop = torch.from_numpy(_gs(33)[0]).cuda()
+    mlp = _mlp(ctm, params)
+    mlp.laplacian(X)
+    a = mlp.backward(gop)
+    b = mlp.backward(gop)
+    for (aw, ab), (bw, bb) in zip(a, b):
+        assert torch.equal(aw, bw) and torch.equal(ab, bb)
+    c = mlp.backward(gop, grads=[(w.clone(), v.clone()) for w, v in a], accumulate=True)
+    for (aw, ab), (cw, cb) in zip(a, c):
+        torch.testing.assert_close(cw, 2 * aw, rtol=1e-6, atol=0)
+    assert torch.all(a[-1][1] == 0)  # gf = None: d/db_L of sum gop op = 0
+    mlp.biharmonic(X)  # not differentiable: clears the tape
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        mlp.backward(gop)
