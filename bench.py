@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
     ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard",
-                                   "stochastic_biharmonic", "biharmonic_nested"],
+                                   "stochastic_biharmonic", "biharmonic_nested", "laplacian_train"],
                     default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -61,6 +61,8 @@ def workload(args):
     D = 5 if args.op in ("biharmonic", "stochastic_biharmonic", "biharmonic_nested") else 50
     names = {
         "laplacian": "C1 exact Laplacian",
+        "laplacian_train": ("C1 PINN training step: exact Laplacian forward (grad mode) + loss cotangent + "
+                            "ctm_backward + gradient all-reduce (N>1) + SGD update via ctm_set_weights"),
         "standard": "C1 exact Laplacian by STANDARD Taylor mode (1+2D vectors; the paper's baseline)",
         "weighted": "C2 weighted Laplacian (dense full-rank sigma, R=50)",
         "randomized": f"C3 randomized Laplacian (Rademacher, S={args.S}, generated in-kernel)",
@@ -136,6 +138,9 @@ def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
     def run(X):
         if op in ("laplacian", "standard"):
             O.laplacian(net, X, O.O1)
+        elif op == "laplacian_train":
+            from oracle import grad as OG
+            OG.k2_grad(net.Ws, net.bs, X, np.eye(D), np.ones(D), np.ones(X.shape[0]) / X.shape[0])
         elif op == "weighted":
             O.weighted_laplacian(net, X, sig, O.O1)
         elif op == "randomized":
@@ -219,9 +224,38 @@ def main():
     sig = torch.from_numpy(make_sigma(D, D, kind="dense")).to(dev)
     op_out = torch.empty(N, device=dev)
     f_out = torch.empty(N, device=dev)
+    train = args.op == "laplacian_train"
+    if train:
+        from paper_2505_13644_b200.dist import allreduce_grads
+
+        mlp.grad_enable()
+        pdev = [(torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)) for W, b in params]
+        grads = [(torch.empty_like(W), torch.empty_like(b)) for W, b in pdev]
+        flat_p = [t for pair in pdev for t in pair]
+        flat_g = [t for pair in grads for t in pair]
+        # Poisson-type residual: Laplacian f(x) - g(x), g = sum_d sin(pi x_d) (synthetic source)
+        target = torch.sin(torch.pi * X).sum(1)
+        res = torch.empty(N, device=dev)
+        n_glob = N * world
+        launches = {}
+
+    def train_step(Xd):
+        mlp.laplacian(Xd, out=op_out, f_out=f_out)
+        launches["fwd"] = mlp.last_plan()["launches"]
+        torch.sub(op_out, target, out=res)
+        res.mul_(2.0 / n_glob)  # d/d op_n of mean_n (op_n - g_n)^2
+        mlp.backward(res, grads=grads)
+        launches["bwd"] = mlp.last_plan()["launches"]
+        if world > 1:
+            allreduce_grads(grads)
+        torch._foreach_add_(flat_p, flat_g, alpha=-1e-4)
+        mlp.set_weights(pdev)
+        launches["upd"] = mlp.last_plan()["launches"]
 
     def step(Xd):
-        if args.op == "laplacian":
+        if train:
+            train_step(Xd)
+        elif args.op == "laplacian":
             mlp.laplacian(Xd, out=op_out, f_out=f_out)
         elif args.op == "standard":
             mlp.laplacian_standard(Xd, out=op_out, f_out=f_out)
@@ -252,6 +286,8 @@ def main():
     for _ in range(max(3, args.warmup)):
         step(X)
     torch.cuda.synchronize()
+    if train:
+        mlp.laplacian(X, out=op_out, f_out=f_out)  # plan of the forward
     plan = mlp.last_plan()
 
     clocks = ClockSampler(local)
@@ -318,18 +354,24 @@ def main():
     bf16_sust = peaks.get("bf16_tflops_sustained", 1400.0)
     tensor_peak = bf16_sust                # the layer MMAs are kind::f16 with bf16 operands
     useful_peak = tensor_peak / 3.0        # 3xBF16: three tensor products per useful product
-    lay = prof["layer"]
+    dom = max(("layer", "bwd", "wgrad"), key=lambda k: prof[k]["ms"]) if train else "layer"
+    lay = prof[dom]
     achieved = lay["work"] / (lay["ms"] / 1e3) / 1e12 if lay["ms"] > 0 else None
+    kernel_name = {
+        "layer": "jet_layer_kernel (layers 2-4: tcgen05 3xBF16 GEMM + tanh Taylor epilogue)",
+        "bwd": "jet_layer_kernel<kBwd2> (adjoint layers: tcgen05 3xBF16 W^T GEMM + transposed Taylor rule)",
+        "wgrad": "weight-gradient GEMMs Z_bar^T B (cuBLAS, 3 bf16 GEMMs per layer, fp32 accumulate)",
+    }[dom]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "layer_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh_:
             tj = json.load(fh_)
-        traffic = tj.get(args.op, {}).get("dram_bytes_per_launch")
+        traffic = tj.get(args.op, {}).get("dram_bytes_per_launch") if not train else None
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
         "frac": (achieved / useful_peak) if achieved else None, "traffic": traffic,
-        "kernel": "jet_layer_kernel (layers 2-4: tcgen05 3xBF16 GEMM + tanh Taylor epilogue)",
+        "kernel": kernel_name,
         "peak_basis": (f"{peak_src} bf16 sustained {bf16_sust} TF/s / 3 (3xBF16 split: three bf16 tensor "
                        "products per useful fp32-accurate product)"),
         "tensor_pipe_frac": (3.0 * achieved / tensor_peak) if achieved else None,
@@ -354,7 +396,9 @@ def main():
             "dtype": "f32 (3xbf16 tensor products, fp32 accumulate)", "data": "synthetic",
             "config": {"workload": wl, "op": args.op, "N_per_gpu": N, "D": D, "widths": widths,
                        "slots_per_point": plan["slots_per_point"], "points_per_tile": plan["points_per_tile"],
-                       "mma_n": plan["mma_n"], "parallelism": f"dp{world} (points sharded, no collective in step)",
+                       "mma_n": plan["mma_n"],
+                       "parallelism": (f"dp{world} (points sharded; gradient all-reduce, one 5 MB NCCL bucket)"
+                                       if train else f"dp{world} (points sharded, no collective in step)"),
                        "l2": "flushed between timed steps (256 MiB write, outside the step events); "
                              "step working set > 10 GB >> L2"},
             "roofline": roofline,
@@ -362,7 +406,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": N * D * 4,
                     "d2h_bytes_per_step": 2 * N * 4},
             "clocks": clk,
-            "gpu_launches": plan["launches"] * args.steps,
+            "gpu_launches": (sum(launches.values()) if train else plan["launches"]) * args.steps,
         }
         print(json.dumps(line), flush=True)
     mlp.close()

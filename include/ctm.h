@@ -109,6 +109,13 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, in
 ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                           void *stream);
 
+/* Replace the weights of a loaded MLP (same widths), e.g. after an optimizer step: the
+ * library re-derives every weight-dependent array (bf16 pairs, W1^T, the fixed
+ * directions' W1 V, W^T in grad mode) with kernels on `stream`, asynchronously; W, b as
+ * in ctm_load_mlp (device, caller-owned; must stay valid until `stream` passes this
+ * call). Clears the recorded tape. Errors: CTM_EINVAL, CTM_ESHAPE, CTM_ECUDA. */
+ctm_status ctm_set_weights(ctm_mlp_t mlp, const float *const *W, const float *const *b, void *stream);
+
 /* Hidden-layer activation of a loaded MLP (default CTM_ACT_TANH, the paper's).
  * Every operator applies the Taylor rules of the selected s with its derivatives
  * s', s'', s''', s'''' (sin: cos, -sin, -cos, sin; square z^2: 2z, 2, 0, 0; identity:
@@ -214,7 +221,10 @@ typedef enum {
     CTM_KIND_SEED = 1,    /* layer 1: seed + affine + tanh rule                 */
     CTM_KIND_LAYER = 2,   /* hidden layers: tcgen05 GEMM + Taylor epilogue      */
     CTM_KIND_FINAL = 3,   /* readout / finalize                                 */
-    CTM_KIND_COUNT = 4
+    CTM_KIND_BWD = 4,     /* ctm_backward: adjoint layers (tcgen05, W^T GEMM + transposed rule) */
+    CTM_KIND_WGRAD = 5,   /* ctm_backward: weight-gradient GEMMs Z_bar^T B (work = 2 rows K M)  */
+    CTM_KIND_BAUX = 6,    /* ctm_backward: readout adjoint, bias sums, crops                    */
+    CTM_KIND_COUNT = 7
 } ctm_kernel_kind;
 
 ctm_status ctm_profile_enable(ctm_mlp_t mlp, int32_t enable);

@@ -39,6 +39,7 @@ ABI = {
                                                  _VP]),
     "ctm_set_activation": (ctypes.c_int, [_VP, ctypes.c_int]),
     "ctm_grad_enable": (ctypes.c_int, [_VP, _I32]),
+    "ctm_set_weights": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
     "ctm_backward": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "ctm_last_error": (ctypes.c_char_p, []),
@@ -47,7 +48,7 @@ ABI = {
     "ctm_profile_enable": (ctypes.c_int, [_VP, _I32]),
     "ctm_profile_read": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
 }
-KINDS = ("prep", "seed", "layer", "final")
+KINDS = ("prep", "seed", "layer", "final", "bwd", "wgrad", "baux")
 
 _lib = None
 
@@ -243,6 +244,18 @@ class MLP:
                                                self._p(f_out), _stream_ptr(stream, self.device)),
                "ctm_stochastic_biharmonic")
         return out, f_out
+
+    def set_weights(self, params: Sequence, stream=None):
+        """Replace the weights (same widths) asynchronously on ``stream`` (e.g. after an
+        optimizer step). Keeps device copies alive until the next call."""
+        Ws = [_dev_f32(W, self.device, "W") for W, _ in params]
+        bs = [_dev_f32(b, self.device, "b").reshape(-1) for _, b in params]
+        if [Ws[0].shape[1]] + [W.shape[0] for W in Ws] != list(self.widths):
+            raise CTMError("set_weights: widths differ from the loaded MLP")
+        W_arr = (_VP * len(Ws))(*[W.data_ptr() for W in Ws])
+        b_arr = (_VP * len(bs))(*[b.data_ptr() for b in bs])
+        _check(lib().ctm_set_weights(self._h, W_arr, b_arr, _stream_ptr(stream, self.device)), "ctm_set_weights")
+        self._keep = (Ws, bs)
 
     # ------------------------------------------------------------------ differentiable path
     def grad_enable(self, enable: bool = True):

@@ -52,11 +52,15 @@ __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
     const float tb = p.c * go * wl;  // adjoint of the collapsed top h_top
     const float hb0 = gfn * wl;      // adjoint of h0
     float szz = 0.f;
+    const float* __restrict__ zs = zr + ldz;
+    uint16_t* __restrict__ oh = p.out_hi + (row + 1) * ldo + m;
+    uint16_t* __restrict__ ol = p.out_lo + (row + 1) * ldo + m;
+#pragma unroll 4
     for (int r = 0; r < p.P - 2; ++r) {
-      const float z1 = zr[(size_t)(1 + r) * ldz];
+      const float z1 = zs[(size_t)r * ldz];
       const float w = p.jw ? p.jw[r] : 1.f;
       szz = fmaf(w * z1, z1, szz);
-      store_pair(p.out_hi, p.out_lo, (row + 1 + r) * ldo + m, 2.f * A.d2 * w * z1 * tb);
+      store_pair(oh, ol, (size_t)r * ldo, 2.f * A.d2 * w * z1 * tb);
     }
     store_pair(p.out_hi, p.out_lo, (row + p.P - 1) * ldo + m, A.d1 * tb);
     store_pair(p.out_hi, p.out_lo, row * ldo + m, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb);
@@ -82,14 +86,22 @@ __global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict_
   part[(size_t)g * ncols + m] = acc;
 }
 
-// out[m] (=|+=) sum_g part[g, m], g = 0..G-1 in order, for m < ncols
-__global__ void reduce_groups_kernel(const float* __restrict__ part, int G, int ncols, float* __restrict__ out,
-                                     int accumulate) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= ncols) return;
+// out[m] (=|+=) sum_g part[g, m] for m < ncols, deterministic: block (32, 32) handles 32
+// columns; thread (x, y) sums groups y, y + 32, ... in order, then a fixed smem tree over y
+__global__ void __launch_bounds__(1024) reduce_groups_kernel(const float* __restrict__ part, int G, int ncols,
+                                                             float* __restrict__ out, int accumulate) {
+  __shared__ float red[32][33];
+  const int m = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
-  for (int g = 0; g < G; ++g) s += part[(size_t)g * ncols + m];
-  out[m] = accumulate ? out[m] + s : s;
+  if (m < ncols)
+    for (int g = threadIdx.y; g < G; g += 32) s += part[(size_t)g * ncols + m];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    if ((int)threadIdx.y < o) red[threadIdx.y][threadIdx.x] += red[threadIdx.y + o][threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.y == 0 && m < ncols) out[m] = accumulate ? out[m] + red[0][threadIdx.x] : red[0][threadIdx.x];
 }
 
 // out[0] (=|+=) sum_n v[n] (one block, fixed order: strided partials then a tree)

@@ -108,7 +108,9 @@ struct ctm_mlp {
   std::vector<CUtensorMap> mapA_hi, mapA_lo;
   // output layer
   float* w_out = nullptr;     // [wpad[L-1]]
-  float b_out = 0.f;
+  float* b_out = nullptr;     // [1] device (updated asynchronously by ctm_set_weights)
+  float* eyeD = nullptr;      // [D, D] identity (Laplacian directions)
+  float* bih_dirs = nullptr;  // [J_bih, D] biharmonic family directions
   // fixed direction sets
   float* U_lap = nullptr;     // [D, ld1]: z1 for e_d
   float* c_lap = nullptr;     // [ld1]
@@ -173,7 +175,7 @@ ctm_status free_all(ctm_mlp* h) {
     if (p) cudaFree(p);
     p = nullptr;
   };
-  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1hi); F(h->W1lo);
+  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1hi); F(h->W1lo); F(h->b_out); F(h->eyeD); F(h->bih_dirs);
   for (auto& p : h->Whi) F(p);
   for (auto& p : h->Wlo) F(p);
   for (auto& p : h->bias) F(p);
@@ -743,6 +745,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
 // [Kin, Mout] = row-major [Mout, Kin].
 ctm_status weight_grad_gemm(ctm_mlp* h, const uint16_t* Bhi, const uint16_t* Blo, int Kin, const uint16_t* Zhi,
                             const uint16_t* Zlo, int Mout, int64_t rows, float* C, cudaStream_t st) {
+  ProfScope ps(h, CTM_KIND_WGRAD, 2.0 * (double)rows * Kin * Mout, st);
   if (cublasSetStream(h->cublas, st) != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasSetStream");
   const float one = 1.f, zero = 0.f;
   const uint16_t* As[3] = {Bhi, Blo, Bhi};
@@ -759,12 +762,14 @@ ctm_status weight_grad_gemm(ctm_mlp* h, const uint16_t* Bhi, const uint16_t* Blo
 // out[m] (=|+=) sum_n Zb[n * P + 0, m] for m < ncols (the bias gradient: bias on slot 0 only)
 ctm_status bias_grad(ctm_mlp* h, const uint16_t* Zhi, const uint16_t* Zlo, int ld, int ncols, float* out, int acc,
                      cudaStream_t st) {
-  const int G = 128;
+  const int G = 1024;  // point groups: enough independent rows in flight per column
   ctm_status s = ensure(h->tape.part, h->tape.part_elems, (size_t)G * std::max(ncols, 1));
   if (s != CTM_OK) return s;
+  ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
+  h->last_launches += 2;
   ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Zhi, Zlo, nullptr, h->tape.N, h->tape.P, ld, ncols,
                                                                    G, h->tape.part);
-  ctm::reduce_groups_kernel<<<(ncols + 127) / 128, 128, 0, st>>>(h->tape.part, G, ncols, out, acc);
+  ctm::reduce_groups_kernel<<<(ncols + 31) / 32, dim3(32, 32), 0, st>>>(h->tape.part, G, ncols, out, acc);
   return CTM_OK;
 }
 
@@ -785,9 +790,12 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   s = ensure(T.dWpad, T.dWpad_elems, dwmax);
   if (s != CTM_OK) return s;
   const float* jw = T.weighted ? T.weights : nullptr;
+  h->last_launches = 0;
   // ---- readout and the last hidden rule, transposed
   {
-    const int G = 128, w = h->wpad[L - 1];
+    ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
+    h->last_launches += 3;
+    const int G = 1024, w = h->wpad[L - 1];
     s = ensure(T.part, T.part_elems, (size_t)G * w);
     if (s != CTM_OK) return s;
     ctm::TopBwdParams tp{};
@@ -808,7 +816,7 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     tp.dw_part = T.part;
     tp.G = G;
     ctm::top_bwd_kernel<<<dim3(w / 128, G), 128, 0, st>>>(tp);
-    ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 127) / 128, 128, 0, st>>>(T.part, G, w, dW[L - 1], acc);
+    ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 31) / 32, dim3(32, 32), 0, st>>>(T.part, G, w, dW[L - 1], acc);
     if (gf)
       ctm::vector_sum_kernel<<<1, 256, 0, st>>>(gf, N, db[L - 1], acc);
     else if (!acc)
@@ -822,6 +830,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     if (s != CTM_OK) return s;
     {
       const int64_t n = (int64_t)h->widths[l] * h->widths[l - 1];
+      ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
+      ++h->last_launches;
       ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, Kin, h->widths[l], h->widths[l - 1],
                                                                     dW[l - 1], acc);
     }
@@ -854,7 +864,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     s = set_layer_attr<ctm::kBwd2>(h);
     if (s != CTM_OK) return s;
     {
-      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * N * P * h->widths[l - 1] * h->widths[l], st);
+      ProfScope ps(h, CTM_KIND_BWD, 2.0 * N * P * h->widths[l - 1] * h->widths[l], st);
+      ++h->last_launches;
       ctm::jet_layer_kernel<ctm::kBwd2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
           h->mapAT_hi[l - 2], h->mapAT_lo[l - 2], mb_hi, mb_lo, lp);
     }
@@ -865,6 +876,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   if (s != CTM_OK) return s;
   {
     const int64_t n = (int64_t)h->widths[1] * h->widths[0];
+    ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
+    ++h->last_launches;
     ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, h->k1pad, h->widths[1], h->widths[0], dW[0],
                                                                   acc);
   }
@@ -872,6 +885,44 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   if (s != CTM_OK) return s;
   CTM_CUDA(cudaGetLastError());
   return CTM_OK;
+}
+
+// Every array derived from the weights, written on `st` (load and ctm_set_weights):
+// W1^T and b1, the bf16 pairs of every tensor-core layer (and W_l^T in grad mode), the
+// padded output weights, and the fixed direction sets' U = W1 V, c = sum w (W1 v)^K.
+void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cudaStream_t st) {
+  const int L = h->L, D = h->widths[0], ld1 = h->wpad[1];
+  {
+    const int64_t n = (int64_t)D * ld1;
+    ctm::transpose_w1_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], b[0], h->widths[1], D, ld1, h->W1T,
+                                                                          h->b1);
+  }
+  {
+    const int64_t n = (int64_t)ld1 * h->k1pad;
+    ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], b[0], h->widths[1], D, ld1, h->k1pad,
+                                                                           h->W1hi, h->W1lo, h->b1);
+  }
+  for (int l = 2; l <= L - 1; ++l) {
+    const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
+    const int64_t n = (int64_t)mpad * kpad;
+    ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        W[l - 1], b[l - 1], h->widths[l], h->widths[l - 1], mpad, kpad, h->Whi[l - 2], h->Wlo[l - 2], h->bias[l - 2]);
+    if (!h->WThi.empty())
+      ctm::transpose_pair_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Whi[l - 2], h->Wlo[l - 2], mpad, kpad,
+                                                                              h->WThi[l - 2], h->WTlo[l - 2]);
+  }
+  {
+    const int lpad = h->wpad[L - 1];
+    ctm::pad_vector_kernel<<<(lpad + 255) / 256, 256, 0, st>>>(W[L - 1], h->widths[L - 1], lpad, h->w_out);
+    cudaMemcpyAsync(h->b_out, b[L - 1], sizeof(float), cudaMemcpyDeviceToDevice, st);
+  }
+  ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->eyeD, D, nullptr, 2, h->U_lap,
+                                                                 h->c_lap);
+  if (h->J_bih)
+    ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->bih_dirs, h->J_bih, h->w_bih, 4,
+                                                                   h->U_bih, h->c_bih);
+  h->last_launches = 4 + (L - 2) * (h->WThi.empty() ? 1 : 2) + (h->J_bih ? 1 : 0);
+  h->tape.valid = false;
 }
 
 ctm_status check_common(ctm_mlp* h, const float* X, int64_t N, float* op_out, float* f_out) {
@@ -945,28 +996,17 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     }                                                                                         \
   } while (0)
 
-  // layer 1: transposed copy
+  // ---- allocations and tensor maps (the values are written by derive_weights)
+  h->k1pad = round_up(D, ctm::kBK);
   LOAD_CUDA(cudaMalloc(&h->W1T, sizeof(float) * (size_t)D * ld1));
   LOAD_CUDA(cudaMalloc(&h->b1, sizeof(float) * ld1));
-  {
-    const int64_t n = (int64_t)D * ld1;
-    ctm::transpose_w1_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[0], b[0], widths[1], D, ld1, h->W1T, h->b1);
+  LOAD_CUDA(cudaMalloc(&h->W1hi, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
+  LOAD_CUDA(cudaMalloc(&h->W1lo, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
+  if (!make_map(&h->mapA1_hi, h->W1hi, h->k1pad, ld1, ctm::kBM) ||
+      !make_map(&h->mapA1_lo, h->W1lo, h->k1pad, ld1, ctm::kBM)) {
+    fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W1");
+    return bail(CTM_ECUDA);
   }
-  // layer 1 as a tensor-core layer (used by the randomized operator)
-  {
-    h->k1pad = round_up(D, ctm::kBK);
-    LOAD_CUDA(cudaMalloc(&h->W1hi, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
-    LOAD_CUDA(cudaMalloc(&h->W1lo, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
-    const int64_t n = (int64_t)ld1 * h->k1pad;
-    ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[0], b[0], widths[1], D, ld1, h->k1pad,
-                                                                      h->W1hi, h->W1lo, h->b1);
-    if (!make_map(&h->mapA1_hi, h->W1hi, h->k1pad, ld1, ctm::kBM) ||
-        !make_map(&h->mapA1_lo, h->W1lo, h->k1pad, ld1, ctm::kBM)) {
-      fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W1");
-      return bail(CTM_ECUDA);
-    }
-  }
-  // hidden GEMM layers
   for (int l = 2; l <= n_layers - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
     uint16_t *whi, *wlo;
@@ -977,9 +1017,6 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     h->Wlo.push_back(wlo);
     LOAD_CUDA(cudaMalloc(&bp, sizeof(float) * mpad));
     h->bias.push_back(bp);
-    const int64_t n = (int64_t)mpad * kpad;
-    ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256>>>(W[l - 1], b[l - 1], widths[l], widths[l - 1],
-                                                                      mpad, kpad, whi, wlo, bp);
     CUtensorMap mh, ml;
     if (!make_map(&mh, whi, kpad, mpad, ctm::kBM) || !make_map(&ml, wlo, kpad, mpad, ctm::kBM)) {
       fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for weights");
@@ -988,40 +1025,25 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     h->mapA_hi.push_back(mh);
     h->mapA_lo.push_back(ml);
   }
-  // output layer
-  {
-    const int wl = widths[n_layers - 1], lpad = h->wpad[n_layers - 1];
-    LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * lpad));
-    ctm::pad_vector_kernel<<<(lpad + 255) / 256, 256>>>(W[n_layers - 1], wl, lpad, h->w_out);
-    LOAD_CUDA(cudaMemcpy(&h->b_out, b[n_layers - 1], sizeof(float), cudaMemcpyDeviceToHost));
-  }
-  // fixed direction sets: Laplacian (e_d) and, for D <= 7, the biharmonic family
-  {
+  LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * h->wpad[n_layers - 1]));
+  LOAD_CUDA(cudaMalloc(&h->b_out, sizeof(float)));
+  {  // fixed direction sets: the Laplacian's e_d and, for D <= 7, the biharmonic family
     std::vector<float> eye((size_t)D * D, 0.f);
     for (int d = 0; d < D; ++d) eye[(size_t)d * D + d] = 1.f;
-    float* dd;
-    LOAD_CUDA(cudaMalloc(&dd, sizeof(float) * eye.size()));
-    LOAD_CUDA(cudaMemcpy(dd, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
+    LOAD_CUDA(cudaMalloc(&h->eyeD, sizeof(float) * eye.size()));
+    LOAD_CUDA(cudaMemcpy(h->eyeD, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
     LOAD_CUDA(cudaMalloc(&h->U_lap, sizeof(float) * (size_t)D * ld1));
     LOAD_CUDA(cudaMalloc(&h->c_lap, sizeof(float) * ld1));
-    ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128>>>(h->W1T, D, ld1, dd, D, nullptr, 2, h->U_lap, h->c_lap);
-    LOAD_CUDA(cudaDeviceSynchronize());
-    cudaFree(dd);
     if (3 * (D * (3 * D - 1) / 2) + 2 <= ctm::kMaxN) {
       std::vector<float> dirs, w;
       biharmonic_family(D, dirs, w);
       h->J_bih = (int)w.size();
-      float* dv;
-      LOAD_CUDA(cudaMalloc(&dv, sizeof(float) * dirs.size()));
-      LOAD_CUDA(cudaMemcpy(dv, dirs.data(), sizeof(float) * dirs.size(), cudaMemcpyHostToDevice));
+      LOAD_CUDA(cudaMalloc(&h->bih_dirs, sizeof(float) * dirs.size()));
+      LOAD_CUDA(cudaMemcpy(h->bih_dirs, dirs.data(), sizeof(float) * dirs.size(), cudaMemcpyHostToDevice));
       LOAD_CUDA(cudaMalloc(&h->w_bih, sizeof(float) * w.size()));
       LOAD_CUDA(cudaMemcpy(h->w_bih, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice));
       LOAD_CUDA(cudaMalloc(&h->U_bih, sizeof(float) * (size_t)h->J_bih * ld1));
       LOAD_CUDA(cudaMalloc(&h->c_bih, sizeof(float) * ld1));
-      ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128>>>(h->W1T, D, ld1, dv, h->J_bih, h->w_bih, 4, h->U_bih,
-                                                              h->c_bih);
-      LOAD_CUDA(cudaDeviceSynchronize());
-      cudaFree(dv);
     }
   }
   {
@@ -1029,6 +1051,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     LOAD_CUDA(cudaMalloc(&h->w_ones, sizeof(float) * ones.size()));
     LOAD_CUDA(cudaMemcpy(h->w_ones, ones.data(), sizeof(float) * ones.size(), cudaMemcpyHostToDevice));
   }
+  derive_weights(h, W, b, 0);
   LOAD_CUDA(cudaGetLastError());
   LOAD_CUDA(cudaDeviceSynchronize());
 #undef LOAD_CUDA
@@ -1153,6 +1176,19 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act) {
                     CTM_ACT_SQUARE == ctm::kActSquare && CTM_ACT_SIN == ctm::kActSin,
                 "ABI activation codes");
   mlp->act = (int)act;
+  return CTM_OK;
+}
+
+ctm_status ctm_set_weights(ctm_mlp_t mlp, const float* const* W, const float* const* b, void* stream) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (!W || !b) return fail(CTM_EINVAL, "NULL W/b arrays");
+  for (int l = 0; l < mlp->L; ++l)
+    if (!W[l] || !b[l] || !aligned16(W[l]) || !aligned16(b[l]))
+      return fail(W[l] && b[l] ? CTM_ESHAPE : CTM_EINVAL, "weights must be non-NULL and 16-byte aligned");
+  DeviceGuard g(mlp->device);
+  derive_weights(mlp, W, b, (cudaStream_t)stream);
+  CTM_CUDA(cudaGetLastError());
   return CTM_OK;
 }
 

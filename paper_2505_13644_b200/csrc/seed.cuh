@@ -379,7 +379,7 @@ __global__ void prep_sigma_kernel(const float* __restrict__ W1T, int D, int ld, 
 }
 
 // op[n] = scale * sum_t partial[n, t, 1];  f[n] = b_out + sum_t partial[n, t, 0]   (fixed order)
-__global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, int64_t N, float b_out, float scale,
+__global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, int64_t N, const float* __restrict__ b_out, float scale,
                                 float* __restrict__ op, float* __restrict__ f) {
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -389,14 +389,14 @@ __global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, 
     s1 += partial[(n * m_tiles + t) * 2 + 1];
   }
   op[n] = scale * s1;
-  if (f) f[n] = b_out + s0;
+  if (f) f[n] = *b_out + s0;
 }
 
 // Readout straight from a layer block (nets with a single hidden layer):
 // one warp per point, lanes over features.
 // standard != 0: the op is sum_r w_out . h2_r over rows 2, 4, .., P-1 (standard mode)
 __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo, int ld, int P,
-                                     int width, const float* __restrict__ w_out, float b_out, float scale,
+                                     int width, const float* __restrict__ w_out, const float* __restrict__ b_out, float scale,
                                      int64_t N, float* __restrict__ op, float* __restrict__ f, int standard) {
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -421,7 +421,7 @@ __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint
   }
   if (lane == 0) {
     op[n] = scale * s1;
-    if (f) f[n] = b_out + s0;
+    if (f) f[n] = *b_out + s0;
   }
 }
 

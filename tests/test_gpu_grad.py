@@ -147,3 +147,42 @@ def test_backward_is_deterministic_accumulates_and_needs_a_tape(ctm):
     mlp.biharmonic(X)  # not differentiable: clears the tape
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
         mlp.backward(gop)
+
+
+def test_set_weights_matches_a_fresh_load_bitwise(ctm):
+    p0 = mlp_params([5, 64, 48, 1], 0)
+    p1 = mlp_params([5, 64, 48, 1], 1)
+    X = torch.from_numpy(points(19, 5)).cuda()
+    a = _mlp(ctm, p0)
+    a.set_weights([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in p1])
+    b = _mlp(ctm, p1)
+    for name in ("laplacian", "biharmonic", "biharmonic_nested"):
+        oa, fa = getattr(a, name)(X)
+        ob, fb = getattr(b, name)(X)
+        assert torch.equal(oa, ob) and torch.equal(fa, fb), name
+    gop = torch.from_numpy(_gs(19)[0]).cuda()
+    a.laplacian(X)
+    b.laplacian(X)
+    for (wa, ba), (wb, bb) in zip(a.backward(gop), b.backward(gop)):
+        assert torch.equal(wa, wb) and torch.equal(ba, bb)
+
+
+def test_sharded_gradients_sum_to_the_full_batch(ctm):
+    """Data parallelism on one GPU: the gradient of the full batch equals the sum of the
+    two shards' gradients (accumulate=True), randomized directions keyed on point_offset."""
+    params = mlp_params([6, 64, 64, 1], 0)
+    N = 40
+    X = torch.from_numpy(points(N, 6)).cuda()
+    gop, gf = (torch.from_numpy(t).cuda() for t in _gs(N))
+    mlp = _mlp(ctm, params)
+    mlp.randomized_laplacian(X, S=7, seed=5)
+    full = mlp.backward(gop, gf)
+    mlp.randomized_laplacian(X[:17], S=7, seed=5, point_offset=0)
+    acc = mlp.backward(gop[:17], gf[:17])
+    mlp.randomized_laplacian(X[17:], S=7, seed=5, point_offset=17)
+    acc = mlp.backward(gop[17:], gf[17:], grads=acc, accumulate=True)
+    for (fw, fb), (aw, ab) in zip(full, acc):
+        scale = max(fw.abs().max().item(), 1e-30)
+        assert (fw - aw).abs().max().item() / scale < 1e-5
+        scale = max(fb.abs().max().item(), 1e-30)
+        assert (fb - ab).abs().max().item() / scale < 1e-5

@@ -121,3 +121,44 @@ def test_bench_reference_arm_runs_on_cpu(tmp_path):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle"
+
+
+def _worker_grad(rank, world, port, q):
+    """Data-parallel training on a world-2 gloo group: each rank differentiates its shard
+    (the fp64 oracle stands in for ctm_backward on CPU), allreduce_grads sums them."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import numpy as np
+
+    from oracle import grad as OG
+    from paper_2505_13644_b200.dist import allreduce_grads, shard
+    from tests._util import random_params
+
+    Ws, bs = random_params([3, 8, 6, 1], 4)
+    n = 11
+    X = np.random.default_rng(0).uniform(-1, 1, (n, 3))
+    gop = np.random.default_rng(1).standard_normal(n)
+    gf = np.random.default_rng(2).standard_normal(n)
+    off, cnt = shard(n, rank, world)
+    sl = slice(off, off + cnt)
+    _, _, dW, db = OG.k2_grad(Ws, bs, X[sl], np.eye(3), np.ones(3), gop[sl], gf[sl])
+    grads = [(torch.from_numpy(w.copy()), torch.from_numpy(b.copy())) for w, b in zip(dW, db)]
+    allreduce_grads(grads)
+    _, _, fW, fb = OG.k2_grad(Ws, bs, X, np.eye(3), np.ones(3), gop, gf)
+    err = max(max(np.max(np.abs(g.numpy() - w)) for (g, _), w in zip(grads, fW)),
+              max(np.max(np.abs(g.numpy() - b)) for (_, g), b in zip(grads, fb)))
+    q.put((rank, float(err)))
+    dist.destroy_process_group()
+
+
+def test_data_parallel_gradient_allreduce_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_grad, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] < 1e-12 and res[1] < 1e-12, res
