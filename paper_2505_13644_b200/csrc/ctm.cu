@@ -130,7 +130,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
-  bool smem_attr_set[7] = {false, false, false, false, false, false, false};
+  bool smem_attr_set[32] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
   std::vector<uint16_t*> WThi, WTlo;        // W_l^T bf16 pairs [wpad[l-1], wpad[l]], l = 2..L-1
@@ -312,13 +312,24 @@ struct ProfScope {
 };
 
 // cudaFuncSetAttribute is per device: tracked per handle (a handle lives on one device)
-template <int KORD>
+template <int KORD, int FLAGS = 0>
 ctm_status set_layer_attr(ctm_mlp* h) {
-  if (!h->smem_attr_set[KORD]) {
-    CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (!h->smem_attr_set[KORD * 4 + FLAGS]) {
+    CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD, FLAGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctm::kLayerSmem));
-    h->smem_attr_set[KORD] = true;
+    h->smem_attr_set[KORD * 4 + FLAGS] = true;
   }
+  return CTM_OK;
+}
+
+template <int KORD, int FLAGS>
+ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& ahi, const CUtensorMap& alo,
+                               const CUtensorMap& bhi, const CUtensorMap& blo, const ctm::LayerParams& lp,
+                               cudaStream_t st) {
+  ctm_status s = set_layer_attr<KORD, FLAGS>(h);
+  if (s != CTM_OK) return s;
+  ctm::jet_layer_kernel<KORD, FLAGS><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(ahi, alo, bhi, blo,
+                                                                                                    lp);
   return CTM_OK;
 }
 
@@ -500,27 +511,22 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     {
       ProfScope ps(h, CTM_KIND_LAYER, 2.0 * n * P * gl.w_in * gl.w_out, st);
       ctm_status s;
+      const int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
       if (KORD == 2) {
-        s = set_layer_attr<2>(h);
-        if (s != CTM_OK) return s;
-        ctm::jet_layer_kernel<2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
-                                                                                              mb_hi, mb_lo, lp);
+        switch (flags) {
+          case 0: s = launch_layer_kernel<2, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
+          case 1: s = launch_layer_kernel<2, 1>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
+          case 2: s = launch_layer_kernel<2, 2>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
+          default: s = launch_layer_kernel<2, 3>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
+        }
       } else if (KORD == 4) {
-        s = set_layer_attr<4>(h);
-        if (s != CTM_OK) return s;
-        ctm::jet_layer_kernel<4><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(*gl.a_hi, *gl.a_lo,
-                                                                                              mb_hi, mb_lo, lp);
+        s = launch_layer_kernel<4, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
       } else if (KORD == ctm::kNest) {
-        s = set_layer_attr<ctm::kNest>(h);
-        if (s != CTM_OK) return s;
-        ctm::jet_layer_kernel<ctm::kNest><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
-            *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp);
+        s = launch_layer_kernel<ctm::kNest, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
       } else {
-        s = set_layer_attr<ctm::kStd2>(h);
-        if (s != CTM_OK) return s;
-        ctm::jet_layer_kernel<ctm::kStd2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
-            *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp);
+        s = launch_layer_kernel<ctm::kStd2, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
       }
+      if (s != CTM_OK) return s;
     }
     ++launches;
     if (li == 0 && after_first) CTM_CUDA(cudaEventRecord(after_first, st));
@@ -861,13 +867,11 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     lp.ldzi = Kin;
     const int64_t n_tiles = (N + T.ppt - 1) / T.ppt;
     const int64_t grid = 2 * std::min<int64_t>(n_tiles * (lp.m_tiles / 2), h->sm_count / 2);
-    s = set_layer_attr<ctm::kBwd2>(h);
-    if (s != CTM_OK) return s;
     {
       ProfScope ps(h, CTM_KIND_BWD, 2.0 * N * P * h->widths[l - 1] * h->widths[l], st);
       ++h->last_launches;
-      ctm::jet_layer_kernel<ctm::kBwd2><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(
-          h->mapAT_hi[l - 2], h->mapAT_lo[l - 2], mb_hi, mb_lo, lp);
+      s = launch_layer_kernel<ctm::kBwd2, 0>(h, grid, h->mapAT_hi[l - 2], h->mapAT_lo[l - 2], mb_hi, mb_lo, lp, st);
+      if (s != CTM_OK) return s;
     }
     cur ^= 1;
   }

@@ -126,7 +126,12 @@ __device__ __forceinline__ float warp_sum(float v) {
 // two epilogue warp groups at a jet boundary `split`: part 1 = the primal and middle slots
 // [1, split), part 2 = middle slots [split, ..) and the top; the partial collapsed sum of
 // part 1 reaches part 2 through xacc (this thread's slot) and the named barrier bar_id.
-template <int KORD>
+// FLAGS (compile time, K=2 only): kFlagWeighted = collapse sum_r w_r z1_r^2 with the smem
+// weights; kFlagSaveZ = also store the pre-activations (grad mode). The plain operators
+// compile to the loop without either.
+constexpr int kFlagWeighted = 1, kFlagSaveZ = 2;
+
+template <int KORD, int FLAGS = 0>
 __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
                                                float wo, const float* jw, int part, int split, float* xacc,
                                                int bar_id, float& fpart, float& opart) {
@@ -143,8 +148,9 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   fpart = (part == 2) ? 0.f : wo * t;
   opart = 0.f;
   if (!p.readout && part != 2) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
-  float* zp = p.z_out ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
-  if (zp && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
+  constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
+  float* zp = kSaveZ ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
+  if (kSaveZ && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
   uint16_t* ph = p.out_hi + (size_t)(row + mb) * ld + m;
   uint16_t* pl = p.out_lo + (size_t)(row + mb) * ld + m;
   // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
@@ -152,12 +158,12 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   float acc = 0.f;            // the collapsed sum over directions (standard: sum_r h2_r at readout)
   float z1 = 0.f, z2 = 0.f;   // K=4 jet state
   int which = 0, jj = (KORD == 4) ? (mb - 1) / 3 : mb - 1;
-  const bool wsum = (KORD == 2) && p.weighted;
+  constexpr bool wsum = (KORD == 2) && (FLAGS & kFlagWeighted) != 0;
   auto middle = [&](float z) {
     float h;
     if (KORD == 2) {
       h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
-      if (wsum)
+      if constexpr (wsum)
         acc = fmaf(jw[jj++] * z, z, acc);  // sum_r w_r z_{1,r}^2
       else
         acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
@@ -189,7 +195,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     if (!p.readout) store_pair(ph, pl, 0, h);
     ph += ld;
     pl += ld;
-    if (zp) {
+    if constexpr (kSaveZ) {
       *zp = z;
       zp += p.ldz;
     }
@@ -231,7 +237,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float zt = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
   ptx::tmem_ld_wait();
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
-  if (zp) *zp = zt;
+  if constexpr (kSaveZ) *zp = zt;
   opart = wo * top;
   if (!p.readout) store_pair(ph, pl, 0, top);
 }
@@ -501,7 +507,7 @@ __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_p
 //            two TMEM accumulators; commits multicast to both CTAs (empty_bar, tmem_full);
 //   warps 2-9 epilogue on this CTA's 128 accumulator lanes; releases a buffer with a
 //            remote arrive on the leader's tmem_empty (8 warps x 2 CTAs).
-template <int KORD>
+template <int KORD, int FLAGS = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     jet_layer_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                      const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
@@ -658,7 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       } else if (p.pts_per_tile == 1) {
         // one point per tile: both warp groups share it (split at a jet / pair boundary)
         float fpart, opart;
-        epilogue_point<KORD>(p, tbase, row0, m, bias, wo, jw, g + 1, split, xacc + (local & 1u) * kBM + m_local,
+        epilogue_point<KORD, FLAGS>(p, tbase, row0, m, bias, wo, jw, g + 1, split, xacc + (local & 1u) * kBM + m_local,
                              2 + q, fpart, opart);
         if (p.readout) {
           const float v = warp_sum(g == 0 ? fpart : opart);
@@ -667,7 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       } else {
         for (int pt = g; pt < npts; pt += 2) {
           float fpart, opart;
-          epilogue_point<KORD>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, 0, 0,
+          epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, 0, 0,
                                nullptr, 0, fpart, opart);
           if (p.readout) {
             fpart = warp_sum(fpart);
