@@ -48,5 +48,17 @@ run("C1 standard Taylor mode", 50, lambda m, X: m.laplacian_standard(X), lambda 
 Vg = np.random.default_rng(7).standard_normal((N, 16, 5)).astype(np.float32)
 run("stochastic biharmonic S=16", 5, lambda m, X: m.stochastic_biharmonic(X, V=torch.from_numpy(Vg).cuda()),
     lambda n, X: O.stochastic_biharmonic(n, X, Vg.astype(np.float64)))
+run("C4 biharmonic, nested Laplacians", 5, lambda m, X: m.biharmonic_nested(X), lambda n, X: O.biharmonic(n, X))
+sx = None
+
+
+def _pw_gpu(m, X):
+    global sx
+    from synth import sigma_field
+    sx = sigma_field(X.cpu().numpy(), 50)
+    return m.weighted_laplacian_pointwise(X, torch.from_numpy(sx).cuda())
+
+
+run("C2 weighted, sigma(x)", 50, _pw_gpu, lambda n, X: O.weighted_laplacian_pointwise(n, X, sx.astype(np.float64)))
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(res, open(os.path.join(ROOT, "gpurun_out", "parity_sweep.json"), "w"), indent=1)
