@@ -130,7 +130,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
-  bool smem_attr_set[32] = {};  // per (KORD, FLAGS) kernel instance
+  bool smem_attr_set[64] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
   std::vector<uint16_t*> WThi, WTlo;        // W_l^T bf16 pairs [wpad[l-1], wpad[l]], l = 2..L-1
@@ -314,10 +314,10 @@ struct ProfScope {
 // cudaFuncSetAttribute is per device: tracked per handle (a handle lives on one device)
 template <int KORD, int FLAGS = 0>
 ctm_status set_layer_attr(ctm_mlp* h) {
-  if (!h->smem_attr_set[KORD * 4 + FLAGS]) {
+  if (!h->smem_attr_set[KORD * 8 + FLAGS]) {
     CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD, FLAGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctm::kLayerSmem));
-    h->smem_attr_set[KORD * 4 + FLAGS] = true;
+    h->smem_attr_set[KORD * 8 + FLAGS] = true;
   }
   return CTM_OK;
 }
@@ -328,7 +328,7 @@ ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& ahi,
                                cudaStream_t st) {
   ctm_status s = set_layer_attr<KORD, FLAGS>(h);
   if (s != CTM_OK) return s;
-  ctm::jet_layer_kernel<KORD, FLAGS><<<(unsigned)grid, ctm::kLayerThreads, ctm::kLayerSmem, st>>>(ahi, alo, bhi, blo,
+  ctm::jet_layer_kernel<KORD, FLAGS><<<(unsigned)grid, ctm::layer_threads<KORD, FLAGS>(), ctm::kLayerSmem, st>>>(ahi, alo, bhi, blo,
                                                                                                     lp);
   return CTM_OK;
 }
@@ -511,9 +511,13 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     {
       ProfScope ps(h, CTM_KIND_LAYER, 2.0 * n * P * gl.w_in * gl.w_out, st);
       ctm_status s;
-      const int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
+      int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
+      if (KORD == 2 && flags == 0 && pl.ppt >= 8) flags = ctm::kFlagWide;
       if (KORD == 2) {
         switch (flags) {
+          case ctm::kFlagWide:
+            s = launch_layer_kernel<2, ctm::kFlagWide>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+            break;
           case 0: s = launch_layer_kernel<2, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
           case 1: s = launch_layer_kernel<2, 1>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
           case 2: s = launch_layer_kernel<2, 2>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;

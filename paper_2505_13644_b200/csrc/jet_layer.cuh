@@ -33,7 +33,7 @@ constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
 constexpr int kMaxW = 256;                       // per-direction weights in smem (K=2: R+2 <= 256)
-constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue
+constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue (2 groups)
 constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                            4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxW * 4 + 2 * kBM * 4 /*xacc*/;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
@@ -130,6 +130,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 // weights; kFlagSaveZ = also store the pre-activations (grad mode). The plain operators
 // compile to the loop without either.
 constexpr int kFlagWeighted = 1, kFlagSaveZ = 2;
+// kFlagWide (plain K=2 only): 4 epilogue warp groups instead of 2, chosen by the host when a
+// tile holds >= 8 points (small P: the epilogue, not the MMA, bounds the tile).
+constexpr int kFlagWide = 4;
 
 template <int KORD, int FLAGS = 0>
 __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
@@ -507,8 +510,21 @@ __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_p
 //            two TMEM accumulators; commits multicast to both CTAs (empty_bar, tmem_full);
 //   warps 2-9 epilogue on this CTA's 128 accumulator lanes; releases a buffer with a
 //            remote arrive on the leader's tmem_empty (8 warps x 2 CTAs).
+// Epilogue warp groups (4 warps each, one per TMEM lane quadrant) of a kernel instance. The
+// plain K=2 rule is light enough to run with 4 groups (576 threads within the 113-register
+// budget), which doubles the epilogue's point throughput when many small points share a
+// tile (randomized S=8: +15%); with 4 points per tile (C1) 2 groups are faster.
+template <int KORD, int FLAGS>
+__host__ __device__ constexpr int epi_groups() {
+  return (FLAGS & kFlagWide) ? 4 : 2;
+}
+template <int KORD, int FLAGS>
+__host__ __device__ constexpr int layer_threads() {
+  return 64 + 128 * epi_groups<KORD, FLAGS>();
+}
+
 template <int KORD, int FLAGS = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, FLAGS>(), 1)
     jet_layer_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                      const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
                      const LayerParams p) {
@@ -523,6 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
   float* xacc = jw + kMaxW;                                                 // [2][128] split-point partials
 
+  constexpr int EG = epi_groups<KORD, FLAGS>();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -544,7 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tmem_full_bar[b], 1);
-      ptx::mbar_init(&tmem_empty_bar[b], 16);  // 8 epilogue warps in each CTA of the pair
+      ptx::mbar_init(&tmem_empty_bar[b], 8 * EG);  // 4 EG epilogue warps in each CTA of the pair
     }
     ptx::fence_mbar_init();
   }
@@ -643,12 +660,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
       if (KORD == kBwd2) {
-        for (int pt = g; pt < npts; pt += 2)
+        for (int pt = g; pt < npts; pt += EG)
           epilogue_bwd2(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);
       } else if (KORD == kNest) {
         // nested biharmonic: a point is never split; with one point per tile (D >= 14)
         // only warp group 0 works on it
-        for (int pt = g; pt < npts; pt += 2) {
+        for (int pt = g; pt < npts; pt += EG) {
           float fpart, opart;
           epilogue_nested_any(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, fpart,
                               opart);
@@ -662,16 +679,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
           }
         }
       } else if (p.pts_per_tile == 1) {
-        // one point per tile: both warp groups share it (split at a jet / pair boundary)
-        float fpart, opart;
-        epilogue_point<KORD, FLAGS>(p, tbase, row0, m, bias, wo, jw, g + 1, split, xacc + (local & 1u) * kBM + m_local,
-                             2 + q, fpart, opart);
-        if (p.readout) {
-          const float v = warp_sum(g == 0 ? fpart : opart);
-          if (lane == 0) red[(q * kMaxPtsPerTile + 0) * 2 + g] = v;
+        // one point per tile: warp groups 0 and 1 share it (split at a jet / pair boundary)
+        if (g < 2) {
+          float fpart, opart;
+          epilogue_point<KORD, FLAGS>(p, tbase, row0, m, bias, wo, jw, g + 1, split,
+                                      xacc + (local & 1u) * kBM + m_local, 2 + q, fpart, opart);
+          if (p.readout) {
+            const float v = warp_sum(g == 0 ? fpart : opart);
+            if (lane == 0) red[(q * kMaxPtsPerTile + 0) * 2 + g] = v;
+          }
         }
       } else {
-        for (int pt = g; pt < npts; pt += 2) {
+        for (int pt = g; pt < npts; pt += EG) {
           float fpart, opart;
           epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, 0, 0,
                                nullptr, 0, fpart, opart);
@@ -690,15 +709,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLayerThreads, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_remote(&tmem_empty_bar[buf], 0);
       if (p.readout) {
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps only
-        for (int j = threadIdx.x - 64; j < npts * 2; j += 256) {
+        asm volatile("bar.sync 1, %0;" ::"r"(128 * EG) : "memory");  // the epilogue warps only
+        for (int j = threadIdx.x - 64; j < npts * 2; j += 128 * EG) {
           const int pj = j >> 1, comp = j & 1;
           const float s = red[(0 * kMaxPtsPerTile + pj) * 2 + comp] + red[(1 * kMaxPtsPerTile + pj) * 2 + comp] +
                           red[(2 * kMaxPtsPerTile + pj) * 2 + comp] + red[(3 * kMaxPtsPerTile + pj) * 2 + comp];
           const int64_t n = n_tile * p.pts_per_tile + pj;
           p.partial[(n * p.m_tiles + m_tile) * 2 + comp] = s;
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // red[] is reused by the next tile
+        asm volatile("bar.sync 1, %0;" ::"r"(128 * EG) : "memory");  // red[] is reused by the next tile
       }
     }
   }
