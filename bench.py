@@ -367,7 +367,8 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as fh_:
             tj = json.load(fh_)
-        traffic = tj.get(args.op, {}).get("dram_bytes_per_launch") if not train else None
+        key = f"{args.op}_S{args.S}" if args.op == "randomized" else args.op
+        traffic = tj.get(key, {}).get("dram_bytes_per_launch")
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
         "frac": (achieved / useful_peak) if achieved else None, "traffic": traffic,
