@@ -186,3 +186,25 @@ def test_sharded_gradients_sum_to_the_full_batch(ctm):
         assert (fw - aw).abs().max().item() / scale < 1e-5
         scale = max(fb.abs().max().item(), 1e-30)
         assert (fb - ab).abs().max().item() / scale < 1e-5
+
+
+def test_full_size_gradient_is_the_sum_of_its_shards(ctm):
+    """C1 at N = 16384 (the training bench's batch): a property that holds at any size —
+    the gradient of the batch equals the accumulated gradients of four quarter batches, up
+    to the fp32 order of the 852k-row reductions (~sqrt(K) u = 6e-5 worst case; GTOL)."""
+    params = mlp_params(widths_for(50), 0)
+    N = 16384
+    X = torch.from_numpy(points(N, 50)).cuda()
+    gop, gf = (torch.from_numpy(t).cuda() / N for t in _gs(N))
+    mlp = _mlp(ctm, params)
+    mlp.laplacian(X)
+    full = mlp.backward(gop, gf)
+    acc = None
+    for q in range(4):
+        sl = slice(q * N // 4, (q + 1) * N // 4)
+        mlp.laplacian(X[sl])
+        acc = mlp.backward(gop[sl], gf[sl], grads=acc, accumulate=acc is not None)
+    for (fw, fb), (aw, ab) in zip(full, acc):
+        for a, b in ((fw, aw), (fb, ab)):
+            scale = max(a.abs().max().item(), 1e-30)
+            assert (a - b).abs().max().item() / scale < GTOL

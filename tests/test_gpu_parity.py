@@ -561,3 +561,57 @@ def test_c1_full_batch_sampled(ctm):
     idx = np.arange(0, N, 512) + (np.arange(32) % 4)
     want, fwant, norm = O.laplacian(onet, X[idx].astype(np.float64), O.O1)
     check(op.cpu()[idx], want, norm, f.cpu()[idx], fwant)
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled
+def _sample_idx(N, k=32):
+    """k points spread over the batch, including tile-boundary positions (offsets 0..3)."""
+    base = np.arange(0, N, max(1, N // k))[:k]
+    return np.unique(np.minimum(base + np.arange(len(base)) % 4, N - 1))
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3-S8", "C3-S32", "C3-S128", "C4", "C4-nested", "sigma-x"])
+def test_full_size_sampled(ctm, cfg):
+    """Every BASELINE config at N = 16384 in the bench's launch configuration (same
+    operator call, same generated directions); the oracle checks a spread sample."""
+    N = 16384
+    D = 5 if cfg.startswith("C4") else 50
+    params, onet = nets(widths_for(D))
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    mlp = gpu_mlp(ctm, params)
+    idx = _sample_idx(N)
+    Xs = X[idx].astype(np.float64)
+    if cfg == "C2":
+        sig = make_sigma(D, D, kind="dense")
+        op, f = mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())
+        want, fw, norm = O.weighted_laplacian(onet, Xs, sig.astype(np.float64))
+    elif cfg.startswith("C3"):
+        S = int(cfg.split("S")[1])
+        op, f = mlp.randomized_laplacian(Xc, S=S, seed=2)
+        V = np.concatenate([O.rademacher(2, int(n), 1, S, D) for n in idx])  # keyed on the global index
+        want, fw, norm = O.randomized_laplacian(onet, Xs, V)
+    elif cfg == "C4":
+        op, f = mlp.biharmonic(Xc)
+        want, fw, norm = O.biharmonic(onet, Xs)
+    elif cfg == "C4-nested":
+        op, f = mlp.biharmonic_nested(Xc)
+        want, fw, norm = O.biharmonic(onet, Xs)
+    else:
+        sx = sigma_field(X, D)
+        op, f = mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())
+        want, fw, norm = O.weighted_laplacian_pointwise(onet, Xs, sx[idx].astype(np.float64))
+    torch.cuda.synchronize()
+    check(op.cpu()[idx], want, norm, f.cpu()[idx], fw)
+
+
+@pytest.mark.parametrize("N", [128, 1000, 4096])
+def test_c1_batch_sweep_sampled(ctm, N):
+    """The C1 batch sweep (BASELINE: N = 128 ... 16384): ragged tile counts per size."""
+    params, onet = nets(C1_WIDTHS)
+    X = points(N, 50)
+    mlp = gpu_mlp(ctm, params)
+    op, f = mlp.laplacian(torch.from_numpy(X).cuda())
+    idx = _sample_idx(N, 24)
+    want, fw, norm = O.laplacian(onet, X[idx].astype(np.float64))
+    check(op.cpu()[idx], want, norm, f.cpu()[idx], fw)
