@@ -35,7 +35,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "collapsed-Taylor Laplacian points/s, D=50 MLP, 1/2/4/8 B200; % TC peak"
-PAPER_PTS_PER_S = 1.0 / 0.33e-3  # 0.33 ms/datum marginal, RTX 6000, PyTorch (context only)
+# The paper's own per-datum times for the same workload on its hardware (context):
+# P:1205 collapsed Taylor 0.33 ms/datum, standard Taylor 0.60 ms/datum (exact Laplacian, D=50 MLP,
+# RTX 6000, PyTorch). No other operator has a published absolute number.
+PAPER_PTS_PER_S = {"laplacian": 1.0 / 0.33e-3, "standard": 1.0 / 0.60e-3}
 
 
 def parse():
@@ -392,12 +395,14 @@ def main():
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak",
-            "vs_baseline": value / PAPER_PTS_PER_S,
-            "vs_baseline_ref": "paper P:1205 collapsed Taylor 0.33 ms/datum marginal on RTX 6000 (context)",
+            "vs_baseline": (value / PAPER_PTS_PER_S[args.op]) if args.op in PAPER_PTS_PER_S else None,
+            "vs_baseline_ref": ("paper P:1205, marginal ms/datum on an RTX 6000, PyTorch (another machine: context)"
+                                if args.op in PAPER_PTS_PER_S else "no published number for this operator"),
             "dtype": "f32 (3xbf16 tensor products, fp32 accumulate)", "data": "synthetic",
             "config": {"workload": wl, "op": args.op, "N_per_gpu": N, "D": D, "widths": widths,
                        "slots_per_point": plan["slots_per_point"], "points_per_tile": plan["points_per_tile"],
-                       "mma_n": plan["mma_n"],
+                       "mma_n": plan["mma_n"], "direction_blocks": plan["blocks"],
+                       "directions_per_block": plan["per_block"],
                        "parallelism": (f"dp{world} (points sharded; gradient all-reduce, one 5 MB NCCL bucket)"
                                        if train else f"dp{world} (points sharded, no collective in step)"),
                        "l2": "flushed between timed steps (256 MiB write, outside the step events); "

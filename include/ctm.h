@@ -28,6 +28,17 @@
  *    cores on bf16 pairs as 3xBF16 (hi*hi + hi*lo + lo*hi, fp32 accumulation); the Taylor
  *    rules run in fp32.  Accuracy target: |op - op_fp64| <= 1e-4 * sum_r
  *    |c_r f_{K,r}|.
+ *  - Direction blocks: a point's R directions (K=4: J jets) may be split into nb
+ *    blocks of rb, each propagated as its own slot group [x0; its directions; its
+ *    partial collapsed top] of P = rb + 2 (K=2), 3 rb + 2 (K=4) or 1 + 2 rb
+ *    (standard mode) slots; the partial tops are summed at the readout. This is exact
+ *    because the top coefficient enters the Taylor rule of Eq. 7 linearly.
+ *    A block must fit one MMA tile (P <= 256); the number of directions is otherwise
+ *    bounded only by memory (N * nb * P < 2^31 slot rows) and, for weighted sums and
+ *    K=4, by 2048 weights per point. The block size depends only on the operator and
+ *    R (never on N), so results stay independent of how a batch is split; it is chosen
+ *    by a cost model unless fixed with ctm_set_direction_block. Grad mode
+ *    (ctm_grad_enable) uses one block per point (P <= 256).
  */
 #ifndef CTM_H
 #define CTM_H
@@ -68,7 +79,7 @@ ctm_status ctm_free_mlp(ctm_mlp_t mlp);
 
 /* Exact Laplacian, Eq. 8 exact case: op[n] = sum_d <d^2 f(x_n), e_d^{(x)2}>.
  *   X [N, D]; op_out [N]; f_out [N] or NULL (f(x_n)).
- * Slots per point P = D + 2 (CTM_EUNSUPPORTED if P > 256). */
+ * Slots per point P = D + 2 (split into direction blocks when that is faster). */
 ctm_status ctm_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                          void *stream);
 
@@ -77,14 +88,14 @@ ctm_status ctm_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out
  * (x0, and per direction x_{1,d}, x_{2,d}); the top coefficients are sliced and
  * summed only at the output. The paper's baseline, exposed to measure the
  * collapsed/standard ratio of Table `tab:benchmark-ratios` on B200.
- * P = 1 + 2D <= 256 (D <= 127), else CTM_EUNSUPPORTED. */
+ * P = 1 + 2D per point, split into direction blocks of 1 + 2 rb slots. */
 ctm_status ctm_laplacian_standard(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                                   void *stream);
 
 /* Weighted Laplacian, Eq. 10 exact case:
  * op[n] = <d^2 f(x_n), sigma sigma^T> = sum_r <d^2 f, s_r^{(x)2}>,
- *   sigma [D, R] (columns s_r; constant across points), R >= 1,
- *   R + 2 <= 256. */
+ *   sigma [D, R] (columns s_r; constant across points), R >= 1 (R > 254 runs
+ *   in direction blocks). */
 ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma,
                                   int32_t R, float *op_out, float *f_out, void *stream);
 
@@ -96,7 +107,8 @@ ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, cons
  *     (top bit set -> -1); CTM_GAUSSIAN = Box-Muller on splitmix64
  *     counters 2i, 2i+1 (parity tests pass Gaussian V explicitly).
  *   point_offset: global index of X[0] (shard-invariant generation), >= 0.
- *   sigma [D, Rv] or NULL (then Rv must equal D). 1 <= S, S + 2 <= 256. */
+ *   sigma [D, Rv] or NULL (then Rv must equal D), Rv <= 256. S >= 1 (direction blocks
+ *   of the S samples; the 1/S scale is applied once at the readout). */
 ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S,
                                     const float *V, ctm_dist dist, uint64_t seed,
                                     int64_t point_offset, const float *sigma, int32_t Rv,
@@ -105,9 +117,16 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, in
 /* Exact biharmonic, Eq. 12 exact case, by collapsed 4th-order Taylor
  * mode through the interpolation family of Eq. `ttc_for_biharm_final`
  * (gamma of Fig. 3): J = D(3D-1)/2 jets collapsed into
- * ONE weighted top slot (P = 3J + 2 <= 256, i.e. D <= 7). */
+ * ONE weighted top slot per direction block (P = 3J + 2 for one block; D <= 7 fits one
+ * tile, larger D runs in blocks of jets). CTM_EUNSUPPORTED for J > 2048 (D > 36). */
 ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                           void *stream);
+
+/* Direction blocks (see Conventions): rb > 0 fixes the directions (K=4: jets) per block
+ * for later operator calls on this handle (clipped to the operator's R); 0 restores the
+ * planner. The value changes the summation order of the collapsed top, not the operator:
+ * results for different rb agree to rounding. Host-side. CTM_EINVAL for NULL or rb < 0. */
+ctm_status ctm_set_direction_block(ctm_mlp_t mlp, int32_t rb);
 
 /* Replace the weights of a loaded MLP (same widths), e.g. after an optimizer step: the
  * library re-derives every weight-dependent array (bf16 pairs, W1^T, the fixed
@@ -127,9 +146,9 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
 /* Weighted Laplacian with a point-dependent sigma (Eq. 10; "sigma can depend on x0",
  * P:686): op[n] = <d^2 f(x_n), sigma(x_n) sigma(x_n)^T> = sum_r <d^2 f(x_n), s_r(x_n)^2>.
  *   sigma_x [N, D, R] device, fp32: sigma(x_n) row-major [D, R] for each point (the
- *   caller evaluates sigma at its points). P = R + 2 <= 256. Layer 1 runs on the tensor
- *   cores as for ctm_randomized_laplacian with explicit V. Errors: CTM_EINVAL (NULL
- *   sigma_x, R < 1), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (R > 254, D > 256). */
+ *   caller evaluates sigma at its points). P = R + 2 (direction blocks for large R). Layer
+ *   1 runs on the tensor cores as for ctm_randomized_laplacian with explicit V. Errors:
+ *   CTM_EINVAL (NULL sigma_x, R < 1), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 256). */
 ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma_x,
                                             int32_t R, float *op_out, float *f_out, void *stream);
 
@@ -141,9 +160,10 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64
  * collapsed: one summed, weighted top coefficient (Eq. 7).
  *   dirs [J, D] (per_point = 0: the same directions for every point; U = W1 u_j is
  *   computed once per call) or [N, J, D] (per_point = 1); weights [J]; device, fp32.
- *   P = J + 2 (K = 2) or 3J + 2 (K = 4) <= 256; per-point K = 4 also needs J*D <= 12288.
+ *   P = J + 2 (K = 2) or 3J + 2 (K = 4) per point, in direction blocks; J <= 2048;
+ *   per-point K = 4 also needs J*D <= 12288.
  * Errors: CTM_EINVAL (NULL dirs/weights, J < 1), CTM_ESHAPE (misaligned),
- * CTM_EUNSUPPORTED (K not 2 or 4, slot cap, D > 256). */
+ * CTM_EUNSUPPORTED (K not 2 or 4, J > 2048, D > 256). */
 ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float *X, int64_t N, int32_t K, int32_t J,
                                const float *dirs, int32_t per_point, const float *weights, float *op_out,
                                float *f_out, void *stream);
@@ -165,7 +185,8 @@ ctm_status ctm_biharmonic_nested(ctm_mlp_t mlp, const float *X, int64_t N, float
  * E<d^4 f, v^4> = 3 Laplacian^2 f, Q1).
  *   V [N, S, D] explicit directions, or NULL: generated in-kernel (Box-Muller on the
  *   splitmix64 counters 2i, 2i+1 of i = ((point_offset+n)*S+s)*D+d).
- *   dist must be CTM_GAUSSIAN. P = 3S + 2 <= 256 (S <= 84). */
+ *   dist must be CTM_GAUSSIAN. P = 3S + 2 per point, in blocks of samples; S <= 2048 and
+ *   S*D <= 12288. */
 ctm_status ctm_stochastic_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S, const float *V,
                                      ctm_dist dist, uint64_t seed, int64_t point_offset, float *op_out,
                                      float *f_out, void *stream);
@@ -207,6 +228,19 @@ const char *ctm_last_error(void);
  * MMA N of the hidden-layer GEMMs. */
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t *launches, int32_t *slots_per_point,
                          int32_t *points_per_tile, int32_t *mma_n);
+
+/* The direction blocks of the last operator call: blocks per point and directions (K=4:
+ * jets) per block; slots_per_point of ctm_last_plan is the slot count of ONE block.
+ * HOST-side. */
+ctm_status ctm_last_blocks(ctm_mlp_t mlp, int32_t *blocks, int32_t *per_block);
+
+/* The planner itself (HOST-only, no device, no handle): for an operator of kind
+ * order = 2 (collapsed K=2), 4 (collapsed K=4) or 3 (standard Taylor mode) with R
+ * directions (jets) and forced_rb as in ctm_set_direction_block, the block split and
+ * tile plan an operator call would use. CTM_EINVAL for a bad order or R < 1;
+ * CTM_EUNSUPPORTED if no block fits a tile. Any output pointer may be NULL. */
+ctm_status ctm_plan_blocks(int32_t order, int32_t R, int32_t forced_rb, int32_t *blocks, int32_t *per_block,
+                           int32_t *slots_per_block, int32_t *points_per_tile, int32_t *mma_n);
 
 /* Per-kernel timing (measurement support for bench.py; off by default).
  * When enabled, every launch of an operator call is bracketed by CUDA events

@@ -45,6 +45,9 @@ ABI = {
     "ctm_last_error": (ctypes.c_char_p, []),
     "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                                      ctypes.POINTER(_I32)]),
+    "ctm_last_blocks": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "ctm_set_direction_block": (ctypes.c_int, [_VP, _I32]),
+    "ctm_plan_blocks": (ctypes.c_int, [_I32, _I32, _I32] + [ctypes.POINTER(_I32)] * 5),
     "ctm_profile_enable": (ctypes.c_int, [_VP, _I32]),
     "ctm_profile_read": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
 }
@@ -92,6 +95,15 @@ def _dev_f32(t: torch.Tensor, device, name: str) -> torch.Tensor:
     if t.data_ptr() % 16:
         t = t.clone()
     return t
+
+
+def plan_blocks(order: int, R: int, forced_rb: int = 0) -> dict:
+    """The library's direction-block planner (host only, no GPU): ``ctm_plan_blocks``."""
+    out = [_I32() for _ in range(5)]
+    _check(lib().ctm_plan_blocks(int(order), int(R), int(forced_rb), *[ctypes.byref(o) for o in out]),
+           "ctm_plan_blocks")
+    keys = ("blocks", "per_block", "slots_per_block", "points_per_tile", "mma_n")
+    return {k: o.value for k, o in zip(keys, out)}
 
 
 ACTIVATIONS = {"tanh": 0, "identity": 1, "square": 2, "sin": 3}  # ctm_activation
@@ -283,7 +295,14 @@ class MLP:
         a, b, c, d = _I32(), _I32(), _I32(), _I32()
         _check(lib().ctm_last_plan(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
                "ctm_last_plan")
-        return {"launches": a.value, "slots_per_point": b.value, "points_per_tile": c.value, "mma_n": d.value}
+        nb, rb = _I32(), _I32()
+        _check(lib().ctm_last_blocks(self._h, ctypes.byref(nb), ctypes.byref(rb)), "ctm_last_blocks")
+        return {"launches": a.value, "slots_per_point": b.value, "points_per_tile": c.value, "mma_n": d.value,
+                "blocks": nb.value, "per_block": rb.value}
+
+    def set_direction_block(self, rb: int = 0):
+        """Fix the directions per block of later calls (0: the library's planner); ctm.h."""
+        _check(lib().ctm_set_direction_block(self._h, int(rb)), "ctm_set_direction_block")
 
     def profile(self, enable: bool = True):
         """Bracket every launch with CUDA events on its stream (see ctm_profile_read)."""

@@ -117,19 +117,22 @@ struct ctm_mlp {
   float* U_bih = nullptr;     // [J, ld1]
   float* c_bih = nullptr;     // [ld1]
   float* w_bih = nullptr;     // [J] jet weights
-  float* w_ones = nullptr;    // [kMaxJets] unit weights (stochastic biharmonic: plain sum over samples)
+  float* w_ones = nullptr;    // [kMaxW] unit weights (stochastic biharmonic: plain sum over samples)
   int J_bih = 0;
   // per-call scratch
   float* U_call = nullptr;
   float* c_call = nullptr;
   size_t U_call_elems = 0, c_call_elems = 0;
+  float* c_blk = nullptr;     // [blocks, ld1] per-block constants of a fixed set split into blocks
+  size_t c_blk_elems = 0;
+  int forced_rb = 0;          // ctm_set_direction_block: directions per block (0 = planner)
   // workspace (bf16 hi, lo planes): see ensure_workspace
   uint16_t* blk[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   size_t blk_elems[4] = {0, 0, 0, 0};
   float* partial = nullptr;
   size_t partial_elems = 0;
   // last plan
-  int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0;
+  int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0, last_nb = 1, last_rb = 0;
   bool smem_attr_set[64] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
@@ -180,7 +183,7 @@ ctm_status free_all(ctm_mlp* h) {
   for (auto& p : h->Wlo) F(p);
   for (auto& p : h->bias) F(p);
   F(h->U_lap); F(h->c_lap); F(h->w_ones); F(h->U_bih); F(h->c_bih); F(h->w_bih);
-  F(h->U_call); F(h->c_call);
+  F(h->U_call); F(h->c_call); F(h->c_blk);
   for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
   F(h->partial);
@@ -333,18 +336,74 @@ ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& ahi,
   return CTM_OK;
 }
 
+// Tile plan of one operator call. A point's R directions (K=4: jets) are split into nb
+// blocks of rb (the last one zero padded); each block is a sub-point of P slots
+// [x0; its directions; its partial collapsed top]. The collapsed top enters the Taylor rule
+// of Eq. 7 linearly and the direction sum is additive, so the partial tops of
+// the blocks sum to the point's top at every layer ("direction blocks");
+// each block repeats the primal. ppt sub-points share one MMA N tile of nmma columns.
 struct Plan {
   int P = 0, ppt = 0, nmma = 0;
+  int nb = 1, rb = 0;
 };
 
-Plan make_plan(int P) {
-  Plan pl;
-  pl.P = P;
+void tile_plan(Plan& pl) {
   int k = 1;
-  while (round_up((k + 1) * P, 16) <= ctm::kMaxN && k + 1 <= ctm::kMaxPtsPerTile) ++k;
+  while (round_up((k + 1) * pl.P, 16) <= ctm::kMaxN && k + 1 <= ctm::kMaxPtsPerTile) ++k;
   pl.ppt = k;
-  pl.nmma = round_up(k * P, 16);
-  return pl;
+  pl.nmma = round_up(k * pl.P, 16);
+}
+
+// slots of a block of rb directions: K=2 rb + 2, K=4 3 rb + 2 (jets of 3), standard 1 + 2 rb
+int block_slots(int KORD, int rb) {
+  return KORD == 4 ? 3 * rb + 2 : KORD == ctm::kStd2 ? 1 + 2 * rb : rb + 2;
+}
+
+// Modelled cost per point (relative units), from the round-1 sweep of the layer kernel over
+// N: a tile of N columns runs at eff(N) = min(1, 2N / (256 + N)) of the
+// tensor-pipe ceiling (the W tile is re-staged per N tile: N = 144 -> 0.72, 208 -> 0.90,
+// >= 240 -> 0.97-1), plus the HBM write of the layer-1 block (0.17 per slot row, C1 ratio).
+double plan_cost(const Plan& pl) {
+  const double eff = std::min(1.0, 2.0 * pl.nmma / (256.0 + pl.nmma));
+  return (double)pl.nb * pl.nmma / pl.ppt / eff + 0.17 * pl.nb * pl.P;
+}
+
+// R directions (jets): forced_rb > 0 fixes the block size; otherwise the cheapest split by
+// plan_cost, keeping one block unless a split is modelled > 3% cheaper. P_fixed > 0 (nested
+// biharmonic): no blocks. Returns P = 0 if no block fits a tile (P <= 256).
+Plan make_plan(int KORD, int R, int forced_rb, bool allow_blocks, int P_fixed = 0) {
+  Plan best;
+  if (P_fixed > 0 || R < 1) {
+    best.P = P_fixed > 0 ? P_fixed : block_slots(KORD, std::max(R, 0));
+    best.rb = std::max(R, 0);
+    if (best.P > ctm::kMaxN) best.P = 0;
+    else tile_plan(best);
+    return best;
+  }
+  auto make = [&](int rb) {
+    Plan pl;
+    pl.rb = rb;
+    pl.nb = (R + rb - 1) / rb;
+    pl.P = block_slots(KORD, rb);
+    if (pl.P > ctm::kMaxN) pl.P = 0;
+    else tile_plan(pl);
+    return pl;
+  };
+  if (!allow_blocks) return make(R);
+  if (forced_rb > 0) return make(std::min(forced_rb, R));
+  const Plan one = make(R);
+  double best_cost = 1e300;
+  for (int nb = 1; nb <= R; ++nb) {
+    const int rb = (R + nb - 1) / nb;
+    if (nb > 1 && (R + rb - 1) / rb != nb) continue;  // same rb as a smaller nb
+    const Plan pl = make(rb);
+    if (pl.P == 0) continue;
+    const double c = plan_cost(pl);
+    if (c < best_cost) best_cost = c, best = pl;
+    if (pl.P <= 8) break;                              // smaller blocks only add primal copies
+  }
+  if (one.P > 0 && plan_cost(one) <= 1.03 * best_cost) return one;
+  return best;
 }
 
 enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST, OP_DSUM, OP_WLAP_X };
@@ -395,15 +454,16 @@ struct LayerIO {
 
 // Layer 1 for fixed direction sets (and the stochastic biharmonic) for points
 // [p0, p0 + n): writes the layer-1 output block into buf.
-ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p0, int64_t n, uint16_t* const* buf,
-                       const float* UT, const float* csum, int R, cudaStream_t st, int& launches,
+ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, int64_t p0, int64_t n,
+                       uint16_t* const* buf, const float* UT, const float* csum, int R, cudaStream_t st, int& launches,
                        float* z_out = nullptr) {
+  const int P = pl.P;
   const int D = h->widths[0], ld1 = h->wpad[1];
   const int threads = std::min(ctm::kSeedThreads, ld1 / 4);
   const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
   const int64_t blocks = n * mchunks;
   if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
-  ProfScope ps(h, CTM_KIND_SEED, (double)n * P * h->widths[1] * 4.0, st);
+  ProfScope ps(h, CTM_KIND_SEED, (double)n * pl.nb * P * h->widths[1] * 4.0, st);
   if (stoch_k4(a)) {
     ctm::SeedStochParams bp{};
     bp.X = a.X + p0 * D;
@@ -416,6 +476,8 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
     bp.w = (a.op == OP_DSUM) ? a.weights : nullptr;
     bp.seed = a.seed;
     bp.point_offset = a.point_offset + p0;
+    bp.blocks = pl.nb;
+    bp.rb = pl.rb;
     bp.out_hi = buf[0];
     bp.out_lo = buf[1];
     bp.act = h->act;
@@ -432,6 +494,8 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, int P, int64_t p
     sp.UT = UT;
     sp.csum = csum;
     sp.R = R;
+    sp.blocks = pl.nb;
+    sp.rb = (KORD == ctm::kNest) ? R : pl.rb;
     sp.out_hi = buf[0];
     sp.out_lo = buf[1];
     sp.act = h->act;
@@ -456,18 +520,19 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
                          int64_t p0, int64_t n, uint16_t* const* in, float scale, cudaStream_t st,
                          cudaEvent_t after_first, int& launches, const std::vector<LayerIO>* io = nullptr) {
   const int P = pl.P;
-  const int64_t rows = n * (int64_t)P;
+  const int64_t nsub = n * pl.nb;  // sub-points (direction blocks) = the kernel's points
+  const int64_t rows = nsub * (int64_t)P;
   if (layers.empty()) {  // a single hidden layer: read the layer-1 block
     const int threads = 256, ppb = threads / 32;
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((n + ppb - 1) / ppb), threads, 0, st>>>(
-        in[0], in[1], h->wpad[1], P, h->widths[1], h->w_out, h->b_out, scale, n, a.op_out + p0,
+        in[0], in[1], h->wpad[1], P, pl.nb, h->widths[1], h->w_out, h->b_out, scale, n, a.op_out + p0,
         a.f_out ? a.f_out + p0 : nullptr, a.op == OP_LAP_STD);
     ++launches;
     if (after_first) CTM_CUDA(cudaEventRecord(after_first, st));
     return CTM_OK;
   }
-  const int64_t n_tiles = (n + pl.ppt - 1) / pl.ppt;
+  const int64_t n_tiles = (nsub + pl.ppt - 1) / pl.ppt;
   uint16_t* const* src = in;
   int dst = 0;
   for (size_t li = 0; li < layers.size(); ++li) {
@@ -487,11 +552,13 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     lp.z_out = io ? (*io)[li].z : nullptr;
     lp.ldz = gl.mpad;
     lp.m_tiles = m_tiles;
-    lp.n_points = n;
+    lp.n_points = nsub;
     lp.P = P;
     lp.pts_per_tile = pl.ppt;
     lp.n_mma = pl.nmma;
     lp.k_iters = gl.kpad / ctm::kBK;
+    lp.blocks = pl.nb;
+    lp.rb = std::max(pl.rb, 1);
     switch (a.op) {
       case OP_SBIH: lp.jet_w = h->w_ones; lp.J = a.S; break;
       case OP_BIH: lp.jet_w = h->w_bih; lp.J = h->J_bih; break;
@@ -500,7 +567,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       default: break;
     }
     if (last) {
-      ctm_status s = ensure(h->partial, h->partial_elems, (size_t)n * m_tiles * 2);
+      ctm_status s = ensure(h->partial, h->partial_elems, (size_t)nsub * m_tiles * 2);
       if (s != CTM_OK) return s;
       lp.readout = 1;
       lp.w_out = h->w_out;
@@ -509,7 +576,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     // persistent CTA pairs: an even grid, at most one CTA per SM
     const int64_t grid = 2 * std::min<int64_t>(n_tiles * (m_tiles / 2), h->sm_count / 2);
     {
-      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * n * P * gl.w_in * gl.w_out, st);
+      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * nsub * P * gl.w_in * gl.w_out, st);
       ctm_status s;
       int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
       if (KORD == 2 && flags == 0 && pl.ppt >= 8) flags = ctm::kFlagWide;
@@ -537,7 +604,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     if (last) {
       ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
       ctm::finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-          h->partial, m_tiles, n, h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr);
+          h->partial, m_tiles, pl.nb, n, h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr);
       ++launches;
     }
     src = io ? (*io)[li].out : h->blk[dst];
@@ -580,36 +647,42 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
                    : (a.op == OP_LAP_STD)                                             ? ctm::kStd2
                    : (a.op == OP_BIH_NEST)                                            ? ctm::kNest
                                                                                       : 2;
-  int P = 0;
+  int R = 0;  // directions (K=4: jets) of the operator
   switch (a.op) {
-    case OP_LAP: P = D + 2; break;
-    case OP_WLAP: P = a.R + 2; break;
-    case OP_RLAP: P = a.S + 2; break;
-    case OP_BIH: P = 3 * h->J_bih + 2; break;
-    case OP_LAP_STD: P = 1 + 2 * D; break;
-    case OP_SBIH: P = 3 * a.S + 2; break;
-    case OP_BIH_NEST: P = 2 + 2 * D + D * (D + 1) / 2; break;
-    case OP_DSUM: P = (a.K == 4 ? 3 : 1) * a.J + 2; break;
-    case OP_WLAP_X: P = a.S + 2; break;
+    case OP_LAP: case OP_LAP_STD: R = D; break;
+    case OP_WLAP: R = a.R; break;
+    case OP_RLAP: case OP_SBIH: case OP_WLAP_X: R = a.S; break;
+    case OP_BIH: R = h->J_bih; break;
+    case OP_DSUM: R = a.J; break;
+    case OP_BIH_NEST: break;
   }
-  if (P > ctm::kMaxN)
-    return fail(CTM_EUNSUPPORTED, "slots per point " + std::to_string(P) + " exceed the cap of 256");
+  // grad mode records one block per point (the backward kernels have no block structure)
+  const bool grad = h->grad && differentiable(a);
+  const Plan pl = make_plan(KORD, R, h->forced_rb, !grad,
+                            a.op == OP_BIH_NEST ? 2 + 2 * D + D * (D + 1) / 2 : 0);
+  if (pl.P == 0)
+    return fail(CTM_EUNSUPPORTED, grad ? "grad mode: slots per point exceed the cap of 256 (one block per point)"
+                                       : "direction block does not fit one tile (slots per block > 256)");
   if (stoch_k4(a) && (int64_t)a.S * D > 12288)
     return fail(CTM_EUNSUPPORTED, "S * D > 12288 for per-point K=4 directions");
-  const Plan pl = make_plan(P);
+  if ((KORD == 4 || a.op == OP_DSUM) && (int64_t)pl.nb * pl.rb > ctm::kMaxW)
+    return fail(CTM_EUNSUPPORTED, "more than 2048 weighted directions (jets) per point");
+  const int P = pl.P;
   h->last_P = pl.P;
   h->last_ppt = pl.ppt;
   h->last_nmma = pl.nmma;
+  h->last_nb = pl.nb;
+  h->last_rb = pl.rb;
   h->last_launches = 0;
   if (a.N == 0) return CTM_OK;
-  if (a.N * (int64_t)P > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "N * slots exceeds 2^31 rows");
+  const int64_t rows_total = a.N * pl.nb * (int64_t)P;
+  if (rows_total > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "N * slots exceeds 2^31 rows");
 
   DeviceGuard g(h->device);
   cudaStream_t st = a.stream;
   int launches = 0;
   ctm_status s;
   // grad mode: record the tape of this call (differentiable operators only)
-  const bool grad = h->grad && differentiable(a);
   h->tape.valid = false;
   std::vector<LayerIO> io;
   if (grad) {
@@ -633,7 +706,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   if (random_k2(a)) {
     // per-point K=2 directions: the input block [x0; u_1..u_S; 0], then layer 1 on the
     // tensor cores like every other layer
-    s = ensure_workspace(h, a.N * (int64_t)P, 1);
+    s = ensure_workspace(h, rows_total, 1);
     if (s != CTM_OK) return s;
     ctm::SeedRandomParams rp{};
     rp.X = a.X;
@@ -647,10 +720,12 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.point_offset = a.point_offset;
     rp.gaussian = a.gaussian;
     rp.v_trans = a.v_trans;
+    rp.blocks = pl.nb;
+    rp.rb = pl.rb;
     rp.out_hi = grad ? tapeB0[0] : h->blk[2][0];
     rp.out_lo = grad ? tapeB0[1] : h->blk[2][1];
     {
-      ProfScope ps(h, CTM_KIND_SEED, (double)a.N * P * h->k1pad * 4.0, st);
+      ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 4.0, st);
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
     }
     ++launches;
@@ -662,11 +737,9 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     // fixed direction sets (or the K=4 stochastic seed): U and the per-feature constant
     const float* UT = h->U_lap;
     const float* csum = h->c_lap;
-    int R = D;
     if (a.op == OP_BIH) {
       UT = h->U_bih;
       csum = h->c_bih;
-      R = h->J_bih;
     } else if (a.op == OP_DSUM && !a.per_point) {  // U = W1 u_j, c = sum_j w_j (W1 u_j)^K for this call
       s = ensure(h->U_call, h->U_call_elems, (size_t)a.J * ld1);
       if (s != CTM_OK) return s;
@@ -680,7 +753,6 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       ++launches;
       UT = h->U_call;
       csum = h->c_call;
-      R = a.J;
     } else if (a.op == OP_WLAP) {  // U = W1 sigma for this call
       s = ensure(h->U_call, h->U_call_elems, (size_t)a.R * ld1);
       if (s != CTM_OK) return s;
@@ -694,14 +766,25 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       ++launches;
       UT = h->U_call;
       csum = h->c_call;
-      R = a.R;
     }
     const float scale = (a.op == OP_SBIH) ? 1.f / (3.f * (float)a.S) : 1.f;  // Eq. 12 stochastic: 1/(3S), Q1
     // Sequential: running the HBM-write-bound seed of one chunk beside the power-capped
     // tensor-core layers of another was measured slower (2.58-2.65 M vs 2.68 M points/s at
     // C1): the two compete for the 1 kW budget rather than for SMs.
-    s = ensure_workspace(h, a.N * (int64_t)P, 1);
+    s = ensure_workspace(h, rows_total, 1);
     if (s != CTM_OK) return s;
+    if (pl.nb > 1 && csum) {  // per-block constants of the fixed set
+      s = ensure(h->c_blk, h->c_blk_elems, (size_t)pl.nb * ld1);
+      if (s != CTM_OK) return s;
+      {
+        ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
+        const float* w = (a.op == OP_BIH) ? h->w_bih : (a.op == OP_DSUM) ? a.weights : nullptr;
+        ctm::block_csum_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(UT, R, ld1, w, KORD == 4 ? 4 : 2, pl.nb, pl.rb,
+                                                                  h->c_blk);
+      }
+      ++launches;
+      csum = h->c_blk;
+    }
     if (grad) {
       // the layer-1 input block B_0 = [x0; u_r; 0] for dW_1 (directions shared by all points)
       ctm::SeedRandomParams rp{};
@@ -716,13 +799,15 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       } else {
         rp.S = a.J, rp.Rv = D, rp.V = a.dirs, rp.ldv = D;
       }
+      rp.blocks = 1;
+      rp.rb = rp.S;
       rp.out_hi = tapeB0[0];
       rp.out_lo = tapeB0[1];
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
       ++launches;
     }
-    s = launch_seed(h, a, KORD, P, 0, a.N, grad ? tapeB1 : h->blk[2], UT, csum, R, st, launches,
-                    grad ? h->tape.Z[1] : nullptr);
+    s = launch_seed(h, a, KORD, pl, 0, a.N, grad ? tapeB1 : h->blk[2], UT, csum, a.op == OP_BIH_NEST ? D : R, st,
+                    launches, grad ? h->tape.Z[1] : nullptr);
     if (s != CTM_OK) return s;
     s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB1 : h->blk[2], scale, st, nullptr, launches,
                       grad ? &io : nullptr);
@@ -866,6 +951,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     lp.k_iters = Mout / ctm::kBK;
     lp.jet_w = jw;
     lp.J = T.J;
+    lp.blocks = 1;
+    lp.rb = std::max(T.J, 1);
     lp.weighted = T.weighted;
     lp.z_in = T.Z[l - 1];
     lp.ldzi = Kin;
@@ -1042,7 +1129,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     LOAD_CUDA(cudaMemcpy(h->eyeD, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
     LOAD_CUDA(cudaMalloc(&h->U_lap, sizeof(float) * (size_t)D * ld1));
     LOAD_CUDA(cudaMalloc(&h->c_lap, sizeof(float) * ld1));
-    if (3 * (D * (3 * D - 1) / 2) + 2 <= ctm::kMaxN) {
+    if (D * (3 * D - 1) / 2 <= ctm::kMaxW) {  // the jet weights of all blocks live in smem
       std::vector<float> dirs, w;
       biharmonic_family(D, dirs, w);
       h->J_bih = (int)w.size();
@@ -1055,7 +1142,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     }
   }
   {
-    std::vector<float> ones(ctm::kMaxJets, 1.f);
+    std::vector<float> ones(ctm::kMaxW, 1.f);
     LOAD_CUDA(cudaMalloc(&h->w_ones, sizeof(float) * ones.size()));
     LOAD_CUDA(cudaMemcpy(h->w_ones, ones.data(), sizeof(float) * ones.size(), cudaMemcpyHostToDevice));
   }
@@ -1127,7 +1214,7 @@ ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, float* op_ou
   ctm_status s = check_common(mlp, X, N, op_out, f_out);
   if (s != CTM_OK) return s;
   if (mlp->J_bih == 0)
-    return fail(CTM_EUNSUPPORTED, "biharmonic needs 3J+2 <= 256 slots, i.e. D <= 7");
+    return fail(CTM_EUNSUPPORTED, "biharmonic needs J = D(3D-1)/2 <= 2048 jets, i.e. D <= 36");
   CallArgs a{OP_BIH, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
   return run(mlp, a);
 }
@@ -1310,6 +1397,37 @@ ctm_status ctm_stochastic_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, i
   CallArgs a{OP_SBIH, X, N, nullptr, 0, S, V, seed, point_offset, mlp->widths[0], 1, op_out, f_out,
              (cudaStream_t)stream};
   return run(mlp, a);
+}
+
+ctm_status ctm_set_direction_block(ctm_mlp_t mlp, int32_t rb) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (rb < 0) return fail(CTM_EINVAL, "rb < 0");
+  mlp->forced_rb = rb;
+  return CTM_OK;
+}
+
+ctm_status ctm_last_blocks(ctm_mlp_t mlp, int32_t* blocks, int32_t* per_block) {
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (blocks) *blocks = mlp->last_nb;
+  if (per_block) *per_block = mlp->last_rb;
+  return CTM_OK;
+}
+
+ctm_status ctm_plan_blocks(int32_t order, int32_t R, int32_t forced_rb, int32_t* blocks, int32_t* per_block,
+                           int32_t* slots_per_block, int32_t* points_per_tile, int32_t* mma_n) {
+  g_last_error.clear();
+  if ((order != 2 && order != 3 && order != 4) || R < 1 || forced_rb < 0)
+    return fail(CTM_EINVAL, "need order 2, 3 or 4, R >= 1 and forced_rb >= 0");
+  const int KORD = (order == 3) ? ctm::kStd2 : order;
+  const Plan pl = make_plan(KORD, R, forced_rb, true);
+  if (pl.P == 0) return fail(CTM_EUNSUPPORTED, "no direction block fits a tile");
+  if (blocks) *blocks = pl.nb;
+  if (per_block) *per_block = pl.rb;
+  if (slots_per_block) *slots_per_block = pl.P;
+  if (points_per_tile) *points_per_tile = pl.ppt;
+  if (mma_n) *mma_n = pl.nmma;
+  return CTM_OK;
 }
 
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t* launches, int32_t* slots_per_point, int32_t* points_per_tile,

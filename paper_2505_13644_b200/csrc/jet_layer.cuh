@@ -32,7 +32,7 @@ constexpr int kBTileBytes = (kMaxN / 2) * kBK * 2;  // 8 KB: a CTA of the pair s
 constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
-constexpr int kMaxW = 256;                       // per-direction weights in smem (K=2: R+2 <= 256)
+constexpr int kMaxW = 2048;                      // per-direction weights in smem (all blocks of a point)
 constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue (2 groups)
 constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                            4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxW * 4 + 2 * kBM * 4 /*xacc*/;
@@ -82,6 +82,8 @@ __device__ __forceinline__ ActD act_derivs(int act, float z) {
   return r;
 }
 
+// Kept at 128 bytes: one more 8-byte word changed ptxas's unrolling of the epilogue and cost
+// 3-5% of layer time (measured A/B, K=4 and K=2 instances).
 struct LayerParams {
   const float* bias;      // [Mpad]
   uint16_t* out_hi;       // [rows, ldo] bf16 pair
@@ -95,8 +97,14 @@ struct LayerParams {
   int k_iters;            // Kpad / kBK
   const float* jet_w;     // K=4: weights of the J jets in the collapsed slot; K=2 if weighted
   int J;                  // K=4: jets; kNest: D; K=2 weighted: directions
-  int weighted;           // K=2: collapse sum_r w_r z_{1,r}^2 (directional sums, Eq. 5 with weights)
-  int act;                // kAct*
+  // Direction blocks: a point's directions are split into `blocks` groups of
+  // `rb` directions, each propagated as its own slot group [x0; its directions; partial top]
+  // ("sub-point"). n_points counts sub-points; sub-point i holds directions
+  // (i % blocks) * rb .. +rb-1 of point i / blocks, so its weights start at jw[(i % blocks) * rb].
+  int blocks;
+  int rb;
+  int16_t weighted;       // K=2: collapse sum_r w_r z_{1,r}^2 (directional sums, Eq. 5 with weights)
+  int16_t act;            // kAct*
   float* z_out;           // forward, grad mode: the pre-activations z of every slot (fp32) or nullptr
   int ldz;
   const float* z_in;      // kBwd2: this layer's saved pre-activations (fp32)
@@ -105,6 +113,7 @@ struct LayerParams {
   const float* w_out;     // [Mpad] output-layer weights (zero padded)
   float* partial;         // [n_points, m_tiles, 2]
 };
+static_assert(sizeof(LayerParams) == 128, "LayerParams grew past 128 bytes (see above)");
 
 __device__ __forceinline__ void store_pair(uint16_t* hi, uint16_t* lo, size_t idx, float v) {
   uint16_t h, l;
@@ -119,7 +128,8 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// One point of one tile, for the feature owned by this thread: TMEM columns
+// One point (sub-point) of one tile, for the feature owned by this thread; jw points at
+// the weights of its direction block. TMEM columns
 // [tcol, tcol + P) hold z for slots 0..P-1. Writes the output slots (bf16 pairs) or, on
 // the readout layer, returns w_out*h0 and w_out*(top) for the reduction.
 // part 0: the whole point. A tile holding a single point (P > 128) is split between the
@@ -566,8 +576,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
-  if (KORD == 4 || p.weighted)
-    for (int j = threadIdx.x; j < p.J; j += blockDim.x) jw[j] = p.jet_w[j];
+  if (KORD == 4 || p.weighted)  // all blocks' weights; a padded last block reads zeros
+    for (int j = threadIdx.x; j < p.blocks * p.rb; j += blockDim.x) jw[j] = (j < p.J) ? p.jet_w[j] : 0.f;
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barrier inits and TMEM allocation visible to the pair
   ptx::tc_fence_after();
@@ -654,6 +664,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       const int m = m_tile * kBM + m_local;
       const float bias = p.bias ? p.bias[m] : 0.f;
       const float wo = p.readout ? p.w_out[m] : 0.f;
+      // direction block of the tile's first sub-point (weights offset jbase, see LayerParams)
+      constexpr bool kW = (KORD == 4) || (FLAGS & kFlagWeighted) != 0;  // instances that read jw
+      const int blk0 = (kW && p.blocks > 1) ? (int)((n_tile * p.pts_per_tile) % p.blocks) : 0;
       const int64_t pts_left = p.n_points - n_tile * p.pts_per_tile;
       const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
       ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
@@ -682,7 +695,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         // one point per tile: warp groups 0 and 1 share it (split at a jet / pair boundary)
         if (g < 2) {
           float fpart, opart;
-          epilogue_point<KORD, FLAGS>(p, tbase, row0, m, bias, wo, jw, g + 1, split,
+          const int jbase = blk0 * p.rb;  // one sub-point per tile
+          epilogue_point<KORD, FLAGS>(p, tbase, row0, m, bias, wo, jw + jbase, g + 1, split,
                                       xacc + (local & 1u) * kBM + m_local, 2 + q, fpart, opart);
           if (p.readout) {
             const float v = warp_sum(g == 0 ? fpart : opart);
@@ -692,8 +706,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       } else {
         for (int pt = g; pt < npts; pt += EG) {
           float fpart, opart;
-          epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, jw, 0, 0,
-                               nullptr, 0, fpart, opart);
+          const int jbase = (kW && p.blocks > 1) ? ((blk0 + pt) % p.blocks) * p.rb : 0;
+          epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
+                                      jw + jbase, 0, 0, nullptr, 0, fpart, opart);
           if (p.readout) {
             fpart = warp_sum(fpart);
             opart = warp_sum(opart);

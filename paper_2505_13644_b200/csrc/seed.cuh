@@ -33,15 +33,18 @@ struct SeedParams {
   const float* W1T;      // [D, ld]   (W1 transposed, zero padded columns)
   const float* b1;       // [ld]
   int ld;                // padded width of layer 1 (= output ld)
-  int P;
-  // FIXED directions: z1_r = UT[r, m], csum[m] = sum_r z1^2 (K=2) or sum_j w_j z1^4 (K=4)
+  int P;                 // slots per sub-point (one direction block)
+  // FIXED directions: z1_r = UT[r, m]; csum[b * ld + m] = the sum over the directions r of
+  // block b of z1_r^2 (K=2) or w_r z1_r^4 (K=4)
   const float* UT;       // [R, ld]
-  const float* csum;     // [ld]
+  const float* csum;     // [blocks, ld]
   int R;                 // K=2: number of directions; K=4: number of jets J
-  uint16_t* out_hi;      // [N*P, ld] bf16 pair
+  int blocks;            // direction blocks per point (jet_layer.cuh, LayerParams::blocks)
+  int rb;                // directions (K=4: jets) per block; the last block is zero padded
+  uint16_t* out_hi;      // [N*blocks*P, ld] bf16 pair
   uint16_t* out_lo;
   int act;               // kAct*
-  float* z_out;          // K=2, grad mode: pre-activations [N*P, ld] (z0, W1 u_r, 0) or nullptr
+  float* z_out;          // K=2, grad mode (one block): pre-activations [N*P, ld] (z0, W1 u_r, 0) or nullptr
 };
 
 // four adjacent features -> one 8-byte store into each of the hi and lo planes
@@ -56,11 +59,18 @@ __device__ __forceinline__ void seed_store4(uint16_t* hi, uint16_t* lo, size_t i
   *reinterpret_cast<uint2*>(lo + idx) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
 }
 
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
 // Fixed direction sets (K=2: e_d or sigma columns; K=4: the biharmonic family).
 // grid: one block per (point, 4*blockDim-feature chunk); each thread owns 4 adjacent
-// features, so loads are float4 and the bf16-pair stores are 8 bytes wide.
+// features, so loads are float4 and the bf16-pair stores are 8 bytes wide. Direction
+// block b of the point gets its own slot group [h0; its directions; its partial top], with
+// zero rows for the padding of the last block.
 template <int KORD>
-__global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedParams p) {
+// (min blocks per SM: the register budget of the single-block kernel, which this store-bound
+// kernel needs for its occupancy: 40 registers for K=2 / standard, 48 for K=4 / nested)
+__global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6 : 5)
+    seed_layer_kernel(const SeedParams p) {
   __shared__ float xs[256];
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
@@ -69,10 +79,9 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
   for (int d = threadIdx.x; d < p.D; d += blockDim.x) xs[d] = p.X[n * p.D + d];
   __syncthreads();
   if (m >= p.ld) return;  // ld is a multiple of 128: a thread's 4 features are all in or all out
-  const size_t row0 = (size_t)n * p.P;
-  float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
+  float4 z0 = ldg4(p.b1 + m);
   for (int d = 0; d < p.D; ++d) {
-    const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
+    const float4 w = ldg4(p.W1T + (size_t)d * p.ld + m);
     z0.x = fmaf(w.x, xs[d], z0.x);
     z0.y = fmaf(w.y, xs[d], z0.y);
     z0.z = fmaf(w.z, xs[d], z0.z);
@@ -85,73 +94,90 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
     const ActD A = act_derivs(p.act, zz[i]);  // s, s', s'', s''', s''''
     t[i] = A.d0; d1[i] = A.d1; d2[i] = A.d2; d3[i] = A.d3; d4[i] = A.d4;
   }
-  seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
-  const float4 cs = __ldg(reinterpret_cast<const float4*>(p.csum + m));
+  // one loop over the blocks per rule, so each rule keeps only its own derivatives live
+  // (the K=2 loop runs at the register count, and occupancy, of a single-block kernel)
+#define CTM_BLOCK_BEGIN                                                  \
+  for (int b = 0; b < p.blocks; ++b) {                                   \
+    const size_t row0 = ((size_t)n * p.blocks + b) * p.P;                \
+    const int r0 = b * p.rb;                                             \
+    const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;                  \
+    seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+#define CTM_BLOCK_END }
   if (KORD == kStd2) {
+    CTM_BLOCK_BEGIN
     // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
 #pragma unroll 4
-    for (int r = 0; r < p.R; ++r) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m));
-      const size_t rr = row0 + 1 + 2 * r;
+    for (int r = r0; r < r0 + p.rb; ++r) {
+      const float4 u = (r < r1) ? ldg4(p.UT + (size_t)r * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const size_t rr = row0 + 1 + 2 * (r - r0);
       seed_store4(p.out_hi, p.out_lo, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
       seed_store4(p.out_hi, p.out_lo, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
     }
+    CTM_BLOCK_END
   } else if (KORD == 2) {
-    if (p.z_out) {  // grad mode: the layer-1 pre-activations for the backward pass
+    if (p.z_out) {  // grad mode (one block): the layer-1 pre-activations for the backward pass
+      const size_t row0 = (size_t)n * p.P;
       *reinterpret_cast<float4*>(p.z_out + row0 * p.ld + m) = z0;
       for (int r = 0; r < p.R; ++r)
-        *reinterpret_cast<float4*>(p.z_out + (row0 + 1 + r) * p.ld + m) =
-            __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m));
+        *reinterpret_cast<float4*>(p.z_out + (row0 + 1 + r) * p.ld + m) = ldg4(p.UT + (size_t)r * p.ld + m);
       *reinterpret_cast<float4*>(p.z_out + (row0 + 1 + p.R) * p.ld + m) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    CTM_BLOCK_BEGIN
     // batches of 4 rows: the 4 loads of U are in flight together (latency, not bandwidth,
     // bounded this loop when each load fed its stores one at a time)
-    int r = 0;
-    for (; r + 4 <= p.R; r += 4) {
+    int r = r0;
+    for (; r + 4 <= r1; r += 4) {
       float4 u[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)(r + i) * p.ld + m));
+      for (int i = 0; i < 4; ++i) u[i] = ldg4(p.UT + (size_t)(r + i) * p.ld + m);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
+        seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0 + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
                     d1[2] * u[i].z, d1[3] * u[i].w);
     }
-    for (; r < p.R; ++r) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)r * p.ld + m));
-      seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
+    for (; r < r1; ++r) {
+      const float4 u = ldg4(p.UT + (size_t)r * p.ld + m);
+      seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
                   d1[3] * u.w);
     }
+    for (; r < r0 + p.rb; ++r) seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0) * p.ld + m, 0.f, 0.f, 0.f, 0.f);
     // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
-    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + p.R) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
+    const float4 cs = ldg4(p.csum + (size_t)b * p.ld + m);
+    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + p.rb) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
                 d2[3] * cs.w);
+    CTM_BLOCK_END
   } else if (KORD == kNest) {
-    // nested biharmonic, layer 1: g_a = W1[:, a] = UT[a] and H = L = Q = 0 at the input,
-    // so h_a = s' g_a, H'_ab = s'' g_a g_b, L'_a = s''' g_a |g|^2, Q' = s'''' |g|^4 (the
-    // epilogue rule of jet_layer.cuh with H = L = Q = 0); |g|^2 = csum.
+    // nested biharmonic, layer 1 (one block): g_a = W1[:, a] = UT[a] and H = L = Q = 0 at
+    // the input, so h_a = s' g_a, H'_ab = s'' g_a g_b, L'_a = s''' g_a |g|^2,
+    // Q' = s'''' |g|^4 (the epilogue rule of jet_layer.cuh with H = L = Q = 0); |g|^2 = csum.
+    const size_t row0 = (size_t)n * p.P;
+    seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    const float4 cs = ldg4(p.csum + m);
     size_t r = row0 + 1;
     for (int a = 0; a < p.R; ++a, ++r) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)a * p.ld + m));
+      const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
       seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
     }
     for (int a = 0; a < p.R; ++a) {
-      const float4 ua = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)a * p.ld + m));
-      for (int b = a; b < p.R; ++b, ++r) {
-        const float4 ub = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)b * p.ld + m));
-        seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d2[0] * ua.x * ub.x, d2[1] * ua.y * ub.y,
-                    d2[2] * ua.z * ub.z, d2[3] * ua.w * ub.w);
+      const float4 ua = ldg4(p.UT + (size_t)a * p.ld + m);
+      for (int c = a; c < p.R; ++c, ++r) {
+        const float4 uc = ldg4(p.UT + (size_t)c * p.ld + m);
+        seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y,
+                    d2[2] * ua.z * uc.z, d2[3] * ua.w * uc.w);
       }
     }
     for (int a = 0; a < p.R; ++a, ++r) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)a * p.ld + m));
+      const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
       seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
                   d3[3] * u.w * cs.w);
     }
     seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
                 d4[3] * cs.w * cs.w);
   } else {
-    for (int j = 0; j < p.R; ++j) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(p.UT + (size_t)j * p.ld + m));
+    CTM_BLOCK_BEGIN
+    for (int j = r0; j < r0 + p.rb; ++j) {
+      const float4 u = (j < r1) ? ldg4(p.UT + (size_t)j * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float z[4] = {u.x, u.y, u.z, u.w};
       float h1[4], h2[4], h3[4];
 #pragma unroll
@@ -160,15 +186,19 @@ __global__ void __launch_bounds__(kSeedThreads) seed_layer_kernel(const SeedPara
         h2[i] = d2[i] * z[i] * z[i];                // h2 (z2 = 0)
         h3[i] = d3[i] * z[i] * z[i] * z[i];         // h3 (z2 = z3 = 0)
       }
-      const size_t r = row0 + 1 + 3 * j;
+      const size_t r = row0 + 1 + 3 * (j - r0);
       seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
       seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
       seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
     }
-    // sum_w h4 = tanh'''' * sum_j w_j z1_j^4   (z2 = z3 = z4 = 0)
-    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + 3 * p.R) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
+    // sum_w h4 = tanh'''' * sum_j w_j z1_j^4 over the block's jets   (z2 = z3 = z4 = 0)
+    const float4 cs = ldg4(p.csum + (size_t)b * p.ld + m);
+    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + 3 * p.rb) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
                 d4[3] * cs.w);
+    CTM_BLOCK_END
   }
+#undef CTM_BLOCK_BEGIN
+#undef CTM_BLOCK_END
 }
 
 // Stochastic biharmonic (Eq. 12 stochastic), layer 1 in fp32 on the CUDA
@@ -188,7 +218,9 @@ struct SeedStochParams {
   const float* w;        // [S] weights of the collapsed sum, or nullptr (all 1)
   uint64_t seed;
   int64_t point_offset;
-  uint16_t* out_hi;      // [N*(3S+2), ld]
+  int blocks;            // sample blocks per point, `rb` samples each (last one zero padded)
+  int rb;
+  uint16_t* out_hi;      // [N*blocks*(3rb+2), ld]
   uint16_t* out_lo;
   int act;
 };
@@ -213,8 +245,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   }
   __syncthreads();
   if (m >= p.ld) return;
-  const int P = 3 * p.S + 2;
-  const size_t row0 = (size_t)n * P;
+  const int P = 3 * p.rb + 2;  // slots per block
   float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
   for (int d = 0; d < p.D; ++d) {
     const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
@@ -224,39 +255,45 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
     z0.w = fmaf(w.w, xs[d], z0.w);
   }
   const float zz[4] = {z0.x, z0.y, z0.z, z0.w};
-  float t[4], d1[4], d2[4], d3[4], d4[4], acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float t[4], d1[4], d2[4], d3[4], d4[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const ActD A = act_derivs(p.act, zz[i]);
     t[i] = A.d0; d1[i] = A.d1; d2[i] = A.d2; d3[i] = A.d3; d4[i] = A.d4;
   }
-  seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
-  for (int s = 0; s < p.S; ++s) {
-    float z[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int d = 0; d < p.D; ++d) {
-      const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
-      const float v = vsh[s * p.D + d];
-      z[0] = fmaf(w.x, v, z[0]);
-      z[1] = fmaf(w.y, v, z[1]);
-      z[2] = fmaf(w.z, v, z[2]);
-      z[3] = fmaf(w.w, v, z[3]);
-    }
-    float h1[4], h2[4], h3[4];
+  for (int b = 0; b < p.blocks; ++b) {
+    const size_t row0 = ((size_t)n * p.blocks + b) * P;
+    seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s = b * p.rb; s < (b + 1) * p.rb; ++s) {
+      float z[4] = {0.f, 0.f, 0.f, 0.f};
+      if (s < p.S) {
+        for (int d = 0; d < p.D; ++d) {
+          const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
+          const float v = vsh[s * p.D + d];
+          z[0] = fmaf(w.x, v, z[0]);
+          z[1] = fmaf(w.y, v, z[1]);
+          z[2] = fmaf(w.z, v, z[2]);
+          z[3] = fmaf(w.w, v, z[3]);
+        }
+      }
+      float h1[4], h2[4], h3[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float z2 = z[i] * z[i];
-      h1[i] = d1[i] * z[i];
-      h2[i] = d2[i] * z2;
-      h3[i] = d3[i] * z2 * z[i];
-      acc[i] = fmaf(p.w ? p.w[s] * z2 : z2, z2, acc[i]);
+      for (int i = 0; i < 4; ++i) {
+        const float z2 = z[i] * z[i];
+        h1[i] = d1[i] * z[i];
+        h2[i] = d2[i] * z2;
+        h3[i] = d3[i] * z2 * z[i];
+        acc[i] = fmaf((p.w && s < p.S) ? p.w[s] * z2 : z2, z2, acc[i]);
+      }
+      const size_t r = row0 + 1 + 3 * (size_t)(s - b * p.rb);
+      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+      seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+      seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
     }
-    const size_t r = row0 + 1 + 3 * (size_t)s;
-    seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
-    seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
-    seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+    seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
+                d4[3] * acc[3]);
   }
-  seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
-              d4[3] * acc[3]);
 }
 
 // Randomized directions: the layer-1 INPUT block of the collapsed jet,
@@ -278,7 +315,9 @@ struct SeedRandomParams {
   uint64_t seed;
   int64_t point_offset;
   int gaussian;          // generated directions: 0 Rademacher, 1 standard normal
-  uint16_t* out_hi;
+  int blocks;            // direction blocks per point, `rb` directions each (last one zero padded)
+  int rb;
+  uint16_t* out_hi;      // [N*blocks*(rb+2), ldk]
   uint16_t* out_lo;
 };
 
@@ -294,16 +333,22 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx) {
 __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
   __shared__ float vs[kSeedChunk];
   const int64_t n = blockIdx.x;
-  const int P = p.S + 2;
-  const size_t row0 = (size_t)n * P;
-  const int q4 = p.ldk / 4;  // 4-column groups per row
-  // primal row and the zero top row
+  const int P = p.rb + 2;                       // slots per block
+  const size_t pt0 = (size_t)n * p.blocks;      // first sub-point of this point
+  const int q4 = p.ldk / 4;                     // 4-column groups per row
+  // direction s lives in row 1 + s % rb of sub-point s / rb
+  auto dir_row = [&](int s) { return (pt0 + s / p.rb) * P + 1 + s % p.rb; };
+  // every block's primal row and zero top row, and the zero rows of the last block's padding
   for (int c4 = threadIdx.x; c4 < q4; c4 += blockDim.x) {
     float x[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = (4 * c4 + i < p.D) ? p.X[n * p.D + 4 * c4 + i] : 0.f;
-    seed_store4(p.out_hi, p.out_lo, row0 * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
-    seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+    for (int b = 0; b < p.blocks; ++b) {
+      seed_store4(p.out_hi, p.out_lo, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
+      seed_store4(p.out_hi, p.out_lo, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+    }
+    for (int s = p.S; s < p.blocks * p.rb; ++s)
+      seed_store4(p.out_hi, p.out_lo, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
   }
   const int per_chunk = kSeedChunk / p.Rv;
   for (int s0 = 0; s0 < p.S; s0 += per_chunk) {
@@ -340,8 +385,25 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
         }
         u[i] = val;
       }
-      seed_store4(p.out_hi, p.out_lo, (row0 + 1 + s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
+      seed_store4(p.out_hi, p.out_lo, dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
     }
+  }
+}
+
+// csum[b * ld + m] = sum over the directions r of block b (r < R) of w_r UT[r, m]^pow
+// (pow 2 or 4; w nullptr = all ones): the per-block constants of the fixed direction sets.
+__global__ void block_csum_kernel(const float* __restrict__ UT, int R, int ld, const float* __restrict__ w, int pow,
+                                  int blocks, int rb, float* __restrict__ csum) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= ld) return;
+  for (int b = 0; b < blocks; ++b) {
+    float cs = 0.f;
+    for (int r = b * rb; r < (b + 1) * rb && r < R; ++r) {
+      const float u = UT[(size_t)r * ld + m];
+      const float u2 = u * u;
+      cs = fmaf(w ? w[r] : 1.f, pow == 2 ? u2 : u2 * u2, cs);
+    }
+    csum[(size_t)b * ld + m] = cs;
   }
 }
 
@@ -378,39 +440,44 @@ __global__ void prep_sigma_kernel(const float* __restrict__ W1T, int D, int ld, 
   if (csum) csum[m] = cs;
 }
 
-// op[n] = scale * sum_t partial[n, t, 1];  f[n] = b_out + sum_t partial[n, t, 0]   (fixed order)
-__global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, int64_t N, const float* __restrict__ b_out, float scale,
-                                float* __restrict__ op, float* __restrict__ f) {
+// op[n] = scale * sum_b sum_t partial[n*blocks + b, t, 1];  f[n] = b_out + sum_t partial[n*blocks, t, 0]
+// (fixed order; every block carries the primal, its first block gives f)
+__global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, int blocks, int64_t N,
+                                const float* __restrict__ b_out, float scale, float* __restrict__ op,
+                                float* __restrict__ f) {
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float s0 = 0.f, s1 = 0.f;
-  for (int t = 0; t < m_tiles; ++t) {
-    s0 += partial[(n * m_tiles + t) * 2 + 0];
-    s1 += partial[(n * m_tiles + t) * 2 + 1];
-  }
+  const float* pp = partial + n * blocks * m_tiles * 2;
+  for (int t = 0; t < m_tiles; ++t) s0 += pp[t * 2 + 0];
+  for (int i = 0; i < blocks * m_tiles; ++i) s1 += pp[i * 2 + 1];
   op[n] = scale * s1;
   if (f) f[n] = *b_out + s0;
 }
 
 // Readout straight from a layer block (nets with a single hidden layer):
-// one warp per point, lanes over features.
+// one warp per point, lanes over features; `blocks` sub-points of P slots per point.
 // standard != 0: the op is sum_r w_out . h2_r over rows 2, 4, .., P-1 (standard mode)
 __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo, int ld, int P,
-                                     int width, const float* __restrict__ w_out, const float* __restrict__ b_out, float scale,
-                                     int64_t N, float* __restrict__ op, float* __restrict__ f, int standard) {
+                                     int blocks, int width, const float* __restrict__ w_out,
+                                     const float* __restrict__ b_out, float scale, int64_t N, float* __restrict__ op,
+                                     float* __restrict__ f, int standard) {
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
-  const size_t r0 = (size_t)n * P * ld, rt = ((size_t)n * P + P - 1) * ld;
   float s0 = 0.f, s1 = 0.f;
-  for (int m = lane; m < width; m += 32) {
-    s0 = fmaf(w_out[m], ptx::bf16_val(hi[r0 + m]) + ptx::bf16_val(lo[r0 + m]), s0);
-    if (!standard) {
-      s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
-    } else {
-      for (int r = 2; r < P; r += 2) {
-        const size_t ri = ((size_t)n * P + r) * ld;
-        s1 = fmaf(w_out[m], ptx::bf16_val(hi[ri + m]) + ptx::bf16_val(lo[ri + m]), s1);
+  for (int b = 0; b < blocks; ++b) {
+    const size_t sp = (size_t)n * blocks + b;
+    const size_t r0 = sp * P * ld, rt = (sp * P + P - 1) * ld;
+    for (int m = lane; m < width; m += 32) {
+      if (b == 0) s0 = fmaf(w_out[m], ptx::bf16_val(hi[r0 + m]) + ptx::bf16_val(lo[r0 + m]), s0);
+      if (!standard) {
+        s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
+      } else {
+        for (int r = 2; r < P; r += 2) {
+          const size_t ri = (sp * P + r) * ld;
+          s1 = fmaf(w_out[m], ptx::bf16_val(hi[ri + m]) + ptx::bf16_val(lo[ri + m]), s1);
+        }
       }
     }
   }

@@ -118,7 +118,8 @@ def test_laplacian_standard_mode_parity(ctm, widths, N):
     X = points(N, widths[0])
     mlp = gpu_mlp(ctm, params)
     op, f = mlp.laplacian_standard(torch.from_numpy(X).cuda())
-    assert mlp.last_plan()["slots_per_point"] == 1 + 2 * widths[0]
+    pl = mlp.last_plan()
+    assert pl["slots_per_point"] == 1 + 2 * pl["per_block"] and pl["blocks"] * pl["per_block"] >= widths[0]
     want, fwant, norm = O.laplacian(onet, X.astype(np.float64), O.O1)
     check(op, want, norm, f, fwant)
 
@@ -256,8 +257,9 @@ def test_directional_sum_parity(ctm, K, per_point, widths, N, J):
     op, f = mlp.directional_sum(torch.from_numpy(X).cuda(), K, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())
     want, fwant, norm = O.directional_sum(onet, X.astype(np.float64), K, dirs.astype(np.float64), w.astype(np.float64))
     check(op, want, norm, f, fwant)
-    P = (J if K == 2 else 3 * J) + 2
-    assert mlp.last_plan()["slots_per_point"] == P
+    pl = mlp.last_plan()
+    assert pl["slots_per_point"] == (pl["per_block"] if K == 2 else 3 * pl["per_block"]) + 2
+    assert pl["blocks"] * pl["per_block"] >= J
 
 
 def test_directional_sum_eq15_family_mixed_partial(ctm):
@@ -281,7 +283,7 @@ def test_directional_sum_errors(ctm):
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
         mlp.directional_sum(X, 3, torch.ones(2, 4), torch.ones(2))
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
-        mlp.directional_sum(X, 4, torch.ones(85, 4), torch.ones(85))  # 3J + 2 > 256
+        mlp.directional_sum(X, 4, torch.ones(2049, 4), torch.ones(2049))  # > 2048 weights per point
 
 
 # ------------------------------------------------------------------ other activations (NEXT-4)
@@ -390,7 +392,8 @@ def test_stochastic_biharmonic_parity(ctm, widths, N, S):
     V = gaussian_directions(N, S, widths[0])
     mlp = gpu_mlp(ctm, params)
     op, f = mlp.stochastic_biharmonic(torch.from_numpy(X).cuda(), V=torch.from_numpy(V).cuda())
-    assert mlp.last_plan()["slots_per_point"] == 3 * S + 2
+    pl = mlp.last_plan()
+    assert pl["slots_per_point"] == 3 * pl["per_block"] + 2 and pl["blocks"] * pl["per_block"] >= S
     want, fwant, norm = O.stochastic_biharmonic(onet, X.astype(np.float64), V.astype(np.float64), O.O1)
     check(op, want, norm, f, fwant)
 
@@ -509,22 +512,30 @@ def test_edge_shapes_all_operators(ctm, widths, N):
 
 
 def test_slot_cap_exactly_256(ctm):
-    """P = 256 (one point per tile, MMA N = 256) for the weighted (R = 254) and the
-    randomized (S = 254) Laplacian; P = 257 is refused."""
+    """P = 256 in one block (one point per tile, MMA N = 256) for the weighted (R = 254)
+    and the randomized (S = 254) Laplacian; R = 255 runs in direction blocks, and a forced
+    block of 255 directions (P = 257) is refused."""
     params, onet = nets([6, 32, 32, 1])
     X = points(3, 6)
     Xc = torch.from_numpy(X).cuda()
     mlp = gpu_mlp(ctm, params)
     sig = make_sigma(6, 254, kind="rect")
     want, _, norm = O.weighted_laplacian(onet, X.astype(np.float64), sig.astype(np.float64))
+    mlp.set_direction_block(254)
     check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
-    assert mlp.last_plan() == {"launches": mlp.last_plan()["launches"], "slots_per_point": 256,
-                               "points_per_tile": 1, "mma_n": 256}
+    pl = mlp.last_plan()
+    assert (pl["slots_per_point"], pl["points_per_tile"], pl["mma_n"], pl["blocks"]) == (256, 1, 256, 1)
     V = O.rademacher(8, 0, 3, 254, 6)
     want, _, norm = O.randomized_laplacian(onet, X.astype(np.float64), V)
     check(mlp.randomized_laplacian(Xc, S=254, seed=8)[0], want, norm)
+    sig = make_sigma(6, 255, kind="rect")
+    want, _, norm = O.weighted_laplacian(onet, X.astype(np.float64), sig.astype(np.float64))
+    mlp.set_direction_block(0)
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
+    assert mlp.last_plan()["blocks"] >= 2
+    mlp.set_direction_block(255)
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
-        mlp.weighted_laplacian(Xc, torch.from_numpy(make_sigma(6, 255, kind="rect")).cuda())
+        mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())
 
 
 def test_empty_batch_is_noop(ctm):
@@ -537,10 +548,13 @@ def test_empty_batch_is_noop(ctm):
 def test_errors_are_status_codes(ctm):
     params, _ = nets([8, 16, 1])
     mlp = gpu_mlp(ctm, params)
+    mlp.set_direction_block(300)
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
-        mlp.biharmonic(torch.zeros(2, 8).cuda())  # D = 8 > 7: 3J + 2 > 256
+        mlp.randomized_laplacian(torch.zeros(2, 8).cuda(), S=300)  # one block of 302 slots
+    mlp.set_direction_block(0)
+    p38, _ = nets([38, 16, 1])
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
-        mlp.randomized_laplacian(torch.zeros(2, 8).cuda(), S=255)
+        gpu_mlp(ctm, p38).biharmonic(torch.zeros(2, 38).cuda())  # J = 2147 > 2048 jet weights
     X = torch.zeros(9, 8).cuda()
     out = torch.empty(5, device="cuda")
     with pytest.raises(ctm.CTMError, match="ESHAPE"):
@@ -615,3 +629,138 @@ def test_c1_batch_sweep_sampled(ctm, N):
     idx = _sample_idx(N, 24)
     want, fw, norm = O.laplacian(onet, X[idx].astype(np.float64))
     check(op.cpu()[idx], want, norm, f.cpu()[idx], fw)
+
+
+# ------------------------------------------------------------------ direction blocks
+@pytest.mark.parametrize("rb", [7, 16, 49])
+def test_direction_blocks_k2_parity(ctm, rb):
+    """Forced direction blocks (ctm_set_direction_block) on the C1 net: each block carries
+    the primal and a partial collapsed top (linear in Eq. 7), summed at the readout; the
+    last block is zero padded (50 = 7*7 + 1, 3*16 + 2, 49 + 1)."""
+    params, onet = nets(C1_WIDTHS)
+    N = 29
+    X = points(N, 50)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    mlp.set_direction_block(rb)
+    want, fw, norm = O.laplacian(onet, Xd)
+    op, f = mlp.laplacian(Xc)
+    pl = mlp.last_plan()
+    assert (pl["blocks"], pl["per_block"], pl["slots_per_point"]) == (-(-50 // rb), rb, rb + 2)
+    check(op, want, norm, f, fw)
+    check(mlp.laplacian_standard(Xc)[0], want, norm)
+    sig = make_sigma(50, 50, kind="dense")
+    want, _, norm = O.weighted_laplacian(onet, Xd, sig.astype(np.float64))
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
+    V = O.rademacher(4, 0, N, 40, 50)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    check(mlp.randomized_laplacian(Xc, S=40, seed=4)[0], want, norm)
+    sx = sigma_field(X, 50)
+    want, _, norm = O.weighted_laplacian_pointwise(onet, Xd, sx.astype(np.float64))
+    check(mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())[0], want, norm)
+
+
+@pytest.mark.parametrize("rb", [4, 12])
+def test_direction_blocks_k4_parity(ctm, rb):
+    """Blocks of jets for the K=4 operators on the C4 net: the interpolation biharmonic
+    (35 jets, weighted top per block), the stochastic biharmonic (S = 16) and weighted
+    directional sums with shared and per-point directions."""
+    params, onet = nets(C4_WIDTHS)
+    N = 21
+    X = points(N, 5)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    mlp.set_direction_block(rb)
+    want, fw, norm = O.biharmonic(onet, Xd)
+    op, f = mlp.biharmonic(Xc)
+    assert mlp.last_plan()["blocks"] == -(-35 // rb)
+    check(op, want, norm, f, fw)
+    V = gaussian_directions(N, 16, 5)
+    want, _, norm = O.stochastic_biharmonic(onet, Xd, V.astype(np.float64), O.O1)
+    check(mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(V).cuda())[0], want, norm)
+    w = signed_weights(14)
+    for K in (2, 4):
+        for per_point in (False, True):
+            dirs = gaussian_directions(N, 14, 5, seed=6) if per_point else gaussian_directions(1, 14, 5, seed=6)[0]
+            want, _, norm = O.directional_sum(onet, Xd, K, dirs.astype(np.float64), w.astype(np.float64))
+            got = mlp.directional_sum(Xc, K, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())[0]
+            check(got, want, norm)
+
+
+@pytest.mark.parametrize("widths,N", [([5, 12, 1], 6), ([3, 40, 32, 1], 9)])
+def test_direction_blocks_small_nets(ctm, widths, N):
+    """Blocks through the single-hidden-layer readout (layer-1 block read directly) and
+    through the tensor-core layer 1 of per-point directions."""
+    params, onet = nets(widths)
+    D = widths[0]
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    mlp.set_direction_block(2)
+    want, fw, norm = O.laplacian(onet, Xd)
+    op, f = mlp.laplacian(Xc)
+    check(op, want, norm, f, fw)
+    check(mlp.laplacian_standard(Xc)[0], want, norm)
+    V = O.rademacher(5, 0, N, 7, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    check(mlp.randomized_laplacian(Xc, S=7, seed=5)[0], want, norm)
+    want, fw, norm = O.biharmonic(onet, Xd)
+    check(mlp.biharmonic(Xc)[0], want, norm)
+
+
+@pytest.mark.parametrize("case", ["S300", "R400", "std-D130", "bih-D8", "bih-D10", "dsum4-J100"])
+def test_beyond_one_tile(ctm, case):
+    """Operators whose directions no longer fit one MMA tile (the former P <= 256 cap)
+    run in direction blocks chosen by the planner."""
+    if case == "std-D130":
+        widths = [130, 64, 48, 1]
+    elif case.startswith("bih"):
+        widths = [int(case.split("D")[1]), 64, 48, 1]
+    else:
+        widths = [6, 64, 48, 1]
+    params, onet = nets(widths)
+    D = widths[0]
+    N = 5
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    if case == "S300":
+        V = O.rademacher(3, 0, N, 300, D)
+        want, _, norm = O.randomized_laplacian(onet, Xd, V)
+        op = mlp.randomized_laplacian(Xc, S=300, seed=3)[0]
+    elif case == "R400":
+        sig = make_sigma(D, 400, kind="rect")
+        want, _, norm = O.weighted_laplacian(onet, Xd, sig.astype(np.float64))
+        op = mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0]
+    elif case == "std-D130":
+        want, _, norm = O.laplacian(onet, Xd)
+        op = mlp.laplacian_standard(Xc)[0]
+    elif case.startswith("bih"):
+        want, _, norm = O.biharmonic(onet, Xd)
+        op = mlp.biharmonic(Xc)[0]
+    else:
+        dirs = gaussian_directions(N, 100, D, seed=6)
+        w = signed_weights(100)
+        want, _, norm = O.directional_sum(onet, Xd, 4, dirs.astype(np.float64), w.astype(np.float64))
+        op = mlp.directional_sum(Xc, 4, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())[0]
+    assert mlp.last_plan()["blocks"] >= 2
+    check(op, want, norm)
+
+
+def test_direction_blocks_split_batches_bitwise(ctm):
+    """The block split depends on S only, so a batch split into calls is bit-identical
+    (S = 128 runs in blocks by the planner)."""
+    params, _ = nets(C1_WIDTHS)
+    N = 3001
+    X = torch.from_numpy(points(N, 50)).cuda()
+    mlp = gpu_mlp(ctm, params)
+    full = mlp.randomized_laplacian(X, S=128, seed=5)[0].clone()
+    assert mlp.last_plan()["blocks"] > 1
+    parts = torch.cat([mlp.randomized_laplacian(X[:1400], S=128, seed=5)[0].clone(),
+                       mlp.randomized_laplacian(X[1400:], S=128, seed=5, point_offset=1400)[0].clone()])
+    torch.cuda.synchronize()
+    assert torch.equal(full, parts)

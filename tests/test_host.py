@@ -162,3 +162,45 @@ def test_data_parallel_gradient_allreduce_world2_gloo():
     for p in ps:
         p.join(timeout=60)
     assert res[0] < 1e-12 and res[1] < 1e-12, res
+
+
+# ------------------------------------------------------------------ direction-block planner
+def _slots(order, rb):
+    return 3 * rb + 2 if order == 4 else (1 + 2 * rb if order == 3 else rb + 2)
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_direction_block_planner_invariants(order):
+    """ctm_plan_blocks (host only): the blocks cover the R directions with padding only in
+    the last block, a block fits one MMA tile, and the tile holds ppt blocks."""
+    import paper_2505_13644_b200 as ctm
+
+    for R in list(range(1, 70)) + [84, 85, 100, 127, 128, 129, 254, 255, 300, 1000, 2048]:
+        pl = ctm.plan_blocks(order, R)
+        nb, rb, P, ppt, n = (pl[k] for k in ("blocks", "per_block", "slots_per_block", "points_per_tile", "mma_n"))
+        assert nb * rb >= R > (nb - 1) * rb, (R, pl)
+        assert P == _slots(order, rb) and P <= 256
+        assert n % 16 == 0 and ppt * P <= n <= 256 and (ppt + 1) * P > 256 or ppt == 128, (R, pl)
+        assert ctm.plan_blocks(order, R) == pl  # a function of (order, R) only: never of N
+
+
+def test_direction_block_planner_choices():
+    import paper_2505_13644_b200 as ctm
+
+    # C1 (R = D = 50, P = 52, four points in N = 208) stays one block
+    assert ctm.plan_blocks(2, 50)["blocks"] == 1
+    # C3 S = 128 (P = 130 alone in an N = 144 tile) is split into wide-tile blocks
+    pl = ctm.plan_blocks(2, 128)
+    assert pl["blocks"] > 1 and pl["mma_n"] >= 240
+    # C4 biharmonic (J = 35) stays one block of 107 slots
+    assert ctm.plan_blocks(4, 35)["slots_per_block"] == 107
+    # beyond one tile: S = 255 and J = 85 need blocks
+    assert ctm.plan_blocks(2, 255)["blocks"] >= 2 and ctm.plan_blocks(4, 85)["blocks"] >= 2
+    # forced block sizes are honoured (clipped to R); one that does not fit a tile is refused
+    assert ctm.plan_blocks(2, 50, 7) == {"blocks": 8, "per_block": 7, "slots_per_block": 9,
+                                         "points_per_tile": 28, "mma_n": 256}
+    assert ctm.plan_blocks(2, 5, 9)["per_block"] == 5
+    with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
+        ctm.plan_blocks(2, 300, 300)
+    with pytest.raises(ctm.CTMError, match="EINVAL"):
+        ctm.plan_blocks(5, 10)
