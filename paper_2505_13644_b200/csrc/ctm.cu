@@ -1430,6 +1430,18 @@ ctm_status ctm_plan_blocks(int32_t order, int32_t R, int32_t forced_rb, int32_t*
   return CTM_OK;
 }
 
+#ifdef CTM_EXP_STATS
+int ctm_debug_stats(unsigned long long* out, int reset) {  // experiment build only
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, ctm::g_stats, sizeof(ctm::g_stats));
+  if (reset) {
+    static unsigned long long zero[256][8];
+    cudaMemcpyToSymbol(ctm::g_stats, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif
+
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t* launches, int32_t* slots_per_point, int32_t* points_per_tile,
                          int32_t* mma_n) {
   if (!mlp) return fail(CTM_EINVAL, "NULL handle");

@@ -23,6 +23,23 @@
 
 namespace ctm {
 
+// Experiment switches (all off in the product build; scripts/experiments/README.md): a
+// build with -DCTM_EXP_<NAME> isolates one cost of the layer kernel.
+//   NOTMA     MMAs on stale operands (no L2 -> smem traffic)      NOEPI  no epilogue work
+//   NOSTORE   epilogue computes but does not store                 HALFSTORE  stores hi only
+//   L2STORE   same stores into an L2-resident per-CTA scratch      STATS  per-role cycle counters
+#ifdef CTM_EXP_STATS
+__device__ unsigned long long g_stats[256][8];
+#define STAT_T0() const long long t0_ = clock64()
+#define STAT_ADD(i) atomicAdd(&g_stats[blockIdx.x][i], (unsigned long long)(clock64() - t0_))
+#else
+#define STAT_T0()
+#define STAT_ADD(i)
+#endif
+#ifdef CTM_EXP_L2STORE
+__device__ uint16_t g_scratch[256u * 98304u];
+#endif
+
 constexpr int kBM = 128;                         // features per CTA = TMEM lanes (a CTA pair spans 256)
 constexpr int kBK = 32;                          // bf16 K per stage: 64-byte rows, SWIZZLE_64B
 constexpr int kStages = 6;
@@ -117,6 +134,22 @@ static_assert(sizeof(LayerParams) == 128, "LayerParams grew past 128 bytes (see 
 
 __device__ __forceinline__ void store_pair(uint16_t* hi, uint16_t* lo, size_t idx, float v) {
   uint16_t h, l;
+#ifdef CTM_EXP_NOSTORE
+  if (v != 1234.5678f) return;
+#endif
+#ifdef CTM_EXP_L2STORE
+  {
+    const size_t e = (size_t)blockIdx.x * 98304u + (size_t)((((uintptr_t)(hi + idx)) >> 1) % 49152u);
+    ptx::bf16_split(v, h, l);
+    g_scratch[e] = h;
+    g_scratch[e + 49152u] = l;
+    return;
+  }
+#endif
+#ifdef CTM_EXP_HALFSTORE
+  hi[idx] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  return;
+#endif
   ptx::bf16_split(v, h, l);
   hi[idx] = h;
   lo[idx] = l;
@@ -172,7 +205,8 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   float z1 = 0.f, z2 = 0.f;   // K=4 jet state
   int which = 0, jj = (KORD == 4) ? (mb - 1) / 3 : mb - 1;
   constexpr bool wsum = (KORD == 2) && (FLAGS & kFlagWeighted) != 0;
-  auto middle = [&](float z) {
+  bool direct = true;  // experiment BLOCKED: the batch loop stores instead
+  auto middle = [&](float z) -> float {
     float h;
     if (KORD == 2) {
       h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
@@ -205,13 +239,14 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
       }
       which = (which == 2) ? 0 : which + 1;
     }
-    if (!p.readout) store_pair(ph, pl, 0, h);
+    if (!p.readout && direct) store_pair(ph, pl, 0, h);
     ph += ld;
     pl += ld;
     if constexpr (kSaveZ) {
       *zp = z;
       zp += p.ldz;
     }
+    return h;
   };
   const int cnt = me - mb;
   int s = 0;
@@ -219,8 +254,32 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     float v[16];
     ptx::tmem_ld16(tcol + (uint32_t)(mb + s), v);
     ptx::tmem_ld_wait();
+#ifdef CTM_EXP_BLOCKED  // experiment: 8 slots per 16-byte store (rowblock layout; wrong values)
+    direct = false;
+    float hv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) hv[i] = middle(v[i]);
+    if (!p.readout) {
+      uint32_t wh[8], wl[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint16_t h0, l0, h1, l1;
+        ptx::bf16_split(hv[2 * i], h0, l0);
+        ptx::bf16_split(hv[2 * i + 1], h1, l1);
+        wh[i] = h0 | ((uint32_t)h1 << 16);
+        wl[i] = l0 | ((uint32_t)l1 << 16);
+      }
+      const size_t b = ((size_t)((row + mb + s) >> 3) * ld + m) * 8;
+      *reinterpret_cast<uint4*>(p.out_hi + b) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+      *reinterpret_cast<uint4*>(p.out_hi + b + (size_t)ld * 8) = make_uint4(wh[4], wh[5], wh[6], wh[7]);
+      *reinterpret_cast<uint4*>(p.out_lo + b) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+      *reinterpret_cast<uint4*>(p.out_lo + b + (size_t)ld * 8) = make_uint4(wl[4], wl[5], wl[6], wl[7]);
+    }
+    direct = true;
+#else
 #pragma unroll
     for (int i = 0; i < 16; ++i) middle(v[i]);
+#endif
   }
   const int rem = cnt - s;  // 0..15, warp-uniform
   if (rem > 0) {
@@ -496,6 +555,17 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
 // Returns false past the pair's last tile.
 __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_pairs, int64_t n_tiles, int64_t& n,
                                         int& m) {
+#ifdef CTM_EXP_MSPREAD  // experiment: the m_pairs feature tiles of a point group run on m_pairs pairs at once
+  {
+    const int groups = npairs / m_pairs;
+    if (n_tiles >= groups) {
+      if (pair >= groups * m_pairs) return false;
+      n = pair / m_pairs + k * groups;
+      m = pair % m_pairs;
+      return n < n_tiles;
+    }
+  }
+#endif
   if (n_tiles >= npairs) {
     n = pair + (k / m_pairs) * npairs;
     m = (int)(k % m_pairs);
@@ -595,7 +665,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
           const uint32_t s = it % kStages;
           const uint32_t ph = (it / kStages) & 1u;
-          ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
+          {
+            STAT_T0();
+            ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
+            STAT_ADD(0);  // producer waits for a free stage
+          }
+#ifdef CTM_EXP_NOTMA
+          if (rank == 0) ptx::mbar_arrive(&full_bar[s]);
+          continue;
+#endif
           uint8_t* st = smem + s * kStageBytes;
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * (2u * kATileBytes + 2u * b_bytes));
           const int k0 = kb * kBK;
@@ -609,6 +687,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader, one thread)
     if (rank == 0 && lane == 0) {
+#ifdef CTM_EXP_STATS
+      const long long tstart = clock64();
+#endif
       const uint32_t idesc = ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
       uint32_t it = 0, local = 0;
       int64_t nt;
@@ -616,13 +697,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       for (; tile_of(local, pair, npairs, m_pairs, n_tiles, nt, mp); ++local) {
         const uint32_t buf = local & 1u;
         const uint32_t use = local >> 1;
-        ptx::mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
+        {
+          STAT_T0();
+          ptx::mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
+          STAT_ADD(1);  // MMA waits for the epilogue to free an accumulator
+        }
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
         for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
           const uint32_t s = it % kStages;
           const uint32_t ph = (it / kStages) & 1u;
-          ptx::mbar_wait(&full_bar[s], ph);
+          {
+            STAT_T0();
+            ptx::mbar_wait(&full_bar[s], ph);
+            STAT_ADD(2);  // MMA waits for TMA
+          }
           ptx::tc_fence_after();
           const uint32_t a_hi = ptx::smem_u32(smem + s * kStageBytes);
           const uint32_t a_lo = a_hi + kATileBytes;
@@ -643,6 +732,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         }
         ptx::mma_commit_pair(&tmem_full_bar[buf]);  // both CTAs' accumulator halves complete
       }
+#ifdef CTM_EXP_STATS
+      g_stats[blockIdx.x][3] += clock64() - tstart;  // MMA issuer lifetime
+      g_stats[blockIdx.x][7] += local;               // tiles
+#endif
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..9, both CTAs)
@@ -669,9 +762,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       const int blk0 = (kW && p.blocks > 1) ? (int)((n_tile * p.pts_per_tile) % p.blocks) : 0;
       const int64_t pts_left = p.n_points - n_tile * p.pts_per_tile;
       const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);
-      ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
+      {
+        STAT_T0();
+        ptx::mbar_wait(&tmem_full_bar[buf], use & 1u);
+        if (warp == 2 && lane == 0) STAT_ADD(4);  // epilogue waits for an accumulator
+      }
+#ifdef CTM_EXP_STATS
+      const long long tw_ = clock64();
+#endif
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
+#ifdef CTM_EXP_NOEPI
+      if (true) {
+      } else
+#endif
       if (KORD == kBwd2) {
         for (int pt = g; pt < npts; pt += EG)
           epilogue_bwd2(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);
@@ -723,6 +827,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_remote(&tmem_empty_bar[buf], 0);
+#ifdef CTM_EXP_STATS
+      if (lane == 0) atomicAdd(&g_stats[blockIdx.x][5 + (warp == 2 ? 0 : 1)], (unsigned long long)(clock64() - tw_));
+#endif
       if (p.readout) {
         asm volatile("bar.sync 1, %0;" ::"r"(128 * EG) : "memory");  // the epilogue warps only
         for (int j = threadIdx.x - 64; j < npts * 2; j += 128 * EG) {
