@@ -52,6 +52,8 @@ def parse():
                                    "stochastic_biharmonic", "biharmonic_nested", "laplacian_train"],
                     default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
+    ap.add_argument("--direction-block", type=int, default=0,
+                    help="directions per block (ctm_set_direction_block); 0 = the library's planner")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: total CPU seconds spread over the warm-up + timed steps")
@@ -221,6 +223,7 @@ def main():
     N = args.n
     params = mlp_params(widths, 0)
     mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=local)
+    mlp.set_direction_block(args.direction_block)
     # each rank: its own contiguous slice of the global point set (global index rank*N ...)
     X_host = points(N * world, D, 1)[rank * N:(rank + 1) * N]
     X = torch.from_numpy(X_host).to(dev)
