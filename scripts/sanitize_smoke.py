@@ -26,6 +26,16 @@ for widths in ([5, 16, 16, 1], [50, 64, 64, 1]):
     for K in (2, 4):
         outs.append(mlp.directional_sum(X, K, torch.from_numpy(gaussian_directions(1, 3, D)[0]).cuda(), w)[0])
         outs.append(mlp.directional_sum(X, K, torch.from_numpy(gaussian_directions(9, 3, D)).cuda(), w)[0])
+    # direction blocks (forced small blocks: many sub-points, padded last block)
+    mlp.set_direction_block(2)
+    outs += [mlp.laplacian(X)[0], mlp.laplacian_standard(X)[0], mlp.randomized_laplacian(X, S=7, seed=1)[0],
+             mlp.weighted_laplacian(X, torch.from_numpy(sigma(D, D)).cuda())[0]]
+    if D <= 7:
+        outs += [mlp.biharmonic(X)[0], mlp.stochastic_biharmonic(X, S=5, seed=2)[0]]
+    for K in (2, 4):
+        outs.append(mlp.directional_sum(X, K, torch.from_numpy(gaussian_directions(9, 5, D)).cuda(),
+                                        torch.from_numpy(signed_weights(5)).cuda())[0])
+    mlp.set_direction_block(0)
     # differentiable path: forward in grad mode, backward, weight update
     mlp.grad_enable()
     for call in (lambda: mlp.laplacian(X), lambda: mlp.randomized_laplacian(X, S=4, seed=1),
