@@ -28,6 +28,7 @@ namespace ctm {
 //   NOTMA     MMAs on stale operands (no L2 -> smem traffic)      NOEPI  no epilogue work
 //   NOSTORE   epilogue computes but does not store                 HALFSTORE  stores hi only
 //   L2STORE   same stores into an L2-resident per-CTA scratch      STATS  per-role cycle counters
+//   (BLOCKED, MSPREAD: measured variants described in scripts/experiments/README.md)
 #ifdef CTM_EXP_STATS
 __device__ unsigned long long g_stats[256][8];
 #define STAT_T0() const long long t0_ = clock64()
@@ -201,96 +202,95 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   uint16_t* pl = p.out_lo + (size_t)(row + mb) * ld + m;
   // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
   //      standard-mode pairs (z1_r, z2_r) with no collapse
-  float acc = 0.f;            // the collapsed sum over directions (standard: sum_r h2_r at readout)
-  float z1 = 0.f, z2 = 0.f;   // K=4 jet state
-  int which = 0, jj = (KORD == 4) ? (mb - 1) / 3 : mb - 1;
-  constexpr bool wsum = (KORD == 2) && (FLAGS & kFlagWeighted) != 0;
-  bool direct = true;  // experiment BLOCKED: the batch loop stores instead
-  auto middle = [&](float z) -> float {
-    float h;
-    if (KORD == 2) {
-      h = d1 * z;             // h_{1,r} = tanh' z_{1,r}
+  float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
+  int jj = (KORD == 4) ? (mb - 1) / 3 : mb - 1;  // weight index of the first direction / jet
+  auto put = [&](float h) {
+    if (!p.readout) store_pair(ph, pl, 0, h);
+    ph += ld;
+    pl += ld;
+  };
+  if constexpr (KORD == 4) {
+    // jets (z1, z2, z3), read 5 at a time (15 of 16 columns) so each slot's role is a
+    // compile-time index in the unrolled loop
+    auto jet = [&](float z1, float z2, float z3) {
+      put(d1 * z1);
+      put(d2 * z1 * z1 + d1 * z2);
+      put(d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3);
+      const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 + 3.f * d2 * z2 * z2;
+      acc = fmaf(jw[jj], nl, acc);
+      ++jj;
+    };
+    const int nj = (me - mb) / 3;
+    int j = 0;
+    for (; j + 5 <= nj; j += 5) {
+      float v[16];
+      ptx::tmem_ld16(tcol + (uint32_t)(mb + 3 * j), v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 5; ++u) jet(v[3 * u], v[3 * u + 1], v[3 * u + 2]);
+    }
+    for (; j < nj; ++j) {
+      float v[4];
+      ptx::tmem_ld4(tcol + (uint32_t)(mb + 3 * j), v);
+      ptx::tmem_ld_wait();
+      jet(v[0], v[1], v[2]);
+    }
+  } else if constexpr (KORD == kStd2) {
+    // standard mode: per direction (h1_r, h2_r) with no collapse, 8 pairs per 16 columns
+    auto pair = [&](float z1, float z2) {
+      put(d1 * z1);                             // h_{1,r}
+      const float h2 = fmaf(d2 * z1, z1, d1 * z2);  // h_{2,r} = tanh'' z1^2 + tanh' z2 (Eq. 1)
+      acc += h2;
+      put(h2);
+    };
+    const int np = (me - mb) / 2;
+    int j = 0;
+    for (; j + 8 <= np; j += 8) {
+      float v[16];
+      ptx::tmem_ld16(tcol + (uint32_t)(mb + 2 * j), v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pair(v[2 * u], v[2 * u + 1]);
+    }
+    for (; j < np; ++j) {
+      float v[2];
+      ptx::tmem_ld2(tcol + (uint32_t)(mb + 2 * j), v);
+      ptx::tmem_ld_wait();
+      pair(v[0], v[1]);
+    }
+  } else {
+    constexpr bool wsum = (FLAGS & kFlagWeighted) != 0;
+    auto middle = [&](float z) {
+      put(d1 * z);  // h_{1,r} = tanh' z_{1,r}
       if constexpr (wsum)
         acc = fmaf(jw[jj++] * z, z, acc);  // sum_r w_r z_{1,r}^2
       else
         acc = fmaf(z, z, acc);  // sum_r z_{1,r}^2
-    } else if (KORD == kStd2) {
-      if (which == 0) {
-        z1 = z;
-        h = d1 * z1;                    // h_{1,r}
-      } else {
-        h = fmaf(d2 * z1, z1, d1 * z);  // h_{2,r} = tanh'' z1^2 + tanh' z2 (Eq. 1, per direction)
-        acc += h;
+      if constexpr (kSaveZ) {
+        *zp = z;
+        zp += p.ldz;
       }
-      which ^= 1;
-    } else {
-      if (which == 0) {
-        z1 = z;
-        h = d1 * z1;
-      } else if (which == 1) {
-        z2 = z;
-        h = d2 * z1 * z1 + d1 * z2;
-      } else {
-        const float z3 = z;
-        h = d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3;
-        const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 + 3.f * d2 * z2 * z2;
-        acc = fmaf(jw[jj], nl, acc);
-        ++jj;
-      }
-      which = (which == 2) ? 0 : which + 1;
+    };
+    const int cnt = me - mb;
+    int s = 0;
+    for (; s + 16 <= cnt; s += 16) {
+      float v[16];
+      ptx::tmem_ld16(tcol + (uint32_t)(mb + s), v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) middle(v[i]);
     }
-    if (!p.readout && direct) store_pair(ph, pl, 0, h);
-    ph += ld;
-    pl += ld;
-    if constexpr (kSaveZ) {
-      *zp = z;
-      zp += p.ldz;
+    const int rem = cnt - s;  // 0..15, warp-uniform
+    if (rem > 0) {
+      float v[15];
+#pragma unroll
+      for (int i = 0; i < 15; ++i)
+        if (i < rem) v[i] = ptx::tmem_ld1(tcol + (uint32_t)(mb + s + i));
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 15; ++i)
+        if (i < rem) middle(v[i]);
     }
-    return h;
-  };
-  const int cnt = me - mb;
-  int s = 0;
-  for (; s + 16 <= cnt; s += 16) {
-    float v[16];
-    ptx::tmem_ld16(tcol + (uint32_t)(mb + s), v);
-    ptx::tmem_ld_wait();
-#ifdef CTM_EXP_BLOCKED  // experiment: 8 slots per 16-byte store (rowblock layout; wrong values)
-    direct = false;
-    float hv[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) hv[i] = middle(v[i]);
-    if (!p.readout) {
-      uint32_t wh[8], wl[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        uint16_t h0, l0, h1, l1;
-        ptx::bf16_split(hv[2 * i], h0, l0);
-        ptx::bf16_split(hv[2 * i + 1], h1, l1);
-        wh[i] = h0 | ((uint32_t)h1 << 16);
-        wl[i] = l0 | ((uint32_t)l1 << 16);
-      }
-      const size_t b = ((size_t)((row + mb + s) >> 3) * ld + m) * 8;
-      *reinterpret_cast<uint4*>(p.out_hi + b) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
-      *reinterpret_cast<uint4*>(p.out_hi + b + (size_t)ld * 8) = make_uint4(wh[4], wh[5], wh[6], wh[7]);
-      *reinterpret_cast<uint4*>(p.out_lo + b) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
-      *reinterpret_cast<uint4*>(p.out_lo + b + (size_t)ld * 8) = make_uint4(wl[4], wl[5], wl[6], wl[7]);
-    }
-    direct = true;
-#else
-#pragma unroll
-    for (int i = 0; i < 16; ++i) middle(v[i]);
-#endif
-  }
-  const int rem = cnt - s;  // 0..15, warp-uniform
-  if (rem > 0) {
-    float v[15];
-#pragma unroll
-    for (int i = 0; i < 15; ++i)
-      if (i < rem) v[i] = ptx::tmem_ld1(tcol + (uint32_t)(mb + s + i));
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 15; ++i)
-      if (i < rem) middle(v[i]);
   }
   if (part == 1) {  // hand the partial collapsed sum to part 2
     *xacc = acc;
