@@ -331,8 +331,19 @@ ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& ahi,
                                cudaStream_t st) {
   ctm_status s = set_layer_attr<KORD, FLAGS>(h);
   if (s != CTM_OK) return s;
-  ctm::jet_layer_kernel<KORD, FLAGS><<<(unsigned)grid, ctm::layer_threads<KORD, FLAGS>(), ctm::kLayerSmem, st>>>(ahi, alo, bhi, blo,
-                                                                                                    lp);
+  // programmatic dependent launch: the prologue (barriers, TMEM allocation, descriptor
+  // prefetch) overlaps the previous kernel's tail; the kernel waits before reading its input
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(ctm::layer_threads<KORD, FLAGS>());
+  cfg.dynamicSmemBytes = ctm::kLayerSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::jet_layer_kernel<KORD, FLAGS>, ahi, alo, bhi, blo, lp));
   return CTM_OK;
 }
 
@@ -603,8 +614,17 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     if (li == 0 && after_first) CTM_CUDA(cudaEventRecord(after_first, st));
     if (last) {
       ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
-      ctm::finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-          h->partial, m_tiles, pl.nb, n, h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)((n + 255) / 256));
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::finalize_kernel, (const float*)h->partial, m_tiles, pl.nb, n,
+                                  (const float*)h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr));
       ++launches;
     }
     src = io ? (*io)[li].out : h->blk[dst];

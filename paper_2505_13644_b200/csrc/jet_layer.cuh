@@ -524,7 +524,13 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
     float v[16], z[16];
     ptx::tmem_ld16(tcol + (uint32_t)(1 + s), v);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) z[i] = zr[(size_t)(1 + s + i) * ldz];
+    for (int i = 0; i < 16; ++i) {
+#ifdef CTM_EXP_NOZ  // experiment: no saved-Z loads in the adjoint batch loop (wrong values)
+      z[i] = v[i] * 0.5f;
+#else
+      z[i] = zr[(size_t)(1 + s + i) * ldz];
+#endif
+    }
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < 16; ++i) one(v[i], z[i], s + i);
@@ -652,6 +658,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
   ptx::cluster_sync();  // barrier inits and TMEM allocation visible to the pair
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: the prologue above overlaps the previous kernel's tail; everything below reads
+  // its output (B operands via TMA) or overwrites the buffer it read, so wait for it here
+  ptx::pdl_launch_dependents();
+  ptx::pdl_wait_prior();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)

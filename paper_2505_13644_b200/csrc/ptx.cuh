@@ -232,6 +232,12 @@ __device__ __forceinline__ void bf16_split(float v, uint16_t& hi, uint16_t& lo) 
   hi = __bfloat16_as_ushort(h);
   lo = __bfloat16_as_ushort(l);
 }
+// Programmatic dependent launch: the next kernel in the stream may start its prologue
+// once every CTA of this grid has called launch_dependents (or exited); wait_prior blocks
+// until the previous grid has completed and its memory is visible.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prior() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float bf16_val(uint16_t b) { return __bfloat162float(__ushort_as_bfloat16(b)); }
 
 }  // namespace ptx

@@ -445,6 +445,7 @@ __global__ void prep_sigma_kernel(const float* __restrict__ W1T, int D, int ld, 
 __global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, int blocks, int64_t N,
                                 const float* __restrict__ b_out, float scale, float* __restrict__ op,
                                 float* __restrict__ f) {
+  ptx::pdl_wait_prior();  // launched as a programmatic dependent of the last layer kernel
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float s0 = 0.f, s1 = 0.f;
