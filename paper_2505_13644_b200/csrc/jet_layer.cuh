@@ -314,6 +314,50 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   if (!p.readout) store_pair(ph, pl, 0, top);
 }
 
+// The K=2 rule for a point of P <= 16 slots whose 16 columns lie in the accumulator buffer:
+// one TMEM load and one wait for the whole point (the general loop waits for the primal,
+// the middle slots and the top separately). Same operations in the same order as
+// epilogue_point, so the two give identical bits.
+template <int FLAGS>
+__device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint32_t tcol, int64_t row, int m,
+                                                     float bias, float wo, const float* jw, float& fpart,
+                                                     float& opart) {
+  constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
+  constexpr bool wsum = (FLAGS & kFlagWeighted) != 0;
+  const int P = p.P;
+  const size_t ld = (size_t)p.ldo;
+  float v[16];
+  ptx::tmem_ld16(tcol, v);
+  ptx::tmem_ld_wait();
+  const float z0 = v[0] + bias;
+  const ActD A = act_derivs(p.act, z0);
+  fpart = wo * A.d0;
+  uint16_t* ph = p.out_hi + (size_t)row * ld + m;
+  uint16_t* pl = p.out_lo + (size_t)row * ld + m;
+  float* zp = kSaveZ ? p.z_out + (size_t)row * p.ldz + m : nullptr;
+  if (!p.readout) store_pair(ph, pl, 0, A.d0);
+  if constexpr (kSaveZ) zp[0] = z0;
+  float acc = 0.f, zt = 0.f;
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    if (i < P - 1) {
+      const float z = v[i];
+      if (!p.readout) store_pair(ph, pl, (size_t)i * ld, A.d1 * z);
+      if constexpr (wsum)
+        acc = fmaf(jw[i - 1] * z, z, acc);
+      else
+        acc = fmaf(z, z, acc);
+      if constexpr (kSaveZ) zp[(size_t)i * p.ldz] = z;
+    } else if (i == P - 1) {
+      zt = v[i];
+    }
+  }
+  const float top = A.d1 * zt + A.d2 * acc;
+  if constexpr (kSaveZ) zp[(size_t)(P - 1) * p.ldz] = zt;
+  opart = wo * top;
+  if (!p.readout) store_pair(ph, pl, (size_t)(P - 1) * ld, top);
+}
+
 // Nested-Laplacian biharmonic epilogue (kNest) for one point, the whole point in this
 // thread (no split). With s = tanh and the slots of the layout above (multivariate chain
 // rule for h = s(z)):
@@ -821,8 +865,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         for (int pt = g; pt < npts; pt += EG) {
           float fpart, opart;
           const int jbase = (kW && p.blocks > 1) ? ((blk0 + pt) % p.blocks) * p.rb : 0;
-          epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
-                                      jw + jbase, 0, 0, nullptr, 0, fpart, opart);
+          // (the plain K=2 instance runs only with < 8 points per tile, i.e. P > 28: no small path)
+          constexpr bool kSmall = (KORD == 2) && (FLAGS != 0);
+          if (kSmall && p.P <= 16 && pt * p.P + 16 <= kMaxN)
+            epilogue_point_small<FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
+                                        jw + jbase, fpart, opart);
+          else
+            epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
+                                        jw + jbase, 0, 0, nullptr, 0, fpart, opart);
           if (p.readout) {
             fpart = warp_sum(fpart);
             opart = warp_sum(opart);
