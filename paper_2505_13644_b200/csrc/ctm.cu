@@ -230,11 +230,13 @@ ctm_status ensure_pair(uint16_t*& hi, uint16_t*& lo, size_t& have, size_t need) 
   return CTM_OK;
 }
 
-// blk[0], blk[1]: layer ping-pong blocks [rows, ldmax]; blk[2] (and blk[3] if nseed > 1):
+// blk[0], blk[1]: layer ping-pong blocks [rows, ldmax over hidden layers 1..L-1]; blk[2] (and blk[3] if nseed > 1):
 // layer-1 blocks (seed output or random input block) [rows, max(ld1, k1pad)].
 ctm_status ensure_workspace(ctm_mlp* h, int64_t rows, int nseed) {
+  // the ping-pong blocks hold every tensor-core layer's output, including layer 1's when
+  // per-point directions run layer 1 on the tensor cores (ld = wpad[1])
   int ldmax = 0;
-  for (int l = 2; l < h->L; ++l) ldmax = std::max(ldmax, h->wpad[l]);
+  for (int l = 1; l < h->L; ++l) ldmax = std::max(ldmax, h->wpad[l]);
   const int ld_seed = std::max(h->wpad[1], h->k1pad);
   const size_t need[4] = {(size_t)rows * ldmax, (size_t)rows * ldmax, (size_t)rows * ld_seed,
                           nseed > 1 ? (size_t)rows * ld_seed : 0};

@@ -764,3 +764,69 @@ def test_direction_blocks_split_batches_bitwise(ctm):
                        mlp.randomized_laplacian(X[1400:], S=128, seed=5, point_offset=1400)[0].clone()])
     torch.cuda.synchronize()
     assert torch.equal(full, parts)
+
+
+def test_first_hidden_layer_widest_per_point_directions(ctm):
+    """Regression (found by the shape fuzz): with per-point directions layer 1 runs on the
+    tensor cores and writes the ping-pong blocks; a first hidden layer wider than the
+    later ones (264 -> 512 padded vs 12 -> 256) must be covered by the workspace size.
+    A fresh handle sizes the workspace exactly for this call."""
+    widths = [37, 264, 12, 1]
+    params, onet = nets(widths, seed=1)
+    N = 36
+    X = points(N, 37, seed=1)
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    V = O.rademacher(7, 0, N, 230, 37)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    check(mlp.randomized_laplacian(torch.from_numpy(X).cuda(), S=230, seed=7)[0], want, norm)
+    sx = sigma_field(X, 37)
+    want, _, norm = O.weighted_laplacian_pointwise(onet, Xd, sx.astype(np.float64))
+    check(gpu_mlp(ctm, params).weighted_laplacian_pointwise(torch.from_numpy(X).cuda(),
+                                                            torch.from_numpy(sx).cuda())[0], want, norm)
+
+
+# ------------------------------------------------------------------ randomized shapes
+@pytest.mark.parametrize("case", range(12))
+def test_fuzz_shapes_all_operators(ctm, case):
+    """Random nets (D, depth, widths), batch sizes and direction counts, every operator
+    against the oracle. Widths straddle the 256-feature pair tile and the direction counts
+    straddle one MMA tile, so plans with one and several direction blocks, ragged last
+    tiles and padded features all occur. Tiny nets (hidden widths <= 64) carry the R9
+    bound for the K = 2 operators, as in test_edge_shapes_all_operators."""
+    rng = np.random.default_rng(1000 + case)
+    D = int(rng.integers(1, 41))
+    depth = int(rng.integers(1, 4))
+    hidden = [int(rng.integers(8, 321)) for _ in range(depth)]
+    widths = [D] + hidden + [1]
+    N = int(rng.integers(1, 71))
+    params, onet = nets(widths, seed=case)
+    X = points(N, D, seed=case)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    tiny = max(hidden) <= 64
+    Ws, bs = onet.Ws, onet.bs
+    mlp = gpu_mlp(ctm, params)
+    want, fw, norm = O.laplacian(onet, Xd)
+    mag = magnitude_k2(Ws, bs, Xd, np.eye(D), 1.0) if tiny else None
+    op, f = mlp.laplacian(Xc)
+    check(op, want, norm, f, fw, mag=mag)
+    check(mlp.laplacian_standard(Xc)[0], want, norm, mag=mag)
+    R = int(rng.integers(1, 300))
+    sig = make_sigma(D, R, kind="rect")
+    want, _, norm = O.weighted_laplacian(onet, Xd, sig.astype(np.float64))
+    mag = magnitude_k2(Ws, bs, Xd, sig.astype(np.float64).T, 1.0) if tiny else None
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm, mag=mag)
+    S = int(rng.integers(1, 300))
+    V = O.rademacher(7, 0, N, S, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    mag = magnitude_k2(Ws, bs, Xd, V, 1.0 / S) if tiny else None
+    check(mlp.randomized_laplacian(Xc, S=S, seed=7)[0], want, norm, mag=mag)
+    if D <= 8:
+        want, fw, norm = O.biharmonic(onet, Xd)
+        check(mlp.biharmonic(Xc)[0], want, norm)
+        check(mlp.biharmonic_nested(Xc)[0], want, norm)
+        Sg = int(rng.integers(1, 40))
+        Vg = gaussian_directions(N, Sg, D, seed=case)
+        want, _, norm = O.stochastic_biharmonic(onet, Xd, Vg.astype(np.float64), O.O1)
+        check(mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(Vg).cuda())[0], want, norm)
