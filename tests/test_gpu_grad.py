@@ -208,3 +208,46 @@ def test_full_size_gradient_is_the_sum_of_its_shards(ctm):
         for a, b in ((fw, aw), (fb, ab)):
             scale = max(a.abs().max().item(), 1e-30)
             assert (a - b).abs().max().item() / scale < GTOL
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_fuzz_shapes_gradients(ctm, case):
+    """Random nets, batch sizes and direction sets through the differentiable path: the
+    exact, weighted and randomized Laplacians and a signed directional sum, each forward in
+    grad mode then ctm_backward, against the fp64 reverse-mode oracle."""
+    rng = np.random.default_rng(2000 + case)
+    D = int(rng.integers(1, 33))
+    hidden = [int(rng.integers(8, 300)) for _ in range(int(rng.integers(1, 4)))]
+    widths = [D] + hidden + [1]
+    N = int(rng.integers(1, 25))
+    params = mlp_params(widths, case)
+    X = points(N, D, seed=case)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    Ws = [W.astype(np.float64) for W, _ in params]
+    bs = [b.astype(np.float64) for _, b in params]
+    gop, gf = _gs(N, seed=case)
+    go, gfc = torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda()
+    mlp = _mlp(ctm, params)
+    which = ["lap", "wlap", "rlap", "dsum"][case % 4]
+    if which == "lap":
+        mlp.laplacian(Xc)
+        dirs, w = np.eye(D), np.ones(D)
+    elif which == "wlap":
+        R = int(rng.integers(1, 90))
+        sig = make_sigma(D, R, kind="rect")
+        mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())
+        dirs, w = sig.astype(np.float64).T, np.ones(R)
+    elif which == "rlap":
+        S = int(rng.integers(1, 90))
+        mlp.randomized_laplacian(Xc, S=S, seed=case)
+        dirs, w = O.rademacher(case, 0, N, S, D), np.full(S, 1.0 / S)
+    else:
+        J = int(rng.integers(1, 60))
+        d = gaussian_directions(N, J, D, seed=case)
+        ws = signed_weights(J, seed=case)
+        mlp.directional_sum(Xc, 2, torch.from_numpy(d).cuda(), torch.from_numpy(ws).cuda())
+        dirs, w = d.astype(np.float64), ws.astype(np.float64)
+    grads = mlp.backward(go, gfc)
+    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, dirs, w, gop, gf)
+    _check_grads(f"fuzz{case}_{which}_{widths}_N{N}", grads, dW, db)

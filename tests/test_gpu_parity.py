@@ -830,3 +830,37 @@ def test_fuzz_shapes_all_operators(ctm, case):
         Vg = gaussian_directions(N, Sg, D, seed=case)
         want, _, norm = O.stochastic_biharmonic(onet, Xd, Vg.astype(np.float64), O.O1)
         check(mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(Vg).cuda())[0], want, norm)
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_fuzz_directional_sums_blocks_activations(ctm, case):
+    """Random nets with a random activation, weighted directional sums of K = 2 and 4
+    (shared and per-point directions), sigma(x), and forced direction-block sizes."""
+    rng = np.random.default_rng(3000 + case)
+    D = int(rng.integers(1, 24))
+    hidden = [int(rng.integers(65, 300)) for _ in range(int(rng.integers(1, 4)))]
+    widths = [D] + hidden + [1]
+    act = ["tanh", "sin"][case % 2]
+    N = int(rng.integers(1, 50))
+    params, _ = nets(widths, seed=100 + case)
+    onet = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params], act)
+    X = points(N, D, seed=case)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act=act)
+    rb = int(rng.integers(0, 40))  # 0 = the planner
+    mlp.set_direction_block(rb)
+    for K in (2, 4):
+        J = int(rng.integers(1, 120 if K == 2 else 50))
+        w = signed_weights(J, seed=case)
+        per_point = bool(rng.integers(0, 2))
+        dirs = gaussian_directions(N, J, D, seed=case) if per_point else gaussian_directions(1, J, D, seed=case)[0]
+        if K == 4 and per_point and J * D > 12288:
+            continue
+        want, _, norm = O.directional_sum(onet, Xd, K, dirs.astype(np.float64), w.astype(np.float64))
+        got = mlp.directional_sum(Xc, K, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())[0]
+        check(got, want, norm)
+    R = int(rng.integers(1, 80))
+    sx = sigma_field(X, R, seed=case)
+    want, _, norm = O.weighted_laplacian_pointwise(onet, Xd, sx.astype(np.float64))
+    check(mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())[0], want, norm)
