@@ -864,3 +864,50 @@ def test_fuzz_directional_sums_blocks_activations(ctm, case):
     sx = sigma_field(X, R, seed=case)
     want, _, norm = O.weighted_laplacian_pointwise(onet, Xd, sx.astype(np.float64))
     check(mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())[0], want, norm)
+
+
+def test_call_sequences_are_stateless(ctm):
+    """One handle through a random sequence of operator calls (growing and shrinking
+    workspaces, per-call direction matrices, direction blocks, grad mode on and off) gives
+    bit-for-bit the results of a fresh handle for every call: no call depends on what ran
+    before it on the handle."""
+    widths = [12, 300, 96, 1]
+    params, _ = nets(widths, seed=5)
+    rng = np.random.default_rng(77)
+    shared = gpu_mlp(ctm, params)
+
+    def call(m, kind, X, arg):
+        if kind == "lap":
+            return m.laplacian(X)[0]
+        if kind == "std":
+            return m.laplacian_standard(X)[0]
+        if kind == "wlap":
+            return m.weighted_laplacian(X, torch.from_numpy(make_sigma(12, arg, kind="rect")).cuda())[0]
+        if kind == "rlap":
+            return m.randomized_laplacian(X, S=arg, seed=3)[0]
+        if kind == "bih":
+            return m.biharmonic(X)[0]
+        if kind == "nest":
+            return m.biharmonic_nested(X)[0]
+        if kind == "sbih":
+            return m.stochastic_biharmonic(X, S=arg, seed=4)[0]
+        dirs = torch.from_numpy(gaussian_directions(1, arg, 12, seed=arg)[0]).cuda()
+        return m.directional_sum(X, 4, dirs, torch.from_numpy(signed_weights(arg)).cuda())[0]
+
+    kinds = ["lap", "std", "wlap", "rlap", "bih", "nest", "sbih", "dsum4"]
+    grad = False
+    for step in range(24):
+        kind = kinds[int(rng.integers(0, len(kinds)))]
+        N = int(rng.integers(1, 400))
+        arg = int(rng.integers(1, 200 if kind in ("wlap", "rlap") else 40))
+        X = torch.from_numpy(points(N, 12, seed=step)).cuda()
+        if step % 5 == 3:
+            grad = bool(step % 2)
+            shared.grad_enable(grad)
+        got = call(shared, kind, X, arg).clone()
+        fresh = gpu_mlp(ctm, params)
+        fresh.grad_enable(grad)  # grad mode keeps one direction block per point
+        want = call(fresh, kind, X, arg)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (step, kind, N, arg)
+        fresh.close()
