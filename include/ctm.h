@@ -70,7 +70,7 @@ typedef enum { CTM_RADEMACHER = 0, CTM_GAUSSIAN = 1 } ctm_dist;
  * The weights are copied (pre-split into bf16 hi/lo pairs, padded); the call
  * synchronises the device before returning, so W and b may be freed after.
  * Errors: CTM_EINVAL (NULL, n_layers < 2, width < 1), CTM_EUNSUPPORTED
- * (widths[n_layers] != 1, hidden width > 8192), CTM_ECUDA, CTM_ENOMEM. */
+ * (widths[n_layers] != 1, D > 4096, hidden width > 8192), CTM_ECUDA, CTM_ENOMEM. */
 ctm_status ctm_load_mlp(int32_t n_layers, const int32_t *widths, const float *const *W,
                         const float *const *b, int32_t device, ctm_mlp_t *out);
 
@@ -107,7 +107,7 @@ ctm_status ctm_weighted_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, cons
  *     (top bit set -> -1); CTM_GAUSSIAN = Box-Muller on splitmix64
  *     counters 2i, 2i+1 (parity tests pass Gaussian V explicitly).
  *   point_offset: global index of X[0] (shard-invariant generation), >= 0.
- *   sigma [D, Rv] or NULL (then Rv must equal D), Rv <= 256. S >= 1 (direction blocks
+ *   sigma [D, Rv] or NULL (then Rv must equal D), Rv <= 4096. S >= 1 (direction blocks
  *   of the S samples; the 1/S scale is applied once at the readout). */
 ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S,
                                     const float *V, ctm_dist dist, uint64_t seed,
@@ -148,7 +148,7 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
  *   sigma_x [N, D, R] device, fp32: sigma(x_n) row-major [D, R] for each point (the
  *   caller evaluates sigma at its points). P = R + 2 (direction blocks for large R). Layer
  *   1 runs on the tensor cores as for ctm_randomized_laplacian with explicit V. Errors:
- *   CTM_EINVAL (NULL sigma_x, R < 1), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 256). */
+ *   CTM_EINVAL (NULL sigma_x, R < 1), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 4096). */
 ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma_x,
                                             int32_t R, float *op_out, float *f_out, void *stream);
 
@@ -163,7 +163,7 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64
  *   P = J + 2 (K = 2) or 3J + 2 (K = 4) per point, in direction blocks; J <= 2048;
  *   per-point K = 4 also needs J*D <= 12288.
  * Errors: CTM_EINVAL (NULL dirs/weights, J < 1), CTM_ESHAPE (misaligned),
- * CTM_EUNSUPPORTED (K not 2 or 4, J > 2048, D > 256). */
+ * CTM_EUNSUPPORTED (K not 2 or 4, J > 2048, D > 4096). */
 ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float *X, int64_t N, int32_t K, int32_t J,
                                const float *dirs, int32_t per_point, const float *weights, float *op_out,
                                float *f_out, void *stream);

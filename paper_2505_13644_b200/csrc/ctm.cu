@@ -72,6 +72,8 @@ bool make_map(CUtensorMap* m, const uint16_t* base, uint64_t cols, uint64_t rows
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+constexpr int kMaxD = 4096;  // input dimension (and Rv) cap: layer-1 K, seed staging chunks
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct DeviceGuard {
@@ -109,7 +111,6 @@ struct ctm_mlp {
   // output layer
   float* w_out = nullptr;     // [wpad[L-1]]
   float* b_out = nullptr;     // [1] device (updated asynchronously by ctm_set_weights)
-  float* eyeD = nullptr;      // [D, D] identity (Laplacian directions)
   float* bih_dirs = nullptr;  // [J_bih, D] biharmonic family directions
   // fixed direction sets
   float* U_lap = nullptr;     // [D, ld1]: z1 for e_d
@@ -178,7 +179,7 @@ ctm_status free_all(ctm_mlp* h) {
     if (p) cudaFree(p);
     p = nullptr;
   };
-  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1hi); F(h->W1lo); F(h->b_out); F(h->eyeD); F(h->bih_dirs);
+  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1hi); F(h->W1lo); F(h->b_out); F(h->bih_dirs);
   for (auto& p : h->Whi) F(p);
   for (auto& p : h->Wlo) F(p);
   for (auto& p : h->bias) F(p);
@@ -1033,8 +1034,7 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
     ctm::pad_vector_kernel<<<(lpad + 255) / 256, 256, 0, st>>>(W[L - 1], h->widths[L - 1], lpad, h->w_out);
     cudaMemcpyAsync(h->b_out, b[L - 1], sizeof(float), cudaMemcpyDeviceToDevice, st);
   }
-  ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->eyeD, D, nullptr, 2, h->U_lap,
-                                                                 h->c_lap);
+  ctm::prep_laplacian_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->U_lap, h->c_lap);
   if (h->J_bih)
     ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->bih_dirs, h->J_bih, h->w_bih, 4,
                                                                    h->U_bih, h->c_bih);
@@ -1078,7 +1078,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
   for (int l = 0; l <= n_layers; ++l)
     if (widths[l] < 1) return fail(CTM_EINVAL, "width < 1");
   if (widths[n_layers] != 1) return fail(CTM_EUNSUPPORTED, "only scalar-output MLPs (widths[L] == 1)");
-  if (widths[0] > 256) return fail(CTM_EUNSUPPORTED, "input dimension D > 256");
+  if (widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "input dimension D > 4096");
   for (int l = 1; l < n_layers; ++l)
     if (widths[l] > 8192) return fail(CTM_EUNSUPPORTED, "hidden width > 8192");
   for (int l = 0; l < n_layers; ++l)
@@ -1144,11 +1144,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
   }
   LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * h->wpad[n_layers - 1]));
   LOAD_CUDA(cudaMalloc(&h->b_out, sizeof(float)));
-  {  // fixed direction sets: the Laplacian's e_d and, for D <= 7, the biharmonic family
-    std::vector<float> eye((size_t)D * D, 0.f);
-    for (int d = 0; d < D; ++d) eye[(size_t)d * D + d] = 1.f;
-    LOAD_CUDA(cudaMalloc(&h->eyeD, sizeof(float) * eye.size()));
-    LOAD_CUDA(cudaMemcpy(h->eyeD, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
+  {  // fixed direction sets: the Laplacian's e_d and, for D <= 36, the biharmonic family
     LOAD_CUDA(cudaMalloc(&h->U_lap, sizeof(float) * (size_t)D * ld1));
     LOAD_CUDA(cudaMalloc(&h->c_lap, sizeof(float) * ld1));
     if (D * (3 * D - 1) / 2 <= ctm::kMaxW) {  // the jet weights of all blocks live in smem
@@ -1225,7 +1221,7 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, in
   if (dist != CTM_RADEMACHER && dist != CTM_GAUSSIAN) return fail(CTM_EINVAL, "bad dist");
   if (!sigma && Rv != mlp->widths[0]) return fail(CTM_ESHAPE, "Rv must equal D when sigma is NULL");
   if ((V && !aligned16(V)) || (sigma && !aligned16(sigma))) return fail(CTM_ESHAPE, "V/sigma must be 16-byte aligned");
-  if (Rv > 256) return fail(CTM_EUNSUPPORTED, "Rv > 256");
+  if (Rv > kMaxD) return fail(CTM_EUNSUPPORTED, "Rv > 4096");
   CallArgs a{OP_RLAP, X, N, sigma, 0, S, V, seed, point_offset, Rv, dist == CTM_GAUSSIAN, op_out, f_out,
              (cudaStream_t)stream};
   return run(mlp, a);
@@ -1260,7 +1256,7 @@ ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float* X, int64_t N, int32_t
   if (K != 2 && K != 4) return fail(CTM_EUNSUPPORTED, "K must be 2 or 4");
   if (J < 1 || !dirs || !weights) return fail(CTM_EINVAL, "need J >= 1, dirs and weights");
   if (!aligned16(dirs) || !aligned16(weights)) return fail(CTM_ESHAPE, "dirs/weights must be 16-byte aligned");
-  if (mlp->widths[0] > 256) return fail(CTM_EUNSUPPORTED, "D > 256");
+  if (mlp->widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "D > 4096");
   CallArgs a{OP_DSUM, X, N, nullptr, 0, per_point ? J : 0, per_point ? dirs : nullptr, 0, 0, mlp->widths[0], 0,
              op_out, f_out, (cudaStream_t)stream};
   a.K = K;
@@ -1278,7 +1274,7 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64
   if (s != CTM_OK) return s;
   if (R < 1 || !sigma_x) return fail(CTM_EINVAL, "need sigma_x and R >= 1");
   if (!aligned16(sigma_x)) return fail(CTM_ESHAPE, "sigma_x must be 16-byte aligned");
-  if (mlp->widths[0] > 256) return fail(CTM_EUNSUPPORTED, "D > 256");
+  if (mlp->widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "D > 4096");
   CallArgs a{OP_WLAP_X, X, N, nullptr, 0, R, sigma_x, 0, 0, mlp->widths[0], 0, op_out, f_out, (cudaStream_t)stream};
   a.v_trans = 1;
   return run(mlp, a);
@@ -1415,7 +1411,7 @@ ctm_status ctm_stochastic_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, i
   if (dist != CTM_GAUSSIAN)
     return fail(CTM_EINVAL, "the stochastic biharmonic needs standard normal directions (CTM_GAUSSIAN)");
   if (V && !aligned16(V)) return fail(CTM_ESHAPE, "V must be 16-byte aligned");
-  if (mlp->widths[0] > 256) return fail(CTM_EUNSUPPORTED, "D > 256");
+  if (mlp->widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "D > 4096");
   CallArgs a{OP_SBIH, X, N, nullptr, 0, S, V, seed, point_offset, mlp->widths[0], 1, op_out, f_out,
              (cudaStream_t)stream};
   return run(mlp, a);

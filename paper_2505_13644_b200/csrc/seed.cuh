@@ -71,21 +71,20 @@ template <int KORD>
 // kernel needs for its occupancy: 40 registers for K=2 / standard, 48 for K=4 / nested)
 __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6 : 5)
     seed_layer_kernel(const SeedParams p) {
-  __shared__ float xs[256];
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
   const int m = (blockIdx.x % mchunks) * feats + 4 * threadIdx.x;
-  for (int d = threadIdx.x; d < p.D; d += blockDim.x) xs[d] = p.X[n * p.D + d];
-  __syncthreads();
   if (m >= p.ld) return;  // ld is a multiple of 128: a thread's 4 features are all in or all out
+  const float* x = p.X + n * p.D;  // every thread reads the same x_d: a broadcast load
   float4 z0 = ldg4(p.b1 + m);
   for (int d = 0; d < p.D; ++d) {
     const float4 w = ldg4(p.W1T + (size_t)d * p.ld + m);
-    z0.x = fmaf(w.x, xs[d], z0.x);
-    z0.y = fmaf(w.y, xs[d], z0.y);
-    z0.z = fmaf(w.z, xs[d], z0.z);
-    z0.w = fmaf(w.w, xs[d], z0.w);
+    const float xd = __ldg(x + d);
+    z0.x = fmaf(w.x, xd, z0.x);
+    z0.y = fmaf(w.y, xd, z0.y);
+    z0.z = fmaf(w.z, xd, z0.z);
+    z0.w = fmaf(w.w, xd, z0.w);
   }
   const float zz[4] = {z0.x, z0.y, z0.z, z0.w};
   float t[4], d1[4], d2[4], d3[4], d4[4];
@@ -229,12 +228,10 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx);
 
 __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(const SeedStochParams p) {
   extern __shared__ float vsh[];  // [S, D]
-  __shared__ float xs[256];
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
   const int m = (blockIdx.x % mchunks) * feats + 4 * threadIdx.x;
-  for (int d = threadIdx.x; d < p.D; d += blockDim.x) xs[d] = p.X[n * p.D + d];
   for (int e = threadIdx.x; e < p.S * p.D; e += blockDim.x) {
     if (p.V) {
       vsh[e] = p.V[(size_t)n * p.S * p.D + e];
@@ -249,10 +246,11 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
   for (int d = 0; d < p.D; ++d) {
     const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
-    z0.x = fmaf(w.x, xs[d], z0.x);
-    z0.y = fmaf(w.y, xs[d], z0.y);
-    z0.z = fmaf(w.z, xs[d], z0.z);
-    z0.w = fmaf(w.w, xs[d], z0.w);
+    const float xd = __ldg(p.X + n * p.D + d);
+    z0.x = fmaf(w.x, xd, z0.x);
+    z0.y = fmaf(w.y, xd, z0.y);
+    z0.z = fmaf(w.z, xd, z0.z);
+    z0.w = fmaf(w.w, xd, z0.w);
   }
   const float zz[4] = {z0.x, z0.y, z0.z, z0.w};
   float t[4], d1[4], d2[4], d3[4], d4[4];
@@ -423,6 +421,21 @@ __global__ void prep_directions_kernel(const float* __restrict__ W1T, int D, int
     cs = fmaf(w ? w[r] : 1.f, pow == 2 ? u2 : u2 * u2, cs);
   }
   if (csum) csum[m] = cs;
+}
+
+// The Laplacian's fixed directions e_d: UT[d, m] = W1T[d, m] (z1 of e_d is column d of W1)
+// and csum[m] = sum_d W1T[d, m]^2. One thread per feature.
+__global__ void prep_laplacian_kernel(const float* __restrict__ W1T, int D, int ld, float* __restrict__ UT,
+                                      float* __restrict__ csum) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= ld) return;
+  float cs = 0.f;
+  for (int d = 0; d < D; ++d) {
+    const float u = W1T[(size_t)d * ld + m];
+    UT[(size_t)d * ld + m] = u;
+    cs = fmaf(u, u, cs);
+  }
+  csum[m] = cs;
 }
 
 // AT[r, m] = sum_d W1T[d, m] sigma[d, r]  (sigma [D, R] row-major)

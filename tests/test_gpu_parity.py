@@ -911,3 +911,34 @@ def test_call_sequences_are_stateless(ctm):
         torch.cuda.synchronize()
         assert torch.equal(got, want), (step, kind, N, arg)
         fresh.close()
+
+
+@pytest.mark.parametrize("D", [257, 1000])
+def test_high_dimension(ctm, D):
+    """Input dimensions beyond 256 (the exact Laplacian then needs direction blocks: D
+    directions; layer 1 of per-point directions is a K = D GEMM; σ(x) with R = 8)."""
+    widths = [D, 96, 64, 1]
+    params, onet = nets(widths, seed=3)
+    N = 9
+    X = points(N, D, seed=3)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    want, fw, norm = O.laplacian(onet, Xd)
+    op, f = mlp.laplacian(Xc)
+    assert mlp.last_plan()["blocks"] >= 2
+    check(op, want, norm, f, fw)
+    V = O.rademacher(5, 0, N, 12, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    check(mlp.randomized_laplacian(Xc, S=12, seed=5)[0], want, norm)
+    sig = make_sigma(D, 20, kind="rect")
+    want, _, norm = O.weighted_laplacian(onet, Xd, sig.astype(np.float64))
+    check(mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())[0], want, norm)
+    sx = sigma_field(X, 8)
+    want, _, norm = O.weighted_laplacian_pointwise(onet, Xd, sx.astype(np.float64))
+    check(mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())[0], want, norm)
+    w = signed_weights(6)
+    dirs = gaussian_directions(N, 6, D, seed=4)
+    for K in (2, 4):
+        want, _, norm = O.directional_sum(onet, Xd, K, dirs.astype(np.float64), w.astype(np.float64))
+        check(mlp.directional_sum(Xc, K, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())[0], want, norm)
