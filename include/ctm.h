@@ -19,7 +19,8 @@
  *  - A handle is not re-entrant: concurrent calls on one handle are undefined
  *    (one handle per stream/thread). The handle owns a grow-only workspace.
  *  - Errors are status codes; nothing is thrown or aborted. Arguments are
- *    validated before any launch. N == 0 is a no-op returning CTM_OK.
+ *    validated before any launch. N == 0 is a no-op returning CTM_OK (per-point
+ *    arrays such as sigma_x or per-point dirs may then be NULL).
  *    ctm_last_error() gives a thread-local detail message.
  *  - Results are bitwise deterministic run to run, and independent of how a
  *    batch is split into calls (no reduction depends on N or on a point's

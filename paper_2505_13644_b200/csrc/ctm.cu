@@ -1254,7 +1254,7 @@ ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float* X, int64_t N, int32_t
   ctm_status s = check_common(mlp, X, N, op_out, f_out);
   if (s != CTM_OK) return s;
   if (K != 2 && K != 4) return fail(CTM_EUNSUPPORTED, "K must be 2 or 4");
-  if (J < 1 || !dirs || !weights) return fail(CTM_EINVAL, "need J >= 1, dirs and weights");
+  if (J < 1 || !weights || (!dirs && !(per_point && N == 0))) return fail(CTM_EINVAL, "need J >= 1, dirs and weights");
   if (!aligned16(dirs) || !aligned16(weights)) return fail(CTM_ESHAPE, "dirs/weights must be 16-byte aligned");
   if (mlp->widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "D > 4096");
   CallArgs a{OP_DSUM, X, N, nullptr, 0, per_point ? J : 0, per_point ? dirs : nullptr, 0, 0, mlp->widths[0], 0,
@@ -1272,7 +1272,7 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64
   g_last_error.clear();
   ctm_status s = check_common(mlp, X, N, op_out, f_out);
   if (s != CTM_OK) return s;
-  if (R < 1 || !sigma_x) return fail(CTM_EINVAL, "need sigma_x and R >= 1");
+  if (R < 1 || (!sigma_x && N > 0)) return fail(CTM_EINVAL, "need sigma_x and R >= 1");
   if (!aligned16(sigma_x)) return fail(CTM_ESHAPE, "sigma_x must be 16-byte aligned");
   if (mlp->widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "D > 4096");
   CallArgs a{OP_WLAP_X, X, N, nullptr, 0, R, sigma_x, 0, 0, mlp->widths[0], 0, op_out, f_out, (cudaStream_t)stream};

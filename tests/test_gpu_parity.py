@@ -942,3 +942,43 @@ def test_high_dimension(ctm, D):
     for K in (2, 4):
         want, _, norm = O.directional_sum(onet, Xd, K, dirs.astype(np.float64), w.astype(np.float64))
         check(mlp.directional_sum(Xc, K, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())[0], want, norm)
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_fuzz_fourth_order(ctm, case):
+    """Random nets through the K = 4 operators: the interpolation biharmonic (D up to 12,
+    J up to 210 jets -> direction blocks), the nested biharmonic (D up to 20) and the
+    stochastic biharmonic (S up to 100), against the oracle."""
+    rng = np.random.default_rng(4000 + case)
+    D = int(rng.integers(1, 13))
+    hidden = [int(rng.integers(65, 300)) for _ in range(int(rng.integers(1, 4)))]
+    widths = [D] + hidden + [1]
+    N = int(rng.integers(1, 40))
+    params, onet = nets(widths, seed=200 + case)
+    X = points(N, D, seed=case)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    want, fw, norm = O.biharmonic(onet, Xd)
+    op, f = mlp.biharmonic(Xc)
+    check(op, want, norm, f, fw)
+    check(mlp.biharmonic_nested(Xc)[0], want, norm)
+    S = int(rng.integers(1, 101))
+    if S * D <= 12288:
+        V = gaussian_directions(N, S, D, seed=case)
+        want, _, norm = O.stochastic_biharmonic(onet, Xd, V.astype(np.float64), O.O1)
+        check(mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(V).cuda())[0], want, norm)
+
+
+def test_empty_batch_every_operator(ctm):
+    params, _ = nets([5, 16, 16, 1])
+    mlp = gpu_mlp(ctm, params)
+    X = torch.empty(0, 5).cuda()
+    outs = [mlp.laplacian(X)[0], mlp.laplacian_standard(X)[0],
+            mlp.weighted_laplacian(X, torch.from_numpy(make_sigma(5, 3, kind="rect")).cuda())[0],
+            mlp.randomized_laplacian(X, S=4, seed=1)[0], mlp.biharmonic(X)[0], mlp.biharmonic_nested(X)[0],
+            mlp.stochastic_biharmonic(X, S=3, seed=1)[0],
+            mlp.weighted_laplacian_pointwise(X, torch.empty(0, 5, 3).cuda())[0],
+            mlp.directional_sum(X, 4, torch.ones(2, 5).cuda(), torch.ones(2).cuda())[0],
+            mlp.directional_sum(X, 2, torch.empty(0, 2, 5).cuda(), torch.ones(2).cuda())[0]]
+    assert all(o.numel() == 0 for o in outs)
