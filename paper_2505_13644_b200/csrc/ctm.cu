@@ -796,7 +796,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     // C1): the two compete for the 1 kW budget rather than for SMs.
     s = ensure_workspace(h, rows_total, 1);
     if (s != CTM_OK) return s;
-    if (pl.nb > 1 && csum) {  // per-block constants of the fixed set
+    if (pl.nb > 1 && !stoch_k4(a)) {  // per-block constants of the fixed set (UT has R rows)
       s = ensure(h->c_blk, h->c_blk_elems, (size_t)pl.nb * ld1);
       if (s != CTM_OK) return s;
       {
