@@ -292,13 +292,10 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
         if (i < rem) middle(v[i]);
     }
   }
-  if (part == 1) {  // hand the partial collapsed sum to part 2
-    *xacc = acc;
+  if (part != 0) {  // part 1 hands its partial collapsed sum to part 2 (one barrier site for both)
+    if (part == 1) *xacc = acc;
     asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-    return;
-  }
-  if (part == 2) {
-    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    if (part == 1) return;
     acc += *xacc;
   }
   if (KORD == kStd2) {  // standard mode: the top coefficients are sliced and summed only here
