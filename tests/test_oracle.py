@@ -586,3 +586,21 @@ def test_interpolation_family_eq15_recovers_mixed_partials(i):
         (gr,) = torch.autograd.grad(g, xt, create_graph=True)
         g = gr[ax]
     assert abs(got - g.item()) < 1e-10 * max(1.0, abs(g.item()))
+
+
+def test_direction_blocks_are_exact_in_the_collapsed_route():
+    """The GPU's direction blocks rest on Eq. 7 being linear in the collapsed
+    top: propagating a direction set in blocks, each with its own primal and partial top,
+    and adding the block results gives the collapsed result of the whole set. Checked on
+    the oracle's collapsed route O3 (K = 2 and K = 4, uneven blocks), against O1."""
+    rng = np.random.default_rng(11)
+    Ws, bs = random_params([6, 20, 16, 1], 3)
+    net = O.Net(Ws, bs)
+    X = rng.uniform(-1, 1, size=(5, 6))
+    for K, J in ((2, 23), (4, 17)):
+        dirs = rng.standard_normal((J, 6))
+        w = rng.uniform(-1, 1, size=J)
+        whole, _, norm = O.directional_sum(net, X, K, dirs, w, O.O1)
+        cuts = [0, 7, 8, 15, J]
+        parts = sum(O.directional_sum(net, X, K, dirs[a:b], w[a:b], O.O3)[0] for a, b in zip(cuts, cuts[1:]))
+        assert np.max(np.abs(parts - whole) / norm) < 1e-12
