@@ -251,3 +251,17 @@ def test_fuzz_shapes_gradients(ctm, case):
     grads = mlp.backward(go, gfc)
     _, _, dW, db = OG.k2_grad(Ws, bs, Xd, dirs, w, gop, gf)
     _check_grads(f"fuzz{case}_{which}_{widths}_N{N}", grads, dW, db)
+
+
+def test_pinn_poisson_example_trains(ctm):
+    """examples/pinn_poisson.py: 150 Adam steps through ctm_laplacian + ctm_backward (two
+    backward calls per step, the second accumulating) reduce the PINN loss by > 10x."""
+    import importlib.util
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("pinn_poisson", os.path.join(root, "examples", "pinn_poisson.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    hist, err = mod.train(D=3, steps=150, N=1024, Nb=256, width=64, log_every=0)
+    assert all(np.isfinite(hist))
+    assert np.mean(hist[-10:]) < 0.1 * np.mean(hist[:5]), (hist[:5], hist[-10:])
