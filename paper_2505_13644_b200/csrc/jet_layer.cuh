@@ -784,6 +784,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
             const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, 512, kSw64);
             const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, 512, kSw64);
             const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, 512, kSw64);
+#ifdef CTM_EXP_TSA
+            // experiment: A staged into TMEM columns [240, 256) of buffer 0 (free while
+            // N <= 240), then read from TMEM by the MMAs (no repeated A reads from smem)
+            if (p.n_mma <= 240) {
+              const uint32_t ta_hi = tmem_base + 240u, ta_lo = tmem_base + 248u;
+              ptx::tmem_cp_128x256b_pair(ta_hi, dah);
+              ptx::tmem_cp_128x256b_pair(ta_lo, dal);
+              ptx::mma_bf16_pair_ts(d_tmem, ta_lo, dbh, idesc, (kb | ks) != 0);  // lo * hi
+              ptx::mma_bf16_pair_ts(d_tmem, ta_hi, dbl, idesc, 1u);               // hi * lo
+              ptx::mma_bf16_pair_ts(d_tmem, ta_hi, dbh, idesc, 1u);               // hi * hi
+              continue;
+            }
+#endif
             ptx::mma_bf16_pair(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
             ptx::mma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
             ptx::mma_bf16_pair(d_tmem, dah, dbh, idesc, 1u);               // hi * hi

@@ -123,6 +123,22 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, 
       : "memory");
 }
 // Arrive on the mbarrier at this offset in both CTAs of the pair once the MMAs complete.
+// A from tensor memory ("TS"): A is read from this CTA's TMEM columns at a_tmem (128 lanes
+// x K=16 bf16 = 8 columns), B from shared memory as in mma_bf16_pair.
+__device__ __forceinline__ void mma_bf16_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// shared memory -> tensor memory copy of a 128-row x 32-byte operand slice (both CTAs of
+// the pair, each from its own shared memory at the descriptor's offset)
+__device__ __forceinline__ void tmem_cp_128x256b_pair(uint32_t taddr, uint64_t s_desc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(s_desc) : "memory");
+}
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
