@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
     ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard",
-                                   "stochastic_biharmonic", "biharmonic_nested", "laplacian_train"],
+                                   "stochastic_biharmonic", "biharmonic_nested", "biharmonic_standard", "laplacian_train"],
                     default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--direction-block", type=int, default=0,
@@ -63,7 +63,7 @@ def parse():
 def workload(args):
     from synth import widths_for
 
-    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic", "biharmonic_nested") else 50
+    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic", "biharmonic_nested", "biharmonic_standard") else 50
     names = {
         "laplacian": "C1 exact Laplacian",
         "laplacian_train": ("C1 PINN training step: exact Laplacian forward (grad mode) + loss cotangent + "
@@ -73,6 +73,7 @@ def workload(args):
         "randomized": f"C3 randomized Laplacian (Rademacher, S={args.S}, generated in-kernel)",
         "biharmonic": "C4 exact biharmonic (interpolation family, J=35)",
         "biharmonic_nested": "C4 exact biharmonic by nested collapsed Laplacians (P:4073; 27 vectors)",
+        "biharmonic_standard": "C4 exact biharmonic by STANDARD 4th-order Taylor mode (1+4J = 141 vectors; the paper's baseline)",
         "stochastic_biharmonic": f"stochastic biharmonic (Gaussian, S={args.S}, generated in-kernel)",
     }
     w = widths_for(D)
@@ -273,6 +274,8 @@ def main():
             mlp.stochastic_biharmonic(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out)
         elif args.op == "biharmonic_nested":
             mlp.biharmonic_nested(Xd, out=op_out, f_out=f_out)
+        elif args.op == "biharmonic_standard":
+            mlp.biharmonic_standard(Xd, out=op_out, f_out=f_out)
         else:
             mlp.biharmonic(Xd, out=op_out, f_out=f_out)
 

@@ -129,6 +129,15 @@ ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float *X, int64_t N, float *op_ou
  * results for different rb agree to rounding. Host-side. CTM_EINVAL for NULL or rb < 0. */
 ctm_status ctm_set_direction_block(ctm_mlp_t mlp, int32_t rb);
 
+/* Exact biharmonic by STANDARD (uncollapsed) 4th-order Taylor mode through the same
+ * interpolation family as ctm_biharmonic: every layer propagates 1 + 4J vectors (x0 and,
+ * per jet, x1..x4); the weighted top coefficients are summed only at the output. The
+ * paper's baseline for the biharmonic rows of Table `tab:benchmark-ratios` (P:3850-3923:
+ * 141 vs 109 vectors at D = 5); same value, arguments and errors as ctm_biharmonic.
+ * Slots per direction block 1 + 4 rb. */
+ctm_status ctm_biharmonic_standard(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
+                                   void *stream);
+
 /* Replace the weights of a loaded MLP (same widths), e.g. after an optimizer step: the
  * library re-derives every weight-dependent array (bf16 pairs, W1^T, the fixed
  * directions' W1 V, W^T in grad mode) with kernels on `stream`, asynchronously; W, b as
@@ -236,7 +245,7 @@ ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t *launches, int32_t *slots_per_po
 ctm_status ctm_last_blocks(ctm_mlp_t mlp, int32_t *blocks, int32_t *per_block);
 
 /* The planner itself (HOST-only, no device, no handle): for an operator of kind
- * order = 2 (collapsed K=2), 4 (collapsed K=4) or 3 (standard Taylor mode) with R
+ * order = 2 (collapsed K=2), 4 (collapsed K=4), 3 (standard K=2) or 5 (standard K=4) with R
  * directions (jets) and forced_rb as in ctm_set_direction_block, the block split and
  * tile plan an operator call would use. CTM_EINVAL for a bad order or R < 1;
  * CTM_EUNSUPPORTED if no block fits a tile. Any output pointer may be NULL. */

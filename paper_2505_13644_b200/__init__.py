@@ -33,6 +33,7 @@ ABI = {
     ),
     "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_biharmonic_nested": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_biharmonic_standard": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_weighted_laplacian_pointwise": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
     "ctm_directional_sum": (ctypes.c_int, [_VP, _VP, _I64, _I32, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
@@ -207,6 +208,13 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_biharmonic(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                     _stream_ptr(stream, self.device)), "ctm_biharmonic")
+        return out, f_out
+
+    def biharmonic_standard(self, X, out=None, f_out=None, want_f=True, stream=None):
+        """The same biharmonic by standard (uncollapsed) Taylor mode: 1 + 4J vectors (baseline)."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        _check(lib().ctm_biharmonic_standard(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
+                                             _stream_ptr(stream, self.device)), "ctm_biharmonic_standard")
         return out, f_out
 
     def weighted_laplacian_pointwise(self, X, sigma_x, out=None, f_out=None, want_f=True, stream=None):

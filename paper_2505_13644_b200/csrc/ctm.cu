@@ -368,9 +368,10 @@ void tile_plan(Plan& pl) {
   pl.nmma = round_up(k * pl.P, 16);
 }
 
-// slots of a block of rb directions: K=2 rb + 2, K=4 3 rb + 2 (jets of 3), standard 1 + 2 rb
+// slots of a block of rb directions: K=2 rb + 2, K=4 3 rb + 2 (jets of 3), standard 1 + 2 rb,
+// standard K=4 1 + 4 rb
 int block_slots(int KORD, int rb) {
-  return KORD == 4 ? 3 * rb + 2 : KORD == ctm::kStd2 ? 1 + 2 * rb : rb + 2;
+  return KORD == 4 ? 3 * rb + 2 : KORD == ctm::kStd2 ? 1 + 2 * rb : KORD == ctm::kStd4 ? 1 + 4 * rb : rb + 2;
 }
 
 // Modelled cost per point (relative units), from the round-1 sweep of the layer kernel over
@@ -420,7 +421,7 @@ Plan make_plan(int KORD, int R, int forced_rb, bool allow_blocks, int P_fixed = 
   return best;
 }
 
-enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST, OP_DSUM, OP_WLAP_X };
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST, OP_DSUM, OP_WLAP_X, OP_BIH_STD };
 
 struct CallArgs {
   Op op;
@@ -520,6 +521,8 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
       ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
     else if (KORD == ctm::kNest)
       ctm::seed_layer_kernel<ctm::kNest><<<(unsigned)blocks, threads, 0, st>>>(sp);
+    else if (KORD == ctm::kStd4)
+      ctm::seed_layer_kernel<ctm::kStd4><<<(unsigned)blocks, threads, 0, st>>>(sp);
     else
       ctm::seed_layer_kernel<ctm::kStd2><<<(unsigned)blocks, threads, 0, st>>>(sp);
   }
@@ -541,7 +544,8 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((n + ppb - 1) / ppb), threads, 0, st>>>(
         in[0], in[1], h->wpad[1], P, pl.nb, h->widths[1], h->w_out, h->b_out, scale, n, a.op_out + p0,
-        a.f_out ? a.f_out + p0 : nullptr, a.op == OP_LAP_STD);
+        a.f_out ? a.f_out + p0 : nullptr, a.op == OP_LAP_STD ? 2 : a.op == OP_BIH_STD ? 4 : 0, h->w_bih,
+        std::max(pl.rb, 1), h->J_bih);
     ++launches;
     if (after_first) CTM_CUDA(cudaEventRecord(after_first, st));
     return CTM_OK;
@@ -575,7 +579,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     lp.rb = std::max(pl.rb, 1);
     switch (a.op) {
       case OP_SBIH: lp.jet_w = h->w_ones; lp.J = a.S; break;
-      case OP_BIH: lp.jet_w = h->w_bih; lp.J = h->J_bih; break;
+      case OP_BIH: case OP_BIH_STD: lp.jet_w = h->w_bih; lp.J = h->J_bih; break;
       case OP_BIH_NEST: lp.J = h->widths[0]; break;
       case OP_DSUM: lp.jet_w = a.weights; lp.J = a.J; lp.weighted = (a.K == 2); break;
       default: break;
@@ -608,6 +612,8 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
         s = launch_layer_kernel<4, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
       } else if (KORD == ctm::kNest) {
         s = launch_layer_kernel<ctm::kNest, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+      } else if (KORD == ctm::kStd4) {
+        s = launch_layer_kernel<ctm::kStd4, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
       } else {
         s = launch_layer_kernel<ctm::kStd2, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
       }
@@ -668,6 +674,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int ld1 = h->wpad[1];
   const int KORD = (a.op == OP_BIH || a.op == OP_SBIH || (a.op == OP_DSUM && a.K == 4)) ? 4
                    : (a.op == OP_LAP_STD)                                             ? ctm::kStd2
+                   : (a.op == OP_BIH_STD)                                             ? ctm::kStd4
                    : (a.op == OP_BIH_NEST)                                            ? ctm::kNest
                                                                                       : 2;
   int R = 0;  // directions (K=4: jets) of the operator
@@ -675,7 +682,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     case OP_LAP: case OP_LAP_STD: R = D; break;
     case OP_WLAP: R = a.R; break;
     case OP_RLAP: case OP_SBIH: case OP_WLAP_X: R = a.S; break;
-    case OP_BIH: R = h->J_bih; break;
+    case OP_BIH: case OP_BIH_STD: R = h->J_bih; break;
     case OP_DSUM: R = a.J; break;
     case OP_BIH_NEST: break;
   }
@@ -688,7 +695,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
                                        : "direction block does not fit one tile (slots per block > 256)");
   if (stoch_k4(a) && (int64_t)a.S * D > 12288)
     return fail(CTM_EUNSUPPORTED, "S * D > 12288 for per-point K=4 directions");
-  if ((KORD == 4 || a.op == OP_DSUM) && (int64_t)pl.nb * pl.rb > ctm::kMaxW)
+  if ((KORD == 4 || KORD == ctm::kStd4 || a.op == OP_DSUM) && (int64_t)pl.nb * pl.rb > ctm::kMaxW)
     return fail(CTM_EUNSUPPORTED, "more than 2048 weighted directions (jets) per point");
   const int P = pl.P;
   h->last_P = pl.P;
@@ -760,7 +767,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     // fixed direction sets (or the K=4 stochastic seed): U and the per-feature constant
     const float* UT = h->U_lap;
     const float* csum = h->c_lap;
-    if (a.op == OP_BIH) {
+    if (a.op == OP_BIH || a.op == OP_BIH_STD) {
       UT = h->U_bih;
       csum = h->c_bih;
     } else if (a.op == OP_DSUM && !a.per_point) {  // U = W1 u_j, c = sum_j w_j (W1 u_j)^K for this call
@@ -801,7 +808,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       if (s != CTM_OK) return s;
       {
         ProfScope ps(h, CTM_KIND_PREP, 0.0, st);
-        const float* w = (a.op == OP_BIH) ? h->w_bih : (a.op == OP_DSUM) ? a.weights : nullptr;
+        const float* w = (a.op == OP_BIH || a.op == OP_BIH_STD) ? h->w_bih : (a.op == OP_DSUM) ? a.weights : nullptr;
         ctm::block_csum_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(UT, R, ld1, w, KORD == 4 ? 4 : 2, pl.nb, pl.rb,
                                                                   h->c_blk);
       }
@@ -1237,6 +1244,17 @@ ctm_status ctm_biharmonic(ctm_mlp_t mlp, const float* X, int64_t N, float* op_ou
   return run(mlp, a);
 }
 
+ctm_status ctm_biharmonic_standard(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out, float* f_out,
+                                   void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (mlp->J_bih == 0)
+    return fail(CTM_EUNSUPPORTED, "biharmonic needs J = D(3D-1)/2 <= 2048 jets, i.e. D <= 36");
+  CallArgs a{OP_BIH_STD, X, N, nullptr, 0, 0, nullptr, 0, 0, 0, 0, op_out, f_out, (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
 ctm_status ctm_biharmonic_nested(ctm_mlp_t mlp, const float* X, int64_t N, float* op_out, float* f_out,
                                  void* stream) {
   g_last_error.clear();
@@ -1435,9 +1453,9 @@ ctm_status ctm_last_blocks(ctm_mlp_t mlp, int32_t* blocks, int32_t* per_block) {
 ctm_status ctm_plan_blocks(int32_t order, int32_t R, int32_t forced_rb, int32_t* blocks, int32_t* per_block,
                            int32_t* slots_per_block, int32_t* points_per_tile, int32_t* mma_n) {
   g_last_error.clear();
-  if ((order != 2 && order != 3 && order != 4) || R < 1 || forced_rb < 0)
-    return fail(CTM_EINVAL, "need order 2, 3 or 4, R >= 1 and forced_rb >= 0");
-  const int KORD = (order == 3) ? ctm::kStd2 : order;
+  if ((order != 2 && order != 3 && order != 4 && order != 5) || R < 1 || forced_rb < 0)
+    return fail(CTM_EINVAL, "need order 2, 3, 4 or 5, R >= 1 and forced_rb >= 0");
+  const int KORD = (order == 3) ? ctm::kStd2 : (order == 5) ? ctm::kStd4 : order;
   const Plan pl = make_plan(KORD, R, forced_rb, true);
   if (pl.P == 0) return fail(CTM_EUNSUPPORTED, "no direction block fits a tile");
   if (blocks) *blocks = pl.nb;

@@ -60,6 +60,11 @@ constexpr uint32_t kSw64 = 4;                    // descriptor layout code for S
 // top), kStd2 = K=2 STANDARD Taylor mode (1 + 2R slots, the per-direction top
 // coefficients are propagated and only summed at the output) -- the paper's baseline.
 constexpr int kStd2 = 3;
+// kStd4: K=4 STANDARD Taylor mode for a weighted jet family (the biharmonic of Eq. 12 by
+// the interpolation directions, uncollapsed): 1 + 4J slots, per jet (z1, z2, z3, z4); the
+// per-jet top coefficients h4_j are weighted and summed only at the readout -- the
+// paper's baseline for the biharmonic rows of Table `tab:benchmark-ratios`.
+constexpr int kStd4 = 7;
 // kNest: the biharmonic by NESTED collapsed Laplacians, with the slots
 // of the nest that are equal by symmetry of partial derivatives stored once: per point
 // [z | g_a = d_a z (D) | H_ab = d_a d_b z, a <= b packed row-major (D(D+1)/2) |
@@ -184,7 +189,8 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
                                                int bar_id, float& fpart, float& opart) {
   const int P = p.P;
   const int ld = p.ldo;
-  const int nmid = (KORD == kStd2) ? P - 1 : P - 2;  // middle slots are 1 .. nmid
+  constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
+  const int nmid = kStd ? P - 1 : P - 2;  // middle slots are 1 .. nmid
   const int mb = (part == 2) ? split : 1;
   const int me = (part == 1) ? split : nmid + 1;
   // ---- slot 0: the primal; the bias enters here only (affine rule)
@@ -203,7 +209,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
   //      standard-mode pairs (z1_r, z2_r) with no collapse
   float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
-  int jj = (KORD == 4) ? (mb - 1) / 3 : mb - 1;  // weight index of the first direction / jet
+  int jj = (KORD == 4) ? (mb - 1) / 3 : (KORD == kStd4) ? (mb - 1) / 4 : mb - 1;  // first direction / jet
   auto put = [&](float h) {
     if (!p.readout) store_pair(ph, pl, 0, h);
     ph += ld;
@@ -234,6 +240,34 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
       ptx::tmem_ld4(tcol + (uint32_t)(mb + 3 * j), v);
       ptx::tmem_ld_wait();
       jet(v[0], v[1], v[2]);
+    }
+  } else if constexpr (KORD == kStd4) {
+    // standard K=4 mode: per jet (h1, h2, h3, h4), the weighted h4 summed for the readout
+    // (cheat-sheet rows k <= 4, per jet); 4 jets per 16 columns
+    auto jet4 = [&](float z1, float z2, float z3, float z4) {
+      put(d1 * z1);
+      put(d2 * z1 * z1 + d1 * z2);
+      put(d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3);
+      const float h4 = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 + 3.f * d2 * z2 * z2 +
+                       d1 * z4;
+      put(h4);
+      acc = fmaf(jw[jj], h4, acc);
+      ++jj;
+    };
+    const int nj = (me - mb) / 4;
+    int j = 0;
+    for (; j + 4 <= nj; j += 4) {
+      float v[16];
+      ptx::tmem_ld16(tcol + (uint32_t)(mb + 4 * j), v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) jet4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+    }
+    for (; j < nj; ++j) {
+      float v[4];
+      ptx::tmem_ld4(tcol + (uint32_t)(mb + 4 * j), v);
+      ptx::tmem_ld_wait();
+      jet4(v[0], v[1], v[2], v[3]);
     }
   } else if constexpr (KORD == kStd2) {
     // standard mode: per direction (h1_r, h2_r) with no collapse, 8 pairs per 16 columns
@@ -298,7 +332,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     if (part == 1) return;
     acc += *xacc;
   }
-  if (KORD == kStd2) {  // standard mode: the top coefficients are sliced and summed only here
+  if (kStd) {  // standard mode: the top coefficients are sliced and summed only here
     opart = wo * acc;
     return;
   }
@@ -702,7 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
-  if (KORD == 4 || p.weighted)  // all blocks' weights; a padded last block reads zeros
+  if (KORD == 4 || KORD == kStd4 || p.weighted)  // all blocks' weights; a padded last block reads zeros
     for (int j = threadIdx.x; j < p.blocks * p.rb; j += blockDim.x) jw[j] = (j < p.J) ? p.jet_w[j] : 0.f;
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barrier inits and TMEM allocation visible to the pair
@@ -815,8 +849,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     const int q = warp & 3;
     const int g = (warp - 2) >> 2;
     // split of a single point's middle slots between the groups, at a unit boundary
-    const int unit = (KORD == 4) ? 3 : (KORD == kStd2) ? 2 : 1;
-    const int nunits = ((KORD == kStd2) ? p.P - 1 : p.P - 2) / unit;
+    const int unit = (KORD == 4) ? 3 : (KORD == kStd2) ? 2 : (KORD == kStd4) ? 4 : 1;
+    const int nunits = ((KORD == kStd2 || KORD == kStd4) ? p.P - 1 : p.P - 2) / unit;
     const int split = 1 + (nunits / 2) * unit;
     const int m_local = q * 32 + lane;
     uint32_t local = 0;
@@ -831,7 +865,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       const float bias = p.bias ? p.bias[m] : 0.f;
       const float wo = p.readout ? p.w_out[m] : 0.f;
       // direction block of the tile's first sub-point (weights offset jbase, see LayerParams)
-      constexpr bool kW = (KORD == 4) || (FLAGS & kFlagWeighted) != 0;  // instances that read jw
+      constexpr bool kW = (KORD == 4) || (KORD == kStd4) || (FLAGS & kFlagWeighted) != 0;  // instances reading jw
       const int blk0 = (kW && p.blocks > 1) ? (int)((n_tile * p.pts_per_tile) % p.blocks) : 0;
       const int64_t pts_left = p.n_points - n_tile * p.pts_per_tile;
       const int npts = (int)(pts_left < p.pts_per_tile ? pts_left : p.pts_per_tile);

@@ -114,6 +114,27 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
     }
     CTM_BLOCK_END
+  } else if (KORD == kStd4) {
+    CTM_BLOCK_BEGIN
+    // standard K=4 mode: per jet (h1, h2, h3, h4) = (s' u, s'' u^2, s''' u^3, s'''' u^4)  (x2 = x3 = x4 = 0)
+    for (int j = r0; j < r0 + p.rb; ++j) {
+      const float4 u = (j < r1) ? ldg4(p.UT + (size_t)j * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float z[4] = {u.x, u.y, u.z, u.w};
+      float h[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float z2 = z[i] * z[i];
+        h[0][i] = d1[i] * z[i];
+        h[1][i] = d2[i] * z2;
+        h[2][i] = d3[i] * z2 * z[i];
+        h[3][i] = d4[i] * z2 * z2;
+      }
+      const size_t r = row0 + 1 + 4 * (j - r0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        seed_store4(p.out_hi, p.out_lo, (r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3]);
+    }
+    CTM_BLOCK_END
   } else if (KORD == 2) {
     if (p.z_out) {  // grad mode (one block): the layer-1 pre-activations for the backward pass
       const size_t row0 = (size_t)n * p.P;
@@ -471,11 +492,14 @@ __global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, 
 
 // Readout straight from a layer block (nets with a single hidden layer):
 // one warp per point, lanes over features; `blocks` sub-points of P slots per point.
-// standard != 0: the op is sum_r w_out . h2_r over rows 2, 4, .., P-1 (standard mode)
+// standard == 2: the op is sum_r w_out . h2_r over rows 2, 4, .., P-1 (standard mode);
+// standard == 4: sum_j jw[j] w_out . h4_j over rows 4, 8, .., P-1 (standard K=4 mode, jw
+// indexed over all blocks of the point)
 __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo, int ld, int P,
                                      int blocks, int width, const float* __restrict__ w_out,
                                      const float* __restrict__ b_out, float scale, int64_t N, float* __restrict__ op,
-                                     float* __restrict__ f, int standard) {
+                                     float* __restrict__ f, int standard, const float* __restrict__ jw, int rb,
+                                     int J) {
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
@@ -488,9 +512,11 @@ __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint
       if (!standard) {
         s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
       } else {
-        for (int r = 2; r < P; r += 2) {
+        for (int r = standard; r < P; r += standard) {
           const size_t ri = (sp * P + r) * ld;
-          s1 = fmaf(w_out[m], ptx::bf16_val(hi[ri + m]) + ptx::bf16_val(lo[ri + m]), s1);
+          const int j = b * rb + r / 4 - 1;
+          const float c = (standard == 4) ? ((j < J) ? jw[j] : 0.f) : 1.f;
+          s1 = fmaf(c * w_out[m], ptx::bf16_val(hi[ri + m]) + ptx::bf16_val(lo[ri + m]), s1);
         }
       }
     }

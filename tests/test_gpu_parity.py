@@ -982,3 +982,21 @@ def test_empty_batch_every_operator(ctm):
             mlp.directional_sum(X, 4, torch.ones(2, 5).cuda(), torch.ones(2).cuda())[0],
             mlp.directional_sum(X, 2, torch.empty(0, 2, 5).cuda(), torch.ones(2).cuda())[0]]
     assert all(o.numel() == 0 for o in outs)
+
+
+@pytest.mark.parametrize("widths,N,rb", [([2, 2, 1], 3, 0), ([5, 16, 16, 1], 8, 0), (C4_WIDTHS, 29, 0),
+                                         (C4_WIDTHS, 11, 35), (C4_WIDTHS, 11, 9), ([7, 96, 80, 1], 5, 0)])
+def test_biharmonic_standard_mode_parity(ctm, widths, N, rb):
+    """Standard (uncollapsed) K=4 Taylor mode through the interpolation family: the same
+    operator as the collapsed route (Eq. 7 is exact), 1 + 4J vectors; single-hidden-layer
+    readout, one block of 35 jets (P = 141) and uneven blocks."""
+    params, onet = nets(widths)
+    D = widths[0]
+    X = points(N, D)
+    mlp = gpu_mlp(ctm, params)
+    mlp.set_direction_block(rb)
+    op, f = mlp.biharmonic_standard(torch.from_numpy(X).cuda())
+    pl = mlp.last_plan()
+    assert pl["slots_per_point"] == 1 + 4 * pl["per_block"]
+    want, fwant, norm = O.biharmonic(onet, X.astype(np.float64), O.O1)
+    check(op, want, norm, f, fwant)

@@ -166,10 +166,10 @@ def test_data_parallel_gradient_allreduce_world2_gloo():
 
 # ------------------------------------------------------------------ direction-block planner
 def _slots(order, rb):
-    return 3 * rb + 2 if order == 4 else (1 + 2 * rb if order == 3 else rb + 2)
+    return {4: 3 * rb + 2, 3: 1 + 2 * rb, 5: 1 + 4 * rb}.get(order, rb + 2)
 
 
-@pytest.mark.parametrize("order", [2, 3, 4])
+@pytest.mark.parametrize("order", [2, 3, 4, 5])
 def test_direction_block_planner_invariants(order):
     """ctm_plan_blocks (host only): the blocks cover the R directions with padding only in
     the last block, a block fits one MMA tile, and the tile holds ppt blocks."""
