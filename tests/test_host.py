@@ -203,4 +203,4 @@ def test_direction_block_planner_choices():
     with pytest.raises(ctm.CTMError, match="EUNSUPPORTED"):
         ctm.plan_blocks(2, 300, 300)
     with pytest.raises(ctm.CTMError, match="EINVAL"):
-        ctm.plan_blocks(5, 10)
+        ctm.plan_blocks(6, 10)
