@@ -246,7 +246,7 @@ def main():
         n_glob = N * world
         launches = {}
 
-    def train_step(Xd):
+    def train_step(Xd, op_out=op_out, f_out=f_out):
         mlp.laplacian(Xd, out=op_out, f_out=f_out)
         launches["fwd"] = mlp.last_plan()["launches"]
         torch.sub(op_out, target, out=res)
@@ -259,9 +259,9 @@ def main():
         mlp.set_weights(pdev)
         launches["upd"] = mlp.last_plan()["launches"]
 
-    def step(Xd):
+    def step(Xd, op_out=op_out, f_out=f_out):
         if train:
-            train_step(Xd)
+            train_step(Xd, op_out, f_out)
         elif args.op == "laplacian":
             mlp.laplacian(Xd, out=op_out, f_out=f_out)
         elif args.op == "standard":
@@ -321,35 +321,66 @@ def main():
     best_ms = max_over_ranks(min(step_ms))      # the paper's protocol: best of the repetitions
     median_ms = max_over_ranks(float(np.median(step_ms)))
 
-    # ---------------- end to end: pinned host X -> device, operator, result -> pinned host
+    # ---------------- end to end, pipelined: every step uploads its inputs from pinned host
+    # memory on a copy stream, runs the operator on the compute stream and downloads its
+    # results to pinned host memory on a third stream; two buffer sets let step i+1's upload
+    # and step i-1's download overlap step i's kernels (each step's bytes still cross PCIe
+    # inside the timed region). No L2 flush: the step's working set is > 10 GB >> L2.
     Xh = torch.from_numpy(X_host.copy()).pin_memory()
-    oh = torch.empty(N, dtype=torch.float32).pin_memory()
-    fh = torch.empty(N, dtype=torch.float32).pin_memory()
-    Xd = torch.empty_like(X)
-    for _ in range(2):
-        Xd.copy_(Xh, non_blocking=True)
-        step(Xd)
-        oh.copy_(op_out, non_blocking=True)
-        fh.copy_(f_out, non_blocking=True)
-    torch.cuda.synchronize()
-    evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ohs = [torch.empty(N, dtype=torch.float32).pin_memory() for _ in range(2)]
+    fhs = [torch.empty(N, dtype=torch.float32).pin_memory() for _ in range(2)]
+    Xds = [torch.empty_like(X) for _ in range(2)]
+    outs = [(torch.empty(N, device=dev), torch.empty(N, device=dev)) for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    comp = torch.cuda.current_stream(dev)
+
+    def e2e_run(nsteps, t0=None, t1=None):
+        done, downloaded = [], []
+        if t0 is not None:
+            t0.record(s_in)
+        for i in range(nsteps):
+            b = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(done[i - 2])          # step i-2 no longer reads Xds[b]
+                Xds[b].copy_(Xh, non_blocking=True)
+                up = torch.cuda.Event()
+                up.record(s_in)
+            comp.wait_event(up)
+            if i >= 2:
+                comp.wait_event(downloaded[i - 2])        # outs[b] of step i-2 is on the host
+            step(Xds[b], outs[b][0], outs[b][1])
+            e = torch.cuda.Event()
+            e.record(comp)
+            done.append(e)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(e)
+                ohs[b].copy_(outs[b][0], non_blocking=True)
+                fhs[b].copy_(outs[b][1], non_blocking=True)
+                d = torch.cuda.Event()
+                d.record(s_out)
+                downloaded.append(d)
+        if t1 is not None:
+            s_out.wait_event(done[-1])
+            t1.record(s_out)
+        torch.cuda.synchronize()
+        return (nsteps - 1) % 2
+
+    e2e_run(2)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    for a, b in evs2:
-        flush_buf.zero_()
-        a.record()
-        Xd.copy_(Xh, non_blocking=True)
-        step(Xd)
-        oh.copy_(op_out, non_blocking=True)
-        fh.copy_(f_out, non_blocking=True)
-        b.record()
-    torch.cuda.synchronize()
+    last = e2e_run(args.steps, t0, t1)
     barrier()
-    e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs2))
+    e2e_ms = max_over_ranks(t0.elapsed_time(t1))
+    oh = ohs[last]
+
     clk = clocks.stop()
 
-    # sanity: the e2e result equals the device-resident one bit for bit
-    assert torch.equal(oh, op_out.cpu()), "e2e result differs from the device-resident run"
+    # sanity: the e2e result equals the device-resident one bit for bit (the training step
+    # updates the weights every step, so its results move on)
+    if not train:
+        assert torch.equal(oh, op_out.cpu()), "e2e result differs from the device-resident run"
 
     value = N * world * args.steps / (total_ms / 1e3)
     e2e_value = N * world * args.steps / (e2e_ms / 1e3)
