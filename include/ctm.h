@@ -162,6 +162,18 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
 ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma_x,
                                             int32_t R, float *op_out, float *f_out, void *stream);
 
+/* Weighted Laplacian for an arbitrary symmetric, possibly INDEFINITE weighting C
+ * ("For indefinite D, we can simply apply this scheme to the positive and negative
+ * eigen-spaces"): op[n] = <d^2 f(x_n), C> = sum_i lambda_i <d^2 f(x_n), q_i^{(x)2}> with
+ * C = sum_i lambda_i q_i q_i^T. The eigendecomposition runs on the device per call
+ * (cuSOLVER syevd in fp64, O(D^3), a setup step), then the collapsed K=2 directional sum
+ * with directions q_i and signed weights lambda_i (one collapsed top).
+ *   C [D, D] device, fp32, row-major, symmetric (the lower triangle is read).
+ * Errors: CTM_EINVAL (NULL C), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 2048),
+ * CTM_ECUDA (cuSOLVER). */
+ctm_status ctm_weighted_laplacian_indefinite(ctm_mlp_t mlp, const float *X, int64_t N, const float *C,
+                                             float *op_out, float *f_out, void *stream);
+
 /* General linear operator of degree K as a weighted sum of K-th directional derivatives
  * (Eq. 5 `eq:sum-k-directional` P:548-558 with coefficients; the general approach of
  * Eq. 13-15, reduces <d^K f, C> to this form with the weights gamma_{i,j}/K!

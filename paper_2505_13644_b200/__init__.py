@@ -34,6 +34,7 @@ ABI = {
     "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_biharmonic_nested": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_biharmonic_standard": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_weighted_laplacian_indefinite": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP, _VP]),
     "ctm_weighted_laplacian_pointwise": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
     "ctm_directional_sum": (ctypes.c_int, [_VP, _VP, _I64, _I32, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
@@ -208,6 +209,17 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_biharmonic(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                     _stream_ptr(stream, self.device)), "ctm_biharmonic")
+        return out, f_out
+
+    def weighted_laplacian_indefinite(self, X, C, out=None, f_out=None, want_f=True, stream=None):
+        """<d^2 f, C> for a symmetric, possibly indefinite C [D, D] (eigen-directions)."""
+        X, N, out, f_out = self._io(X, out, f_out, want_f)
+        C = _dev_f32(C, self.device, "C")
+        if tuple(C.shape) != (self.D, self.D):
+            raise CTMError("C must be [D, D]")
+        _check(lib().ctm_weighted_laplacian_indefinite(self._h, X.data_ptr(), N, C.data_ptr(), out.data_ptr(),
+                                                       self._p(f_out), _stream_ptr(stream, self.device)),
+               "ctm_weighted_laplacian_indefinite")
         return out, f_out
 
     def biharmonic_standard(self, X, out=None, f_out=None, want_f=True, stream=None):

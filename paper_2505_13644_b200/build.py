@@ -19,7 +19,9 @@ FLAGS = [
     "-Xptxas", "-v",
     f"-I{os.path.join(ROOT, 'include')}",
 ]
-LIBS = ["-lcublas"]  # the weight-gradient GEMMs of the differentiable path (plain long-K GEMMs)
+# cuBLAS: the weight-gradient GEMMs of the differentiable path (plain long-K GEMMs);
+# cuSOLVER: the eigendecomposition of an indefinite weighting (a per-call setup step)
+LIBS = ["-lcublas", "-lcusolver"]
 
 
 def stale() -> bool:

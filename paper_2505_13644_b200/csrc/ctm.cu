@@ -7,6 +7,7 @@
 //           (the last hidden layer reduces straight against the output weights)
 //   final   op = c * (w_L . sum h_K), f = w_L . h0 + b_L
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -141,6 +142,15 @@ struct ctm_mlp {
   std::vector<CUtensorMap> mapAT_hi, mapAT_lo;
   float* eye = nullptr;                     // [256, 256] identity: fixed direction sets as shared V
   cublasHandle_t cublas = nullptr;
+  // indefinite weightings (ctm_weighted_laplacian_indefinite): eigendecomposition state
+  cusolverDnHandle_t cusolver = nullptr;
+  double* eig_a = nullptr;   // [D, D] fp64 copy of the weighting, then its eigenvectors
+  double* eig_w = nullptr;   // [D] eigenvalues
+  double* eig_work = nullptr;
+  int eig_lwork = 0;
+  int* eig_info = nullptr;
+  float* eig_dirs = nullptr;  // [D, D] eigenvectors as directions (rows), fp32
+  float* eig_vals = nullptr;  // [D] eigenvalues as direction weights, fp32
   struct Tape {
     bool valid = false;
     int64_t N = 0;
@@ -199,6 +209,9 @@ ctm_status free_all(ctm_mlp* h) {
     for (int j = 0; j < 2; ++j) F(h->tape.Zb[i][j]);
   if (h->cublas) cublasDestroy(h->cublas);
   h->cublas = nullptr;
+  if (h->cusolver) cusolverDnDestroy(h->cusolver);
+  h->cusolver = nullptr;
+  F(h->eig_a); F(h->eig_w); F(h->eig_work); F(h->eig_info); F(h->eig_dirs); F(h->eig_vals);
   for (auto& r : h->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1283,6 +1296,54 @@ ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float* X, int64_t N, int32_t
   a.per_point = per_point != 0;
   a.weights = weights;
   return run(mlp, a);
+}
+
+ctm_status ctm_weighted_laplacian_indefinite(ctm_mlp_t mlp, const float* X, int64_t N, const float* C, float* op_out,
+                                             float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (!C) return fail(CTM_EINVAL, "need the weighting C");
+  if (!aligned16(C)) return fail(CTM_ESHAPE, "C must be 16-byte aligned");
+  const int D = mlp->widths[0];
+  if (D > ctm::kMaxW) return fail(CTM_EUNSUPPORTED, "D > 2048 eigen-directions");
+  DeviceGuard g(mlp->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!mlp->cusolver) {
+    if (cusolverDnCreate(&mlp->cusolver) != CUSOLVER_STATUS_SUCCESS) {
+      mlp->cusolver = nullptr;
+      return fail(CTM_ECUDA, "cusolverDnCreate failed");
+    }
+    CTM_CUDA(cudaMalloc(&mlp->eig_a, sizeof(double) * (size_t)D * D));
+    CTM_CUDA(cudaMalloc(&mlp->eig_w, sizeof(double) * D));
+    CTM_CUDA(cudaMalloc(&mlp->eig_info, sizeof(int)));
+    CTM_CUDA(cudaMalloc(&mlp->eig_dirs, sizeof(float) * (size_t)D * D));
+    CTM_CUDA(cudaMalloc(&mlp->eig_vals, sizeof(float) * D));
+    if (cusolverDnDsyevd_bufferSize(mlp->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, mlp->eig_a, D,
+                                    mlp->eig_w, &mlp->eig_lwork) != CUSOLVER_STATUS_SUCCESS)
+      return fail(CTM_ECUDA, "cusolverDnDsyevd_bufferSize failed");
+    CTM_CUDA(cudaMalloc(&mlp->eig_work, sizeof(double) * std::max(mlp->eig_lwork, 1)));
+  }
+  if (N == 0) return CTM_OK;
+  // C = sum_i lambda_i q_i q_i^T ("apply this scheme to the positive and negative
+  // eigen-spaces"): the collapsed K=2 directional sum with directions q_i, weights lambda_i
+  ctm::to_f64_kernel<<<(D * D + 255) / 256, 256, 0, st>>>(C, (int64_t)D * D, mlp->eig_a);
+  if (cusolverDnSetStream(mlp->cusolver, st) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDsyevd(mlp->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, mlp->eig_a, D, mlp->eig_w,
+                       mlp->eig_work, mlp->eig_lwork, mlp->eig_info) != CUSOLVER_STATUS_SUCCESS)
+    return fail(CTM_ECUDA, "cusolverDnDsyevd failed");
+  // column i of the column-major eigenvector matrix is contiguous: it is direction row i
+  ctm::to_f32_kernel<<<(D * D + 255) / 256, 256, 0, st>>>(mlp->eig_a, (int64_t)D * D, mlp->eig_dirs);
+  ctm::to_f32_kernel<<<(D + 255) / 256, 256, 0, st>>>(mlp->eig_w, (int64_t)D, mlp->eig_vals);
+  CallArgs a{OP_DSUM, X, N, nullptr, 0, 0, nullptr, 0, 0, D, 0, op_out, f_out, st};
+  a.K = 2;
+  a.J = D;
+  a.dirs = mlp->eig_dirs;
+  a.per_point = 0;
+  a.weights = mlp->eig_vals;
+  s = run(mlp, a);
+  mlp->last_launches += 3;  // the conversions (cuSOLVER's own kernels not counted)
+  return s;
 }
 
 ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64_t N, const float* sigma_x, int32_t R,

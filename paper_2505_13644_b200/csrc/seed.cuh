@@ -555,6 +555,15 @@ __global__ void transpose_w1_kernel(const float* __restrict__ W1, const float* _
   if (d == 0) b1p[m] = (m < w1) ? b1[m] : 0.f;
 }
 
+__global__ void to_f64_kernel(const float* __restrict__ src, int64_t n, double* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = (double)src[i];
+}
+__global__ void to_f32_kernel(const double* __restrict__ src, int64_t n, float* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = (float)src[i];
+}
+
 __global__ void pad_vector_kernel(const float* __restrict__ src, int n, int npad, float* __restrict__ dst) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < npad) dst[i] = (i < n) ? src[i] : 0.f;

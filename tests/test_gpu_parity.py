@@ -1000,3 +1000,37 @@ def test_biharmonic_standard_mode_parity(ctm, widths, N, rb):
     assert pl["slots_per_point"] == 1 + 4 * pl["per_block"]
     want, fwant, norm = O.biharmonic(onet, X.astype(np.float64), O.O1)
     check(op, want, norm, f, fwant)
+
+
+@pytest.mark.parametrize("widths,N", [([5, 32, 24, 1], 7), (C1_WIDTHS, 5)])
+def test_weighted_laplacian_indefinite(ctm, widths, N):
+    """<d^2 f, C> for a symmetric INDEFINITE C (eigen-spaces of both signs), against
+    the exact Hessian of the fp64 net by torch autograd (independent of the oracle and of
+    any eigendecomposition); the normaliser is sum_i |lambda_i q_i^T H q_i|."""
+    params, _ = nets(widths, seed=9)
+    D = widths[0]
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((D, D))
+    C = ((A + A.T) / 2).astype(np.float32)
+    lam, Q = np.linalg.eigh(C.astype(np.float64))
+    assert lam.min() < 0 < lam.max()
+    X = points(N, D, seed=9)
+    Ws = [torch.tensor(W, dtype=torch.float64) for W, _ in params]
+    bs = [torch.tensor(b, dtype=torch.float64) for _, b in params]
+
+    def f(x):
+        h = x
+        for l, (W, b) in enumerate(zip(Ws, bs)):
+            h = W @ h + b
+            if l + 1 < len(Ws):
+                h = torch.tanh(h)
+        return h[0]
+
+    want, norm = np.empty(N), np.empty(N)
+    for n in range(N):
+        H = torch.autograd.functional.hessian(f, torch.tensor(X[n], dtype=torch.float64)).numpy()
+        want[n] = np.sum(H * C.astype(np.float64))
+        norm[n] = np.sum(np.abs(lam * np.einsum("ai,ab,bi->i", Q, H, Q)))
+    mlp = gpu_mlp(ctm, params)
+    op, _ = mlp.weighted_laplacian_indefinite(torch.from_numpy(X).cuda(), torch.from_numpy(C).cuda())
+    check(op, want, norm)
