@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="points per GPU")
     ap.add_argument("--op", choices=["laplacian", "weighted", "randomized", "biharmonic", "standard",
-                                   "stochastic_biharmonic", "biharmonic_nested", "biharmonic_standard", "laplacian_train"],
+                                   "stochastic_biharmonic", "biharmonic_nested", "biharmonic_standard", "randomized_standard",
+                                   "stochastic_biharmonic_standard", "laplacian_train"],
                     default="laplacian")
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--direction-block", type=int, default=0,
@@ -63,7 +64,8 @@ def parse():
 def workload(args):
     from synth import widths_for
 
-    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic", "biharmonic_nested", "biharmonic_standard") else 50
+    D = 5 if args.op in ("biharmonic", "stochastic_biharmonic", "biharmonic_nested", "biharmonic_standard",
+                         "stochastic_biharmonic_standard") else 50
     names = {
         "laplacian": "C1 exact Laplacian",
         "laplacian_train": ("C1 PINN training step: exact Laplacian forward (grad mode) + loss cotangent + "
@@ -75,6 +77,8 @@ def workload(args):
         "biharmonic_nested": "C4 exact biharmonic by nested collapsed Laplacians (P:4073; 27 vectors)",
         "biharmonic_standard": "C4 exact biharmonic by STANDARD 4th-order Taylor mode (1+4J = 141 vectors; the paper's baseline)",
         "stochastic_biharmonic": f"stochastic biharmonic (Gaussian, S={args.S}, generated in-kernel)",
+        "randomized_standard": f"C3 randomized Laplacian by STANDARD Taylor mode (S={args.S}; 1+2S vectors, baseline)",
+        "stochastic_biharmonic_standard": f"stochastic biharmonic by STANDARD Taylor mode (S={args.S}; 1+4S vectors, baseline)",
     }
     w = widths_for(D)
     return D, w, f"{names[args.op]}, tanh MLP {'-'.join(map(str, w[:-1]))}-1, N={args.n} points per GPU"
@@ -149,9 +153,9 @@ def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
             OG.k2_grad(net.Ws, net.bs, X, np.eye(D), np.ones(D), np.ones(X.shape[0]) / X.shape[0])
         elif op == "weighted":
             O.weighted_laplacian(net, X, sig, O.O1)
-        elif op == "randomized":
+        elif op in ("randomized", "randomized_standard"):
             O.randomized_laplacian(net, X, O.rademacher(2, 0, X.shape[0], S, D), route=O.O1)
-        elif op == "stochastic_biharmonic":
+        elif op in ("stochastic_biharmonic", "stochastic_biharmonic_standard"):
             V = np.random.default_rng(2).standard_normal((X.shape[0], S, D))
             O.stochastic_biharmonic(net, X, V, O.O1)
         elif op == "biharmonic_nested":
@@ -276,6 +280,12 @@ def main():
             mlp.biharmonic_nested(Xd, out=op_out, f_out=f_out)
         elif args.op == "biharmonic_standard":
             mlp.biharmonic_standard(Xd, out=op_out, f_out=f_out)
+        elif args.op == "randomized_standard":
+            mlp.randomized_laplacian(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out,
+                                     standard=True)
+        elif args.op == "stochastic_biharmonic_standard":
+            mlp.stochastic_biharmonic(Xd, S=args.S, seed=2, point_offset=rank * N, out=op_out, f_out=f_out,
+                                      standard=True)
         else:
             mlp.biharmonic(Xd, out=op_out, f_out=f_out)
 

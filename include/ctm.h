@@ -138,6 +138,19 @@ ctm_status ctm_set_direction_block(ctm_mlp_t mlp, int32_t rb);
 ctm_status ctm_biharmonic_standard(ctm_mlp_t mlp, const float *X, int64_t N, float *op_out, float *f_out,
                                    void *stream);
 
+/* The randomized Laplacian and the stochastic biharmonic by STANDARD (uncollapsed) Taylor
+ * mode: the same estimators, arguments, generated directions and errors as
+ * ctm_randomized_laplacian / ctm_stochastic_biharmonic, with 1 + 2S (resp. 1 + 4S)
+ * propagated vectors and the per-sample top coefficients summed only at the output. The
+ * paper's baselines for the stochastic rows of Table `tab:benchmark-ratios`. */
+ctm_status ctm_randomized_laplacian_standard(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S,
+                                             const float *V, ctm_dist dist, uint64_t seed,
+                                             int64_t point_offset, const float *sigma, int32_t Rv,
+                                             float *op_out, float *f_out, void *stream);
+ctm_status ctm_stochastic_biharmonic_standard(ctm_mlp_t mlp, const float *X, int64_t N, int32_t S, const float *V,
+                                              ctm_dist dist, uint64_t seed, int64_t point_offset, float *op_out,
+                                              float *f_out, void *stream);
+
 /* Replace the weights of a loaded MLP (same widths), e.g. after an optimizer step: the
  * library re-derives every weight-dependent array (bf16 pairs, W1^T, the fixed
  * directions' W1 V, W^T in grad mode) with kernels on `stream`, asynchronously; W, b as

@@ -34,6 +34,12 @@ ABI = {
     "ctm_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_biharmonic_nested": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
     "ctm_biharmonic_standard": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP]),
+    "ctm_randomized_laplacian_standard": (
+        ctypes.c_int,
+        [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _I32, _VP, _VP, _VP],
+    ),
+    "ctm_stochastic_biharmonic_standard": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP,
+                                                          _VP, _VP]),
     "ctm_weighted_laplacian_indefinite": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP, _VP]),
     "ctm_weighted_laplacian_pointwise": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
     "ctm_directional_sum": (ctypes.c_int, [_VP, _VP, _I64, _I32, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
@@ -183,8 +189,9 @@ class MLP:
         return out, f_out
 
     def randomized_laplacian(self, X, S=None, V=None, seed=0, point_offset=0, sigma=None, dist="rademacher",
-                             out=None, f_out=None, want_f=True, stream=None):
-        """(1/S) sum_s <d^2 f, (sigma v_s)^2> (Eq. 8/10 stochastic). V [N, S, Rv] or generated."""
+                             out=None, f_out=None, want_f=True, stream=None, standard=False):
+        """(1/S) sum_s <d^2 f, (sigma v_s)^2> (Eq. 8/10 stochastic). V [N, S, Rv] or generated.
+        standard=True: the same estimator by standard (uncollapsed) Taylor mode (baseline)."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         if V is not None:
             V = _dev_f32(V, self.device, "V")
@@ -198,10 +205,10 @@ class MLP:
         if S is None:
             raise CTMError("S is required when V is not given")
         d = {"rademacher": CTM_RADEMACHER, "gaussian": CTM_GAUSSIAN}[dist]
-        _check(lib().ctm_randomized_laplacian(self._h, X.data_ptr(), N, int(S), self._p(V), d, int(seed) & (2**64 - 1),
-                                              int(point_offset), self._p(sigma), int(Rv), out.data_ptr(),
-                                              self._p(f_out), _stream_ptr(stream, self.device)),
-               "ctm_randomized_laplacian")
+        fn = lib().ctm_randomized_laplacian_standard if standard else lib().ctm_randomized_laplacian
+        _check(fn(self._h, X.data_ptr(), N, int(S), self._p(V), d, int(seed) & (2**64 - 1), int(point_offset),
+                  self._p(sigma), int(Rv), out.data_ptr(), self._p(f_out), _stream_ptr(stream, self.device)),
+               "ctm_randomized_laplacian" + ("_standard" if standard else ""))
         return out, f_out
 
     def biharmonic(self, X, out=None, f_out=None, want_f=True, stream=None):
@@ -263,18 +270,19 @@ class MLP:
         return out, f_out
 
     def stochastic_biharmonic(self, X, S=None, V=None, seed=0, point_offset=0, out=None, f_out=None, want_f=True,
-                              stream=None):
-        """1/(3S) sum_s <d^4 f, v_s^4>, v_s ~ N(0, I) (Eq. 12 stochastic; V [N, S, D] or generated)."""
+                              stream=None, standard=False):
+        """1/(3S) sum_s <d^4 f, v_s^4>, v_s ~ N(0, I) (Eq. 12 stochastic; V [N, S, D] or generated).
+        standard=True: the same estimator by standard (uncollapsed) Taylor mode (baseline)."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         if V is not None:
             V = _dev_f32(V, self.device, "V")
             S = V.shape[1]
         if S is None:
             raise CTMError("S is required when V is not given")
-        _check(lib().ctm_stochastic_biharmonic(self._h, X.data_ptr(), N, int(S), self._p(V), CTM_GAUSSIAN,
-                                               int(seed) & (2**64 - 1), int(point_offset), out.data_ptr(),
-                                               self._p(f_out), _stream_ptr(stream, self.device)),
-               "ctm_stochastic_biharmonic")
+        fn = lib().ctm_stochastic_biharmonic_standard if standard else lib().ctm_stochastic_biharmonic
+        _check(fn(self._h, X.data_ptr(), N, int(S), self._p(V), CTM_GAUSSIAN, int(seed) & (2**64 - 1),
+                  int(point_offset), out.data_ptr(), self._p(f_out), _stream_ptr(stream, self.device)),
+               "ctm_stochastic_biharmonic" + ("_standard" if standard else ""))
         return out, f_out
 
     def set_weights(self, params: Sequence, stream=None):

@@ -434,7 +434,8 @@ Plan make_plan(int KORD, int R, int forced_rb, bool allow_blocks, int P_fixed = 
   return best;
 }
 
-enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST, OP_DSUM, OP_WLAP_X, OP_BIH_STD };
+enum Op { OP_LAP, OP_WLAP, OP_RLAP, OP_BIH, OP_LAP_STD, OP_SBIH, OP_BIH_NEST, OP_DSUM, OP_WLAP_X, OP_BIH_STD,
+          OP_RLAP_STD, OP_SBIH_STD };
 
 struct CallArgs {
   Op op;
@@ -462,10 +463,12 @@ struct CallArgs {
 
 // per-point K=2 directions: the input block [x0; u; 0] and layer 1 on the tensor cores
 bool random_k2(const CallArgs& a) {
-  return a.op == OP_RLAP || a.op == OP_WLAP_X || (a.op == OP_DSUM && a.per_point && a.K == 2);
+  return a.op == OP_RLAP || a.op == OP_RLAP_STD || a.op == OP_WLAP_X || (a.op == OP_DSUM && a.per_point && a.K == 2);
 }
 // per-point K=4 directions: layer 1 in fp32 on the CUDA cores (seed_stoch_biharmonic_kernel)
-bool stoch_k4(const CallArgs& a) { return a.op == OP_SBIH || (a.op == OP_DSUM && a.per_point && a.K == 4); }
+bool stoch_k4(const CallArgs& a) {
+  return a.op == OP_SBIH || a.op == OP_SBIH_STD || (a.op == OP_DSUM && a.per_point && a.K == 4);
+}
 
 struct GemmLayer {
   const CUtensorMap* a_hi;
@@ -506,6 +509,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     bp.point_offset = a.point_offset + p0;
     bp.blocks = pl.nb;
     bp.rb = pl.rb;
+    bp.standard = (a.op == OP_SBIH_STD);
     bp.out_hi = buf[0];
     bp.out_lo = buf[1];
     bp.act = h->act;
@@ -557,8 +561,9 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((n + ppb - 1) / ppb), threads, 0, st>>>(
         in[0], in[1], h->wpad[1], P, pl.nb, h->widths[1], h->w_out, h->b_out, scale, n, a.op_out + p0,
-        a.f_out ? a.f_out + p0 : nullptr, a.op == OP_LAP_STD ? 2 : a.op == OP_BIH_STD ? 4 : 0, h->w_bih,
-        std::max(pl.rb, 1), h->J_bih);
+        a.f_out ? a.f_out + p0 : nullptr,
+        (a.op == OP_LAP_STD || a.op == OP_RLAP_STD) ? 2 : (a.op == OP_BIH_STD || a.op == OP_SBIH_STD) ? 4 : 0,
+        a.op == OP_SBIH_STD ? h->w_ones : h->w_bih, std::max(pl.rb, 1), a.op == OP_SBIH_STD ? a.S : h->J_bih);
     ++launches;
     if (after_first) CTM_CUDA(cudaEventRecord(after_first, st));
     return CTM_OK;
@@ -591,7 +596,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     lp.blocks = pl.nb;
     lp.rb = std::max(pl.rb, 1);
     switch (a.op) {
-      case OP_SBIH: lp.jet_w = h->w_ones; lp.J = a.S; break;
+      case OP_SBIH: case OP_SBIH_STD: lp.jet_w = h->w_ones; lp.J = a.S; break;
       case OP_BIH: case OP_BIH_STD: lp.jet_w = h->w_bih; lp.J = h->J_bih; break;
       case OP_BIH_NEST: lp.J = h->widths[0]; break;
       case OP_DSUM: lp.jet_w = a.weights; lp.J = a.J; lp.weighted = (a.K == 2); break;
@@ -686,15 +691,15 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int D = h->widths[0];
   const int ld1 = h->wpad[1];
   const int KORD = (a.op == OP_BIH || a.op == OP_SBIH || (a.op == OP_DSUM && a.K == 4)) ? 4
-                   : (a.op == OP_LAP_STD)                                             ? ctm::kStd2
-                   : (a.op == OP_BIH_STD)                                             ? ctm::kStd4
+                   : (a.op == OP_LAP_STD || a.op == OP_RLAP_STD)                      ? ctm::kStd2
+                   : (a.op == OP_BIH_STD || a.op == OP_SBIH_STD)                      ? ctm::kStd4
                    : (a.op == OP_BIH_NEST)                                            ? ctm::kNest
                                                                                       : 2;
   int R = 0;  // directions (K=4: jets) of the operator
   switch (a.op) {
     case OP_LAP: case OP_LAP_STD: R = D; break;
     case OP_WLAP: R = a.R; break;
-    case OP_RLAP: case OP_SBIH: case OP_WLAP_X: R = a.S; break;
+    case OP_RLAP: case OP_SBIH: case OP_WLAP_X: case OP_RLAP_STD: case OP_SBIH_STD: R = a.S; break;
     case OP_BIH: case OP_BIH_STD: R = h->J_bih; break;
     case OP_DSUM: R = a.J; break;
     case OP_BIH_NEST: break;
@@ -765,6 +770,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.v_trans = a.v_trans;
     rp.blocks = pl.nb;
     rp.rb = pl.rb;
+    rp.standard = (a.op == OP_RLAP_STD);
     rp.out_hi = grad ? tapeB0[0] : h->blk[2][0];
     rp.out_lo = grad ? tapeB0[1] : h->blk[2][1];
     {
@@ -772,7 +778,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
     }
     ++launches;
-    const float scale = (a.op == OP_RLAP) ? 1.f / (float)a.S : 1.f;  // Eq. 8/10 stochastic: the mean
+    const float scale = (a.op == OP_RLAP || a.op == OP_RLAP_STD) ? 1.f / (float)a.S : 1.f;  // Eq. 8/10 stochastic
     s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB0 : h->blk[2], scale, st, nullptr, launches,
                       grad ? &io : nullptr);
     if (s != CTM_OK) return s;
@@ -810,7 +816,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       UT = h->U_call;
       csum = h->c_call;
     }
-    const float scale = (a.op == OP_SBIH) ? 1.f / (3.f * (float)a.S) : 1.f;  // Eq. 12 stochastic: 1/(3S), Q1
+    const float scale = (a.op == OP_SBIH || a.op == OP_SBIH_STD) ? 1.f / (3.f * (float)a.S) : 1.f;  // Eq. 12: 1/(3S), Q1
     // Sequential: running the HBM-write-bound seed of one chunk beside the power-capped
     // tensor-core layers of another was measured slower (2.58-2.65 M vs 2.68 M points/s at
     // C1): the two compete for the 1 kW budget rather than for SMs.
@@ -1243,6 +1249,38 @@ ctm_status ctm_randomized_laplacian(ctm_mlp_t mlp, const float* X, int64_t N, in
   if ((V && !aligned16(V)) || (sigma && !aligned16(sigma))) return fail(CTM_ESHAPE, "V/sigma must be 16-byte aligned");
   if (Rv > kMaxD) return fail(CTM_EUNSUPPORTED, "Rv > 4096");
   CallArgs a{OP_RLAP, X, N, sigma, 0, S, V, seed, point_offset, Rv, dist == CTM_GAUSSIAN, op_out, f_out,
+             (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_randomized_laplacian_standard(ctm_mlp_t mlp, const float* X, int64_t N, int32_t S, const float* V,
+                                             ctm_dist dist, uint64_t seed, int64_t point_offset, const float* sigma,
+                                             int32_t Rv, float* op_out, float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (S < 1 || Rv < 1 || point_offset < 0) return fail(CTM_EINVAL, "need S >= 1, Rv >= 1, point_offset >= 0");
+  if (dist != CTM_RADEMACHER && dist != CTM_GAUSSIAN) return fail(CTM_EINVAL, "bad dist");
+  if (!sigma && Rv != mlp->widths[0]) return fail(CTM_ESHAPE, "Rv must equal D when sigma is NULL");
+  if ((V && !aligned16(V)) || (sigma && !aligned16(sigma))) return fail(CTM_ESHAPE, "V/sigma must be 16-byte aligned");
+  if (Rv > kMaxD) return fail(CTM_EUNSUPPORTED, "Rv > 4096");
+  CallArgs a{OP_RLAP_STD, X, N, sigma, 0, S, V, seed, point_offset, Rv, dist == CTM_GAUSSIAN, op_out, f_out,
+             (cudaStream_t)stream};
+  return run(mlp, a);
+}
+
+ctm_status ctm_stochastic_biharmonic_standard(ctm_mlp_t mlp, const float* X, int64_t N, int32_t S, const float* V,
+                                              ctm_dist dist, uint64_t seed, int64_t point_offset, float* op_out,
+                                              float* f_out, void* stream) {
+  g_last_error.clear();
+  ctm_status s = check_common(mlp, X, N, op_out, f_out);
+  if (s != CTM_OK) return s;
+  if (S < 1 || point_offset < 0) return fail(CTM_EINVAL, "need S >= 1 and point_offset >= 0");
+  if (dist != CTM_GAUSSIAN)
+    return fail(CTM_EINVAL, "the stochastic biharmonic needs standard normal directions (CTM_GAUSSIAN)");
+  if (V && !aligned16(V)) return fail(CTM_ESHAPE, "V must be 16-byte aligned");
+  if (mlp->widths[0] > kMaxD) return fail(CTM_EUNSUPPORTED, "D > 4096");
+  CallArgs a{OP_SBIH_STD, X, N, nullptr, 0, S, V, seed, point_offset, mlp->widths[0], 1, op_out, f_out,
              (cudaStream_t)stream};
   return run(mlp, a);
 }

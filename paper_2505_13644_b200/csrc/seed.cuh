@@ -240,7 +240,8 @@ struct SeedStochParams {
   int64_t point_offset;
   int blocks;            // sample blocks per point, `rb` samples each (last one zero padded)
   int rb;
-  uint16_t* out_hi;      // [N*blocks*(3rb+2), ld]
+  int standard;          // 1: standard K=4 layout, per sample (h1, h2, h3, h4), 1 + 4 rb rows
+  uint16_t* out_hi;      // [N*blocks*(3rb+2), ld] (standard: [N*blocks*(1+4rb), ld])
   uint16_t* out_lo;
   int act;
 };
@@ -263,7 +264,8 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   }
   __syncthreads();
   if (m >= p.ld) return;
-  const int P = 3 * p.rb + 2;  // slots per block
+  const int P = p.standard ? 1 + 4 * p.rb : 3 * p.rb + 2;  // slots per block
+  const int st = p.standard ? 4 : 3;                       // rows per sample
   float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
   for (int d = 0; d < p.D; ++d) {
     const float4 w = __ldg(reinterpret_cast<const float4*>(p.W1T + (size_t)d * p.ld + m));
@@ -305,13 +307,20 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
         h3[i] = d3[i] * z2 * z[i];
         acc[i] = fmaf((p.w && s < p.S) ? p.w[s] * z2 : z2, z2, acc[i]);
       }
-      const size_t r = row0 + 1 + 3 * (size_t)(s - b * p.rb);
+      const size_t r = row0 + 1 + st * (size_t)(s - b * p.rb);
       seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
       seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
       seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+      if (p.standard) {  // h4 of this sample = s'''' z1^4   (x2 = x3 = x4 = 0)
+        float h4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h4[i] = d4[i] * (z[i] * z[i]) * (z[i] * z[i]);
+        seed_store4(p.out_hi, p.out_lo, (r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3]);
+      }
     }
-    seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
-                d4[3] * acc[3]);
+    if (!p.standard)
+      seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
+                  d4[3] * acc[3]);
   }
 }
 
@@ -336,7 +345,8 @@ struct SeedRandomParams {
   int gaussian;          // generated directions: 0 Rademacher, 1 standard normal
   int blocks;            // direction blocks per point, `rb` directions each (last one zero padded)
   int rb;
-  uint16_t* out_hi;      // [N*blocks*(rb+2), ldk]
+  int standard;          // 1: standard Taylor mode layout [x0; (u_s, 0) per direction], 1 + 2 rb rows
+  uint16_t* out_hi;      // [N*blocks*(rb+2), ldk] (standard: [N*blocks*(1+2rb), ldk])
   uint16_t* out_lo;
 };
 
@@ -352,20 +362,25 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx) {
 __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
   __shared__ float vs[kSeedChunk];
   const int64_t n = blockIdx.x;
-  const int P = p.rb + 2;                       // slots per block
+  const int st = p.standard ? 2 : 1;            // rows per direction
+  const int P = p.standard ? 1 + 2 * p.rb : p.rb + 2;  // slots per block
   const size_t pt0 = (size_t)n * p.blocks;      // first sub-point of this point
   const int q4 = p.ldk / 4;                     // 4-column groups per row
-  // direction s lives in row 1 + s % rb of sub-point s / rb
-  auto dir_row = [&](int s) { return (pt0 + s / p.rb) * P + 1 + s % p.rb; };
-  // every block's primal row and zero top row, and the zero rows of the last block's padding
+  // direction s lives in row 1 + st (s % rb) of sub-point s / rb
+  auto dir_row = [&](int s) { return (pt0 + s / p.rb) * P + 1 + st * (s % p.rb); };
+  // every block's primal row and zero top row (standard: the zero x2 row of every
+  // direction), and the zero rows of the last block's padding
   for (int c4 = threadIdx.x; c4 < q4; c4 += blockDim.x) {
     float x[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = (4 * c4 + i < p.D) ? p.X[n * p.D + 4 * c4 + i] : 0.f;
     for (int b = 0; b < p.blocks; ++b) {
       seed_store4(p.out_hi, p.out_lo, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
-      seed_store4(p.out_hi, p.out_lo, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+      if (!p.standard) seed_store4(p.out_hi, p.out_lo, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
     }
+    if (p.standard)
+      for (int s = 0; s < p.blocks * p.rb; ++s)
+        seed_store4(p.out_hi, p.out_lo, (dir_row(s) + 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
     for (int s = p.S; s < p.blocks * p.rb; ++s)
       seed_store4(p.out_hi, p.out_lo, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
   }

@@ -1034,3 +1034,26 @@ def test_weighted_laplacian_indefinite(ctm, widths, N):
     mlp = gpu_mlp(ctm, params)
     op, _ = mlp.weighted_laplacian_indefinite(torch.from_numpy(X).cuda(), torch.from_numpy(C).cuda())
     check(op, want, norm)
+
+
+@pytest.mark.parametrize("widths,N", [([4, 40, 32, 1], 9), ([6, 24, 1], 5), (C1_WIDTHS, 7)])
+def test_stochastic_standard_modes_parity(ctm, widths, N):
+    """The randomized Laplacian and the stochastic biharmonic by standard (uncollapsed)
+    Taylor mode give the collapsed estimators' values for the same directions (Eq. 7 is
+    exact), against the oracle; generated directions match the collapsed call."""
+    params, onet = nets(widths)
+    D = widths[0]
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    mlp = gpu_mlp(ctm, params)
+    V = O.rademacher(6, 0, N, 11, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    a = mlp.randomized_laplacian(Xc, S=11, seed=6, standard=True)[0]
+    check(a, want, norm)
+    b = mlp.randomized_laplacian(Xc, S=11, seed=6)[0]
+    check(b, a.double().cpu().numpy(), norm, tol=2 * TOL)
+    if D <= 8:
+        Vg = gaussian_directions(N, 7, D, seed=3)
+        want, _, norm = O.stochastic_biharmonic(onet, Xd, Vg.astype(np.float64), O.O1)
+        check(mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(Vg).cuda(), standard=True)[0], want, norm)
