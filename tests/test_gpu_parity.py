@@ -1057,3 +1057,25 @@ def test_stochastic_standard_modes_parity(ctm, widths, N):
         Vg = gaussian_directions(N, 7, D, seed=3)
         want, _, norm = O.stochastic_biharmonic(onet, Xd, Vg.astype(np.float64), O.O1)
         check(mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(Vg).cuda(), standard=True)[0], want, norm)
+
+
+def test_two_handles_on_two_streams(ctm):
+    """One handle per stream (ctm.h): two handles driven concurrently on two CUDA streams,
+    with interleaved calls, give bit-for-bit the results of sequential calls."""
+    params, _ = nets(C1_WIDTHS)
+    X = torch.from_numpy(points(700, 50)).cuda()
+    a, b = gpu_mlp(ctm, params), gpu_mlp(ctm, params)
+    ref_lap = a.laplacian(X)[0].clone()
+    ref_r = b.randomized_laplacian(X, S=16, seed=3)[0].clone()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            o1 = a.laplacian(X, stream=s1)[0]
+        with torch.cuda.stream(s2):
+            o2 = b.randomized_laplacian(X, S=16, seed=3, stream=s2)[0]
+        outs.append((o1, o2))
+    torch.cuda.synchronize()
+    for o1, o2 in outs:
+        assert torch.equal(o1, ref_lap) and torch.equal(o2, ref_r)
