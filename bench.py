@@ -432,6 +432,15 @@ def main():
         "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
         "launches_per_step": {k: v["launches"] / args.steps for k, v in prof.items()},
     }
+    # the HBM-bound stage: layer 1 written by the seed kernel (fixed direction sets; bytes
+    # written = the layer-1 block, bf16 pairs) against the measured HBM bandwidth
+    sd = prof["seed"]
+    hbm = peaks.get("hbm_gbs", 6546.0)
+    if sd["ms"] > 0 and sd["work"] > 0:
+        gbs = sd["work"] / (sd["ms"] / 1e3) / 1e9
+        roofline["seed_hbm"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                "note": "algorithmic bytes written by the seed kernel per its event time; the peak "
+                                        "is the measured copy (read+write) bandwidth"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
