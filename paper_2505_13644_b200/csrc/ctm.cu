@@ -58,7 +58,7 @@ EncodeTiledFn get_encode() {
 }
 
 // 2D bf16 tensor map: inner dim `cols` (contiguous), outer `rows`; box {kBK, box_rows}
-// (64-byte rows); SWIZZLE_64B, matching the UMMA descriptors of jet_layer.cuh.
+// (128-byte rows); SWIZZLE_128B, matching the UMMA descriptors of jet_layer.cuh.
 bool make_map(CUtensorMap* m, const uint16_t* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
@@ -67,7 +67,8 @@ bool make_map(CUtensorMap* m, const uint16_t* base, uint64_t cols, uint64_t rows
   cuuint32_t box[2] = {(cuuint32_t)ctm::kBK, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
