@@ -183,7 +183,9 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64
  * with directions q_i and signed weights lambda_i (one collapsed top).
  *   C [D, D] device, fp32, row-major, symmetric (the lower triangle is read).
  * Errors: CTM_EINVAL (NULL C), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 2048),
- * CTM_ECUDA (cuSOLVER). */
+ * CTM_ECUDA (a cuSOLVER call failed). The call stays asynchronous, so the solver's
+ * convergence flag (devInfo) is not read back; syevd on a symmetric matrix converges in
+ * practice. */
 ctm_status ctm_weighted_laplacian_indefinite(ctm_mlp_t mlp, const float *X, int64_t N, const float *C,
                                              float *op_out, float *f_out, void *stream);
 
