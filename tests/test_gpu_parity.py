@@ -1079,3 +1079,32 @@ def test_two_handles_on_two_streams(ctm):
     torch.cuda.synchronize()
     for o1, o2 in outs:
         assert torch.equal(o1, ref_lap) and torch.equal(o2, ref_r)
+
+
+def test_square_net_closed_forms_standard_modes_and_blocks(ctm):
+    """f = ||x||^4 (square(1^T square(x))) through the standard modes and forced direction
+    blocks: Laplacian 4(D+2)||x||^2; biharmonic 8D(D+2); randomized (1/S) sum_s
+    (4||x||^2 ||v||^2 + 8 (v.x)^2); stochastic biharmonic 1/(3S) sum_s 24 ||v_s||^4."""
+    D = 5
+    params = [(np.eye(D, dtype=np.float32), np.zeros(D, np.float32)), (np.ones((1, D), np.float32), np.zeros(1, np.float32)),
+              (np.ones((1, 1), np.float32), np.zeros(1, np.float32))]
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act="square")
+    N = 17
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    r2 = np.sum(Xd ** 2, 1)
+    V = gaussian_directions(N, 6, D, seed=4).astype(np.float64)
+    for rb in (0, 2):
+        mlp.set_direction_block(rb)
+        np.testing.assert_allclose(mlp.laplacian_standard(Xc)[0].double().cpu().numpy(), 4 * (D + 2) * r2, rtol=2e-5)
+        np.testing.assert_allclose(mlp.biharmonic_standard(Xc)[0].double().cpu().numpy(), 8 * D * (D + 2), rtol=2e-5)
+        got = mlp.randomized_laplacian(Xc, V=torch.from_numpy(V.astype(np.float32)).cuda(), dist="gaussian",
+                                       standard=True)[0].double().cpu().numpy()
+        Vf = V.astype(np.float32).astype(np.float64)
+        want = np.mean(4 * r2[:, None] * np.sum(Vf ** 2, 2) + 8 * np.einsum("nsd,nd->ns", Vf, Xd) ** 2, 1)
+        np.testing.assert_allclose(got, want, rtol=2e-5)
+        got = mlp.stochastic_biharmonic(Xc, V=torch.from_numpy(V.astype(np.float32)).cuda(),
+                                        standard=True)[0].double().cpu().numpy()
+        want = np.sum(24 * np.sum(Vf ** 2, 2) ** 2, 1) / (3 * 6)
+        np.testing.assert_allclose(got, want, rtol=2e-5)
