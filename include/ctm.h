@@ -160,10 +160,10 @@ ctm_status ctm_set_weights(ctm_mlp_t mlp, const float *const *W, const float *co
 
 /* Hidden-layer activation of a loaded MLP (default CTM_ACT_TANH, the paper's).
  * Every operator applies the Taylor rules of the selected s with its derivatives
- * s', s'', s''', s'''' (sin: cos, -sin, -cos, sin; square z^2: 2z, 2, 0, 0; identity:
- * 1, 0, 0, 0). Host-side setting, takes effect for the next call. CTM_EINVAL for an
+ * s', s'', s''', s'''' (sin: cos, -sin, -cos, sin; exp: all exp z, SPEC S:123 names sin/exp;
+ * square z^2: 2z, 2, 0, 0; identity: 1, 0, 0, 0). Host-side setting, takes effect for the next call. CTM_EINVAL for an
  * unknown code or a NULL handle. */
-typedef enum { CTM_ACT_TANH = 0, CTM_ACT_IDENTITY = 1, CTM_ACT_SQUARE = 2, CTM_ACT_SIN = 3 } ctm_activation;
+typedef enum { CTM_ACT_TANH = 0, CTM_ACT_IDENTITY = 1, CTM_ACT_SQUARE = 2, CTM_ACT_SIN = 3, CTM_ACT_EXP = 4 } ctm_activation;
 ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
 
 /* Weighted Laplacian with a point-dependent sigma (Eq. 10; "sigma can depend on x0",

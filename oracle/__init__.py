@@ -22,9 +22,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ctmo.c")
 _LIB = os.path.join(_HERE, "libctmo.so")
 
-TANH, IDENTITY, SQUARE, SIN = 0, 1, 2, 3
+TANH, IDENTITY, SQUARE, SIN, EXP = 0, 1, 2, 3, 4
 O1, O2, O3 = 1, 2, 3
-ACTS = {"tanh": TANH, "identity": IDENTITY, "square": SQUARE, "sin": SIN}
+ACTS = {"tanh": TANH, "identity": IDENTITY, "square": SQUARE, "sin": SIN, "exp": EXP}
 
 
 def build(force: bool = False) -> str:

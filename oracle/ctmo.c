@@ -64,6 +64,9 @@ void ctmo_act_derivs(int32_t act, double z, double *d)
     case CTMO_SIN:
         d[0] = sin(z); d[1] = cos(z); d[2] = -sin(z); d[3] = -cos(z); d[4] = sin(z);
         break;
+    case CTMO_EXP:  /* every derivative of exp is exp */
+        d[0] = d[1] = d[2] = d[3] = d[4] = exp(z);
+        break;
     default:
         d[0] = d[1] = d[2] = d[3] = d[4] = NAN;
     }

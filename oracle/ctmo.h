@@ -22,7 +22,7 @@ extern "C" {
 
 /* Elementwise activation of the hidden layers. The product path is tanh-only
  * (P:1032); the others exist so closed forms can be expressed as MLPs. */
-enum { CTMO_TANH = 0, CTMO_IDENTITY = 1, CTMO_SQUARE = 2, CTMO_SIN = 3 };
+enum { CTMO_TANH = 0, CTMO_IDENTITY = 1, CTMO_SQUARE = 2, CTMO_SIN = 3, CTMO_EXP = 4 };
 
 /* Evaluation routes:
  *  O1 vanilla (standard) Taylor mode: one K-jet per direction, top coefficients

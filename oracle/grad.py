@@ -27,7 +27,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-_ACTS = ("tanh", "identity", "square", "sin")
+_ACTS = ("tanh", "identity", "square", "sin", "exp")
 
 
 def _derivs(act: str, z: torch.Tensor):
@@ -39,6 +39,9 @@ def _derivs(act: str, z: torch.Tensor):
         return torch.sin(z), torch.cos(z), -torch.sin(z)
     if act == "square":
         return z * z, 2 * z, torch.full_like(z, 2.0)
+    if act == "exp":
+        e = torch.exp(z)
+        return e, e, e
     if act == "identity":
         return z, torch.ones_like(z), torch.zeros_like(z)
     raise ValueError(act)

@@ -114,14 +114,14 @@ def plan_blocks(order: int, R: int, forced_rb: int = 0) -> dict:
     return {k: o.value for k, o in zip(keys, out)}
 
 
-ACTIVATIONS = {"tanh": 0, "identity": 1, "square": 2, "sin": 3}  # ctm_activation
+ACTIVATIONS = {"tanh": 0, "identity": 1, "square": 2, "sin": 3, "exp": 4}  # ctm_activation
 
 
 class MLP:
     """An MLP f: R^D -> R loaded into libctm (weights copied to the device).
 
     params: sequence of (W_l [w_l, w_{l-1}], b_l [w_l]) as in ``torch.nn.Linear``;
-    the activation (tanh by default; or sin, identity, square) after every layer
+    the activation (tanh by default; or sin, exp, identity, square) after every layer
     but the last.
     """
 

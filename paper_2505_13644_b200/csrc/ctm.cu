@@ -1401,10 +1401,11 @@ ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64
 ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act) {
   g_last_error.clear();
   if (!mlp) return fail(CTM_EINVAL, "NULL handle");
-  if (act != CTM_ACT_TANH && act != CTM_ACT_IDENTITY && act != CTM_ACT_SQUARE && act != CTM_ACT_SIN)
+  if (act != CTM_ACT_TANH && act != CTM_ACT_IDENTITY && act != CTM_ACT_SQUARE && act != CTM_ACT_SIN &&
+      act != CTM_ACT_EXP)
     return fail(CTM_EINVAL, "unknown activation");
   static_assert(CTM_ACT_TANH == ctm::kActTanh && CTM_ACT_IDENTITY == ctm::kActIdentity &&
-                    CTM_ACT_SQUARE == ctm::kActSquare && CTM_ACT_SIN == ctm::kActSin,
+                    CTM_ACT_SQUARE == ctm::kActSquare && CTM_ACT_SIN == ctm::kActSin && CTM_ACT_EXP == ctm::kActExp,
                 "ABI activation codes");
   mlp->act = (int)act;
   return CTM_OK;

@@ -80,9 +80,9 @@ constexpr int kNestMaxD = 20;
 constexpr int kBwd2 = 6;
 
 // Hidden-layer activation s and its derivatives s', s'', s''', s'''' at z (the Taylor
-// rules only ever need these five numbers). tanh is the paper's; sin, identity
+// rules only ever need these five numbers). tanh is the paper's; sin, exp, identity
 // and square extend the path and turn closed forms into GPU tests.
-enum : int { kActTanh = 0, kActIdentity = 1, kActSquare = 2, kActSin = 3 };
+enum : int { kActTanh = 0, kActIdentity = 1, kActSquare = 2, kActSin = 3, kActExp = 4 };
 struct ActD {
   float d0, d1, d2, d3, d4;
 };
@@ -100,6 +100,9 @@ __device__ __forceinline__ ActD act_derivs(int act, float z) {
     float sn, cs;
     sincosf(z, &sn, &cs);
     r.d0 = sn; r.d1 = cs; r.d2 = -sn; r.d3 = -cs; r.d4 = sn;
+  } else if (act == kActExp) {
+    const float e = expf(z);
+    r.d0 = e; r.d1 = e; r.d2 = e; r.d3 = e; r.d4 = e;
   } else if (act == kActSquare) {
     r.d0 = z * z; r.d1 = 2.f * z; r.d2 = 2.f; r.d3 = 0.f; r.d4 = 0.f;
   } else {

@@ -117,17 +117,18 @@ def test_weighted_randomized_pointwise_and_directional_gradients(ctm):
         _check_grads(f"directional_pp{int(per_point)}", mlp.backward(g_op, g_f), dW, db)
 
 
-def test_sin_activation_gradients(ctm):
+@pytest.mark.parametrize("act", ["sin", "exp"])
+def test_sin_exp_activation_gradients(ctm, act):
     widths = [4, 32, 24, 1]
     params = mlp_params(widths, 0)
     X = points(8, 4)
     gop, gf = _gs(8)
-    mlp = _mlp(ctm, params, act="sin")
+    mlp = _mlp(ctm, params, act=act)
     mlp.laplacian(torch.from_numpy(X).cuda())
     grads = mlp.backward(torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda())
     _, _, dW, db = OG.k2_grad([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params],
-                              X.astype(np.float64), np.eye(4), np.ones(4), gop, gf, act="sin")
-    _check_grads("sin", grads, dW, db)
+                              X.astype(np.float64), np.eye(4), np.ones(4), gop, gf, act=act)
+    _check_grads(act, grads, dW, db)
 
 
 def test_backward_is_deterministic_accumulates_and_needs_a_tape(ctm):

@@ -310,15 +310,18 @@ def test_square_net_closed_forms_on_gpu(ctm):
     np.testing.assert_allclose(got.double().cpu().numpy(), want, rtol=2e-5, atol=1e-5 * abs(want))
 
 
-@pytest.mark.parametrize("widths,N", [([5, 40, 32, 1], 13), (C1_WIDTHS, 9)])
-def test_sin_activation_parity_all_operators(ctm, widths, N):
+@pytest.mark.parametrize("widths,N,act", [([5, 40, 32, 1], 13, "sin"), (C1_WIDTHS, 9, "sin"),
+                                          ([5, 40, 32, 1], 13, "exp"), (C1_WIDTHS, 9, "exp")])
+def test_sin_exp_activation_parity_all_operators(ctm, widths, N, act):
     params, _ = nets(widths)
-    onet = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params], "sin")
+    if act == "exp":  # keep exp's pre-activations O(1) through the depth
+        params = [(W * np.float32(0.3 if l < len(params) - 1 else 1.0), b) for l, (W, b) in enumerate(params)]
+    onet = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params], act)
     D = widths[0]
     X = points(N, D)
     Xc = torch.from_numpy(X).cuda()
     Xd = X.astype(np.float64)
-    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act="sin")
+    mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0, act=act)
     want, fw, norm = O.laplacian(onet, Xd)
     op, f = mlp.laplacian(Xc)
     check(op, want, norm, f, fw)

@@ -106,9 +106,9 @@ def test_biharmonic_set_1d_is_fourth_derivative():
 # --------------------------------------------------------------------------
 # Activation derivatives: central differences
 # --------------------------------------------------------------------------
-@pytest.mark.parametrize("act", ["tanh", "sin", "square", "identity"])
+@pytest.mark.parametrize("act", ["tanh", "sin", "exp", "square", "identity"])
 def test_act_derivs_finite_differences(act):
-    ref0 = {"tanh": np.tanh, "sin": np.sin, "square": np.square, "identity": lambda z: z}[act]
+    ref0 = {"tanh": np.tanh, "sin": np.sin, "exp": np.exp, "square": np.square, "identity": lambda z: z}[act]
     h = 1e-4
     for z in (-1.3, -0.2, 0.0, 0.4, 1.1, 2.2):
         d = O.act_derivs(act, z)
@@ -197,6 +197,27 @@ def test_sum_of_sines(route):
     sig = rng.standard_normal((D, 2))
     diagD = np.sum(sig**2, axis=1)  # (sigma sigma^T)_dd ; H is diagonal
     np.testing.assert_allclose(O.weighted_laplacian(net, X, sig, route)[0], -(s * a * bvec**2 * diagD).sum(1), rtol=1e-12)
+
+
+
+@pytest.mark.parametrize("route", ROUTES)
+def test_sum_of_exponentials(route):
+    # f = sum_j c_j exp(a_j^T x + b_j) (exp activation): every derivative of
+    # exp is exp, so Laplacian = sum_j c_j e_j ||a_j||^2, weighted: ||sigma^T a_j||^2,
+    # biharmonic = sum_j c_j e_j ||a_j||^4.
+    rng = np.random.default_rng(10)
+    D, H = 3, 4
+    A, b, c = rng.uniform(-0.8, 0.8, (H, D)), rng.uniform(-0.5, 0.5, H), rng.uniform(-1, 1, H)
+    net = O.Net([A, c[None, :]], [b, np.array([0.2])], "exp")
+    X = _pts(5, D)
+    e = np.exp(X @ A.T + b)
+    n2 = np.sum(A**2, 1)
+    np.testing.assert_allclose(O.forward(net, X), e @ c + 0.2, rtol=1e-13)
+    np.testing.assert_allclose(O.laplacian(net, X, route)[0], e @ (c * n2), rtol=1e-12)
+    np.testing.assert_allclose(O.biharmonic(net, X, route)[0], e @ (c * n2**2), rtol=1e-11)
+    sig = rng.standard_normal((D, 2))
+    np.testing.assert_allclose(O.weighted_laplacian(net, X, sig, route)[0], e @ (c * np.sum((A @ sig) ** 2, 1)),
+                               rtol=1e-12)
 
 
 def _tanh_derivs_autograd(z, k):

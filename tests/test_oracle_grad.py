@@ -11,7 +11,7 @@ def _pts(N, D, seed=5):
     return np.random.default_rng(seed).uniform(-1, 1, size=(N, D))
 
 
-@pytest.mark.parametrize("act", ["tanh", "sin"])
+@pytest.mark.parametrize("act", ["tanh", "sin", "exp"])
 def test_values_match_the_c_oracle(act):
     D = 4
     Ws, bs = random_params([D, 9, 7, 1], 3, scale=1.5)
