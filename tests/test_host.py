@@ -204,3 +204,46 @@ def test_direction_block_planner_choices():
         ctm.plan_blocks(2, 300, 300)
     with pytest.raises(ctm.CTMError, match="EINVAL"):
         ctm.plan_blocks(6, 10)
+
+
+def test_product_package_never_touches_the_oracle():
+    """The product path (the package and its kernels) shares no code with oracle/ and
+    never imports it; only tests, smoke() and bench's CPU arms may."""
+    import ast
+    import pathlib
+
+    pkg = pathlib.Path(__file__).resolve().parents[1] / "paper_2505_13644_b200"
+    files = list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("*.h"))
+    assert files
+    for f in files:
+        src = f.read_text()
+        if f.suffix == ".py":
+            for node in ast.walk(ast.parse(src)):
+                if isinstance(node, ast.Import):
+                    assert all(not a.name.split(".")[0] == "oracle" for a in node.names), f
+                elif isinstance(node, ast.ImportFrom):
+                    assert (node.module or "").split(".")[0] != "oracle", f
+        else:
+            assert "ctmo" not in src and "oracle/" not in src, f
+
+
+def test_product_path_fails_loudly_without_the_library(monkeypatch, tmp_path):
+    """No CPU fallback: with libctm.so missing, loading raises instead of computing."""
+    import paper_2505_13644_b200 as ctm
+
+    monkeypatch.setattr(ctm, "_lib", None)
+    monkeypatch.setattr(ctm, "LIB_PATH", str(tmp_path / "libctm.so"))
+    with pytest.raises(ctm.CTMError, match="no fallback"):
+        ctm.lib()
+
+
+def test_product_path_raises_without_a_gpu():
+    """On a machine without a CUDA device the operators raise (nothing runs on the CPU)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2505_13644_b200 as ctm
+
+    with pytest.raises(Exception):
+        ctm.MLP([(torch.zeros(4, 3), torch.zeros(4)), (torch.zeros(1, 4), torch.zeros(1))], device=0)
