@@ -625,3 +625,26 @@ def test_direction_blocks_are_exact_in_the_collapsed_route():
         cuts = [0, 7, 8, 15, J]
         parts = sum(O.directional_sum(net, X, K, dirs[a:b], w[a:b], O.O3)[0] for a, b in zip(cuts, cuts[1:]))
         assert np.max(np.abs(parts - whole) / norm) < 1e-12
+
+
+def test_spec_worked_examples():
+    """The worked examples SPEC.md prints (tests/golden/spec_worked_examples.txt, cited per row)."""
+    want = {r[0]: float(r[1]) for r in golden("spec_worked_examples.txt")}
+    I = np.eye
+    for x0, name in ((np.pi / 4, "appC_sin_2jet_x0_pi4"), (0.0, "appC_sin_2jet_x0_0")):
+        net = O.Net([I(1), I(1)], [np.zeros(1), np.zeros(1)], "sin")  # f = sin(x), D = 1
+        for route in ROUTES:
+            got = O.directional_sum(net, np.array([[x0]]), 2, np.array([[1.0], [2.0]]), np.ones(2), route=route)[0]
+            np.testing.assert_allclose(got, want[name], rtol=1e-14, atol=1e-15)
+    half = lambda D: O.Net([I(D), np.full((1, D), 0.5)], [np.zeros(D), np.zeros(1)], "square")  # 1/2 ||x||^2
+    X7 = _pts(3, 7)
+    for route in ROUTES:
+        np.testing.assert_allclose(O.laplacian(half(7), X7, route)[0], want["half_norm2_D7_laplacian"], rtol=1e-13)
+        sig = np.zeros((4, 1))
+        sig[0, 0] = 2.0
+        np.testing.assert_allclose(O.weighted_laplacian(half(4), _pts(3, 4), sig, route)[0],
+                                   want["weighted_diag2_half_norm2"], rtol=1e-13)
+        norm4 = O.Net([I(2), np.ones((1, 2)), np.ones((1, 1))], [np.zeros(2), np.zeros(1), np.zeros(1)], "square")
+        np.testing.assert_allclose(O.biharmonic(norm4, _pts(3, 2), route)[0], want["norm4_D2_biharmonic"], rtol=1e-12)
+        x1p4 = O.Net([np.array([[1.0, 0, 0]]), np.ones((1, 1)), np.ones((1, 1))], [np.zeros(1)] * 3, "square")
+        np.testing.assert_allclose(O.biharmonic(x1p4, _pts(3, 3), route)[0], want["x1pow4_D3_biharmonic"], rtol=1e-12)
