@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import oracle as O
-from tests._util import magnitude_k2
+from tests._util import golden, magnitude_k2
 from synth import (gaussian_directions, mlp_params, points, sigma as make_sigma, sigma_field, signed_weights,
                    widths_for)
 
@@ -1111,3 +1111,31 @@ def test_square_net_closed_forms_standard_modes_and_blocks(ctm):
                                         standard=True)[0].double().cpu().numpy()
         want = np.sum(24 * np.sum(Vf ** 2, 2) ** 2, 1) / (3 * 6)
         np.testing.assert_allclose(got, want, rtol=2e-5)
+
+
+def test_spec_worked_examples_through_the_library(ctm):
+    """SPEC's worked examples (tests/golden/spec_worked_examples.txt) through the C ABI."""
+    want = {r[0]: float(r[1]) for r in golden("spec_worked_examples.txt")}
+    T = lambda a: torch.tensor(np.asarray(a, np.float32))
+    I = lambda D: np.eye(D, dtype=np.float32)
+    z = lambda n: np.zeros(n, np.float32)
+    sin_net = ctm.MLP([(T(I(1)), T(z(1))), (T(I(1)), T(z(1)))], device=0, act="sin")
+    for x0, name in ((np.pi / 4, "appC_sin_2jet_x0_pi4"), (0.0, "appC_sin_2jet_x0_0")):
+        got = sin_net.directional_sum(T([[x0]]).cuda(), 2, T([[1.0], [2.0]]).cuda(), T([1.0, 1.0]).cuda())[0]
+        np.testing.assert_allclose(got.double().cpu().numpy(), want[name], rtol=2e-5, atol=1e-5)
+
+    def half(D):
+        return ctm.MLP([(T(I(D)), T(z(D))), (T(np.full((1, D), 0.5)), T(z(1)))], device=0, act="square")
+
+    X = lambda N, D: torch.from_numpy(points(N, D)).cuda()
+    np.testing.assert_allclose(half(7).laplacian(X(5, 7))[0].cpu().numpy(), want["half_norm2_D7_laplacian"], rtol=2e-5)
+    sig = np.zeros((4, 1), np.float32)
+    sig[0, 0] = 2.0
+    np.testing.assert_allclose(half(4).weighted_laplacian(X(5, 4), T(sig).cuda())[0].cpu().numpy(),
+                               want["weighted_diag2_half_norm2"], rtol=2e-5)
+    norm4 = ctm.MLP([(T(I(2)), T(z(2))), (T(np.ones((1, 2))), T(z(1))), (T(np.ones((1, 1))), T(z(1)))], device=0,
+                    act="square")
+    np.testing.assert_allclose(norm4.biharmonic(X(5, 2))[0].cpu().numpy(), want["norm4_D2_biharmonic"], rtol=2e-5)
+    x1p4 = ctm.MLP([(T([[1.0, 0, 0]]), T(z(1))), (T(np.ones((1, 1))), T(z(1))), (T(np.ones((1, 1))), T(z(1)))],
+                   device=0, act="square")
+    np.testing.assert_allclose(x1p4.biharmonic(X(5, 3))[0].cpu().numpy(), want["x1pow4_D3_biharmonic"], rtol=2e-5)
