@@ -33,7 +33,50 @@ def rel_err(a, b, norm):
     return np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.asarray(norm))
 
 
-def magnitude_k2(Ws, bs, X, dirs, coef):
+def _abs_derivs(act, z):
+    """s and |s'|, |s''|, |s'''|, |s''''| of the activation at z (textbook derivatives)."""
+    if act == "tanh":
+        t = np.tanh(z)
+        s = 1.0 - t * t
+        return t, np.abs(s), np.abs(2 * t * s), np.abs(s * (6 * t * t - 2)), np.abs(8 * t * s * (2 - 3 * t * t))
+    if act == "sin":
+        sn, cs = np.abs(np.sin(z)), np.abs(np.cos(z))
+        return np.sin(z), cs, sn, cs, sn
+    raise ValueError(act)
+
+
+def magnitude_k4(Ws, bs, X, dirs, coef, act="tanh"):
+    """Running magnitude M of the fourth-order Taylor computation (K = 4), as magnitude_k2
+    for K = 2: the vanilla per-jet rules (Eq. 3 with K = 4, the rows of P:1370-1424)
+        x1' = s1 x1,  x2' = s2 x1^2 + s1 x2,  x3' = s3 x1^3 + 3 s2 x1 x2 + s1 x3,
+        x4' = s4 x1^4 + 6 s3 x1^2 x2 + 4 s2 x1 x3 + 3 s2 x2^2 + s1 x4     (sk = k-th derivative)
+    with every quantity replaced by a bound of its absolute value, and
+    M = sum_j |c_j| |w_out| A4_j. Ws/bs fp64; X [N, D]; dirs [J, D] or [N, J, D]; coef
+    scalar or [J]. Test infrastructure only."""
+    X = np.asarray(X, np.float64)
+    dirs = np.asarray(dirs, np.float64)
+    if dirs.ndim == 2:
+        dirs = np.broadcast_to(dirs, (X.shape[0],) + dirs.shape)
+    c = np.abs(np.broadcast_to(np.asarray(coef, np.float64), dirs.shape[1:2]))
+    out = np.empty(X.shape[0])
+    for n, x in enumerate(X):
+        h0 = x
+        A1 = np.abs(dirs[n])
+        A2 = np.zeros_like(A1)
+        A3 = np.zeros_like(A1)
+        A4 = np.zeros_like(A1)
+        for W, b in zip(Ws[:-1], bs[:-1]):
+            aW = np.abs(W)
+            z0 = W @ h0 + b
+            Z1, Z2, Z3, Z4 = A1 @ aW.T, A2 @ aW.T, A3 @ aW.T, A4 @ aW.T
+            h0, d1, d2, d3, d4 = _abs_derivs(act, z0)
+            A1, A2, A3, A4 = (d1 * Z1, d2 * Z1**2 + d1 * Z2, d3 * Z1**3 + 3 * d2 * Z1 * Z2 + d1 * Z3,
+                              d4 * Z1**4 + 6 * d3 * Z1**2 * Z2 + 4 * d2 * Z1 * Z3 + 3 * d2 * Z2**2 + d1 * Z4)
+        out[n] = float(c @ (A4 @ np.abs(Ws[-1][0])))
+    return out
+
+
+def magnitude_k2(Ws, bs, X, dirs, coef, act="tanh"):
     """Running magnitude M of the second-order Taylor computation (K = 2, tanh).
 
     The same coefficient rules as the oracle's vanilla route (Eq. 3 with K = 2:
@@ -63,9 +106,7 @@ def magnitude_k2(Ws, bs, X, dirs, coef):
             aW = np.abs(W)
             z0 = W @ h0 + b
             Z1, Z2 = A1 @ aW.T, A2 @ aW.T
-            t = np.tanh(z0)
-            d1 = 1.0 - t * t
-            d2 = -2.0 * t * d1
-            h0, A1, A2 = t, np.abs(d1) * Z1, np.abs(d2) * Z1 ** 2 + np.abs(d1) * Z2
+            t, d1, d2, _, _ = _abs_derivs(act, z0)
+            h0, A1, A2 = t, d1 * Z1, d2 * Z1 ** 2 + d1 * Z2
         out[n] = float(c @ (A2 @ np.abs(Ws[-1][0])))
     return out

@@ -1,9 +1,10 @@
 """Pins for the condition-aware fallback bound used by the small-net GPU edge tests
 (tests/_util.magnitude_k2, DESIGN.md §5 reading R9). CPU only."""
 import numpy as np
+import pytest
 
 import oracle as O
-from tests._util import magnitude_k2, random_params
+from tests._util import magnitude_k2, magnitude_k4, random_params
 
 
 def test_magnitude_equals_value_when_nothing_cancels():
@@ -64,3 +65,62 @@ def test_magnitude_is_homogeneous_and_catches_a_dropped_term():
         x2 = d2 * z1 ** 2                               # dropped: + d1 * z2
         bad[n] = float((x2 @ Ws[2][0]).sum())
     assert np.all(np.abs(bad - want) > 1e-3 * M)
+
+
+def test_magnitude_k4_equals_value_when_nothing_cancels():
+    """One hidden layer, D = 1: f'''' = sum_j w2_j s''''(z_j) w1_j^4. With
+    w2_j = sign(s''''(z_j)) every term is non-negative, so M equals the exact f''''."""
+    Ws, bs = random_params([1, 9, 1], seed=4)
+    x = np.array([[0.21]])
+    z = Ws[0] @ x[0] + bs[0]
+    t = np.tanh(z)
+    s4 = 8 * t * (1 - t * t) * (2 - 3 * t * t)
+    Ws[1] = np.sign(s4)[None, :] * np.abs(Ws[1])
+    want, _, _ = O.biharmonic(O.Net(Ws, bs), x)
+    assert want[0] > 0
+    np.testing.assert_allclose(magnitude_k4(Ws, bs, x, np.eye(1), 1.0), want, rtol=1e-12)
+
+
+@pytest.mark.parametrize("act", ["tanh", "sin"])
+def test_magnitude_k4_bounds_the_normaliser(act):
+    """Triangle inequality: M >= sum_j |c_j f_{4,j}| for the biharmonic family and for
+    random weighted jets (shared and per point), deep nets, any signs."""
+    rng = np.random.default_rng(2)
+    for trial in range(8):
+        D = int(rng.integers(1, 5))
+        widths = [D] + [int(rng.integers(4, 30)) for _ in range(int(rng.integers(1, 4)))] + [1]
+        Ws, bs = random_params(widths, seed=trial)
+        net = O.Net(Ws, bs, act)
+        X = rng.uniform(-1, 1, size=(3, D))
+        dirs, coef = O.biharmonic_set(D)
+        _, _, norm = O.biharmonic(net, X)
+        assert np.all(magnitude_k4(Ws, bs, X, dirs, coef, act) >= norm * (1 - 1e-12))
+        U = rng.normal(size=(3, 4, D))
+        w = rng.normal(size=4)
+        _, _, norm = O.directional_sum(net, X, 4, U, w)
+        assert np.all(magnitude_k4(Ws, bs, X, U, w, act) >= norm * (1 - 1e-12))
+
+
+def test_magnitude_k4_catches_a_dropped_term():
+    """Dropping any one term of the K = 4 rule in one layer moves f'''' by more than
+    10x the fallback tolerance (1e-5 M), so the fallback cannot hide that bug."""
+    Ws, bs = random_params([1, 12, 10, 1], seed=9)
+    x = np.array([0.3])
+    want = O.biharmonic(O.Net(Ws, bs, "tanh"), x[None, :])[0][0]
+
+    def derivs(z):
+        t = np.tanh(z)
+        s1 = 1 - t * t
+        return t, s1, -2 * t * s1, s1 * (6 * t * t - 2), 8 * t * s1 * (2 - 3 * t * t)
+
+    t, s1, s2, s3, s4 = derivs(Ws[0] @ x + bs[0])
+    u = Ws[0][:, 0]
+    x1, x2, x3, x4 = s1 * u, s2 * u**2, s3 * u**3, s4 * u**4
+    z1, z2, z3, z4 = Ws[1] @ x1, Ws[1] @ x2, Ws[1] @ x3, Ws[1] @ x4
+    _, s1, s2, s3, s4 = derivs(Ws[1] @ t + bs[1])
+    good = s4 * z1**4 + 6 * s3 * z1**2 * z2 + 4 * s2 * z1 * z3 + 3 * s2 * z2**2 + s1 * z4
+    np.testing.assert_allclose(Ws[2][0] @ good, want, rtol=1e-10)  # the restated rule is the oracle's
+    M = magnitude_k4(Ws, bs, x[None, :], np.eye(1), 1.0)[0]
+    for term in (s4 * z1**4, 6 * s3 * z1**2 * z2, 4 * s2 * z1 * z3, 3 * s2 * z2**2, s1 * z4):
+        bad = Ws[2][0] @ (good - term)
+        assert abs(bad - want) > 1e-4 * M  # 10x the fallback tolerance 1e-5 M
