@@ -180,6 +180,12 @@ def oracle_rate(D, widths, op, S, budget_s, seed_pts=1):
 def reference_arm(args, rank):
     if rank != 0:
         return
+    # rank 0 runs alone (the other ranks exit without work): give the oracle every host
+    # core, as at N = 1 (torchrun exports OMP_NUM_THREADS=1 to each rank)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import oracle as O
+
+        O.set_num_threads(os.cpu_count() or 1)
     D, widths, wl = workload(args)
     per_step = []
     total_pts = 0

@@ -79,6 +79,8 @@ def lib():
         _lib.ctmo_splitmix64.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         _lib.ctmo_splitmix64.restype = ctypes.c_uint64
         _lib.ctmo_num_threads.restype = ctypes.c_int32
+        _lib.ctmo_set_num_threads.argtypes = [i32]
+        _lib.ctmo_set_num_threads.restype = None
     return _lib
 
 
@@ -242,3 +244,8 @@ def splitmix64(seed: int, idx: int) -> int:
 
 def num_threads() -> int:
     return int(lib().ctmo_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops over points (no arithmetic change)."""
+    lib().ctmo_set_num_threads(int(n))

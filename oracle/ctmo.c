@@ -968,6 +968,17 @@ void ctmo_rademacher(uint64_t seed, int64_t point_offset, int64_t N, int32_t S, 
             }
 }
 
+/* Host threads for the OpenMP loops over points (bench.py's reference arm runs on rank 0
+ * alone under torchrun, which sets OMP_NUM_THREADS=1 for every rank). No arithmetic. */
+void ctmo_set_num_threads(int32_t n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int32_t ctmo_num_threads(void)
 {
 #ifdef _OPENMP

@@ -121,6 +121,7 @@ void ctmo_rademacher(uint64_t seed, int64_t point_offset, int64_t N, int32_t S, 
 uint64_t ctmo_splitmix64(uint64_t seed, uint64_t idx);
 
 /* Number of OpenMP threads the oracle uses (for the cpu_baseline report). */
+void ctmo_set_num_threads(int32_t n);
 int32_t ctmo_num_threads(void);
 
 #ifdef __cplusplus
