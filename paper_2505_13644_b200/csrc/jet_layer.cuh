@@ -355,13 +355,13 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
 // one TMEM load and one wait for the whole point (the general loop waits for the primal,
 // the middle slots and the top separately). Same operations in the same order as
 // epilogue_point, so the two give identical bits.
-template <int FLAGS>
+template <int FLAGS, int PC = 0>
 __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint32_t tcol, int64_t row, int m,
                                                      float bias, float wo, const float* jw, float& fpart,
                                                      float& opart) {
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
   constexpr bool wsum = (FLAGS & kFlagWeighted) != 0;
-  const int P = p.P;
+  const int P = PC > 0 ? PC : p.P;  // PC: the slot count as a compile-time constant
   const size_t ld = (size_t)p.ldo;
   float v[16];
   ptx::tmem_ld16(tcol, v);
@@ -926,10 +926,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           const int jbase = (kW && p.blocks > 1) ? ((blk0 + pt) % p.blocks) * p.rb : 0;
           // (the plain K=2 instance runs only with < 8 points per tile, i.e. P > 28: no small path)
           constexpr bool kSmall = (KORD == 2) && (FLAGS != 0);
-          if (kSmall && p.P <= 16 && pt * p.P + 16 <= kMaxN)
-            epilogue_point_small<FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
-                                        jw + jbase, fpart, opart);
-          else
+          if (kSmall && p.P <= 16 && pt * p.P + 16 <= kMaxN) {
+            // P <= 12 as a compile-time constant: no runtime slot guards in the unrolled
+            // loop (the epilogue is issue-bound there: S=4 +6%, S=8 +1.6%; P = 13..16 gained
+            // nothing measurable and keep the runtime-P instance)
+            const uint32_t tc = tbase + (uint32_t)(pt * p.P);
+            const int64_t rw = row0 + (int64_t)pt * p.P;
+            switch (p.P) {
+#define CTM_SMALL_CASE(n) \
+  case n: epilogue_point_small<FLAGS, n>(p, tc, rw, m, bias, wo, jw + jbase, fpart, opart); break;
+              CTM_SMALL_CASE(3) CTM_SMALL_CASE(4) CTM_SMALL_CASE(5) CTM_SMALL_CASE(6) CTM_SMALL_CASE(7)
+              CTM_SMALL_CASE(8) CTM_SMALL_CASE(9) CTM_SMALL_CASE(10) CTM_SMALL_CASE(11) CTM_SMALL_CASE(12)
+#undef CTM_SMALL_CASE
+              default: epilogue_point_small<FLAGS>(p, tc, rw, m, bias, wo, jw + jbase, fpart, opart); break;
+            }
+          } else
             epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
                                         jw + jbase, 0, 0, nullptr, 0, fpart, opart);
           if (p.readout) {
