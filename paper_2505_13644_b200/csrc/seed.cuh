@@ -144,15 +144,20 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       *reinterpret_cast<float4*>(p.z_out + (row0 + 1 + p.R) * p.ld + m) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     CTM_BLOCK_BEGIN
-    // batches of 4 rows: the 4 loads of U are in flight together (latency, not bandwidth,
-    // bounded this loop when each load fed its stores one at a time)
     int r = r0;
-    for (; r + 4 <= r1; r += 4) {
-      float4 u[4];
+// batches of 8 rows: 8 loads of U^T in flight per thread (the loads, not the stores, bound
+// this loop -- ncu: 42% of stall samples at the first use of a U^T value; C1 seed
+// 0.60-0.62 -> 0.50-0.54 ms against batches of 4; 16 ran out of registers under the
+// launch bound and was slower)
+#ifndef CTM_SEED_BATCH
+#define CTM_SEED_BATCH 8
+#endif
+    for (; r + CTM_SEED_BATCH <= r1; r += CTM_SEED_BATCH) {
+      float4 u[CTM_SEED_BATCH];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) u[i] = ldg4(p.UT + (size_t)(r + i) * p.ld + m);
+      for (int i = 0; i < CTM_SEED_BATCH; ++i) u[i] = ldg4(p.UT + (size_t)(r + i) * p.ld + m);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < CTM_SEED_BATCH; ++i)
         seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0 + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
                     d1[2] * u[i].z, d1[3] * u[i].w);
     }
