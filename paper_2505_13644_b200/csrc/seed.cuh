@@ -105,14 +105,25 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
   if (KORD == kStd2) {
     CTM_BLOCK_BEGIN
     // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
-#pragma unroll 4
-    for (int r = r0; r < r0 + p.rb; ++r) {
-      const float4 u = (r < r1) ? ldg4(p.UT + (size_t)r * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f);
+    auto pair = [&](const float4 u, int r) {
       const size_t rr = row0 + 1 + 2 * (r - r0);
       seed_store4(p.out_hi, p.out_lo, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
       seed_store4(p.out_hi, p.out_lo, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
+    };
+    int r = r0;
+#ifndef CTM_SEED_BATCHS
+#define CTM_SEED_BATCHS 8
+#endif
+    for (; r + CTM_SEED_BATCHS <= r1; r += CTM_SEED_BATCHS) {  // U^T loads in flight together
+      float4 u[CTM_SEED_BATCHS];
+#pragma unroll
+      for (int i = 0; i < CTM_SEED_BATCHS; ++i) u[i] = ldg4(p.UT + (size_t)(r + i) * p.ld + m);
+#pragma unroll
+      for (int i = 0; i < CTM_SEED_BATCHS; ++i) pair(u[i], r + i);
     }
+    for (; r < r0 + p.rb; ++r)
+      pair((r < r1) ? ldg4(p.UT + (size_t)r * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f), r);
     CTM_BLOCK_END
   } else if (KORD == kStd4) {
     CTM_BLOCK_BEGIN
