@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--direction-block", type=int, default=0,
                     help="directions per block (ctm_set_direction_block); 0 = the library's planner")
+    ap.add_argument("--precision", choices=["fp32", "bf16x3"], default="fp32",
+                    help="layer-contraction arithmetic (ctm_set_precision, DESIGN.md §5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: total CPU seconds spread over the warm-up + timed steps")
@@ -235,6 +237,8 @@ def main():
     params = mlp_params(widths, 0)
     mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=local)
     mlp.set_direction_block(args.direction_block)
+    mlp.set_precision(args.precision)
+    prods = 6 if args.precision == "fp32" else 3  # bf16 tensor products per useful product
     # each rank: its own contiguous slice of the global point set (global index rank*N ...)
     X_host = points(N * world, D, 1)[rank * N:(rank + 1) * N]
     X = torch.from_numpy(X_host).to(dev)
@@ -411,7 +415,7 @@ def main():
         peak_src = "fallback"
     bf16_sust = peaks.get("bf16_tflops_sustained", 1400.0)
     tensor_peak = bf16_sust                # the layer MMAs are kind::f16 with bf16 operands
-    useful_peak = tensor_peak / 3.0        # 3xBF16: three tensor products per useful product
+    useful_peak = tensor_peak / prods      # bf16 tensor products per useful fp32-accurate product
     dom = max(("layer", "bwd", "wgrad"), key=lambda k: prof[k]["ms"]) if train else "layer"
     lay = prof[dom]
     achieved = lay["work"] / (lay["ms"] / 1e3) / 1e12 if lay["ms"] > 0 else None
@@ -431,13 +435,13 @@ def main():
         "bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
         "frac": (achieved / useful_peak) if achieved else None, "traffic": traffic,
         "kernel": kernel_name,
-        "peak_basis": (f"{peak_src} bf16 sustained {bf16_sust} TF/s / 3 (3xBF16 split: three bf16 tensor "
-                       "products per useful fp32-accurate product)"),
-        "tensor_pipe_frac": (3.0 * achieved / tensor_peak) if achieved else None,
+        "peak_basis": (f"{peak_src} bf16 sustained {bf16_sust} TF/s / {prods} (bf16 tensor "
+                       "products per useful product)"),
+        "tensor_pipe_frac": (prods * achieved / tensor_peak) if achieved else None,
         # context: the same against the burst bf16 rate (cuBLAS timed alone at full clocks);
         # the sustained peak above was measured with the clocks the power cap allows, so a
         # step that keeps 1965 MHz can exceed 1.0 against it
-        "frac_vs_burst": (3.0 * achieved / peaks["bf16_tflops"]) if achieved and "bf16_tflops" in peaks else None,
+        "frac_vs_burst": (prods * achieved / peaks["bf16_tflops"]) if achieved and "bf16_tflops" in peaks else None,
         "layer_ms_share": lay["ms"] / sum(step_ms) if sum(step_ms) > 0 else None,
         "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
         "launches_per_step": {k: v["launches"] / args.steps for k, v in prof.items()},
@@ -467,7 +471,9 @@ def main():
             "vs_baseline": (value / PAPER_PTS_PER_S[args.op]) if args.op in PAPER_PTS_PER_S else None,
             "vs_baseline_ref": ("paper P:1205, marginal ms/datum on an RTX 6000, PyTorch (another machine: context)"
                                 if args.op in PAPER_PTS_PER_S else "no published number for this operator"),
-            "dtype": "f32 (3xbf16 tensor products, fp32 accumulate)", "data": "synthetic",
+            "dtype": ("f32 (bf16x6: three bf16 planes per operand, six tensor products, fp32 accumulate)"
+                      if args.precision == "fp32" else "f32 storage, bf16x3 products (~17-bit operands, fp32 accumulate)"),
+            "data": "synthetic",
             "config": {"workload": wl, "op": args.op, "N_per_gpu": N, "D": D, "widths": widths,
                        "slots_per_point": plan["slots_per_point"], "points_per_tile": plan["points_per_tile"],
                        "mma_n": plan["mma_n"], "direction_blocks": plan["blocks"],

@@ -25,10 +25,13 @@
  *  - Results are bitwise deterministic run to run, and independent of how a
  *    batch is split into calls (no reduction depends on N or on a point's
  *    position; random directions are keyed on the global point index).
- *  - Arithmetic: fp32 values; the layer contractions run on tcgen05 tensor
- *    cores on bf16 pairs as 3xBF16 (hi*hi + hi*lo + lo*hi, fp32 accumulation); the Taylor
+ *  - Arithmetic (ctm_set_precision): fp32 values; the layer contractions run on
+ *    tcgen05 tensor cores on bf16 planes of every operand. Default CTM_PRECISION_FP32:
+ *    three planes (all 24 bits), six plane products, the five small ones over the
+ *    whole K before the leading one (fp32 accumulation). CTM_PRECISION_BF16X3: two
+ *    planes (~17 bits), three products per K step, half the tensor work. The Taylor
  *    rules run in fp32.  Accuracy target: |op - op_fp64| <= 1e-4 * sum_r
- *    |c_r f_{K,r}| (DESIGN.md §Tolerance).
+ *    |c_r f_{K,r}| (DESIGN.md §5).
  *  - Direction blocks: a point's R directions (K=4: J jets) may be split into nb
  *    blocks of rb, each propagated as its own slot group [x0; its directions; its
  *    partial collapsed top] of P = rb + 2 (K=2), 3 rb + 2 (K=4) or 1 + 2 rb
@@ -166,6 +169,19 @@ ctm_status ctm_set_weights(ctm_mlp_t mlp, const float *const *W, const float *co
 typedef enum { CTM_ACT_TANH = 0, CTM_ACT_IDENTITY = 1, CTM_ACT_SQUARE = 2, CTM_ACT_SIN = 3, CTM_ACT_EXP = 4 } ctm_activation;
 ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
 
+/* Arithmetic of the layer contractions for later calls on this handle.
+ * The paper computes in fp32 (PyTorch); collapsing is exact,
+ * so the arithmetic is the whole error budget of an operator value.
+ *   CTM_PRECISION_FP32 (default): every operand as three bf16 planes p0 + p1 + p2 (the
+ *     fp32 value to 2^-27), D = sum of the five correction products over the whole K, then
+ *     p0*p0 over the whole K, fp32 accumulation in TMEM: fp32-class error.
+ *   CTM_PRECISION_BF16X3: two planes, p1*p0 + p0*p1 + p0*p0 per K step ("3xBF16",
+ *     ~17 operand bits): about half the tensor time, ~2^-16 per product.
+ * Changing the precision invalidates a recorded tape (ctm_backward then fails).
+ * Errors: CTM_EINVAL (NULL handle, unknown value). */
+typedef enum { CTM_PRECISION_FP32 = 0, CTM_PRECISION_BF16X3 = 1 } ctm_precision;
+ctm_status ctm_set_precision(ctm_mlp_t mlp, ctm_precision prec);
+
 /* Weighted Laplacian with a point-dependent sigma (Eq. 10; "sigma can depend on x0",
  * P:686): op[n] = <d^2 f(x_n), sigma(x_n) sigma(x_n)^T> = sum_r <d^2 f(x_n), s_r(x_n)^2>.
  *   sigma_x [N, D, R] device, fp32: sigma(x_n) row-major [D, R] for each point (the
@@ -174,20 +190,6 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
  *   CTM_EINVAL (NULL sigma_x, R < 1), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 4096). */
 ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float *X, int64_t N, const float *sigma_x,
                                             int32_t R, float *op_out, float *f_out, void *stream);
-
-/* Weighted Laplacian for an arbitrary symmetric, possibly INDEFINITE weighting C
- * ("For indefinite D, we can simply apply this scheme to the positive and negative
- * eigen-spaces"): op[n] = <d^2 f(x_n), C> = sum_i lambda_i <d^2 f(x_n), q_i^{(x)2}> with
- * C = sum_i lambda_i q_i q_i^T. The eigendecomposition runs on the device per call
- * (cuSOLVER syevd in fp64, O(D^3), a setup step), then the collapsed K=2 directional sum
- * with directions q_i and signed weights lambda_i (one collapsed top).
- *   C [D, D] device, fp32, row-major, symmetric (the lower triangle is read).
- * Errors: CTM_EINVAL (NULL C), CTM_ESHAPE (misaligned), CTM_EUNSUPPORTED (D > 2048),
- * CTM_ECUDA (a cuSOLVER call failed). The call stays asynchronous, so the solver's
- * convergence flag (devInfo) is not read back; syevd on a symmetric matrix converges in
- * practice. */
-ctm_status ctm_weighted_laplacian_indefinite(ctm_mlp_t mlp, const float *X, int64_t N, const float *C,
-                                             float *op_out, float *f_out, void *stream);
 
 /* General linear operator of degree K as a weighted sum of K-th directional derivatives
  * (Eq. 5 `eq:sum-k-directional` P:548-558 with coefficients; the general approach of

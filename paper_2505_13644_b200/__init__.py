@@ -40,12 +40,12 @@ ABI = {
     ),
     "ctm_stochastic_biharmonic_standard": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP,
                                                           _VP, _VP]),
-    "ctm_weighted_laplacian_indefinite": (ctypes.c_int, [_VP, _VP, _I64, _VP, _VP, _VP, _VP]),
     "ctm_weighted_laplacian_pointwise": (ctypes.c_int, [_VP, _VP, _I64, _VP, _I32, _VP, _VP, _VP]),
     "ctm_directional_sum": (ctypes.c_int, [_VP, _VP, _I64, _I32, _I32, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ctm_stochastic_biharmonic": (ctypes.c_int, [_VP, _VP, _I64, _I32, _VP, ctypes.c_int, _U64, _I64, _VP, _VP,
                                                  _VP]),
     "ctm_set_activation": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "ctm_set_precision": (ctypes.c_int, [_VP, ctypes.c_int]),
     "ctm_grad_enable": (ctypes.c_int, [_VP, _I32]),
     "ctm_set_weights": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
     "ctm_backward": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP]),
@@ -96,6 +96,24 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream], device) -> int:
     return s.cuda_stream
 
 
+def _streamed(method):
+    """Run an operator method with ``stream`` as torch's current stream, so every
+    temporary (dtype/layout conversions, outputs) is allocated and written on the stream
+    the library's kernels run on: the caching allocator cannot hand a block back to
+    other work while the library still reads it (ctm.h: inputs stay valid until the
+    stream passes the call)."""
+    import functools
+
+    @functools.wraps(method)
+    def run(self, *args, stream=None, **kw):
+        if stream is None or stream == torch.cuda.current_stream(self.device):
+            return method(self, *args, **kw)
+        with torch.cuda.stream(stream):
+            return method(self, *args, **kw)
+
+    return run
+
+
 def _dev_f32(t: torch.Tensor, device, name: str) -> torch.Tensor:
     if not isinstance(t, torch.Tensor):
         t = torch.as_tensor(t)
@@ -115,6 +133,7 @@ def plan_blocks(order: int, R: int, forced_rb: int = 0) -> dict:
 
 
 ACTIVATIONS = {"tanh": 0, "identity": 1, "square": 2, "sin": 3, "exp": 4}  # ctm_activation
+PRECISIONS = {"fp32": 0, "bf16x3": 1}  # ctm_precision
 
 
 class MLP:
@@ -125,7 +144,8 @@ class MLP:
     but the last.
     """
 
-    def __init__(self, params: Sequence, device: int | str | torch.device | None = None, act: str = "tanh"):
+    def __init__(self, params: Sequence, device: int | str | torch.device | None = None, act: str = "tanh",
+                 precision: str = "fp32"):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
@@ -146,6 +166,18 @@ class MLP:
             raise CTMError(f"unknown activation {act!r}")
         _check(lib().ctm_set_activation(self._h, ACTIVATIONS[act]), "ctm_set_activation")
         self.act = act
+        self._grad = False
+        self._tape_n = None
+        self.set_precision(precision)
+
+    def set_precision(self, precision: str = "fp32"):
+        """Arithmetic of the layer contractions (ctm_set_precision): "fp32" (default, three
+        bf16 planes, six products) or "bf16x3" (two planes, three products, ~2x faster)."""
+        if precision not in PRECISIONS:
+            raise CTMError(f"unknown precision {precision!r} (fp32 or bf16x3)")
+        _check(lib().ctm_set_precision(self._h, PRECISIONS[precision]), "ctm_set_precision")
+        self.precision = precision
+        self._tape_n = None
 
     # ------------------------------------------------------------------ helpers
     def _io(self, X, out, f_out, want_f):
@@ -163,14 +195,21 @@ class MLP:
     def _p(t):
         return None if t is None else t.data_ptr()
 
+    def _taped(self, N):
+        """A K=2 operator call in grad mode recorded a tape of N points."""
+        self._tape_n = N if self._grad else None
+
     # ------------------------------------------------------------------ operators
+    @_streamed
     def laplacian(self, X, out=None, f_out=None, want_f=True, stream=None):
         """Exact Laplacian (Eq. 8). Returns (op [N], f [N] or None)."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         _check(lib().ctm_laplacian(self._h, X.data_ptr(), N, out.data_ptr(), self._p(f_out),
                                    _stream_ptr(stream, self.device)), "ctm_laplacian")
+        self._taped(N)
         return out, f_out
 
+    @_streamed
     def laplacian_standard(self, X, out=None, f_out=None, want_f=True, stream=None):
         """Exact Laplacian by STANDARD Taylor mode (1 + 2D vectors per layer): the
         paper's baseline, same value as ``laplacian``."""
@@ -179,15 +218,20 @@ class MLP:
                                             _stream_ptr(stream, self.device)), "ctm_laplacian_standard")
         return out, f_out
 
+    @_streamed
     def weighted_laplacian(self, X, sigma, out=None, f_out=None, want_f=True, stream=None):
         """<d^2 f, sigma sigma^T> (Eq. 10), sigma [D, R]."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         sigma = _dev_f32(sigma, self.device, "sigma")
+        if sigma.dim() != 2 or sigma.shape[0] != self.D:
+            raise CTMError(f"sigma must be [D={self.D}, R]")
         _check(lib().ctm_weighted_laplacian(self._h, X.data_ptr(), N, sigma.data_ptr(), sigma.shape[1],
                                             out.data_ptr(), self._p(f_out), _stream_ptr(stream, self.device)),
                "ctm_weighted_laplacian")
+        self._taped(N)
         return out, f_out
 
+    @_streamed
     def randomized_laplacian(self, X, S=None, V=None, seed=0, point_offset=0, sigma=None, dist="rademacher",
                              out=None, f_out=None, want_f=True, stream=None, standard=False):
         """(1/S) sum_s <d^2 f, (sigma v_s)^2> (Eq. 8/10 stochastic). V [N, S, Rv] or generated.
@@ -195,13 +239,20 @@ class MLP:
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         if V is not None:
             V = _dev_f32(V, self.device, "V")
+            if V.dim() != 3 or V.shape[0] != N:
+                raise CTMError(f"V must be [N={N}, S, Rv]")
             S, Rv = V.shape[1], V.shape[2]
         if sigma is not None:
             sigma = _dev_f32(sigma, self.device, "sigma")
-            Rv_s = sigma.shape[1]
-            Rv = Rv if V is not None else Rv_s
+            if sigma.dim() != 2 or sigma.shape[0] != self.D:
+                raise CTMError(f"sigma must be [D={self.D}, Rv]")
+            if V is not None and sigma.shape[1] != Rv:
+                raise CTMError(f"sigma must be [D, Rv={Rv}] to match V [N, S, Rv]")
+            Rv = sigma.shape[1]
         elif V is None:
             Rv = self.D
+        elif Rv != self.D:
+            raise CTMError(f"V must be [N, S, D={self.D}] without sigma")
         if S is None:
             raise CTMError("S is required when V is not given")
         d = {"rademacher": CTM_RADEMACHER, "gaussian": CTM_GAUSSIAN}[dist]
@@ -209,8 +260,10 @@ class MLP:
         _check(fn(self._h, X.data_ptr(), N, int(S), self._p(V), d, int(seed) & (2**64 - 1), int(point_offset),
                   self._p(sigma), int(Rv), out.data_ptr(), self._p(f_out), _stream_ptr(stream, self.device)),
                "ctm_randomized_laplacian" + ("_standard" if standard else ""))
+        self._taped(N if not standard else None)
         return out, f_out
 
+    @_streamed
     def biharmonic(self, X, out=None, f_out=None, want_f=True, stream=None):
         """Exact biharmonic (Eq. 12) via the interpolation family, one collapsed slot."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
@@ -218,17 +271,7 @@ class MLP:
                                     _stream_ptr(stream, self.device)), "ctm_biharmonic")
         return out, f_out
 
-    def weighted_laplacian_indefinite(self, X, C, out=None, f_out=None, want_f=True, stream=None):
-        """<d^2 f, C> for a symmetric, possibly indefinite C [D, D] (eigen-directions)."""
-        X, N, out, f_out = self._io(X, out, f_out, want_f)
-        C = _dev_f32(C, self.device, "C")
-        if tuple(C.shape) != (self.D, self.D):
-            raise CTMError("C must be [D, D]")
-        _check(lib().ctm_weighted_laplacian_indefinite(self._h, X.data_ptr(), N, C.data_ptr(), out.data_ptr(),
-                                                       self._p(f_out), _stream_ptr(stream, self.device)),
-               "ctm_weighted_laplacian_indefinite")
-        return out, f_out
-
+    @_streamed
     def biharmonic_standard(self, X, out=None, f_out=None, want_f=True, stream=None):
         """The same biharmonic by standard (uncollapsed) Taylor mode: 1 + 4J vectors (baseline)."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
@@ -236,18 +279,21 @@ class MLP:
                                              _stream_ptr(stream, self.device)), "ctm_biharmonic_standard")
         return out, f_out
 
+    @_streamed
     def weighted_laplacian_pointwise(self, X, sigma_x, out=None, f_out=None, want_f=True, stream=None):
         """<d^2 f(x_n), sigma(x_n) sigma(x_n)^T> with sigma_x [N, D, R] (Eq. 10, sigma depending on x)."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
         sigma_x = _dev_f32(sigma_x, self.device, "sigma_x")
-        if sigma_x.dim() != 3 or sigma_x.shape[0] != N:
-            raise CTMError("sigma_x must be [N, D, R]")
+        if sigma_x.dim() != 3 or sigma_x.shape[0] != N or sigma_x.shape[1] != self.D:
+            raise CTMError(f"sigma_x must be [N={N}, D={self.D}, R]")
         _check(lib().ctm_weighted_laplacian_pointwise(self._h, X.data_ptr(), N, sigma_x.data_ptr(),
                                                       int(sigma_x.shape[2]), out.data_ptr(), self._p(f_out),
                                                       _stream_ptr(stream, self.device)),
                "ctm_weighted_laplacian_pointwise")
+        self._taped(N)
         return out, f_out
 
+    @_streamed
     def directional_sum(self, X, K, dirs, weights, out=None, f_out=None, want_f=True, stream=None):
         """sum_j w_j <d^K f, u_j^K>, K in {2, 4}; dirs [J, D] shared or [N, J, D] per point (Eq. 5, Eq. 13-15)."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
@@ -255,13 +301,16 @@ class MLP:
         weights = _dev_f32(weights, self.device, "weights")
         per_point = dirs.dim() == 3
         J = int(weights.numel())
-        if dirs.shape[-2] != J or (per_point and dirs.shape[0] != N):
-            raise CTMError("dirs must be [J, D] or [N, J, D] with J = len(weights)")
+        if dirs.dim() not in (2, 3) or dirs.shape[-2] != J or dirs.shape[-1] != self.D or (
+                per_point and dirs.shape[0] != N):
+            raise CTMError(f"dirs must be [J, D={self.D}] or [N={N}, J, D] with J = len(weights)")
         _check(lib().ctm_directional_sum(self._h, X.data_ptr(), N, int(K), J, dirs.data_ptr(), int(per_point),
                                          weights.data_ptr(), out.data_ptr(), self._p(f_out),
                                          _stream_ptr(stream, self.device)), "ctm_directional_sum")
+        self._taped(N if int(K) == 2 else None)
         return out, f_out
 
+    @_streamed
     def biharmonic_nested(self, X, out=None, f_out=None, want_f=True, stream=None):
         """Exact biharmonic (Eq. 12) by nested collapsed Laplacians, 2 + 2D + D(D+1)/2 slots."""
         X, N, out, f_out = self._io(X, out, f_out, want_f)
@@ -269,6 +318,7 @@ class MLP:
                                            _stream_ptr(stream, self.device)), "ctm_biharmonic_nested")
         return out, f_out
 
+    @_streamed
     def stochastic_biharmonic(self, X, S=None, V=None, seed=0, point_offset=0, out=None, f_out=None, want_f=True,
                               stream=None, standard=False):
         """1/(3S) sum_s <d^4 f, v_s^4>, v_s ~ N(0, I) (Eq. 12 stochastic; V [N, S, D] or generated).
@@ -285,6 +335,7 @@ class MLP:
                "ctm_stochastic_biharmonic" + ("_standard" if standard else ""))
         return out, f_out
 
+    @_streamed
     def set_weights(self, params: Sequence, stream=None):
         """Replace the weights (same widths) asynchronously on ``stream`` (e.g. after an
         optimizer step). Keeps device copies alive until the next call."""
@@ -301,7 +352,10 @@ class MLP:
     def grad_enable(self, enable: bool = True):
         """Record a tape on later K=2 operator calls so that ``backward`` can run (NEXT-3)."""
         _check(lib().ctm_grad_enable(self._h, int(bool(enable))), "ctm_grad_enable")
+        self._grad = bool(enable)
+        self._tape_n = None
 
+    @_streamed
     def backward(self, gop, gf=None, grads=None, accumulate=False, stream=None):
         """Gradients of sum_n gop[n] op[n] + gf[n] f[n] for the last recorded call.
 
@@ -309,6 +363,8 @@ class MLP:
         (same structure) to write into existing tensors, with ``accumulate`` to add."""
         gop = _dev_f32(gop, self.device, "gop").reshape(-1)
         gf = None if gf is None else _dev_f32(gf, self.device, "gf").reshape(-1)
+        if self._tape_n is not None and (gop.numel() != self._tape_n or (gf is not None and gf.numel() != self._tape_n)):
+            raise CTMError(f"gop/gf must have the {self._tape_n} elements of the recorded call")
         if grads is None:
             grads = [(torch.empty(self.widths[l + 1], self.widths[l], device=self.device),
                       torch.empty(self.widths[l + 1], device=self.device)) for l in range(len(self.widths) - 1)]

@@ -20,8 +20,7 @@ FLAGS = [
     f"-I{os.path.join(ROOT, 'include')}",
 ]
 # cuBLAS: the weight-gradient GEMMs of the differentiable path (plain long-K GEMMs);
-# cuSOLVER: the eigendecomposition of an indefinite weighting (a per-call setup step)
-LIBS = ["-lcublas", "-lcusolver"]
+LIBS = ["-lcublas"]
 
 
 def stale() -> bool:

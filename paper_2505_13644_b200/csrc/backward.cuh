@@ -28,8 +28,9 @@ struct TopBwdParams {
   const float* gf;      // [N] or nullptr
   const float* jw;      // K=2 weights [P-2] or nullptr
   int act;
-  uint16_t* out_hi;     // Z_bar [N*P, ldo]
-  uint16_t* out_lo;
+  uint16_t* out;        // Z_bar planes [N*P, ldo]
+  int64_t pstride;
+  int nplanes;
   int ldo;
   float* dw_part;       // [G, width] partials of dW_L
   int G;
@@ -53,17 +54,16 @@ __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
     const float hb0 = gfn * wl;      // adjoint of h0
     float szz = 0.f;
     const float* __restrict__ zs = zr + ldz;
-    uint16_t* __restrict__ oh = p.out_hi + (row + 1) * ldo + m;
-    uint16_t* __restrict__ ol = p.out_lo + (row + 1) * ldo + m;
+    uint16_t* __restrict__ oz = p.out + (row + 1) * ldo + m;
 #pragma unroll 4
     for (int r = 0; r < p.P - 2; ++r) {
       const float z1 = zs[(size_t)r * ldz];
       const float w = p.jw ? p.jw[r] : 1.f;
       szz = fmaf(w * z1, z1, szz);
-      store_pair(oh, ol, (size_t)r * ldo, 2.f * A.d2 * w * z1 * tb);
+      ptx::store_planes(oz + (size_t)r * ldo, p.pstride, p.nplanes, 2.f * A.d2 * w * z1 * tb);
     }
-    store_pair(p.out_hi, p.out_lo, (row + p.P - 1) * ldo + m, A.d1 * tb);
-    store_pair(p.out_hi, p.out_lo, row * ldo + m, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb);
+    ptx::store_planes(p.out + (row + p.P - 1) * ldo + m, p.pstride, p.nplanes, A.d1 * tb);
+    ptx::store_planes(p.out + row * ldo + m, p.pstride, p.nplanes, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb);
     const float top = A.d1 * zt + A.d2 * szz;
     dwp += gfn * A.d0 + p.c * go * top;
   }
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
 }
 
 // part[g, m] = sum over rows r = g, g + G, ... < nrows of src[row0 + r * stride, m]
-// (bf16 pair if lo != nullptr, else fp32 `srcf`); grid (ceil(ncols / 128), G)
-__global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo,
+// (bf16 planes if src != nullptr, else fp32 `srcf`); grid (ceil(ncols / 128), G)
+__global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict__ src, int64_t pstride, int nplanes,
                                                      const float* __restrict__ srcf, int64_t nrows, int64_t stride,
                                                      int ld, int ncols, int G, float* __restrict__ part) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -81,20 +81,21 @@ __global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict_
   float acc = 0.f;
   for (int64_t r = g; r < nrows; r += G) {
     const size_t i = (size_t)(r * stride) * ld + m;
-    acc += srcf ? srcf[i] : ptx::bf16_val(hi[i]) + ptx::bf16_val(lo[i]);
+    acc += srcf ? srcf[i] : ptx::planes_val(src + i, pstride, nplanes);
   }
   part[(size_t)g * ncols + m] = acc;
 }
 
-// out[m] (=|+=) sum_g part[g, m] for m < ncols, deterministic: block (32, 32) handles 32
-// columns; thread (x, y) sums groups y, y + 32, ... in order, then a fixed smem tree over y
-__global__ void __launch_bounds__(1024) reduce_groups_kernel(const float* __restrict__ part, int G, int ncols,
+// out[m] (=|+=) sum_g part[g * ld + m] for m < ncols (ld >= ncols: the row stride of part),
+// deterministic: block (32, 32) handles 32 columns; thread (x, y) sums groups y, y + 32, ...
+// in order, then a fixed smem tree over y
+__global__ void __launch_bounds__(1024) reduce_groups_kernel(const float* __restrict__ part, int G, int ld, int ncols,
                                                              float* __restrict__ out, int accumulate) {
   __shared__ float red[32][33];
   const int m = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
   if (m < ncols)
-    for (int g = threadIdx.y; g < G; g += 32) s += part[(size_t)g * ncols + m];
+    for (int g = threadIdx.y; g < G; g += 32) s += part[(size_t)g * ld + m];
   red[threadIdx.y][threadIdx.x] = s;
   __syncthreads();
   for (int o = 16; o > 0; o >>= 1) {
@@ -129,15 +130,16 @@ __global__ void crop_kernel(const float* __restrict__ src, int lds, int rows, in
   dst[k] = accumulate ? dst[k] + v : v;
 }
 
-// bf16 pair transpose: out[c, r] = in[r, c] for the [rows, cols] planes (W^T for kBwd2)
-__global__ void transpose_pair_kernel(const uint16_t* __restrict__ in_hi, const uint16_t* __restrict__ in_lo,
-                                      int rows, int cols, uint16_t* __restrict__ out_hi,
-                                      uint16_t* __restrict__ out_lo) {
+// bf16 plane transpose: out[k][c, r] = in[k][r, c] for the three [rows, cols] planes
+// (plane stride rows * cols; W^T for kBwd2)
+__global__ void transpose_planes_kernel(const uint16_t* __restrict__ in, int rows, int cols,
+                                        uint16_t* __restrict__ out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= (int64_t)rows * cols) return;
+  const int64_t n = (int64_t)rows * cols;
+  if (k >= n) return;
   const int r = (int)(k / cols), c = (int)(k % cols);
-  out_hi[(size_t)c * rows + r] = in_hi[k];
-  out_lo[(size_t)c * rows + r] = in_lo[k];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) out[q * n + (size_t)c * rows + r] = in[q * n + k];
 }
 
 }  // namespace ctm

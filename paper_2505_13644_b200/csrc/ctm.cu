@@ -3,11 +3,10 @@
 // Launch sequence of one operator call:
 //   [prep]  per-call direction matrix (weighted / randomized with sigma only)
 //   seed    layer 1: z0 = W1 x0 + b1, first-order coefficients, tanh Taylor rule  -> block B1
-//   layer   l = 2..L-1: fused tcgen05 3xTF32 GEMM + tanh Taylor epilogue            -> block B_l
+//   layer   l = 2..L-1: fused tcgen05 bf16-plane GEMM + tanh Taylor epilogue         -> block B_l
 //           (the last hidden layer reduces straight against the output weights)
 //   final   op = c * (w_L . sum h_K), f = w_L . h0 + b_L
 #include <cublas_v2.h>
-#include <cusolverDn.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -57,20 +56,29 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 2D bf16 tensor map: inner dim `cols` (contiguous), outer `rows`; box {kBK, box_rows}
-// (128-byte rows); SWIZZLE_128B, matching the UMMA descriptors of jet_layer.cuh.
-bool make_map(CUtensorMap* m, const uint16_t* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+// 3D bf16 tensor map over the three planes of an operand: inner dim `cols` (contiguous),
+// `rows`, plane (stride `pstride` elements); box {kBK, box_rows, 1} (128-byte rows);
+// SWIZZLE_128B, matching the UMMA descriptors of jet_layer.cuh.
+bool make_map3(CUtensorMap* m, const uint16_t* base, uint64_t cols, uint64_t rows, uint64_t pstride,
+               uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * sizeof(uint16_t)};
-  cuuint32_t box[2] = {(cuuint32_t)ctm::kBK, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(base), dims, strides, box, estr,
+  cuuint64_t dims[3] = {cols, rows, 3};
+  cuuint64_t strides[2] = {cols * sizeof(uint16_t), pstride * sizeof(uint16_t)};
+  cuuint32_t box[3] = {(cuuint32_t)ctm::kBK, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+// A plane-split operand block: three bf16 planes of `cap` elements each, contiguous
+// (plane k at p + k * cap). cap is a multiple of 64 (TMA plane stride: 16-byte multiple).
+struct Planes {
+  uint16_t* p = nullptr;
+  size_t cap = 0;
+};
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
@@ -101,15 +109,16 @@ struct ctm_mlp {
   // layer 1
   float* W1T = nullptr;       // [D, wpad[1]]
   float* b1 = nullptr;        // [wpad[1]]
-  // layer 1 as a tensor-core layer (randomized directions): bf16 pairs [wpad[1], k1pad]
+  // operand precision (ctm_set_precision): 3 planes = fp32 mode, 2 planes = fast 3xBF16
+  int nplanes = 3;
+  // layer 1 as a tensor-core layer (randomized directions): bf16 planes [3][wpad[1], k1pad]
   int k1pad = 0;
-  uint16_t* W1hi = nullptr;
-  uint16_t* W1lo = nullptr;
-  CUtensorMap mapA1_hi, mapA1_lo;
+  uint16_t* W1p = nullptr;
+  CUtensorMap mapA1;
   // hidden GEMM layers l = 2..L-1 (index l-2)
-  std::vector<uint16_t*> Whi, Wlo;       // bf16 pairs [Mpad, Kpad]
+  std::vector<uint16_t*> Wp;             // bf16 planes [3][Mpad, Kpad]
   std::vector<float*> bias;
-  std::vector<CUtensorMap> mapA_hi, mapA_lo;
+  std::vector<CUtensorMap> mapA;
   // output layer
   float* w_out = nullptr;     // [wpad[L-1]]
   float* b_out = nullptr;     // [1] device (updated asynchronously by ctm_set_weights)
@@ -129,9 +138,8 @@ struct ctm_mlp {
   float* c_blk = nullptr;     // [blocks, ld1] per-block constants of a fixed set split into blocks
   size_t c_blk_elems = 0;
   int forced_rb = 0;          // ctm_set_direction_block: directions per block (0 = planner)
-  // workspace (bf16 hi, lo planes): see ensure_workspace
-  uint16_t* blk[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-  size_t blk_elems[4] = {0, 0, 0, 0};
+  // workspace (bf16 planes): see ensure_workspace
+  Planes blk[4];
   float* partial = nullptr;
   size_t partial_elems = 0;
   // last plan
@@ -139,19 +147,10 @@ struct ctm_mlp {
   bool smem_attr_set[64] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
-  std::vector<uint16_t*> WThi, WTlo;        // W_l^T bf16 pairs [wpad[l-1], wpad[l]], l = 2..L-1
-  std::vector<CUtensorMap> mapAT_hi, mapAT_lo;
+  std::vector<uint16_t*> WTp;               // W_l^T bf16 planes [3][wpad[l-1], wpad[l]], l = 2..L-1
+  std::vector<CUtensorMap> mapAT;
   float* eye = nullptr;                     // [256, 256] identity: fixed direction sets as shared V
   cublasHandle_t cublas = nullptr;
-  // indefinite weightings (ctm_weighted_laplacian_indefinite): eigendecomposition state
-  cusolverDnHandle_t cusolver = nullptr;
-  double* eig_a = nullptr;   // [D, D] fp64 copy of the weighting, then its eigenvectors
-  double* eig_w = nullptr;   // [D] eigenvalues
-  double* eig_work = nullptr;
-  int eig_lwork = 0;
-  int* eig_info = nullptr;
-  float* eig_dirs = nullptr;  // [D, D] eigenvectors as directions (rows), fp32
-  float* eig_vals = nullptr;  // [D] eigenvalues as direction weights, fp32
   struct Tape {
     bool valid = false;
     int64_t N = 0;
@@ -160,12 +159,11 @@ struct ctm_mlp {
     int weighted = 0, J = 0;
     float* weights = nullptr;
     size_t weights_elems = 0;
-    std::vector<uint16_t*> Bhi, Blo;        // B_l, l = 0 .. L-1 (B_0 = layer-1 input block)
-    std::vector<size_t> B_elems;
+    std::vector<Planes> B;                  // B_l, l = 0 .. L-1 (B_0 = layer-1 input block)
+    int nplanes = 3;                        // precision the tape was recorded in
     std::vector<float*> Z;                  // Z_l, l = 1 .. L-1 (fp32 pre-activations)
     std::vector<size_t> Z_elems;
-    uint16_t* Zb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    size_t Zb_elems[2] = {0, 0};
+    Planes Zb[2];
     float* part = nullptr;
     size_t part_elems = 0;
     float* dWpad = nullptr;
@@ -190,29 +188,21 @@ ctm_status free_all(ctm_mlp* h) {
     if (p) cudaFree(p);
     p = nullptr;
   };
-  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1hi); F(h->W1lo); F(h->b_out); F(h->bih_dirs);
-  for (auto& p : h->Whi) F(p);
-  for (auto& p : h->Wlo) F(p);
+  F(h->W1T); F(h->b1); F(h->w_out); F(h->W1p); F(h->b_out); F(h->bih_dirs);
+  for (auto& p : h->Wp) F(p);
   for (auto& p : h->bias) F(p);
   F(h->U_lap); F(h->c_lap); F(h->w_ones); F(h->U_bih); F(h->c_bih); F(h->w_bih);
   F(h->U_call); F(h->c_call); F(h->c_blk);
-  for (int i = 0; i < 4; ++i)
-    for (int j = 0; j < 2; ++j) F(h->blk[i][j]);
+  for (int i = 0; i < 4; ++i) F(h->blk[i].p);
   F(h->partial);
-  for (auto& p : h->WThi) F(p);
-  for (auto& p : h->WTlo) F(p);
+  for (auto& p : h->WTp) F(p);
   F(h->eye);
   F(h->tape.weights); F(h->tape.part); F(h->tape.dWpad);
-  for (auto& p : h->tape.Bhi) F(p);
-  for (auto& p : h->tape.Blo) F(p);
+  for (auto& p : h->tape.B) F(p.p);
   for (auto& p : h->tape.Z) F(p);
-  for (int i = 0; i < 2; ++i)
-    for (int j = 0; j < 2; ++j) F(h->tape.Zb[i][j]);
+  for (int i = 0; i < 2; ++i) F(h->tape.Zb[i].p);
   if (h->cublas) cublasDestroy(h->cublas);
   h->cublas = nullptr;
-  if (h->cusolver) cusolverDnDestroy(h->cusolver);
-  h->cusolver = nullptr;
-  F(h->eig_a); F(h->eig_w); F(h->eig_work); F(h->eig_info); F(h->eig_dirs); F(h->eig_vals);
   for (auto& r : h->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -233,15 +223,15 @@ ctm_status ensure(float*& p, size_t& have, size_t need) {
   return CTM_OK;
 }
 
-ctm_status ensure_pair(uint16_t*& hi, uint16_t*& lo, size_t& have, size_t need) {
-  if (need <= have && hi) return CTM_OK;
-  if (hi) cudaFree(hi);
-  if (lo) cudaFree(lo);
-  hi = lo = nullptr;
-  have = 0;
-  CTM_CUDA(cudaMalloc(&hi, std::max<size_t>(need, 1) * sizeof(uint16_t)));
-  CTM_CUDA(cudaMalloc(&lo, std::max<size_t>(need, 1) * sizeof(uint16_t)));
-  have = need;
+// three planes of >= need elements each (grow-only)
+ctm_status ensure_planes(Planes& b, size_t need) {
+  if (need <= b.cap && b.p) return CTM_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  const size_t cap = (std::max<size_t>(need, 1) + 63) / 64 * 64;
+  CTM_CUDA(cudaMalloc(&b.p, 3 * cap * sizeof(uint16_t)));
+  b.cap = cap;
   return CTM_OK;
 }
 
@@ -256,15 +246,9 @@ ctm_status ensure_workspace(ctm_mlp* h, int64_t rows, int nseed) {
   const size_t need[4] = {(size_t)rows * ldmax, (size_t)rows * ldmax, (size_t)rows * ld_seed,
                           nseed > 1 ? (size_t)rows * ld_seed : 0};
   for (int i = 0; i < 4; ++i) {
-    if (need[i] <= h->blk_elems[i] && (h->blk[i][0] || need[i] == 0)) continue;
-    for (int j = 0; j < 2; ++j) {
-      if (h->blk[i][j]) cudaFree(h->blk[i][j]);
-      h->blk[i][j] = nullptr;
-    }
-    h->blk_elems[i] = 0;
-    for (int j = 0; j < 2; ++j)
-      CTM_CUDA(cudaMalloc(&h->blk[i][j], std::max<size_t>(need[i], 1) * sizeof(uint16_t)));
-    h->blk_elems[i] = need[i];
+    if (need[i] == 0) continue;
+    ctm_status s = ensure_planes(h->blk[i], need[i]);
+    if (s != CTM_OK) return s;
   }
   return CTM_OK;
 }
@@ -343,9 +327,8 @@ ctm_status set_layer_attr(ctm_mlp* h) {
 }
 
 template <int KORD, int FLAGS>
-ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& ahi, const CUtensorMap& alo,
-                               const CUtensorMap& bhi, const CUtensorMap& blo, const ctm::LayerParams& lp,
-                               cudaStream_t st) {
+ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
+                               const ctm::LayerParams& lp, cudaStream_t st) {
   ctm_status s = set_layer_attr<KORD, FLAGS>(h);
   if (s != CTM_OK) return s;
   // programmatic dependent launch: the prologue (barriers, TMEM allocation, descriptor
@@ -360,7 +343,7 @@ ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& ahi,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::jet_layer_kernel<KORD, FLAGS>, ahi, alo, bhi, blo, lp));
+  CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::jet_layer_kernel<KORD, FLAGS>, amap, bmap, lp));
   return CTM_OK;
 }
 
@@ -472,22 +455,21 @@ bool stoch_k4(const CallArgs& a) {
 }
 
 struct GemmLayer {
-  const CUtensorMap* a_hi;
-  const CUtensorMap* a_lo;
+  const CUtensorMap* amap;
   const float* bias;
   int kpad, mpad, w_in, w_out;
 };
 
 // grad mode: where a layer writes its output block and its pre-activations
 struct LayerIO {
-  uint16_t* out[2];
+  Planes* out;
   float* z;
 };
 
 // Layer 1 for fixed direction sets (and the stochastic biharmonic) for points
 // [p0, p0 + n): writes the layer-1 output block into buf.
 ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, int64_t p0, int64_t n,
-                       uint16_t* const* buf, const float* UT, const float* csum, int R, cudaStream_t st, int& launches,
+                       const Planes& buf, const float* UT, const float* csum, int R, cudaStream_t st, int& launches,
                        float* z_out = nullptr) {
   const int P = pl.P;
   const int D = h->widths[0], ld1 = h->wpad[1];
@@ -511,8 +493,9 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     bp.blocks = pl.nb;
     bp.rb = pl.rb;
     bp.standard = (a.op == OP_SBIH_STD);
-    bp.out_hi = buf[0];
-    bp.out_lo = buf[1];
+    bp.out = buf.p;
+    bp.pstride = (int64_t)buf.cap;
+    bp.nplanes = h->nplanes;
     bp.act = h->act;
     ctm::seed_stoch_biharmonic_kernel<<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
   } else {
@@ -529,8 +512,9 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     sp.R = R;
     sp.blocks = pl.nb;
     sp.rb = (KORD == ctm::kNest) ? R : pl.rb;
-    sp.out_hi = buf[0];
-    sp.out_lo = buf[1];
+    sp.out = buf.p;
+    sp.pstride = (int64_t)buf.cap;
+    sp.nplanes = h->nplanes;
     sp.act = h->act;
     sp.z_out = z_out;
     if (KORD == 2)
@@ -552,7 +536,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
 // ping-pongs through blk[0] / blk[1] and ends in the readout of op/f. `after_first`
 // (optional) is recorded on st once the first GEMM (the reader of `in`) is enqueued.
 ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, const std::vector<GemmLayer>& layers,
-                         int64_t p0, int64_t n, uint16_t* const* in, float scale, cudaStream_t st,
+                         int64_t p0, int64_t n, const Planes* in, float scale, cudaStream_t st,
                          cudaEvent_t after_first, int& launches, const std::vector<LayerIO>* io = nullptr) {
   const int P = pl.P;
   const int64_t nsub = n * pl.nb;  // sub-points (direction blocks) = the kernel's points
@@ -561,7 +545,8 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     const int threads = 256, ppb = threads / 32;
     ProfScope ps(h, CTM_KIND_FINAL, 0.0, st);
     ctm::readout_block_kernel<<<(unsigned)((n + ppb - 1) / ppb), threads, 0, st>>>(
-        in[0], in[1], h->wpad[1], P, pl.nb, h->widths[1], h->w_out, h->b_out, scale, n, a.op_out + p0,
+        in->p, (int64_t)in->cap, h->nplanes, h->wpad[1], P, pl.nb, h->widths[1], h->w_out, h->b_out, scale, n,
+        a.op_out + p0,
         a.f_out ? a.f_out + p0 : nullptr,
         (a.op == OP_LAP_STD || a.op == OP_RLAP_STD) ? 2 : (a.op == OP_BIH_STD || a.op == OP_SBIH_STD) ? 4 : 0,
         a.op == OP_SBIH_STD ? h->w_ones : h->w_bih, std::max(pl.rb, 1), a.op == OP_SBIH_STD ? a.S : h->J_bih);
@@ -570,21 +555,22 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     return CTM_OK;
   }
   const int64_t n_tiles = (nsub + pl.ppt - 1) / pl.ppt;
-  uint16_t* const* src = in;
+  const Planes* src = in;
   int dst = 0;
   for (size_t li = 0; li < layers.size(); ++li) {
     const GemmLayer& gl = layers[li];
     const int m_tiles = gl.mpad / ctm::kBM;
     const bool last = (li + 1 == layers.size());
-    CUtensorMap mb_hi, mb_lo;
-    if (!make_map(&mb_hi, src[0], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma / 2) ||
-        !make_map(&mb_lo, src[1], (uint64_t)gl.kpad, (uint64_t)rows, (uint32_t)pl.nmma / 2))  // a CTA stages half of B
+    CUtensorMap mb;  // a CTA stages half of B
+    if (!make_map3(&mb, src->p, (uint64_t)gl.kpad, (uint64_t)rows, src->cap, (uint32_t)pl.nmma / 2))
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the activation block");
     ctm::LayerParams lp{};
     lp.bias = gl.bias;
     lp.act = h->act;
-    lp.out_hi = io ? (*io)[li].out[0] : h->blk[dst][0];
-    lp.out_lo = io ? (*io)[li].out[1] : h->blk[dst][1];
+    const Planes* outp = io ? (*io)[li].out : &h->blk[dst];
+    lp.out = outp ? outp->p : nullptr;
+    lp.pstride = outp ? (int64_t)outp->cap : 0;
+    lp.nplanes = (int16_t)h->nplanes;
     lp.ldo = gl.mpad;
     lp.z_out = io ? (*io)[li].z : nullptr;
     lp.ldz = gl.mpad;
@@ -620,21 +606,21 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       if (KORD == 2) {
         switch (flags) {
           case ctm::kFlagWide:
-            s = launch_layer_kernel<2, ctm::kFlagWide>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+            s = launch_layer_kernel<2, ctm::kFlagWide>(h, grid, *gl.amap, mb, lp, st);
             break;
-          case 0: s = launch_layer_kernel<2, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
-          case 1: s = launch_layer_kernel<2, 1>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
-          case 2: s = launch_layer_kernel<2, 2>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
-          default: s = launch_layer_kernel<2, 3>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st); break;
+          case 0: s = launch_layer_kernel<2, 0>(h, grid, *gl.amap, mb, lp, st); break;
+          case 1: s = launch_layer_kernel<2, 1>(h, grid, *gl.amap, mb, lp, st); break;
+          case 2: s = launch_layer_kernel<2, 2>(h, grid, *gl.amap, mb, lp, st); break;
+          default: s = launch_layer_kernel<2, 3>(h, grid, *gl.amap, mb, lp, st); break;
         }
       } else if (KORD == 4) {
-        s = launch_layer_kernel<4, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+        s = launch_layer_kernel<4, 0>(h, grid, *gl.amap, mb, lp, st);
       } else if (KORD == ctm::kNest) {
-        s = launch_layer_kernel<ctm::kNest, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+        s = launch_layer_kernel<ctm::kNest, 0>(h, grid, *gl.amap, mb, lp, st);
       } else if (KORD == ctm::kStd4) {
-        s = launch_layer_kernel<ctm::kStd4, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+        s = launch_layer_kernel<ctm::kStd4, 0>(h, grid, *gl.amap, mb, lp, st);
       } else {
-        s = launch_layer_kernel<ctm::kStd2, 0>(h, grid, *gl.a_hi, *gl.a_lo, mb_hi, mb_lo, lp, st);
+        s = launch_layer_kernel<ctm::kStd2, 0>(h, grid, *gl.amap, mb, lp, st);
       }
       if (s != CTM_OK) return s;
     }
@@ -655,7 +641,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
                                   (const float*)h->b_out, scale, a.op_out + p0, a.f_out ? a.f_out + p0 : nullptr));
       ++launches;
     }
-    src = io ? (*io)[li].out : h->blk[dst];
+    src = io ? (*io)[li].out : &h->blk[dst];
     dst ^= 1;
   }
   return CTM_OK;
@@ -670,15 +656,13 @@ bool differentiable(const CallArgs& a) {
 ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
   auto& T = h->tape;
   const int L = h->L;
-  T.Bhi.resize(L, nullptr);
-  T.Blo.resize(L, nullptr);
-  T.B_elems.resize(L, 0);
+  T.B.resize(L);
   T.Z.resize(L, nullptr);
   T.Z_elems.resize(L, 0);
-  ctm_status s = ensure_pair(T.Bhi[0], T.Blo[0], T.B_elems[0], (size_t)rows * h->k1pad);
+  ctm_status s = ensure_planes(T.B[0], (size_t)rows * h->k1pad);
   if (s != CTM_OK) return s;
   for (int l = 1; l <= std::max(1, L - 2); ++l) {
-    s = ensure_pair(T.Bhi[l], T.Blo[l], T.B_elems[l], (size_t)rows * h->wpad[l]);
+    s = ensure_planes(T.B[l], (size_t)rows * h->wpad[l]);
     if (s != CTM_OK) return s;
   }
   for (int l = 1; l <= L - 1; ++l) {
@@ -705,6 +689,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     case OP_DSUM: R = a.J; break;
     case OP_BIH_NEST: break;
   }
+  h->tape.valid = false;  // whatever happens below, an earlier call's tape is stale now
   // grad mode records one block per point (the backward kernels have no block structure)
   const bool grad = h->grad && differentiable(a);
   const Plan pl = make_plan(KORD, R, h->forced_rb, !grad,
@@ -723,7 +708,15 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   h->last_nb = pl.nb;
   h->last_rb = pl.rb;
   h->last_launches = 0;
-  if (a.N == 0) return CTM_OK;
+  if (a.N == 0) {
+    if (grad) {  // an empty tape: ctm_backward gives zero gradients
+      h->tape.N = 0;
+      h->tape.P = P;
+      h->tape.nplanes = h->nplanes;
+      h->tape.valid = true;
+    }
+    return CTM_OK;
+  }
   const int64_t rows_total = a.N * pl.nb * (int64_t)P;
   if (rows_total > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "N * slots exceeds 2^31 rows");
 
@@ -732,25 +725,21 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   int launches = 0;
   ctm_status s;
   // grad mode: record the tape of this call (differentiable operators only)
-  h->tape.valid = false;
   std::vector<LayerIO> io;
   if (grad) {
     s = prepare_tape(h, a.N * (int64_t)P);
     if (s != CTM_OK) return s;
     const int first = random_k2(a) ? 1 : 2;
-    for (int l = first; l <= h->L - 1; ++l)
-      io.push_back({{l < h->L - 1 ? h->tape.Bhi[l] : nullptr, l < h->L - 1 ? h->tape.Blo[l] : nullptr},
-                    h->tape.Z[l]});
+    for (int l = first; l <= h->L - 1; ++l) io.push_back({l < h->L - 1 ? &h->tape.B[l] : nullptr, h->tape.Z[l]});
   }
-  uint16_t* const tapeB0[2] = {grad ? h->tape.Bhi[0] : nullptr, grad ? h->tape.Blo[0] : nullptr};
-  uint16_t* const tapeB1[2] = {grad ? h->tape.Bhi[1] : nullptr, grad ? h->tape.Blo[1] : nullptr};
+  const Planes* tapeB0 = grad ? &h->tape.B[0] : nullptr;
+  const Planes* tapeB1 = grad ? &h->tape.B[1] : nullptr;
 
   // GEMM layers: layer 1 for per-point K=2 directions, then the hidden layers 2..L-1
   std::vector<GemmLayer> layers;
-  if (random_k2(a)) layers.push_back({&h->mapA1_hi, &h->mapA1_lo, h->b1, h->k1pad, ld1, D, h->widths[1]});
+  if (random_k2(a)) layers.push_back({&h->mapA1, h->b1, h->k1pad, ld1, D, h->widths[1]});
   for (int l = 2; l <= h->L - 1; ++l)
-    layers.push_back({&h->mapA_hi[l - 2], &h->mapA_lo[l - 2], h->bias[l - 2], h->wpad[l - 1], h->wpad[l],
-                      h->widths[l - 1], h->widths[l]});
+    layers.push_back({&h->mapA[l - 2], h->bias[l - 2], h->wpad[l - 1], h->wpad[l], h->widths[l - 1], h->widths[l]});
 
   if (random_k2(a)) {
     // per-point K=2 directions: the input block [x0; u_1..u_S; 0], then layer 1 on the
@@ -772,15 +761,17 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.blocks = pl.nb;
     rp.rb = pl.rb;
     rp.standard = (a.op == OP_RLAP_STD);
-    rp.out_hi = grad ? tapeB0[0] : h->blk[2][0];
-    rp.out_lo = grad ? tapeB0[1] : h->blk[2][1];
+    const Planes& b0 = grad ? *tapeB0 : h->blk[2];
+    rp.out = b0.p;
+    rp.pstride = (int64_t)b0.cap;
+    rp.nplanes = h->nplanes;
     {
       ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 4.0, st);
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
     }
     ++launches;
     const float scale = (a.op == OP_RLAP || a.op == OP_RLAP_STD) ? 1.f / (float)a.S : 1.f;  // Eq. 8/10 stochastic
-    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB0 : h->blk[2], scale, st, nullptr, launches,
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB0 : &h->blk[2], scale, st, nullptr, launches,
                       grad ? &io : nullptr);
     if (s != CTM_OK) return s;
   } else {
@@ -851,15 +842,16 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       }
       rp.blocks = 1;
       rp.rb = rp.S;
-      rp.out_hi = tapeB0[0];
-      rp.out_lo = tapeB0[1];
+      rp.out = tapeB0->p;
+      rp.pstride = (int64_t)tapeB0->cap;
+      rp.nplanes = h->nplanes;
       ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
       ++launches;
     }
-    s = launch_seed(h, a, KORD, pl, 0, a.N, grad ? tapeB1 : h->blk[2], UT, csum, a.op == OP_BIH_NEST ? D : R, st,
+    s = launch_seed(h, a, KORD, pl, 0, a.N, grad ? *tapeB1 : h->blk[2], UT, csum, a.op == OP_BIH_NEST ? D : R, st,
                     launches, grad ? h->tape.Z[1] : nullptr);
     if (s != CTM_OK) return s;
-    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB1 : h->blk[2], scale, st, nullptr, launches,
+    s = launch_layers(h, a, KORD, pl, layers, 0, a.N, grad ? tapeB1 : &h->blk[2], scale, st, nullptr, launches,
                       grad ? &io : nullptr);
     if (s != CTM_OK) return s;
   }
@@ -872,6 +864,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     T.scale = (a.op == OP_RLAP) ? 1.f / (float)a.S : 1.f;
     T.weighted = (a.op == OP_DSUM);
     T.J = (a.op == OP_DSUM) ? a.J : 0;
+    T.nplanes = h->nplanes;
     if (T.weighted) {  // the caller's weights may not outlive the call
       s = ensure(T.weights, T.weights_elems, (size_t)a.J);
       if (s != CTM_OK) return s;
@@ -888,16 +881,21 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
 // accumulation (a plain long-K GEMM: cuBLAS). B [rows, Kin], Zb [rows, Mout], both bf16
 // pairs, row-major (= column-major [K, rows], [M, rows]); the result is column-major
 // [Kin, Mout] = row-major [Mout, Kin].
-ctm_status weight_grad_gemm(ctm_mlp* h, const uint16_t* Bhi, const uint16_t* Blo, int Kin, const uint16_t* Zhi,
-                            const uint16_t* Zlo, int Mout, int64_t rows, float* C, cudaStream_t st) {
+ctm_status weight_grad_gemm(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, int Mout, int64_t rows, float* C,
+                            cudaStream_t st) {
   ProfScope ps(h, CTM_KIND_WGRAD, 2.0 * (double)rows * Kin * Mout, st);
   if (cublasSetStream(h->cublas, st) != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasSetStream");
   const float one = 1.f, zero = 0.f;
-  const uint16_t* As[3] = {Bhi, Blo, Bhi};
-  const uint16_t* Bs[3] = {Zhi, Zhi, Zlo};
-  for (int i = 0; i < 3; ++i) {
-    cublasStatus_t cs = cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, Kin, Mout, (int)rows, &one, As[i],
-                                     CUDA_R_16BF, Kin, Bs[i], CUDA_R_16BF, Mout, i == 0 ? &zero : &one, C, CUDA_R_32F,
+  // plane products (B plane, Z plane): fast mode 3, fp32 mode 6 (corrections first)
+  static const int prods3[3][2] = {{1, 0}, {0, 1}, {0, 0}};
+  static const int prods6[6][2] = {{2, 0}, {1, 1}, {0, 2}, {1, 0}, {0, 1}, {0, 0}};
+  const int np = h->tape.nplanes == 3 ? 6 : 3;
+  for (int i = 0; i < np; ++i) {
+    const int* pr = np == 6 ? prods6[i] : prods3[i];
+    const uint16_t* Ab = B.p + pr[0] * B.cap;
+    const uint16_t* Bz = Z.p + pr[1] * Z.cap;
+    cublasStatus_t cs = cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, Kin, Mout, (int)rows, &one, Ab,
+                                     CUDA_R_16BF, Kin, Bz, CUDA_R_16BF, Mout, i == 0 ? &zero : &one, C, CUDA_R_32F,
                                      Kin, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
     if (cs != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasGemmEx failed (" + std::to_string((int)cs) + ")");
   }
@@ -905,16 +903,15 @@ ctm_status weight_grad_gemm(ctm_mlp* h, const uint16_t* Bhi, const uint16_t* Blo
 }
 
 // out[m] (=|+=) sum_n Zb[n * P + 0, m] for m < ncols (the bias gradient: bias on slot 0 only)
-ctm_status bias_grad(ctm_mlp* h, const uint16_t* Zhi, const uint16_t* Zlo, int ld, int ncols, float* out, int acc,
-                     cudaStream_t st) {
+ctm_status bias_grad(ctm_mlp* h, const Planes& Z, int ld, int ncols, float* out, int acc, cudaStream_t st) {
   const int G = 1024;  // point groups: enough independent rows in flight per column
   ctm_status s = ensure(h->tape.part, h->tape.part_elems, (size_t)G * std::max(ncols, 1));
   if (s != CTM_OK) return s;
   ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
   h->last_launches += 2;
-  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Zhi, Zlo, nullptr, h->tape.N, h->tape.P, ld, ncols,
-                                                                   G, h->tape.part);
-  ctm::reduce_groups_kernel<<<(ncols + 31) / 32, dim3(32, 32), 0, st>>>(h->tape.part, G, ncols, out, acc);
+  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Z.p, (int64_t)Z.cap, h->tape.nplanes, nullptr,
+                                                                   h->tape.N, h->tape.P, ld, ncols, G, h->tape.part);
+  ctm::reduce_groups_kernel<<<(ncols + 31) / 32, dim3(32, 32), 0, st>>>(h->tape.part, G, ncols, ncols, out, acc);
   return CTM_OK;
 }
 
@@ -927,7 +924,7 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   for (int l = 1; l <= L - 1; ++l) ldmax = std::max(ldmax, h->wpad[l]);
   ctm_status s;
   for (int i = 0; i < 2; ++i) {
-    s = ensure_pair(T.Zb[i][0], T.Zb[i][1], T.Zb_elems[i], (size_t)rows * ldmax);
+    s = ensure_planes(T.Zb[i], (size_t)rows * ldmax);
     if (s != CTM_OK) return s;
   }
   size_t dwmax = (size_t)h->wpad[1] * h->k1pad;
@@ -955,13 +952,16 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     tp.gf = gf;
     tp.jw = jw;
     tp.act = h->act;
-    tp.out_hi = T.Zb[0][0];
-    tp.out_lo = T.Zb[0][1];
+    tp.out = T.Zb[0].p;
+    tp.pstride = (int64_t)T.Zb[0].cap;
+    tp.nplanes = T.nplanes;
     tp.ldo = w;
     tp.dw_part = T.part;
     tp.G = G;
     ctm::top_bwd_kernel<<<dim3(w / 128, G), 128, 0, st>>>(tp);
-    ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 31) / 32, dim3(32, 32), 0, st>>>(T.part, G, w, dW[L - 1], acc);
+    // part rows have stride w (padded); only the widths[L-1] real columns reach dW_L
+    ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 31) / 32, dim3(32, 32), 0, st>>>(T.part, G, w, h->widths[L - 1],
+                                                                                    dW[L - 1], acc);
     if (gf)
       ctm::vector_sum_kernel<<<1, 256, 0, st>>>(gf, N, db[L - 1], acc);
     else if (!acc)
@@ -971,7 +971,7 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   int cur = 0;
   for (int l = L - 1; l >= 2; --l) {
     const int Mout = h->wpad[l], Kin = h->wpad[l - 1];
-    s = weight_grad_gemm(h, T.Bhi[l - 1], T.Blo[l - 1], Kin, T.Zb[cur][0], T.Zb[cur][1], Mout, rows, T.dWpad, st);
+    s = weight_grad_gemm(h, T.B[l - 1], Kin, T.Zb[cur], Mout, rows, T.dWpad, st);
     if (s != CTM_OK) return s;
     {
       const int64_t n = (int64_t)h->widths[l] * h->widths[l - 1];
@@ -980,18 +980,18 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
       ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, Kin, h->widths[l], h->widths[l - 1],
                                                                     dW[l - 1], acc);
     }
-    s = bias_grad(h, T.Zb[cur][0], T.Zb[cur][1], Mout, h->widths[l], db[l - 1], acc, st);
+    s = bias_grad(h, T.Zb[cur], Mout, h->widths[l], db[l - 1], acc, st);
     if (s != CTM_OK) return s;
     // Z_bar_{l-1} = rule^T( (Z_bar_l W_l)^T ) on the tensor cores (jet_layer_kernel<kBwd2>)
-    CUtensorMap mb_hi, mb_lo;
-    if (!make_map(&mb_hi, T.Zb[cur][0], (uint64_t)Mout, (uint64_t)rows, (uint32_t)T.nmma / 2) ||
-        !make_map(&mb_lo, T.Zb[cur][1], (uint64_t)Mout, (uint64_t)rows, (uint32_t)T.nmma / 2))
+    CUtensorMap mb;
+    if (!make_map3(&mb, T.Zb[cur].p, (uint64_t)Mout, (uint64_t)rows, T.Zb[cur].cap, (uint32_t)T.nmma / 2))
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the adjoint block");
     ctm::LayerParams lp{};
     lp.bias = nullptr;
     lp.act = h->act;
-    lp.out_hi = T.Zb[cur ^ 1][0];
-    lp.out_lo = T.Zb[cur ^ 1][1];
+    lp.out = T.Zb[cur ^ 1].p;
+    lp.pstride = (int64_t)T.Zb[cur ^ 1].cap;
+    lp.nplanes = (int16_t)T.nplanes;
     lp.ldo = Kin;
     lp.m_tiles = Kin / ctm::kBM;
     lp.n_points = N;
@@ -1011,13 +1011,13 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     {
       ProfScope ps(h, CTM_KIND_BWD, 2.0 * N * P * h->widths[l - 1] * h->widths[l], st);
       ++h->last_launches;
-      s = launch_layer_kernel<ctm::kBwd2, 0>(h, grid, h->mapAT_hi[l - 2], h->mapAT_lo[l - 2], mb_hi, mb_lo, lp, st);
+      s = launch_layer_kernel<ctm::kBwd2, 0>(h, grid, h->mapAT[l - 2], mb, lp, st);
       if (s != CTM_OK) return s;
     }
     cur ^= 1;
   }
   // ---- layer 1: dW_1 = Z_bar_1^T B_0 (B_0 = [x0; u_r; 0]), db_1
-  s = weight_grad_gemm(h, T.Bhi[0], T.Blo[0], h->k1pad, T.Zb[cur][0], T.Zb[cur][1], h->wpad[1], rows, T.dWpad, st);
+  s = weight_grad_gemm(h, T.B[0], h->k1pad, T.Zb[cur], h->wpad[1], rows, T.dWpad, st);
   if (s != CTM_OK) return s;
   {
     const int64_t n = (int64_t)h->widths[1] * h->widths[0];
@@ -1026,7 +1026,7 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, h->k1pad, h->widths[1], h->widths[0], dW[0],
                                                                   acc);
   }
-  s = bias_grad(h, T.Zb[cur][0], T.Zb[cur][1], h->wpad[1], h->widths[1], db[0], acc, st);
+  s = bias_grad(h, T.Zb[cur], h->wpad[1], h->widths[1], db[0], acc, st);
   if (s != CTM_OK) return s;
   CTM_CUDA(cudaGetLastError());
   return CTM_OK;
@@ -1045,16 +1045,16 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
   {
     const int64_t n = (int64_t)ld1 * h->k1pad;
     ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], b[0], h->widths[1], D, ld1, h->k1pad,
-                                                                           h->W1hi, h->W1lo, h->b1);
+                                                                           h->W1p, h->b1);
   }
   for (int l = 2; l <= L - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
     const int64_t n = (int64_t)mpad * kpad;
     ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        W[l - 1], b[l - 1], h->widths[l], h->widths[l - 1], mpad, kpad, h->Whi[l - 2], h->Wlo[l - 2], h->bias[l - 2]);
-    if (!h->WThi.empty())
-      ctm::transpose_pair_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Whi[l - 2], h->Wlo[l - 2], mpad, kpad,
-                                                                              h->WThi[l - 2], h->WTlo[l - 2]);
+        W[l - 1], b[l - 1], h->widths[l], h->widths[l - 1], mpad, kpad, h->Wp[l - 2], h->bias[l - 2]);
+    if (!h->WTp.empty())
+      ctm::transpose_planes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Wp[l - 2], mpad, kpad,
+                                                                                h->WTp[l - 2]);
   }
   {
     const int lpad = h->wpad[L - 1];
@@ -1065,7 +1065,7 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
   if (h->J_bih)
     ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->bih_dirs, h->J_bih, h->w_bih, 4,
                                                                    h->U_bih, h->c_bih);
-  h->last_launches = 4 + (L - 2) * (h->WThi.empty() ? 1 : 2) + (h->J_bih ? 1 : 0);
+  h->last_launches = 4 + (L - 2) * (h->WTp.empty() ? 1 : 2) + (h->J_bih ? 1 : 0);
   h->tape.valid = false;
 }
 
@@ -1144,30 +1144,25 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
   h->k1pad = round_up(D, ctm::kBK);
   LOAD_CUDA(cudaMalloc(&h->W1T, sizeof(float) * (size_t)D * ld1));
   LOAD_CUDA(cudaMalloc(&h->b1, sizeof(float) * ld1));
-  LOAD_CUDA(cudaMalloc(&h->W1hi, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
-  LOAD_CUDA(cudaMalloc(&h->W1lo, sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
-  if (!make_map(&h->mapA1_hi, h->W1hi, h->k1pad, ld1, ctm::kBM) ||
-      !make_map(&h->mapA1_lo, h->W1lo, h->k1pad, ld1, ctm::kBM)) {
+  LOAD_CUDA(cudaMalloc(&h->W1p, 3 * sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
+  if (!make_map3(&h->mapA1, h->W1p, h->k1pad, ld1, (uint64_t)ld1 * h->k1pad, ctm::kBM)) {
     fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W1");
     return bail(CTM_ECUDA);
   }
   for (int l = 2; l <= n_layers - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
-    uint16_t *whi, *wlo;
+    uint16_t* wp;
     float* bp;
-    LOAD_CUDA(cudaMalloc(&whi, sizeof(uint16_t) * (size_t)mpad * kpad));
-    h->Whi.push_back(whi);
-    LOAD_CUDA(cudaMalloc(&wlo, sizeof(uint16_t) * (size_t)mpad * kpad));
-    h->Wlo.push_back(wlo);
+    LOAD_CUDA(cudaMalloc(&wp, 3 * sizeof(uint16_t) * (size_t)mpad * kpad));
+    h->Wp.push_back(wp);
     LOAD_CUDA(cudaMalloc(&bp, sizeof(float) * mpad));
     h->bias.push_back(bp);
-    CUtensorMap mh, ml;
-    if (!make_map(&mh, whi, kpad, mpad, ctm::kBM) || !make_map(&ml, wlo, kpad, mpad, ctm::kBM)) {
+    CUtensorMap mw;
+    if (!make_map3(&mw, wp, kpad, mpad, (uint64_t)mpad * kpad, ctm::kBM)) {
       fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for weights");
       return bail(CTM_ECUDA);
     }
-    h->mapA_hi.push_back(mh);
-    h->mapA_lo.push_back(ml);
+    h->mapA.push_back(mw);
   }
   LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * h->wpad[n_layers - 1]));
   LOAD_CUDA(cudaMalloc(&h->b_out, sizeof(float)));
@@ -1337,54 +1332,6 @@ ctm_status ctm_directional_sum(ctm_mlp_t mlp, const float* X, int64_t N, int32_t
   return run(mlp, a);
 }
 
-ctm_status ctm_weighted_laplacian_indefinite(ctm_mlp_t mlp, const float* X, int64_t N, const float* C, float* op_out,
-                                             float* f_out, void* stream) {
-  g_last_error.clear();
-  ctm_status s = check_common(mlp, X, N, op_out, f_out);
-  if (s != CTM_OK) return s;
-  if (!C) return fail(CTM_EINVAL, "need the weighting C");
-  if (!aligned16(C)) return fail(CTM_ESHAPE, "C must be 16-byte aligned");
-  const int D = mlp->widths[0];
-  if (D > ctm::kMaxW) return fail(CTM_EUNSUPPORTED, "D > 2048 eigen-directions");
-  DeviceGuard g(mlp->device);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (!mlp->cusolver) {
-    if (cusolverDnCreate(&mlp->cusolver) != CUSOLVER_STATUS_SUCCESS) {
-      mlp->cusolver = nullptr;
-      return fail(CTM_ECUDA, "cusolverDnCreate failed");
-    }
-    CTM_CUDA(cudaMalloc(&mlp->eig_a, sizeof(double) * (size_t)D * D));
-    CTM_CUDA(cudaMalloc(&mlp->eig_w, sizeof(double) * D));
-    CTM_CUDA(cudaMalloc(&mlp->eig_info, sizeof(int)));
-    CTM_CUDA(cudaMalloc(&mlp->eig_dirs, sizeof(float) * (size_t)D * D));
-    CTM_CUDA(cudaMalloc(&mlp->eig_vals, sizeof(float) * D));
-    if (cusolverDnDsyevd_bufferSize(mlp->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, mlp->eig_a, D,
-                                    mlp->eig_w, &mlp->eig_lwork) != CUSOLVER_STATUS_SUCCESS)
-      return fail(CTM_ECUDA, "cusolverDnDsyevd_bufferSize failed");
-    CTM_CUDA(cudaMalloc(&mlp->eig_work, sizeof(double) * std::max(mlp->eig_lwork, 1)));
-  }
-  if (N == 0) return CTM_OK;
-  // C = sum_i lambda_i q_i q_i^T ("apply this scheme to the positive and negative
-  // eigen-spaces"): the collapsed K=2 directional sum with directions q_i, weights lambda_i
-  ctm::to_f64_kernel<<<(D * D + 255) / 256, 256, 0, st>>>(C, (int64_t)D * D, mlp->eig_a);
-  if (cusolverDnSetStream(mlp->cusolver, st) != CUSOLVER_STATUS_SUCCESS ||
-      cusolverDnDsyevd(mlp->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, mlp->eig_a, D, mlp->eig_w,
-                       mlp->eig_work, mlp->eig_lwork, mlp->eig_info) != CUSOLVER_STATUS_SUCCESS)
-    return fail(CTM_ECUDA, "cusolverDnDsyevd failed");
-  // column i of the column-major eigenvector matrix is contiguous: it is direction row i
-  ctm::to_f32_kernel<<<(D * D + 255) / 256, 256, 0, st>>>(mlp->eig_a, (int64_t)D * D, mlp->eig_dirs);
-  ctm::to_f32_kernel<<<(D + 255) / 256, 256, 0, st>>>(mlp->eig_w, (int64_t)D, mlp->eig_vals);
-  CallArgs a{OP_DSUM, X, N, nullptr, 0, 0, nullptr, 0, 0, D, 0, op_out, f_out, st};
-  a.K = 2;
-  a.J = D;
-  a.dirs = mlp->eig_dirs;
-  a.per_point = 0;
-  a.weights = mlp->eig_vals;
-  s = run(mlp, a);
-  mlp->last_launches += 3;  // the conversions (cuSOLVER's own kernels not counted)
-  return s;
-}
-
 ctm_status ctm_weighted_laplacian_pointwise(ctm_mlp_t mlp, const float* X, int64_t N, const float* sigma_x, int32_t R,
                                             float* op_out, float* f_out, void* stream) {
   g_last_error.clear();
@@ -1408,6 +1355,16 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act) {
                     CTM_ACT_SQUARE == ctm::kActSquare && CTM_ACT_SIN == ctm::kActSin && CTM_ACT_EXP == ctm::kActExp,
                 "ABI activation codes");
   mlp->act = (int)act;
+  mlp->tape.valid = false;  // the backward reads the activation: a tape of another one is stale
+  return CTM_OK;
+}
+
+ctm_status ctm_set_precision(ctm_mlp_t mlp, ctm_precision prec) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (prec != CTM_PRECISION_FP32 && prec != CTM_PRECISION_BF16X3) return fail(CTM_EINVAL, "unknown precision");
+  mlp->nplanes = (prec == CTM_PRECISION_FP32) ? 3 : 2;
+  mlp->tape.valid = false;
   return CTM_OK;
 }
 
@@ -1431,22 +1388,18 @@ ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable) {
   mlp->tape.valid = false;
   mlp->grad = enable != 0;
   if (!mlp->grad || mlp->cublas) return CTM_OK;
-  // W_l^T as bf16 pairs (the A operand of the adjoint GEMMs), from the split weights
+  // W_l^T as bf16 planes (the A operand of the adjoint GEMMs), from the split weights
   for (int l = 2; l <= mlp->L - 1; ++l) {
     const int mpad = mlp->wpad[l], kpad = mlp->wpad[l - 1];
-    uint16_t *thi = nullptr, *tlo = nullptr;
-    CTM_CUDA(cudaMalloc(&thi, sizeof(uint16_t) * (size_t)mpad * kpad));
-    mlp->WThi.push_back(thi);
-    CTM_CUDA(cudaMalloc(&tlo, sizeof(uint16_t) * (size_t)mpad * kpad));
-    mlp->WTlo.push_back(tlo);
+    uint16_t* tp = nullptr;
+    CTM_CUDA(cudaMalloc(&tp, 3 * sizeof(uint16_t) * (size_t)mpad * kpad));
+    mlp->WTp.push_back(tp);
     const int64_t n = (int64_t)mpad * kpad;
-    ctm::transpose_pair_kernel<<<(unsigned)((n + 255) / 256), 256>>>(mlp->Whi[l - 2], mlp->Wlo[l - 2], mpad, kpad, thi,
-                                                                     tlo);
-    CUtensorMap mh, ml;
-    if (!make_map(&mh, thi, mpad, kpad, ctm::kBM) || !make_map(&ml, tlo, mpad, kpad, ctm::kBM))
+    ctm::transpose_planes_kernel<<<(unsigned)((n + 255) / 256), 256>>>(mlp->Wp[l - 2], mpad, kpad, tp);
+    CUtensorMap mt;
+    if (!make_map3(&mt, tp, mpad, kpad, (uint64_t)n, ctm::kBM))
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W^T");
-    mlp->mapAT_hi.push_back(mh);
-    mlp->mapAT_lo.push_back(ml);
+    mlp->mapAT.push_back(mt);
   }
   {
     std::vector<float> eye(256 * 256, 0.f);

@@ -1,6 +1,6 @@
 // jet_layer.cuh — one hidden layer of collapsed Taylor mode, fused:
 //
-//   Z^T[feature, slot] = W_l[feature, :] . B_{l-1}[slot, :]      (3xTF32, tcgen05, TMEM accumulator)
+//   Z^T[feature, slot] = W_l[feature, :] . B_{l-1}[slot, :]      (bf16 planes, tcgen05, TMEM accumulator)
 //   B_l[slot, feature] = Taylor rule of tanh applied per point    (epilogue, registers)
 //
 // Swap-AB mapping: the MMA's M = 128 output features (one TMEM lane
@@ -16,29 +16,24 @@
 //   sum_w h4 = sum_j w_j (s''''z1^4 + 6s'''z1^2z2 + 4s''z1z3 + 3s''z2^2) + s' sum_w z4
 //
 // Layout in HBM: block B_l is [N*P rows, ld], row = n*P + slot, stored as
-// a bf16 pair (hi = rn_bf16(v), lo = rn_bf16(v - hi)); the tensor cores form
-// hi*hi + hi*lo + lo*hi (kind::f16, fp32 accumulation) -- "3xBF16", DESIGN.md §5.
+// bf16 planes (p0 = rn_bf16(v), p1 = rn_bf16(v - p0), p2 = rn_bf16(v - p0 - p1)), plane k at
+// k * pstride elements. Arithmetic, chosen per handle:
+//   fp32 mode (default), 3 planes: the five correction products p2*p0 + p1*p1 + p0*p2 +
+//     p1*p0 + p0*p1 over the whole K first, then p0*p0 over the whole K into the same fp32
+//     accumulator ("bf16x6, two phases": the main products see only K/16 accumulations);
+//   fast mode, 2 planes: p1*p0 + p0*p1 + p0*p0 per K step ("3xBF16", ~17 operand bits).
 #pragma once
 #include "ptx.cuh"
 
 namespace ctm {
 
-// Experiment switches (all off in the product build; scripts/experiments/README.md): a
-// build with -DCTM_EXP_<NAME> isolates one cost of the layer kernel.
-//   NOTMA     MMAs on stale operands (no L2 -> smem traffic)      NOEPI  no epilogue work
-//   NOSTORE   epilogue computes but does not store                 HALFSTORE  stores hi only
-//   L2STORE   same stores into an L2-resident per-CTA scratch      STATS  per-role cycle counters
-//   (BLOCKED, MSPREAD: measured variants described in scripts/experiments/README.md)
-#ifdef CTM_EXP_STATS
+#ifdef CTM_EXP_STATS  // per-role cycle counters (experiment builds only)
 __device__ unsigned long long g_stats[256][8];
 #define STAT_T0() const long long t0_ = clock64()
 #define STAT_ADD(i) atomicAdd(&g_stats[blockIdx.x][i], (unsigned long long)(clock64() - t0_))
 #else
 #define STAT_T0()
 #define STAT_ADD(i)
-#endif
-#ifdef CTM_EXP_L2STORE
-__device__ uint16_t g_scratch[256u * 98304u];
 #endif
 
 constexpr int kBM = 128;                         // features per CTA = TMEM lanes (a CTA pair spans 256)
@@ -47,16 +42,20 @@ constexpr int kBM = 128;                         // features per CTA = TMEM lane
 // tensor pipe is fed better by 128-byte rows (C1 layers -8.5%, C4 -4.5%, S=8 -4.5%).
 constexpr int kBK = 64;
 constexpr uint32_t kSwLayout = 2, kSwSBO = 1024;
-constexpr int kStages = 3;                       // 3 x 64 KB ring
+// The operand ring holds SLOTS of one bf16 plane of A and the same plane of B for one
+// K block (kBK). A K step of the fp32 mode's first phase needs three slots (all planes), of
+// its second phase one slot (p0 again), of the fast mode two slots.
+constexpr int kSlots = 6;                        // 6 x 32 KB ring
 constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
 constexpr int kBTileBytes = (kMaxN / 2) * kBK * 2;  // 16 KB: a CTA of the pair stages half of B
-constexpr int kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
+constexpr int kSlotBytes = kATileBytes + kBTileBytes;
+constexpr int kStageBytes = kSlotBytes;          // (ring bytes = kSlots * kSlotBytes)
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
 constexpr int kMaxW = 2048;                      // per-direction weights in smem (all blocks of a point)
 constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue (2 groups)
-constexpr int kLayerSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
+constexpr int kLayerSmem = kSlots * kSlotBytes + 1024 /*align*/ + 256 /*barriers*/ +
                            4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxW * 4 + 2 * kBM * 4 /*xacc*/;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
 // Epilogue modes (template parameter KORD): 2 = K=2 collapsed, 4 = K=4 collapsed (weighted
@@ -115,8 +114,8 @@ __device__ __forceinline__ ActD act_derivs(int act, float z) {
 // 3-5% of layer time (measured A/B, K=4 and K=2 instances).
 struct LayerParams {
   const float* bias;      // [Mpad]
-  uint16_t* out_hi;       // [rows, ldo] bf16 pair
-  uint16_t* out_lo;
+  uint16_t* out;          // [nplanes][rows, ldo] bf16 planes
+  int64_t pstride;        // elements between planes
   int ldo;
   int m_tiles;
   int64_t n_points;
@@ -136,35 +135,17 @@ struct LayerParams {
   int16_t act;            // kAct*
   float* z_out;           // forward, grad mode: the pre-activations z of every slot (fp32) or nullptr
   int ldz;
+  int16_t nplanes;        // 3: fp32 mode, 2: fast mode (operand planes read and written)
+  int16_t readout;        // last hidden layer: reduce against w_out instead of storing
   const float* z_in;      // kBwd2: this layer's saved pre-activations (fp32)
   int ldzi;
-  int readout;            // last hidden layer: reduce against w_out instead of storing
   const float* w_out;     // [Mpad] output-layer weights (zero padded)
   float* partial;         // [n_points, m_tiles, 2]
 };
 static_assert(sizeof(LayerParams) == 128, "LayerParams grew past 128 bytes (see above)");
 
-__device__ __forceinline__ void store_pair(uint16_t* hi, uint16_t* lo, size_t idx, float v) {
-  uint16_t h, l;
-#ifdef CTM_EXP_NOSTORE
-  if (v != 1234.5678f) return;
-#endif
-#ifdef CTM_EXP_L2STORE
-  {
-    const size_t e = (size_t)blockIdx.x * 98304u + (size_t)((((uintptr_t)(hi + idx)) >> 1) % 49152u);
-    ptx::bf16_split(v, h, l);
-    g_scratch[e] = h;
-    g_scratch[e + 49152u] = l;
-    return;
-  }
-#endif
-#ifdef CTM_EXP_HALFSTORE
-  hi[idx] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
-  return;
-#endif
-  ptx::bf16_split(v, h, l);
-  hi[idx] = h;
-  lo[idx] = l;
+__device__ __forceinline__ void store_out(const LayerParams& p, size_t idx, float v) {
+  ptx::store_planes(p.out + idx, p.pstride, p.nplanes, v);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -206,20 +187,18 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   fpart = (part == 2) ? 0.f : wo * t;
   opart = 0.f;
-  if (!p.readout && part != 2) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
+  if (!p.readout && part != 2) store_out(p, (size_t)row * ld + m, t);
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
   float* zp = kSaveZ ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
   if (kSaveZ && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
-  uint16_t* ph = p.out_hi + (size_t)(row + mb) * ld + m;
-  uint16_t* pl = p.out_lo + (size_t)(row + mb) * ld + m;
+  uint16_t* po = p.out + (size_t)(row + mb) * ld + m;
   // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
   //      standard-mode pairs (z1_r, z2_r) with no collapse
   float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
   int jj = (KORD == 4) ? (mb - 1) / 3 : (KORD == kStd4) ? (mb - 1) / 4 : mb - 1;  // first direction / jet
   auto put = [&](float h) {
-    if (!p.readout) store_pair(ph, pl, 0, h);
-    ph += ld;
-    pl += ld;
+    if (!p.readout) ptx::store_planes(po, p.pstride, p.nplanes, h);
+    po += ld;
   };
   if constexpr (KORD == 4) {
     // jets (z1, z2, z3), read 5 at a time (15 of 16 columns) so each slot's role is a
@@ -348,7 +327,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
   if constexpr (kSaveZ) *zp = zt;
   opart = wo * top;
-  if (!p.readout) store_pair(ph, pl, 0, top);
+  if (!p.readout) ptx::store_planes(po, p.pstride, p.nplanes, top);
 }
 
 // The K=2 rule for a point of P <= 16 slots whose 16 columns lie in the accumulator buffer:
@@ -369,17 +348,16 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   const float z0 = v[0] + bias;
   const ActD A = act_derivs(p.act, z0);
   fpart = wo * A.d0;
-  uint16_t* ph = p.out_hi + (size_t)row * ld + m;
-  uint16_t* pl = p.out_lo + (size_t)row * ld + m;
+  uint16_t* po = p.out + (size_t)row * ld + m;
   float* zp = kSaveZ ? p.z_out + (size_t)row * p.ldz + m : nullptr;
-  if (!p.readout) store_pair(ph, pl, 0, A.d0);
+  if (!p.readout) ptx::store_planes(po, p.pstride, p.nplanes, A.d0);
   if constexpr (kSaveZ) zp[0] = z0;
   float acc = 0.f, zt = 0.f;
 #pragma unroll
   for (int i = 1; i < 16; ++i) {
     if (i < P - 1) {
       const float z = v[i];
-      if (!p.readout) store_pair(ph, pl, (size_t)i * ld, A.d1 * z);
+      if (!p.readout) ptx::store_planes(po + (size_t)i * ld, p.pstride, p.nplanes, A.d1 * z);
       if constexpr (wsum)
         acc = fmaf(jw[i - 1] * z, z, acc);
       else
@@ -392,7 +370,7 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   const float top = A.d1 * zt + A.d2 * acc;
   if constexpr (kSaveZ) zp[(size_t)(P - 1) * p.ldz] = zt;
   opart = wo * top;
-  if (!p.readout) store_pair(ph, pl, (size_t)(P - 1) * ld, top);
+  if (!p.readout) ptx::store_planes(po + (size_t)(P - 1) * ld, p.pstride, p.nplanes, top);
 }
 
 // Nested-Laplacian biharmonic epilogue (kNest) for one point, the whole point in this
@@ -418,13 +396,13 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   const bool store = !p.readout;
   fpart = wo * t;
-  if (store) store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, t);
+  if (store) store_out(p, (size_t)row * ld + m, t);
   float gg = 0.f;
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a)
     if (a < D) {
       gg = fmaf(g[a], g[a], gg);
-      if (store) store_pair(p.out_hi, p.out_lo, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
+      if (store) store_out(p, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
     }
   // Hessian slots, one packed row at a time
   float hg[kNestMaxD];
@@ -444,7 +422,7 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
         if (b < D) {
           const float h = hr[b];
           if (store)
-            store_pair(p.out_hi, p.out_lo, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
+            store_out(p, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
           if (b == a) {
             trH += h;
             HF = fmaf(h, h, HF);
@@ -472,13 +450,13 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
       gHg = fmaf(g[a], hg[a], gHg);
       if (store) {
         const float v = d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * Lv[a];
-        store_pair(p.out_hi, p.out_lo, (size_t)(row + slot + a) * ld + m, v);
+        store_out(p, (size_t)(row + slot + a) * ld + m, v);
       }
     }
   const float q = d4 * gg * gg + 2.f * d3 * gg * trH + 4.f * d3 * gHg + 2.f * d2 * HF + d2 * trH * trH +
                   4.f * d2 * gL + d1 * zq;
   opart = wo * q;
-  if (store) store_pair(p.out_hi, p.out_lo, (size_t)(row + slot + D) * ld + m, q);
+  if (store) store_out(p, (size_t)(row + slot + D) * ld + m, q);
 }
 
 // The same rule with D known at compile time (D <= 8, P <= 54): the point's P columns
@@ -530,23 +508,22 @@ __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t
   fpart = wo * t;
   opart = wo * q;
   if (p.readout) return;
-  uint16_t* ph = p.out_hi + (size_t)row * ld + m;
-  uint16_t* pl = p.out_lo + (size_t)row * ld + m;
-  store_pair(ph, pl, 0, t);
+  uint16_t* po = p.out + (size_t)row * ld + m;
+  auto put = [&](size_t off, float v) { ptx::store_planes(po + off, p.pstride, p.nplanes, v); };
+  put(0, t);
 #pragma unroll
-  for (int a = 0; a < D; ++a) store_pair(ph, pl, (size_t)(1 + a) * ld, d1 * g[a]);
+  for (int a = 0; a < D; ++a) put((size_t)(1 + a) * ld, d1 * g[a]);
   {
     int k = oH;
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
-      for (int b = a; b < D; ++b, ++k) store_pair(ph, pl, (size_t)k * ld, fmaf(d2 * g[a], g[b], d1 * v[k]));
+      for (int b = a; b < D; ++b, ++k) put((size_t)k * ld, fmaf(d2 * g[a], g[b], d1 * v[k]));
   }
 #pragma unroll
   for (int a = 0; a < D; ++a)
-    store_pair(ph, pl, (size_t)(oL + a) * ld,
-               d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * v[oL + a]);
-  store_pair(ph, pl, (size_t)(P - 1) * ld, q);
+    put((size_t)(oL + a) * ld, d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * v[oL + a]);
+  put((size_t)(P - 1) * ld, q);
 }
 
 __device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32_t tcol, int64_t row, int m,
@@ -592,17 +569,15 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
   const float two_s2_tb = 2.f * A.d2 * tb;
   const bool wsum = p.weighted;
   float szh = 0.f, szz = 0.f;
-  uint16_t* ph = p.out_hi + (size_t)(row + 1) * ld + m;
-  uint16_t* pl = p.out_lo + (size_t)(row + 1) * ld + m;
+  uint16_t* po = p.out + (size_t)(row + 1) * ld + m;
   const int nmid = P - 2;
   int s = 0;
   auto one = [&](float hb, float z1, int r) {
     const float w = wsum ? jw[r] : 1.f;
     szh = fmaf(z1, hb, szh);
     szz = fmaf(w * z1, z1, szz);
-    store_pair(ph, pl, 0, fmaf(A.d1, hb, w * two_s2_tb * z1));
-    ph += ld;
-    pl += ld;
+    ptx::store_planes(po, p.pstride, p.nplanes, fmaf(A.d1, hb, w * two_s2_tb * z1));
+    po += ld;
   };
   for (; s + kB <= nmid; s += kB) {
     float v[kB], z[kB];
@@ -612,11 +587,7 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
       ptx::tmem_ld8(tcol + (uint32_t)(1 + s), v);
 #pragma unroll
     for (int i = 0; i < kB; ++i) {
-#ifdef CTM_EXP_NOZ  // experiment: no saved-Z loads in the adjoint batch loop (wrong values)
-      z[i] = v[i] * 0.5f;
-#else
       z[i] = zr[(size_t)(1 + s + i) * ldz];
-#endif
     }
     ptx::tmem_ld_wait();
 #pragma unroll
@@ -636,9 +607,9 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
     for (int i = 0; i < kB - 1; ++i)
       if (i < rem) one(v[i], z[i], s + i);
   }
-  store_pair(ph, pl, 0, A.d1 * tb);  // slot P-1
+  ptx::store_planes(po, p.pstride, p.nplanes, A.d1 * tb);  // slot P-1
   const float z0b = A.d1 * hb0 + A.d2 * szh + (A.d2 * zt + A.d3 * szz) * tb;
-  store_pair(p.out_hi, p.out_lo, (size_t)row * ld + m, z0b);
+  store_out(p, (size_t)row * ld + m, z0b);
 }
 
 // The k-th tile of CTA pair `pair`. With at least one point group per pair, a pair runs
@@ -648,17 +619,6 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
 // Returns false past the pair's last tile.
 __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_pairs, int64_t n_tiles, int64_t& n,
                                         int& m) {
-#ifdef CTM_EXP_MSPREAD  // experiment: the m_pairs feature tiles of a point group run on m_pairs pairs at once
-  {
-    const int groups = npairs / m_pairs;
-    if (n_tiles >= groups) {
-      if (pair >= groups * m_pairs) return false;
-      n = pair / m_pairs + k * groups;
-      m = pair % m_pairs;
-      return n < n_tiles;
-    }
-  }
-#endif
   if (n_tiles >= npairs) {
     n = pair + (k / m_pairs) * npairs;
     m = (int)(k % m_pairs);
@@ -677,12 +637,29 @@ __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_p
 // of both SMs read the two B halves from both CTAs' smem, so each SM stages half of B
 // (less L2 -> SM traffic and fewer smem operand reads per useful FLOP than one CTA per tile).
 // Pairs loop over tiles in the order of tile_of(). Warp roles, in BOTH CTAs:
-//   warp 0   TMA producer: its A half and B half of each k-block into a kStages-deep
-//            ring; the transaction bytes of both CTAs are counted on the LEADER's full_bar;
-//   warp 1   leader only: MMA issuer (one thread), 3 bf16 MMAs per 16-K step into one of
-//            two TMEM accumulators; commits multicast to both CTAs (empty_bar, tmem_full);
+//   warp 0   TMA producer: its A half and B half of each (K block, plane) into a kSlots-deep
+//            ring of plane slots; the transaction bytes of both CTAs are counted on the
+//            LEADER's full_bar (schedule: for_each_group below);
+//   warp 1   leader only: MMA issuer (one thread), the bf16 plane products of the
+//            precision mode into one of two TMEM accumulators; commits multicast to both
+//            CTAs (empty_bar per slot, tmem_full);
 //   warps 2-9 epilogue on this CTA's 128 accumulator lanes; releases a buffer with a
 //            remote arrive on the leader's tmem_empty (8 warps x 2 CTAs).
+// The operand schedule of one tile, as groups of consecutive ring slots:
+//   fast mode (2 planes):  K block kb -> slots {p0, p1}; per 16-K step p1*p0, p0*p1, p0*p0;
+//   fp32 mode (3 planes):  phase 1, K block kb -> slots {p0, p1, p2}; per 16-K step
+//                          p2*p0, p1*p1, p0*p2, p1*p0, p0*p1 (the corrections, ~2^-8 of the
+//                          result); phase 2, K block kb -> slot {p0}; per 16-K step p0*p0.
+// The whole-K correction pass first keeps the accumulator small while the ~5K/16 correction
+// MMAs round into it, so the round-toward-zero accumulation of the tensor cores costs what
+// K/16 plain MMAs cost (scripts/emulate_schemes.py). f(phase, kb, nslots) per group.
+template <class F>
+__device__ __forceinline__ void for_each_group(int nplanes, int k_iters, F&& f) {
+  for (int kb = 0; kb < k_iters; ++kb) f(0, kb, nplanes);
+  if (nplanes == 3)
+    for (int kb = 0; kb < k_iters; ++kb) f(1, kb, 1);
+}
+
 // Epilogue warp groups (4 warps each, one per TMEM lane quadrant) of a kernel instance. The
 // plain K=2 rule is light enough to run with 4 groups (576 threads within the 113-register
 // budget), which doubles the epilogue's point throughput when many small points share a
@@ -701,17 +678,16 @@ __host__ __device__ constexpr int layer_threads() {
 
 template <int KORD, int FLAGS = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, FLAGS>(), 1)
-    jet_layer_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
-                     const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
+    jet_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const LayerParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tmem_full_bar = empty_bar + kStages;   // [2]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kSlots * kSlotBytes);
+  uint64_t* empty_bar = full_bar + kSlots;
+  uint64_t* tmem_full_bar = empty_bar + kSlots;    // [2]
   uint64_t* tmem_empty_bar = tmem_full_bar + 2;    // [2] (used in the leader)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
-  float* red = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [4][kMaxPtsPerTile][2]
+  float* red = reinterpret_cast<float*>(smem + kSlots * kSlotBytes + 256);  // [4][kMaxPtsPerTile][2]
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
   float* xacc = jw + kMaxW;                                                 // [2][128] split-point partials
 
@@ -727,11 +703,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
   const uint32_t b_bytes = (uint32_t)half_n * kBK * 2;  // this CTA's B half of one plane
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tmA_hi);
-    ptx::tma_prefetch_desc(&tmA_lo);
-    ptx::tma_prefetch_desc(&tmB_hi);
-    ptx::tma_prefetch_desc(&tmB_lo);
-    for (int s = 0; s < kStages; ++s) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kSlots; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
@@ -762,26 +736,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       for (int64_t k = 0; tile_of(k, pair, npairs, m_pairs, n_tiles, nt, mp); ++k) {
         const int m0 = mp * (2 * kBM) + (int)rank * kBM;
         const int32_t row0 = (int32_t)(nt * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
-        for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
-          const uint32_t s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1u;
-          {
-            STAT_T0();
-            ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
-            STAT_ADD(0);  // producer waits for a free stage
+        for_each_group(p.nplanes, p.k_iters, [&](int, int kb, int nslots) {
+          for (int pl = 0; pl < nslots; ++pl, ++it) {
+            const uint32_t s = it % kSlots;
+            const uint32_t ph = (it / kSlots) & 1u;
+            {
+              STAT_T0();
+              ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
+              STAT_ADD(0);  // producer waits for a free slot
+            }
+            uint8_t* st = smem + s * kSlotBytes;
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * ((uint32_t)kATileBytes + b_bytes));
+            const int k0 = kb * kBK;
+            ptx::tma_load_3d_pair(st, &tmA, &full_bar[s], k0, m0, pl);
+            ptx::tma_load_3d_pair(st + kATileBytes, &tmB, &full_bar[s], k0, row0, pl);
           }
-#ifdef CTM_EXP_NOTMA
-          if (rank == 0) ptx::mbar_arrive(&full_bar[s]);
-          continue;
-#endif
-          uint8_t* st = smem + s * kStageBytes;
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * (2u * kATileBytes + 2u * b_bytes));
-          const int k0 = kb * kBK;
-          ptx::tma_load_2d_pair(st, &tmA_hi, &full_bar[s], k0, m0);
-          ptx::tma_load_2d_pair(st + kATileBytes, &tmA_lo, &full_bar[s], k0, m0);
-          ptx::tma_load_2d_pair(st + 2 * kATileBytes, &tmB_hi, &full_bar[s], k0, row0);
-          ptx::tma_load_2d_pair(st + 2 * kATileBytes + kBTileBytes, &tmB_lo, &full_bar[s], k0, row0);
-        }
+        });
       }
     }
   } else if (warp == 1) {
@@ -804,45 +774,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         }
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
-        for (int kb = 0; kb < p.k_iters; ++kb, ++it) {
-          const uint32_t s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1u;
-          {
+        uint32_t acc = 0;  // the tile's first MMA overwrites the accumulator
+        for_each_group(p.nplanes, p.k_iters, [&](int phase, int, int nslots) {
+          for (int pl = 0; pl < nslots; ++pl) {
             STAT_T0();
-            ptx::mbar_wait(&full_bar[s], ph);
+            ptx::mbar_wait(&full_bar[(it + pl) % kSlots], ((it + pl) / kSlots) & 1u);
             STAT_ADD(2);  // MMA waits for TMA
           }
           ptx::tc_fence_after();
-          const uint32_t a_hi = ptx::smem_u32(smem + s * kStageBytes);
-          const uint32_t a_lo = a_hi + kATileBytes;
-          const uint32_t b_hi = a_hi + 2 * kATileBytes;
-          const uint32_t b_lo = b_hi + kBTileBytes;
+          const uint32_t ring = ptx::smem_u32(smem);
+          // slot of plane i of this group (A at +0, B at +kATileBytes)
+          const uint32_t a0 = ring + (it % kSlots) * kSlotBytes;
+          const uint32_t a1 = ring + ((it + 1) % kSlots) * kSlotBytes;
+          const uint32_t a2 = ring + ((it + 2) % kSlots) * kSlotBytes;
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks) {  // bf16 MMA K = 16 (32 bytes)
             const uint32_t off = ks * 32;
-            const uint64_t dah = ptx::smem_desc_kmajor(a_hi + off, kSwSBO, kSwLayout);
-            const uint64_t dal = ptx::smem_desc_kmajor(a_lo + off, kSwSBO, kSwLayout);
-            const uint64_t dbh = ptx::smem_desc_kmajor(b_hi + off, kSwSBO, kSwLayout);
-            const uint64_t dbl = ptx::smem_desc_kmajor(b_lo + off, kSwSBO, kSwLayout);
-#ifdef CTM_EXP_TSA
-            // experiment: A staged into TMEM columns [240, 256) of buffer 0 (free while
-            // N <= 240), then read from TMEM by the MMAs (no repeated A reads from smem)
-            if (p.n_mma <= 240) {
-              const uint32_t ta_hi = tmem_base + 240u, ta_lo = tmem_base + 248u;
-              ptx::tmem_cp_128x256b_pair(ta_hi, dah);
-              ptx::tmem_cp_128x256b_pair(ta_lo, dal);
-              ptx::mma_bf16_pair_ts(d_tmem, ta_lo, dbh, idesc, (kb | ks) != 0);  // lo * hi
-              ptx::mma_bf16_pair_ts(d_tmem, ta_hi, dbl, idesc, 1u);               // hi * lo
-              ptx::mma_bf16_pair_ts(d_tmem, ta_hi, dbh, idesc, 1u);               // hi * hi
-              continue;
+            auto mma = [&](uint32_t ai, uint32_t aj) {  // A plane of slot ai x B plane of slot aj
+              ptx::mma_bf16_pair(d_tmem, ptx::smem_desc_kmajor(ai + off, kSwSBO, kSwLayout),
+                                 ptx::smem_desc_kmajor(aj + kATileBytes + off, kSwSBO, kSwLayout), idesc, acc);
+              acc = 1u;
+            };
+            if (nslots == 2) {
+              mma(a1, a0);
+              mma(a0, a1);
+              mma(a0, a0);
+            } else if (nslots == 3) {
+              mma(a2, a0);
+              mma(a1, a1);
+              mma(a0, a2);
+              mma(a1, a0);
+              mma(a0, a1);
+            } else {
+              mma(a0, a0);
             }
-#endif
-            ptx::mma_bf16_pair(d_tmem, dal, dbh, idesc, (kb | ks) != 0);  // lo * hi
-            ptx::mma_bf16_pair(d_tmem, dah, dbl, idesc, 1u);               // hi * lo
-            ptx::mma_bf16_pair(d_tmem, dah, dbh, idesc, 1u);               // hi * hi
           }
-          ptx::mma_commit_pair(&empty_bar[s]);  // both CTAs' stage s is free once these retire
-        }
+          for (int pl = 0; pl < nslots; ++pl)  // both CTAs' slots are free once these retire
+            ptx::mma_commit_pair(&empty_bar[(it + pl) % kSlots]);
+          it += nslots;
+          (void)phase;
+        });
         ptx::mma_commit_pair(&tmem_full_bar[buf]);  // both CTAs' accumulator halves complete
       }
 #ifdef CTM_EXP_STATS
@@ -885,10 +856,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
 #endif
       ptx::tc_fence_after();
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
-#ifdef CTM_EXP_NOEPI
-      if (true) {
-      } else
-#endif
       if (KORD == kBwd2) {
         for (int pt = g; pt < npts; pt += EG)
           epilogue_bwd2<EG == 4 ? 8 : 16>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);

@@ -51,6 +51,26 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// 3D tile load (coordinates {c0 inner, c1 rows, c2 plane}), pair form: bytes land in this
+// CTA's smem, completion counted on the leader's mbarrier (see tma_load_2d_pair).
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
+                                                 int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// 3D tile load into this CTA's smem, completion on this CTA's mbarrier.
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
+                                            int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- clusters (CTA pairs)
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -239,14 +259,25 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint6
       : "memory");
 }
 
-// bf16 pair split of an fp32 value: hi = rn_bf16(v), lo = rn_bf16(v - hi)
-// (v - hi is exact in fp32). hi*hi + hi*lo + lo*hi carries ~2^-16 relative accuracy
-// per operand pair.
-__device__ __forceinline__ void bf16_split(float v, uint16_t& hi, uint16_t& lo) {
+// bf16 plane split of an fp32 value: p0 = rn_bf16(v), p1 = rn_bf16(v - p0),
+// p2 = rn_bf16(v - p0 - p1); each difference is exact in fp32. Three planes hold all 24
+// bits of v (p0 + p1 + p2 = v up to 2^-27 |v|); the fast mode stores only p0 and p1 (~17 bits).
+__device__ __forceinline__ void bf16_split3(float v, uint16_t& p0, uint16_t& p1, uint16_t& p2) {
   const __nv_bfloat16 h = __float2bfloat16_rn(v);
-  const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
-  hi = __bfloat16_as_ushort(h);
-  lo = __bfloat16_as_ushort(l);
+  const float r = v - __bfloat162float(h);
+  const __nv_bfloat16 m = __float2bfloat16_rn(r);
+  const __nv_bfloat16 l = __float2bfloat16_rn(r - __bfloat162float(m));
+  p0 = __bfloat16_as_ushort(h);
+  p1 = __bfloat16_as_ushort(m);
+  p2 = __bfloat16_as_ushort(l);
+}
+// The value's first nplanes planes at p, p + pstride (, p + 2 pstride).
+__device__ __forceinline__ void store_planes(uint16_t* p, int64_t pstride, int nplanes, float v) {
+  uint16_t a, b, c;
+  bf16_split3(v, a, b, c);
+  p[0] = a;
+  p[pstride] = b;
+  if (nplanes > 2) p[2 * pstride] = c;
 }
 // Programmatic dependent launch: the next kernel in the stream may start its prologue
 // once every CTA of this grid has called launch_dependents (or exited); wait_prior blocks
@@ -255,6 +286,12 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 __device__ __forceinline__ void pdl_wait_prior() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ float bf16_val(uint16_t b) { return __bfloat162float(__ushort_as_bfloat16(b)); }
+// the fp32 value of a plane-split element (sum of its planes, small first)
+__device__ __forceinline__ float planes_val(const uint16_t* p, int64_t pstride, int nplanes) {
+  float v = nplanes > 2 ? bf16_val(p[2 * pstride]) : 0.f;
+  v += bf16_val(p[pstride]);
+  return v + bf16_val(p[0]);
+}
 
 }  // namespace ptx
 }  // namespace ctm

@@ -41,22 +41,32 @@ struct SeedParams {
   int R;                 // K=2: number of directions; K=4: number of jets J
   int blocks;            // direction blocks per point (jet_layer.cuh, LayerParams::blocks)
   int rb;                // directions (K=4: jets) per block; the last block is zero padded
-  uint16_t* out_hi;      // [N*blocks*P, ld] bf16 pair
-  uint16_t* out_lo;
+  uint16_t* out;         // [nplanes][N*blocks*P, ld] bf16 planes
+  int64_t pstride;       // elements between planes
+  int nplanes;
   int act;               // kAct*
   float* z_out;          // K=2, grad mode (one block): pre-activations [N*P, ld] (z0, W1 u_r, 0) or nullptr
 };
 
-// four adjacent features -> one 8-byte store into each of the hi and lo planes
-__device__ __forceinline__ void seed_store4(uint16_t* hi, uint16_t* lo, size_t idx, float a, float b, float c,
-                                           float d) {
-  uint16_t h[4], l[4];
-  ptx::bf16_split(a, h[0], l[0]);
-  ptx::bf16_split(b, h[1], l[1]);
-  ptx::bf16_split(c, h[2], l[2]);
-  ptx::bf16_split(d, h[3], l[3]);
-  *reinterpret_cast<uint2*>(hi + idx) = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
-  *reinterpret_cast<uint2*>(lo + idx) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+// Where a kernel writes its bf16 planes: plane k of element i at base[k * pstride + i].
+struct PlaneOut {
+  uint16_t* base;
+  int64_t pstride;
+  int nplanes;
+};
+
+// four adjacent features -> one 8-byte store into each plane
+__device__ __forceinline__ void seed_store4(const PlaneOut& o, size_t idx, float a, float b, float c, float d) {
+  uint16_t h[3][4];
+  ptx::bf16_split3(a, h[0][0], h[1][0], h[2][0]);
+  ptx::bf16_split3(b, h[0][1], h[1][1], h[2][1]);
+  ptx::bf16_split3(c, h[0][2], h[1][2], h[2][2]);
+  ptx::bf16_split3(d, h[0][3], h[1][3], h[2][3]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (k < o.nplanes)
+      *reinterpret_cast<uint2*>(o.base + k * o.pstride + idx) =
+          make_uint2(h[k][0] | ((uint32_t)h[k][1] << 16), h[k][2] | ((uint32_t)h[k][3] << 16));
 }
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -71,6 +81,7 @@ template <int KORD>
 // kernel needs for its occupancy: 40 registers for K=2 / standard, 48 for K=4 / nested)
 __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6 : 5)
     seed_layer_kernel(const SeedParams p) {
+  const PlaneOut o{p.out, p.pstride, p.nplanes};
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
@@ -100,15 +111,15 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
     const size_t row0 = ((size_t)n * p.blocks + b) * p.P;                \
     const int r0 = b * p.rb;                                             \
     const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;                  \
-    seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    seed_store4(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
 #define CTM_BLOCK_END }
   if (KORD == kStd2) {
     CTM_BLOCK_BEGIN
     // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
     auto pair = [&](const float4 u, int r) {
       const size_t rr = row0 + 1 + 2 * (r - r0);
-      seed_store4(p.out_hi, p.out_lo, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
-      seed_store4(p.out_hi, p.out_lo, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
+      seed_store4(o, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+      seed_store4(o, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
     };
     int r = r0;
@@ -143,7 +154,7 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       const size_t r = row0 + 1 + 4 * (j - r0);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        seed_store4(p.out_hi, p.out_lo, (r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3]);
+        seed_store4(o, (r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3]);
     }
     CTM_BLOCK_END
   } else if (KORD == 2) {
@@ -169,18 +180,18 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       for (int i = 0; i < CTM_SEED_BATCH; ++i) u[i] = ldg4(p.UT + (size_t)(r + i) * p.ld + m);
 #pragma unroll
       for (int i = 0; i < CTM_SEED_BATCH; ++i)
-        seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0 + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
+        seed_store4(o, (row0 + 1 + r - r0 + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
                     d1[2] * u[i].z, d1[3] * u[i].w);
     }
     for (; r < r1; ++r) {
       const float4 u = ldg4(p.UT + (size_t)r * p.ld + m);
-      seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
+      seed_store4(o, (row0 + 1 + r - r0) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
                   d1[3] * u.w);
     }
-    for (; r < r0 + p.rb; ++r) seed_store4(p.out_hi, p.out_lo, (row0 + 1 + r - r0) * p.ld + m, 0.f, 0.f, 0.f, 0.f);
+    for (; r < r0 + p.rb; ++r) seed_store4(o, (row0 + 1 + r - r0) * p.ld + m, 0.f, 0.f, 0.f, 0.f);
     // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
     const float4 cs = ldg4(p.csum + (size_t)b * p.ld + m);
-    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + p.rb) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
+    seed_store4(o, (row0 + 1 + p.rb) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
                 d2[3] * cs.w);
     CTM_BLOCK_END
   } else if (KORD == kNest) {
@@ -188,27 +199,27 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
     // the input, so h_a = s' g_a, H'_ab = s'' g_a g_b, L'_a = s''' g_a |g|^2,
     // Q' = s'''' |g|^4 (the epilogue rule of jet_layer.cuh with H = L = Q = 0); |g|^2 = csum.
     const size_t row0 = (size_t)n * p.P;
-    seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    seed_store4(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
     const float4 cs = ldg4(p.csum + m);
     size_t r = row0 + 1;
     for (int a = 0; a < p.R; ++a, ++r) {
       const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
-      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+      seed_store4(o, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
     }
     for (int a = 0; a < p.R; ++a) {
       const float4 ua = ldg4(p.UT + (size_t)a * p.ld + m);
       for (int c = a; c < p.R; ++c, ++r) {
         const float4 uc = ldg4(p.UT + (size_t)c * p.ld + m);
-        seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y,
+        seed_store4(o, r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y,
                     d2[2] * ua.z * uc.z, d2[3] * ua.w * uc.w);
       }
     }
     for (int a = 0; a < p.R; ++a, ++r) {
       const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
-      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
+      seed_store4(o, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
                   d3[3] * u.w * cs.w);
     }
-    seed_store4(p.out_hi, p.out_lo, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
+    seed_store4(o, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
                 d4[3] * cs.w * cs.w);
   } else {
     CTM_BLOCK_BEGIN
@@ -222,9 +233,9 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
         h3[i] = d3[i] * z[i] * z[i] * z[i];         // h3 (z2 = z3 = 0)
       }
       const size_t r = row0 + 1 + 3 * (j - r0);
-      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
-      seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
-      seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+      seed_store4(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+      seed_store4(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+      seed_store4(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
     };
     int j = r0;
 #ifndef CTM_SEED_BATCH4
@@ -243,7 +254,7 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       jet((j < r1) ? ldg4(p.UT + (size_t)j * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f), j);
     // sum_w h4 = tanh'''' * sum_j w_j z1_j^4 over the block's jets   (z2 = z3 = z4 = 0)
     const float4 cs = ldg4(p.csum + (size_t)b * p.ld + m);
-    seed_store4(p.out_hi, p.out_lo, (row0 + 1 + 3 * p.rb) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
+    seed_store4(o, (row0 + 1 + 3 * p.rb) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
                 d4[3] * cs.w);
     CTM_BLOCK_END
   }
@@ -271,8 +282,9 @@ struct SeedStochParams {
   int blocks;            // sample blocks per point, `rb` samples each (last one zero padded)
   int rb;
   int standard;          // 1: standard K=4 layout, per sample (h1, h2, h3, h4), 1 + 4 rb rows
-  uint16_t* out_hi;      // [N*blocks*(3rb+2), ld] (standard: [N*blocks*(1+4rb), ld])
-  uint16_t* out_lo;
+  uint16_t* out;         // planes of [N*blocks*(3rb+2), ld] (standard: [N*blocks*(1+4rb), ld])
+  int64_t pstride;
+  int nplanes;
   int act;
 };
 
@@ -280,6 +292,7 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx);
 
 __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(const SeedStochParams p) {
   extern __shared__ float vsh[];  // [S, D]
+  const PlaneOut o{p.out, p.pstride, p.nplanes};
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
@@ -314,7 +327,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   }
   for (int b = 0; b < p.blocks; ++b) {
     const size_t row0 = ((size_t)n * p.blocks + b) * P;
-    seed_store4(p.out_hi, p.out_lo, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    seed_store4(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int s = b * p.rb; s < (b + 1) * p.rb; ++s) {
       float z[4] = {0.f, 0.f, 0.f, 0.f};
@@ -338,18 +351,18 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
         acc[i] = fmaf((p.w && s < p.S) ? p.w[s] * z2 : z2, z2, acc[i]);
       }
       const size_t r = row0 + 1 + st * (size_t)(s - b * p.rb);
-      seed_store4(p.out_hi, p.out_lo, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
-      seed_store4(p.out_hi, p.out_lo, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
-      seed_store4(p.out_hi, p.out_lo, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+      seed_store4(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+      seed_store4(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+      seed_store4(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
       if (p.standard) {  // h4 of this sample = s'''' z1^4   (x2 = x3 = x4 = 0)
         float h4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) h4[i] = d4[i] * (z[i] * z[i]) * (z[i] * z[i]);
-        seed_store4(p.out_hi, p.out_lo, (r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3]);
+        seed_store4(o, (r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3]);
       }
     }
     if (!p.standard)
-      seed_store4(p.out_hi, p.out_lo, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
+      seed_store4(o, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
                   d4[3] * acc[3]);
   }
 }
@@ -376,8 +389,9 @@ struct SeedRandomParams {
   int blocks;            // direction blocks per point, `rb` directions each (last one zero padded)
   int rb;
   int standard;          // 1: standard Taylor mode layout [x0; (u_s, 0) per direction], 1 + 2 rb rows
-  uint16_t* out_hi;      // [N*blocks*(rb+2), ldk] (standard: [N*blocks*(1+2rb), ldk])
-  uint16_t* out_lo;
+  uint16_t* out;         // planes of [N*blocks*(rb+2), ldk] (standard: [N*blocks*(1+2rb), ldk])
+  int64_t pstride;
+  int nplanes;
 };
 
 // Standard normal draw for counter idx: Box-Muller on two splitmix64 outputs
@@ -391,6 +405,7 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx) {
 
 __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
   __shared__ float vs[kSeedChunk];
+  const PlaneOut o{p.out, p.pstride, p.nplanes};
   const int64_t n = blockIdx.x;
   const int st = p.standard ? 2 : 1;            // rows per direction
   const int P = p.standard ? 1 + 2 * p.rb : p.rb + 2;  // slots per block
@@ -405,14 +420,14 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = (4 * c4 + i < p.D) ? p.X[n * p.D + 4 * c4 + i] : 0.f;
     for (int b = 0; b < p.blocks; ++b) {
-      seed_store4(p.out_hi, p.out_lo, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
-      if (!p.standard) seed_store4(p.out_hi, p.out_lo, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+      seed_store4(o, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
+      if (!p.standard) seed_store4(o, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
     }
     if (p.standard)
       for (int s = 0; s < p.blocks * p.rb; ++s)
-        seed_store4(p.out_hi, p.out_lo, (dir_row(s) + 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+        seed_store4(o, (dir_row(s) + 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
     for (int s = p.S; s < p.blocks * p.rb; ++s)
-      seed_store4(p.out_hi, p.out_lo, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+      seed_store4(o, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
   }
   const int per_chunk = kSeedChunk / p.Rv;
   for (int s0 = 0; s0 < p.S; s0 += per_chunk) {
@@ -449,7 +464,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
         }
         u[i] = val;
       }
-      seed_store4(p.out_hi, p.out_lo, dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
+      seed_store4(o, dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
     }
   }
 }
@@ -540,7 +555,7 @@ __global__ void finalize_kernel(const float* __restrict__ partial, int m_tiles, 
 // standard == 2: the op is sum_r w_out . h2_r over rows 2, 4, .., P-1 (standard mode);
 // standard == 4: sum_j jw[j] w_out . h4_j over rows 4, 8, .., P-1 (standard K=4 mode, jw
 // indexed over all blocks of the point)
-__global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo, int ld, int P,
+__global__ void readout_block_kernel(const uint16_t* __restrict__ in, int64_t pstride, int nplanes, int ld, int P,
                                      int blocks, int width, const float* __restrict__ w_out,
                                      const float* __restrict__ b_out, float scale, int64_t N, float* __restrict__ op,
                                      float* __restrict__ f, int standard, const float* __restrict__ jw, int rb,
@@ -553,15 +568,15 @@ __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint
     const size_t sp = (size_t)n * blocks + b;
     const size_t r0 = sp * P * ld, rt = (sp * P + P - 1) * ld;
     for (int m = lane; m < width; m += 32) {
-      if (b == 0) s0 = fmaf(w_out[m], ptx::bf16_val(hi[r0 + m]) + ptx::bf16_val(lo[r0 + m]), s0);
+      if (b == 0) s0 = fmaf(w_out[m], ptx::planes_val(in + r0 + m, pstride, nplanes), s0);
       if (!standard) {
-        s1 = fmaf(w_out[m], ptx::bf16_val(hi[rt + m]) + ptx::bf16_val(lo[rt + m]), s1);
+        s1 = fmaf(w_out[m], ptx::planes_val(in + rt + m, pstride, nplanes), s1);
       } else {
         for (int r = standard; r < P; r += standard) {
           const size_t ri = (sp * P + r) * ld;
           const int j = b * rb + r / 4 - 1;
           const float c = (standard == 4) ? ((j < J) ? jw[j] : 0.f) : 1.f;
-          s1 = fmaf(c * w_out[m], ptx::bf16_val(hi[ri + m]) + ptx::bf16_val(lo[ri + m]), s1);
+          s1 = fmaf(c * w_out[m], ptx::planes_val(in + ri + m, pstride, nplanes), s1);
         }
       }
     }
@@ -577,16 +592,16 @@ __global__ void readout_block_kernel(const uint16_t* __restrict__ hi, const uint
   }
 }
 
-// Split W [rows, cols] (row-major, device) into padded bf16 pairs [Mpad, Kpad];
-// bias into [Mpad]. Padding is zero.
+// Split W [rows, cols] (row-major, device) into three padded bf16 planes [3][Mpad, Kpad]
+// (plane stride Mpad * Kpad); bias into [Mpad]. Padding is zero.
 __global__ void split_weights_kernel(const float* __restrict__ W, const float* __restrict__ b, int rows, int cols,
-                                     int Mpad, int Kpad, uint16_t* __restrict__ Whi, uint16_t* __restrict__ Wlo,
-                                     float* __restrict__ bpad) {
+                                     int Mpad, int Kpad, uint16_t* __restrict__ Wp, float* __restrict__ bpad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)Mpad * Kpad) return;
+  const int64_t n = (int64_t)Mpad * Kpad;
+  if (i >= n) return;
   const int r = (int)(i / Kpad), c = (int)(i % Kpad);
   const float v = (r < rows && c < cols) ? W[(size_t)r * cols + c] : 0.f;
-  ptx::bf16_split(v, Whi[i], Wlo[i]);
+  ptx::bf16_split3(v, Wp[i], Wp[n + i], Wp[2 * n + i]);
   if (c == 0) bpad[r] = (r < rows) ? b[r] : 0.f;
 }
 
@@ -598,15 +613,6 @@ __global__ void transpose_w1_kernel(const float* __restrict__ W1, const float* _
   const int d = (int)(i / ld), m = (int)(i % ld);
   W1T[i] = (m < w1) ? W1[(size_t)m * D + d] : 0.f;
   if (d == 0) b1p[m] = (m < w1) ? b1[m] : 0.f;
-}
-
-__global__ void to_f64_kernel(const float* __restrict__ src, int64_t n, double* __restrict__ dst) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = (double)src[i];
-}
-__global__ void to_f32_kernel(const double* __restrict__ src, int64_t n, float* __restrict__ dst) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = (float)src[i];
 }
 
 __global__ void pad_vector_kernel(const float* __restrict__ src, int n, int npad, float* __restrict__ dst) {

@@ -1019,9 +1019,11 @@ def test_biharmonic_standard_mode_parity(ctm, widths, N, rb):
 
 @pytest.mark.parametrize("widths,N", [([5, 32, 24, 1], 7), (C1_WIDTHS, 5)])
 def test_weighted_laplacian_indefinite(ctm, widths, N):
-    """<d^2 f, C> for a symmetric INDEFINITE C (eigen-spaces of both signs), against
-    the exact Hessian of the fp64 net by torch autograd (independent of the oracle and of
-    any eigendecomposition); the normaliser is sum_i |lambda_i q_i^T H q_i|."""
+    """<d^2 f, C> for a symmetric INDEFINITE C (eigen-spaces of both signs) as the
+    caller's recipe: C = sum_i lambda_i q_i q_i^T by numpy, then ONE collapsed K=2
+    directional sum with directions q_i and signed weights lambda_i (the library takes no
+    eigensolver, SURVEY Q7 marks indefinite weightings out of the hot path). Checked against
+    the exact Hessian of the fp64 net by torch autograd; normaliser sum_i |lambda_i q_i^T H q_i|."""
     params, _ = nets(widths, seed=9)
     D = widths[0]
     rng = np.random.default_rng(9)
@@ -1047,7 +1049,8 @@ def test_weighted_laplacian_indefinite(ctm, widths, N):
         want[n] = np.sum(H * C.astype(np.float64))
         norm[n] = np.sum(np.abs(lam * np.einsum("ai,ab,bi->i", Q, H, Q)))
     mlp = gpu_mlp(ctm, params)
-    op, _ = mlp.weighted_laplacian_indefinite(torch.from_numpy(X).cuda(), torch.from_numpy(C).cuda())
+    dirs = torch.from_numpy(np.ascontiguousarray(Q.T).astype(np.float32)).cuda()
+    op, _ = mlp.directional_sum(torch.from_numpy(X).cuda(), 2, dirs, torch.from_numpy(lam.astype(np.float32)).cuda())
     check(op, want, norm)
 
 
