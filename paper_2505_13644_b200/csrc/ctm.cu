@@ -466,6 +466,13 @@ struct LayerIO {
   float* z;
 };
 
+void launch_seed_random(int nplanes, int64_t N, const ctm::SeedRandomParams& rp, cudaStream_t st) {
+  if (nplanes == 3)
+    ctm::seed_random_kernel<3><<<(unsigned)N, ctm::kSeedThreads, 0, st>>>(rp);
+  else
+    ctm::seed_random_kernel<2><<<(unsigned)N, ctm::kSeedThreads, 0, st>>>(rp);
+}
+
 // Layer 1 for fixed direction sets (and the stochastic biharmonic) for points
 // [p0, p0 + n): writes the layer-1 output block into buf.
 ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, int64_t p0, int64_t n,
@@ -497,7 +504,10 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     bp.pstride = (int64_t)buf.cap;
     bp.nplanes = h->nplanes;
     bp.act = h->act;
-    ctm::seed_stoch_biharmonic_kernel<<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
+    if (h->nplanes == 3)
+      ctm::seed_stoch_biharmonic_kernel<3><<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
+    else
+      ctm::seed_stoch_biharmonic_kernel<2><<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
   } else {
     ctm::SeedParams sp{};
     sp.X = a.X + p0 * D;
@@ -517,16 +527,20 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     sp.nplanes = h->nplanes;
     sp.act = h->act;
     sp.z_out = z_out;
+#define CTM_SEED(K)                                                            \
+  (h->nplanes == 3 ? ctm::seed_layer_kernel<K, 3><<<(unsigned)blocks, threads, 0, st>>>(sp) \
+                   : ctm::seed_layer_kernel<K, 2><<<(unsigned)blocks, threads, 0, st>>>(sp))
     if (KORD == 2)
-      ctm::seed_layer_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      CTM_SEED(2);
     else if (KORD == 4)
-      ctm::seed_layer_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      CTM_SEED(4);
     else if (KORD == ctm::kNest)
-      ctm::seed_layer_kernel<ctm::kNest><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      CTM_SEED(ctm::kNest);
     else if (KORD == ctm::kStd4)
-      ctm::seed_layer_kernel<ctm::kStd4><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      CTM_SEED(ctm::kStd4);
     else
-      ctm::seed_layer_kernel<ctm::kStd2><<<(unsigned)blocks, threads, 0, st>>>(sp);
+      CTM_SEED(ctm::kStd2);
+#undef CTM_SEED
   }
   ++launches;
   return CTM_OK;
@@ -767,7 +781,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.nplanes = h->nplanes;
     {
       ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 4.0, st);
-      ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
+      launch_seed_random(h->nplanes, a.N, rp, st);
     }
     ++launches;
     const float scale = (a.op == OP_RLAP || a.op == OP_RLAP_STD) ? 1.f / (float)a.S : 1.f;  // Eq. 8/10 stochastic
@@ -845,7 +859,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       rp.out = tapeB0->p;
       rp.pstride = (int64_t)tapeB0->cap;
       rp.nplanes = h->nplanes;
-      ctm::seed_random_kernel<<<(unsigned)a.N, ctm::kSeedThreads, 0, st>>>(rp);
+      launch_seed_random(h->nplanes, a.N, rp, st);
       ++launches;
     }
     s = launch_seed(h, a, KORD, pl, 0, a.N, grad ? *tapeB1 : h->blk[2], UT, csum, a.op == OP_BIH_NEST ? D : R, st,

@@ -755,12 +755,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader, one thread)
-    if (rank == 0 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader warp, one elected lane)
+    // The whole warp runs the schedule (waits, descriptor arithmetic in uniform registers);
+    // one elected lane issues. A lane-0-only branch made every MMA a divergent R2UR loop and
+    // left the tensor pipe waiting on the issuing thread (STATS build: issuer busy 89%).
+    if (rank == 0) {
 #ifdef CTM_EXP_STATS
       const long long tstart = clock64();
 #endif
       const uint32_t idesc = ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
+      // K-major SW128 descriptor of slot 0's A tile (slot s: + s * kSlotBytes >> 4)
+      const uint64_t desc0 = ptx::smem_desc_kmajor(ptx::smem_u32(smem), kSwSBO, kSwLayout);
       uint32_t it = 0, local = 0;
       int64_t nt;
       int mp;
@@ -770,7 +775,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         {
           STAT_T0();
           ptx::mbar_wait(&tmem_empty_bar[buf], (use & 1u) ^ 1u);
-          STAT_ADD(1);  // MMA waits for the epilogue to free an accumulator
+          if (lane == 0) STAT_ADD(1);  // MMA waits for the epilogue to free an accumulator
         }
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
@@ -779,46 +784,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           for (int pl = 0; pl < nslots; ++pl) {
             STAT_T0();
             ptx::mbar_wait(&full_bar[(it + pl) % kSlots], ((it + pl) / kSlots) & 1u);
-            STAT_ADD(2);  // MMA waits for TMA
+            if (lane == 0) STAT_ADD(2);  // MMA waits for TMA
           }
           ptx::tc_fence_after();
-          const uint32_t ring = ptx::smem_u32(smem);
-          // slot of plane i of this group (A at +0, B at +kATileBytes)
-          const uint32_t a0 = ring + (it % kSlots) * kSlotBytes;
-          const uint32_t a1 = ring + ((it + 1) % kSlots) * kSlotBytes;
-          const uint32_t a2 = ring + ((it + 2) % kSlots) * kSlotBytes;
+          // descriptors of plane i of this group (A at the slot, B at +kATileBytes); the
+          // start-address field is addr >> 4 in the low bits, so a K step of 32 bytes adds 2
+          // (the single issuing thread must keep up with one MMA per ~100 tensor cycles)
+          constexpr uint64_t kS = kSlotBytes >> 4;
+          const uint64_t dA0 = desc0 + (it % kSlots) * kS, dA1 = desc0 + ((it + 1) % kSlots) * kS,
+                         dA2 = desc0 + ((it + 2) % kSlots) * kS;
+          constexpr uint64_t kB = kATileBytes >> 4;
+          if (ptx::elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks) {  // bf16 MMA K = 16 (32 bytes)
-            const uint32_t off = ks * 32;
-            auto mma = [&](uint32_t ai, uint32_t aj) {  // A plane of slot ai x B plane of slot aj
-              ptx::mma_bf16_pair(d_tmem, ptx::smem_desc_kmajor(ai + off, kSwSBO, kSwLayout),
-                                 ptx::smem_desc_kmajor(aj + kATileBytes + off, kSwSBO, kSwLayout), idesc, acc);
-              acc = 1u;
-            };
+            const uint64_t o = 2u * ks;
             if (nslots == 2) {
-              mma(a1, a0);
-              mma(a0, a1);
-              mma(a0, a0);
+              ptx::mma_bf16_pair(d_tmem, dA1 + o, dA0 + kB + o, idesc, acc);
+              ptx::mma_bf16_pair(d_tmem, dA0 + o, dA1 + kB + o, idesc, 1u);
+              ptx::mma_bf16_pair(d_tmem, dA0 + o, dA0 + kB + o, idesc, 1u);
             } else if (nslots == 3) {
-              mma(a2, a0);
-              mma(a1, a1);
-              mma(a0, a2);
-              mma(a1, a0);
-              mma(a0, a1);
+              ptx::mma_bf16_pair(d_tmem, dA2 + o, dA0 + kB + o, idesc, acc);
+              ptx::mma_bf16_pair(d_tmem, dA1 + o, dA1 + kB + o, idesc, 1u);
+              ptx::mma_bf16_pair(d_tmem, dA0 + o, dA2 + kB + o, idesc, 1u);
+              ptx::mma_bf16_pair(d_tmem, dA1 + o, dA0 + kB + o, idesc, 1u);
+              ptx::mma_bf16_pair(d_tmem, dA0 + o, dA1 + kB + o, idesc, 1u);
             } else {
-              mma(a0, a0);
+              ptx::mma_bf16_pair(d_tmem, dA0 + o, dA0 + kB + o, idesc, acc);
             }
+            acc = 1u;
           }
           for (int pl = 0; pl < nslots; ++pl)  // both CTAs' slots are free once these retire
             ptx::mma_commit_pair(&empty_bar[(it + pl) % kSlots]);
+          }
+          __syncwarp();
+          acc = 1u;
           it += nslots;
           (void)phase;
         });
-        ptx::mma_commit_pair(&tmem_full_bar[buf]);  // both CTAs' accumulator halves complete
+        if (ptx::elect_one()) ptx::mma_commit_pair(&tmem_full_bar[buf]);  // both CTAs' accumulator halves complete
+        __syncwarp();
       }
 #ifdef CTM_EXP_STATS
-      g_stats[blockIdx.x][3] += clock64() - tstart;  // MMA issuer lifetime
-      g_stats[blockIdx.x][7] += local;               // tiles
+      if (lane == 0) {
+        g_stats[blockIdx.x][3] += clock64() - tstart;  // MMA issuer lifetime
+        g_stats[blockIdx.x][7] += local;               // tiles
+      }
 #endif
     }
   } else {

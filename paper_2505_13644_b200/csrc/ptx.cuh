@@ -142,6 +142,16 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, 
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One lane of a converged warp (elect.sync): issue single-thread instructions (tcgen05.mma,
+// commits) from converged code so their operands stay in uniform registers (no per-MMA
+// R2UR waterfall loop of a divergent lane-0 branch).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 // Arrive on the mbarrier at this offset in both CTAs of the pair once the MMAs complete.
 // A from tensor memory ("TS"): A is read from this CTA's TMEM columns at a_tmem (128 lanes
 // x K=16 bf16 = 8 columns), B from shared memory as in mma_bf16_pair.
@@ -271,13 +281,19 @@ __device__ __forceinline__ void bf16_split3(float v, uint16_t& p0, uint16_t& p1,
   p1 = __bfloat16_as_ushort(m);
   p2 = __bfloat16_as_ushort(l);
 }
-// The value's first nplanes planes at p, p + pstride (, p + 2 pstride).
+// The value's first nplanes planes at p, p + pstride (, p + 2 pstride) (the third plane
+// is only computed when stored).
 __device__ __forceinline__ void store_planes(uint16_t* p, int64_t pstride, int nplanes, float v) {
-  uint16_t a, b, c;
-  bf16_split3(v, a, b, c);
-  p[0] = a;
-  p[pstride] = b;
-  if (nplanes > 2) p[2 * pstride] = c;
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  const float r = v - __bfloat162float(h);
+  const __nv_bfloat16 m = __float2bfloat16_rn(r);
+  p[0] = __bfloat16_as_ushort(h);
+  p[pstride] = __bfloat16_as_ushort(m);
+#ifdef CTM_EXP_NP2  // experiment: the fast mode's two planes at compile time
+  (void)nplanes;
+#else
+  if (nplanes > 2) p[2 * pstride] = __bfloat16_as_ushort(__float2bfloat16_rn(r - __bfloat162float(m)));
+#endif
 }
 // Programmatic dependent launch: the next kernel in the stream may start its prologue
 // once every CTA of this grid has called launch_dependents (or exited); wait_prior blocks

@@ -55,18 +55,24 @@ struct PlaneOut {
   int nplanes;
 };
 
-// four adjacent features -> one 8-byte store into each plane
+// four adjacent features -> one 8-byte store into each of the NP planes (plane by plane,
+// so only the four residuals stay live: the seed kernels run at 40-48 registers)
+template <int NP>
 __device__ __forceinline__ void seed_store4(const PlaneOut& o, size_t idx, float a, float b, float c, float d) {
-  uint16_t h[3][4];
-  ptx::bf16_split3(a, h[0][0], h[1][0], h[2][0]);
-  ptx::bf16_split3(b, h[0][1], h[1][1], h[2][1]);
-  ptx::bf16_split3(c, h[0][2], h[1][2], h[2][2]);
-  ptx::bf16_split3(d, h[0][3], h[1][3], h[2][3]);
+  float r[4] = {a, b, c, d};
+  uint16_t* dst = o.base + idx;
 #pragma unroll
-  for (int k = 0; k < 3; ++k)
-    if (k < o.nplanes)
-      *reinterpret_cast<uint2*>(o.base + k * o.pstride + idx) =
-          make_uint2(h[k][0] | ((uint32_t)h[k][1] << 16), h[k][2] | ((uint32_t)h[k][3] << 16));
+  for (int k = 0; k < NP; ++k) {
+    uint32_t h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat16 q = __float2bfloat16_rn(r[i]);
+      h[i] = __bfloat16_as_ushort(q);
+      r[i] -= __bfloat162float(q);  // exact in fp32
+    }
+    *reinterpret_cast<uint2*>(dst) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+    dst += o.pstride;
+  }
 }
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -76,7 +82,7 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 // features, so loads are float4 and the bf16-pair stores are 8 bytes wide. Direction
 // block b of the point gets its own slot group [h0; its directions; its partial top], with
 // zero rows for the padding of the last block.
-template <int KORD>
+template <int KORD, int NP>
 // (min blocks per SM: the register budget of the single-block kernel, which this store-bound
 // kernel needs for its occupancy: 40 registers for K=2 / standard, 48 for K=4 / nested)
 __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6 : 5)
@@ -111,15 +117,15 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
     const size_t row0 = ((size_t)n * p.blocks + b) * p.P;                \
     const int r0 = b * p.rb;                                             \
     const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;                  \
-    seed_store4(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
 #define CTM_BLOCK_END }
   if (KORD == kStd2) {
     CTM_BLOCK_BEGIN
     // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
     auto pair = [&](const float4 u, int r) {
       const size_t rr = row0 + 1 + 2 * (r - r0);
-      seed_store4(o, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
-      seed_store4(o, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
+      seed_store4<NP>(o, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+      seed_store4<NP>(o, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
                   d2[2] * u.z * u.z, d2[3] * u.w * u.w);
     };
     int r = r0;
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       const size_t r = row0 + 1 + 4 * (j - r0);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        seed_store4(o, (r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3]);
+        seed_store4<NP>(o, (r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3]);
     }
     CTM_BLOCK_END
   } else if (KORD == 2) {
@@ -180,18 +186,18 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       for (int i = 0; i < CTM_SEED_BATCH; ++i) u[i] = ldg4(p.UT + (size_t)(r + i) * p.ld + m);
 #pragma unroll
       for (int i = 0; i < CTM_SEED_BATCH; ++i)
-        seed_store4(o, (row0 + 1 + r - r0 + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
+        seed_store4<NP>(o, (row0 + 1 + r - r0 + i) * p.ld + m, d1[0] * u[i].x, d1[1] * u[i].y,
                     d1[2] * u[i].z, d1[3] * u[i].w);
     }
     for (; r < r1; ++r) {
       const float4 u = ldg4(p.UT + (size_t)r * p.ld + m);
-      seed_store4(o, (row0 + 1 + r - r0) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
+      seed_store4<NP>(o, (row0 + 1 + r - r0) * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z,
                   d1[3] * u.w);
     }
-    for (; r < r0 + p.rb; ++r) seed_store4(o, (row0 + 1 + r - r0) * p.ld + m, 0.f, 0.f, 0.f, 0.f);
+    for (; r < r0 + p.rb; ++r) seed_store4<NP>(o, (row0 + 1 + r - r0) * p.ld + m, 0.f, 0.f, 0.f, 0.f);
     // sum h2 = tanh' * 0 + tanh'' * sum_r z1_r^2   (the input top coefficient is 0)
     const float4 cs = ldg4(p.csum + (size_t)b * p.ld + m);
-    seed_store4(o, (row0 + 1 + p.rb) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
+    seed_store4<NP>(o, (row0 + 1 + p.rb) * p.ld + m, d2[0] * cs.x, d2[1] * cs.y, d2[2] * cs.z,
                 d2[3] * cs.w);
     CTM_BLOCK_END
   } else if (KORD == kNest) {
@@ -199,27 +205,27 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
     // the input, so h_a = s' g_a, H'_ab = s'' g_a g_b, L'_a = s''' g_a |g|^2,
     // Q' = s'''' |g|^4 (the epilogue rule of jet_layer.cuh with H = L = Q = 0); |g|^2 = csum.
     const size_t row0 = (size_t)n * p.P;
-    seed_store4(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
     const float4 cs = ldg4(p.csum + m);
     size_t r = row0 + 1;
     for (int a = 0; a < p.R; ++a, ++r) {
       const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
-      seed_store4(o, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+      seed_store4<NP>(o, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
     }
     for (int a = 0; a < p.R; ++a) {
       const float4 ua = ldg4(p.UT + (size_t)a * p.ld + m);
       for (int c = a; c < p.R; ++c, ++r) {
         const float4 uc = ldg4(p.UT + (size_t)c * p.ld + m);
-        seed_store4(o, r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y,
+        seed_store4<NP>(o, r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y,
                     d2[2] * ua.z * uc.z, d2[3] * ua.w * uc.w);
       }
     }
     for (int a = 0; a < p.R; ++a, ++r) {
       const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
-      seed_store4(o, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
+      seed_store4<NP>(o, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
                   d3[3] * u.w * cs.w);
     }
-    seed_store4(o, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
+    seed_store4<NP>(o, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
                 d4[3] * cs.w * cs.w);
   } else {
     CTM_BLOCK_BEGIN
@@ -233,9 +239,9 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
         h3[i] = d3[i] * z[i] * z[i] * z[i];         // h3 (z2 = z3 = 0)
       }
       const size_t r = row0 + 1 + 3 * (j - r0);
-      seed_store4(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
-      seed_store4(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
-      seed_store4(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+      seed_store4<NP>(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+      seed_store4<NP>(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+      seed_store4<NP>(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
     };
     int j = r0;
 #ifndef CTM_SEED_BATCH4
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
       jet((j < r1) ? ldg4(p.UT + (size_t)j * p.ld + m) : make_float4(0.f, 0.f, 0.f, 0.f), j);
     // sum_w h4 = tanh'''' * sum_j w_j z1_j^4 over the block's jets   (z2 = z3 = z4 = 0)
     const float4 cs = ldg4(p.csum + (size_t)b * p.ld + m);
-    seed_store4(o, (row0 + 1 + 3 * p.rb) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
+    seed_store4<NP>(o, (row0 + 1 + 3 * p.rb) * p.ld + m, d4[0] * cs.x, d4[1] * cs.y, d4[2] * cs.z,
                 d4[3] * cs.w);
     CTM_BLOCK_END
   }
@@ -290,6 +296,7 @@ struct SeedStochParams {
 
 __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx);
 
+template <int NP>
 __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(const SeedStochParams p) {
   extern __shared__ float vsh[];  // [S, D]
   const PlaneOut o{p.out, p.pstride, p.nplanes};
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   }
   for (int b = 0; b < p.blocks; ++b) {
     const size_t row0 = ((size_t)n * p.blocks + b) * P;
-    seed_store4(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int s = b * p.rb; s < (b + 1) * p.rb; ++s) {
       float z[4] = {0.f, 0.f, 0.f, 0.f};
@@ -351,18 +358,18 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
         acc[i] = fmaf((p.w && s < p.S) ? p.w[s] * z2 : z2, z2, acc[i]);
       }
       const size_t r = row0 + 1 + st * (size_t)(s - b * p.rb);
-      seed_store4(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
-      seed_store4(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
-      seed_store4(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+      seed_store4<NP>(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
+      seed_store4<NP>(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
+      seed_store4<NP>(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
       if (p.standard) {  // h4 of this sample = s'''' z1^4   (x2 = x3 = x4 = 0)
         float h4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) h4[i] = d4[i] * (z[i] * z[i]) * (z[i] * z[i]);
-        seed_store4(o, (r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3]);
+        seed_store4<NP>(o, (r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3]);
       }
     }
     if (!p.standard)
-      seed_store4(o, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
+      seed_store4<NP>(o, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
                   d4[3] * acc[3]);
   }
 }
@@ -403,6 +410,7 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx) {
   return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
 }
 
+template <int NP>
 __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
   __shared__ float vs[kSeedChunk];
   const PlaneOut o{p.out, p.pstride, p.nplanes};
@@ -420,14 +428,14 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = (4 * c4 + i < p.D) ? p.X[n * p.D + 4 * c4 + i] : 0.f;
     for (int b = 0; b < p.blocks; ++b) {
-      seed_store4(o, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
-      if (!p.standard) seed_store4(o, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+      seed_store4<NP>(o, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
+      if (!p.standard) seed_store4<NP>(o, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
     }
     if (p.standard)
       for (int s = 0; s < p.blocks * p.rb; ++s)
-        seed_store4(o, (dir_row(s) + 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+        seed_store4<NP>(o, (dir_row(s) + 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
     for (int s = p.S; s < p.blocks * p.rb; ++s)
-      seed_store4(o, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+      seed_store4<NP>(o, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
   }
   const int per_chunk = kSeedChunk / p.Rv;
   for (int s0 = 0; s0 < p.S; s0 += per_chunk) {
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
         }
         u[i] = val;
       }
-      seed_store4(o, dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
+      seed_store4<NP>(o, dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
     }
   }
 }

@@ -1,5 +1,5 @@
 """Experiment harness (CTM_EXP_STATS build): per-role cycle counters of the layer kernel.
-usage: python scripts/exp_stats.py <op> [S]   (run from a tree built with -DCTM_EXP_STATS)"""
+usage: python scripts/exp_stats.py <op> [S] [precision]   (run from a tree built with -DCTM_EXP_STATS)"""
 import ctypes
 import sys
 
@@ -15,6 +15,8 @@ S = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 D = 5 if "biharmonic" in op else 50
 params = mlp_params(widths_for(D), 0)
 mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0)
+if len(sys.argv) > 3 and hasattr(mlp, "set_precision"):
+    mlp.set_precision(sys.argv[3])
 X = torch.from_numpy(points(16384, D)).cuda()
 fn = getattr(mlp, op)
 kw = {"S": S, "seed": 2} if op in ("randomized_laplacian", "stochastic_biharmonic") else {}
