@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libctm.so")
 SOURCES = ["ctm.cu"]
-HEADERS = ["ptx.cuh", "jet_layer.cuh", "seed.cuh", "backward.cuh"]
+HEADERS = ["ptx.cuh", "jet_layer.cuh", "seed.cuh", "backward.cuh", "wgrad.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -19,8 +19,7 @@ FLAGS = [
     "-Xptxas", "-v",
     f"-I{os.path.join(ROOT, 'include')}",
 ]
-# cuBLAS: the weight-gradient GEMMs of the differentiable path (plain long-K GEMMs);
-LIBS = ["-lcublas"]
+LIBS: list[str] = []
 
 
 def stale() -> bool:

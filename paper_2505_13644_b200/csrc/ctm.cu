@@ -6,7 +6,6 @@
 //   layer   l = 2..L-1: fused tcgen05 bf16-plane GEMM + tanh Taylor epilogue         -> block B_l
 //           (the last hidden layer reduces straight against the output weights)
 //   final   op = c * (w_L . sum h_K), f = w_L . h0 + b_L
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -22,6 +21,7 @@
 #include "backward.cuh"
 #include "jet_layer.cuh"
 #include "seed.cuh"
+#include "wgrad.cuh"
 
 namespace {
 
@@ -150,7 +150,7 @@ struct ctm_mlp {
   std::vector<uint16_t*> WTp;               // W_l^T bf16 planes [3][wpad[l-1], wpad[l]], l = 2..L-1
   std::vector<CUtensorMap> mapAT;
   float* eye = nullptr;                     // [256, 256] identity: fixed direction sets as shared V
-  cublasHandle_t cublas = nullptr;
+  bool wgrad_attr[2] = {false, false};    // dynamic smem attribute set (wgrad_kernel<128>, <256>)
   struct Tape {
     bool valid = false;
     int64_t N = 0;
@@ -166,8 +166,8 @@ struct ctm_mlp {
     Planes Zb[2];
     float* part = nullptr;
     size_t part_elems = 0;
-    float* dWpad = nullptr;
-    size_t dWpad_elems = 0;
+    float* wpart = nullptr;                 // weight-gradient split partials
+    size_t wpart_elems = 0;
   } tape;
   // profiling (events around launches)
   bool profiling = false;
@@ -197,12 +197,10 @@ ctm_status free_all(ctm_mlp* h) {
   F(h->partial);
   for (auto& p : h->WTp) F(p);
   F(h->eye);
-  F(h->tape.weights); F(h->tape.part); F(h->tape.dWpad);
+  F(h->tape.weights); F(h->tape.part); F(h->tape.wpart);
   for (auto& p : h->tape.B) F(p.p);
   for (auto& p : h->tape.Z) F(p);
   for (int i = 0; i < 2; ++i) F(h->tape.Zb[i].p);
-  if (h->cublas) cublasDestroy(h->cublas);
-  h->cublas = nullptr;
   for (auto& r : h->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -891,28 +889,68 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   return CTM_OK;
 }
 
-// dW_pad[Mout, Kin] = Zb^T B over `rows` slot rows, 3xBF16: hi*hi + lo*hi + hi*lo with fp32
-// accumulation (a plain long-K GEMM: cuBLAS). B [rows, Kin], Zb [rows, Mout], both bf16
-// pairs, row-major (= column-major [K, rows], [M, rows]); the result is column-major
-// [Kin, Mout] = row-major [Mout, Kin].
-ctm_status weight_grad_gemm(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, int Mout, int64_t rows, float* C,
-                            cudaStream_t st) {
-  ProfScope ps(h, CTM_KIND_WGRAD, 2.0 * (double)rows * Kin * Mout, st);
-  if (cublasSetStream(h->cublas, st) != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasSetStream");
-  const float one = 1.f, zero = 0.f;
-  // plane products (B plane, Z plane): fast mode 3, fp32 mode 6 (corrections first)
-  static const int prods3[3][2] = {{1, 0}, {0, 1}, {0, 0}};
-  static const int prods6[6][2] = {{2, 0}, {1, 1}, {0, 2}, {1, 0}, {0, 1}, {0, 0}};
-  const int np = h->tape.nplanes == 3 ? 6 : 3;
-  for (int i = 0; i < np; ++i) {
-    const int* pr = np == 6 ? prods6[i] : prods3[i];
-    const uint16_t* Ab = B.p + pr[0] * B.cap;
-    const uint16_t* Bz = Z.p + pr[1] * Z.cap;
-    cublasStatus_t cs = cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, Kin, Mout, (int)rows, &one, Ab,
-                                     CUDA_R_16BF, Kin, Bz, CUDA_R_16BF, Mout, i == 0 ? &zero : &one, C, CUDA_R_32F,
-                                     Kin, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-    if (cs != CUBLAS_STATUS_SUCCESS) return fail(CTM_ECUDA, "cublasGemmEx failed (" + std::to_string((int)cs) + ")");
+// dW[o, i] (o < rows_out, i < cols_in, caller's layout; = or +=) = sum over the slot rows
+// of Z[row, o] B[row, i] (Z [rows, Mout], B [rows, Kin], both bf16 planes): wgrad_kernel
+// (tcgen05, MN-major operands, fixed K splits, chunked TMEM accumulation) and
+// wgrad_reduce_kernel (the splits summed in order, cropped into dW). Deterministic.
+ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, int Mout, int64_t rows, int rows_out,
+                       int cols_in, float* dW, int acc, cudaStream_t st) {
+  auto& T = h->tape;
+  const int N = (Kin % 256 == 0) ? 256 : 128;
+  ctm::WgradParams wp{};
+  wp.rows = rows;
+  wp.k_blocks = (int)((rows + 63) / 64);
+  wp.m_pairs = Mout / 256;
+  wp.n_tiles = (Kin + N - 1) / N;
+  const int tiles = wp.m_pairs * wp.n_tiles;
+  const int npairs = h->sm_count / 2;
+  wp.splits = std::max(1, std::min(npairs / tiles, wp.k_blocks));
+  wp.kb_per_split = (wp.k_blocks + wp.splits - 1) / wp.splits;
+  wp.nplanes = T.nplanes;
+  const int units = tiles * wp.splits;
+  ctm_status s = ensure(T.wpart, T.wpart_elems, (size_t)units * 256 * N);
+  if (s != CTM_OK) return s;
+  wp.part = T.wpart;
+  CUtensorMap mz, mb;
+  if (!make_map3(&mz, Z.p, (uint64_t)Mout, (uint64_t)rows, Z.cap, 64) ||
+      !make_map3(&mb, B.p, (uint64_t)Kin, (uint64_t)rows, B.cap, 64))
+    return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the weight-gradient operands");
+  const int grid = 2 * std::min(units, npairs);
+  {
+    ProfScope ps(h, CTM_KIND_WGRAD, 2.0 * (double)T.N * T.P * rows_out * cols_in, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(320);
+    cfg.dynamicSmemBytes = ctm::kWgradSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (N == 256) {
+      if (!h->wgrad_attr[1]) {
+        CTM_CUDA(cudaFuncSetAttribute(ctm::wgrad_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      ctm::kWgradSmem));
+        h->wgrad_attr[1] = true;
+      }
+      CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::wgrad_kernel<256>, mz, mb, wp));
+    } else {
+      if (!h->wgrad_attr[0]) {
+        CTM_CUDA(cudaFuncSetAttribute(ctm::wgrad_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      ctm::kWgradSmem));
+        h->wgrad_attr[0] = true;
+      }
+      CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::wgrad_kernel<128>, mz, mb, wp));
+    }
   }
+  {
+    const int64_t n = (int64_t)rows_out * cols_in;
+    ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
+    ctm::wgrad_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.wpart, N, wp.n_tiles, wp.splits, rows_out,
+                                                                        cols_in, dW, acc);
+  }
+  h->last_launches += 2;
   return CTM_OK;
 }
 
@@ -941,10 +979,6 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     s = ensure_planes(T.Zb[i], (size_t)rows * ldmax);
     if (s != CTM_OK) return s;
   }
-  size_t dwmax = (size_t)h->wpad[1] * h->k1pad;
-  for (int l = 2; l <= L - 1; ++l) dwmax = std::max(dwmax, (size_t)h->wpad[l] * h->wpad[l - 1]);
-  s = ensure(T.dWpad, T.dWpad_elems, dwmax);
-  if (s != CTM_OK) return s;
   const float* jw = T.weighted ? T.weights : nullptr;
   h->last_launches = 0;
   // ---- readout and the last hidden rule, transposed
@@ -985,15 +1019,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   int cur = 0;
   for (int l = L - 1; l >= 2; --l) {
     const int Mout = h->wpad[l], Kin = h->wpad[l - 1];
-    s = weight_grad_gemm(h, T.B[l - 1], Kin, T.Zb[cur], Mout, rows, T.dWpad, st);
+    s = weight_grad(h, T.B[l - 1], Kin, T.Zb[cur], Mout, rows, h->widths[l], h->widths[l - 1], dW[l - 1], acc, st);
     if (s != CTM_OK) return s;
-    {
-      const int64_t n = (int64_t)h->widths[l] * h->widths[l - 1];
-      ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
-      ++h->last_launches;
-      ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, Kin, h->widths[l], h->widths[l - 1],
-                                                                    dW[l - 1], acc);
-    }
     s = bias_grad(h, T.Zb[cur], Mout, h->widths[l], db[l - 1], acc, st);
     if (s != CTM_OK) return s;
     // Z_bar_{l-1} = rule^T( (Z_bar_l W_l)^T ) on the tensor cores (jet_layer_kernel<kBwd2>)
@@ -1031,15 +1058,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     cur ^= 1;
   }
   // ---- layer 1: dW_1 = Z_bar_1^T B_0 (B_0 = [x0; u_r; 0]), db_1
-  s = weight_grad_gemm(h, T.B[0], h->k1pad, T.Zb[cur], h->wpad[1], rows, T.dWpad, st);
+  s = weight_grad(h, T.B[0], h->k1pad, T.Zb[cur], h->wpad[1], rows, h->widths[1], h->widths[0], dW[0], acc, st);
   if (s != CTM_OK) return s;
-  {
-    const int64_t n = (int64_t)h->widths[1] * h->widths[0];
-    ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
-    ++h->last_launches;
-    ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.dWpad, h->k1pad, h->widths[1], h->widths[0], dW[0],
-                                                                  acc);
-  }
   s = bias_grad(h, T.Zb[cur], h->wpad[1], h->widths[1], db[0], acc, st);
   if (s != CTM_OK) return s;
   CTM_CUDA(cudaGetLastError());
@@ -1401,7 +1421,7 @@ ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable) {
   DeviceGuard g(mlp->device);
   mlp->tape.valid = false;
   mlp->grad = enable != 0;
-  if (!mlp->grad || mlp->cublas) return CTM_OK;
+  if (!mlp->grad || !mlp->WTp.empty()) return CTM_OK;
   // W_l^T as bf16 planes (the A operand of the adjoint GEMMs), from the split weights
   for (int l = 2; l <= mlp->L - 1; ++l) {
     const int mpad = mlp->wpad[l], kpad = mlp->wpad[l - 1];
@@ -1420,10 +1440,6 @@ ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable) {
     for (int i = 0; i < 256; ++i) eye[i * 257] = 1.f;
     CTM_CUDA(cudaMalloc(&mlp->eye, sizeof(float) * eye.size()));
     CTM_CUDA(cudaMemcpy(mlp->eye, eye.data(), sizeof(float) * eye.size(), cudaMemcpyHostToDevice));
-  }
-  if (cublasCreate(&mlp->cublas) != CUBLAS_STATUS_SUCCESS) {
-    mlp->cublas = nullptr;
-    return fail(CTM_ECUDA, "cublasCreate failed");
   }
   CTM_CUDA(cudaDeviceSynchronize());
   return CTM_OK;
