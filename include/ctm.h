@@ -281,6 +281,17 @@ ctm_status ctm_last_blocks(ctm_mlp_t mlp, int32_t *blocks, int32_t *per_block);
 ctm_status ctm_plan_blocks(int32_t order, int32_t R, int32_t forced_rb, int32_t *blocks, int32_t *per_block,
                            int32_t *slots_per_block, int32_t *points_per_tile, int32_t *mma_n);
 
+/* The layer contraction alone (a diagnostic for the GEMM-only accuracy test; SURVEY §8(c)
+ * "Parity unpinned": the plane split and the tensor-core accumulation are covered by the
+ * end-to-end parity plus this). Z = B W_l^T for hidden layer `layer` (2 <= layer <= L-1,
+ * 1-based as W_l in ctm_load_mlp: W_l [w_l, w_{l-1}]), no bias, through the operator
+ * path's own kernel (jet_layer_kernel, the handle's precision mode) with the Taylor rule
+ * bypassed: the epilogue stores the raw fp32 accumulator of every slot row.
+ *   B [rows, w_{l-1}] device fp32 (split into bf16 planes on the device), Z [rows, w_l]
+ *   device fp32. Asynchronous on `stream`. Errors: CTM_EINVAL (NULL pointers, rows < 0,
+ *   layer out of range), CTM_ESHAPE (misaligned). */
+ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float *B, int64_t rows, float *Z, void *stream);
+
 /* Per-kernel timing (measurement support for bench.py; off by default).
  * When enabled, every launch of an operator call is bracketed by CUDA events
  * recorded on the call's stream. ctm_profile_read synchronises those events

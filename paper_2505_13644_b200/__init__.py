@@ -56,6 +56,7 @@ ABI = {
     "ctm_last_blocks": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "ctm_set_direction_block": (ctypes.c_int, [_VP, _I32]),
     "ctm_plan_blocks": (ctypes.c_int, [_I32, _I32, _I32] + [ctypes.POINTER(_I32)] * 5),
+    "ctm_gemm_probe": (ctypes.c_int, [_VP, _I32, _VP, _I64, _VP, _VP]),
     "ctm_profile_enable": (ctypes.c_int, [_VP, _I32]),
     "ctm_profile_read": (ctypes.c_int, [_VP, _VP, _VP, _VP]),
 }
@@ -374,6 +375,19 @@ class MLP:
         _check(lib().ctm_backward(self._h, gop.data_ptr(), self._p(gf), dW, db, int(bool(accumulate)),
                                   _stream_ptr(stream, self.device)), "ctm_backward")
         return grads
+
+    @_streamed
+    def gemm_probe(self, layer: int, B, Z=None, stream=None):
+        """Z = B W_layer^T (no bias) through the layer kernel with the Taylor rule bypassed
+        (ctm_gemm_probe; the GEMM-only accuracy test). layer is 1-based (2 .. L-1)."""
+        B = _dev_f32(B, self.device, "B")
+        if B.dim() != 2 or B.shape[1] != self.widths[layer - 1]:
+            raise CTMError(f"B must be [rows, {self.widths[layer - 1]}]")
+        if Z is None:
+            Z = torch.empty(B.shape[0], self.widths[layer], device=self.device, dtype=torch.float32)
+        _check(lib().ctm_gemm_probe(self._h, int(layer), B.data_ptr(), B.shape[0], Z.data_ptr(),
+                                    _stream_ptr(stream, self.device)), "ctm_gemm_probe")
+        return Z
 
     def last_plan(self) -> dict:
         a, b, c, d = _I32(), _I32(), _I32(), _I32()

@@ -140,6 +140,10 @@ struct ctm_mlp {
   int forced_rb = 0;          // ctm_set_direction_block: directions per block (0 = planner)
   // workspace (bf16 planes): see ensure_workspace
   Planes blk[4];
+  // ctm_gemm_probe scratch
+  Planes probe_in, probe_out;
+  float* probe_z = nullptr;
+  size_t probe_z_elems = 0;
   float* partial = nullptr;
   size_t partial_elems = 0;
   // last plan
@@ -194,6 +198,7 @@ ctm_status free_all(ctm_mlp* h) {
   F(h->U_lap); F(h->c_lap); F(h->w_ones); F(h->U_bih); F(h->c_bih); F(h->w_bih);
   F(h->U_call); F(h->c_call); F(h->c_blk);
   for (int i = 0; i < 4; ++i) F(h->blk[i].p);
+  F(h->probe_in.p); F(h->probe_out.p); F(h->probe_z);
   F(h->partial);
   for (auto& p : h->WTp) F(p);
   F(h->eye);
@@ -1466,6 +1471,68 @@ ctm_status ctm_backward(ctm_mlp_t mlp, const float* gop, const float* gf, float*
     return CTM_OK;
   }
   return backward(mlp, gop, gf, dW, db, accumulate != 0, (cudaStream_t)stream);
+}
+
+ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float* B, int64_t rows, float* Z, void* stream) {
+  g_last_error.clear();
+  if (!mlp) return fail(CTM_EINVAL, "NULL handle");
+  if (layer < 2 || layer > mlp->L - 1) return fail(CTM_EINVAL, "layer must be a hidden GEMM layer (2 .. L-1)");
+  if (rows < 0 || (rows > 0 && (!B || !Z))) return fail(CTM_EINVAL, "need B, Z and rows >= 0");
+  if ((B && !aligned16(B)) || (Z && !aligned16(Z))) return fail(CTM_ESHAPE, "B/Z must be 16-byte aligned");
+  if (rows == 0) return CTM_OK;
+  ctm_mlp* h = mlp;
+  DeviceGuard g(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int w_in = h->widths[layer - 1], w_out = h->widths[layer];
+  const int kpad = h->wpad[layer - 1], mpad = h->wpad[layer];
+  constexpr int P = 16;  // slot rows per "point": 16 points fill an N = 256 tile
+  const int64_t rows_pad = (rows + P - 1) / P * P;
+  if (rows_pad > (int64_t)INT32_MAX) return fail(CTM_EUNSUPPORTED, "too many rows");
+  ctm_status s = ensure_planes(h->probe_in, (size_t)rows_pad * kpad);
+  if (s != CTM_OK) return s;
+  s = ensure_planes(h->probe_out, (size_t)rows_pad * mpad);
+  if (s != CTM_OK) return s;
+  s = ensure(h->probe_z, h->probe_z_elems, (size_t)rows_pad * mpad);
+  if (s != CTM_OK) return s;
+  {
+    const int64_t n = rows_pad * kpad;
+    if (h->nplanes == 3)
+      ctm::split_rows_kernel<3><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, rows, w_in, rows_pad, kpad,
+                                                                            h->probe_in.p, (int64_t)h->probe_in.cap);
+    else
+      ctm::split_rows_kernel<2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, rows, w_in, rows_pad, kpad,
+                                                                            h->probe_in.p, (int64_t)h->probe_in.cap);
+  }
+  CUtensorMap mb;
+  if (!make_map3(&mb, h->probe_in.p, (uint64_t)kpad, (uint64_t)rows_pad, h->probe_in.cap, 128))
+    return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for the probe block");
+  ctm::LayerParams lp{};
+  lp.bias = nullptr;
+  lp.act = h->act;
+  lp.out = h->probe_out.p;
+  lp.pstride = (int64_t)h->probe_out.cap;
+  lp.nplanes = (int16_t)h->nplanes;
+  lp.ldo = mpad;
+  lp.z_out = h->probe_z;
+  lp.ldz = mpad;
+  lp.m_tiles = mpad / ctm::kBM;
+  lp.n_points = rows_pad / P;
+  lp.P = P;
+  lp.pts_per_tile = 256 / P;
+  lp.n_mma = 256;
+  lp.k_iters = kpad / ctm::kBK;
+  lp.blocks = 1;
+  lp.rb = P - 2;
+  const int64_t n_tiles = (lp.n_points + lp.pts_per_tile - 1) / lp.pts_per_tile;
+  const int64_t grid = 2 * std::min<int64_t>(n_tiles * (lp.m_tiles / 2), h->sm_count / 2);
+  s = launch_layer_kernel<2, ctm::kFlagSaveZ>(h, grid, h->mapA[layer - 2], mb, lp, st);
+  if (s != CTM_OK) return s;
+  {
+    const int64_t n = rows * (int64_t)w_out;
+    ctm::crop_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->probe_z, mpad, (int)rows, w_out, Z, 0);
+  }
+  CTM_CUDA(cudaGetLastError());
+  return CTM_OK;
 }
 
 ctm_status ctm_profile_enable(ctm_mlp_t mlp, int32_t enable) {

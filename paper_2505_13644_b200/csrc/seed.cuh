@@ -623,6 +623,23 @@ __global__ void transpose_w1_kernel(const float* __restrict__ W1, const float* _
   if (d == 0) b1p[m] = (m < w1) ? b1[m] : 0.f;
 }
 
+// out planes [rows_pad, ldp] <- src [rows, cols] (fp32), zero padded (ctm_gemm_probe)
+template <int NP>
+__global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, int cols, int64_t rows_pad, int ldp,
+                                  uint16_t* __restrict__ out, int64_t pstride) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows_pad * ldp) return;
+  const int64_t r = k / ldp;
+  const int c = (int)(k % ldp);
+  float v = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    out[q * pstride + k] = __bfloat16_as_ushort(b);
+    v -= __bfloat162float(b);
+  }
+}
+
 __global__ void pad_vector_kernel(const float* __restrict__ src, int n, int npad, float* __restrict__ dst) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < npad) dst[i] = (i < n) ? src[i] : 0.f;

@@ -19,38 +19,7 @@ import oracle as O  # noqa: E402
 from synth import gaussian_directions, mlp_params, points, sigma as make_sigma, sigma_field, signed_weights  # noqa: E402
 
 
-def derivs32(act, z):
-    if act == "tanh":
-        t = np.tanh(z)
-        s = np.float32(1) - t * t
-        return t, s, -2 * t * s, s * (6 * t * t - 2), 8 * t * s * (2 - 3 * t * t)
-    sn, cs = np.sin(z), np.cos(z)
-    return sn, cs, -sn, -cs, sn
-
-
-def vanilla32(params, act, X, dirs, coef, K):
-    """sum_j coef_j <d^K f(x), u_j^K> in float32, one jet per direction (vanilla Taylor mode)."""
-    X = X.astype(np.float32)
-    dirs = np.asarray(dirs, np.float32)
-    if dirs.ndim == 2:
-        dirs = np.broadcast_to(dirs, (X.shape[0],) + dirs.shape)
-    coef = np.broadcast_to(np.asarray(coef, np.float32), dirs.shape[1:2])
-    out = np.empty(X.shape[0])
-    for n in range(X.shape[0]):
-        h0 = X[n]
-        x = [dirs[n].copy()] + [np.zeros_like(dirs[n]) for _ in range(K - 1)]
-        for W, b in params[:-1]:
-            z0 = W @ h0 + b
-            z = [xi @ W.T for xi in x]
-            h0, s1, s2, s3, s4 = derivs32(act, z0)
-            if K == 2:
-                x = [s1 * z[0], s2 * z[0] * z[0] + s1 * z[1]]
-            else:
-                z1, z2, z3, z4 = z
-                x = [s1 * z1, s2 * z1 * z1 + s1 * z2, s3 * z1 * z1 * z1 + 3 * s2 * z1 * z2 + s1 * z3,
-                     s4 * z1**4 + 6 * s3 * z1 * z1 * z2 + 4 * s2 * z1 * z3 + 3 * s2 * z2 * z2 + s1 * z4]
-        out[n] = float(np.float32(coef @ (x[-1] @ params[-1][0][0])))
-    return out
+from tests._util import vanilla32  # noqa: E402  (plain fp32 vanilla Taylor rules)
 
 
 def report(tag, got32, want, norm):

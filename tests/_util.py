@@ -110,3 +110,51 @@ def magnitude_k2(Ws, bs, X, dirs, coef, act="tanh"):
             h0, A1, A2 = t, d1 * Z1, d2 * Z1 ** 2 + d1 * Z2
         out[n] = float(c @ (A2 @ np.abs(Ws[-1][0])))
     return out
+
+
+def _derivs32(act, z):
+    if act == "tanh":
+        t = np.tanh(z)
+        s = np.float32(1) - t * t
+        return t, s, -2 * t * s, s * (6 * t * t - 2), 8 * t * s * (2 - 3 * t * t)
+    if act == "sin":
+        sn, cs = np.sin(z), np.cos(z)
+        return sn, cs, -sn, -cs, sn
+    raise ValueError(act)
+
+
+def vanilla32(params, act, X, dirs, coef, K):
+    """sum_j coef_j <d^K f(x), u_j^K> by PLAIN fp32 arithmetic: the vanilla Taylor rules (Eq. 3
+    with K = 2 or 4, one jet per direction, the rows of P:1370-1424) in numpy float32 end to
+    end (BLAS sgemm for the linear layers). The reference for "what plain fp32 gets" at a
+    point (reading R9). params: the fp32 (W, b) list; X [n, D]; dirs [J, D] or
+    [n, J, D]; coef scalar or [J]. Test infrastructure only."""
+    X = np.asarray(X, np.float32)
+    dirs = np.asarray(dirs, np.float32)
+    if dirs.ndim == 2:
+        dirs = np.broadcast_to(dirs, (X.shape[0],) + dirs.shape)
+    coef = np.broadcast_to(np.asarray(coef, np.float32), dirs.shape[1:2])
+    out = np.empty(X.shape[0])
+    for n in range(X.shape[0]):
+        h0 = X[n]
+        x = [dirs[n].copy()] + [np.zeros_like(dirs[n]) for _ in range(K - 1)]
+        for W, b in params[:-1]:
+            z0 = W @ h0 + b
+            z = [xi @ W.T for xi in x]
+            h0, s1, s2, s3, s4 = _derivs32(act, z0)
+            if K == 2:
+                x = [s1 * z[0], s2 * z[0] * z[0] + s1 * z[1]]
+            else:
+                z1, z2, z3, z4 = z
+                x = [s1 * z1, s2 * z1 * z1 + s1 * z2, s3 * z1 * z1 * z1 + 3 * s2 * z1 * z2 + s1 * z3,
+                     s4 * z1**4 + 6 * s3 * z1 * z1 * z2 + 4 * s2 * z1 * z3 + 3 * s2 * z2 * z2 + s1 * z4]
+        out[n] = float(np.float32(coef @ (x[-1] @ params[-1][0][0])))
+    return out
+
+
+def ref32(params, X, dirs, coef, K, act="tanh"):
+    """A closure idx -> plain-fp32 values at points idx (vanilla32), for check()'s R9 rule."""
+    def f(idx):
+        d = np.asarray(dirs)
+        return vanilla32(params, act, np.asarray(X)[idx], d[idx] if d.ndim == 3 else d, coef, K)
+    return f

@@ -211,7 +211,7 @@ def test_full_size_gradient_is_the_sum_of_its_shards(ctm):
             assert (a - b).abs().max().item() / scale < GTOL
 
 
-@pytest.mark.parametrize("case", range(int(os.environ.get("CTM_FUZZ_GRAD", "8"))))
+@pytest.mark.parametrize("case", range(int(os.environ.get("CTM_FUZZ_GRAD", "16"))))
 def test_fuzz_shapes_gradients(ctm, case):
     """Random nets, batch sizes and direction sets through the differentiable path: the
     exact, weighted and randomized Laplacians and a signed directional sum, each forward in

@@ -124,3 +124,23 @@ def test_magnitude_k4_catches_a_dropped_term():
     for term in (s4 * z1**4, 6 * s3 * z1**2 * z2, 4 * s2 * z1 * z3, 3 * s2 * z2**2, s1 * z4):
         bad = Ws[2][0] @ (good - term)
         assert abs(bad - want) > 1e-4 * M  # 10x the fallback tolerance 1e-5 M
+
+
+@pytest.mark.parametrize("K,act", [(2, "tanh"), (4, "tanh"), (2, "sin"), (4, "sin")])
+def test_vanilla32_is_the_vanilla_rules_in_fp32(K, act):
+    """The plain-fp32 reference of reading R9 (tests/_util.vanilla32) computes the operator:
+    on a well-conditioned small net it matches the fp64 oracle to fp32 accuracy, and it is
+    genuinely fp32 (not bitwise the fp64 value)."""
+    from synth import mlp_params, points
+    from tests._util import vanilla32
+
+    params = mlp_params([3, 24, 16, 1], 5)
+    net = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params], act)
+    X = points(6, 3, seed=5)
+    dirs = np.random.default_rng(5).standard_normal((4, 3)).astype(np.float32)
+    w = np.array([0.5, -1.0, 2.0, 0.25], np.float32)
+    want, _, norm = O.directional_sum(net, X.astype(np.float64), K, dirs.astype(np.float64), w.astype(np.float64))
+    got = vanilla32(params, act, X, dirs, w, K)
+    err = np.abs(got - want) / norm
+    assert err.max() <= 1e-4
+    assert np.any(got != want)
