@@ -297,8 +297,10 @@ ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float *B, int64_t 
  * recorded on the call's stream. ctm_profile_read synchronises those events
  * and returns, per kernel kind, the summed device time (ms), the number of
  * launches, and the algorithmic work those launches did (FLOP for
- * CTM_KIND_LAYER = 2 * N * P * w_in * w_out useful products; bytes written
- * for CTM_KIND_SEED = N * P * w_1 * 4, a bf16 pair), then clears the accumulators.
+ * CTM_KIND_LAYER = 2 * N * P * w_in * w_out useful products, P the point's slots with all
+ * its directions in one block; bytes written for CTM_KIND_SEED = the layer-1 block's slot
+ * rows x padded width x 2 bytes x planes; FLOP for CTM_KIND_WGRAD = 2 * N * P * w_l * w_{l-1}),
+ * then clears the accumulators.
  * arrays: ms[CTM_KIND_COUNT], launches[CTM_KIND_COUNT], work[CTM_KIND_COUNT]. */
 typedef enum {
     CTM_KIND_PREP = 0,    /* per-call direction matrices (W1 sigma)            */

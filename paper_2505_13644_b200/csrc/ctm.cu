@@ -359,6 +359,7 @@ ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap
 struct Plan {
   int P = 0, ppt = 0, nmma = 0;
   int nb = 1, rb = 0;
+  int useful_P = 0;  // slots of the point with all its directions in one block (roofline work)
 };
 
 void tile_plan(Plan& pl) {
@@ -386,7 +387,13 @@ double plan_cost(const Plan& pl) {
 // R directions (jets): forced_rb > 0 fixes the block size; otherwise the cheapest split by
 // plan_cost, keeping one block unless a split is modelled > 3% cheaper. P_fixed > 0 (nested
 // biharmonic): no blocks. Returns P = 0 if no block fits a tile (P <= 256).
+Plan make_plan_blocks(int KORD, int R, int forced_rb, bool allow_blocks, int P_fixed);
 Plan make_plan(int KORD, int R, int forced_rb, bool allow_blocks, int P_fixed = 0) {
+  Plan pl = make_plan_blocks(KORD, R, forced_rb, allow_blocks, P_fixed);
+  pl.useful_P = P_fixed > 0 ? P_fixed : block_slots(KORD, std::max(R, 0));
+  return pl;
+}
+Plan make_plan_blocks(int KORD, int R, int forced_rb, bool allow_blocks, int P_fixed) {
   Plan best;
   if (P_fixed > 0 || R < 1) {
     best.P = P_fixed > 0 ? P_fixed : block_slots(KORD, std::max(R, 0));
@@ -487,7 +494,8 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
   const int mchunks = (ld1 + 4 * threads - 1) / (4 * threads);
   const int64_t blocks = n * mchunks;
   if (blocks > INT32_MAX) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
-  ProfScope ps(h, CTM_KIND_SEED, (double)n * pl.nb * P * h->widths[1] * 4.0, st);
+  // bytes written: the layer-1 block, every slot row of every direction block, bf16 planes
+  ProfScope ps(h, CTM_KIND_SEED, (double)n * pl.nb * P * ld1 * 2.0 * h->nplanes, st);
   if (stoch_k4(a)) {
     ctm::SeedStochParams bp{};
     bp.X = a.X + p0 * D;
@@ -616,7 +624,9 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
     // persistent CTA pairs: an even grid, at most one CTA per SM
     const int64_t grid = 2 * std::min<int64_t>(n_tiles * (m_tiles / 2), h->sm_count / 2);
     {
-      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * nsub * P * gl.w_in * gl.w_out, st);
+      // useful FLOP: the point's slots with all directions in one block (the duplicated
+      // primal / top rows and zero padding of direction blocks are not counted)
+      ProfScope ps(h, CTM_KIND_LAYER, 2.0 * n * pl.useful_P * gl.w_in * gl.w_out, st);
       ctm_status s;
       int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
       if (KORD == 2 && flags == 0 && pl.ppt >= 8) flags = ctm::kFlagWide;
@@ -783,7 +793,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.pstride = (int64_t)b0.cap;
     rp.nplanes = h->nplanes;
     {
-      ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 4.0, st);
+      ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 2.0 * h->nplanes, st);
       launch_seed_random(h->nplanes, a.N, rp, st);
     }
     ++launches;

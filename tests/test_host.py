@@ -247,3 +247,62 @@ def test_product_path_raises_without_a_gpu():
 
     with pytest.raises(Exception):
         ctm.MLP([(torch.zeros(4, 3), torch.zeros(4)), (torch.zeros(1, 4), torch.zeros(1))], device=0)
+
+
+def _worker_strong(rank, world, port, n_total, q):
+    """bench.py --scaling strong on a world-2 gloo group with the fp64 oracle standing in for
+    the GPU operator: each rank evaluates its dist.shard slice of the global point set with the
+    global point_offset (randomized directions keyed on the global index), the results are
+    all_gathered, and rank 0 compares them bitwise with one process evaluating all points."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    from paper_2505_13644_b200.dist import gather, shard
+    from synth import mlp_params, points
+
+    params = mlp_params([4, 12, 10, 1], 0)
+    net = O.Net([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params])
+    Xall = points(n_total, 4, 1).astype(np.float64)
+    off, cnt = shard(n_total, rank, world)
+    V = O.rademacher(2, off, cnt, 3, 4)          # generated from the GLOBAL point index
+    op, f, _ = O.randomized_laplacian(net, Xall[off:off + cnt], V)
+    g_op = gather(torch.from_numpy(op), n_total)
+    g_f = gather(torch.from_numpy(f), n_total)
+    if rank == 0:
+        op1, f1, _ = O.randomized_laplacian(net, Xall, O.rademacher(2, 0, n_total, 3, 4))
+        q.put(bool(torch.equal(g_op, torch.from_numpy(op1)) and torch.equal(g_f, torch.from_numpy(f1))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_total", [9, 16])
+def test_strong_scaling_bookkeeping_world2_gloo(n_total):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_strong, args=(r, 2, port, n_total, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    ok = q.get(timeout=180)
+    for p in ps:
+        p.join(timeout=60)
+    assert ok
+
+
+def test_bench_strong_scaling_cli_and_workload_string():
+    """The strong-scaling workload names the total batch (both arms print the same config)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    sys_argv = ["bench.py", "--scaling", "strong", "--n-total", "4096"]
+    import sys
+
+    old = sys.argv
+    sys.argv = sys_argv
+    try:
+        args = bench.parse()
+    finally:
+        sys.argv = old
+    D, widths, wl = bench.workload(args)
+    assert args.scaling == "strong" and "N=4096 points split over the GPUs" in wl
