@@ -103,6 +103,7 @@ struct ctm_mlp {
   int device = 0;
   int act = ctm::kActTanh;    // hidden-layer activation (ctm_set_activation)
   int sm_count = 148;
+  bool seed_fixed_attr = false;  // max dynamic smem of the seed_fixed_kernel instances set
   int L = 0;                  // affine layers
   std::vector<int> widths;    // L + 1
   std::vector<int> wpad;      // hidden widths padded to 128 (index = layer)
@@ -538,6 +539,39 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     sp.nplanes = h->nplanes;
     sp.act = h->act;
     sp.z_out = z_out;
+    // forward K=2 fixed sets: the streaming seed (tables in shared memory) when its slice of
+    // W1^T and U^T fits (C1 seed 0.93 -> 0.83 ms in the bench step). Grad mode (z_out) and the
+    // other rules keep seed_layer_kernel; the K=4 instance of the streaming seed was 6% slower
+    // than it in the power-capped C4 step (1.70-1.75 vs 1.61-1.65 ms), so K=4 stays there too.
+    const size_t fsm = ctm::seed_fixed_smem(D, R, pl.nb);
+    constexpr size_t kFixedSmemMax = 200 * 1024;
+    if (KORD == 2 && !z_out && fsm <= kFixedSmemMax && ld1 % ctm::kSeedFixedFeats == 0 && n > 0) {
+      if (!h->seed_fixed_attr) {
+        CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kFixedSmemMax));
+        CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kFixedSmemMax));
+        h->seed_fixed_attr = true;
+      }
+      // one wave: as many blocks as are resident at once (registers, shared memory)
+      const int slices = ld1 / ctm::kSeedFixedFeats;
+      const int thr = ctm::kSeedFixedWarps * 32;
+      int per_sm = 1;
+      CTM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm,
+          h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3> : ctm::seed_fixed_kernel<2, 2>,
+          thr, fsm));
+      const int64_t want = std::max<int64_t>(1, (int64_t)h->sm_count * std::max(per_sm, 1) / slices);
+      const int64_t groups0 = std::min<int64_t>(want, (n + ctm::kSeedFixedWarps - 1) / ctm::kSeedFixedWarps);
+      const int64_t ppg = (n + groups0 - 1) / groups0;
+      const int64_t groups = (n + ppg - 1) / ppg;
+      if (groups > 65535) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
+      const dim3 grid((unsigned)slices, (unsigned)groups);
+      (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3><<<grid, thr, fsm, st>>>(sp, ppg)
+                       : ctm::seed_fixed_kernel<2, 2><<<grid, thr, fsm, st>>>(sp, ppg));
+      ++launches;
+      return CTM_OK;
+    }
 #define CTM_SEED(K)                                                            \
   (h->nplanes == 3 ? ctm::seed_layer_kernel<K, 3><<<(unsigned)blocks, threads, 0, st>>>(sp) \
                    : ctm::seed_layer_kernel<K, 2><<<(unsigned)blocks, threads, 0, st>>>(sp))

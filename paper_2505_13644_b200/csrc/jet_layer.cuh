@@ -612,18 +612,14 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
   store_out(p, (size_t)row * ld + m, z0b);
 }
 
-// The k-th tile of CTA pair `pair`. With at least one point group per pair, a pair runs
-// all feature tiles of a point group back to back (n-tile pair + (k / m_pairs) * npairs,
-// feature pair k % m_pairs), so the group's B operand is re-read from L2 while resident;
-// small batches spread the tiles (tile pair + k * npairs) to keep every pair busy.
-// Returns false past the pair's last tile.
+// The k-th tile of CTA pair `pair`: tile t = pair + k * npairs, feature pair t % m_pairs of
+// point group t / m_pairs. Consecutive tiles run on consecutive pairs at the same time, so
+// the m_pairs feature tiles of a point group read its B operand together: one HBM read,
+// the other reads hit L2 (ncu, C1 fp32 mode: layer-2 DRAM reads 7.8 -> 3.9 GB, layer time
+// -7%, against running a group's feature tiles back to back on one pair, whose re-reads
+// were evicted by the output writes in between). Returns false past the pair's last tile.
 __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_pairs, int64_t n_tiles, int64_t& n,
                                         int& m) {
-  if (n_tiles >= npairs) {
-    n = pair + (k / m_pairs) * npairs;
-    m = (int)(k % m_pairs);
-    return n < n_tiles;
-  }
   const int64_t tile = pair + k * npairs;
   n = tile / m_pairs;
   m = (int)(tile % m_pairs);

@@ -38,6 +38,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- TMA
+// Bulk prefetch of `bytes` (multiple of 16, 16-B aligned) from global memory into L2.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
@@ -317,11 +322,13 @@ __device__ __forceinline__ void store_planes(uint16_t* p, int64_t pstride, int n
   const __nv_bfloat16 h = __float2bfloat16_rn(v);
   const float r = v - __bfloat162float(h);
   const __nv_bfloat16 m = __float2bfloat16_rn(r);
+#ifdef CTM_EXP_CS  // experiment: streaming (evict-first) stores of the output planes
+  __stcs(p, __bfloat16_as_ushort(h));
+  __stcs(p + pstride, __bfloat16_as_ushort(m));
+  if (nplanes > 2) __stcs(p + 2 * pstride, __bfloat16_as_ushort(__float2bfloat16_rn(r - __bfloat162float(m))));
+#else
   p[0] = __bfloat16_as_ushort(h);
   p[pstride] = __bfloat16_as_ushort(m);
-#ifdef CTM_EXP_NP2  // experiment: the fast mode's two planes at compile time
-  (void)nplanes;
-#else
   if (nplanes > 2) p[2 * pstride] = __bfloat16_as_ushort(__float2bfloat16_rn(r - __bfloat162float(m)));
 #endif
 }

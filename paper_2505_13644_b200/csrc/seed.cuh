@@ -268,6 +268,95 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
 #undef CTM_BLOCK_END
 }
 
+// Fixed direction sets, K=2 (e_d, sigma columns) and K=4 (the biharmonic family), forward
+// only: the same layer-1 rule as seed_layer_kernel, laid out as a streaming store. A block
+// owns a 128-feature slice of layer 1 for a contiguous range of points and stages that
+// slice of W1^T, U^T, csum and b1 in shared memory once; each warp then runs one point at
+// a time (lane: 4 adjacent features), reading the tables from shared memory, so the loop
+// in front of the stores has no global-load latency (seed_layer_kernel re-reads U^T from
+// L2 for every point: ncu put 42% of its stall samples at the first use of a U^T value).
+// Writes are 256 contiguous bytes per warp per plane row.
+//   K=2: h0 = s(z0); h1_r = s'(z0) u_r; sum h2 = s''(z0) sum_r u_r^2      (x2 = 0)
+//   K=4: per jet h1 = s' u, h2 = s'' u^2, h3 = s''' u^3; sum_w h4 = s'''' sum_j w_j u_j^4
+// grid (ld / 128 slices, point groups); dynamic smem: seed_fixed_smem() bytes.
+constexpr int kSeedFixedFeats = 128;
+constexpr int kSeedFixedWarps = 8;
+__host__ __device__ inline size_t seed_fixed_smem(int D, int R, int blocks) {
+  return ((size_t)(D + R + blocks + 1) * kSeedFixedFeats + (size_t)kSeedFixedWarps * D) * sizeof(float);
+}
+
+template <int KORD, int NP>
+__global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const SeedParams p, int64_t pts_per_group) {
+  extern __shared__ float sm[];
+  constexpr int F = kSeedFixedFeats;
+  float* w1s = sm;                          // [D][F]
+  float* us = w1s + (size_t)p.D * F;        // [R][F]
+  float* cs = us + (size_t)p.R * F;         // [blocks][F]
+  float* bs = cs + (size_t)p.blocks * F;    // [F]
+  float* xs = bs + F;                       // [warps][D]
+  const int f0 = blockIdx.x * F;
+  for (int i = threadIdx.x; i < (p.D + p.R + p.blocks + 1) * (F / 4); i += blockDim.x) {
+    const int row = i / (F / 4), c4 = 4 * (i % (F / 4));
+    const float* src = row < p.D ? p.W1T + (size_t)row * p.ld
+                     : row < p.D + p.R ? p.UT + (size_t)(row - p.D) * p.ld
+                     : row < p.D + p.R + p.blocks ? p.csum + (size_t)(row - p.D - p.R) * p.ld
+                     : p.b1;
+    *reinterpret_cast<float4*>(sm + (size_t)row * F + c4) = ldg4(src + f0 + c4);
+  }
+  __syncthreads();
+  const PlaneOut o{p.out, p.pstride, p.nplanes};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = 4 * lane;
+  const int m = f0 + c;
+  float* xw = xs + warp * p.D;
+  const int64_t nb = blockIdx.y * pts_per_group;
+  const int64_t ne = (nb + pts_per_group < p.n_points) ? nb + pts_per_group : p.n_points;
+  constexpr int ROWS = (KORD == 4) ? 3 : 1;  // rows per direction (jet)
+  for (int64_t n = nb + warp; n < ne; n += kSeedFixedWarps) {
+    for (int d = lane; d < p.D; d += 32) xw[d] = __ldg(p.X + n * p.D + d);
+    __syncwarp();
+    float4 z0 = *reinterpret_cast<const float4*>(bs + c);
+    for (int d = 0; d < p.D; ++d) {
+      const float4 w = *reinterpret_cast<const float4*>(w1s + (size_t)d * F + c);
+      const float xd = xw[d];
+      z0.x = fmaf(w.x, xd, z0.x);
+      z0.y = fmaf(w.y, xd, z0.y);
+      z0.z = fmaf(w.z, xd, z0.z);
+      z0.w = fmaf(w.w, xd, z0.w);
+    }
+    __syncwarp();  // xw is rewritten for the warp's next point
+    // (four explicit calls: a loop over a local array was not unrolled and went to local memory)
+    const ActD A0 = act_derivs(p.act, z0.x), A1 = act_derivs(p.act, z0.y), A2 = act_derivs(p.act, z0.z),
+               A3 = act_derivs(p.act, z0.w);
+    const float t[4] = {A0.d0, A1.d0, A2.d0, A3.d0}, d1[4] = {A0.d1, A1.d1, A2.d1, A3.d1},
+                d2[4] = {A0.d2, A1.d2, A2.d2, A3.d2}, d3[4] = {A0.d3, A1.d3, A2.d3, A3.d3},
+                d4[4] = {A0.d4, A1.d4, A2.d4, A3.d4};
+    for (int b = 0; b < p.blocks; ++b) {
+      const size_t row0 = ((size_t)n * p.blocks + b) * p.P;
+      const int r0 = b * p.rb;
+      const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;
+      seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+      size_t row = row0 + 1;
+      for (int r = r0; r < r0 + p.rb; ++r, row += ROWS) {
+        const float4 u = (r < r1) ? *reinterpret_cast<const float4*>(us + (size_t)r * F + c)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        seed_store4<NP>(o, row * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+        if (KORD == 4) {
+          seed_store4<NP>(o, (row + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z,
+                          d2[3] * u.w * u.w);
+          seed_store4<NP>(o, (row + 2) * p.ld + m, d3[0] * u.x * u.x * u.x, d3[1] * u.y * u.y * u.y,
+                          d3[2] * u.z * u.z * u.z, d3[3] * u.w * u.w * u.w);
+        }
+      }
+      const float4 q = *reinterpret_cast<const float4*>(cs + (size_t)b * F + c);
+      if (KORD == 4)
+        seed_store4<NP>(o, row * p.ld + m, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w);
+      else
+        seed_store4<NP>(o, row * p.ld + m, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w);
+    }
+  }
+}
+
 // Stochastic biharmonic (Eq. 12 stochastic), layer 1 in fp32 on the CUDA
 // cores: per point, S standard normal directions v_s (explicit or generated), and for
 // each feature z1_s = W1 v_s; writes h1, h2, h3 per sample (x2 = x3 = 0) and the

@@ -178,6 +178,40 @@ def test_weighted_identity_is_laplacian_bitwise(ctm):
     np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-6, atol=1e-6)
 
 
+@pytest.mark.parametrize("widths,N,rb", [([50, 768, 64, 1], 37, 0), ([20, 256, 32, 1], 19, 7),
+                                         ([130, 128, 16, 1], 11, 0)])
+def test_streaming_seed_matches_grad_mode_seed_bitwise(ctm, widths, N, rb):
+    """The forward-only K=2 seed (seed_fixed_kernel, tables in shared memory) and the grad-mode
+    seed (seed_layer_kernel, which also saves z) apply the same operations in the same order:
+    op and f agree bit for bit, with and without direction blocks; D = 130 with 132 slots
+    still fits the streaming kernel's shared memory."""
+    params, _ = nets(widths, seed=11)
+    X = torch.from_numpy(points(N, widths[0], seed=11)).cuda()
+    sig = torch.from_numpy(make_sigma(widths[0], 9, kind="rect")).cuda()
+    fwd, grd = gpu_mlp(ctm, params), gpu_mlp(ctm, params)
+    grd.grad_enable()
+    # one block per point unless rb is given (grad mode always keeps one; the planner may
+    # otherwise split D = 130 directions into blocks, which reorders the collapsed sums)
+    fwd.set_direction_block(rb if rb else widths[0])
+    outs = []
+    for m in (fwd, grd):
+        op, f = m.laplacian(X)
+        wop, wf = m.weighted_laplacian(X, sig)
+        outs.append([t.clone() for t in (op, f, wop, wf)])
+    torch.cuda.synchronize()
+    if rb:  # blocks change the summation order of the collapsed top: compare to the oracle instead
+        _, onet = nets(widths, seed=11)
+        want, fw, norm = O.laplacian(onet, X.double().cpu().numpy())
+        check(outs[0][0], want, norm, outs[0][1], fw)
+        assert fwd.last_plan()["blocks"] >= 2
+    else:
+        assert fwd.last_plan()["blocks"] == 1
+        for a, b in zip(*outs):
+            assert torch.equal(a, b)
+    fwd.close()
+    grd.close()
+
+
 # ------------------------------------------------------------------ randomized
 @pytest.mark.parametrize("S", [8, 32, 128])
 def test_randomized_rademacher_generated(ctm, S):
