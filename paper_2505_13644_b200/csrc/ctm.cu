@@ -149,7 +149,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0, last_nb = 1, last_rb = 0;
-  bool smem_attr_set[64] = {};  // per (KORD, FLAGS) kernel instance
+  bool smem_attr_set[128] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
   std::vector<uint16_t*> WTp;               // W_l^T bf16 planes [3][wpad[l-1], wpad[l]], l = 2..L-1
@@ -322,17 +322,18 @@ struct ProfScope {
 // cudaFuncSetAttribute is per device: tracked per handle (a handle lives on one device)
 template <int KORD, int FLAGS = 0>
 ctm_status set_layer_attr(ctm_mlp* h) {
-  if (!h->smem_attr_set[KORD * 8 + FLAGS]) {
+  static_assert(KORD < 8 && FLAGS < 16, "smem_attr_set index");
+  if (!h->smem_attr_set[KORD * 16 + FLAGS]) {
     CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD, FLAGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctm::kLayerSmem));
-    h->smem_attr_set[KORD * 8 + FLAGS] = true;
+    h->smem_attr_set[KORD * 16 + FLAGS] = true;
   }
   return CTM_OK;
 }
 
 template <int KORD, int FLAGS>
-ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
-                               const ctm::LayerParams& lp, cudaStream_t st) {
+ctm_status launch_layer_instance(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
+                                 const ctm::LayerParams& lp, cudaStream_t st) {
   ctm_status s = set_layer_attr<KORD, FLAGS>(h);
   if (s != CTM_OK) return s;
   // programmatic dependent launch: the prologue (barriers, TMEM allocation, descriptor
@@ -349,6 +350,14 @@ ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap
   cfg.numAttrs = 1;
   CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::jet_layer_kernel<KORD, FLAGS>, amap, bmap, lp));
   return CTM_OK;
+}
+
+// the instance with the handle's plane count (lp.nplanes) as a compile-time constant
+template <int KORD, int FLAGS>
+ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
+                               const ctm::LayerParams& lp, cudaStream_t st) {
+  if (lp.nplanes == 2) return launch_layer_instance<KORD, FLAGS | ctm::kFlagNP2>(h, grid, amap, bmap, lp, st);
+  return launch_layer_instance<KORD, FLAGS>(h, grid, amap, bmap, lp, st);
 }
 
 // Tile plan of one operator call. A point's R directions (K=4: jets) are split into nb

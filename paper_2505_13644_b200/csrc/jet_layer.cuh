@@ -144,8 +144,9 @@ struct LayerParams {
 };
 static_assert(sizeof(LayerParams) == 128, "LayerParams grew past 128 bytes (see above)");
 
+template <int NPL>
 __device__ __forceinline__ void store_out(const LayerParams& p, size_t idx, float v) {
-  ptx::store_planes(p.out + idx, p.pstride, p.nplanes, v);
+  ptx::store_planes<NPL>(p.out + idx, p.pstride, v);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -169,11 +170,19 @@ constexpr int kFlagWeighted = 1, kFlagSaveZ = 2;
 // kFlagWide (plain K=2 only): 4 epilogue warp groups instead of 2, chosen by the host when a
 // tile holds >= 8 points (small P: the epilogue, not the MMA, bounds the tile).
 constexpr int kFlagWide = 4;
+// kFlagNP2: the fast mode's two operand planes (ctm_set_precision); without it three (the
+// fp32 mode). The plane count is a compile-time constant of every layer-kernel instance.
+constexpr int kFlagNP2 = 8;
+template <int FLAGS>
+__host__ __device__ constexpr int planes_of() {
+  return (FLAGS & kFlagNP2) ? 2 : 3;
+}
 
 template <int KORD, int FLAGS = 0>
 __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
                                                float wo, const float* jw, int part, int split, float* xacc,
                                                int bar_id, float& fpart, float& opart) {
+  constexpr int NPL = planes_of<FLAGS>();
   const int P = p.P;
   const int ld = p.ldo;
   constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
@@ -187,7 +196,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   fpart = (part == 2) ? 0.f : wo * t;
   opart = 0.f;
-  if (!p.readout && part != 2) store_out(p, (size_t)row * ld + m, t);
+  if (!p.readout && part != 2) store_out<NPL>(p, (size_t)row * ld + m, t);
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
   float* zp = kSaveZ ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
   if (kSaveZ && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
@@ -197,7 +206,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
   int jj = (KORD == 4) ? (mb - 1) / 3 : (KORD == kStd4) ? (mb - 1) / 4 : mb - 1;  // first direction / jet
   auto put = [&](float h) {
-    if (!p.readout) ptx::store_planes(po, p.pstride, p.nplanes, h);
+    if (!p.readout) ptx::store_planes<NPL>(po, p.pstride, h);
     po += ld;
   };
   if constexpr (KORD == 4) {
@@ -327,7 +336,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
   if constexpr (kSaveZ) *zp = zt;
   opart = wo * top;
-  if (!p.readout) ptx::store_planes(po, p.pstride, p.nplanes, top);
+  if (!p.readout) ptx::store_planes<NPL>(po, p.pstride, top);
 }
 
 // The K=2 rule for a point of P <= 16 slots whose 16 columns lie in the accumulator buffer:
@@ -339,6 +348,7 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
                                                      float bias, float wo, const float* jw, float& fpart,
                                                      float& opart) {
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
+  constexpr int NPL = planes_of<FLAGS>();
   constexpr bool wsum = (FLAGS & kFlagWeighted) != 0;
   const int P = PC > 0 ? PC : p.P;  // PC: the slot count as a compile-time constant
   const size_t ld = (size_t)p.ldo;
@@ -350,14 +360,14 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   fpart = wo * A.d0;
   uint16_t* po = p.out + (size_t)row * ld + m;
   float* zp = kSaveZ ? p.z_out + (size_t)row * p.ldz + m : nullptr;
-  if (!p.readout) ptx::store_planes(po, p.pstride, p.nplanes, A.d0);
+  if (!p.readout) ptx::store_planes<NPL>(po, p.pstride, A.d0);
   if constexpr (kSaveZ) zp[0] = z0;
   float acc = 0.f, zt = 0.f;
 #pragma unroll
   for (int i = 1; i < 16; ++i) {
     if (i < P - 1) {
       const float z = v[i];
-      if (!p.readout) ptx::store_planes(po + (size_t)i * ld, p.pstride, p.nplanes, A.d1 * z);
+      if (!p.readout) ptx::store_planes<NPL>(po + (size_t)i * ld, p.pstride, A.d1 * z);
       if constexpr (wsum)
         acc = fmaf(jw[i - 1] * z, z, acc);
       else
@@ -370,7 +380,7 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   const float top = A.d1 * zt + A.d2 * acc;
   if constexpr (kSaveZ) zp[(size_t)(P - 1) * p.ldz] = zt;
   opart = wo * top;
-  if (!p.readout) ptx::store_planes(po + (size_t)(P - 1) * ld, p.pstride, p.nplanes, top);
+  if (!p.readout) ptx::store_planes<NPL>(po + (size_t)(P - 1) * ld, p.pstride, top);
 }
 
 // Nested-Laplacian biharmonic epilogue (kNest) for one point, the whole point in this
@@ -383,6 +393,7 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
 //           + 4 s'' g^T L + s' Q
 // (D = 1 gives the K=4 Faa di Bruno row of the cheat sheet.) Register
 // arrays are sized kNestMaxD and indexed with compile-time indices under runtime guards.
+template <int NPL>
 __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
                                                 float wo, float& fpart, float& opart) {
   const int D = p.J;
@@ -396,13 +407,13 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   const bool store = !p.readout;
   fpart = wo * t;
-  if (store) store_out(p, (size_t)row * ld + m, t);
+  if (store) store_out<NPL>(p, (size_t)row * ld + m, t);
   float gg = 0.f;
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a)
     if (a < D) {
       gg = fmaf(g[a], g[a], gg);
-      if (store) store_out(p, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
+      if (store) store_out<NPL>(p, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
     }
   // Hessian slots, one packed row at a time
   float hg[kNestMaxD];
@@ -422,7 +433,7 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
         if (b < D) {
           const float h = hr[b];
           if (store)
-            store_out(p, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
+            store_out<NPL>(p, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
           if (b == a) {
             trH += h;
             HF = fmaf(h, h, HF);
@@ -450,19 +461,19 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
       gHg = fmaf(g[a], hg[a], gHg);
       if (store) {
         const float v = d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * Lv[a];
-        store_out(p, (size_t)(row + slot + a) * ld + m, v);
+        store_out<NPL>(p, (size_t)(row + slot + a) * ld + m, v);
       }
     }
   const float q = d4 * gg * gg + 2.f * d3 * gg * trH + 4.f * d3 * gHg + 2.f * d2 * HF + d2 * trH * trH +
                   4.f * d2 * gL + d1 * zq;
   opart = wo * q;
-  if (store) store_out(p, (size_t)(row + slot + D) * ld + m, q);
+  if (store) store_out<NPL>(p, (size_t)(row + slot + D) * ld + m, q);
 }
 
 // The same rule with D known at compile time (D <= 8, P <= 54): the point's P columns
 // are read with one burst of x16/x8/x4/x2/x1 loads and a single wait, and every slot
 // index is a constant, so the whole point lives in registers.
-template <int D>
+template <int D, int NPL>
 __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t tcol, int64_t row, int m,
                                                   float bias, float wo, float& fpart, float& opart) {
   constexpr int T = D * (D + 1) / 2;
@@ -509,7 +520,7 @@ __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t
   opart = wo * q;
   if (p.readout) return;
   uint16_t* po = p.out + (size_t)row * ld + m;
-  auto put = [&](size_t off, float v) { ptx::store_planes(po + off, p.pstride, p.nplanes, v); };
+  auto put = [&](size_t off, float v) { ptx::store_planes<NPL>(po + off, p.pstride, v); };
   put(0, t);
 #pragma unroll
   for (int a = 0; a < D; ++a) put((size_t)(1 + a) * ld, d1 * g[a]);
@@ -526,18 +537,19 @@ __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t
   put((size_t)(P - 1) * ld, q);
 }
 
+template <int NPL>
 __device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32_t tcol, int64_t row, int m,
                                                     float bias, float wo, float& fpart, float& opart) {
   switch (p.J) {
-    case 1: epilogue_nested_d<1>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 2: epilogue_nested_d<2>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 3: epilogue_nested_d<3>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 4: epilogue_nested_d<4>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 5: epilogue_nested_d<5>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 6: epilogue_nested_d<6>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 7: epilogue_nested_d<7>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 8: epilogue_nested_d<8>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    default: epilogue_nested(p, tcol, row, m, bias, wo, fpart, opart);
+    case 1: epilogue_nested_d<1, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 2: epilogue_nested_d<2, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 3: epilogue_nested_d<3, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 4: epilogue_nested_d<4, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 5: epilogue_nested_d<5, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 6: epilogue_nested_d<6, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 7: epilogue_nested_d<7, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    case 8: epilogue_nested_d<8, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
+    default: epilogue_nested<NPL>(p, tcol, row, m, bias, wo, fpart, opart);
   }
 }
 
@@ -553,7 +565,7 @@ __device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32
 // (w_r = 1 unless p.weighted). Writes Z_bar of this layer as bf16 pairs.
 // kB: slots per TMEM load / z-load batch (16; 8 keeps the register count of the 4-group
 // adjoint instance low)
-template <int kB>
+template <int kB, int NPL>
 __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tcol, int64_t row, int m,
                                               const float* jw) {
   const int P = p.P;
@@ -576,7 +588,7 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
     const float w = wsum ? jw[r] : 1.f;
     szh = fmaf(z1, hb, szh);
     szz = fmaf(w * z1, z1, szz);
-    ptx::store_planes(po, p.pstride, p.nplanes, fmaf(A.d1, hb, w * two_s2_tb * z1));
+    ptx::store_planes<NPL>(po, p.pstride, fmaf(A.d1, hb, w * two_s2_tb * z1));
     po += ld;
   };
   for (; s + kB <= nmid; s += kB) {
@@ -607,9 +619,9 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
     for (int i = 0; i < kB - 1; ++i)
       if (i < rem) one(v[i], z[i], s + i);
   }
-  ptx::store_planes(po, p.pstride, p.nplanes, A.d1 * tb);  // slot P-1
+  ptx::store_planes<NPL>(po, p.pstride, A.d1 * tb);  // slot P-1
   const float z0b = A.d1 * hb0 + A.d2 * szh + (A.d2 * zt + A.d3 * szz) * tb;
-  store_out(p, (size_t)row * ld + m, z0b);
+  store_out<NPL>(p, (size_t)row * ld + m, z0b);
 }
 
 // The k-th tile of CTA pair `pair`: tile t = pair + k * npairs, feature pair t % m_pairs of
@@ -688,6 +700,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
   float* xacc = jw + kMaxW;                                                 // [2][128] split-point partials
 
   constexpr int EG = epi_groups<KORD, FLAGS>();
+  constexpr int NPL = planes_of<FLAGS>();  // operand planes read and written
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -732,7 +745,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       for (int64_t k = 0; tile_of(k, pair, npairs, m_pairs, n_tiles, nt, mp); ++k) {
         const int m0 = mp * (2 * kBM) + (int)rank * kBM;
         const int32_t row0 = (int32_t)(nt * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
-        for_each_group(p.nplanes, p.k_iters, [&](int, int kb, int nslots) {
+        for_each_group(NPL, p.k_iters, [&](int, int kb, int nslots) {
           for (int pl = 0; pl < nslots; ++pl, ++it) {
             const uint32_t s = it % kSlots;
             const uint32_t ph = (it / kSlots) & 1u;
@@ -776,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
         uint32_t acc = 0;  // the tile's first MMA overwrites the accumulator
-        for_each_group(p.nplanes, p.k_iters, [&](int phase, int, int nslots) {
+        for_each_group(NPL, p.k_iters, [&](int phase, int, int nslots) {
           for (int pl = 0; pl < nslots; ++pl) {
             STAT_T0();
             ptx::mbar_wait(&full_bar[(it + pl) % kSlots], ((it + pl) / kSlots) & 1u);
@@ -864,13 +877,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
       if (KORD == kBwd2) {
         for (int pt = g; pt < npts; pt += EG)
-          epilogue_bwd2<EG == 4 ? 8 : 16>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);
+          epilogue_bwd2<EG == 4 ? 8 : 16, NPL>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);
       } else if (KORD == kNest) {
         // nested biharmonic: a point is never split; with one point per tile (D >= 14)
         // only warp group 0 works on it
         for (int pt = g; pt < npts; pt += EG) {
           float fpart, opart;
-          epilogue_nested_any(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, fpart,
+          epilogue_nested_any<NPL>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, fpart,
                               opart);
           if (p.readout) {
             fpart = warp_sum(fpart);
@@ -898,7 +911,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           float fpart, opart;
           const int jbase = (kW && p.blocks > 1) ? ((blk0 + pt) % p.blocks) * p.rb : 0;
           // (the plain K=2 instance runs only with < 8 points per tile, i.e. P > 28: no small path)
-          constexpr bool kSmall = (KORD == 2) && (FLAGS != 0);
+          constexpr bool kSmall = (KORD == 2) && ((FLAGS & ~kFlagNP2) != 0);
           if (kSmall && p.P <= 16 && pt * p.P + 16 <= kMaxN) {
             // P <= 12 as a compile-time constant: no runtime slot guards in the unrolled
             // loop (the epilogue is issue-bound there: S=4 +6%, S=8 +1.6%; P = 13..16 gained
