@@ -559,7 +559,7 @@ def main():
         with open(tpath) as fh_:
             tj = json.load(fh_)
         key = (f"{args.op}_S{args.S}" if args.op == "randomized" else args.op) + f"_{args.precision}"
-        traffic = tj.get(key, {}).get("dram_bytes_per_launch")
+        traffic = tj.get(key, {}).get({"layer": "", "bwd": "bwd_"}.get(dom, "wgrad_") + "dram_bytes_per_launch")
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": useful_peak, "unit": "TFLOP/s",
         "frac": (achieved / useful_peak) if achieved else None, "traffic": traffic,
