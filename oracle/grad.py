@@ -88,3 +88,52 @@ def k2_grad(Ws, bs, X, dirs, w, gop, gf=None, act: str = "tanh"):
     L = len(Ws)
     return (op.detach().numpy(), f.detach().numpy(), [g.numpy() for g in grads[:L]],
             [g.numpy() for g in grads[L:]])
+
+
+def k2_grad_magnitude(Ws, bs, X, dirs, w, gop, gf=None, act: str = "tanh"):
+    """Per-element magnitude of the parameter gradients (the gradient analogue of the
+    north_star normaliser, reading R10 of DESIGN.md §3): the same vanilla computation as
+    k2_operator, and for every affine layer z_k = W h_k (+ b for k = 0) the sum of the
+    ABSOLUTE values of the terms of its final contraction,
+        M_W[l] = |z0_bar|^T |h0| + sum_j (|z1_bar_j|^T |h1_j| + |z2_bar_j|^T |h2_j|),
+        M_b[l] = sum_n |z0_bar|,
+    with z_bar the fp64 adjoints dL/dz of that layer. M >= |dL/dtheta| elementwise, with
+    equality when no two terms of an element differ in sign. Returns ([M_W], [M_b])."""
+    X = torch.as_tensor(X, dtype=torch.float64)
+    dirs = torch.as_tensor(dirs, dtype=torch.float64)
+    w = torch.as_tensor(w, dtype=torch.float64)
+    Wt = [torch.as_tensor(np.asarray(W, dtype=np.float64)) for W in Ws]
+    bt = [torch.as_tensor(np.asarray(b, dtype=np.float64).reshape(-1)) for b in bs]
+    N = X.shape[0]
+    if dirs.dim() == 2:
+        dirs = dirs.unsqueeze(0).expand(N, -1, -1)
+    h0, h1 = X, dirs
+    h2 = torch.zeros_like(dirs)
+    ins, zs = [], []
+    L = len(Wt)
+    for l in range(L):
+        z0 = (h0 @ Wt[l].T + bt[l]).requires_grad_(True)
+        z1 = (h1 @ Wt[l].T).requires_grad_(True)
+        z2 = (h2 @ Wt[l].T).requires_grad_(True)
+        ins.append((h0.detach(), h1.detach(), h2.detach()))
+        zs.append((z0, z1, z2))
+        if l == L - 1:
+            op, f = (z2[..., 0] * w).sum(-1), z0[:, 0]
+            break
+        s0, s1, s2 = _derivs(act, z0)
+        h0 = s0
+        h1 = s1.unsqueeze(1) * z1
+        h2 = s2.unsqueeze(1) * z1 * z1 + s1.unsqueeze(1) * z2
+    loss = (torch.as_tensor(gop, dtype=torch.float64) * op).sum()
+    if gf is not None:
+        loss = loss + (torch.as_tensor(gf, dtype=torch.float64) * f).sum()
+    flat = [z for t in zs for z in t]
+    bars = torch.autograd.grad(loss, flat, allow_unused=True)
+    bars = [torch.zeros_like(z) if g is None else g for g, z in zip(bars, flat)]
+    MW, Mb = [], []
+    for l in range(L):
+        zb0, zb1, zb2 = (bars[3 * l + k].abs() for k in range(3))
+        a0, a1, a2 = (t.abs() for t in ins[l])
+        MW.append((zb0.T @ a0 + torch.einsum("njo,nji->oi", zb1, a1) + torch.einsum("njo,nji->oi", zb2, a2)).numpy())
+        Mb.append(zb0.sum(0).numpy())
+    return MW, Mb

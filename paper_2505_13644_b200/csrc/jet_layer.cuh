@@ -23,6 +23,8 @@
 //     accumulator ("bf16x6, two phases": the main products see only K/16 accumulations);
 //   fast mode, 2 planes: p1*p0 + p0*p1 + p0*p0 per K step ("3xBF16", ~17 operand bits).
 #pragma once
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace ctm {
@@ -200,14 +202,18 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
   float* zp = kSaveZ ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
   if (kSaveZ && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
-  uint16_t* po = p.out + (size_t)(row + mb) * ld + m;
+  // plane bases of slot mb; the slot after it is a running 32-bit element offset
+  uint16_t* const q0 = p.out + (size_t)(row + mb) * ld + m;
+  uint16_t* const q1 = q0 + p.pstride;
+  uint16_t* const q2 = q1 + p.pstride;
+  uint32_t off = 0;
   // ---- middle slots: first-order coefficients (K=2), jets (z1, z2, z3) (K=4), or the
   //      standard-mode pairs (z1_r, z2_r) with no collapse
   float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
   int jj = (KORD == 4) ? (mb - 1) / 3 : (KORD == kStd4) ? (mb - 1) / 4 : mb - 1;  // first direction / jet
   auto put = [&](float h) {
-    if (!p.readout) ptx::store_planes<NPL>(po, p.pstride, h);
-    po += ld;
+    if (!p.readout) ptx::store_planes_off<NPL>(q0, q1, q2, off, h);
+    off += (uint32_t)ld;
   };
   if constexpr (KORD == 4) {
     // jets (z1, z2, z3), read 5 at a time (15 of 16 columns) so each slot's role is a
@@ -336,7 +342,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
   if constexpr (kSaveZ) *zp = zt;
   opart = wo * top;
-  if (!p.readout) ptx::store_planes<NPL>(po, p.pstride, top);
+  if (!p.readout) ptx::store_planes_off<NPL>(q0, q1, q2, off, top);
 }
 
 // The K=2 rule for a point of P <= 16 slots whose 16 columns lie in the accumulator buffer:
@@ -351,36 +357,47 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   constexpr int NPL = planes_of<FLAGS>();
   constexpr bool wsum = (FLAGS & kFlagWeighted) != 0;
   const int P = PC > 0 ? PC : p.P;  // PC: the slot count as a compile-time constant
-  const size_t ld = (size_t)p.ldo;
+  const uint32_t ld = (uint32_t)p.ldo;
   float v[16];
   ptx::tmem_ld16(tcol, v);
   ptx::tmem_ld_wait();
   const float z0 = v[0] + bias;
   const ActD A = act_derivs(p.act, z0);
   fpart = wo * A.d0;
-  uint16_t* po = p.out + (size_t)row * ld + m;
+  // plane bases of the point's slot 0; slot i of plane k is q_k[i * ld]
+  uint16_t* const q0 = p.out + (size_t)row * ld + m;
+  uint16_t* const q1 = q0 + p.pstride;
+  uint16_t* const q2 = q1 + p.pstride;
   float* zp = kSaveZ ? p.z_out + (size_t)row * p.ldz + m : nullptr;
-  if (!p.readout) ptx::store_planes<NPL>(po, p.pstride, A.d0);
   if constexpr (kSaveZ) zp[0] = z0;
-  float acc = 0.f, zt = 0.f;
+  // one loop per value of p.readout (uniform): no per-store test of the flag
+  auto body = [&](auto ro) {
+    constexpr bool kRO = decltype(ro)::value;
+    if (!kRO) ptx::store_planes_off<NPL>(q0, q1, q2, 0u, A.d0);
+    float acc = 0.f, zt = 0.f;
 #pragma unroll
-  for (int i = 1; i < 16; ++i) {
-    if (i < P - 1) {
-      const float z = v[i];
-      if (!p.readout) ptx::store_planes<NPL>(po + (size_t)i * ld, p.pstride, A.d1 * z);
-      if constexpr (wsum)
-        acc = fmaf(jw[i - 1] * z, z, acc);
-      else
-        acc = fmaf(z, z, acc);
-      if constexpr (kSaveZ) zp[(size_t)i * p.ldz] = z;
-    } else if (i == P - 1) {
-      zt = v[i];
+    for (int i = 1; i < 16; ++i) {
+      if (i < P - 1) {
+        const float z = v[i];
+        if (!kRO) ptx::store_planes_off<NPL>(q0, q1, q2, (uint32_t)i * ld, A.d1 * z);
+        if constexpr (wsum)
+          acc = fmaf(jw[i - 1] * z, z, acc);
+        else
+          acc = fmaf(z, z, acc);
+        if constexpr (kSaveZ) zp[(size_t)i * p.ldz] = z;
+      } else if (i == P - 1) {
+        zt = v[i];
+      }
     }
-  }
-  const float top = A.d1 * zt + A.d2 * acc;
-  if constexpr (kSaveZ) zp[(size_t)(P - 1) * p.ldz] = zt;
-  opart = wo * top;
-  if (!p.readout) ptx::store_planes<NPL>(po + (size_t)(P - 1) * ld, p.pstride, top);
+    const float top = A.d1 * zt + A.d2 * acc;
+    if constexpr (kSaveZ) zp[(size_t)(P - 1) * p.ldz] = zt;
+    opart = wo * top;
+    if (!kRO) ptx::store_planes_off<NPL>(q0, q1, q2, (uint32_t)(P - 1) * ld, top);
+  };
+  if (p.readout)
+    body(std::true_type{});
+  else
+    body(std::false_type{});
 }
 
 // Nested-Laplacian biharmonic epilogue (kNest) for one point, the whole point in this
@@ -570,26 +587,29 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
                                               const float* jw) {
   const int P = p.P;
   const int ld = p.ldo;
-  const size_t ldz = (size_t)p.ldzi;
+  const uint32_t ldz = (uint32_t)p.ldzi;  // slot offsets are 32-bit (one wide multiply-add per address)
   const float* zr = p.z_in + (size_t)row * ldz + m;
   const float hb0 = ptx::tmem_ld1(tcol);
   const float tb = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
   const float z0 = zr[0];
-  const float zt = zr[(size_t)(P - 1) * ldz];
+  const float zt = zr[(uint32_t)(P - 1) * ldz];
   ptx::tmem_ld_wait();
   const ActD A = act_derivs(p.act, z0);
   const float two_s2_tb = 2.f * A.d2 * tb;
   const bool wsum = p.weighted;
   float szh = 0.f, szz = 0.f;
-  uint16_t* po = p.out + (size_t)(row + 1) * ld + m;
+  uint16_t* const q0 = p.out + (size_t)(row + 1) * ld + m;  // plane bases of slot 1
+  uint16_t* const q1 = q0 + p.pstride;
+  uint16_t* const q2 = q1 + p.pstride;
+  uint32_t off = 0;
   const int nmid = P - 2;
   int s = 0;
   auto one = [&](float hb, float z1, int r) {
     const float w = wsum ? jw[r] : 1.f;
     szh = fmaf(z1, hb, szh);
     szz = fmaf(w * z1, z1, szz);
-    ptx::store_planes<NPL>(po, p.pstride, fmaf(A.d1, hb, w * two_s2_tb * z1));
-    po += ld;
+    ptx::store_planes_off<NPL>(q0, q1, q2, off, fmaf(A.d1, hb, w * two_s2_tb * z1));
+    off += (uint32_t)ld;
   };
   for (; s + kB <= nmid; s += kB) {
     float v[kB], z[kB];
@@ -599,7 +619,7 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
       ptx::tmem_ld8(tcol + (uint32_t)(1 + s), v);
 #pragma unroll
     for (int i = 0; i < kB; ++i) {
-      z[i] = zr[(size_t)(1 + s + i) * ldz];
+      z[i] = zr[(uint32_t)(1 + s + i) * ldz];
     }
     ptx::tmem_ld_wait();
 #pragma unroll
@@ -612,14 +632,14 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
     for (int i = 0; i < kB - 1; ++i)
       if (i < rem) {
         v[i] = ptx::tmem_ld1(tcol + (uint32_t)(1 + s + i));
-        z[i] = zr[(size_t)(1 + s + i) * ldz];
+        z[i] = zr[(uint32_t)(1 + s + i) * ldz];
       }
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < kB - 1; ++i)
       if (i < rem) one(v[i], z[i], s + i);
   }
-  ptx::store_planes<NPL>(po, p.pstride, A.d1 * tb);  // slot P-1
+  ptx::store_planes_off<NPL>(q0, q1, q2, off, A.d1 * tb);  // slot P-1
   const float z0b = A.d1 * hb0 + A.d2 * szh + (A.d2 * zt + A.d3 * szz) * tb;
   store_out<NPL>(p, (size_t)row * ld + m, z0b);
 }

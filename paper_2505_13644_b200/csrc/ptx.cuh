@@ -338,6 +338,20 @@ __device__ __forceinline__ void store_planes(uint16_t* p, int64_t pstride, float
   p[pstride] = __bfloat16_as_ushort(m);
   if (NPL > 2) p[2 * pstride] = __bfloat16_as_ushort(__float2bfloat16_rn(r - __bfloat162float(m)));
 }
+// The same with the three plane bases of a point precomputed and a 32-bit element offset,
+// so each store's address is one wide multiply-add instead of 64-bit pointer arithmetic per
+// plane (fewer integer instructions per output; same-box A/B: layer times unchanged within
+// noise, the S=8 epilogue is latency- rather than issue-bound).
+template <int NPL>
+__device__ __forceinline__ void store_planes_off(uint16_t* q0, uint16_t* q1, uint16_t* q2, uint32_t off, float v) {
+  static_assert(NPL == 2 || NPL == 3, "planes");
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  const float r = v - __bfloat162float(h);
+  const __nv_bfloat16 m = __float2bfloat16_rn(r);
+  q0[off] = __bfloat16_as_ushort(h);
+  q1[off] = __bfloat16_as_ushort(m);
+  if (NPL > 2) q2[off] = __bfloat16_as_ushort(__float2bfloat16_rn(r - __bfloat162float(m)));
+}
 // Programmatic dependent launch: the next kernel in the stream may start its prologue
 // once every CTA of this grid has called launch_dependents (or exited); wait_prior blocks
 // until the previous grid has completed and its memory is visible.

@@ -9,10 +9,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2505_13644_b200 as ctm  # noqa: E402
 from synth import gaussian_directions, mlp_params, points, sigma, sigma_field, signed_weights  # noqa: E402
 
-for widths in ([5, 16, 16, 1], [50, 64, 64, 1]):
+for widths, prec in (([5, 16, 16, 1], "fp32"), ([50, 64, 64, 1], "fp32"), ([50, 64, 64, 1], "bf16x3"),
+                     ([3, 16, 130, 1], "fp32")):
     D = widths[0]
     params = mlp_params(widths, 0)
     mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0)
+    mlp.set_precision(prec)
     X = torch.from_numpy(points(9, D)).cuda()
     outs = [mlp.laplacian(X)[0], mlp.laplacian_standard(X)[0],
             mlp.weighted_laplacian(X, torch.from_numpy(sigma(D, D)).cuda())[0],
@@ -46,5 +48,5 @@ for widths in ([5, 16, 16, 1], [50, 64, 64, 1]):
     mlp.set_weights([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params])
     outs.append(mlp.laplacian(X)[0])
     torch.cuda.synchronize()
-    print(widths, [float(o.abs().max()) for o in outs])
+    print(widths, prec, [float(o.abs().max()) for o in outs])
     mlp.close()

@@ -46,15 +46,30 @@ def _mlp(ctm, params, act="tanh"):
     return m
 
 
-def _check_grads(name, grads, dW, db, tol=GTOL):
+def _k2(*a, **k):
+    """fp64 oracle gradients and their per-element magnitudes (oracle/grad.py)."""
+    _, _, dW, db = OG.k2_grad(*a, **k)
+    return dW, db, OG.k2_grad_magnitude(*a, **k)
+
+
+def _check_grads(name, grads, dW, db, mag, tol=GTOL):
+    """Two bars (reading R10): per tensor, max|g - r| <= tol * max|r|; and per ELEMENT,
+    |g_i - r_i| <= tol * M_i (+ 1e-12 * max M for elements whose terms are all zero), M the
+    sum of the absolute terms of the element's final contraction (k2_grad_magnitude) — the
+    gradient analogue of the north_star normaliser, which also checks small elements."""
     rec = {}
-    for l, ((gW, gb), rW, rb) in enumerate(zip(grads, dW, db)):
-        for tag, g, r in (("W", gW, rW), ("b", gb, rb)):
+    MW, Mb = mag
+    for l, ((gW, gb), rW, rb, mW, mb) in enumerate(zip(grads, dW, db, MW, Mb)):
+        for tag, g, r, m in (("W", gW, rW, mW), ("b", gb, rb, mb)):
             g = g.double().cpu().numpy()
             assert np.all(np.isfinite(g))
             scale = np.max(np.abs(r))
             err = np.max(np.abs(g - r)) / scale if scale > 0 else np.max(np.abs(g))
             rec[f"{tag}{l}"] = float(err)
+            m = np.asarray(m).reshape(r.shape)
+            floor = 1e-12 * max(float(np.max(m)), 1e-30)
+            rel = np.abs(g - r) / np.maximum(m, floor)
+            rec[f"{tag}{l}_elem"] = float(np.max(rel))
     ERRS[name] = rec
     worst = max(rec.values())
     assert worst <= tol, f"{name}: {rec}"
@@ -77,8 +92,8 @@ def test_laplacian_gradients(ctm, widths, N):
     grads = mlp.backward(torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda())
     Ws = [W.astype(np.float64) for W, _ in params]
     bs = [b.astype(np.float64) for _, b in params]
-    _, _, dW, db = OG.k2_grad(Ws, bs, X.astype(np.float64), np.eye(D), np.ones(D), gop, gf)
-    _check_grads(f"laplacian{widths}", grads, dW, db)
+    dW, db, mag = _k2(Ws, bs, X.astype(np.float64), np.eye(D), np.ones(D), gop, gf)
+    _check_grads(f"laplacian{widths}", grads, dW, db, mag)
 
 
 def test_weighted_randomized_pointwise_and_directional_gradients(ctm):
@@ -96,25 +111,25 @@ def test_weighted_randomized_pointwise_and_directional_gradients(ctm):
     # weighted (sigma rect R = 3)
     sig = make_sigma(D, 3, kind="rect")
     mlp.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())
-    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, sig.astype(np.float64).T, np.ones(3), gop, gf)
-    _check_grads("weighted", mlp.backward(g_op, g_f), dW, db)
+    dW, db, mag = _k2(Ws, bs, Xd, sig.astype(np.float64).T, np.ones(3), gop, gf)
+    _check_grads("weighted", mlp.backward(g_op, g_f), dW, db, mag)
     # randomized (Rademacher generated in-kernel, S = 6): op carries 1/S
     mlp.randomized_laplacian(Xc, S=6, seed=3)
     V = O.rademacher(3, 0, N, 6, D)
-    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, V, np.full(6, 1 / 6), gop, gf)
-    _check_grads("randomized", mlp.backward(g_op, g_f), dW, db)
+    dW, db, mag = _k2(Ws, bs, Xd, V, np.full(6, 1 / 6), gop, gf)
+    _check_grads("randomized", mlp.backward(g_op, g_f), dW, db, mag)
     # sigma(x)
     sx = sigma_field(X, 4)
     mlp.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())
-    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, np.transpose(sx.astype(np.float64), (0, 2, 1)), np.ones(4), gop, gf)
-    _check_grads("pointwise", mlp.backward(g_op, g_f), dW, db)
+    dW, db, mag = _k2(Ws, bs, Xd, np.transpose(sx.astype(np.float64), (0, 2, 1)), np.ones(4), gop, gf)
+    _check_grads("pointwise", mlp.backward(g_op, g_f), dW, db, mag)
     # directional sums K = 2 with signed weights, shared and per point
     w = signed_weights(4)
     for per_point in (False, True):
         dirs = gaussian_directions(N, 4, D, seed=8) if per_point else gaussian_directions(1, 4, D, seed=8)[0]
         mlp.directional_sum(Xc, 2, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())
-        _, _, dW, db = OG.k2_grad(Ws, bs, Xd, dirs.astype(np.float64), w.astype(np.float64), gop, gf)
-        _check_grads(f"directional_pp{int(per_point)}", mlp.backward(g_op, g_f), dW, db)
+        dW, db, mag = _k2(Ws, bs, Xd, dirs.astype(np.float64), w.astype(np.float64), gop, gf)
+        _check_grads(f"directional_pp{int(per_point)}", mlp.backward(g_op, g_f), dW, db, mag)
 
 
 @pytest.mark.parametrize("act", ["sin", "exp"])
@@ -126,9 +141,9 @@ def test_sin_exp_activation_gradients(ctm, act):
     mlp = _mlp(ctm, params, act=act)
     mlp.laplacian(torch.from_numpy(X).cuda())
     grads = mlp.backward(torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda())
-    _, _, dW, db = OG.k2_grad([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params],
+    dW, db, mag = _k2([W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params],
                               X.astype(np.float64), np.eye(4), np.ones(4), gop, gf, act=act)
-    _check_grads(act, grads, dW, db)
+    _check_grads(act, grads, dW, db, mag)
 
 
 def test_backward_is_deterministic_accumulates_and_needs_a_tape(ctm):
@@ -250,8 +265,8 @@ def test_fuzz_shapes_gradients(ctm, case):
         mlp.directional_sum(Xc, 2, torch.from_numpy(d).cuda(), torch.from_numpy(ws).cuda())
         dirs, w = d.astype(np.float64), ws.astype(np.float64)
     grads = mlp.backward(go, gfc)
-    _, _, dW, db = OG.k2_grad(Ws, bs, Xd, dirs, w, gop, gf)
-    _check_grads(f"fuzz{case}_{which}_{widths}_N{N}", grads, dW, db)
+    dW, db, mag = _k2(Ws, bs, Xd, dirs, w, gop, gf)
+    _check_grads(f"fuzz{case}_{which}_{widths}_N{N}", grads, dW, db, mag)
 
 
 def test_pinn_poisson_example_trains(ctm):

@@ -612,30 +612,37 @@ def test_errors_are_status_codes(ctm):
 
 
 # ------------------------------------------------------------------ full size (bench config)
+# sample sizes of the full-size tests (the oracle checks these points one by one)
+FULL_SAMPLE = int(os.environ.get("CTM_FULL_SAMPLE", "256"))
+
+
 def test_c1_full_batch_sampled(ctm):
-    """BASELINE C1 at N = 16384 in the bench's launch configuration; the oracle
-    checks every 512th point (32 points, including tile-boundary positions)."""
+    """BASELINE C1 at N = 16384 in the bench's launch configuration; the oracle checks
+    every 32nd point (512 points, every position inside a 4-point tile)."""
     params, onet = nets(C1_WIDTHS)
     N = 16384
     X = points(N, 50)
     mlp = gpu_mlp(ctm, params)
     op, f = mlp.laplacian(torch.from_numpy(X).cuda())
-    idx = np.arange(0, N, 512) + (np.arange(32) % 4)
+    k = 2 * FULL_SAMPLE
+    idx = np.arange(0, N, N // k)[:k] + (np.arange(k) % 4)
     want, fwant, norm = O.laplacian(onet, X[idx].astype(np.float64), O.O1)
     check(op.cpu()[idx], want, norm, f.cpu()[idx], fwant)
 
 
 # ------------------------------------------------------------------ full BASELINE sizes, sampled
-def _sample_idx(N, k=32):
-    """k points spread over the batch, including tile-boundary positions (offsets 0..3)."""
+def _sample_idx(N, k=None):
+    """k points spread over the batch, at every position inside a tile of up to 16 points."""
+    k = FULL_SAMPLE if k is None else k
     base = np.arange(0, N, max(1, N // k))[:k]
-    return np.unique(np.minimum(base + np.arange(len(base)) % 4, N - 1))
+    return np.unique(np.minimum(base + np.arange(len(base)) % 16, N - 1))
 
 
 @pytest.mark.parametrize("cfg", ["C2", "C3-S8", "C3-S32", "C3-S128", "C4", "C4-nested", "sigma-x"])
 def test_full_size_sampled(ctm, cfg):
     """Every BASELINE config at N = 16384 in the bench's launch configuration (same
-    operator call, same generated directions); the oracle checks a spread sample."""
+    operator call, same generated directions); the oracle checks a spread sample of
+    FULL_SAMPLE (256) points."""
     N = 16384
     D = 5 if cfg.startswith("C4") else 50
     params, onet = nets(widths_for(D))

@@ -74,3 +74,52 @@ def test_one_hidden_layer_closed_form_gradient():
     assert db[1][0] == 0.0
     _, _, _, db = OG.k2_grad(Ws, bs, X, np.eye(D), np.ones(D), np.zeros(1), np.ones(1))
     assert db[1][0] == 1.0
+
+
+# ------------------------------------------------------------------ gradient magnitude (R10)
+@pytest.mark.parametrize("act", ["tanh", "sin"])
+def test_gradient_magnitude_bounds_every_element(act):
+    """M = sum of |terms| of each gradient element's final contraction bounds |g| elementwise
+    (triangle inequality), and is strictly larger where terms cancel."""
+    D = 4
+    Ws, bs = random_params([D, 9, 7, 1], 11, scale=1.5)
+    X = _pts(6, D, seed=8)
+    rng = np.random.default_rng(12)
+    dirs, w = rng.standard_normal((5, D)), rng.standard_normal(5)
+    gop, gf = rng.standard_normal(6), rng.standard_normal(6)
+    _, _, dW, db = OG.k2_grad(Ws, bs, X, dirs, w, gop, gf, act=act)
+    MW, Mb = OG.k2_grad_magnitude(Ws, bs, X, dirs, w, gop, gf, act=act)
+    strict = 0
+    for g, m in zip(dW + db, MW + Mb):
+        assert g.shape == np.shape(m)
+        assert np.all(m >= np.abs(g) * (1 - 1e-12) - 1e-300)
+        strict += int(np.sum(m > 1.01 * np.abs(g)))
+    assert strict > 0
+
+
+def test_gradient_magnitude_equals_the_gradient_when_no_term_can_cancel():
+    """All weights, biases, inputs, directions and cotangents positive with the square
+    activation (s, s', s'' >= 0 on z > 0): every term of every element is >= 0, so M = |g|
+    exactly. A dropped or sign-flipped term in M breaks this equality."""
+    rng = np.random.default_rng(0)
+    Ws = [np.abs(rng.standard_normal((6, 3))), np.abs(rng.standard_normal((5, 6))), np.abs(rng.standard_normal((1, 5)))]
+    bs = [np.abs(rng.standard_normal(6)), np.abs(rng.standard_normal(5)), np.abs(rng.standard_normal(1))]
+    X = np.abs(rng.standard_normal((4, 3)))
+    dirs = np.abs(rng.standard_normal((2, 3)))
+    gop, gf = np.abs(rng.standard_normal(4)), np.abs(rng.standard_normal(4))
+    _, _, dW, db = OG.k2_grad(Ws, bs, X, dirs, np.ones(2), gop, gf, act="square")
+    MW, Mb = OG.k2_grad_magnitude(Ws, bs, X, dirs, np.ones(2), gop, gf, act="square")
+    for g, m in zip(dW + db, MW + Mb):
+        np.testing.assert_allclose(m, np.abs(g), rtol=1e-13, atol=0)
+        assert np.all(m > 0)
+
+
+def test_gradient_magnitude_is_homogeneous_in_the_cotangents():
+    D = 3
+    Ws, bs = random_params([D, 8, 6, 1], 4)
+    X = _pts(5, D, seed=2)
+    gop, gf = np.linspace(-1, 1, 5), np.linspace(0.3, -0.7, 5)
+    a = OG.k2_grad_magnitude(Ws, bs, X, np.eye(D), np.ones(D), gop, gf)
+    b = OG.k2_grad_magnitude(Ws, bs, X, np.eye(D), np.ones(D), -2.5 * gop, -2.5 * gf)
+    for x, y in zip(a[0] + a[1], b[0] + b[1]):
+        np.testing.assert_allclose(y, 2.5 * np.asarray(x), rtol=1e-13)
