@@ -211,7 +211,7 @@ def cpu_model():
     return None
 
 
-def cpu_baseline(D, widths, op, S):
+def cpu_baseline(D, widths, op, S, flop_pt=None):
     """the oracle on the box's host cores: vanilla fp64 O1 (the headline
     cpu_baseline value) and collapsed fp64 O3 (the same schedule as the GPU) on all cores,
     O1 on one thread, with the CPU model; about 20 s of CPU work in all."""
@@ -230,6 +230,12 @@ def cpu_baseline(D, widths, op, S):
     finally:
         O.set_num_threads(nthr)
     out["single_thread"] = {"value": r1, "sample": f"{M1} points, {dt1:.1f} s, O1, 1 thread"}
+    if flop_pt:  # achieved fp64 GFLOP/s at the method's useful flop count per point
+        out["useful_mflop_per_point"] = flop_pt / 1e6
+        out["useful_gflops"] = rate * flop_pt / 1e9
+        if "o3_collapsed" in out:
+            out["o3_collapsed"]["useful_gflops"] = out["o3_collapsed"]["value"] * flop_pt / 1e9
+        out["single_thread"]["useful_gflops"] = r1 * flop_pt / 1e9
     return out
 
 
@@ -597,7 +603,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(D, widths, args.op, args.S)
+        flop_pt = prof["layer"]["work"] / (args.steps * N) if prof["layer"]["work"] > 0 else None
+        cpu = cpu_baseline(D, widths, args.op, args.S, flop_pt)
 
     if rank == 0:
         line = {
