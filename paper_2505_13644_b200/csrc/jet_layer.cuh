@@ -47,10 +47,15 @@ constexpr uint32_t kSwLayout = 2, kSwSBO = 1024;
 // The operand ring holds SLOTS of one bf16 plane of A and the same plane of B for one
 // K block (kBK). A K step of the fp32 mode's first phase needs three slots (all planes), of
 // its second phase one slot (p0 again), of the fast mode two slots.
-constexpr int kSlots = 6;                        // 6 x 32 KB ring
 constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
+#ifdef CTM_EXP_RING7  // experiment: 7 slots of 29 KB (valid for MMA N <= 208 only: C1)
+constexpr int kSlots = 7;
+constexpr int kBTileBytes = 104 * kBK * 2;
+#else
+constexpr int kSlots = 6;                        // 6 x 32 KB ring
 constexpr int kBTileBytes = (kMaxN / 2) * kBK * 2;  // 16 KB: a CTA of the pair stages half of B
+#endif
 constexpr int kSlotBytes = kATileBytes + kBTileBytes;
 constexpr int kStageBytes = kSlotBytes;          // (ring bytes = kSlots * kSlotBytes)
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128

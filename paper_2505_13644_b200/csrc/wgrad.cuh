@@ -27,7 +27,9 @@
 namespace ctm {
 
 constexpr int kWgChunkKB = 16;   // 64-row K blocks per TMEM accumulation chunk (1024 rows)
-constexpr int kWgradSmem = kSlots * kSlotBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kWgSlots = 6;                     // 6 x 32 KB operand ring (plane slots, as jet_layer.cuh)
+constexpr int kWgSlotBytes = 32 * 1024;
+constexpr int kWgradSmem = kWgSlots * kWgSlotBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 struct WgradParams {
   int64_t rows;        // K: slot rows
@@ -48,13 +50,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   constexpr int kHalfN = N / 2;                         // B columns staged by each CTA
   constexpr uint32_t kABytes = 128 * 64 * 2;            // 128 o x 64 rows (two 64-o atoms)
   constexpr uint32_t kBBytes = kHalfN * 64 * 2;         // N/2 i x 64 rows
-  constexpr uint32_t kSlot = kSlotBytes;                // 32 KB ring slots (jet_layer.cuh)
+  constexpr uint32_t kSlot = kWgSlotBytes;
   static_assert(kABytes + kBBytes <= (uint32_t)kSlot, "slot size");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kSlots * kSlot);
-  uint64_t* empty_bar = full_bar + kSlots;
-  uint64_t* tmem_full_bar = empty_bar + kSlots;   // [2]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kWgSlots * kSlot);
+  uint64_t* empty_bar = full_bar + kWgSlots;
+  uint64_t* tmem_full_bar = empty_bar + kWgSlots;   // [2]
   uint64_t* tmem_empty_bar = tmem_full_bar + 2;    // [2] (leader)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
 
@@ -68,7 +70,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmZ);
     ptx::tma_prefetch_desc(&tmB);
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < kWgSlots; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
@@ -110,8 +112,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           for_each_group(p.nplanes, nkb, [&](int, int kb, int nslots) {
             const int r0 = (c0 + kb) * 64;
             for (int pl = 0; pl < nslots; ++pl, ++it) {
-              const uint32_t s = it % kSlots;
-              ptx::mbar_wait(&empty_bar[s], ((it / kSlots) & 1u) ^ 1u);
+              const uint32_t s = it % kWgSlots;
+              ptx::mbar_wait(&empty_bar[s], ((it / kWgSlots) & 1u) ^ 1u);
               uint8_t* st = smem + s * kSlot;
               if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * (kABytes + kBBytes));
               ptx::tma_load_3d_pair(st, &tmZ, &full_bar[s], o0, r0, pl);
@@ -143,10 +145,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           uint32_t acc = 0;
           for_each_group(p.nplanes, nkb, [&](int, int, int nslots) {
             for (int pl = 0; pl < nslots; ++pl)
-              ptx::mbar_wait(&full_bar[(it + pl) % kSlots], ((it + pl) / kSlots) & 1u);
+              ptx::mbar_wait(&full_bar[(it + pl) % kWgSlots], ((it + pl) / kWgSlots) & 1u);
             ptx::tc_fence_after();
-            const uint64_t dA0 = desc0 + (it % kSlots) * kS, dA1 = desc0 + ((it + 1) % kSlots) * kS,
-                           dA2 = desc0 + ((it + 2) % kSlots) * kS;
+            const uint64_t dA0 = desc0 + (it % kWgSlots) * kS, dA1 = desc0 + ((it + 1) % kWgSlots) * kS,
+                           dA2 = desc0 + ((it + 2) % kWgSlots) * kS;
             if (ptx::elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {  // 16 rows = 2 K groups of 8 rows = 2048 bytes
@@ -166,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                 }
                 acc = 1u;
               }
-              for (int pl = 0; pl < nslots; ++pl) ptx::mma_commit_pair(&empty_bar[(it + pl) % kSlots]);
+              for (int pl = 0; pl < nslots; ++pl) ptx::mma_commit_pair(&empty_bar[(it + pl) % kWgSlots]);
             }
             __syncwarp();
             acc = 1u;
