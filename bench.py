@@ -7,7 +7,7 @@ config C1 = exact Laplacian of the tanh MLP 50-768-768-512-512-1 on
 N = 16384 points per GPU, in the library's default fp32 mode.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--scaling weak|strong] [--precision fp32|bf16x3] [--op ...]
+                    [--scaling weak|strong] [--precision fp32|fp16x3|bf16x3] [--op ...]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Scaling: "weak" (default) = every rank evaluates its own N points
@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--direction-block", type=int, default=0,
                     help="directions per block (ctm_set_direction_block); 0 = the library's planner")
-    ap.add_argument("--precision", choices=["fp32", "bf16x3"], default="fp32",
+    ap.add_argument("--precision", choices=["fp32", "fp16x3", "bf16x3"], default="fp32",
                     help="layer-contraction arithmetic (ctm_set_precision, DESIGN.md §5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
@@ -342,7 +342,8 @@ def main():
     mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=local)
     mlp.set_direction_block(args.direction_block)
     mlp.set_precision(args.precision)
-    prods = 6 if args.precision == "fp32" else 3  # bf16 tensor products per useful product
+    prods = 6 if args.precision == "fp32" else 3  # tensor products per useful product (after the
+    # warm-up: the arithmetic the calls actually ran in, an fp16x3 handle runs uncovered calls in fp32)
     # each rank: its own contiguous slice of the global point set (global index offset ...)
     X_host = points(n_glob, D, 1)[offset:offset + N]
     X = torch.from_numpy(X_host).to(dev)
@@ -419,6 +420,10 @@ def main():
     if train:
         mlp.laplacian(X, out=op_out, f_out=f_out)  # plan of the forward
     plan = mlp.last_plan()
+    ran = "fp32" if train else mlp.last_precision()  # training runs the fp32 mode in every precision but bf16x3
+    if train and args.precision == "bf16x3":
+        ran = "bf16x3"
+    prods = 6 if ran == "fp32" else 3
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -553,7 +558,8 @@ def main():
     dom = max(("layer", "bwd", "wgrad"), key=lambda k: prof[k]["ms"]) if train else "layer"
     lay = prof[dom]
     achieved = lay["work"] / (lay["ms"] / 1e3) / 1e12 if lay["ms"] > 0 else None
-    mode = "bf16x6 (three planes, fp32 mode)" if prods == 6 else "3xBF16 (two planes, fast mode)"
+    mode = {"fp32": "bf16x6 (three planes, fp32 mode)", "fp16x3": "fp16x3 (two scaled fp16 planes, 3xTF32-class)",
+            "bf16x3": "3xBF16 (two planes, fast mode)"}[ran]
     kernel_name = {
         "layer": f"jet_layer_kernel (hidden layers: tcgen05 {mode} GEMM + tanh Taylor epilogue)",
         "bwd": f"jet_layer_kernel<kBwd2> (adjoint layers: tcgen05 {mode} W^T GEMM + transposed Taylor rule)",
@@ -615,10 +621,12 @@ def main():
             "vs_baseline": (value / PAPER_PTS_PER_S[args.op]) if args.op in PAPER_PTS_PER_S else None,
             "vs_baseline_ref": ("paper P:1205, marginal ms/datum on an RTX 6000, PyTorch (another machine: context)"
                                 if args.op in PAPER_PTS_PER_S else "no published number for this operator"),
-            "dtype": ("f32 (bf16x6: three bf16 planes per operand, six tensor products, fp32 accumulate)"
-                      if args.precision == "fp32" else "f32 storage, bf16x3 products (~17-bit operands, fp32 accumulate)"),
+            "dtype": {"fp32": "f32 (bf16x6: three bf16 planes per operand, six tensor products, fp32 accumulate)",
+                      "fp16x3": "f32 (fp16x3: two power-of-two-scaled fp16 planes per operand = 22-bit operands as "
+                                "in 3xTF32, three tensor products, fp32 accumulate)",
+                      "bf16x3": "f32 storage, bf16x3 products (~17-bit operands, fp32 accumulate)"}[ran],
             "data": "synthetic",
-            "config": {"workload": wl, "op": args.op, "precision": args.precision,
+            "config": {"workload": wl, "op": args.op, "precision": args.precision, "precision_ran": ran,
                        "N_per_gpu": N, "N_total": n_glob, "D": D, "widths": widths,
                        "slots_per_point": plan["slots_per_point"], "points_per_tile": plan["points_per_tile"],
                        "mma_n": plan["mma_n"], "direction_blocks": plan["blocks"],

@@ -177,9 +177,19 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
  *     p0*p0 over the whole K, fp32 accumulation in TMEM: fp32-class error.
  *   CTM_PRECISION_BF16X3: two planes, p1*p0 + p0*p1 + p0*p0 per K step ("3xBF16",
  *     ~17 operand bits): about half the tensor time, ~2^-16 per product.
+ *   CTM_PRECISION_FP16X3: two fp16 planes (11 + 11 significant bits, the operand split of
+ *     3xTF32) of power-of-two scaled values: weights per layer, slot blocks per slot type
+ *     (primal / first order / collapsed top) from a rigorous bound on the block's values
+ *     (the previous block's recorded max |value| and ||W||_inf), so no plane overflows;
+ *     p1*p0 + p0*p1 over the whole K, then p0*p0: three products, ~2^-21 per product, the
+ *     tensor time and energy of BF16X3. Covers the K=2 collapsed forward
+ *     operators (laplacian, weighted, randomized without sigma, sigma(x), K=2 directional
+ *     sums) of tanh and sin nets with at least two points per MMA tile; other calls on an
+ *     FP16X3 handle (K=4, nested, standard modes, grad mode, other activations) run in
+ *     CTM_PRECISION_FP32.
  * Changing the precision invalidates a recorded tape (ctm_backward then fails).
  * Errors: CTM_EINVAL (NULL handle, unknown value). */
-typedef enum { CTM_PRECISION_FP32 = 0, CTM_PRECISION_BF16X3 = 1 } ctm_precision;
+typedef enum { CTM_PRECISION_FP32 = 0, CTM_PRECISION_BF16X3 = 1, CTM_PRECISION_FP16X3 = 2 } ctm_precision;
 ctm_status ctm_set_precision(ctm_mlp_t mlp, ctm_precision prec);
 
 /* Weighted Laplacian with a point-dependent sigma (Eq. 10; "sigma can depend on x0",
@@ -272,6 +282,11 @@ ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t *launches, int32_t *slots_per_po
  * jets) per block; slots_per_point of ctm_last_plan is the slot count of ONE block.
  * HOST-side. */
 ctm_status ctm_last_blocks(ctm_mlp_t mlp, int32_t *blocks, int32_t *per_block);
+
+/* The arithmetic the last operator call ran in (a ctm_precision value; an FP16X3 handle
+ * runs the calls its mode does not cover in CTM_PRECISION_FP32, see ctm_set_precision).
+ * HOST-side. CTM_EINVAL for a NULL handle or output. */
+ctm_status ctm_last_precision(ctm_mlp_t mlp, int32_t *precision);
 
 /* The planner itself (HOST-only, no device, no handle): for an operator of kind
  * order = 2 (collapsed K=2), 4 (collapsed K=4), 3 (standard K=2) or 5 (standard K=4) with R

@@ -51,6 +51,7 @@ ABI = {
     "ctm_backward": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP]),
     "ctm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "ctm_last_error": (ctypes.c_char_p, []),
+    "ctm_last_precision": (ctypes.c_int, [_VP, ctypes.POINTER(_I32)]),
     "ctm_last_plan": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                                      ctypes.POINTER(_I32)]),
     "ctm_last_blocks": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
@@ -134,7 +135,7 @@ def plan_blocks(order: int, R: int, forced_rb: int = 0) -> dict:
 
 
 ACTIVATIONS = {"tanh": 0, "identity": 1, "square": 2, "sin": 3, "exp": 4}  # ctm_activation
-PRECISIONS = {"fp32": 0, "bf16x3": 1}  # ctm_precision
+PRECISIONS = {"fp32": 0, "bf16x3": 1, "fp16x3": 2}  # ctm_precision
 
 
 class MLP:
@@ -146,7 +147,7 @@ class MLP:
     """
 
     def __init__(self, params: Sequence, device: int | str | torch.device | None = None, act: str = "tanh",
-                 precision: str = "fp32"):
+                 precision: str | None = None):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
@@ -169,13 +170,16 @@ class MLP:
         self.act = act
         self._grad = False
         self._tape_n = None
-        self.set_precision(precision)
+        # the environment may choose the default arithmetic of new handles (CTM_PRECISION)
+        self.set_precision(precision or os.environ.get("CTM_PRECISION", "fp32"))
 
     def set_precision(self, precision: str = "fp32"):
         """Arithmetic of the layer contractions (ctm_set_precision): "fp32" (default, three
-        bf16 planes, six products) or "bf16x3" (two planes, three products, ~2x faster)."""
+        bf16 planes, six products), "fp16x3" (two scaled fp16 planes, three products: the
+        3xTF32 operand split at bf16 speed, K=2 forward operators; others run fp32) or
+        "bf16x3" (two bf16 planes, three products, ~17 bits)."""
         if precision not in PRECISIONS:
-            raise CTMError(f"unknown precision {precision!r} (fp32 or bf16x3)")
+            raise CTMError(f"unknown precision {precision!r} (fp32, fp16x3 or bf16x3)")
         _check(lib().ctm_set_precision(self._h, PRECISIONS[precision]), "ctm_set_precision")
         self.precision = precision
         self._tape_n = None
@@ -388,6 +392,12 @@ class MLP:
         _check(lib().ctm_gemm_probe(self._h, int(layer), B.data_ptr(), B.shape[0], Z.data_ptr(),
                                     _stream_ptr(stream, self.device)), "ctm_gemm_probe")
         return Z
+
+    def last_precision(self) -> str:
+        """The arithmetic the last operator call ran in (ctm_last_precision)."""
+        v = _I32()
+        _check(lib().ctm_last_precision(self._h, ctypes.byref(v)), "ctm_last_precision")
+        return {c: k for k, c in PRECISIONS.items()}[v.value]
 
     def last_plan(self) -> dict:
         a, b, c, d = _I32(), _I32(), _I32(), _I32()

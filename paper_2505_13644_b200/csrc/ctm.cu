@@ -104,14 +104,31 @@ struct ctm_mlp {
   int act = ctm::kActTanh;    // hidden-layer activation (ctm_set_activation)
   int sm_count = 148;
   bool seed_fixed_attr = false;  // max dynamic smem of the seed_fixed_kernel instances set
+  bool seed_f16_attr = false;
   int L = 0;                  // affine layers
   std::vector<int> widths;    // L + 1
   std::vector<int> wpad;      // hidden widths padded to 128 (index = layer)
   // layer 1
   float* W1T = nullptr;       // [D, wpad[1]]
   float* b1 = nullptr;        // [wpad[1]]
-  // operand precision (ctm_set_precision): 3 planes = fp32 mode, 2 planes = fast 3xBF16
+  // operand precision (ctm_set_precision): 3 planes = fp32 mode, 2 planes = fast 3xBF16 or
+  // (f16) the fp16x3 mode; nplanes is the plane count of the current call (an fp16x3 handle
+  // runs the operators it does not cover in the fp32 mode, see f16_covers)
   int nplanes = 3;
+  int prec = 0;               // ctm_precision of the handle
+  bool cur_f16 = false;       // this call runs in the fp16x3 mode
+  // fp16x3 mode: fp16 weight planes [3][Mpad, Kpad] with per-layer power-of-two scales
+  // (seed.cuh split_weights_f16_kernel), their statistics f16w[2 l] = 2^-(sa+11) (the
+  // accumulator's weight factor), f16w[2 l + 1] = ||W_l||_inf (l = 1 .. L-1; layer 1 = W1p),
+  // one scale record per slot block of a call (f16rec[l]: the output of layer l, [0] the
+  // layer-1 input block of per-point directions), and bound scratch f16b[4]
+  uint16_t* W1p16 = nullptr;
+  CUtensorMap mapA1_16;
+  std::vector<uint16_t*> Wp16;
+  std::vector<CUtensorMap> mapA16;
+  float* f16w = nullptr;
+  ctm::F16Rec* f16rec = nullptr;
+  unsigned* f16b = nullptr;
   // layer 1 as a tensor-core layer (randomized directions): bf16 planes [3][wpad[1], k1pad]
   int k1pad = 0;
   uint16_t* W1p = nullptr;
@@ -149,7 +166,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0, last_nb = 1, last_rb = 0;
-  bool smem_attr_set[128] = {};  // per (KORD, FLAGS) kernel instance
+  bool smem_attr_set[256] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
   std::vector<uint16_t*> WTp;               // W_l^T bf16 planes [3][wpad[l-1], wpad[l]], l = 2..L-1
@@ -202,6 +219,8 @@ ctm_status free_all(ctm_mlp* h) {
   F(h->probe_in.p); F(h->probe_out.p); F(h->probe_z);
   F(h->partial);
   for (auto& p : h->WTp) F(p);
+  F(h->W1p16); F(h->f16w); F(h->f16rec); F(h->f16b);
+  for (auto& p : h->Wp16) F(p);
   F(h->eye);
   F(h->tape.weights); F(h->tape.part); F(h->tape.wpart);
   for (auto& p : h->tape.B) F(p.p);
@@ -322,18 +341,18 @@ struct ProfScope {
 // cudaFuncSetAttribute is per device: tracked per handle (a handle lives on one device)
 template <int KORD, int FLAGS = 0>
 ctm_status set_layer_attr(ctm_mlp* h) {
-  static_assert(KORD < 8 && FLAGS < 16, "smem_attr_set index");
-  if (!h->smem_attr_set[KORD * 16 + FLAGS]) {
+  static_assert(KORD < 8 && FLAGS < 32, "smem_attr_set index");
+  if (!h->smem_attr_set[KORD * 32 + FLAGS]) {
     CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD, FLAGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctm::kLayerSmem));
-    h->smem_attr_set[KORD * 16 + FLAGS] = true;
+    h->smem_attr_set[KORD * 32 + FLAGS] = true;
   }
   return CTM_OK;
 }
 
 template <int KORD, int FLAGS>
 ctm_status launch_layer_instance(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
-                                 const ctm::LayerParams& lp, cudaStream_t st) {
+                                 const ctm::LayerParams& lp, cudaStream_t st, const ctm::F16Args& fa) {
   ctm_status s = set_layer_attr<KORD, FLAGS>(h);
   if (s != CTM_OK) return s;
   // programmatic dependent launch: the prologue (barriers, TMEM allocation, descriptor
@@ -348,16 +367,21 @@ ctm_status launch_layer_instance(ctm_mlp* h, int64_t grid, const CUtensorMap& am
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::jet_layer_kernel<KORD, FLAGS>, amap, bmap, lp));
+  CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::jet_layer_kernel<KORD, FLAGS>, amap, bmap, lp, fa));
   return CTM_OK;
 }
 
 // the instance with the handle's plane count (lp.nplanes) as a compile-time constant
+// (fa.wsc set: the fp16x3 instance, K=2 forward only)
 template <int KORD, int FLAGS>
 ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
-                               const ctm::LayerParams& lp, cudaStream_t st) {
-  if (lp.nplanes == 2) return launch_layer_instance<KORD, FLAGS | ctm::kFlagNP2>(h, grid, amap, bmap, lp, st);
-  return launch_layer_instance<KORD, FLAGS>(h, grid, amap, bmap, lp, st);
+                               const ctm::LayerParams& lp, cudaStream_t st, const ctm::F16Args& fa = {}) {
+  if constexpr (KORD == 2 && (FLAGS & ctm::kFlagSaveZ) == 0) {
+    if (fa.wsc) return launch_layer_instance<KORD, FLAGS | ctm::kFlagF16>(h, grid, amap, bmap, lp, st, fa);
+  }
+  if (fa.wsc) return fail(CTM_EUNSUPPORTED, "fp16x3: K=2 forward layers only");
+  if (lp.nplanes == 2) return launch_layer_instance<KORD, FLAGS | ctm::kFlagNP2>(h, grid, amap, bmap, lp, st, fa);
+  return launch_layer_instance<KORD, FLAGS>(h, grid, amap, bmap, lp, st, fa);
 }
 
 // Tile plan of one operator call. A point's R directions (K=4: jets) are split into nb
@@ -478,6 +502,8 @@ struct GemmLayer {
   const CUtensorMap* amap;
   const float* bias;
   int kpad, mpad, w_in, w_out;
+  const CUtensorMap* amap16;  // fp16x3 weight planes
+  int lidx;                   // network layer index (1 .. L-1)
 };
 
 // grad mode: where a layer writes its output block and its pre-activations
@@ -486,7 +512,24 @@ struct LayerIO {
   float* z;
 };
 
+// sup |s|, |s'|, |s''| of the activations the fp16x3 mode covers (tanh: |tanh''| <= 4/(3 sqrt 3))
+void f16_act_sups(int act, float& s0, float& s1, float& s2) {
+  s0 = 1.f;
+  s1 = 1.f;
+  s2 = (act == ctm::kActTanh) ? 0.7699f : 1.f;
+}
+
+// max |a| over n floats into the bound record out (zeroed at the start of the call)
+void launch_maxabs(const float* a, int64_t n, unsigned* out, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>(1184, (n + 255) / 256);
+  if (blocks > 0) ctm::maxabs_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, n, out);
+}
+
 void launch_seed_random(int nplanes, int64_t N, const ctm::SeedRandomParams& rp, cudaStream_t st) {
+  if (rp.f16_out) {
+    ctm::seed_random_kernel<2, true><<<(unsigned)N, ctm::kSeedThreads, 0, st>>>(rp);
+    return;
+  }
   if (nplanes == 3)
     ctm::seed_random_kernel<3><<<(unsigned)N, ctm::kSeedThreads, 0, st>>>(rp);
   else
@@ -562,13 +605,27 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
                                       (int)kFixedSmemMax));
         h->seed_fixed_attr = true;
       }
+      if (h->cur_f16) {  // fp16x3: bounds of this call's direction images, output record of layer 1
+        if (!h->seed_f16_attr) {
+          CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<2, 2, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixedSmemMax));
+          h->seed_f16_attr = true;
+        }
+        launch_maxabs(UT, (int64_t)R * ld1, h->f16b, st);
+        launch_maxabs(csum, (int64_t)pl.nb * ld1, h->f16b + 1, st);
+        launches += 2;
+        sp.f16_bounds = h->f16b;
+        f16_act_sups(h->act, sp.s0, sp.s1, sp.s2);
+        sp.f16_out = h->f16rec + 1;
+      }
       // one wave: as many blocks as are resident at once (registers, shared memory)
       const int slices = ld1 / ctm::kSeedFixedFeats;
       const int thr = ctm::kSeedFixedWarps * 32;
       int per_sm = 1;
       CTM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm,
-          h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3> : ctm::seed_fixed_kernel<2, 2>,
+          h->cur_f16 ? ctm::seed_fixed_kernel<2, 2, true>
+                     : (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3> : ctm::seed_fixed_kernel<2, 2>),
           thr, fsm));
       const int64_t want = std::max<int64_t>(1, (int64_t)h->sm_count * std::max(per_sm, 1) / slices);
       const int64_t groups0 = std::min<int64_t>(want, (n + ctm::kSeedFixedWarps - 1) / ctm::kSeedFixedWarps);
@@ -576,8 +633,11 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
       const int64_t groups = (n + ppg - 1) / ppg;
       if (groups > 65535) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
       const dim3 grid((unsigned)slices, (unsigned)groups);
-      (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3><<<grid, thr, fsm, st>>>(sp, ppg)
-                       : ctm::seed_fixed_kernel<2, 2><<<grid, thr, fsm, st>>>(sp, ppg));
+      if (h->cur_f16)
+        ctm::seed_fixed_kernel<2, 2, true><<<grid, thr, fsm, st>>>(sp, ppg);
+      else
+        (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3><<<grid, thr, fsm, st>>>(sp, ppg)
+                         : ctm::seed_fixed_kernel<2, 2><<<grid, thr, fsm, st>>>(sp, ppg));
       ++launches;
       return CTM_OK;
     }
@@ -673,15 +733,25 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       ctm_status s;
       int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
       if (KORD == 2 && flags == 0 && pl.ppt >= 8) flags = ctm::kFlagWide;
+      ctm::F16Args fa{};
+      const CUtensorMap* am = gl.amap;
+      if (h->cur_f16) {  // fp16x3: this layer's weight planes, its input and output block records
+        fa.in = h->f16rec + (gl.lidx - 1);
+        fa.out = last ? nullptr : h->f16rec + gl.lidx;
+        fa.wsc = h->f16w + 2 * gl.lidx;
+        f16_act_sups(h->act, fa.s0, fa.s1, fa.s2);
+        fa.rw = lp.weighted ? -1.f : (float)std::max(pl.rb, 1);
+        am = gl.amap16;
+      }
       if (KORD == 2) {
         switch (flags) {
           case ctm::kFlagWide:
-            s = launch_layer_kernel<2, ctm::kFlagWide>(h, grid, *gl.amap, mb, lp, st);
+            s = launch_layer_kernel<2, ctm::kFlagWide>(h, grid, *am, mb, lp, st, fa);
             break;
-          case 0: s = launch_layer_kernel<2, 0>(h, grid, *gl.amap, mb, lp, st); break;
-          case 1: s = launch_layer_kernel<2, 1>(h, grid, *gl.amap, mb, lp, st); break;
-          case 2: s = launch_layer_kernel<2, 2>(h, grid, *gl.amap, mb, lp, st); break;
-          default: s = launch_layer_kernel<2, 3>(h, grid, *gl.amap, mb, lp, st); break;
+          case 0: s = launch_layer_kernel<2, 0>(h, grid, *am, mb, lp, st, fa); break;
+          case 1: s = launch_layer_kernel<2, 1>(h, grid, *am, mb, lp, st, fa); break;
+          case 2: s = launch_layer_kernel<2, 2>(h, grid, *am, mb, lp, st, fa); break;
+          default: s = launch_layer_kernel<2, 3>(h, grid, *am, mb, lp, st, fa); break;
         }
       } else if (KORD == 4) {
         s = launch_layer_kernel<4, 0>(h, grid, *gl.amap, mb, lp, st);
@@ -742,6 +812,20 @@ ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
   return CTM_OK;
 }
 
+// the calls the fp16x3 mode covers (include/ctm.h ctm_set_precision): K=2 collapsed forward
+// operators of tanh / sin nets, random directions without sigma, >= 2 points per tile (no
+// split point), the streaming seed for fixed sets, and at least one tensor-core layer
+bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, bool grad, int R) {
+  if (h->prec != CTM_PRECISION_FP16X3 || grad || KORD != 2 || pl.ppt < 2) return false;
+  if (h->act != ctm::kActTanh && h->act != ctm::kActSin) return false;
+  const bool k2op = a.op == OP_LAP || a.op == OP_WLAP || a.op == OP_RLAP || a.op == OP_WLAP_X ||
+                    (a.op == OP_DSUM && a.K == 2);
+  if (!k2op) return false;
+  if (random_k2(a)) return a.sigma == nullptr;
+  const int D = h->widths[0], ld1 = h->wpad[1];
+  return h->L >= 3 && ctm::seed_fixed_smem(D, R, pl.nb) <= 200 * 1024 && ld1 % ctm::kSeedFixedFeats == 0;
+}
+
 ctm_status run(ctm_mlp* h, const CallArgs& a) {
   const int D = h->widths[0];
   const int ld1 = h->wpad[1];
@@ -771,6 +855,9 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     return fail(CTM_EUNSUPPORTED, "S * D > 12288 for per-point K=4 directions");
   if ((KORD == 4 || KORD == ctm::kStd4 || a.op == OP_DSUM) && (int64_t)pl.nb * pl.rb > ctm::kMaxW)
     return fail(CTM_EUNSUPPORTED, "more than 2048 weighted directions (jets) per point");
+  // arithmetic of this call: an fp16x3 handle runs what the mode does not cover in fp32 mode
+  h->cur_f16 = f16_covers(h, a, KORD, pl, grad, R);
+  h->nplanes = (h->prec == CTM_PRECISION_BF16X3 || h->cur_f16) ? 2 : 3;
   const int P = pl.P;
   h->last_P = pl.P;
   h->last_ppt = pl.ppt;
@@ -794,6 +881,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   cudaStream_t st = a.stream;
   int launches = 0;
   ctm_status s;
+  if (h->cur_f16) {  // fresh scale records and bound scratch for this call
+    CTM_CUDA(cudaMemsetAsync(h->f16rec, 0, sizeof(ctm::F16Rec) * (h->L + 1), st));
+    CTM_CUDA(cudaMemsetAsync(h->f16b, 0, sizeof(unsigned) * 4, st));
+  }
   // grad mode: record the tape of this call (differentiable operators only)
   std::vector<LayerIO> io;
   if (grad) {
@@ -807,9 +898,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
 
   // GEMM layers: layer 1 for per-point K=2 directions, then the hidden layers 2..L-1
   std::vector<GemmLayer> layers;
-  if (random_k2(a)) layers.push_back({&h->mapA1, h->b1, h->k1pad, ld1, D, h->widths[1]});
+  if (random_k2(a)) layers.push_back({&h->mapA1, h->b1, h->k1pad, ld1, D, h->widths[1], &h->mapA1_16, 1});
   for (int l = 2; l <= h->L - 1; ++l)
-    layers.push_back({&h->mapA[l - 2], h->bias[l - 2], h->wpad[l - 1], h->wpad[l], h->widths[l - 1], h->widths[l]});
+    layers.push_back({&h->mapA[l - 2], h->bias[l - 2], h->wpad[l - 1], h->wpad[l], h->widths[l - 1], h->widths[l],
+                      &h->mapA16[l - 2], l});
 
   if (random_k2(a)) {
     // per-point K=2 directions: the input block [x0; u_1..u_S; 0], then layer 1 on the
@@ -835,6 +927,17 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.out = b0.p;
     rp.pstride = (int64_t)b0.cap;
     rp.nplanes = h->nplanes;
+    if (h->cur_f16) {  // fp16x3: bounds of x0 and of explicit directions; the input block's record
+      launch_maxabs(a.X, a.N * (int64_t)D, h->f16b, st);
+      ++launches;
+      if (a.V) {
+        launch_maxabs(a.V, a.N * (int64_t)a.S * a.Rv, h->f16b + 1, st);
+        ++launches;
+      }
+      rp.f16_bounds = h->f16b;
+      rp.vgen = a.gaussian ? 6.f : 1.f;  // |Box-Muller draw| <= sqrt(-2 ln 2^-25) = 5.9
+      rp.f16_out = h->f16rec;
+    }
     {
       ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 2.0 * h->nplanes, st);
       launch_seed_random(h->nplanes, a.N, rp, st);
@@ -1138,6 +1241,17 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
     const int64_t n = (int64_t)ld1 * h->k1pad;
     ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], b[0], h->widths[1], D, ld1, h->k1pad,
                                                                            h->W1p, h->b1);
+    // fp16x3: scale and ||W1||_inf, then the fp16 planes of W1 * 2^sa
+    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(W[0], h->widths[1], D, h->f16w + 2);
+    ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], h->widths[1], D, ld1, h->k1pad,
+                                                                               h->f16w + 2, h->W1p16);
+  }
+  for (int l = 2; l <= L - 1; ++l) {
+    const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
+    const int64_t n = (int64_t)mpad * kpad;
+    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(W[l - 1], h->widths[l], h->widths[l - 1], h->f16w + 2 * l);
+    ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        W[l - 1], h->widths[l], h->widths[l - 1], mpad, kpad, h->f16w + 2 * l, h->Wp16[l - 2]);
   }
   for (int l = 2; l <= L - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
@@ -1157,7 +1271,7 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
   if (h->J_bih)
     ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->bih_dirs, h->J_bih, h->w_bih, 4,
                                                                    h->U_bih, h->c_bih);
-  h->last_launches = 4 + (L - 2) * (h->WTp.empty() ? 1 : 2) + (h->J_bih ? 1 : 0);
+  h->last_launches = 4 + (L - 2) * (h->WTp.empty() ? 1 : 2) + (h->J_bih ? 1 : 0) + 2 * (L - 1);
   h->tape.valid = false;
 }
 
@@ -1255,6 +1369,28 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
       return bail(CTM_ECUDA);
     }
     h->mapA.push_back(mw);
+  }
+  {  // fp16x3 mode: fp16 weight planes, their statistics, the per-call scale records
+    LOAD_CUDA(cudaMalloc(&h->W1p16, 3 * sizeof(uint16_t) * (size_t)ld1 * h->k1pad));
+    if (!make_map3(&h->mapA1_16, h->W1p16, h->k1pad, ld1, (uint64_t)ld1 * h->k1pad, ctm::kBM)) {
+      fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W1 (fp16)");
+      return bail(CTM_ECUDA);
+    }
+    for (int l = 2; l <= n_layers - 1; ++l) {
+      const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
+      uint16_t* wp;
+      LOAD_CUDA(cudaMalloc(&wp, 3 * sizeof(uint16_t) * (size_t)mpad * kpad));
+      h->Wp16.push_back(wp);
+      CUtensorMap mw;
+      if (!make_map3(&mw, wp, kpad, mpad, (uint64_t)mpad * kpad, ctm::kBM)) {
+        fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for weights (fp16)");
+        return bail(CTM_ECUDA);
+      }
+      h->mapA16.push_back(mw);
+    }
+    LOAD_CUDA(cudaMalloc(&h->f16w, sizeof(float) * 2 * (n_layers + 1)));
+    LOAD_CUDA(cudaMalloc(&h->f16rec, sizeof(ctm::F16Rec) * (n_layers + 1)));
+    LOAD_CUDA(cudaMalloc(&h->f16b, sizeof(unsigned) * 4));
   }
   LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * h->wpad[n_layers - 1]));
   LOAD_CUDA(cudaMalloc(&h->b_out, sizeof(float)));
@@ -1454,7 +1590,9 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act) {
 ctm_status ctm_set_precision(ctm_mlp_t mlp, ctm_precision prec) {
   g_last_error.clear();
   if (!mlp) return fail(CTM_EINVAL, "NULL handle");
-  if (prec != CTM_PRECISION_FP32 && prec != CTM_PRECISION_BF16X3) return fail(CTM_EINVAL, "unknown precision");
+  if (prec != CTM_PRECISION_FP32 && prec != CTM_PRECISION_BF16X3 && prec != CTM_PRECISION_FP16X3)
+    return fail(CTM_EINVAL, "unknown precision");
+  mlp->prec = prec;
   mlp->nplanes = (prec == CTM_PRECISION_FP32) ? 3 : 2;
   mlp->tape.valid = false;
   return CTM_OK;
@@ -1547,14 +1685,31 @@ ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float* B, int64_t 
   if (s != CTM_OK) return s;
   s = ensure(h->probe_z, h->probe_z_elems, (size_t)rows_pad * mpad);
   if (s != CTM_OK) return s;
+  // the handle's precision (not the plane count of its last call)
+  const bool f16 = (h->prec == CTM_PRECISION_FP16X3);
+  h->nplanes = (h->prec == CTM_PRECISION_FP32) ? 3 : 2;
+  ctm::F16Args fa{};
   {
     const int64_t n = rows_pad * kpad;
-    if (h->nplanes == 3)
+    if (f16) {  // one scale for every slot type: that of the measured max |B|
+      CTM_CUDA(cudaMemsetAsync(h->f16rec, 0, sizeof(ctm::F16Rec) * 2, st));
+      CTM_CUDA(cudaMemsetAsync(h->f16b, 0, sizeof(unsigned) * 4, st));
+      launch_maxabs(B, rows * (int64_t)w_in, h->f16b, st);
+      ctm::probe_f16_record_kernel<<<1, 1, 0, st>>>(h->f16b, h->f16rec);
+      ctm::split_rows_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+          B, rows, w_in, rows_pad, kpad, h->f16rec, h->probe_in.p, (int64_t)h->probe_in.cap);
+      fa.in = h->f16rec;
+      fa.out = h->f16rec + 1;
+      fa.wsc = h->f16w + 2 * layer;
+      f16_act_sups(h->act, fa.s0, fa.s1, fa.s2);
+      fa.rw = (float)(P - 2);
+    } else if (h->nplanes == 3) {
       ctm::split_rows_kernel<3><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, rows, w_in, rows_pad, kpad,
                                                                             h->probe_in.p, (int64_t)h->probe_in.cap);
-    else
+    } else {
       ctm::split_rows_kernel<2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, rows, w_in, rows_pad, kpad,
                                                                             h->probe_in.p, (int64_t)h->probe_in.cap);
+    }
   }
   CUtensorMap mb;
   if (!make_map3(&mb, h->probe_in.p, (uint64_t)kpad, (uint64_t)rows_pad, h->probe_in.cap, 128))
@@ -1578,7 +1733,8 @@ ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float* B, int64_t 
   lp.rb = P - 2;
   const int64_t n_tiles = (lp.n_points + lp.pts_per_tile - 1) / lp.pts_per_tile;
   const int64_t grid = 2 * std::min<int64_t>(n_tiles * (lp.m_tiles / 2), h->sm_count / 2);
-  s = launch_layer_kernel<2, ctm::kFlagSaveZ>(h, grid, h->mapA[layer - 2], mb, lp, st);
+  s = f16 ? launch_layer_instance<2, ctm::kFlagSaveZ | ctm::kFlagF16>(h, grid, h->mapA16[layer - 2], mb, lp, st, fa)
+          : launch_layer_kernel<2, ctm::kFlagSaveZ>(h, grid, h->mapA[layer - 2], mb, lp, st);
   if (s != CTM_OK) return s;
   {
     const int64_t n = rows * (int64_t)w_out;
@@ -1681,6 +1837,12 @@ int ctm_debug_stats(unsigned long long* out, int reset) {  // experiment build o
   return 0;
 }
 #endif
+
+ctm_status ctm_last_precision(ctm_mlp_t mlp, int32_t* precision) {
+  if (!mlp || !precision) return fail(CTM_EINVAL, "NULL handle or output");
+  *precision = mlp->cur_f16 ? CTM_PRECISION_FP16X3 : (mlp->nplanes == 3 ? CTM_PRECISION_FP32 : CTM_PRECISION_BF16X3);
+  return CTM_OK;
+}
 
 ctm_status ctm_last_plan(ctm_mlp_t mlp, int32_t* launches, int32_t* slots_per_point, int32_t* points_per_tile,
                          int32_t* mma_n) {

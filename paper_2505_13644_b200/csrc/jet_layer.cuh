@@ -180,16 +180,66 @@ constexpr int kFlagWide = 4;
 // kFlagNP2: the fast mode's two operand planes (ctm_set_precision); without it three (the
 // fp32 mode). The plane count is a compile-time constant of every layer-kernel instance.
 constexpr int kFlagNP2 = 8;
+// kFlagF16 (K=2 only): the fp16x3 mode: two fp16 planes per operand with power-of-two scales
+// (weights per layer, slot blocks per slot type), products p1*p0 + p0*p1 over the whole K,
+// then p0*p0. Implies two planes.
+constexpr int kFlagF16 = 16;
 template <int FLAGS>
 __host__ __device__ constexpr int planes_of() {
-  return (FLAGS & kFlagNP2) ? 2 : 3;
+  return (FLAGS & (kFlagNP2 | kFlagF16)) ? 2 : 3;
+}
+
+// fp16x3 scale state of one slot block in device memory: the planes hold fp16 splits of
+// v * scale[t], t the slot type (0 primal, 1 first order, 2 collapsed top); the block's
+// producer records max |v| per type (float bits, atomicMax) for the next layer's bound.
+struct F16Rec {
+  float scale[3];
+  unsigned maxabs[3];
+};
+// per-launch fp16x3 arguments of a layer kernel (zero for the other modes)
+struct F16Args {
+  const F16Rec* in;   // the B operand's block
+  F16Rec* out;        // the output block, or nullptr (readout layer)
+  const float* wsc;   // [0] 2^-(sa+11): the weights' factor in the accumulator (seed.cuh split_weights_f16_kernel),
+                      // [1] ||W||_inf = max_m sum_k |W[m,k]|
+  float s0, s1, s2;   // sup |s|, |s'|, |s''| of the activation
+  float rw;           // sum_r |w_r| over one sub-point's directions (< 0: from the smem weights)
+};
+// the registers an fp16x3 epilogue thread carries: unscale factors of the accumulator per
+// slot type (2^-(sa+11) / scale_in[t]), scales of its output block, running max |output|
+struct F16Ctx {
+  float us[3];
+  float os[3];
+  float mx[3];
+};
+// output scale of a slot type from a bound B on |v|: 2^(14 - e), B = m 2^e, m in [0.5, 1), so
+// |v * scale| <= 2^14 < 65504 (fp16 max)
+__device__ __forceinline__ float f16_scale_for(float B) {
+  if (!(B > 0.f) || !(B < 3.0e38f)) return 1.f;
+  int e;
+  frexpf(B, &e);
+  e = e < -100 ? -100 : (e > 100 ? 100 : e);
+  return ldexpf(1.f, 14 - e);
+}
+// Rigorous bounds of the next block's values from the input block's recorded maxima and the
+// layer's ||W||_inf (Eq. 7 / the K=2 rule): |h0| <= s0; |h1_r| <= s1 G M1;
+// |top| <= s1 G Mt + s2 Rw (G M1)^2.
+__device__ __forceinline__ void f16_out_scales(const F16Args& a, float rw, float* os) {
+  const float G = a.wsc[1];
+  const float M1 = __uint_as_float(a.in->maxabs[1]), Mt = __uint_as_float(a.in->maxabs[2]);
+  const float g1 = G * M1;
+  os[0] = f16_scale_for(a.s0);
+  os[1] = f16_scale_for(a.s1 * g1);
+  os[2] = f16_scale_for(a.s1 * G * Mt + a.s2 * rw * g1 * g1);
 }
 
 template <int KORD, int FLAGS = 0>
 __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
                                                float wo, const float* jw, int part, int split, float* xacc,
-                                               int bar_id, float& fpart, float& opart) {
+                                               int bar_id, float& fpart, float& opart, F16Ctx* fc = nullptr) {
   constexpr int NPL = planes_of<FLAGS>();
+  constexpr bool F16 = (FLAGS & kFlagF16) != 0;  // fp16x3: unscale what is read, scale what is stored
+  static_assert(!F16 || KORD == 2, "fp16x3: K=2 collapsed rule only");
   const int P = p.P;
   const int ld = p.ldo;
   constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
@@ -197,13 +247,21 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   const int mb = (part == 2) ? split : 1;
   const int me = (part == 1) ? split : nmid + 1;
   // ---- slot 0: the primal; the bias enters here only (affine rule)
-  const float z0 = ptx::tmem_ld1(tcol) + bias;
+  const float z0 = (F16 ? ptx::tmem_ld1(tcol) * fc->us[0] : ptx::tmem_ld1(tcol)) + bias;
   ptx::tmem_ld_wait();
   const ActD A = act_derivs(p.act, z0);
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   fpart = (part == 2) ? 0.f : wo * t;
   opart = 0.f;
-  if (!p.readout && part != 2) store_out<NPL>(p, (size_t)row * ld + m, t);
+  if (!p.readout && part != 2) {
+    if constexpr (F16) {
+      uint16_t* const r0 = p.out + (size_t)row * ld + m;
+      ptx::store_f16_off(r0, r0 + p.pstride, 0u, t * fc->os[0]);
+      fc->mx[0] = fmaxf(fc->mx[0], fabsf(t));
+    } else {
+      store_out<NPL>(p, (size_t)row * ld + m, t);
+    }
+  }
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
   float* zp = kSaveZ ? p.z_out + (size_t)(row + mb) * p.ldz + m : nullptr;
   if (kSaveZ && part != 2) p.z_out[(size_t)row * p.ldz + m] = z0;
@@ -217,7 +275,14 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
   int jj = (KORD == 4) ? (mb - 1) / 3 : (KORD == kStd4) ? (mb - 1) / 4 : mb - 1;  // first direction / jet
   auto put = [&](float h) {
-    if (!p.readout) ptx::store_planes_off<NPL>(q0, q1, q2, off, h);
+    if (!p.readout) {
+      if constexpr (F16) {
+        ptx::store_f16_off(q0, q1, off, h * fc->os[1]);
+        fc->mx[1] = fmaxf(fc->mx[1], fabsf(h));
+      } else {
+        ptx::store_planes_off<NPL>(q0, q1, q2, off, h);
+      }
+    }
     off += (uint32_t)ld;
   };
   if constexpr (KORD == 4) {
@@ -311,13 +376,14 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
       }
     };
     const int cnt = me - mb;
+    const float us1 = F16 ? fc->us[1] : 1.f;
     int s = 0;
     for (; s + 16 <= cnt; s += 16) {
       float v[16];
       ptx::tmem_ld16(tcol + (uint32_t)(mb + s), v);
       ptx::tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) middle(v[i]);
+      for (int i = 0; i < 16; ++i) middle(F16 ? v[i] * us1 : v[i]);
     }
     const int rem = cnt - s;  // 0..15, warp-uniform
     if (rem > 0) {
@@ -328,7 +394,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
       ptx::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 15; ++i)
-        if (i < rem) middle(v[i]);
+        if (i < rem) middle(F16 ? v[i] * us1 : v[i]);
     }
   }
   if (part != 0) {  // part 1 hands its partial collapsed sum to part 2 (one barrier site for both)
@@ -342,12 +408,19 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     return;
   }
   // ---- slot P-1: the collapsed top, <dh, sum z_K> + the collapsed non-linear terms (Eq. 7)
-  const float zt = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
+  const float zt = F16 ? ptx::tmem_ld1(tcol + (uint32_t)(P - 1)) * fc->us[2] : ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
   ptx::tmem_ld_wait();
   const float top = d1 * zt + (KORD == 2 ? d2 * acc : acc);
   if constexpr (kSaveZ) *zp = zt;
   opart = wo * top;
-  if (!p.readout) ptx::store_planes_off<NPL>(q0, q1, q2, off, top);
+  if (!p.readout) {
+    if constexpr (F16) {
+      ptx::store_f16_off(q0, q1, off, top * fc->os[2]);
+      fc->mx[2] = fmaxf(fc->mx[2], fabsf(top));
+    } else {
+      ptx::store_planes_off<NPL>(q0, q1, q2, off, top);
+    }
+  }
 }
 
 // The K=2 rule for a point of P <= 16 slots whose 16 columns lie in the accumulator buffer:
@@ -357,7 +430,8 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
 template <int FLAGS, int PC = 0>
 __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint32_t tcol, int64_t row, int m,
                                                      float bias, float wo, const float* jw, float& fpart,
-                                                     float& opart) {
+                                                     float& opart, F16Ctx* fc = nullptr) {
+  constexpr bool F16 = (FLAGS & kFlagF16) != 0;
   constexpr bool kSaveZ = (FLAGS & kFlagSaveZ) != 0;
   constexpr int NPL = planes_of<FLAGS>();
   constexpr bool wsum = (FLAGS & kFlagWeighted) != 0;
@@ -366,6 +440,11 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   float v[16];
   ptx::tmem_ld16(tcol, v);
   ptx::tmem_ld_wait();
+  if constexpr (F16) {
+    v[0] *= fc->us[0];
+#pragma unroll
+    for (int i = 1; i < 16; ++i) v[i] *= (i == P - 1) ? fc->us[2] : fc->us[1];
+  }
   const float z0 = v[0] + bias;
   const ActD A = act_derivs(p.act, z0);
   fpart = wo * A.d0;
@@ -378,13 +457,22 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
   // one loop per value of p.readout (uniform): no per-store test of the flag
   auto body = [&](auto ro) {
     constexpr bool kRO = decltype(ro)::value;
-    if (!kRO) ptx::store_planes_off<NPL>(q0, q1, q2, 0u, A.d0);
+    // one store: fp16x3 scales by the slot type and records the output's max per type
+    auto st = [&](uint32_t off, float h, int type) {
+      if constexpr (F16) {
+        ptx::store_f16_off(q0, q1, off, h * fc->os[type]);
+        fc->mx[type] = fmaxf(fc->mx[type], fabsf(h));
+      } else {
+        ptx::store_planes_off<NPL>(q0, q1, q2, off, h);
+      }
+    };
+    if (!kRO) st(0u, A.d0, 0);
     float acc = 0.f, zt = 0.f;
 #pragma unroll
     for (int i = 1; i < 16; ++i) {
       if (i < P - 1) {
         const float z = v[i];
-        if (!kRO) ptx::store_planes_off<NPL>(q0, q1, q2, (uint32_t)i * ld, A.d1 * z);
+        if (!kRO) st((uint32_t)i * ld, A.d1 * z, 1);
         if constexpr (wsum)
           acc = fmaf(jw[i - 1] * z, z, acc);
         else
@@ -397,7 +485,7 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
     const float top = A.d1 * zt + A.d2 * acc;
     if constexpr (kSaveZ) zp[(size_t)(P - 1) * p.ldz] = zt;
     opart = wo * top;
-    if (!kRO) ptx::store_planes_off<NPL>(q0, q1, q2, (uint32_t)(P - 1) * ld, top);
+    if (!kRO) st((uint32_t)(P - 1) * ld, top, 2);
   };
   if (p.readout)
     body(std::true_type{});
@@ -686,10 +774,11 @@ __device__ __forceinline__ bool tile_of(int64_t k, int pair, int npairs, int m_p
 // The whole-K correction pass first keeps the accumulator small while the ~5K/16 correction
 // MMAs round into it, so the round-toward-zero accumulation of the tensor cores costs what
 // K/16 plain MMAs cost (scripts/emulate_schemes.py). f(phase, kb, nslots) per group.
+// fp16x3 mode (2 planes, two phases): phase 1 {p0, p1} with p1*p0, p0*p1; phase 2 {p0}, p0*p0.
 template <class F>
-__device__ __forceinline__ void for_each_group(int nplanes, int k_iters, F&& f) {
+__device__ __forceinline__ void for_each_group(int nplanes, bool two_phase, int k_iters, F&& f) {
   for (int kb = 0; kb < k_iters; ++kb) f(0, kb, nplanes);
-  if (nplanes == 3)
+  if (nplanes == 3 || two_phase)
     for (int kb = 0; kb < k_iters; ++kb) f(1, kb, 1);
 }
 
@@ -712,7 +801,7 @@ __host__ __device__ constexpr int layer_threads() {
 template <int KORD, int FLAGS = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, FLAGS>(), 1)
     jet_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const LayerParams p) {
+                     const LayerParams p, const F16Args f16) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kSlots * kSlotBytes);
@@ -726,6 +815,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
 
   constexpr int EG = epi_groups<KORD, FLAGS>();
   constexpr int NPL = planes_of<FLAGS>();  // operand planes read and written
+  constexpr bool F16 = (FLAGS & kFlagF16) != 0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -770,7 +860,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       for (int64_t k = 0; tile_of(k, pair, npairs, m_pairs, n_tiles, nt, mp); ++k) {
         const int m0 = mp * (2 * kBM) + (int)rank * kBM;
         const int32_t row0 = (int32_t)(nt * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
-        for_each_group(NPL, p.k_iters, [&](int, int kb, int nslots) {
+        for_each_group(NPL, F16, p.k_iters, [&](int phase, int kb, int nslots) {
           for (int pl = 0; pl < nslots; ++pl, ++it) {
             const uint32_t s = it % kSlots;
             const uint32_t ph = (it / kSlots) & 1u;
@@ -782,7 +872,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
             uint8_t* st = smem + s * kSlotBytes;
             if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * ((uint32_t)kATileBytes + b_bytes));
             const int k0 = kb * kBK;
-            ptx::tma_load_3d_pair(st, &tmA, &full_bar[s], k0, m0, pl);
+            // fp16x3 phase 2: p0 of B with the weights' p0 * 2^11 (plane 2), the scale of the corrections
+            ptx::tma_load_3d_pair(st, &tmA, &full_bar[s], k0, m0, (F16 && phase == 1) ? 2 : pl);
             ptx::tma_load_3d_pair(st + kATileBytes, &tmB, &full_bar[s], k0, row0, pl);
           }
         });
@@ -797,7 +888,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
 #ifdef CTM_EXP_STATS
       const long long tstart = clock64();
 #endif
-      const uint32_t idesc = ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
+      const uint32_t idesc = F16 ? ptx::idesc_f16(2 * kBM, (uint32_t)p.n_mma) : ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
       // K-major SW128 descriptor of slot 0's A tile (slot s: + s * kSlotBytes >> 4)
       const uint64_t desc0 = ptx::smem_desc_kmajor(ptx::smem_u32(smem), kSwSBO, kSwLayout);
       uint32_t it = 0, local = 0;
@@ -814,7 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * (kTmemCols / 2);
         uint32_t acc = 0;  // the tile's first MMA overwrites the accumulator
-        for_each_group(NPL, p.k_iters, [&](int phase, int, int nslots) {
+        for_each_group(NPL, F16, p.k_iters, [&](int phase, int, int nslots) {
           for (int pl = 0; pl < nslots; ++pl) {
             STAT_T0();
             ptx::mbar_wait(&full_bar[(it + pl) % kSlots], ((it + pl) / kSlots) & 1u);
@@ -832,10 +923,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
 #pragma unroll
           for (int ks = 0; ks < kBK / 16; ++ks) {  // bf16 MMA K = 16 (32 bytes)
             const uint64_t o = 2u * ks;
-            if (nslots == 2) {
+            if (nslots == 2) {  // fast mode: + p0*p0 here; fp16x3: p0*p0 in phase 2
               ptx::mma_bf16_pair(d_tmem, dA1 + o, dA0 + kB + o, idesc, acc);
               ptx::mma_bf16_pair(d_tmem, dA0 + o, dA1 + kB + o, idesc, 1u);
-              ptx::mma_bf16_pair(d_tmem, dA0 + o, dA0 + kB + o, idesc, 1u);
+              if (!F16) ptx::mma_bf16_pair(d_tmem, dA0 + o, dA0 + kB + o, idesc, 1u);
             } else if (nslots == 3) {
               ptx::mma_bf16_pair(d_tmem, dA2 + o, dA0 + kB + o, idesc, acc);
               ptx::mma_bf16_pair(d_tmem, dA1 + o, dA1 + kB + o, idesc, 1u);
@@ -874,6 +965,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     const int nunits = ((KORD == kStd2 || KORD == kStd4) ? p.P - 1 : p.P - 2) / unit;
     const int split = 1 + (nunits / 2) * unit;
     const int m_local = q * 32 + lane;
+    // fp16x3: the input block's unscale factors and this layer's output scales (every CTA
+    // computes the same values from the same device data; CTA 0 publishes them)
+    F16Ctx fcx{};
+    if constexpr (F16) {
+      const float wsi = f16.wsc[0];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        fcx.us[t] = wsi / f16.in->scale[t];
+        fcx.mx[t] = 0.f;
+      }
+      if (f16.out) {
+        float rw = f16.rw;
+        if (rw < 0.f) {  // weighted sums: the largest sum |w_r| over the direction blocks
+          rw = 0.f;
+          for (int b = 0; b < p.blocks; ++b) {
+            float sb = 0.f;
+            for (int j = 0; j < p.rb; ++j) sb += fabsf(jw[b * p.rb + j]);
+            rw = fmaxf(rw, sb);
+          }
+        }
+        f16_out_scales(f16, rw, fcx.os);
+        if (blockIdx.x == 0 && threadIdx.x == 64)
+          for (int t = 0; t < 3; ++t) f16.out->scale[t] = fcx.os[t];
+      }
+    }
+    F16Ctx* const fc = F16 ? &fcx : nullptr;
     uint32_t local = 0;
     int64_t n_tile;
     int mp;
@@ -925,7 +1042,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           float fpart, opart;
           const int jbase = blk0 * p.rb;  // one sub-point per tile
           epilogue_point<KORD, FLAGS>(p, tbase, row0, m, bias, wo, jw + jbase, g + 1, split,
-                                      xacc + (local & 1u) * kBM + m_local, 2 + q, fpart, opart);
+                                      xacc + (local & 1u) * kBM + m_local, 2 + q, fpart, opart, fc);
           if (p.readout) {
             const float v = warp_sum(g == 0 ? fpart : opart);
             if (lane == 0) red[(q * kMaxPtsPerTile + 0) * 2 + g] = v;
@@ -945,15 +1062,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
             const int64_t rw = row0 + (int64_t)pt * p.P;
             switch (p.P) {
 #define CTM_SMALL_CASE(n) \
-  case n: epilogue_point_small<FLAGS, n>(p, tc, rw, m, bias, wo, jw + jbase, fpart, opart); break;
+  case n: epilogue_point_small<FLAGS, n>(p, tc, rw, m, bias, wo, jw + jbase, fpart, opart, fc); break;
               CTM_SMALL_CASE(3) CTM_SMALL_CASE(4) CTM_SMALL_CASE(5) CTM_SMALL_CASE(6) CTM_SMALL_CASE(7)
               CTM_SMALL_CASE(8) CTM_SMALL_CASE(9) CTM_SMALL_CASE(10) CTM_SMALL_CASE(11) CTM_SMALL_CASE(12)
 #undef CTM_SMALL_CASE
-              default: epilogue_point_small<FLAGS>(p, tc, rw, m, bias, wo, jw + jbase, fpart, opart); break;
+              default: epilogue_point_small<FLAGS>(p, tc, rw, m, bias, wo, jw + jbase, fpart, opart, fc); break;
             }
           } else
             epilogue_point<KORD, FLAGS>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
-                                        jw + jbase, 0, 0, nullptr, 0, fpart, opart);
+                                        jw + jbase, 0, 0, nullptr, 0, fpart, opart, fc);
           if (p.readout) {
             fpart = warp_sum(fpart);
             opart = warp_sum(opart);
@@ -981,6 +1098,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           p.partial[(n * p.m_tiles + m_tile) * 2 + comp] = s;
         }
         asm volatile("bar.sync 1, %0;" ::"r"(128 * EG) : "memory");  // red[] is reused by the next tile
+      }
+    }
+    if constexpr (F16) {  // this thread's output maxima per slot type into the block's record
+      if (f16.out) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          float v = fcx.mx[t];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+          if (lane == 0 && v > 0.f) atomicMax(&f16.out->maxabs[t], __float_as_uint(v));
+        }
       }
     }
   }

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace ctm {
 namespace ptx {
@@ -285,6 +286,10 @@ __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t smem_addr, uint32_t lb
 // Instruction descriptor, kind::f16 with BF16 A/B, fp32 accumulate, both K-major:
 //  [4,6) D format (1 = f32); [7,10) A format (1 = bf16); [10,13) B format (1 = bf16);
 //  [15] A major (0 = K); [16] B major (0 = K); [17,23) N >> 3; [24,29) M >> 4.
+// kind::f16 with fp16 A and B (formats 0), fp32 accumulate: the fp16x3 mode
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N) {
+  return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
@@ -351,6 +356,24 @@ __device__ __forceinline__ void store_planes_off(uint16_t* q0, uint16_t* q1, uin
   q0[off] = __bfloat16_as_ushort(h);
   q1[off] = __bfloat16_as_ushort(m);
   if (NPL > 2) q2[off] = __bfloat16_as_ushort(__float2bfloat16_rn(r - __bfloat162float(m)));
+}
+// fp16x3 planes: vs = v * scale (a power of two chosen so |vs| <= 2^14),
+// p0 = rn_f16(vs), p1 = rn_f16((vs - p0) * 2^11): 22 significant bits (the difference is
+// exact in fp32); the residual plane is lifted by 2^11 so it is subnormal only where p0 is,
+// which keeps both planes an exact power-of-two multiple of those of v (results do not depend
+// on the block's scale, hence not on how a batch is split). q0/q1 are the plane bases, off a
+// 32-bit element offset.
+constexpr float kF16Lift = 2048.f;
+__device__ __forceinline__ void f16_split(float vs, uint16_t& p0, uint16_t& p1) {
+  const __half h = __float2half_rn(vs);
+  p0 = __half_as_ushort(h);
+  p1 = __half_as_ushort(__float2half_rn((vs - __half2float(h)) * kF16Lift));
+}
+__device__ __forceinline__ void store_f16_off(uint16_t* q0, uint16_t* q1, uint32_t off, float vs) {
+  uint16_t a, b;
+  f16_split(vs, a, b);
+  q0[off] = a;
+  q1[off] = b;
 }
 // Programmatic dependent launch: the next kernel in the stream may start its prologue
 // once every CTA of this grid has called launch_dependents (or exited); wait_prior blocks

@@ -11,6 +11,7 @@
 #pragma once
 #include <cstdint>
 
+#include "jet_layer.cuh"  // ActD, F16Rec, f16_scale_for
 #include "ptx.cuh"
 
 namespace ctm {
@@ -46,6 +47,11 @@ struct SeedParams {
   int nplanes;
   int act;               // kAct*
   float* z_out;          // K=2, grad mode (one block): pre-activations [N*P, ld] (z0, W1 u_r, 0) or nullptr
+  // fp16x3 mode (seed_fixed_kernel<2, 2, true>): bounds [max |U|, max |csum|] (float bits) of
+  // this call's direction images, sup |s|, |s'|, |s''|, and the layer-1 block's record
+  const unsigned* f16_bounds;
+  float s0, s1, s2;
+  F16Rec* f16_out;
 };
 
 // Where a kernel writes its bf16 planes: plane k of element i at base[k * pstride + i].
@@ -73,6 +79,32 @@ __device__ __forceinline__ void seed_store4(const PlaneOut& o, size_t idx, float
     *reinterpret_cast<uint2*>(dst) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
     dst += o.pstride;
   }
+}
+
+// fp16x3 mode (jet_layer.cuh kFlagF16): four adjacent features as two fp16 planes of v * sc
+__device__ __forceinline__ void seed_store4_f16(const PlaneOut& o, size_t idx, float a, float b, float c, float d,
+                                                float sc) {
+  const float x[4] = {a * sc, b * sc, c * sc, d * sc};
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint16_t p0, p1;
+    ptx::f16_split(x[i], p0, p1);
+    h[i] = p0;
+    l[i] = p1;
+  }
+  uint16_t* dst = o.base + idx;
+  *reinterpret_cast<uint2*>(dst) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+  *reinterpret_cast<uint2*>(dst + o.pstride) = make_uint2(l[0] | (l[1] << 16), l[2] | (l[3] << 16));
+}
+__device__ __forceinline__ float max4abs(float a, float b, float c, float d) {
+  return fmaxf(fmaxf(fabsf(a), fabsf(b)), fmaxf(fabsf(c), fabsf(d)));
+}
+// max |v| of a warp's values into a block record (float bits; all lanes call)
+__device__ __forceinline__ void warp_max_record(float v, unsigned* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v > 0.f) atomicMax(dst, __float_as_uint(v));
 }
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -285,7 +317,7 @@ __host__ __device__ inline size_t seed_fixed_smem(int D, int R, int blocks) {
   return ((size_t)(D + R + blocks + 1) * kSeedFixedFeats + (size_t)kSeedFixedWarps * D) * sizeof(float);
 }
 
-template <int KORD, int NP>
+template <int KORD, int NP, bool F16 = false>
 __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const SeedParams p, int64_t pts_per_group) {
   extern __shared__ float sm[];
   constexpr int F = kSeedFixedFeats;
@@ -312,6 +344,29 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
   const int64_t nb = blockIdx.y * pts_per_group;
   const int64_t ne = (nb + pts_per_group < p.n_points) ? nb + pts_per_group : p.n_points;
   constexpr int ROWS = (KORD == 4) ? 3 : 1;  // rows per direction (jet)
+  static_assert(!F16 || (KORD == 2 && NP == 2), "fp16x3: K=2, two planes");
+  // fp16x3: output scales per slot type from |h0| <= s0, |s' u| <= s1 max|U|, |s'' csum| <= s2 max|csum|
+  float os0 = 1.f, os1 = 1.f, os2 = 1.f, mx0 = 0.f, mx1 = 0.f, mx2 = 0.f;
+  if (F16) {
+    os0 = f16_scale_for(p.s0);
+    os1 = f16_scale_for(p.s1 * __uint_as_float(p.f16_bounds[0]));
+    os2 = f16_scale_for(p.s2 * __uint_as_float(p.f16_bounds[1]));
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+      p.f16_out->scale[0] = os0;
+      p.f16_out->scale[1] = os1;
+      p.f16_out->scale[2] = os2;
+    }
+  }
+  auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
+    if constexpr (F16) {
+      const float sc = type == 0 ? os0 : type == 1 ? os1 : os2;
+      seed_store4_f16(o, idx, a, b, c, d, sc);
+      const float mv = max4abs(a, b, c, d);
+      if (type == 0) mx0 = fmaxf(mx0, mv); else if (type == 1) mx1 = fmaxf(mx1, mv); else mx2 = fmaxf(mx2, mv);
+    } else {
+      seed_store4<NP>(o, idx, a, b, c, d);
+    }
+  };
   for (int64_t n = nb + warp; n < ne; n += kSeedFixedWarps) {
     for (int d = lane; d < p.D; d += 32) xw[d] = __ldg(p.X + n * p.D + d);
     __syncwarp();
@@ -335,12 +390,12 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
       const size_t row0 = ((size_t)n * p.blocks + b) * p.P;
       const int r0 = b * p.rb;
       const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;
-      seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+      put4(row0 * p.ld + m, t[0], t[1], t[2], t[3], 0);
       size_t row = row0 + 1;
       for (int r = r0; r < r0 + p.rb; ++r, row += ROWS) {
         const float4 u = (r < r1) ? *reinterpret_cast<const float4*>(us + (size_t)r * F + c)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-        seed_store4<NP>(o, row * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+        put4(row * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w, 1);
         if (KORD == 4) {
           seed_store4<NP>(o, (row + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z,
                           d2[3] * u.w * u.w);
@@ -352,8 +407,13 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
       if (KORD == 4)
         seed_store4<NP>(o, row * p.ld + m, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w);
       else
-        seed_store4<NP>(o, row * p.ld + m, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w);
+        put4(row * p.ld + m, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w, 2);
     }
+  }
+  if constexpr (F16) {
+    warp_max_record(mx0, &p.f16_out->maxabs[0]);
+    warp_max_record(mx1, &p.f16_out->maxabs[1]);
+    warp_max_record(mx2, &p.f16_out->maxabs[2]);
   }
 }
 
@@ -488,6 +548,11 @@ struct SeedRandomParams {
   uint16_t* out;         // planes of [N*blocks*(rb+2), ldk] (standard: [N*blocks*(1+2rb), ldk])
   int64_t pstride;
   int nplanes;
+  // fp16x3 mode (seed_random_kernel<2, true>, no sigma, collapsed layout): bounds [max |x|,
+  // max |V|] (float bits) and the generated directions' bound vgen (Rademacher 1, Gaussian 6)
+  const unsigned* f16_bounds;
+  float vgen;
+  F16Rec* f16_out;
 };
 
 // Standard normal draw for counter idx: Box-Muller on two splitmix64 outputs
@@ -499,10 +564,31 @@ __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx) {
   return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
 }
 
-template <int NP>
+template <int NP, bool F16 = false>
 __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRandomParams p) {
   __shared__ float vs[kSeedChunk];
   const PlaneOut o{p.out, p.pstride, p.nplanes};
+  static_assert(!F16 || NP == 2, "fp16x3: two planes");
+  // fp16x3: primal rows x0 scaled by its bound, direction rows by theirs, zero top rows by 1
+  float os0 = 1.f, os1 = 1.f, mx0 = 0.f, mx1 = 0.f;
+  if (F16) {
+    os0 = f16_scale_for(__uint_as_float(p.f16_bounds[0]));
+    os1 = f16_scale_for(p.V ? __uint_as_float(p.f16_bounds[1]) : p.vgen);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.f16_out->scale[0] = os0;
+      p.f16_out->scale[1] = os1;
+      p.f16_out->scale[2] = 1.f;
+    }
+  }
+  auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
+    if constexpr (F16) {
+      seed_store4_f16(o, idx, a, b, c, d, type == 0 ? os0 : type == 1 ? os1 : 1.f);
+      const float mv = max4abs(a, b, c, d);
+      if (type == 0) mx0 = fmaxf(mx0, mv); else if (type == 1) mx1 = fmaxf(mx1, mv);
+    } else {
+      seed_store4<NP>(o, idx, a, b, c, d);
+    }
+  };
   const int64_t n = blockIdx.x;
   const int st = p.standard ? 2 : 1;            // rows per direction
   const int P = p.standard ? 1 + 2 * p.rb : p.rb + 2;  // slots per block
@@ -517,14 +603,13 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = (4 * c4 + i < p.D) ? p.X[n * p.D + 4 * c4 + i] : 0.f;
     for (int b = 0; b < p.blocks; ++b) {
-      seed_store4<NP>(o, (pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3]);
-      if (!p.standard) seed_store4<NP>(o, ((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+      put4((pt0 + b) * P * p.ldk + 4 * c4, x[0], x[1], x[2], x[3], 0);
+      if (!p.standard) put4(((pt0 + b) * P + P - 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f, 2);
     }
     if (p.standard)
       for (int s = 0; s < p.blocks * p.rb; ++s)
         seed_store4<NP>(o, (dir_row(s) + 1) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
-    for (int s = p.S; s < p.blocks * p.rb; ++s)
-      seed_store4<NP>(o, dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f);
+    for (int s = p.S; s < p.blocks * p.rb; ++s) put4(dir_row(s) * p.ldk + 4 * c4, 0.f, 0.f, 0.f, 0.f, 1);
   }
   const int per_chunk = kSeedChunk / p.Rv;
   for (int s0 = 0; s0 < p.S; s0 += per_chunk) {
@@ -561,8 +646,12 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
         }
         u[i] = val;
       }
-      seed_store4<NP>(o, dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3]);
+      put4(dir_row(s0 + s) * p.ldk + 4 * c4, u[0], u[1], u[2], u[3], 1);
     }
+  }
+  if constexpr (F16) {
+    warp_max_record(mx0, &p.f16_out->maxabs[0]);
+    warp_max_record(mx1, &p.f16_out->maxabs[1]);
   }
 }
 
@@ -702,6 +791,66 @@ __global__ void split_weights_kernel(const float* __restrict__ W, const float* _
   if (c == 0) bpad[r] = (r < rows) ? b[r] : 0.f;
 }
 
+// fp16x3 weight statistics (one block): out[0] = 2^-(sa + 11) with max|W| * 2^sa in (4, 8]
+// (the factor that undoes the planes' scales, see split_weights_f16_kernel), out[1] = ||W||_inf
+// = max_m sum_k |W[m, k]| (the bound of jet_layer.cuh f16_out_scales). W [rows, cols] row-major.
+__global__ void __launch_bounds__(1024) f16_weight_stats_kernel(const float* __restrict__ W, int rows, int cols,
+                                                               float* __restrict__ out) {
+  __shared__ float smax[32], ssum[32];
+  float mx = 0.f, rs = 0.f;
+  for (int r = threadIdx.x >> 5; r < rows; r += 32) {  // one warp per row
+    float a = 0.f, m = 0.f;
+    for (int c = threadIdx.x & 31; c < cols; c += 32) {
+      const float v = fabsf(W[(size_t)r * cols + c]);
+      a += v;
+      m = fmaxf(m, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    rs = fmaxf(rs, a);
+    mx = fmaxf(mx, m);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smax[threadIdx.x >> 5] = mx;
+    ssum[threadIdx.x >> 5] = rs;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 32; ++w) {
+      mx = fmaxf(mx, smax[w]);
+      rs = fmaxf(rs, ssum[w]);
+    }
+    out[0] = 1.f / f16_scale_for(mx);  // 2^(sa + 11) = the scale putting max|W| in (2^13, 2^14]
+    out[1] = rs;
+  }
+}
+// fp16x3 weight planes [3][Mpad, Kpad], zero padded: p0 = rn_f16(W 2^sa), p1 = rn_f16((W 2^sa -
+// p0) 2^11) (the corrections' operands: p1 * B0 and p0 * B1 both carry 2^(sa + 11 + sb)), and
+// p0 2^11 (exact) for the leading product with B0 in phase 2 (the same 2^(sa + 11 + sb)).
+__global__ void split_weights_f16_kernel(const float* __restrict__ W, int rows, int cols, int Mpad, int Kpad,
+                                         const float* __restrict__ stats, uint16_t* __restrict__ Wp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)Mpad * Kpad;
+  if (i >= n) return;
+  const int r = (int)(i / Kpad), c = (int)(i % Kpad);
+  // W * 2^sa with 2^sa = 1 / (stats[0] 2^11): exact (powers of two)
+  const float v = (r < rows && c < cols) ? W[(size_t)r * cols + c] / (stats[0] * ptx::kF16Lift) : 0.f;
+  uint16_t p0, p1;
+  ptx::f16_split(v, p0, p1);
+  Wp[i] = p0;
+  Wp[n + i] = p1;
+  Wp[2 * n + i] = __half_as_ushort(__float2half_rn(__half2float(__ushort_as_half(p0)) * ptx::kF16Lift));
+}
+// max |a_i| over n floats into a record (float bits, atomicMax; the record is zeroed by the caller)
+__global__ void maxabs_kernel(const float* __restrict__ a, int64_t n, unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(a[i]));
+  warp_max_record(m, out);
+}
+
 // W1T [D, ld] = W1^T zero padded; b1 [ld]
 __global__ void transpose_w1_kernel(const float* __restrict__ W1, const float* __restrict__ b1, int w1, int D, int ld,
                                     float* __restrict__ W1T, float* __restrict__ b1p) {
@@ -727,6 +876,29 @@ __global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, i
     out[q * pstride + k] = __bfloat16_as_ushort(b);
     v -= __bfloat162float(b);
   }
+}
+
+// ctm_gemm_probe in the fp16x3 mode: the block's record (every slot type: the scale of the
+// measured max |B| and that max) from the bound scratch b[0]
+__global__ void probe_f16_record_kernel(const unsigned* __restrict__ b, F16Rec* __restrict__ rec) {
+  const float m = __uint_as_float(b[0]);
+  for (int t = 0; t < 3; ++t) {
+    rec->scale[t] = f16_scale_for(m);
+    rec->maxabs[t] = b[0];
+  }
+}
+// ... and its fp16 planes of B * scale [2][rows_pad, ldp]
+__global__ void split_rows_f16_kernel(const float* __restrict__ src, int64_t rows, int cols, int64_t rows_pad, int ldp,
+                                      const F16Rec* __restrict__ rec, uint16_t* __restrict__ out, int64_t pstride) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= rows_pad * ldp) return;
+  const int64_t r = k / ldp;
+  const int c = (int)(k % ldp);
+  const float v = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+  uint16_t p0, p1;
+  ptx::f16_split(v * rec->scale[0], p0, p1);
+  out[k] = p0;
+  out[pstride + k] = p1;
 }
 
 __global__ void pad_vector_kernel(const float* __restrict__ src, int n, int npad, float* __restrict__ dst) {

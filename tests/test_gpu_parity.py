@@ -188,7 +188,9 @@ def test_streaming_seed_matches_grad_mode_seed_bitwise(ctm, widths, N, rb):
     params, _ = nets(widths, seed=11)
     X = torch.from_numpy(points(N, widths[0], seed=11)).cuda()
     sig = torch.from_numpy(make_sigma(widths[0], 9, kind="rect")).cuda()
-    fwd, grd = gpu_mlp(ctm, params), gpu_mlp(ctm, params)
+    mk = lambda: ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0,  # noqa: E731
+                         precision="fp32")  # the grad-mode seed runs the fp32 mode in every precision
+    fwd, grd = mk(), mk()
     grd.grad_enable()
     # one block per point unless rb is given (grad mode always keeps one; the planner may
     # otherwise split D = 130 directions into blocks, which reorders the collapsed sums)
