@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--precision", choices=["fp32", "fp16x3", "bf16x3"], default="fp32",
                     help="layer-contraction arithmetic (ctm_set_precision, DESIGN.md §5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-precisions", action="store_true",
+                    help="skip timing the operator in the other precision modes (the line's other_precisions)")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="--impl reference: total CPU seconds spread over the warm-up + timed steps")
     return ap.parse_args()
@@ -450,6 +452,34 @@ def main():
     median_ms = max_over_ranks(float(np.median(step_ms)))
     clk = clocks.stop()
 
+    # ---------------- the same steps in the other precision modes (same protocol: warm-up, L2
+    # flush between timed steps, CUDA events, max over ranks), for the line's `other_precisions`
+    others = {}
+    if not train and not args.no_other_precisions:
+        for prec in [q for q in ("fp32", "fp16x3", "bf16x3") if q != args.precision]:
+            mlp.set_precision(prec)
+            for _ in range(3):
+                step(X)
+            torch.cuda.synchronize()
+            q_ran = mlp.last_precision()
+            if q_ran != prec:  # the mode does not cover this operator (it ran another arithmetic)
+                continue
+            qevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(args.steps)]
+            barrier()
+            torch.cuda.synchronize()
+            for a, b in qevs:
+                flush_buf.zero_()
+                a.record()
+                step(X)
+                b.record()
+            torch.cuda.synchronize()
+            barrier()
+            q_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in qevs))
+            others[prec] = {"value": n_glob * args.steps / (q_ms / 1e3), "ms_per_step": q_ms / args.steps,
+                            "unit": "points/s"}
+        mlp.set_precision(args.precision)
+
     # ---------------- strong scaling: the same steps with the all_gather of op and f inside
     gather_rec = None
     if strong and not train:
@@ -644,6 +674,12 @@ def main():
         }
         if gather_rec is not None:
             line["with_gather"] = gather_rec
+        if others:
+            line["other_precisions"] = {
+                **others,
+                "note": "the same operator and workload timed in the other ctm_set_precision modes after the main "
+                        "timed region (same protocol; not part of value): fp32 = bf16x6 (24-bit operands), fp16x3 "
+                        "= two scaled fp16 planes (22-bit operands, the 3xTF32 split), bf16x3 = ~17-bit operands"}
         print(json.dumps(line), flush=True)
     mlp.close()
     if world > 1:

@@ -17,13 +17,16 @@ if ! skip tests; then
 fi
 if ! skip bench; then
   timeout 600 python bench.py > $E/bench_laplacian.json 2> $E/bench_laplacian.err
-  for spec in "precision bf16x3" "op weighted" "op standard" "op biharmonic" "op biharmonic_nested" \
+  for spec in "precision bf16x3" "precision fp16x3" "precision fp16x3 --op weighted" \
+              "precision fp16x3 --op randomized --S 8" "precision fp16x3 --op randomized --S 32" \
+              "precision fp16x3 --op randomized --S 128" \
+              "op weighted" "op standard" "op biharmonic" "op biharmonic_nested" \
               "op randomized --S 8" "op randomized --S 32" "op randomized --S 128" \
               "op stochastic_biharmonic --S 16" "op laplacian_train" "op biharmonic_standard" \
               "op randomized_standard --S 8" "op randomized_standard --S 32" \
               "op stochastic_biharmonic_standard --S 16"; do
     name=$(echo $spec | tr ' ' '_' | tr -d '-')
-    timeout 600 python bench.py --no-cpu-baseline --$spec > $E/bench_$name.json 2>> $E/bench_other.err
+    timeout 600 python bench.py --no-cpu-baseline --no-other-precisions --$spec > $E/bench_$name.json 2>> $E/bench_other.err
   done
   timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
     --master-port 29555 bench.py --gpus 1 --steps 20 --warmup 3 --no-cpu-baseline > $E/bench_torchrun1.json 2> $E/bench_torchrun1.err
@@ -46,24 +49,39 @@ fi
 if ! skip sweep; then
   timeout 900 python scripts/parity_sweep.py 2048 > $E/parity_sweep.log 2>&1
   cp gpurun_out/parity_sweep.json $E/ 2>/dev/null
+  CTM_PRECISION=fp16x3 timeout 900 python scripts/parity_sweep.py 2048 > $E/parity_sweep_fp16x3.log 2>&1
+  cp gpurun_out/parity_sweep.json $E/parity_sweep_fp16x3.json 2>/dev/null
+fi
+if ! skip f16suite; then
+  CTM_PRECISION=fp16x3 timeout 1500 python -m pytest tests -q -m gpu --timeout 300 -p no:cacheprovider \
+    > $E/gpu_tests_fp16x3.log 2>&1; echo "pytest rc=$?" >> $E/gpu_tests_fp16x3.log
 fi
 if ! skip soak; then
   CTM_FUZZ_SHAPES=150 CTM_FUZZ_DSUM=120 CTM_FUZZ_K4=80 CTM_FUZZ_GRAD=60 timeout 1800 python -m pytest tests -q -m gpu \
     -k fuzz --timeout 600 -p no:cacheprovider > $E/soak.log 2>&1; echo "soak rc=$?" >> $E/soak.log
   cp gpurun_out/parity_errors.json $E/soak_parity_errors.json 2>/dev/null
   cp gpurun_out/grad_errors.json $E/soak_grad_errors.json 2>/dev/null
+  CTM_PRECISION=fp16x3 CTM_FUZZ_SHAPES=150 CTM_FUZZ_DSUM=120 CTM_FUZZ_K4=80 CTM_FUZZ_GRAD=60 timeout 1800 \
+    python -m pytest tests -q -m gpu -k fuzz --timeout 600 -p no:cacheprovider > $E/soak_fp16x3.log 2>&1
+  echo "soak rc=$?" >> $E/soak_fp16x3.log
+  cp gpurun_out/parity_errors.json $E/soak_parity_errors_fp16x3.json 2>/dev/null
 fi
 if ! skip ncu; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $E/launches_laplacian.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $E/under_ncu_laplacian.log 2>&1
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-other-precisions > $E/under_ncu_laplacian.log 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $E/launches_randomized_S_8.csv \
     python bench.py --op randomized --S 8 --steps 2 --warmup 1 --no-cpu-baseline > $E/under_ncu_s8.log 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $E/launches_laplacian_train.csv \
     python bench.py --op laplacian_train --steps 2 --warmup 1 --no-cpu-baseline > $E/under_ncu_train.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:jet_layer -s 3 -c 3 \
-    -o $E/prof_layer_c1 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $E/ncu_layer.log 2>&1
+    -o $E/prof_layer_c1 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-other-precisions > $E/ncu_layer.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:jet_layer -s 3 -c 3 \
+    -o $E/prof_layer_c1_fp16x3 -f python bench.py --precision fp16x3 --steps 1 --warmup 1 --no-cpu-baseline \
+    --no-other-precisions > $E/ncu_layer_fp16x3.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $E/launches_laplacian_fp16x3.csv \
+    python bench.py --precision fp16x3 --steps 2 --warmup 1 --no-cpu-baseline --no-other-precisions > /dev/null 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:seed -s 1 -c 1 \
-    -o $E/prof_seed_c1 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $E/ncu_seed.log 2>&1
+    -o $E/prof_seed_c1 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-other-precisions > $E/ncu_seed.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:jet_layer_kernel<.int.6" -s 3 -c 1 \
     -o $E/prof_bwd -f python bench.py --op laplacian_train --steps 1 --warmup 1 --no-cpu-baseline > $E/ncu_bwd.log 2>&1
   for r in $E/prof_*.ncu-rep; do python scripts/ncu_summary.py $r > ${r%.ncu-rep}.json 2>/dev/null; done
