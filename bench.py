@@ -452,34 +452,6 @@ def main():
     median_ms = max_over_ranks(float(np.median(step_ms)))
     clk = clocks.stop()
 
-    # ---------------- the same steps in the other precision modes (same protocol: warm-up, L2
-    # flush between timed steps, CUDA events, max over ranks), for the line's `other_precisions`
-    others = {}
-    if not train and not args.no_other_precisions:
-        for prec in [q for q in ("fp32", "fp16x3", "bf16x3") if q != args.precision]:
-            mlp.set_precision(prec)
-            for _ in range(3):
-                step(X)
-            torch.cuda.synchronize()
-            q_ran = mlp.last_precision()
-            if q_ran != prec:  # the mode does not cover this operator (it ran another arithmetic)
-                continue
-            qevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                    for _ in range(args.steps)]
-            barrier()
-            torch.cuda.synchronize()
-            for a, b in qevs:
-                flush_buf.zero_()
-                a.record()
-                step(X)
-                b.record()
-            torch.cuda.synchronize()
-            barrier()
-            q_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in qevs))
-            others[prec] = {"value": n_glob * args.steps / (q_ms / 1e3), "ms_per_step": q_ms / args.steps,
-                            "unit": "points/s"}
-        mlp.set_precision(args.precision)
-
     # ---------------- strong scaling: the same steps with the all_gather of op and f inside
     gather_rec = None
     if strong and not train:
@@ -568,6 +540,35 @@ def main():
 
     value = n_glob * args.steps / (total_ms / 1e3)
     e2e_value = n_glob * args.steps / (e2e_ms / 1e3)
+
+    # ---------------- the same steps in the other precision modes (same protocol: warm-up, L2
+    # flush between timed steps, CUDA events, max over ranks), for the line's `other_precisions`
+    others = {}
+    if not train and not args.no_other_precisions:
+        for prec in [q for q in ("fp32", "fp16x3", "bf16x3") if q != args.precision]:
+            mlp.set_precision(prec)
+            for _ in range(3):
+                step(X)
+            torch.cuda.synchronize()
+            q_ran = mlp.last_precision()
+            if q_ran != prec:  # the mode does not cover this operator (it ran another arithmetic)
+                continue
+            qevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(args.steps)]
+            barrier()
+            torch.cuda.synchronize()
+            for a, b in qevs:
+                flush_buf.zero_()
+                a.record()
+                step(X)
+                b.record()
+            torch.cuda.synchronize()
+            barrier()
+            q_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in qevs))
+            others[prec] = {"value": n_glob * args.steps / (q_ms / 1e3), "ms_per_step": q_ms / args.steps,
+                            "unit": "points/s"}
+        mlp.set_precision(args.precision)
+
 
     # ---------------- roofline of the dominant kernel
     peaks = {}

@@ -85,5 +85,7 @@ if ! skip ncu; then
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:jet_layer_kernel<.int.6" -s 3 -c 1 \
     -o $E/prof_bwd -f python bench.py --op laplacian_train --steps 1 --warmup 1 --no-cpu-baseline > $E/ncu_bwd.log 2>&1
   for r in $E/prof_*.ncu-rep; do python scripts/ncu_summary.py $r > ${r%.ncu-rep}.json 2>/dev/null; done
+  # the reports themselves stay on the box unless KEEP_REPS=1 (gpurun brings back <= 64 MiB)
+  [ -n "$KEEP_REPS" ] || rm -f $E/*.ncu-rep
 fi
 ls -la $E
