@@ -182,11 +182,12 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
  *     (primal / first order / collapsed top) from a rigorous bound on the block's values
  *     (the previous block's recorded max |value| and ||W||_inf), so no plane overflows;
  *     p1*p0 + p0*p1 over the whole K, then p0*p0: three products, ~2^-21 per product, the
- *     tensor time and energy of BF16X3. Covers the K=2 collapsed forward
- *     operators (laplacian, weighted, randomized without sigma, sigma(x), K=2 directional
- *     sums) of tanh and sin nets with at least two points per MMA tile; other calls on an
- *     FP16X3 handle (K=4, nested, standard modes, grad mode, other activations) run in
- *     CTM_PRECISION_FP32.
+ *     tensor time and energy of BF16X3. Covers the collapsed forward
+ *     operators of tanh and sin nets with at least two points per MMA tile: K=2
+ *     (laplacian, weighted, randomized without sigma, sigma(x), K=2 directional sums) and
+ *     K=4 with fixed directions (biharmonic, shared K=4 directional sums); other calls on
+ *     an FP16X3 handle (per-point K=4 directions, nested, standard modes, grad mode, other
+ *     activations) run in CTM_PRECISION_FP32.
  * Changing the precision invalidates a recorded tape (ctm_backward then fails).
  * Errors: CTM_EINVAL (NULL handle, unknown value). */
 typedef enum { CTM_PRECISION_FP32 = 0, CTM_PRECISION_BF16X3 = 1, CTM_PRECISION_FP16X3 = 2 } ctm_precision;

@@ -376,10 +376,10 @@ ctm_status launch_layer_instance(ctm_mlp* h, int64_t grid, const CUtensorMap& am
 template <int KORD, int FLAGS>
 ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
                                const ctm::LayerParams& lp, cudaStream_t st, const ctm::F16Args& fa = {}) {
-  if constexpr (KORD == 2 && (FLAGS & ctm::kFlagSaveZ) == 0) {
+  if constexpr ((KORD == 2 || (KORD == 4 && FLAGS == 0)) && (FLAGS & ctm::kFlagSaveZ) == 0) {
     if (fa.wsc) return launch_layer_instance<KORD, FLAGS | ctm::kFlagF16>(h, grid, amap, bmap, lp, st, fa);
   }
-  if (fa.wsc) return fail(CTM_EUNSUPPORTED, "fp16x3: K=2 forward layers only");
+  if (fa.wsc) return fail(CTM_EUNSUPPORTED, "fp16x3: collapsed K=2 / K=4 forward layers only");
   if (lp.nplanes == 2) return launch_layer_instance<KORD, FLAGS | ctm::kFlagNP2>(h, grid, amap, bmap, lp, st, fa);
   return launch_layer_instance<KORD, FLAGS>(h, grid, amap, bmap, lp, st, fa);
 }
@@ -512,11 +512,15 @@ struct LayerIO {
   float* z;
 };
 
-// sup |s|, |s'|, |s''| of the activations the fp16x3 mode covers (tanh: |tanh''| <= 4/(3 sqrt 3))
-void f16_act_sups(int act, float& s0, float& s1, float& s2) {
+// sups of |s| and its first four derivatives for the activations the fp16x3 mode covers
+// (tanh: |tanh''| <= 4/(3 sqrt 3) = 0.7698, |tanh'''| <= 2 (at 0), |tanh''''| <= 4.0859; sin: 1)
+void f16_act_sups(int act, float& s0, float& s1, float& s2, float& s3, float& s4) {
+  const bool th = (act == ctm::kActTanh);
   s0 = 1.f;
   s1 = 1.f;
-  s2 = (act == ctm::kActTanh) ? 0.7699f : 1.f;
+  s2 = th ? 0.7699f : 1.f;
+  s3 = th ? 2.0001f : 1.f;
+  s4 = th ? 4.0860f : 1.f;
 }
 
 // max |a| over n floats into the bound record out (zeroed at the start of the call)
@@ -597,7 +601,9 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     // than it in the power-capped C4 step (1.70-1.75 vs 1.61-1.65 ms), so K=4 stays there too.
     const size_t fsm = ctm::seed_fixed_smem(D, R, pl.nb);
     constexpr size_t kFixedSmemMax = 200 * 1024;
-    if (KORD == 2 && !z_out && fsm <= kFixedSmemMax && ld1 % ctm::kSeedFixedFeats == 0 && n > 0) {
+    // (the fp16x3 mode's K=4 seed is the streaming kernel too: seed_layer_kernel has no fp16 planes)
+    if ((KORD == 2 || (KORD == 4 && h->cur_f16)) && !z_out && fsm <= kFixedSmemMax &&
+        ld1 % ctm::kSeedFixedFeats == 0 && n > 0) {
       if (!h->seed_fixed_attr) {
         CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kFixedSmemMax));
@@ -605,18 +611,21 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
                                       (int)kFixedSmemMax));
         h->seed_fixed_attr = true;
       }
+      ctm::SeedF16 sf{};
       if (h->cur_f16) {  // fp16x3: bounds of this call's direction images, output record of layer 1
         if (!h->seed_f16_attr) {
           CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<2, 2, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixedSmemMax));
+          CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<4, 2, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixedSmemMax));
           h->seed_f16_attr = true;
         }
         launch_maxabs(UT, (int64_t)R * ld1, h->f16b, st);
         launch_maxabs(csum, (int64_t)pl.nb * ld1, h->f16b + 1, st);
         launches += 2;
-        sp.f16_bounds = h->f16b;
-        f16_act_sups(h->act, sp.s0, sp.s1, sp.s2);
-        sp.f16_out = h->f16rec + 1;
+        sf.bounds = h->f16b;
+        f16_act_sups(h->act, sf.s0, sf.s1, sf.s2, sf.s3, sf.s4);
+        sf.out = h->f16rec + 1;
       }
       // one wave: as many blocks as are resident at once (registers, shared memory)
       const int slices = ld1 / ctm::kSeedFixedFeats;
@@ -624,7 +633,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
       int per_sm = 1;
       CTM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm,
-          h->cur_f16 ? ctm::seed_fixed_kernel<2, 2, true>
+          h->cur_f16 ? (KORD == 4 ? ctm::seed_fixed_kernel<4, 2, true> : ctm::seed_fixed_kernel<2, 2, true>)
                      : (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3> : ctm::seed_fixed_kernel<2, 2>),
           thr, fsm));
       const int64_t want = std::max<int64_t>(1, (int64_t)h->sm_count * std::max(per_sm, 1) / slices);
@@ -633,11 +642,13 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
       const int64_t groups = (n + ppg - 1) / ppg;
       if (groups > 65535) return fail(CTM_EUNSUPPORTED, "batch too large for one call");
       const dim3 grid((unsigned)slices, (unsigned)groups);
-      if (h->cur_f16)
-        ctm::seed_fixed_kernel<2, 2, true><<<grid, thr, fsm, st>>>(sp, ppg);
+      if (h->cur_f16 && KORD == 4)
+        ctm::seed_fixed_kernel<4, 2, true><<<grid, thr, fsm, st>>>(sp, ppg, sf);
+      else if (h->cur_f16)
+        ctm::seed_fixed_kernel<2, 2, true><<<grid, thr, fsm, st>>>(sp, ppg, sf);
       else
-        (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3><<<grid, thr, fsm, st>>>(sp, ppg)
-                         : ctm::seed_fixed_kernel<2, 2><<<grid, thr, fsm, st>>>(sp, ppg));
+        (h->nplanes == 3 ? ctm::seed_fixed_kernel<2, 3><<<grid, thr, fsm, st>>>(sp, ppg, sf)
+                         : ctm::seed_fixed_kernel<2, 2><<<grid, thr, fsm, st>>>(sp, ppg, sf));
       ++launches;
       return CTM_OK;
     }
@@ -739,8 +750,9 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
         fa.in = h->f16rec + (gl.lidx - 1);
         fa.out = last ? nullptr : h->f16rec + gl.lidx;
         fa.wsc = h->f16w + 2 * gl.lidx;
-        f16_act_sups(h->act, fa.s0, fa.s1, fa.s2);
-        fa.rw = lp.weighted ? -1.f : (float)std::max(pl.rb, 1);
+        f16_act_sups(h->act, fa.s0, fa.s1, fa.s2, fa.s3, fa.s4);
+        // K=2: sum |w_r| = rb (unit weights) unless weighted; K=4: the jets' weights (from smem)
+        fa.rw = (lp.weighted || KORD == 4) ? -1.f : (float)std::max(pl.rb, 1);
         am = gl.amap16;
       }
       if (KORD == 2) {
@@ -754,7 +766,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
           default: s = launch_layer_kernel<2, 3>(h, grid, *am, mb, lp, st, fa); break;
         }
       } else if (KORD == 4) {
-        s = launch_layer_kernel<4, 0>(h, grid, *gl.amap, mb, lp, st);
+        s = launch_layer_kernel<4, 0>(h, grid, *am, mb, lp, st, fa);
       } else if (KORD == ctm::kNest) {
         s = launch_layer_kernel<ctm::kNest, 0>(h, grid, *gl.amap, mb, lp, st);
       } else if (KORD == ctm::kStd4) {
@@ -816,11 +828,14 @@ ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
 // operators of tanh / sin nets, random directions without sigma, >= 2 points per tile (no
 // split point), the streaming seed for fixed sets, and at least one tensor-core layer
 bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, bool grad, int R) {
-  if (h->prec != CTM_PRECISION_FP16X3 || grad || KORD != 2 || pl.ppt < 2) return false;
+  if (h->prec != CTM_PRECISION_FP16X3 || grad || (KORD != 2 && KORD != 4) || pl.ppt < 2) return false;
   if (h->act != ctm::kActTanh && h->act != ctm::kActSin) return false;
   const bool k2op = a.op == OP_LAP || a.op == OP_WLAP || a.op == OP_RLAP || a.op == OP_WLAP_X ||
                     (a.op == OP_DSUM && a.K == 2);
-  if (!k2op) return false;
+  // K=4: the fixed interpolation family and shared K=4 directional sums (the per-point K=4
+  // directions' layer 1 runs in fp32 on the CUDA cores, seed_stoch_biharmonic_kernel)
+  const bool k4op = a.op == OP_BIH || (a.op == OP_DSUM && a.K == 4 && !a.per_point);
+  if (!(KORD == 2 ? k2op : k4op)) return false;
   if (random_k2(a)) return a.sigma == nullptr;
   const int D = h->widths[0], ld1 = h->wpad[1];
   return h->L >= 3 && ctm::seed_fixed_smem(D, R, pl.nb) <= 200 * 1024 && ld1 % ctm::kSeedFixedFeats == 0;
@@ -1701,7 +1716,7 @@ ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float* B, int64_t 
       fa.in = h->f16rec;
       fa.out = h->f16rec + 1;
       fa.wsc = h->f16w + 2 * layer;
-      f16_act_sups(h->act, fa.s0, fa.s1, fa.s2);
+      f16_act_sups(h->act, fa.s0, fa.s1, fa.s2, fa.s3, fa.s4);
       fa.rw = (float)(P - 2);
     } else if (h->nplanes == 3) {
       ctm::split_rows_kernel<3><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(B, rows, w_in, rows_pad, kpad,

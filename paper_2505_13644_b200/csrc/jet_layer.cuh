@@ -190,11 +190,13 @@ __host__ __device__ constexpr int planes_of() {
 }
 
 // fp16x3 scale state of one slot block in device memory: the planes hold fp16 splits of
-// v * scale[t], t the slot type (0 primal, 1 first order, 2 collapsed top); the block's
-// producer records max |v| per type (float bits, atomicMax) for the next layer's bound.
+// v * scale[t], t the slot type (0 primal, 1 first order / K=4 h1, 2 collapsed top, 3 K=4 h2,
+// 4 K=4 h3); the block's producer records max |v| per type (float bits, atomicMax) for the
+// next layer's bound.
+constexpr int kF16Types = 5;
 struct F16Rec {
-  float scale[3];
-  unsigned maxabs[3];
+  float scale[kF16Types];
+  unsigned maxabs[kF16Types];
 };
 // per-launch fp16x3 arguments of a layer kernel (zero for the other modes)
 struct F16Args {
@@ -203,14 +205,15 @@ struct F16Args {
   const float* wsc;   // [0] 2^-(sa+11): the weights' factor in the accumulator (seed.cuh split_weights_f16_kernel),
                       // [1] ||W||_inf = max_m sum_k |W[m,k]|
   float s0, s1, s2;   // sup |s|, |s'|, |s''| of the activation
+  float s3, s4;       // sup of the third and fourth derivatives (K=4)
   float rw;           // sum_r |w_r| over one sub-point's directions (< 0: from the smem weights)
 };
 // the registers an fp16x3 epilogue thread carries: unscale factors of the accumulator per
 // slot type (2^-(sa+11) / scale_in[t]), scales of its output block, running max |output|
 struct F16Ctx {
-  float us[3];
-  float os[3];
-  float mx[3];
+  float us[kF16Types];
+  float os[kF16Types];
+  float mx[kF16Types];
 };
 // output scale of a slot type from a bound B on |v|: 2^(14 - e), B = m 2^e, m in [0.5, 1), so
 // |v * scale| <= 2^14 < 65504 (fp16 max)
@@ -231,6 +234,22 @@ __device__ __forceinline__ void f16_out_scales(const F16Args& a, float rw, float
   os[0] = f16_scale_for(a.s0);
   os[1] = f16_scale_for(a.s1 * g1);
   os[2] = f16_scale_for(a.s1 * G * Mt + a.s2 * rw * g1 * g1);
+  os[3] = os[4] = 1.f;
+}
+// The K=4 rule (cheat-sheet rows k <= 4) with g_k = G M_k the bounds of the
+// input jets' coefficients: |h1| <= s1 g1; |h2| <= s2 g1^2 + s1 g2;
+// |h3| <= s3 g1^3 + 3 s2 g1 g2 + s1 g3;
+// |top| <= Rw (s4 g1^4 + 6 s3 g1^2 g2 + 4 s2 g1 g3 + 3 s2 g2^2) + s1 G Mt.
+__device__ __forceinline__ void f16_out_scales4(const F16Args& a, float rw, float* os) {
+  const float G = a.wsc[1];
+  const float g1 = G * __uint_as_float(a.in->maxabs[1]), g2 = G * __uint_as_float(a.in->maxabs[3]),
+              g3 = G * __uint_as_float(a.in->maxabs[4]), gt = G * __uint_as_float(a.in->maxabs[2]);
+  os[0] = f16_scale_for(a.s0);
+  os[1] = f16_scale_for(a.s1 * g1);
+  os[3] = f16_scale_for(a.s2 * g1 * g1 + a.s1 * g2);
+  os[4] = f16_scale_for(a.s3 * g1 * g1 * g1 + 3.f * a.s2 * g1 * g2 + a.s1 * g3);
+  os[2] = f16_scale_for(rw * (a.s4 * g1 * g1 * g1 * g1 + 6.f * a.s3 * g1 * g1 * g2 + 4.f * a.s2 * g1 * g3 +
+                              3.f * a.s2 * g2 * g2) + a.s1 * gt);
 }
 
 template <int KORD, int FLAGS = 0>
@@ -239,7 +258,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
                                                int bar_id, float& fpart, float& opart, F16Ctx* fc = nullptr) {
   constexpr int NPL = planes_of<FLAGS>();
   constexpr bool F16 = (FLAGS & kFlagF16) != 0;  // fp16x3: unscale what is read, scale what is stored
-  static_assert(!F16 || KORD == 2, "fp16x3: K=2 collapsed rule only");
+  static_assert(!F16 || KORD == 2 || KORD == 4, "fp16x3: K=2 and K=4 collapsed rules only");
   const int P = p.P;
   const int ld = p.ldo;
   constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
@@ -274,11 +293,12 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   //      standard-mode pairs (z1_r, z2_r) with no collapse
   float acc = 0.f;  // the collapsed sum over directions (standard: sum_r h2_r at readout)
   int jj = (KORD == 4) ? (mb - 1) / 3 : (KORD == kStd4) ? (mb - 1) / 4 : mb - 1;  // first direction / jet
-  auto put = [&](float h) {
+  // type: the fp16x3 slot type of the stored value (1 first order / h1, 3 h2, 4 h3)
+  auto put = [&](float h, int type = 1) {
     if (!p.readout) {
       if constexpr (F16) {
-        ptx::store_f16_off(q0, q1, off, h * fc->os[1]);
-        fc->mx[1] = fmaxf(fc->mx[1], fabsf(h));
+        ptx::store_f16_off(q0, q1, off, h * fc->os[type]);
+        fc->mx[type] = fmaxf(fc->mx[type], fabsf(h));
       } else {
         ptx::store_planes_off<NPL>(q0, q1, q2, off, h);
       }
@@ -289,9 +309,14 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     // jets (z1, z2, z3), read 5 at a time (15 of 16 columns) so each slot's role is a
     // compile-time index in the unrolled loop
     auto jet = [&](float z1, float z2, float z3) {
-      put(d1 * z1);
-      put(d2 * z1 * z1 + d1 * z2);
-      put(d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3);
+      if constexpr (F16) {  // fp16x3: the jet's coefficients carry the scales of types 1, 3, 4
+        z1 *= fc->us[1];
+        z2 *= fc->us[3];
+        z3 *= fc->us[4];
+      }
+      put(d1 * z1, 1);
+      put(d2 * z1 * z1 + d1 * z2, 3);
+      put(d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3, 4);
       const float nl = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 + 3.f * d2 * z2 * z2;
       acc = fmaf(jw[jj], nl, acc);
       ++jj;
@@ -971,7 +996,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     if constexpr (F16) {
       const float wsi = f16.wsc[0];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
+      for (int t = 0; t < kF16Types; ++t) {
         fcx.us[t] = wsi / f16.in->scale[t];
         fcx.mx[t] = 0.f;
       }
@@ -985,9 +1010,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
             rw = fmaxf(rw, sb);
           }
         }
-        f16_out_scales(f16, rw, fcx.os);
+        if (KORD == 4)
+          f16_out_scales4(f16, rw, fcx.os);
+        else
+          f16_out_scales(f16, rw, fcx.os);
         if (blockIdx.x == 0 && threadIdx.x == 64)
-          for (int t = 0; t < 3; ++t) f16.out->scale[t] = fcx.os[t];
+          for (int t = 0; t < kF16Types; ++t) f16.out->scale[t] = fcx.os[t];
       }
     }
     F16Ctx* const fc = F16 ? &fcx : nullptr;
@@ -1103,7 +1131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     if constexpr (F16) {  // this thread's output maxima per slot type into the block's record
       if (f16.out) {
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
+        for (int t = 0; t < (KORD == 4 ? kF16Types : 3); ++t) {
           float v = fcx.mx[t];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -47,11 +47,14 @@ struct SeedParams {
   int nplanes;
   int act;               // kAct*
   float* z_out;          // K=2, grad mode (one block): pre-activations [N*P, ld] (z0, W1 u_r, 0) or nullptr
-  // fp16x3 mode (seed_fixed_kernel<2, 2, true>): bounds [max |U|, max |csum|] (float bits) of
-  // this call's direction images, sup |s|, |s'|, |s''|, and the layer-1 block's record
-  const unsigned* f16_bounds;
-  float s0, s1, s2;
-  F16Rec* f16_out;
+};
+// fp16x3 mode of seed_fixed_kernel (a parameter of its own: growing SeedParams made ptxas
+// spill in seed_layer_kernel<4, 3>): bounds [max |U|, max |csum|] (float bits) of this call's
+// direction images, the sups of |s| and its first four derivatives, the layer-1 block's record
+struct SeedF16 {
+  const unsigned* bounds;
+  float s0, s1, s2, s3, s4;
+  F16Rec* out;
 };
 
 // Where a kernel writes its bf16 planes: plane k of element i at base[k * pstride + i].
@@ -318,7 +321,8 @@ __host__ __device__ inline size_t seed_fixed_smem(int D, int R, int blocks) {
 }
 
 template <int KORD, int NP, bool F16 = false>
-__global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const SeedParams p, int64_t pts_per_group) {
+__global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const SeedParams p, int64_t pts_per_group,
+                                                                          const SeedF16 f) {
   extern __shared__ float sm[];
   constexpr int F = kSeedFixedFeats;
   float* w1s = sm;                          // [D][F]
@@ -344,25 +348,29 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
   const int64_t nb = blockIdx.y * pts_per_group;
   const int64_t ne = (nb + pts_per_group < p.n_points) ? nb + pts_per_group : p.n_points;
   constexpr int ROWS = (KORD == 4) ? 3 : 1;  // rows per direction (jet)
-  static_assert(!F16 || (KORD == 2 && NP == 2), "fp16x3: K=2, two planes");
-  // fp16x3: output scales per slot type from |h0| <= s0, |s' u| <= s1 max|U|, |s'' csum| <= s2 max|csum|
-  float os0 = 1.f, os1 = 1.f, os2 = 1.f, mx0 = 0.f, mx1 = 0.f, mx2 = 0.f;
+  static_assert(!F16 || NP == 2, "fp16x3: two planes");
+  // fp16x3: output scales per slot type (jet_layer.cuh F16Rec) from |h0| <= s0 and, with
+  // U = max|U| and C = max|csum|: K=2 |s' u| <= s1 U, |s'' csum| <= s2 C; K=4 |s' u| <= s1 U,
+  // |s'' u^2| <= s2 U^2, |s''' u^3| <= s3 U^3, |s'''' csum| <= s4 C
+  float os[kF16Types], mx[kF16Types];
+#pragma unroll
+  for (int t = 0; t < kF16Types; ++t) os[t] = 1.f, mx[t] = 0.f;
   if (F16) {
-    os0 = f16_scale_for(p.s0);
-    os1 = f16_scale_for(p.s1 * __uint_as_float(p.f16_bounds[0]));
-    os2 = f16_scale_for(p.s2 * __uint_as_float(p.f16_bounds[1]));
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-      p.f16_out->scale[0] = os0;
-      p.f16_out->scale[1] = os1;
-      p.f16_out->scale[2] = os2;
+    const float U = __uint_as_float(f.bounds[0]), C = __uint_as_float(f.bounds[1]);
+    os[0] = f16_scale_for(f.s0);
+    os[1] = f16_scale_for(f.s1 * U);
+    os[2] = f16_scale_for((KORD == 4 ? f.s4 : f.s2) * C);
+    if (KORD == 4) {
+      os[3] = f16_scale_for(f.s2 * U * U);
+      os[4] = f16_scale_for(f.s3 * U * U * U);
     }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+      for (int t = 0; t < kF16Types; ++t) f.out->scale[t] = os[t];
   }
   auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
     if constexpr (F16) {
-      const float sc = type == 0 ? os0 : type == 1 ? os1 : os2;
-      seed_store4_f16(o, idx, a, b, c, d, sc);
-      const float mv = max4abs(a, b, c, d);
-      if (type == 0) mx0 = fmaxf(mx0, mv); else if (type == 1) mx1 = fmaxf(mx1, mv); else mx2 = fmaxf(mx2, mv);
+      seed_store4_f16(o, idx, a, b, c, d, os[type]);
+      mx[type] = fmaxf(mx[type], max4abs(a, b, c, d));
     } else {
       seed_store4<NP>(o, idx, a, b, c, d);
     }
@@ -397,23 +405,21 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
         put4(row * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w, 1);
         if (KORD == 4) {
-          seed_store4<NP>(o, (row + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z,
-                          d2[3] * u.w * u.w);
-          seed_store4<NP>(o, (row + 2) * p.ld + m, d3[0] * u.x * u.x * u.x, d3[1] * u.y * u.y * u.y,
-                          d3[2] * u.z * u.z * u.z, d3[3] * u.w * u.w * u.w);
+          put4((row + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z, d2[3] * u.w * u.w, 3);
+          put4((row + 2) * p.ld + m, d3[0] * u.x * u.x * u.x, d3[1] * u.y * u.y * u.y, d3[2] * u.z * u.z * u.z,
+               d3[3] * u.w * u.w * u.w, 4);
         }
       }
       const float4 q = *reinterpret_cast<const float4*>(cs + (size_t)b * F + c);
       if (KORD == 4)
-        seed_store4<NP>(o, row * p.ld + m, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w);
+        put4(row * p.ld + m, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w, 2);
       else
         put4(row * p.ld + m, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w, 2);
     }
   }
   if constexpr (F16) {
-    warp_max_record(mx0, &p.f16_out->maxabs[0]);
-    warp_max_record(mx1, &p.f16_out->maxabs[1]);
-    warp_max_record(mx2, &p.f16_out->maxabs[2]);
+#pragma unroll
+    for (int t = 0; t < (KORD == 4 ? kF16Types : 3); ++t) warp_max_record(mx[t], &f.out->maxabs[t]);
   }
 }
 
@@ -577,7 +583,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       p.f16_out->scale[0] = os0;
       p.f16_out->scale[1] = os1;
-      p.f16_out->scale[2] = 1.f;
+      for (int t = 2; t < kF16Types; ++t) p.f16_out->scale[t] = 1.f;
     }
   }
   auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
@@ -882,7 +888,7 @@ __global__ void split_rows_kernel(const float* __restrict__ src, int64_t rows, i
 // measured max |B| and that max) from the bound scratch b[0]
 __global__ void probe_f16_record_kernel(const unsigned* __restrict__ b, F16Rec* __restrict__ rec) {
   const float m = __uint_as_float(b[0]);
-  for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < kF16Types; ++t) {
     rec->scale[t] = f16_scale_for(m);
     rec->maxabs[t] = b[0];
   }

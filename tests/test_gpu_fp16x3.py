@@ -63,7 +63,9 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.randomized_laplacian(X, S=4, seed=1, sigma=torch.from_numpy(make_sigma(5, 5)).cuda())
     assert m.last_precision() == "fp32"  # sigma: not covered
     m.biharmonic(X)
-    assert m.last_precision() == "fp32"
+    assert m.last_precision() == "fp16x3"  # K=4, the interpolation family
+    m.stochastic_biharmonic(X, S=3, seed=2)
+    assert m.last_precision() == "fp32"  # per-point K=4 directions: layer 1 on the CUDA cores
     m.biharmonic_nested(X)
     assert m.last_precision() == "fp32"
     m.laplacian_standard(X)
@@ -117,21 +119,35 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
         assert m.last_precision() == "fp16x3"
         want, _, norm = O.directional_sum(onet, Xd, 2, dirs.astype(np.float64), w.astype(np.float64))
         _check(got, want, norm)
+    if D <= 7:  # K=4: the biharmonic family and a shared K=4 directional sum
+        want, _, norm = O.biharmonic(onet, Xd)
+        _check(m.biharmonic(Xc)[0], want, norm)
+        assert m.last_precision() == "fp16x3"
+    dirs = gaussian_directions(1, 4, D, seed=9)[0]
+    w4 = signed_weights(4)
+    got = m.directional_sum(Xc, 4, torch.from_numpy(dirs).cuda(), torch.from_numpy(w4).cuda())[0]
+    assert m.last_precision() == "fp16x3"
+    want, _, norm = O.directional_sum(onet, Xd, 4, dirs.astype(np.float64), w4.astype(np.float64))
+    _check(got, want, norm)
     m.close()
 
 
-@pytest.mark.parametrize("op,S", [("laplacian", 0), ("randomized", 8), ("randomized", 128)])
+@pytest.mark.parametrize("op,S", [("laplacian", 0), ("randomized", 8), ("randomized", 128), ("biharmonic", 0)])
 def test_fp16x3_full_size_sampled(ctm, op, S):
-    """BASELINE C1 / C3 at N = 16384 in the bench's launch configuration, 256 sampled points."""
-    params, onet = _nets(widths_for(50), 0)
+    """BASELINE C1 / C3 / C4 at N = 16384 in the bench's launch configuration, 256 sampled points."""
+    D = 5 if op == "biharmonic" else 50
+    params, onet = _nets(widths_for(D), 0)
     N = 16384
-    X = points(N, 50)
+    X = points(N, D)
     m = _mlp(ctm, params)
     idx = np.unique(np.minimum(np.arange(0, N, N // 256)[:256] + np.arange(256) % 16, N - 1))
     Xs = X[idx].astype(np.float64)
     if op == "laplacian":
         got = m.laplacian(torch.from_numpy(X).cuda())[0]
         want, _, norm = O.laplacian(onet, Xs)
+    elif op == "biharmonic":
+        got = m.biharmonic(torch.from_numpy(X).cuda())[0]
+        want, _, norm = O.biharmonic(onet, Xs)
     else:
         got = m.randomized_laplacian(torch.from_numpy(X).cuda(), S=S, seed=2)[0]
         V = np.concatenate([O.rademacher(2, int(n), 1, S, 50) for n in idx])
