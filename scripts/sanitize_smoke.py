@@ -10,7 +10,7 @@ import paper_2505_13644_b200 as ctm  # noqa: E402
 from synth import gaussian_directions, mlp_params, points, sigma, sigma_field, signed_weights  # noqa: E402
 
 for widths, prec in (([5, 16, 16, 1], "fp32"), ([50, 64, 64, 1], "fp32"), ([50, 64, 64, 1], "bf16x3"),
-                     ([3, 16, 130, 1], "fp32")):
+                     ([3, 16, 130, 1], "fp32"), ([5, 16, 16, 1], "fp16x3"), ([50, 64, 64, 1], "fp16x3")):
     D = widths[0]
     params = mlp_params(widths, 0)
     mlp = ctm.MLP([(torch.from_numpy(W), torch.from_numpy(b)) for W, b in params], device=0)
