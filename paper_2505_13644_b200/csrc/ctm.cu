@@ -117,6 +117,7 @@ struct ctm_mlp {
   int nplanes = 3;
   int prec = 0;               // ctm_precision of the handle
   bool cur_f16 = false;       // this call runs in the fp16x3 mode
+  bool f16_stale = true;      // the fp16x3 weights do not match the bf16 planes (rebuilt on demand)
   // fp16x3 mode: fp16 weight planes [3][Mpad, Kpad] with per-layer power-of-two scales
   // (seed.cuh split_weights_f16_kernel), their statistics f16w[2 l] = 2^-(sa+11) (the
   // accumulator's weight factor), f16w[2 l + 1] = ||W_l||_inf (l = 1 .. L-1; layer 1 = W1p),
@@ -1243,6 +1244,25 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
 }
 
 // Every array derived from the weights, written on `st` (load and ctm_set_weights):
+// fp16x3 weight planes and statistics of every tensor-core layer (layer 1's W1p and the
+// hidden GEMM layers), from their bf16 planes (seed.cuh split_weights_f16_kernel)
+void derive_f16_weights(ctm_mlp* h, cudaStream_t st) {
+  const int L = h->L, ld1 = h->wpad[1];
+  {
+    const int64_t n = (int64_t)ld1 * h->k1pad;
+    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(h->W1p, ld1, h->k1pad, h->f16w + 2);
+    ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->W1p, n, h->f16w + 2, h->W1p16);
+  }
+  for (int l = 2; l <= L - 1; ++l) {
+    const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
+    const int64_t n = (int64_t)mpad * kpad;
+    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(h->Wp[l - 2], mpad, kpad, h->f16w + 2 * l);
+    ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Wp[l - 2], n, h->f16w + 2 * l,
+                                                                               h->Wp16[l - 2]);
+  }
+  h->f16_stale = false;
+}
+
 // W1^T and b1, the bf16 pairs of every tensor-core layer (and W_l^T in grad mode), the
 // padded output weights, and the fixed direction sets' U = W1 V, c = sum w (W1 v)^K.
 void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cudaStream_t st) {
@@ -1256,17 +1276,6 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
     const int64_t n = (int64_t)ld1 * h->k1pad;
     ctm::split_weights_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], b[0], h->widths[1], D, ld1, h->k1pad,
                                                                            h->W1p, h->b1);
-    // fp16x3: scale and ||W1||_inf, then the fp16 planes of W1 * 2^sa
-    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(W[0], h->widths[1], D, h->f16w + 2);
-    ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W[0], h->widths[1], D, ld1, h->k1pad,
-                                                                               h->f16w + 2, h->W1p16);
-  }
-  for (int l = 2; l <= L - 1; ++l) {
-    const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
-    const int64_t n = (int64_t)mpad * kpad;
-    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(W[l - 1], h->widths[l], h->widths[l - 1], h->f16w + 2 * l);
-    ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        W[l - 1], h->widths[l], h->widths[l - 1], mpad, kpad, h->f16w + 2 * l, h->Wp16[l - 2]);
   }
   for (int l = 2; l <= L - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
@@ -1286,7 +1295,15 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
   if (h->J_bih)
     ctm::prep_directions_kernel<<<(ld1 + 127) / 128, 128, 0, st>>>(h->W1T, D, ld1, h->bih_dirs, h->J_bih, h->w_bih, 4,
                                                                    h->U_bih, h->c_bih);
-  h->last_launches = 4 + (L - 2) * (h->WTp.empty() ? 1 : 2) + (h->J_bih ? 1 : 0) + 2 * (L - 1);
+  h->last_launches = 4 + (L - 2) * (h->WTp.empty() ? 1 : 2) + (h->J_bih ? 1 : 0);
+  // the fp16x3 weights follow (after the bf16 planes, from which they are derived) only if
+  // the handle is in that mode; otherwise they are rebuilt when it switches to it
+  if (h->prec == CTM_PRECISION_FP16X3) {
+    derive_f16_weights(h, st);
+    h->last_launches += 2 * (L - 1);
+  } else {
+    h->f16_stale = true;
+  }
   h->tape.valid = false;
 }
 
@@ -1609,6 +1626,11 @@ ctm_status ctm_set_precision(ctm_mlp_t mlp, ctm_precision prec) {
     return fail(CTM_EINVAL, "unknown precision");
   mlp->prec = prec;
   mlp->nplanes = (prec == CTM_PRECISION_FP32) ? 3 : 2;
+  if (prec == CTM_PRECISION_FP16X3 && mlp->f16_stale) {  // host-side call: build and wait
+    DeviceGuard g(mlp->device);
+    derive_f16_weights(mlp, 0);
+    CTM_CUDA(cudaDeviceSynchronize());
+  }
   mlp->tape.valid = false;
   return CTM_OK;
 }

@@ -797,17 +797,24 @@ __global__ void split_weights_kernel(const float* __restrict__ W, const float* _
   if (c == 0) bpad[r] = (r < rows) ? b[r] : 0.f;
 }
 
-// fp16x3 weight statistics (one block): out[0] = 2^-(sa + 11) with max|W| * 2^sa in (4, 8]
-// (the factor that undoes the planes' scales, see split_weights_f16_kernel), out[1] = ||W||_inf
-// = max_m sum_k |W[m, k]| (the bound of jet_layer.cuh f16_out_scales). W [rows, cols] row-major.
-__global__ void __launch_bounds__(1024) f16_weight_stats_kernel(const float* __restrict__ W, int rows, int cols,
+// fp16x3 weights, derived from the weights' three bf16 planes Wp [3][Mpad, Kpad] (their sum
+// rounds to the fp32 weight exactly: p0 + p1 + p2 is within 2^-27 of it), so they can be
+// (re)built whenever the handle switches to the mode, without the caller's arrays.
+__device__ __forceinline__ float planes3_val(const uint16_t* Wp, int64_t n, int64_t i) {
+  return ptx::bf16_val(Wp[i]) + ptx::bf16_val(Wp[n + i]) + ptx::bf16_val(Wp[2 * n + i]);
+}
+// statistics (one block): out[0] = 2^-(sa + 11) = 1 / (the scale putting max |W| in
+// (2^13, 2^14]), the factor that undoes the planes' scales (split_weights_f16_kernel);
+// out[1] = ||W||_inf = max_m sum_k |W[m, k]| (the bound of jet_layer.cuh f16_out_scales)
+__global__ void __launch_bounds__(1024) f16_weight_stats_kernel(const uint16_t* __restrict__ Wp, int rows, int cols,
                                                                float* __restrict__ out) {
   __shared__ float smax[32], ssum[32];
+  const int64_t n = (int64_t)rows * cols;
   float mx = 0.f, rs = 0.f;
   for (int r = threadIdx.x >> 5; r < rows; r += 32) {  // one warp per row
     float a = 0.f, m = 0.f;
     for (int c = threadIdx.x & 31; c < cols; c += 32) {
-      const float v = fabsf(W[(size_t)r * cols + c]);
+      const float v = fabsf(planes3_val(Wp, n, (int64_t)r * cols + c));
       a += v;
       m = fmaxf(m, v);
     }
@@ -832,22 +839,21 @@ __global__ void __launch_bounds__(1024) f16_weight_stats_kernel(const float* __r
     out[1] = rs;
   }
 }
-// fp16x3 weight planes [3][Mpad, Kpad], zero padded: p0 = rn_f16(W 2^sa), p1 = rn_f16((W 2^sa -
-// p0) 2^11) (the corrections' operands: p1 * B0 and p0 * B1 both carry 2^(sa + 11 + sb)), and
-// p0 2^11 (exact) for the leading product with B0 in phase 2 (the same 2^(sa + 11 + sb)).
-__global__ void split_weights_f16_kernel(const float* __restrict__ W, int rows, int cols, int Mpad, int Kpad,
-                                         const float* __restrict__ stats, uint16_t* __restrict__ Wp) {
+// fp16x3 weight planes [3][Mpad, Kpad] (zero padding stays zero): p0 = rn_f16(W 2^sa),
+// p1 = rn_f16((W 2^sa - p0) 2^11) (the corrections' operands: p1 * B0 and p0 * B1 both carry
+// 2^(sa + 11 + sb)), and p0 2^11 (exact) for the leading product with B0 in phase 2 (the same
+// 2^(sa + 11 + sb)).
+__global__ void split_weights_f16_kernel(const uint16_t* __restrict__ Wp, int64_t n, const float* __restrict__ stats,
+                                         uint16_t* __restrict__ W16) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = (int64_t)Mpad * Kpad;
   if (i >= n) return;
-  const int r = (int)(i / Kpad), c = (int)(i % Kpad);
   // W * 2^sa with 2^sa = 1 / (stats[0] 2^11): exact (powers of two)
-  const float v = (r < rows && c < cols) ? W[(size_t)r * cols + c] / (stats[0] * ptx::kF16Lift) : 0.f;
+  const float v = planes3_val(Wp, n, i) / (stats[0] * ptx::kF16Lift);
   uint16_t p0, p1;
   ptx::f16_split(v, p0, p1);
-  Wp[i] = p0;
-  Wp[n + i] = p1;
-  Wp[2 * n + i] = __half_as_ushort(__float2half_rn(__half2float(__ushort_as_half(p0)) * ptx::kF16Lift));
+  W16[i] = p0;
+  W16[n + i] = p1;
+  W16[2 * n + i] = __half_as_ushort(__float2half_rn(__half2float(__ushort_as_half(p0)) * ptx::kF16Lift));
 }
 // max |a_i| over n floats into a record (float bits, atomicMax; the record is zeroed by the caller)
 __global__ void maxabs_kernel(const float* __restrict__ a, int64_t n, unsigned* __restrict__ out) {
