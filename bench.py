@@ -4,7 +4,9 @@
 One step = one full pass of the hot path (seed + layer 1,
 the three fused tcgen05 layers, readout) over one batch of synthetic points:
 config C1 = exact Laplacian of the tanh MLP 50-768-768-512-512-1 on
-N = 16384 points per GPU, in the library's default fp32 mode.
+N = 16384 points per GPU, in the fp16x3 mode: north_star's 3xTF32 operand split
+(11 + 11 significant bits) on fp16 tensor cores, three products per useful product
+(DESIGN.md §5); --precision fp32 times the library's default 24-bit mode (bf16x6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--scaling weak|strong] [--precision fp32|fp16x3|bf16x3] [--op ...]
@@ -65,7 +67,7 @@ def parse():
     ap.add_argument("--S", type=int, default=8, help="samples for --op randomized")
     ap.add_argument("--direction-block", type=int, default=0,
                     help="directions per block (ctm_set_direction_block); 0 = the library's planner")
-    ap.add_argument("--precision", choices=["fp32", "fp16x3", "bf16x3"], default="fp32",
+    ap.add_argument("--precision", choices=["fp32", "fp16x3", "bf16x3"], default="fp16x3",
                     help="layer-contraction arithmetic (ctm_set_precision, DESIGN.md §5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-precisions", action="store_true",
@@ -545,7 +547,7 @@ def main():
     # flush between timed steps, CUDA events, max over ranks), for the line's `other_precisions`
     others = {}
     if not train and not args.no_other_precisions:
-        for prec in [q for q in ("fp32", "fp16x3", "bf16x3") if q != args.precision]:
+        for prec in [q for q in ("fp32", "fp16x3", "bf16x3") if q not in (args.precision, ran)]:
             mlp.set_precision(prec)
             for _ in range(3):
                 step(X)

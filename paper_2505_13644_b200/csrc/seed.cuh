@@ -67,38 +67,47 @@ struct PlaneOut {
 // four adjacent features -> one 8-byte store into each of the NP planes (plane by plane,
 // so only the four residuals stay live: the seed kernels run at 40-48 registers)
 template <int NP>
-__device__ __forceinline__ void seed_store4(const PlaneOut& o, size_t idx, float a, float b, float c, float d) {
+__device__ __forceinline__ void seed_store4_at(uint16_t* dst, int64_t pstride, float a, float b, float c, float d) {
   float r[4] = {a, b, c, d};
-  uint16_t* dst = o.base + idx;
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
-    uint32_t h[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const __nv_bfloat16 q = __float2bfloat16_rn(r[i]);
-      h[i] = __bfloat16_as_ushort(q);
-      r[i] -= __bfloat162float(q);  // exact in fp32
+    // packed round-to-nearest conversions (one F2FP per pair, the same bits as two scalar
+    // cvt.rn.bf16.f32) and the residuals exact in fp32
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(r[0], r[1]), hi = __floats2bfloat162_rn(r[2], r[3]);
+    if (k + 1 < NP) {
+      const float2 fl = __bfloat1622float2(lo), fh = __bfloat1622float2(hi);
+      r[0] -= fl.x;
+      r[1] -= fl.y;
+      r[2] -= fh.x;
+      r[3] -= fh.y;
     }
-    *reinterpret_cast<uint2*>(dst) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
-    dst += o.pstride;
+    *reinterpret_cast<uint2*>(dst) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    dst += pstride;
   }
 }
+template <int NP>
+__device__ __forceinline__ void seed_store4(const PlaneOut& o, size_t idx, float a, float b, float c, float d) {
+  seed_store4_at<NP>(o.base + idx, o.pstride, a, b, c, d);
+}
 
-// fp16x3 mode (jet_layer.cuh kFlagF16): four adjacent features as two fp16 planes of v * sc
+// fp16x3 mode (jet_layer.cuh kFlagF16): four adjacent ALREADY SCALED features x = v * sc as
+// two fp16 planes, p0 = rn_f16(x), p1 = rn_f16((x - p0) * 2^11) (ptx::f16_split, packed)
+__device__ __forceinline__ void seed_store4_f16s(uint16_t* dst, int64_t pstride, float x0, float x1, float x2,
+                                                 float x3) {
+  const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn((x0 - f01.x) * ptx::kF16Lift, (x1 - f01.y) * ptx::kF16Lift);
+  const __half2 l23 = __floats2half2_rn((x2 - f23.x) * ptx::kF16Lift, (x3 - f23.y) * ptx::kF16Lift);
+  *reinterpret_cast<uint2*>(dst) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  *reinterpret_cast<uint2*>(dst + pstride) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+}
+// (unscaled values: scales them first; the per-element products v * sc are exact)
 __device__ __forceinline__ void seed_store4_f16(const PlaneOut& o, size_t idx, float a, float b, float c, float d,
                                                 float sc) {
-  const float x[4] = {a * sc, b * sc, c * sc, d * sc};
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint16_t p0, p1;
-    ptx::f16_split(x[i], p0, p1);
-    h[i] = p0;
-    l[i] = p1;
-  }
-  uint16_t* dst = o.base + idx;
-  *reinterpret_cast<uint2*>(dst) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
-  *reinterpret_cast<uint2*>(dst + o.pstride) = make_uint2(l[0] | (l[1] << 16), l[2] | (l[3] << 16));
+  seed_store4_f16s(o.base + idx, o.pstride, a * sc, b * sc, c * sc, d * sc);
 }
 __device__ __forceinline__ float max4abs(float a, float b, float c, float d) {
   return fmaxf(fmaxf(fabsf(a), fabsf(b)), fmaxf(fabsf(c), fabsf(d)));
@@ -321,7 +330,7 @@ __host__ __device__ inline size_t seed_fixed_smem(int D, int R, int blocks) {
 }
 
 template <int KORD, int NP, bool F16 = false>
-__global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const SeedParams p, int64_t pts_per_group,
+__global__ void __launch_bounds__(kSeedFixedWarps * 32, 4) seed_fixed_kernel(const SeedParams p, int64_t pts_per_group,
                                                                           const SeedF16 f) {
   extern __shared__ float sm[];
   constexpr int F = kSeedFixedFeats;
@@ -340,7 +349,6 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
     *reinterpret_cast<float4*>(sm + (size_t)row * F + c4) = ldg4(src + f0 + c4);
   }
   __syncthreads();
-  const PlaneOut o{p.out, p.pstride, p.nplanes};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = 4 * lane;
   const int m = f0 + c;
@@ -367,14 +375,18 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
       for (int t = 0; t < kF16Types; ++t) f.out->scale[t] = os[t];
   }
-  auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
+  // one row of 4 adjacent features at dst: fp16x3 takes values ALREADY scaled for their slot
+  // type (the per-point derivative factors carry the scale: (s1 sc) u = (s1 u) sc exactly, as
+  // sc is a power of two) and tracks the type's max |scaled value|; unscaled at the end
+  auto put4 = [&](uint16_t* dst, float a, float b, float c, float d, int type) {
     if constexpr (F16) {
-      seed_store4_f16(o, idx, a, b, c, d, os[type]);
+      seed_store4_f16s(dst, p.pstride, a, b, c, d);
       mx[type] = fmaxf(mx[type], max4abs(a, b, c, d));
     } else {
-      seed_store4<NP>(o, idx, a, b, c, d);
+      seed_store4_at<NP>(dst, p.pstride, a, b, c, d);
     }
   };
+  const int64_t ld = p.ld;
   for (int64_t n = nb + warp; n < ne; n += kSeedFixedWarps) {
     for (int d = lane; d < p.D; d += 32) xw[d] = __ldg(p.X + n * p.D + d);
     __syncwarp();
@@ -391,35 +403,47 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32) seed_fixed_kernel(const 
     // (four explicit calls: a loop over a local array was not unrolled and went to local memory)
     const ActD A0 = act_derivs(p.act, z0.x), A1 = act_derivs(p.act, z0.y), A2 = act_derivs(p.act, z0.z),
                A3 = act_derivs(p.act, z0.w);
-    const float t[4] = {A0.d0, A1.d0, A2.d0, A3.d0}, d1[4] = {A0.d1, A1.d1, A2.d1, A3.d1},
-                d2[4] = {A0.d2, A1.d2, A2.d2, A3.d2}, d3[4] = {A0.d3, A1.d3, A2.d3, A3.d3},
-                d4[4] = {A0.d4, A1.d4, A2.d4, A3.d4};
+    // slot-type scales of the rows (all 1 outside fp16x3): h0 (type 0), s1 u (1), the top (2);
+    // K=4 also s2 u^2 (3) and s3 u^3 (4)
+    const float sc0 = os[0], sc1 = os[1], sc2 = os[2];
+    const float sc3 = (KORD == 4) ? os[3] : 1.f, sc4 = (KORD == 4) ? os[4] : 1.f;
+    const float d2s = (KORD == 4) ? sc3 : sc2;  // K=2: s'' multiplies the top row
+    const float t[4] = {A0.d0 * sc0, A1.d0 * sc0, A2.d0 * sc0, A3.d0 * sc0},
+                d1[4] = {A0.d1 * sc1, A1.d1 * sc1, A2.d1 * sc1, A3.d1 * sc1},
+                d2[4] = {A0.d2 * d2s, A1.d2 * d2s, A2.d2 * d2s, A3.d2 * d2s},
+                d3[4] = {A0.d3 * sc4, A1.d3 * sc4, A2.d3 * sc4, A3.d3 * sc4},
+                d4[4] = {A0.d4 * sc2, A1.d4 * sc2, A2.d4 * sc2, A3.d4 * sc2};
+    uint16_t* dst = p.out + (size_t)n * p.blocks * p.P * ld + m;  // row (n * blocks + b) * P + slot
     for (int b = 0; b < p.blocks; ++b) {
-      const size_t row0 = ((size_t)n * p.blocks + b) * p.P;
       const int r0 = b * p.rb;
       const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;
-      put4(row0 * p.ld + m, t[0], t[1], t[2], t[3], 0);
-      size_t row = row0 + 1;
-      for (int r = r0; r < r0 + p.rb; ++r, row += ROWS) {
+      put4(dst, t[0], t[1], t[2], t[3], 0);
+      dst += ld;
+      for (int r = r0; r < r0 + p.rb; ++r) {
+        // the padding directions of a last block (r >= r1) are zero rows
         const float4 u = (r < r1) ? *reinterpret_cast<const float4*>(us + (size_t)r * F + c)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-        put4(row * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w, 1);
+        put4(dst, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w, 1);
+        dst += ld;
         if (KORD == 4) {
-          put4((row + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z, d2[3] * u.w * u.w, 3);
-          put4((row + 2) * p.ld + m, d3[0] * u.x * u.x * u.x, d3[1] * u.y * u.y * u.y, d3[2] * u.z * u.z * u.z,
+          put4(dst, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z, d2[3] * u.w * u.w, 3);
+          dst += ld;
+          put4(dst, d3[0] * u.x * u.x * u.x, d3[1] * u.y * u.y * u.y, d3[2] * u.z * u.z * u.z,
                d3[3] * u.w * u.w * u.w, 4);
+          dst += ld;
         }
       }
       const float4 q = *reinterpret_cast<const float4*>(cs + (size_t)b * F + c);
       if (KORD == 4)
-        put4(row * p.ld + m, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w, 2);
+        put4(dst, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w, 2);
       else
-        put4(row * p.ld + m, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w, 2);
+        put4(dst, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w, 2);
+      dst += ld;
     }
   }
   if constexpr (F16) {
 #pragma unroll
-    for (int t = 0; t < (KORD == 4 ? kF16Types : 3); ++t) warp_max_record(mx[t], &f.out->maxabs[t]);
+    for (int t = 0; t < (KORD == 4 ? kF16Types : 3); ++t) warp_max_record(mx[t] / os[t], &f.out->maxabs[t]);
   }
 }
 
