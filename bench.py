@@ -424,9 +424,7 @@ def main():
     if train:
         mlp.laplacian(X, out=op_out, f_out=f_out)  # plan of the forward
     plan = mlp.last_plan()
-    ran = "fp32" if train else mlp.last_precision()  # training runs the fp32 mode in every precision but bf16x3
-    if train and args.precision == "bf16x3":
-        ran = "bf16x3"
+    ran = mlp.last_precision()  # the arithmetic the calls ran in (training: the forward's, which the backward follows)
     prods = 6 if ran == "fp32" else 3
 
     clocks = ClockSampler(local)

@@ -34,13 +34,39 @@ struct TopBwdParams {
   int ldo;
   float* dw_part;       // [G, width] partials of dW_L
   int G;
+  // fp16x3 (top_bwd_kernel<true>): Z_bar as two scaled fp16 planes with ONE scale from the
+  // bounds zb = {max |z1|, max |z_top|} of Z and bb (f16_bwd_prep_kernel); maxima per slot type
+  // into f16_out
+  const float* zb;
+  const float* bb;
+  float s1, s2, s3;     // sups of the activation's first three derivatives
+  F16Rec* f16_out;
 };
 
 // grid (width / 128, G); a thread owns one feature and the points n = g, g + G, ...
+// fp16x3 bounds (F16), TB = |c| max|gop| max|w_L|, HB = max|gf| max|w_L|:
+//   |ztb| <= s1 TB;  |z1b_r| <= 2 s2 w Z1 TB;  |z0b| <= s1 HB + (s2 Zt + s3 Rw Z1^2) TB
+template <bool F16 = false>
 __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.y;
-  if (m >= p.width) return;
+  float os = 1.f, mx0 = 0.f, mx1 = 0.f, mxt = 0.f;
+  if constexpr (F16) {
+    const float TB = p.bb[0], HB = p.bb[1], Rw = p.bb[2], wm = p.bb[3], Z1 = p.zb[0], Zt = p.zb[1];
+    const float b = fmaxf(p.s1 * TB, fmaxf(2.f * p.s2 * wm * Z1 * TB, p.s1 * HB + (p.s2 * Zt + p.s3 * Rw * Z1 * Z1) * TB));
+    os = f16_scale_for(b);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+      for (int t = 0; t < kF16Types; ++t) p.f16_out->scale[t] = os;
+  }
+  auto put = [&](uint16_t* q, float v, float& mx) {
+    if constexpr (F16) {
+      ptx::store_f16_off(q, q + p.pstride, 0u, v * os);
+      mx = fmaxf(mx, fabsf(v));
+    } else {
+      ptx::store_planes(q, p.pstride, p.nplanes, v);
+    }
+  };
+  if (m < p.width) {
   const float wl = p.w_out[m];
   const size_t ldz = (size_t)p.ldz, ldo = (size_t)p.ldo;
   float dwp = 0.f;
@@ -60,30 +86,122 @@ __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
       const float z1 = zs[(size_t)r * ldz];
       const float w = p.jw ? p.jw[r] : 1.f;
       szz = fmaf(w * z1, z1, szz);
-      ptx::store_planes(oz + (size_t)r * ldo, p.pstride, p.nplanes, 2.f * A.d2 * w * z1 * tb);
+      put(oz + (size_t)r * ldo, 2.f * A.d2 * w * z1 * tb, mx1);
     }
-    ptx::store_planes(p.out + (row + p.P - 1) * ldo + m, p.pstride, p.nplanes, A.d1 * tb);
-    ptx::store_planes(p.out + row * ldo + m, p.pstride, p.nplanes, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb);
+    put(p.out + (row + p.P - 1) * ldo + m, A.d1 * tb, mxt);
+    put(p.out + row * ldo + m, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb, mx0);
     const float top = A.d1 * zt + A.d2 * szz;
     dwp += gfn * A.d0 + p.c * go * top;
   }
   p.dw_part[(size_t)g * p.width + m] = dwp;
+  }
+  if constexpr (F16) {  // every lane reaches here (the record is per slot type)
+    warp_max_record(mx0, &p.f16_out->maxabs[0]);
+    warp_max_record(mx1, &p.f16_out->maxabs[1]);
+    warp_max_record(mxt, &p.f16_out->maxabs[2]);
+  }
 }
 
 // part[g, m] = sum over rows r = g, g + G, ... < nrows of src[row0 + r * stride, m]
 // (bf16 planes if src != nullptr, else fp32 `srcf`); grid (ceil(ncols / 128), G)
+// (rec != nullptr: fp16x3 planes of src, scaled by rec->scale[0] -- uniform in grad mode)
 __global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict__ src, int64_t pstride, int nplanes,
                                                      const float* __restrict__ srcf, int64_t nrows, int64_t stride,
-                                                     int ld, int ncols, int G, float* __restrict__ part) {
+                                                     int ld, int ncols, int G, float* __restrict__ part,
+                                                     const F16Rec* __restrict__ rec = nullptr) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.y;
   if (m >= ncols) return;
   float acc = 0.f;
+  const float inv = rec ? 1.f / rec->scale[0] : 1.f;
   for (int64_t r = g; r < nrows; r += G) {
     const size_t i = (size_t)(r * stride) * ld + m;
-    acc += srcf ? srcf[i] : ptx::planes_val(src + i, pstride, nplanes);
+    acc += srcf ? srcf[i] : rec ? ptx::f16_val(src + i, pstride) * inv : ptx::planes_val(src + i, pstride, nplanes);
   }
   part[(size_t)g * ncols + m] = acc;
+}
+
+// fp16x3 backward bounds (one block of 1024 threads):
+//   bb = {|c| max|gop| max|w_L|, max|gf| max|w_L|, Rw = sum_r |w_r| (R without weights), max_r |w_r| (1)};
+//   zb[2 l], zb[2 l + 1] = bounds of max |z1|, max |z_top| of the saved Z_l, l = 1 .. L-1:
+//   l = 1: max |U| (the fixed directions' images, ubound) and 0 (x2 = 0); l >= 2: ||W_l||_inf
+//   (G[2 l + 1]) times the recorded maxima of B_{l-1}'s first-order and top slots (rec[l-1]).
+__global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const float* __restrict__ gop, const float* __restrict__ gf,
+                                                           int64_t N, const float* __restrict__ w_out, int wl,
+                                                           float c, const float* __restrict__ jw, int R,
+                                                           const unsigned* __restrict__ ubound,
+                                                           const float* __restrict__ G, const F16Rec* __restrict__ rec,
+                                                           int L, float* __restrict__ bb, float* __restrict__ zb) {
+  __shared__ float red[5][32];
+  float a = 0.f, b = 0.f, w = 0.f, sw = 0.f, mw = 0.f;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+    a = fmaxf(a, fabsf(gop[i]));
+    if (gf) b = fmaxf(b, fabsf(gf[i]));
+  }
+  for (int i = threadIdx.x; i < wl; i += blockDim.x) w = fmaxf(w, fabsf(w_out[i]));
+  if (jw)
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      sw += fabsf(jw[i]);
+      mw = fmaxf(mw, fabsf(jw[i]));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+    sw += __shfl_xor_sync(0xffffffffu, sw, o);
+    mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+    red[2][threadIdx.x >> 5] = w;
+    red[3][threadIdx.x >> 5] = sw;
+    red[4][threadIdx.x >> 5] = mw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      a = fmaxf(a, red[0][k]);
+      b = fmaxf(b, red[1][k]);
+      w = fmaxf(w, red[2][k]);
+      sw += red[3][k];
+      mw = fmaxf(mw, red[4][k]);
+    }
+    bb[0] = fabsf(c) * a * w;
+    bb[1] = b * w;
+    bb[2] = jw ? sw : (float)R;
+    bb[3] = jw ? mw : 1.f;
+    zb[2] = __uint_as_float(ubound[0]);
+    zb[3] = 0.f;
+    for (int l = 2; l <= L - 1; ++l) {
+      zb[2 * l] = G[2 * l + 1] * __uint_as_float(rec[l - 1].maxabs[1]);
+      zb[2 * l + 1] = G[2 * l + 1] * __uint_as_float(rec[l - 1].maxabs[2]);
+    }
+  }
+}
+
+// out[1] = ||W^T||_inf = max_k sum_m |W[m, k]| of bf16 planes [3][rows, cols], out[0] = the
+// forward factor 2^-(sa+11) (the adjoint reads the same scaled fp16 planes, transposed)
+__global__ void __launch_bounds__(1024) f16_colnorm_kernel(const uint16_t* __restrict__ Wp, int rows, int cols,
+                                                          const float* __restrict__ fwd_stats, float* __restrict__ out) {
+  __shared__ float red[32];
+  const int64_t n = (int64_t)rows * cols;
+  float best = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    float a = 0.f;
+    for (int r = 0; r < rows; ++r) a += fabsf(planes3_val(Wp, n, (int64_t)r * cols + c));
+    best = fmaxf(best, a);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) best = fmaxf(best, red[k]);
+    out[0] = fwd_stats[0];
+    out[1] = best;
+  }
 }
 
 // out[m] (=|+=) sum_g part[g * ld + m] for m < ncols (ld >= ncols: the row stride of part),

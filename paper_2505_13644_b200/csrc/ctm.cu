@@ -18,9 +18,9 @@
 #include <vector>
 
 #include "../../include/ctm.h"
-#include "backward.cuh"
 #include "jet_layer.cuh"
 #include "seed.cuh"
+#include "backward.cuh"
 #include "wgrad.cuh"
 
 namespace {
@@ -172,8 +172,18 @@ struct ctm_mlp {
   bool grad = false;
   std::vector<uint16_t*> WTp;               // W_l^T bf16 planes [3][wpad[l-1], wpad[l]], l = 2..L-1
   std::vector<CUtensorMap> mapAT;
+  // fp16x3 training (grad mode in CTM_PRECISION_FP16X3): W_l^T as the forward's fp16 planes
+  // transposed, their statistics f16wT[2 l] = 2^-(sa+11), f16wT[2 l + 1] = ||W_l^T||_inf, the
+  // scale records of the adjoint blocks Z_bar_l (f16zrec[l]), the backward seeds' bounds
+  // f16bb[4] and the saved pre-activations' bounds f16zb[2 l], f16zb[2 l + 1] (backward.cuh)
+  std::vector<uint16_t*> WTp16;
+  std::vector<CUtensorMap> mapAT16;
+  float* f16wT = nullptr;
+  ctm::F16Rec* f16zrec = nullptr;
+  float* f16bb = nullptr;
+  float* f16zb = nullptr;
   float* eye = nullptr;                     // [256, 256] identity: fixed direction sets as shared V
-  bool wgrad_attr[2] = {false, false};    // dynamic smem attribute set (wgrad_kernel<128>, <256>)
+  bool wgrad_attr[4] = {};                  // dynamic smem attribute set (wgrad_kernel<128|256, f16>)
   struct Tape {
     bool valid = false;
     int64_t N = 0;
@@ -184,6 +194,7 @@ struct ctm_mlp {
     size_t weights_elems = 0;
     std::vector<Planes> B;                  // B_l, l = 0 .. L-1 (B_0 = layer-1 input block)
     int nplanes = 3;                        // precision the tape was recorded in
+    bool f16 = false;                       // recorded in the fp16x3 mode (uniform block scales)
     std::vector<float*> Z;                  // Z_l, l = 1 .. L-1 (fp32 pre-activations)
     std::vector<size_t> Z_elems;
     Planes Zb[2];
@@ -222,6 +233,8 @@ ctm_status free_all(ctm_mlp* h) {
   for (auto& p : h->WTp) F(p);
   F(h->W1p16); F(h->f16w); F(h->f16rec); F(h->f16b);
   for (auto& p : h->Wp16) F(p);
+  for (auto& p : h->WTp16) F(p);
+  F(h->f16wT); F(h->f16zrec); F(h->f16bb); F(h->f16zb);
   F(h->eye);
   F(h->tape.weights); F(h->tape.part); F(h->tape.wpart);
   for (auto& p : h->tape.B) F(p.p);
@@ -377,10 +390,10 @@ ctm_status launch_layer_instance(ctm_mlp* h, int64_t grid, const CUtensorMap& am
 template <int KORD, int FLAGS>
 ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
                                const ctm::LayerParams& lp, cudaStream_t st, const ctm::F16Args& fa = {}) {
-  if constexpr ((KORD == 2 || (KORD == 4 && FLAGS == 0)) && (FLAGS & ctm::kFlagSaveZ) == 0) {
+  if constexpr (KORD == 2 || (KORD == 4 && FLAGS == 0) || (KORD == ctm::kBwd2 && FLAGS == 0)) {
     if (fa.wsc) return launch_layer_instance<KORD, FLAGS | ctm::kFlagF16>(h, grid, amap, bmap, lp, st, fa);
   }
-  if (fa.wsc) return fail(CTM_EUNSUPPORTED, "fp16x3: collapsed K=2 / K=4 forward layers only");
+  if (fa.wsc) return fail(CTM_EUNSUPPORTED, "fp16x3: collapsed K=2 / K=4 layers and the K=2 adjoint only");
   if (lp.nplanes == 2) return launch_layer_instance<KORD, FLAGS | ctm::kFlagNP2>(h, grid, amap, bmap, lp, st, fa);
   return launch_layer_instance<KORD, FLAGS>(h, grid, amap, bmap, lp, st, fa);
 }
@@ -603,7 +616,9 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     const size_t fsm = ctm::seed_fixed_smem(D, R, pl.nb);
     constexpr size_t kFixedSmemMax = 200 * 1024;
     // (the fp16x3 mode's K=4 seed is the streaming kernel too: seed_layer_kernel has no fp16 planes)
-    if ((KORD == 2 || (KORD == 4 && h->cur_f16)) && !z_out && fsm <= kFixedSmemMax &&
+    // (grad mode z_out: the fp16x3 mode's seed writes the pre-activations too, seed_layer_kernel
+    // has no fp16 planes; the fp32 mode keeps seed_layer_kernel there)
+    if ((KORD == 2 || (KORD == 4 && h->cur_f16)) && (!z_out || h->cur_f16) && fsm <= kFixedSmemMax &&
         ld1 % ctm::kSeedFixedFeats == 0 && n > 0) {
       if (!h->seed_fixed_attr) {
         CTM_CUDA(cudaFuncSetAttribute(ctm::seed_fixed_kernel<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -627,6 +642,7 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
         sf.bounds = h->f16b;
         f16_act_sups(h->act, sf.s0, sf.s1, sf.s2, sf.s3, sf.s4);
         sf.out = h->f16rec + 1;
+        sf.uniform = z_out != nullptr;  // grad mode: one scale per block (the weight gradients)
       }
       // one wave: as many blocks as are resident at once (registers, shared memory)
       const int slices = ld1 / ctm::kSeedFixedFeats;
@@ -754,6 +770,7 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
         f16_act_sups(h->act, fa.s0, fa.s1, fa.s2, fa.s3, fa.s4);
         // K=2: sum |w_r| = rb (unit weights) unless weighted; K=4: the jets' weights (from smem)
         fa.rw = (lp.weighted || KORD == 4) ? -1.f : (float)std::max(pl.rb, 1);
+        fa.uniform = io != nullptr;
         am = gl.amap16;
       }
       if (KORD == 2) {
@@ -829,7 +846,9 @@ ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
 // operators of tanh / sin nets, random directions without sigma, >= 2 points per tile (no
 // split point), the streaming seed for fixed sets, and at least one tensor-core layer
 bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, bool grad, int R) {
-  if (h->prec != CTM_PRECISION_FP16X3 || grad || (KORD != 2 && KORD != 4) || pl.ppt < 2) return false;
+  if (h->prec != CTM_PRECISION_FP16X3 || (KORD != 2 && KORD != 4) || pl.ppt < 2) return false;
+  // grad mode (fp16x3 training): the K=2 operators of fixed direction sets (uniform block scales)
+  if (grad && (KORD != 2 || random_k2(a) || h->WTp16.empty())) return false;
   if (h->act != ctm::kActTanh && h->act != ctm::kActSin) return false;
   const bool k2op = a.op == OP_LAP || a.op == OP_WLAP || a.op == OP_RLAP || a.op == OP_WLAP_X ||
                     (a.op == OP_DSUM && a.K == 2);
@@ -899,7 +918,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
   ctm_status s;
   if (h->cur_f16) {  // fresh scale records and bound scratch for this call
     CTM_CUDA(cudaMemsetAsync(h->f16rec, 0, sizeof(ctm::F16Rec) * (h->L + 1), st));
-    CTM_CUDA(cudaMemsetAsync(h->f16b, 0, sizeof(unsigned) * 4, st));
+    CTM_CUDA(cudaMemsetAsync(h->f16b, 0, sizeof(unsigned) * 8, st));
   }
   // grad mode: record the tape of this call (differentiable operators only)
   std::vector<LayerIO> io;
@@ -944,13 +963,13 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     rp.pstride = (int64_t)b0.cap;
     rp.nplanes = h->nplanes;
     if (h->cur_f16) {  // fp16x3: bounds of x0 and of explicit directions; the input block's record
-      launch_maxabs(a.X, a.N * (int64_t)D, h->f16b, st);
+      launch_maxabs(a.X, a.N * (int64_t)D, h->f16b + 2, st);
       ++launches;
       if (a.V) {
-        launch_maxabs(a.V, a.N * (int64_t)a.S * a.Rv, h->f16b + 1, st);
+        launch_maxabs(a.V, a.N * (int64_t)a.S * a.Rv, h->f16b + 3, st);
         ++launches;
       }
-      rp.f16_bounds = h->f16b;
+      rp.f16_bounds = h->f16b + 2;
       rp.vgen = a.gaussian ? 6.f : 1.f;  // |Box-Muller draw| <= sqrt(-2 ln 2^-25) = 5.9
       rp.f16_out = h->f16rec;
     }
@@ -1034,7 +1053,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       rp.out = tapeB0->p;
       rp.pstride = (int64_t)tapeB0->cap;
       rp.nplanes = h->nplanes;
-      launch_seed_random(h->nplanes, a.N, rp, st);
+      // (fp16x3 training: B_0 in the fp32 mode's three bf16 planes, read only by the layer-1
+      // weight gradient, which runs in the fp32 mode, see backward())
+      if (h->cur_f16) rp.nplanes = 3;
+      launch_seed_random(rp.nplanes, a.N, rp, st);
       ++launches;
     }
     s = launch_seed(h, a, KORD, pl, 0, a.N, grad ? *tapeB1 : h->blk[2], UT, csum, a.op == OP_BIH_NEST ? D : R, st,
@@ -1054,6 +1076,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     T.weighted = (a.op == OP_DSUM);
     T.J = (a.op == OP_DSUM) ? a.J : 0;
     T.nplanes = h->nplanes;
+    T.f16 = h->cur_f16;
     if (T.weighted) {  // the caller's weights may not outlive the call
       s = ensure(T.weights, T.weights_elems, (size_t)a.J);
       if (s != CTM_OK) return s;
@@ -1071,8 +1094,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
 // (tcgen05, MN-major operands, fixed K splits, chunked TMEM accumulation) and
 // wgrad_reduce_kernel (the splits summed in order, cropped into dW). Deterministic.
 ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, int Mout, int64_t rows, int rows_out,
-                       int cols_in, float* dW, int acc, cudaStream_t st) {
+                       int cols_in, float* dW, int acc, cudaStream_t st, const ctm::F16Rec* zrec = nullptr,
+                       const ctm::F16Rec* brec = nullptr, int nplanes = 0) {
   auto& T = h->tape;
+  const bool f16 = zrec != nullptr;  // fp16x3 operands (uniform scales zrec / brec)
   const int N = (Kin % 256 == 0) ? 256 : 128;
   ctm::WgradParams wp{};
   wp.rows = rows;
@@ -1083,7 +1108,7 @@ ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, in
   const int npairs = h->sm_count / 2;
   wp.splits = std::max(1, std::min(npairs / tiles, wp.k_blocks));
   wp.kb_per_split = (wp.k_blocks + wp.splits - 1) / wp.splits;
-  wp.nplanes = T.nplanes;
+  wp.nplanes = nplanes ? nplanes : T.nplanes;
   const int units = tiles * wp.splits;
   ctm_status s = ensure(T.wpart, T.wpart_elems, (size_t)units * 256 * N);
   if (s != CTM_OK) return s;
@@ -1105,41 +1130,37 @@ ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, in
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (N == 256) {
-      if (!h->wgrad_attr[1]) {
-        CTM_CUDA(cudaFuncSetAttribute(ctm::wgrad_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      ctm::kWgradSmem));
-        h->wgrad_attr[1] = true;
-      }
-      CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::wgrad_kernel<256>, mz, mb, wp));
-    } else {
-      if (!h->wgrad_attr[0]) {
-        CTM_CUDA(cudaFuncSetAttribute(ctm::wgrad_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      ctm::kWgradSmem));
-        h->wgrad_attr[0] = true;
-      }
-      CTM_CUDA(cudaLaunchKernelEx(&cfg, ctm::wgrad_kernel<128>, mz, mb, wp));
+    auto* kern = N == 256 ? (f16 ? ctm::wgrad_kernel<256, true> : ctm::wgrad_kernel<256, false>)
+                          : (f16 ? ctm::wgrad_kernel<128, true> : ctm::wgrad_kernel<128, false>);
+    const int ai = (N == 256 ? 1 : 0) + (f16 ? 2 : 0);
+    if (!h->wgrad_attr[ai]) {
+      CTM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ctm::kWgradSmem));
+      h->wgrad_attr[ai] = true;
     }
+    CTM_CUDA(cudaLaunchKernelEx(&cfg, kern, mz, mb, wp));
   }
   {
     const int64_t n = (int64_t)rows_out * cols_in;
     ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
     ctm::wgrad_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T.wpart, N, wp.n_tiles, wp.splits, rows_out,
-                                                                        cols_in, dW, acc);
+                                                                        cols_in, dW, acc, zrec, brec);
   }
   h->last_launches += 2;
   return CTM_OK;
 }
 
 // out[m] (=|+=) sum_n Zb[n * P + 0, m] for m < ncols (the bias gradient: bias on slot 0 only)
-ctm_status bias_grad(ctm_mlp* h, const Planes& Z, int ld, int ncols, float* out, int acc, cudaStream_t st) {
+ctm_status bias_grad(ctm_mlp* h, const Planes& Z, int ld, int ncols, float* out, int acc, cudaStream_t st,
+                     const ctm::F16Rec* zrec = nullptr, int nplanes = 0) {
   const int G = 1024;  // point groups: enough independent rows in flight per column
   ctm_status s = ensure(h->tape.part, h->tape.part_elems, (size_t)G * std::max(ncols, 1));
   if (s != CTM_OK) return s;
   ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
   h->last_launches += 2;
-  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Z.p, (int64_t)Z.cap, h->tape.nplanes, nullptr,
-                                                                   h->tape.N, h->tape.P, ld, ncols, G, h->tape.part);
+  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Z.p, (int64_t)Z.cap,
+                                                                   nplanes ? nplanes : h->tape.nplanes, nullptr,
+                                                                   h->tape.N, h->tape.P, ld, ncols, G, h->tape.part,
+                                                                   zrec);
   ctm::reduce_groups_kernel<<<(ncols + 31) / 32, dim3(32, 32), 0, st>>>(h->tape.part, G, ncols, ncols, out, acc);
   return CTM_OK;
 }
@@ -1158,6 +1179,20 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   }
   const float* jw = T.weighted ? T.weights : nullptr;
   h->last_launches = 0;
+  const bool f16 = T.f16;
+  // fp16x3 records: the adjoint blocks' scales (f16zrec), the bounds of the backward seeds and
+  // of the saved pre-activations (backward.cuh f16_bwd_prep_kernel)
+  float s0 = 1.f, s1 = 1.f, s2 = 1.f, s3 = 1.f, s4 = 1.f;
+  if (f16) {
+    f16_act_sups(h->act, s0, s1, s2, s3, s4);
+    ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
+    CTM_CUDA(cudaMemsetAsync(h->f16zrec, 0, sizeof(ctm::F16Rec) * (L + 1), st));
+    ctm::f16_bwd_prep_kernel<<<1, 1024, 0, st>>>(gop, gf, N, h->w_out, h->wpad[L - 1], T.scale, jw, P - 2, h->f16b,
+                                                 h->f16w, h->f16rec, L, h->f16bb, h->f16zb);
+    ++h->last_launches;
+  }
+  auto zrec = [&](int l) -> const ctm::F16Rec* { return f16 ? h->f16zrec + l : nullptr; };
+  auto brec = [&](int l) -> const ctm::F16Rec* { return f16 ? h->f16rec + l : nullptr; };
   // ---- readout and the last hidden rule, transposed
   {
     ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
@@ -1183,7 +1218,15 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     tp.ldo = w;
     tp.dw_part = T.part;
     tp.G = G;
-    ctm::top_bwd_kernel<<<dim3(w / 128, G), 128, 0, st>>>(tp);
+    if (f16) {
+      tp.zb = h->f16zb + 2 * (L - 1);
+      tp.bb = h->f16bb;
+      tp.s1 = s1, tp.s2 = s2, tp.s3 = s3;
+      tp.f16_out = h->f16zrec + (L - 1);
+      ctm::top_bwd_kernel<true><<<dim3(w / 128, G), 128, 0, st>>>(tp);
+    } else {
+      ctm::top_bwd_kernel<false><<<dim3(w / 128, G), 128, 0, st>>>(tp);
+    }
     // part rows have stride w (padded); only the widths[L-1] real columns reach dW_L
     ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 31) / 32, dim3(32, 32), 0, st>>>(T.part, G, w, h->widths[L - 1],
                                                                                     dW[L - 1], acc);
@@ -1196,9 +1239,10 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   int cur = 0;
   for (int l = L - 1; l >= 2; --l) {
     const int Mout = h->wpad[l], Kin = h->wpad[l - 1];
-    s = weight_grad(h, T.B[l - 1], Kin, T.Zb[cur], Mout, rows, h->widths[l], h->widths[l - 1], dW[l - 1], acc, st);
+    s = weight_grad(h, T.B[l - 1], Kin, T.Zb[cur], Mout, rows, h->widths[l], h->widths[l - 1], dW[l - 1], acc, st,
+                    zrec(l), brec(l - 1));
     if (s != CTM_OK) return s;
-    s = bias_grad(h, T.Zb[cur], Mout, h->widths[l], db[l - 1], acc, st);
+    s = bias_grad(h, T.Zb[cur], Mout, h->widths[l], db[l - 1], acc, st, zrec(l));
     if (s != CTM_OK) return s;
     // Z_bar_{l-1} = rule^T( (Z_bar_l W_l)^T ) on the tensor cores (jet_layer_kernel<kBwd2>)
     CUtensorMap mb;
@@ -1229,15 +1273,31 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     {
       ProfScope ps(h, CTM_KIND_BWD, 2.0 * N * P * h->widths[l - 1] * h->widths[l], st);
       ++h->last_launches;
-      s = launch_layer_kernel<ctm::kBwd2, 0>(h, grid, h->mapAT[l - 2], mb, lp, st);
+      if (f16) {  // fp16x3: W_l^T fp16 planes, Z_bar_l's record in, Z_bar_{l-1}'s out (one scale)
+        ctm::F16Args fa{};
+        fa.in = h->f16zrec + l;
+        // Z_bar_1 (read only by the layer-1 weight and bias gradients) in the fp32 mode's planes
+        fa.out = (l == 2) ? nullptr : h->f16zrec + (l - 1);
+        fa.out_bf16 = (l == 2);
+        fa.wsc = h->f16wT + 2 * l;
+        fa.s0 = s0, fa.s1 = s1, fa.s2 = s2, fa.s3 = s3, fa.s4 = s4;
+        fa.uniform = 1;
+        fa.zb = h->f16zb + 2 * (l - 1);
+        fa.bb = h->f16bb;
+        s = launch_layer_kernel<ctm::kBwd2, 0>(h, grid, h->mapAT16[l - 2], mb, lp, st, fa);
+      } else {
+        s = launch_layer_kernel<ctm::kBwd2, 0>(h, grid, h->mapAT[l - 2], mb, lp, st);
+      }
       if (s != CTM_OK) return s;
     }
     cur ^= 1;
   }
   // ---- layer 1: dW_1 = Z_bar_1^T B_0 (B_0 = [x0; u_r; 0]), db_1
-  s = weight_grad(h, T.B[0], h->k1pad, T.Zb[cur], h->wpad[1], rows, h->widths[1], h->widths[0], dW[0], acc, st);
+  // (fp16x3 training: Z_bar_1 and B_0 are in the fp32 mode's three bf16 planes, see F16Args::out_bf16)
+  s = weight_grad(h, T.B[0], h->k1pad, T.Zb[cur], h->wpad[1], rows, h->widths[1], h->widths[0], dW[0], acc, st,
+                  nullptr, nullptr, f16 ? 3 : 0);
   if (s != CTM_OK) return s;
-  s = bias_grad(h, T.Zb[cur], h->wpad[1], h->widths[1], db[0], acc, st);
+  s = bias_grad(h, T.Zb[cur], h->wpad[1], h->widths[1], db[0], acc, st, nullptr, f16 ? 3 : 0);
   if (s != CTM_OK) return s;
   CTM_CUDA(cudaGetLastError());
   return CTM_OK;
@@ -1246,6 +1306,15 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
 // Every array derived from the weights, written on `st` (load and ctm_set_weights):
 // fp16x3 weight planes and statistics of every tensor-core layer (layer 1's W1p and the
 // hidden GEMM layers), from their bf16 planes (seed.cuh split_weights_f16_kernel)
+// grad mode: W_l^T of the fp16x3 planes (the adjoint's A operand) and ||W_l^T||_inf
+void derive_f16_transposed(ctm_mlp* h, cudaStream_t st) {
+  for (size_t i = 0; i < h->WTp16.size(); ++i) {
+    const int l = (int)i + 2, mpad = h->wpad[l], kpad = h->wpad[l - 1];
+    const int64_t n = (int64_t)mpad * kpad;
+    ctm::transpose_planes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Wp16[i], mpad, kpad, h->WTp16[i]);
+    ctm::f16_colnorm_kernel<<<1, 1024, 0, st>>>(h->Wp[i], mpad, kpad, h->f16w + 2 * l, h->f16wT + 2 * l);
+  }
+}
 void derive_f16_weights(ctm_mlp* h, cudaStream_t st) {
   const int L = h->L, ld1 = h->wpad[1];
   {
@@ -1260,6 +1329,7 @@ void derive_f16_weights(ctm_mlp* h, cudaStream_t st) {
     ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Wp[l - 2], n, h->f16w + 2 * l,
                                                                                h->Wp16[l - 2]);
   }
+  derive_f16_transposed(h, st);
   h->f16_stale = false;
 }
 
@@ -1422,7 +1492,11 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     }
     LOAD_CUDA(cudaMalloc(&h->f16w, sizeof(float) * 2 * (n_layers + 1)));
     LOAD_CUDA(cudaMalloc(&h->f16rec, sizeof(ctm::F16Rec) * (n_layers + 1)));
-    LOAD_CUDA(cudaMalloc(&h->f16b, sizeof(unsigned) * 4));
+    LOAD_CUDA(cudaMalloc(&h->f16b, sizeof(unsigned) * 8));
+    LOAD_CUDA(cudaMalloc(&h->f16wT, sizeof(float) * 2 * (n_layers + 1)));
+    LOAD_CUDA(cudaMalloc(&h->f16zrec, sizeof(ctm::F16Rec) * (n_layers + 1)));
+    LOAD_CUDA(cudaMalloc(&h->f16bb, sizeof(float) * 4));
+    LOAD_CUDA(cudaMalloc(&h->f16zb, sizeof(float) * 2 * (n_layers + 1)));
   }
   LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * h->wpad[n_layers - 1]));
   LOAD_CUDA(cudaMalloc(&h->b_out, sizeof(float)));
@@ -1667,7 +1741,14 @@ ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable) {
     if (!make_map3(&mt, tp, mpad, kpad, (uint64_t)n, ctm::kBM))
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W^T");
     mlp->mapAT.push_back(mt);
+    uint16_t* tp16 = nullptr;  // fp16x3 training: the same for the fp16 planes
+    CTM_CUDA(cudaMalloc(&tp16, 3 * sizeof(uint16_t) * (size_t)mpad * kpad));
+    mlp->WTp16.push_back(tp16);
+    if (!make_map3(&mt, tp16, mpad, kpad, (uint64_t)n, ctm::kBM))
+      return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W^T (fp16)");
+    mlp->mapAT16.push_back(mt);
   }
+  if (!mlp->f16_stale) derive_f16_transposed(mlp, 0);
   {
     std::vector<float> eye(256 * 256, 0.f);
     for (int i = 0; i < 256; ++i) eye[i * 257] = 1.f;
@@ -1730,7 +1811,7 @@ ctm_status ctm_gemm_probe(ctm_mlp_t mlp, int32_t layer, const float* B, int64_t 
     const int64_t n = rows_pad * kpad;
     if (f16) {  // one scale for every slot type: that of the measured max |B|
       CTM_CUDA(cudaMemsetAsync(h->f16rec, 0, sizeof(ctm::F16Rec) * 2, st));
-      CTM_CUDA(cudaMemsetAsync(h->f16b, 0, sizeof(unsigned) * 4, st));
+      CTM_CUDA(cudaMemsetAsync(h->f16b, 0, sizeof(unsigned) * 8, st));
       launch_maxabs(B, rows * (int64_t)w_in, h->f16b, st);
       ctm::probe_f16_record_kernel<<<1, 1, 0, st>>>(h->f16b, h->f16rec);
       ctm::split_rows_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(

@@ -207,6 +207,16 @@ struct F16Args {
   float s0, s1, s2;   // sup |s|, |s'|, |s''| of the activation
   float s3, s4;       // sup of the third and fourth derivatives (K=4)
   float rw;           // sum_r |w_r| over one sub-point's directions (< 0: from the smem weights)
+  int uniform;        // grad mode: one scale for every slot type of the output block (the weight
+                      // gradients contract over all slot rows, wgrad.cuh)
+  // kBwd2 (the adjoint, fp16x3 training): bounds of the layer's saved pre-activations
+  // zb = {max |z1|, max |z_top|} and of the backward seeds bb = {|c| max|gop| max|w_L|,
+  // max|gf| max|w_L|, sum_r |w_r|, max_r |w_r|} (f16_bwd_prep_kernel)
+  const float* zb;
+  const float* bb;
+  int out_bf16;       // kBwd2 producing Z_bar_1: write the fp32 mode's three bf16 planes (fp32's
+                      // exponent range for the layer-1 weight gradient, whose features may be
+                      // saturated: adjoints ~1e-20 of the block's largest)
 };
 // the registers an fp16x3 epilogue thread carries: unscale factors of the accumulator per
 // slot type (2^-(sa+11) / scale_in[t]), scales of its output block, running max |output|
@@ -214,6 +224,7 @@ struct F16Ctx {
   float us[kF16Types];
   float os[kF16Types];
   float mx[kF16Types];
+  int out_bf16;  // see F16Args
 };
 // output scale of a slot type from a bound B on |v|: 2^(14 - e), B = m 2^e, m in [0.5, 1), so
 // |v * scale| <= 2^14 < 65504 (fp16 max)
@@ -235,6 +246,24 @@ __device__ __forceinline__ void f16_out_scales(const F16Args& a, float rw, float
   os[1] = f16_scale_for(a.s1 * g1);
   os[2] = f16_scale_for(a.s1 * G * Mt + a.s2 * rw * g1 * g1);
   os[3] = os[4] = 1.f;
+  if (a.uniform) os[0] = os[1] = os[2] = os[3] = os[4] = fminf(os[0], fminf(os[1], os[2]));
+}
+// The adjoint of the K=2 rule (epilogue_bwd2) with G = ||W^T||_inf and the input adjoint
+// block's maxima Mb[t]: |hb_t| <= G Mb[t] =: H_t (hb = W^T zb per slot), and with Z1, Zt the
+// bounds of the saved z1, z_top, R = P - 2 directions, Rw = sum |w_r|, w = max |w_r|:
+//   |ztb| <= s1 Ht;  |z1b_r| <= s1 H1 + 2 s2 w Z1 Ht;
+//   |z0b| <= s1 H0 + s2 R Z1 H1 + (s2 Zt + s3 Rw Z1^2) Ht.
+// One scale for the whole output block (grad mode: uniform, see F16Args).
+__device__ __forceinline__ void f16_bwd_scales(const F16Args& a, int R, float* os) {
+  const float G = a.wsc[1];
+  const float H0 = G * __uint_as_float(a.in->maxabs[0]), H1 = G * __uint_as_float(a.in->maxabs[1]),
+              Ht = G * __uint_as_float(a.in->maxabs[2]);
+  const float Z1 = a.zb[0], Zt = a.zb[1], Rw = a.bb[2], wm = a.bb[3];
+  const float bt = a.s1 * Ht;
+  const float b1 = a.s1 * H1 + 2.f * a.s2 * wm * Z1 * Ht;
+  const float b0 = a.s1 * H0 + a.s2 * (float)R * Z1 * H1 + (a.s2 * Zt + a.s3 * Rw * Z1 * Z1) * Ht;
+  const float sc = f16_scale_for(fmaxf(bt, fmaxf(b1, b0)));
+  for (int t = 0; t < kF16Types; ++t) os[t] = sc;
 }
 // The K=4 rule (cheat-sheet rows k <= 4) with g_k = G M_k the bounds of the
 // input jets' coefficients: |h1| <= s1 g1; |h2| <= s2 g1^2 + s1 g2;
@@ -258,7 +287,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
                                                int bar_id, float& fpart, float& opart, F16Ctx* fc = nullptr) {
   constexpr int NPL = planes_of<FLAGS>();
   constexpr bool F16 = (FLAGS & kFlagF16) != 0;  // fp16x3: unscale what is read, scale what is stored
-  static_assert(!F16 || KORD == 2 || KORD == 4, "fp16x3: K=2 and K=4 collapsed rules only");
+  static_assert(!F16 || KORD == 2 || KORD == 4 || KORD == kBwd2, "fp16x3: K=2 and K=4 collapsed rules only");
   const int P = p.P;
   const int ld = p.ldo;
   constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
@@ -700,18 +729,27 @@ __device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32
 // (w_r = 1 unless p.weighted). Writes Z_bar of this layer as bf16 pairs.
 // kB: slots per TMEM load / z-load batch (16; 8 keeps the register count of the 4-group
 // adjoint instance low)
-template <int kB, int NPL>
+template <int kB, int NPL, bool F16 = false>
 __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tcol, int64_t row, int m,
-                                              const float* jw) {
+                                              const float* jw, F16Ctx* fc = nullptr) {
+  // fp16x3 (F16): the accumulator carries the weights' and the input adjoint block's scales
+  // (us, uniform over the slot types in grad mode); outputs are stored scaled by os and their
+  // maxima recorded per slot type (0 z0b, 1 z1b, 2 ztb) for the next layer's bound
   const int P = p.P;
   const int ld = p.ldo;
   const uint32_t ldz = (uint32_t)p.ldzi;  // slot offsets are 32-bit (one wide multiply-add per address)
   const float* zr = p.z_in + (size_t)row * ldz + m;
-  const float hb0 = ptx::tmem_ld1(tcol);
-  const float tb = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
+  float hb0 = ptx::tmem_ld1(tcol);
+  float tb = ptx::tmem_ld1(tcol + (uint32_t)(P - 1));
   const float z0 = zr[0];
   const float zt = zr[(uint32_t)(P - 1) * ldz];
   ptx::tmem_ld_wait();
+  float us1 = 1.f;
+  if constexpr (F16) {
+    hb0 *= fc->us[0];
+    tb *= fc->us[2];
+    us1 = fc->us[1];
+  }
   const ActD A = act_derivs(p.act, z0);
   const float two_s2_tb = 2.f * A.d2 * tb;
   const bool wsum = p.weighted;
@@ -722,11 +760,24 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
   uint32_t off = 0;
   const int nmid = P - 2;
   int s = 0;
+  auto put = [&](float v, int type) {
+    if constexpr (F16) {
+      if (fc->out_bf16) {
+        ptx::store_planes_off<3>(q0, q1, q2, off, v);
+      } else {
+        ptx::store_f16_off(q0, q1, off, v * fc->os[type]);
+        fc->mx[type] = fmaxf(fc->mx[type], fabsf(v));
+      }
+    } else {
+      ptx::store_planes_off<NPL>(q0, q1, q2, off, v);
+    }
+  };
   auto one = [&](float hb, float z1, int r) {
+    if constexpr (F16) hb *= us1;
     const float w = wsum ? jw[r] : 1.f;
     szh = fmaf(z1, hb, szh);
     szz = fmaf(w * z1, z1, szz);
-    ptx::store_planes_off<NPL>(q0, q1, q2, off, fmaf(A.d1, hb, w * two_s2_tb * z1));
+    put(fmaf(A.d1, hb, w * two_s2_tb * z1), 1);
     off += (uint32_t)ld;
   };
   for (; s + kB <= nmid; s += kB) {
@@ -757,9 +808,19 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
     for (int i = 0; i < kB - 1; ++i)
       if (i < rem) one(v[i], z[i], s + i);
   }
-  ptx::store_planes_off<NPL>(q0, q1, q2, off, A.d1 * tb);  // slot P-1
+  put(A.d1 * tb, 2);  // slot P-1
   const float z0b = A.d1 * hb0 + A.d2 * szh + (A.d2 * zt + A.d3 * szz) * tb;
-  store_out<NPL>(p, (size_t)row * ld + m, z0b);
+  if constexpr (F16) {
+    uint16_t* const r0 = p.out + (size_t)row * ld + m;
+    if (fc->out_bf16) {
+      ptx::store_planes<3>(r0, p.pstride, z0b);
+    } else {
+      ptx::store_f16_off(r0, r0 + p.pstride, 0u, z0b * fc->os[0]);
+      fc->mx[0] = fmaxf(fc->mx[0], fabsf(z0b));
+    }
+  } else {
+    store_out<NPL>(p, (size_t)row * ld + m, z0b);
+  }
 }
 
 // The k-th tile of CTA pair `pair`: tile t = pair + k * npairs, feature pair t % m_pairs of
@@ -1000,6 +1061,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         fcx.us[t] = wsi / f16.in->scale[t];
         fcx.mx[t] = 0.f;
       }
+      fcx.out_bf16 = f16.out_bf16;
       if (f16.out) {
         float rw = f16.rw;
         if (rw < 0.f) {  // weighted sums: the largest sum |w_r| over the direction blocks
@@ -1012,6 +1074,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         }
         if (KORD == 4)
           f16_out_scales4(f16, rw, fcx.os);
+        else if (KORD == kBwd2)
+          f16_bwd_scales(f16, p.P - 2, fcx.os);
         else
           f16_out_scales(f16, rw, fcx.os);
         if (blockIdx.x == 0 && threadIdx.x == 64)
@@ -1047,7 +1111,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       const uint32_t tbase = tmem_base + buf * (kTmemCols / 2) + ((uint32_t)(q * 32) << 16);
       if (KORD == kBwd2) {
         for (int pt = g; pt < npts; pt += EG)
-          epilogue_bwd2<EG == 4 ? 8 : 16, NPL>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw);
+          epilogue_bwd2<EG == 4 ? 8 : 16, NPL, F16>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, jw,
+                                                    fc);
       } else if (KORD == kNest) {
         // nested biharmonic: a point is never split; with one point per tile (D >= 14)
         // only warp group 0 works on it

@@ -148,6 +148,18 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, 
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D = A * B + D * 2^-11 (tcgen05.mma's scale-input-d, kind::f16): the fp16x3 weight
+// gradients' first p0*p0 MMA of a chunk takes the accumulator of the lifted correction
+// products (p1 carries 2^11) down to the scale of the main product, so no lifted third
+// plane of an activation block is needed
+__device__ __forceinline__ void mma_f16_pair_unlift(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p, 11;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(1u)
+      : "memory");
+}
 // One lane of a converged warp (elect.sync): issue single-thread instructions (tcgen05.mma,
 // commits) from converged code so their operands stay in uniform registers (no per-MMA
 // R2UR waterfall loop of a divergent lane-0 branch).
@@ -293,6 +305,10 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N) {
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
+// fp16 operands, both MN-major (the fp16x3 weight gradients)
+__host__ __device__ constexpr uint32_t idesc_f16_mn(uint32_t M, uint32_t N) {
+  return idesc_f16(M, N) | (1u << 15) | (1u << 16);
+}
 // The same with both operands MN-major (bits 15 and 16).
 __host__ __device__ constexpr uint32_t idesc_bf16_mn(uint32_t M, uint32_t N) {
   return idesc_bf16(M, N) | (1u << 15) | (1u << 16);
@@ -382,6 +398,10 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 __device__ __forceinline__ void pdl_wait_prior() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ float bf16_val(uint16_t b) { return __bfloat162float(__ushort_as_bfloat16(b)); }
+// the value of an fp16x3 element (two planes, the residual lifted by 2^11), still scaled
+__device__ __forceinline__ float f16_val(const uint16_t* p, int64_t pstride) {
+  return __half2float(__ushort_as_half(p[pstride])) * (1.f / kF16Lift) + __half2float(__ushort_as_half(p[0]));
+}
 // the fp32 value of a plane-split element (sum of its planes, small first)
 __device__ __forceinline__ float planes_val(const uint16_t* p, int64_t pstride, int nplanes) {
   float v = nplanes > 2 ? bf16_val(p[2 * pstride]) : 0.f;

@@ -55,6 +55,7 @@ struct SeedF16 {
   const unsigned* bounds;
   float s0, s1, s2, s3, s4;
   F16Rec* out;
+  int uniform;  // grad mode: one scale for all slot types (the weight gradients contract over rows)
 };
 
 // Where a kernel writes its bf16 planes: plane k of element i at base[k * pstride + i].
@@ -355,7 +356,6 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32, 4) seed_fixed_kernel(con
   float* xw = xs + warp * p.D;
   const int64_t nb = blockIdx.y * pts_per_group;
   const int64_t ne = (nb + pts_per_group < p.n_points) ? nb + pts_per_group : p.n_points;
-  constexpr int ROWS = (KORD == 4) ? 3 : 1;  // rows per direction (jet)
   static_assert(!F16 || NP == 2, "fp16x3: two planes");
   // fp16x3: output scales per slot type (jet_layer.cuh F16Rec) from |h0| <= s0 and, with
   // U = max|U| and C = max|csum|: K=2 |s' u| <= s1 U, |s'' csum| <= s2 C; K=4 |s' u| <= s1 U,
@@ -371,6 +371,11 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32, 4) seed_fixed_kernel(con
     if (KORD == 4) {
       os[3] = f16_scale_for(f.s2 * U * U);
       os[4] = f16_scale_for(f.s3 * U * U * U);
+    }
+    if (f.uniform) {
+      const float u = fminf(os[0], fminf(os[1], os[2]));
+#pragma unroll
+      for (int t = 0; t < kF16Types; ++t) os[t] = u;
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
       for (int t = 0; t < kF16Types; ++t) f.out->scale[t] = os[t];
@@ -414,16 +419,26 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32, 4) seed_fixed_kernel(con
                 d3[4] = {A0.d3 * sc4, A1.d3 * sc4, A2.d3 * sc4, A3.d3 * sc4},
                 d4[4] = {A0.d4 * sc2, A1.d4 * sc2, A2.d4 * sc2, A3.d4 * sc2};
     uint16_t* dst = p.out + (size_t)n * p.blocks * p.P * ld + m;  // row (n * blocks + b) * P + slot
+    // grad mode (K=2, one block): the pre-activations [z0; u_r; 0] of the point's slots
+    float* zd = (KORD == 2 && p.z_out) ? p.z_out + (size_t)n * p.P * ld + m : nullptr;
+    auto putz = [&](float4 v) {
+      if (zd) {
+        *reinterpret_cast<float4*>(zd) = v;
+        zd += ld;
+      }
+    };
     for (int b = 0; b < p.blocks; ++b) {
       const int r0 = b * p.rb;
       const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;
       put4(dst, t[0], t[1], t[2], t[3], 0);
+      putz(z0);
       dst += ld;
       for (int r = r0; r < r0 + p.rb; ++r) {
         // the padding directions of a last block (r >= r1) are zero rows
         const float4 u = (r < r1) ? *reinterpret_cast<const float4*>(us + (size_t)r * F + c)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
         put4(dst, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w, 1);
+        putz(u);
         dst += ld;
         if (KORD == 4) {
           put4(dst, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z, d2[3] * u.w * u.w, 3);
@@ -438,6 +453,7 @@ __global__ void __launch_bounds__(kSeedFixedWarps * 32, 4) seed_fixed_kernel(con
         put4(dst, d4[0] * q.x, d4[1] * q.y, d4[2] * q.z, d4[3] * q.w, 2);
       else
         put4(dst, d2[0] * q.x, d2[1] * q.y, d2[2] * q.z, d2[3] * q.w, 2);
+      putz(make_float4(0.f, 0.f, 0.f, 0.f));  // x2 = 0: the top pre-activation of layer 1
       dst += ld;
     }
   }

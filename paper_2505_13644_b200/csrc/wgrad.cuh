@@ -42,7 +42,12 @@ struct WgradParams {
   float* part;         // [units][256][N], unit = (m_pair * n_tiles + n_tile) * splits + split
 };
 
-template <int N>
+// F16: the fp16x3 mode (jet_layer.cuh kFlagF16): both operands two fp16 planes (the residual
+// lifted by 2^11) with ONE power-of-two scale per block (grad mode records uniform scales);
+// per chunk, phase 1 runs p1*p0 + p0*p1 over the chunk's K (carrying 2^11), phase 2 p0*p0,
+// its first MMA scaling the accumulator by 2^-11 (ptx::mma_f16_pair_unlift). The partial is
+// scale_Z * scale_B times the gradient; wgrad_reduce_kernel undoes it.
+template <int N, bool F16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmB,
                  const WgradParams p) {
@@ -109,7 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int i0 = nt * N + (int)rank * kHalfN;
         for (int c0 = kb0; c0 < kb1; c0 += kWgChunkKB) {
           const int nkb = min(kWgChunkKB, kb1 - c0);
-          for_each_group(p.nplanes, false, nkb, [&](int, int kb, int nslots) {
+          for_each_group(F16 ? 2 : p.nplanes, F16, nkb, [&](int, int kb, int nslots) {
             const int r0 = (c0 + kb) * 64;
             for (int pl = 0; pl < nslots; ++pl, ++it) {
               const uint32_t s = it % kWgSlots;
@@ -129,7 +134,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader warp, elected lane)
     if (rank == 0) {
-      const uint32_t idesc = ptx::idesc_bf16_mn(256, (uint32_t)N);
+      const uint32_t idesc = F16 ? ptx::idesc_f16_mn(256, (uint32_t)N) : ptx::idesc_bf16_mn(256, (uint32_t)N);
       const uint64_t desc0 = ptx::smem_desc_mn(ptx::smem_u32(smem), 8192, 1024);
       constexpr uint64_t kS = kSlot >> 4, kB = kABytes >> 4;
       uint32_t it = 0, chunk = 0;
@@ -143,7 +148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem_base + buf * (uint32_t)N;
           uint32_t acc = 0;
-          for_each_group(p.nplanes, false, nkb, [&](int, int, int nslots) {
+          bool unlift = F16;  // fp16x3: the chunk's first p0*p0 MMA scales the corrections by 2^-11
+          for_each_group(F16 ? 2 : p.nplanes, F16, nkb, [&](int, int, int nslots) {
             for (int pl = 0; pl < nslots; ++pl)
               ptx::mbar_wait(&full_bar[(it + pl) % kWgSlots], ((it + pl) / kWgSlots) & 1u);
             ptx::tc_fence_after();
@@ -156,7 +162,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                 if (nslots == 2) {
                   ptx::mma_bf16_pair(d_tmem, dA1 + o, dA0 + kB + o, idesc, acc);
                   ptx::mma_bf16_pair(d_tmem, dA0 + o, dA1 + kB + o, idesc, 1u);
-                  ptx::mma_bf16_pair(d_tmem, dA0 + o, dA0 + kB + o, idesc, 1u);
+                  if (!F16) ptx::mma_bf16_pair(d_tmem, dA0 + o, dA0 + kB + o, idesc, 1u);
+                } else if (F16 && unlift) {
+                  ptx::mma_f16_pair_unlift(d_tmem, dA0 + o, dA0 + kB + o, idesc);
+                  unlift = false;
                 } else if (nslots == 3) {
                   ptx::mma_bf16_pair(d_tmem, dA2 + o, dA0 + kB + o, idesc, acc);
                   ptx::mma_bf16_pair(d_tmem, dA1 + o, dA1 + kB + o, idesc, 1u);
@@ -225,8 +234,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 
 // dW[o, i] (=|+=) sum_s part[unit(o, i, s)][o % 256][i % N] for o < rows_out, i < cols_in
 // (the caller's nn.Linear layout [rows_out, cols_in]); splits summed in order s = 0, 1, ...
+// (fp16x3: ra / rb are the operands' scale records, the sum is divided by their uniform scales)
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, int N, int n_tiles, int splits, int rows_out,
-                                    int cols_in, float* __restrict__ dW, int accumulate) {
+                                    int cols_in, float* __restrict__ dW, int accumulate,
+                                    const F16Rec* __restrict__ ra = nullptr, const F16Rec* __restrict__ rb = nullptr) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (int64_t)rows_out * cols_in) return;
   const int o = (int)(k / cols_in), i = (int)(k % cols_in);
@@ -234,6 +245,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, int N, int n
   const float* pp = part + ((size_t)tile * splits * 256 + (o % 256)) * N + (i % N);
   float s = 0.f;
   for (int sp = 0; sp < splits; ++sp) s += pp[(size_t)sp * 256 * N];
+  if (ra) s /= ra->scale[0] * rb->scale[0];  // powers of two: exact
   dW[k] = accumulate ? dW[k] + s : s;
 }
 

@@ -72,7 +72,9 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     assert m.last_precision() == "fp32"
     m.grad_enable()
     m.laplacian(X)
-    assert m.last_precision() == "fp32"  # the differentiable path runs fp32
+    assert m.last_precision() == "fp16x3"  # fp16x3 training: fixed direction sets
+    m.randomized_laplacian(X, S=4, seed=1)
+    assert m.last_precision() == "fp32"  # per-point directions in grad mode run fp32
     m.grad_enable(False)
     m.laplacian(X)
     assert m.last_precision() == "fp16x3"
@@ -132,28 +134,38 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
     m.close()
 
 
-@pytest.mark.parametrize("op,S", [("laplacian", 0), ("randomized", 8), ("randomized", 128), ("biharmonic", 0)])
+@pytest.mark.parametrize("op,S", [("laplacian", 0), ("weighted", 0), ("randomized", 8), ("randomized", 32),
+                                  ("randomized", 128), ("biharmonic", 0)])
 def test_fp16x3_full_size_sampled(ctm, op, S):
-    """BASELINE C1 / C3 / C4 at N = 16384 in the bench's launch configuration, 256 sampled points."""
+    """BASELINE C1 / C2 / C3 / C4 at N = 16384 in the bench's launch configuration (the bench's
+    default mode), 256 sampled points at every position inside a tile; op at the north_star
+    metric and f(x) to 1e-5 max(1, |f|)."""
     D = 5 if op == "biharmonic" else 50
     params, onet = _nets(widths_for(D), 0)
     N = 16384
     X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
     m = _mlp(ctm, params)
     idx = np.unique(np.minimum(np.arange(0, N, N // 256)[:256] + np.arange(256) % 16, N - 1))
     Xs = X[idx].astype(np.float64)
     if op == "laplacian":
-        got = m.laplacian(torch.from_numpy(X).cuda())[0]
-        want, _, norm = O.laplacian(onet, Xs)
+        got, f = m.laplacian(Xc)
+        want, fwant, norm = O.laplacian(onet, Xs)
+    elif op == "weighted":
+        sig = make_sigma(D, D, kind="dense")
+        got, f = m.weighted_laplacian(Xc, torch.from_numpy(sig).cuda())
+        want, fwant, norm = O.weighted_laplacian(onet, Xs, sig.astype(np.float64))
     elif op == "biharmonic":
-        got = m.biharmonic(torch.from_numpy(X).cuda())[0]
-        want, _, norm = O.biharmonic(onet, Xs)
+        got, f = m.biharmonic(Xc)
+        want, fwant, norm = O.biharmonic(onet, Xs)
     else:
-        got = m.randomized_laplacian(torch.from_numpy(X).cuda(), S=S, seed=2)[0]
+        got, f = m.randomized_laplacian(Xc, S=S, seed=2)
         V = np.concatenate([O.rademacher(2, int(n), 1, S, 50) for n in idx])
-        want, _, norm = O.randomized_laplacian(onet, Xs, V)
+        want, fwant, norm = O.randomized_laplacian(onet, Xs, V)
     assert m.last_precision() == "fp16x3"
     _check(got.cpu()[idx], want, norm)
+    fe = np.abs(f.double().cpu().numpy()[idx] - fwant) / np.maximum(1.0, np.abs(fwant))
+    assert fe.max() <= 1e-5, fe.max()
     m.close()
 
 
