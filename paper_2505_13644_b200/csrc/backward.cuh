@@ -43,12 +43,14 @@ struct TopBwdParams {
   F16Rec* f16_out;
 };
 
-// grid (width / 128, G); a thread owns one feature and the points n = g, g + G, ...
+// grid (width / 512, G); a thread owns four features and the points n = g, g + G, ...
 // fp16x3 bounds (F16), TB = |c| max|gop| max|w_L|, HB = max|gf| max|w_L|:
 //   |ztb| <= s1 TB;  |z1b_r| <= 2 s2 w Z1 TB;  |z0b| <= s1 HB + (s2 Zt + s3 Rw Z1^2) TB
 template <bool F16 = false>
 __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  // four adjacent features per thread: float4 loads of Z, 8-byte stores into each plane
+  // (the per-element arithmetic is the scalar rule's, in the same order)
+  const int m = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int g = blockIdx.y;
   float os = 1.f, mx0 = 0.f, mx1 = 0.f, mxt = 0.f;
   if constexpr (F16) {
@@ -58,42 +60,64 @@ __global__ void __launch_bounds__(128) top_bwd_kernel(const TopBwdParams p) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
       for (int t = 0; t < kF16Types; ++t) p.f16_out->scale[t] = os;
   }
-  auto put = [&](uint16_t* q, float v, float& mx) {
+  auto put4 = [&](uint16_t* q, const float* v, float& mx) {
     if constexpr (F16) {
-      ptx::store_f16_off(q, q + p.pstride, 0u, v * os);
-      mx = fmaxf(mx, fabsf(v));
+      seed_store4_f16s(q, p.pstride, v[0] * os, v[1] * os, v[2] * os, v[3] * os);
+      mx = fmaxf(mx, max4abs(v[0], v[1], v[2], v[3]));
+    } else if (p.nplanes == 3) {
+      seed_store4_at<3>(q, p.pstride, v[0], v[1], v[2], v[3]);
     } else {
-      ptx::store_planes(q, p.pstride, p.nplanes, v);
+      seed_store4_at<2>(q, p.pstride, v[0], v[1], v[2], v[3]);
     }
   };
   if (m < p.width) {
-  const float wl = p.w_out[m];
-  const size_t ldz = (size_t)p.ldz, ldo = (size_t)p.ldo;
-  float dwp = 0.f;
-  for (int64_t n = g; n < p.N; n += p.G) {
-    const size_t row = (size_t)n * p.P;
-    const float* zr = p.Z + row * ldz + m;
-    const float z0 = zr[0], zt = zr[(size_t)(p.P - 1) * ldz];
-    const ActD A = act_derivs(p.act, z0);
-    const float go = p.gop[n], gfn = p.gf ? p.gf[n] : 0.f;
-    const float tb = p.c * go * wl;  // adjoint of the collapsed top h_top
-    const float hb0 = gfn * wl;      // adjoint of h0
-    float szz = 0.f;
-    const float* __restrict__ zs = zr + ldz;
-    uint16_t* __restrict__ oz = p.out + (row + 1) * ldo + m;
+    const float4 wl4 = *reinterpret_cast<const float4*>(p.w_out + m);
+    const float wl[4] = {wl4.x, wl4.y, wl4.z, wl4.w};
+    const size_t ldz = (size_t)p.ldz, ldo = (size_t)p.ldo;
+    float dwp[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int64_t n = g; n < p.N; n += p.G) {
+      const size_t row = (size_t)n * p.P;
+      const float* zr = p.Z + row * ldz + m;
+      const float4 z04 = *reinterpret_cast<const float4*>(zr);
+      const float4 zt4 = *reinterpret_cast<const float4*>(zr + (size_t)(p.P - 1) * ldz);
+      const float z0[4] = {z04.x, z04.y, z04.z, z04.w}, zt[4] = {zt4.x, zt4.y, zt4.z, zt4.w};
+      const ActD A[4] = {act_derivs(p.act, z0[0]), act_derivs(p.act, z0[1]), act_derivs(p.act, z0[2]),
+                         act_derivs(p.act, z0[3])};
+      const float go = p.gop[n], gfn = p.gf ? p.gf[n] : 0.f;
+      float tb[4], hb0[4], szz[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        tb[i] = p.c * go * wl[i];  // adjoint of the collapsed top h_top
+        hb0[i] = gfn * wl[i];      // adjoint of h0
+        szz[i] = 0.f;
+      }
+      const float* __restrict__ zs = zr + ldz;
+      uint16_t* __restrict__ oz = p.out + (row + 1) * ldo + m;
 #pragma unroll 4
-    for (int r = 0; r < p.P - 2; ++r) {
-      const float z1 = zs[(size_t)r * ldz];
-      const float w = p.jw ? p.jw[r] : 1.f;
-      szz = fmaf(w * z1, z1, szz);
-      put(oz + (size_t)r * ldo, 2.f * A.d2 * w * z1 * tb, mx1);
+      for (int r = 0; r < p.P - 2; ++r) {
+        const float4 z14 = *reinterpret_cast<const float4*>(zs + (size_t)r * ldz);
+        const float z1[4] = {z14.x, z14.y, z14.z, z14.w};
+        const float w = p.jw ? p.jw[r] : 1.f;
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          szz[i] = fmaf(w * z1[i], z1[i], szz[i]);
+          v[i] = 2.f * A[i].d2 * w * z1[i] * tb[i];
+        }
+        put4(oz + (size_t)r * ldo, v, mx1);
+      }
+      float vt[4], v0[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        vt[i] = A[i].d1 * tb[i];
+        v0[i] = A[i].d1 * hb0[i] + (A[i].d2 * zt[i] + A[i].d3 * szz[i]) * tb[i];
+        const float top = A[i].d1 * zt[i] + A[i].d2 * szz[i];
+        dwp[i] += gfn * A[i].d0 + p.c * go * top;
+      }
+      put4(p.out + (row + p.P - 1) * ldo + m, vt, mxt);
+      put4(p.out + row * ldo + m, v0, mx0);
     }
-    put(p.out + (row + p.P - 1) * ldo + m, A.d1 * tb, mxt);
-    put(p.out + row * ldo + m, A.d1 * hb0 + (A.d2 * zt + A.d3 * szz) * tb, mx0);
-    const float top = A.d1 * zt + A.d2 * szz;
-    dwp += gfn * A.d0 + p.c * go * top;
-  }
-  p.dw_part[(size_t)g * p.width + m] = dwp;
+    *reinterpret_cast<float4*>(p.dw_part + (size_t)g * p.width + m) = make_float4(dwp[0], dwp[1], dwp[2], dwp[3]);
   }
   if constexpr (F16) {  // every lane reaches here (the record is per slot type)
     warp_max_record(mx0, &p.f16_out->maxabs[0]);
@@ -178,29 +202,6 @@ __global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const float* __restr
       zb[2 * l] = G[2 * l + 1] * __uint_as_float(rec[l - 1].maxabs[1]);
       zb[2 * l + 1] = G[2 * l + 1] * __uint_as_float(rec[l - 1].maxabs[2]);
     }
-  }
-}
-
-// out[1] = ||W^T||_inf = max_k sum_m |W[m, k]| of bf16 planes [3][rows, cols], out[0] = the
-// forward factor 2^-(sa+11) (the adjoint reads the same scaled fp16 planes, transposed)
-__global__ void __launch_bounds__(1024) f16_colnorm_kernel(const uint16_t* __restrict__ Wp, int rows, int cols,
-                                                          const float* __restrict__ fwd_stats, float* __restrict__ out) {
-  __shared__ float red[32];
-  const int64_t n = (int64_t)rows * cols;
-  float best = 0.f;
-  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-    float a = 0.f;
-    for (int r = 0; r < rows; ++r) a += fabsf(planes3_val(Wp, n, (int64_t)r * cols + c));
-    best = fmaxf(best, a);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) best = fmaxf(best, red[k]);
-    out[0] = fwd_stats[0];
-    out[1] = best;
   }
 }
 

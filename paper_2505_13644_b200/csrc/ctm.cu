@@ -182,6 +182,7 @@ struct ctm_mlp {
   ctm::F16Rec* f16zrec = nullptr;
   float* f16bb = nullptr;
   float* f16zb = nullptr;
+  unsigned* f16acc = nullptr;               // [3 (L+1)] weight-statistics accumulators (derive_f16_weights)
   float* eye = nullptr;                     // [256, 256] identity: fixed direction sets as shared V
   bool wgrad_attr[4] = {};                  // dynamic smem attribute set (wgrad_kernel<128|256, f16>)
   struct Tape {
@@ -234,7 +235,7 @@ ctm_status free_all(ctm_mlp* h) {
   F(h->W1p16); F(h->f16w); F(h->f16rec); F(h->f16b);
   for (auto& p : h->Wp16) F(p);
   for (auto& p : h->WTp16) F(p);
-  F(h->f16wT); F(h->f16zrec); F(h->f16bb); F(h->f16zb);
+  F(h->f16wT); F(h->f16zrec); F(h->f16bb); F(h->f16zb); F(h->f16acc);
   F(h->eye);
   F(h->tape.weights); F(h->tape.part); F(h->tape.wpart);
   for (auto& p : h->tape.B) F(p.p);
@@ -1053,10 +1054,20 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       rp.out = tapeB0->p;
       rp.pstride = (int64_t)tapeB0->cap;
       rp.nplanes = h->nplanes;
-      // (fp16x3 training: B_0 in the fp32 mode's three bf16 planes, read only by the layer-1
-      // weight gradient, which runs in the fp32 mode, see backward())
-      if (h->cur_f16) rp.nplanes = 3;
-      launch_seed_random(rp.nplanes, a.N, rp, st);
+      if (h->cur_f16) {  // fp16x3: B_0 with one scale (bounds max|x|, max|v|, max|sigma| at f16b[2..4])
+        launch_maxabs(a.X, a.N * (int64_t)D, h->f16b + 2, st);
+        launch_maxabs(rp.V, (int64_t)rp.S * rp.ldv, h->f16b + 3, st);
+        launches += 2;
+        if (rp.sigma) {
+          launch_maxabs(rp.sigma, (int64_t)D * a.R, h->f16b + 4, st);
+          ++launches;
+        }
+        rp.f16_bounds = h->f16b + 2;
+        rp.vgen = 1.f;
+        rp.f16_out = h->f16rec;
+        rp.f16_uniform = 1;
+      }
+      launch_seed_random(h->nplanes, a.N, rp, st);
       ++launches;
     }
     s = launch_seed(h, a, KORD, pl, 0, a.N, grad ? *tapeB1 : h->blk[2], UT, csum, a.op == OP_BIH_NEST ? D : R, st,
@@ -1095,7 +1106,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
 // wgrad_reduce_kernel (the splits summed in order, cropped into dW). Deterministic.
 ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, int Mout, int64_t rows, int rows_out,
                        int cols_in, float* dW, int acc, cudaStream_t st, const ctm::F16Rec* zrec = nullptr,
-                       const ctm::F16Rec* brec = nullptr, int nplanes = 0) {
+                       const ctm::F16Rec* brec = nullptr) {
   auto& T = h->tape;
   const bool f16 = zrec != nullptr;  // fp16x3 operands (uniform scales zrec / brec)
   const int N = (Kin % 256 == 0) ? 256 : 128;
@@ -1108,7 +1119,7 @@ ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, in
   const int npairs = h->sm_count / 2;
   wp.splits = std::max(1, std::min(npairs / tiles, wp.k_blocks));
   wp.kb_per_split = (wp.k_blocks + wp.splits - 1) / wp.splits;
-  wp.nplanes = nplanes ? nplanes : T.nplanes;
+  wp.nplanes = T.nplanes;
   const int units = tiles * wp.splits;
   ctm_status s = ensure(T.wpart, T.wpart_elems, (size_t)units * 256 * N);
   if (s != CTM_OK) return s;
@@ -1151,14 +1162,13 @@ ctm_status weight_grad(ctm_mlp* h, const Planes& B, int Kin, const Planes& Z, in
 
 // out[m] (=|+=) sum_n Zb[n * P + 0, m] for m < ncols (the bias gradient: bias on slot 0 only)
 ctm_status bias_grad(ctm_mlp* h, const Planes& Z, int ld, int ncols, float* out, int acc, cudaStream_t st,
-                     const ctm::F16Rec* zrec = nullptr, int nplanes = 0) {
+                     const ctm::F16Rec* zrec = nullptr) {
   const int G = 1024;  // point groups: enough independent rows in flight per column
   ctm_status s = ensure(h->tape.part, h->tape.part_elems, (size_t)G * std::max(ncols, 1));
   if (s != CTM_OK) return s;
   ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
   h->last_launches += 2;
-  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Z.p, (int64_t)Z.cap,
-                                                                   nplanes ? nplanes : h->tape.nplanes, nullptr,
+  ctm::colsum_kernel<<<dim3((ncols + 127) / 128, G), 128, 0, st>>>(Z.p, (int64_t)Z.cap, h->tape.nplanes, nullptr,
                                                                    h->tape.N, h->tape.P, ld, ncols, G, h->tape.part,
                                                                    zrec);
   ctm::reduce_groups_kernel<<<(ncols + 31) / 32, dim3(32, 32), 0, st>>>(h->tape.part, G, ncols, ncols, out, acc);
@@ -1197,7 +1207,7 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
   {
     ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
     h->last_launches += 3;
-    const int G = 1024, w = h->wpad[L - 1];
+    const int G = 2048, w = h->wpad[L - 1];  // point groups of top_bwd_kernel (dW_L partial rows)
     s = ensure(T.part, T.part_elems, (size_t)G * w);
     if (s != CTM_OK) return s;
     ctm::TopBwdParams tp{};
@@ -1223,9 +1233,9 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
       tp.bb = h->f16bb;
       tp.s1 = s1, tp.s2 = s2, tp.s3 = s3;
       tp.f16_out = h->f16zrec + (L - 1);
-      ctm::top_bwd_kernel<true><<<dim3(w / 128, G), 128, 0, st>>>(tp);
+      ctm::top_bwd_kernel<true><<<dim3((w + 511) / 512, G), 128, 0, st>>>(tp);
     } else {
-      ctm::top_bwd_kernel<false><<<dim3(w / 128, G), 128, 0, st>>>(tp);
+      ctm::top_bwd_kernel<false><<<dim3((w + 511) / 512, G), 128, 0, st>>>(tp);
     }
     // part rows have stride w (padded); only the widths[L-1] real columns reach dW_L
     ctm::reduce_groups_kernel<<<(h->widths[L - 1] + 31) / 32, dim3(32, 32), 0, st>>>(T.part, G, w, h->widths[L - 1],
@@ -1276,9 +1286,7 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
       if (f16) {  // fp16x3: W_l^T fp16 planes, Z_bar_l's record in, Z_bar_{l-1}'s out (one scale)
         ctm::F16Args fa{};
         fa.in = h->f16zrec + l;
-        // Z_bar_1 (read only by the layer-1 weight and bias gradients) in the fp32 mode's planes
-        fa.out = (l == 2) ? nullptr : h->f16zrec + (l - 1);
-        fa.out_bf16 = (l == 2);
+        fa.out = h->f16zrec + (l - 1);
         fa.wsc = h->f16wT + 2 * l;
         fa.s0 = s0, fa.s1 = s1, fa.s2 = s2, fa.s3 = s3, fa.s4 = s4;
         fa.uniform = 1;
@@ -1293,11 +1301,10 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     cur ^= 1;
   }
   // ---- layer 1: dW_1 = Z_bar_1^T B_0 (B_0 = [x0; u_r; 0]), db_1
-  // (fp16x3 training: Z_bar_1 and B_0 are in the fp32 mode's three bf16 planes, see F16Args::out_bf16)
   s = weight_grad(h, T.B[0], h->k1pad, T.Zb[cur], h->wpad[1], rows, h->widths[1], h->widths[0], dW[0], acc, st,
-                  nullptr, nullptr, f16 ? 3 : 0);
+                  zrec(1), brec(0));
   if (s != CTM_OK) return s;
-  s = bias_grad(h, T.Zb[cur], h->wpad[1], h->widths[1], db[0], acc, st, nullptr, f16 ? 3 : 0);
+  s = bias_grad(h, T.Zb[cur], h->wpad[1], h->widths[1], db[0], acc, st, zrec(1));
   if (s != CTM_OK) return s;
   CTM_CUDA(cudaGetLastError());
   return CTM_OK;
@@ -1312,20 +1319,27 @@ void derive_f16_transposed(ctm_mlp* h, cudaStream_t st) {
     const int l = (int)i + 2, mpad = h->wpad[l], kpad = h->wpad[l - 1];
     const int64_t n = (int64_t)mpad * kpad;
     ctm::transpose_planes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Wp16[i], mpad, kpad, h->WTp16[i]);
-    ctm::f16_colnorm_kernel<<<1, 1024, 0, st>>>(h->Wp[i], mpad, kpad, h->f16w + 2 * l, h->f16wT + 2 * l);
   }
 }
 void derive_f16_weights(ctm_mlp* h, cudaStream_t st) {
   const int L = h->L, ld1 = h->wpad[1];
   {
     const int64_t n = (int64_t)ld1 * h->k1pad;
-    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(h->W1p, ld1, h->k1pad, h->f16w + 2);
+    cudaMemsetAsync(h->f16acc, 0, sizeof(unsigned) * 3 * (L + 1), st);
+    ctm::f16_weight_norms_kernel<<<(unsigned)((ld1 * 32 + 255) / 256), 256, 0, st>>>(h->W1p, ld1, h->k1pad, 0,
+                                                                                    h->f16acc + 3);
+    ctm::f16_weight_stats_kernel<<<1, 1, 0, st>>>(h->f16acc + 3, h->f16w + 2, nullptr);
     ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->W1p, n, h->f16w + 2, h->W1p16);
   }
   for (int l = 2; l <= L - 1; ++l) {
     const int mpad = h->wpad[l], kpad = h->wpad[l - 1];
     const int64_t n = (int64_t)mpad * kpad;
-    ctm::f16_weight_stats_kernel<<<1, 1024, 0, st>>>(h->Wp[l - 2], mpad, kpad, h->f16w + 2 * l);
+    const bool tr = !h->WTp16.empty();  // grad mode: ||W^T||_inf for the adjoint too
+    const int thr = std::max(mpad * 32, tr ? kpad : 0);
+    ctm::f16_weight_norms_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(h->Wp[l - 2], mpad, kpad, tr ? 1 : 0,
+                                                                               h->f16acc + 3 * l);
+    ctm::f16_weight_stats_kernel<<<1, 1, 0, st>>>(h->f16acc + 3 * l, h->f16w + 2 * l,
+                                                  tr ? h->f16wT + 2 * l : nullptr);
     ctm::split_weights_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->Wp[l - 2], n, h->f16w + 2 * l,
                                                                                h->Wp16[l - 2]);
   }
@@ -1370,7 +1384,7 @@ void derive_weights(ctm_mlp* h, const float* const* W, const float* const* b, cu
   // the handle is in that mode; otherwise they are rebuilt when it switches to it
   if (h->prec == CTM_PRECISION_FP16X3) {
     derive_f16_weights(h, st);
-    h->last_launches += 2 * (L - 1);
+    h->last_launches += 3 * (L - 1) + (int)h->WTp16.size();
   } else {
     h->f16_stale = true;
   }
@@ -1497,6 +1511,7 @@ ctm_status ctm_load_mlp(int32_t n_layers, const int32_t* widths, const float* co
     LOAD_CUDA(cudaMalloc(&h->f16zrec, sizeof(ctm::F16Rec) * (n_layers + 1)));
     LOAD_CUDA(cudaMalloc(&h->f16bb, sizeof(float) * 4));
     LOAD_CUDA(cudaMalloc(&h->f16zb, sizeof(float) * 2 * (n_layers + 1)));
+    LOAD_CUDA(cudaMalloc(&h->f16acc, sizeof(unsigned) * 3 * (n_layers + 1)));
   }
   LOAD_CUDA(cudaMalloc(&h->w_out, sizeof(float) * h->wpad[n_layers - 1]));
   LOAD_CUDA(cudaMalloc(&h->b_out, sizeof(float)));
@@ -1748,7 +1763,7 @@ ctm_status ctm_grad_enable(ctm_mlp_t mlp, int32_t enable) {
       return fail(CTM_ECUDA, "cuTensorMapEncodeTiled failed for W^T (fp16)");
     mlp->mapAT16.push_back(mt);
   }
-  if (!mlp->f16_stale) derive_f16_transposed(mlp, 0);
+  if (!mlp->f16_stale) derive_f16_weights(mlp, 0);  // (||W^T||_inf and the transposed fp16 planes too)
   {
     std::vector<float> eye(256 * 256, 0.f);
     for (int i = 0; i < 256; ++i) eye[i * 257] = 1.f;

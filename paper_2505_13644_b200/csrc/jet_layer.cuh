@@ -214,9 +214,6 @@ struct F16Args {
   // max|gf| max|w_L|, sum_r |w_r|, max_r |w_r|} (f16_bwd_prep_kernel)
   const float* zb;
   const float* bb;
-  int out_bf16;       // kBwd2 producing Z_bar_1: write the fp32 mode's three bf16 planes (fp32's
-                      // exponent range for the layer-1 weight gradient, whose features may be
-                      // saturated: adjoints ~1e-20 of the block's largest)
 };
 // the registers an fp16x3 epilogue thread carries: unscale factors of the accumulator per
 // slot type (2^-(sa+11) / scale_in[t]), scales of its output block, running max |output|
@@ -224,7 +221,6 @@ struct F16Ctx {
   float us[kF16Types];
   float os[kF16Types];
   float mx[kF16Types];
-  int out_bf16;  // see F16Args
 };
 // output scale of a slot type from a bound B on |v|: 2^(14 - e), B = m 2^e, m in [0.5, 1), so
 // |v * scale| <= 2^14 < 65504 (fp16 max)
@@ -762,12 +758,8 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
   int s = 0;
   auto put = [&](float v, int type) {
     if constexpr (F16) {
-      if (fc->out_bf16) {
-        ptx::store_planes_off<3>(q0, q1, q2, off, v);
-      } else {
-        ptx::store_f16_off(q0, q1, off, v * fc->os[type]);
-        fc->mx[type] = fmaxf(fc->mx[type], fabsf(v));
-      }
+      ptx::store_f16_off(q0, q1, off, v * fc->os[type]);
+      fc->mx[type] = fmaxf(fc->mx[type], fabsf(v));
     } else {
       ptx::store_planes_off<NPL>(q0, q1, q2, off, v);
     }
@@ -812,12 +804,8 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
   const float z0b = A.d1 * hb0 + A.d2 * szh + (A.d2 * zt + A.d3 * szz) * tb;
   if constexpr (F16) {
     uint16_t* const r0 = p.out + (size_t)row * ld + m;
-    if (fc->out_bf16) {
-      ptx::store_planes<3>(r0, p.pstride, z0b);
-    } else {
-      ptx::store_f16_off(r0, r0 + p.pstride, 0u, z0b * fc->os[0]);
-      fc->mx[0] = fmaxf(fc->mx[0], fabsf(z0b));
-    }
+    ptx::store_f16_off(r0, r0 + p.pstride, 0u, z0b * fc->os[0]);
+    fc->mx[0] = fmaxf(fc->mx[0], fabsf(z0b));
   } else {
     store_out<NPL>(p, (size_t)row * ld + m, z0b);
   }
@@ -1061,7 +1049,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         fcx.us[t] = wsi / f16.in->scale[t];
         fcx.mx[t] = 0.f;
       }
-      fcx.out_bf16 = f16.out_bf16;
       if (f16.out) {
         float rw = f16.rw;
         if (rw < 0.f) {  // weighted sums: the largest sum |w_r| over the direction blocks

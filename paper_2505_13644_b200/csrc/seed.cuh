@@ -599,6 +599,8 @@ struct SeedRandomParams {
   const unsigned* f16_bounds;
   float vgen;
   F16Rec* f16_out;
+  int f16_uniform;       // grad mode (B_0 of fixed sets, fp16x3 training): one scale for all slot types;
+                         // with sigma, f16_bounds[2] = max |sigma| and |u| <= Rv max|sigma| max|v|
 };
 
 // Standard normal draw for counter idx: Box-Muller on two splitmix64 outputs
@@ -619,16 +621,18 @@ __global__ void __launch_bounds__(kSeedThreads) seed_random_kernel(const SeedRan
   float os0 = 1.f, os1 = 1.f, mx0 = 0.f, mx1 = 0.f;
   if (F16) {
     os0 = f16_scale_for(__uint_as_float(p.f16_bounds[0]));
-    os1 = f16_scale_for(p.V ? __uint_as_float(p.f16_bounds[1]) : p.vgen);
+    const float vb = p.V ? __uint_as_float(p.f16_bounds[1]) : p.vgen;
+    os1 = f16_scale_for(p.sigma ? (float)p.Rv * __uint_as_float(p.f16_bounds[2]) * vb : vb);
+    if (p.f16_uniform) os0 = os1 = fminf(os0, os1);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       p.f16_out->scale[0] = os0;
       p.f16_out->scale[1] = os1;
-      for (int t = 2; t < kF16Types; ++t) p.f16_out->scale[t] = 1.f;
+      for (int t = 2; t < kF16Types; ++t) p.f16_out->scale[t] = p.f16_uniform ? os0 : 1.f;
     }
   }
   auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
     if constexpr (F16) {
-      seed_store4_f16(o, idx, a, b, c, d, type == 0 ? os0 : type == 1 ? os1 : 1.f);
+      seed_store4_f16(o, idx, a, b, c, d, type == 0 ? os0 : type == 1 ? os1 : p.f16_uniform ? os0 : 1.f);
       const float mv = max4abs(a, b, c, d);
       if (type == 0) mx0 = fmaxf(mx0, mv); else if (type == 1) mx1 = fmaxf(mx1, mv);
     } else {
@@ -843,17 +847,19 @@ __global__ void split_weights_kernel(const float* __restrict__ W, const float* _
 __device__ __forceinline__ float planes3_val(const uint16_t* Wp, int64_t n, int64_t i) {
   return ptx::bf16_val(Wp[i]) + ptx::bf16_val(Wp[n + i]) + ptx::bf16_val(Wp[2 * n + i]);
 }
-// statistics (one block): out[0] = 2^-(sa + 11) = 1 / (the scale putting max |W| in
-// (2^13, 2^14]), the factor that undoes the planes' scales (split_weights_f16_kernel);
-// out[1] = ||W||_inf = max_m sum_k |W[m, k]| (the bound of jet_layer.cuh f16_out_scales)
-__global__ void __launch_bounds__(1024) f16_weight_stats_kernel(const uint16_t* __restrict__ Wp, int rows, int cols,
-                                                               float* __restrict__ out) {
-  __shared__ float smax[32], ssum[32];
+// Statistics of bf16-plane weights [3][rows, cols], grid-parallel, into acc (float bits,
+// zeroed by the caller; atomicMax of non-negative floats is order-independent, so the result
+// is deterministic): acc[0] = max |W|, acc[1] = ||W||_inf = max_m sum_k |W[m, k]| (one warp per
+// row, lanes strided over k, then a shuffle tree), and with do_cols acc[2] = ||W^T||_inf =
+// max_k sum_m |W[m, k]| (one thread per column; the adjoint's bound, fp16x3 training).
+__global__ void __launch_bounds__(256) f16_weight_norms_kernel(const uint16_t* __restrict__ Wp, int rows, int cols,
+                                                               int do_cols, unsigned* __restrict__ acc) {
   const int64_t n = (int64_t)rows * cols;
-  float mx = 0.f, rs = 0.f;
-  for (int r = threadIdx.x >> 5; r < rows; r += 32) {  // one warp per row
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = gt >> 5, lane = threadIdx.x & 31;
+  if (r < rows) {  // warp-uniform
     float a = 0.f, m = 0.f;
-    for (int c = threadIdx.x & 31; c < cols; c += 32) {
+    for (int c = lane; c < cols; c += 32) {
       const float v = fabsf(planes3_val(Wp, n, (int64_t)r * cols + c));
       a += v;
       m = fmaxf(m, v);
@@ -862,21 +868,27 @@ __global__ void __launch_bounds__(1024) f16_weight_stats_kernel(const uint16_t* 
       a += __shfl_xor_sync(0xffffffffu, a, o);
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     }
-    rs = fmaxf(rs, a);
-    mx = fmaxf(mx, m);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    smax[threadIdx.x >> 5] = mx;
-    ssum[threadIdx.x >> 5] = rs;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 32; ++w) {
-      mx = fmaxf(mx, smax[w]);
-      rs = fmaxf(rs, ssum[w]);
+    if (lane == 0) {
+      atomicMax(acc + 0, __float_as_uint(m));
+      atomicMax(acc + 1, __float_as_uint(a));
     }
-    out[0] = 1.f / f16_scale_for(mx);  // 2^(sa + 11) = the scale putting max|W| in (2^13, 2^14]
-    out[1] = rs;
+  }
+  if (do_cols && gt < cols) {
+    float s = 0.f;
+    for (int rr = 0; rr < rows; ++rr) s += fabsf(planes3_val(Wp, n, (int64_t)rr * cols + gt));
+    atomicMax(acc + 2, __float_as_uint(s));
+  }
+}
+// out[0] = 2^-(sa + 11) = 1 / (the scale putting max |W| in (2^13, 2^14]), the factor that
+// undoes the planes' scales (split_weights_f16_kernel); out[1] = ||W||_inf (the bound of
+// jet_layer.cuh f16_out_scales); outT (grad mode): the same factor and ||W^T||_inf
+__global__ void f16_weight_stats_kernel(const unsigned* __restrict__ acc, float* __restrict__ out,
+                                        float* __restrict__ outT) {
+  out[0] = 1.f / f16_scale_for(__uint_as_float(acc[0]));
+  out[1] = __uint_as_float(acc[1]);
+  if (outT) {
+    outT[0] = out[0];
+    outT[1] = __uint_as_float(acc[2]);
   }
 }
 // fp16x3 weight planes [3][Mpad, Kpad] (zero padding stays zero): p0 = rn_f16(W 2^sa),

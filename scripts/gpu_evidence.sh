@@ -17,9 +17,11 @@ if ! skip tests; then
 fi
 if ! skip bench; then
   timeout 600 python bench.py > $E/bench_laplacian.json 2> $E/bench_laplacian.err
-  for spec in "precision bf16x3" "precision fp16x3" "precision fp16x3 --op weighted" \
-              "precision fp16x3 --op randomized --S 8" "precision fp16x3 --op randomized --S 32" \
-              "precision fp16x3 --op randomized --S 128" \
+  # (the default line is the fp16x3 mode; "precision fp32" lines time the 24-bit mode)
+  for spec in "precision fp32" "precision bf16x3" "precision fp32 --op weighted" \
+              "precision fp32 --op randomized --S 8" "precision fp32 --op randomized --S 32" \
+              "precision fp32 --op randomized --S 128" "precision fp32 --op biharmonic" \
+              "precision fp32 --op laplacian_train" \
               "op weighted" "op standard" "op biharmonic" "op biharmonic_nested" \
               "op randomized --S 8" "op randomized --S 32" "op randomized --S 128" \
               "op stochastic_biharmonic --S 16" "op laplacian_train" "op biharmonic_standard" \
@@ -76,10 +78,12 @@ if ! skip ncu; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:jet_layer -s 3 -c 3 \
     -o $E/prof_layer_c1 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-other-precisions > $E/ncu_layer.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:jet_layer -s 3 -c 3 \
-    -o $E/prof_layer_c1_fp16x3 -f python bench.py --precision fp16x3 --steps 1 --warmup 1 --no-cpu-baseline \
-    --no-other-precisions > $E/ncu_layer_fp16x3.log 2>&1
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $E/launches_laplacian_fp16x3.csv \
-    python bench.py --precision fp16x3 --steps 2 --warmup 1 --no-cpu-baseline --no-other-precisions > /dev/null 2>&1
+    -o $E/prof_layer_c1_fp32 -f python bench.py --precision fp32 --steps 1 --warmup 1 --no-cpu-baseline \
+    --no-other-precisions > $E/ncu_layer_fp32.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $E/launches_laplacian_fp32.csv \
+    python bench.py --precision fp32 --steps 2 --warmup 1 --no-cpu-baseline --no-other-precisions > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:wgrad_kernel -s 2 -c 1 \
+    -o $E/prof_wgrad -f python bench.py --op laplacian_train --steps 1 --warmup 1 --no-cpu-baseline > $E/ncu_wgrad.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:seed -s 1 -c 1 \
     -o $E/prof_seed_c1 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-other-precisions > $E/ncu_seed.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:jet_layer_kernel<.int.6" -s 3 -c 1 \

@@ -10,6 +10,11 @@ for tool in memcheck synccheck; do
     > $S/fp16x3_tests_$tool.txt 2>&1
   echo "fp16x3 tests $tool rc=$? $(grep -E 'ERROR SUMMARY' $S/fp16x3_tests_$tool.txt | tail -1) $(grep -E 'passed|failed' $S/fp16x3_tests_$tool.txt | tail -1)"
 done
+for tool in memcheck synccheck; do  # fp16x3 training (the full-size C1 shard test is left out: hours under memcheck)
+  timeout 1500 $CS --tool $tool --print-limit 20 python -m pytest tests/test_gpu_grad_fp16x3.py -q -p no:cacheprovider \
+    -k "not full_size" > $S/grad16_tests_$tool.txt 2>&1
+  echo "fp16x3 grad tests $tool rc=$? $(grep -E 'ERROR SUMMARY' $S/grad16_tests_$tool.txt | tail -1) $(grep -E 'passed|failed' $S/grad16_tests_$tool.txt | tail -1)"
+done
 for tool in memcheck synccheck racecheck; do
   timeout 1200 $CS --tool $tool --print-limit 20 python scripts/sanitize_smoke.py > $S/smoke_$tool.txt 2>&1
   echo "smoke(fp16x3) $tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $S/smoke_$tool.txt | tail -1)"

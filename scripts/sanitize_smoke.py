@@ -41,6 +41,7 @@ for widths, prec in (([5, 16, 16, 1], "fp32"), ([50, 64, 64, 1], "fp32"), ([50, 
     # differentiable path: forward in grad mode, backward, weight update
     mlp.grad_enable()
     for call in (lambda: mlp.laplacian(X), lambda: mlp.randomized_laplacian(X, S=4, seed=1),
+                 lambda: mlp.weighted_laplacian(X, torch.from_numpy(sigma(D, D)).cuda()),
                  lambda: mlp.directional_sum(X, 2, torch.from_numpy(gaussian_directions(1, 3, D)[0]).cuda(), w)):
         call()
         g = mlp.backward(torch.ones(9, device="cuda"), torch.ones(9, device="cuda"))
