@@ -73,6 +73,12 @@ SCHEMES = {
     # that type: FP16_BOUND = "max" uses the actual max, "bound" a one-layer bound)
     "fp16x3 two-phase, scaled (1 acc)": ("fp16", 2, [(1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)]),
     "fp16x3 two-phase, unscaled (1 acc)": ("fp16u", 2, [(1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)]),
+    # candidates for less operand traffic: the corrections and the main product per K step
+    # (one group of slots per K block), or the two phases per K CHUNK (phase 2 re-reading the
+    # chunk's resident p0 tiles): the 4th entry is the chunk length in K
+    "fp16x3 interleaved, scaled (1 acc)": ("fp16", 2, [(1, 0, 0), (0, 1, 0), (0, 0, 0)]),
+    "fp16x3 two-phase per 256-K chunk (1 acc)": ("fp16", 2, [(1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)], 256),
+    "fp16x3 two-phase per 128-K chunk (1 acc)": ("fp16", 2, [(1, 0, 0), (0, 1, 0), "phase", (0, 0, 0)], 128),
 }
 
 
@@ -84,7 +90,8 @@ def pow2_scale(maxabs, target=14):
 
 
 def gemm(blk, W, scheme, btype=None):
-    kind, planes, prods = scheme
+    kind, planes, prods = scheme[:3]
+    chunk = scheme[3] if len(scheme) > 3 else blk.shape[1]
     kstep = 8 if kind == "tf32" else 16
     sa = sb = None
     if kind == "fp16":
@@ -106,12 +113,13 @@ def gemm(blk, W, scheme, btype=None):
     if "phase" in prods:
         i = prods.index("phase")
         phases = [prods[:i], prods[i + 1:]]
-    for ph in phases:
-        for k0 in range(0, blk.shape[1], kstep):
-            sl = slice(k0, k0 + kstep)
-            for i, j, a in ph:
-                s = B[j][:, sl].astype(np.float64) @ A[i][:, sl].astype(np.float64).T
-                accs[a] = rz32(accs[a].astype(np.float64) + s)
+    for c0 in range(0, blk.shape[1], chunk):
+        for ph in phases:
+            for k0 in range(c0, min(c0 + chunk, blk.shape[1]), kstep):
+                sl = slice(k0, k0 + kstep)
+                for i, j, a in ph:
+                    s = B[j][:, sl].astype(np.float64) @ A[i][:, sl].astype(np.float64).T
+                    accs[a] = rz32(accs[a].astype(np.float64) + s)
     Z = accs[0].astype(np.float64) + accs[1].astype(np.float64)
     if sa is not None:
         Z = (Z * np.exp2(-sb)[:, None] * np.exp2(-sa)[None, :]).astype(np.float32).astype(np.float64)
