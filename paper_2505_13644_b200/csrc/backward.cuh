@@ -150,18 +150,16 @@ __global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict_
 //   zb[2 l], zb[2 l + 1] = bounds of max |z1|, max |z_top| of the saved Z_l, l = 1 .. L-1:
 //   l = 1: max |U| (the fixed directions' images, ubound) and 0 (x2 = 0); l >= 2: ||W_l||_inf
 //   (G[2 l + 1]) times the recorded maxima of B_{l-1}'s first-order and top slots (rec[l-1]).
-__global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const float* __restrict__ gop, const float* __restrict__ gf,
-                                                           int64_t N, const float* __restrict__ w_out, int wl,
+__global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const unsigned* __restrict__ gmax, int has_gf,
+                                                           const float* __restrict__ w_out, int wl,
                                                            float c, const float* __restrict__ jw, int R,
                                                            const unsigned* __restrict__ ubound,
                                                            const float* __restrict__ G, const F16Rec* __restrict__ rec,
                                                            int L, float* __restrict__ bb, float* __restrict__ zb) {
-  __shared__ float red[5][32];
-  float a = 0.f, b = 0.f, w = 0.f, sw = 0.f, mw = 0.f;
-  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-    a = fmaxf(a, fabsf(gop[i]));
-    if (gf) b = fmaxf(b, fabsf(gf[i]));
-  }
+  __shared__ float red[5][32];  // (rows 2..4 used)
+  // max |gop|, max |gf| come from maxabs_kernel (grid-parallel) in gmax[0], gmax[1]
+  const float a = __uint_as_float(gmax[0]), b = has_gf ? __uint_as_float(gmax[1]) : 0.f;
+  float w = 0.f, sw = 0.f, mw = 0.f;
   for (int i = threadIdx.x; i < wl; i += blockDim.x) w = fmaxf(w, fabsf(w_out[i]));
   if (jw)
     for (int i = threadIdx.x; i < R; i += blockDim.x) {
@@ -170,15 +168,11 @@ __global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const float* __restr
     }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
-    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
     w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
     sw += __shfl_xor_sync(0xffffffffu, sw, o);
     mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
   }
   if ((threadIdx.x & 31) == 0) {
-    red[0][threadIdx.x >> 5] = a;
-    red[1][threadIdx.x >> 5] = b;
     red[2][threadIdx.x >> 5] = w;
     red[3][threadIdx.x >> 5] = sw;
     red[4][threadIdx.x >> 5] = mw;
@@ -186,8 +180,6 @@ __global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const float* __restr
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
-      a = fmaxf(a, red[0][k]);
-      b = fmaxf(b, red[1][k]);
       w = fmaxf(w, red[2][k]);
       sw += red[3][k];
       mw = fmaxf(mw, red[4][k]);

@@ -1197,9 +1197,12 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     f16_act_sups(h->act, s0, s1, s2, s3, s4);
     ProfScope ps(h, CTM_KIND_BAUX, 0.0, st);
     CTM_CUDA(cudaMemsetAsync(h->f16zrec, 0, sizeof(ctm::F16Rec) * (L + 1), st));
-    ctm::f16_bwd_prep_kernel<<<1, 1024, 0, st>>>(gop, gf, N, h->w_out, h->wpad[L - 1], T.scale, jw, P - 2, h->f16b,
-                                                 h->f16w, h->f16rec, L, h->f16bb, h->f16zb);
-    ++h->last_launches;
+    CTM_CUDA(cudaMemsetAsync(h->f16b + 5, 0, sizeof(unsigned) * 2, st));  // max |gop|, max |gf|
+    launch_maxabs(gop, N, h->f16b + 5, st);
+    if (gf) launch_maxabs(gf, N, h->f16b + 6, st);
+    ctm::f16_bwd_prep_kernel<<<1, 1024, 0, st>>>(h->f16b + 5, gf != nullptr, h->w_out, h->wpad[L - 1], T.scale, jw,
+                                                 P - 2, h->f16b, h->f16w, h->f16rec, L, h->f16bb, h->f16zb);
+    h->last_launches += gf ? 3 : 2;
   }
   auto zrec = [&](int l) -> const ctm::F16Rec* { return f16 ? h->f16zrec + l : nullptr; };
   auto brec = [&](int l) -> const ctm::F16Rec* { return f16 ? h->f16rec + l : nullptr; };

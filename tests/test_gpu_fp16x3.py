@@ -169,6 +169,25 @@ def test_fp16x3_full_size_sampled(ctm, op, S):
     m.close()
 
 
+def test_fp16x3_c1_every_point(ctm):
+    """The bench's default line exactly: C1 (D = 50, 768-768-512-512), N = 16384, the fp16x3
+    mode, the same seeded weights and points as bench.py -- EVERY point against the fp64
+    oracle (route O1, ~70 s on the box's cores): op at the north_star metric, f(x) to
+    1e-5 max(1, |f|)."""
+    params, onet = _nets(widths_for(50), 0)
+    N = 16384
+    X = points(N, 50, 1)  # bench.py: points(n_glob, D, 1)
+    m = _mlp(ctm, params)
+    got, f = m.laplacian(torch.from_numpy(X).cuda())
+    assert m.last_precision() == "fp16x3"
+    want, fwant, norm = O.laplacian(onet, X.astype(np.float64))
+    e = _check(got.cpu(), want, norm)
+    fe = np.abs(f.double().cpu().numpy() - fwant) / np.maximum(1.0, np.abs(fwant))
+    assert fe.max() <= 1e-5, fe.max()
+    print(f"C1 fp16x3, all {N} points: max err {e:.2e}, f max err {fe.max():.2e}")
+    m.close()
+
+
 @pytest.mark.parametrize("scale", [1e-3, 30.0])
 def test_fp16x3_scales_follow_the_data(ctm, scale):
     """Inputs far from 1 (x scaled by 1e-3 or 30 -- tiny first-order values, or saturated tanh
