@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) colsum_kernel(const uint16_t* __restrict_
 __global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const unsigned* __restrict__ gmax, int has_gf,
                                                            const float* __restrict__ w_out, int wl,
                                                            float c, const float* __restrict__ jw, int R,
-                                                           const unsigned* __restrict__ ubound,
+                                                           const unsigned* __restrict__ ubound, int random,
                                                            const float* __restrict__ G, const F16Rec* __restrict__ rec,
                                                            int L, float* __restrict__ bb, float* __restrict__ zb) {
   __shared__ float red[5][32];  // (rows 2..4 used)
@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(1024) f16_bwd_prep_kernel(const unsigned* __re
     bb[1] = b * w;
     bb[2] = jw ? sw : (float)R;
     bb[3] = jw ? mw : 1.f;
-    zb[2] = __uint_as_float(ubound[0]);
+    // layer 1: fixed sets z1 = U (max |U| in ubound[0]); per-point directions (layer 1 on
+    // the tensor cores, random != 0) z1 = W1 u, bounded by ||W1||_inf max |u| (rec[0])
+    zb[2] = random ? G[3] * __uint_as_float(rec[0].maxabs[1]) : __uint_as_float(ubound[0]);
     zb[3] = 0.f;
     for (int l = 2; l <= L - 1; ++l) {
       zb[2 * l] = G[2 * l + 1] * __uint_as_float(rec[l - 1].maxabs[1]);

@@ -196,6 +196,7 @@ struct ctm_mlp {
     std::vector<Planes> B;                  // B_l, l = 0 .. L-1 (B_0 = layer-1 input block)
     int nplanes = 3;                        // precision the tape was recorded in
     bool f16 = false;                       // recorded in the fp16x3 mode (uniform block scales)
+    bool random = false;                    // per-point directions (layer 1 on the tensor cores)
     std::vector<float*> Z;                  // Z_l, l = 1 .. L-1 (fp32 pre-activations)
     std::vector<size_t> Z_elems;
     Planes Zb[2];
@@ -848,8 +849,8 @@ ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
 // split point), the streaming seed for fixed sets, and at least one tensor-core layer
 bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, bool grad, int R) {
   if (h->prec != CTM_PRECISION_FP16X3 || (KORD != 2 && KORD != 4) || pl.ppt < 2) return false;
-  // grad mode (fp16x3 training): the K=2 operators of fixed direction sets (uniform block scales)
-  if (grad && (KORD != 2 || random_k2(a) || h->WTp16.empty())) return false;
+  // grad mode (fp16x3 training): the K=2 operators (uniform block scales)
+  if (grad && (KORD != 2 || h->WTp16.empty())) return false;
   if (h->act != ctm::kActTanh && h->act != ctm::kActSin) return false;
   const bool k2op = a.op == OP_LAP || a.op == OP_WLAP || a.op == OP_RLAP || a.op == OP_WLAP_X ||
                     (a.op == OP_DSUM && a.K == 2);
@@ -973,6 +974,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       rp.f16_bounds = h->f16b + 2;
       rp.vgen = a.gaussian ? 6.f : 1.f;  // |Box-Muller draw| <= sqrt(-2 ln 2^-25) = 5.9
       rp.f16_out = h->f16rec;
+      rp.f16_uniform = grad ? 1 : 0;  // fp16x3 training: B_0 feeds the layer-1 weight gradient
     }
     {
       ProfScope ps(h, CTM_KIND_SEED, (double)rows_total * h->k1pad * 2.0 * h->nplanes, st);
@@ -1088,6 +1090,7 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
     T.J = (a.op == OP_DSUM) ? a.J : 0;
     T.nplanes = h->nplanes;
     T.f16 = h->cur_f16;
+    T.random = random_k2(a);
     if (T.weighted) {  // the caller's weights may not outlive the call
       s = ensure(T.weights, T.weights_elems, (size_t)a.J);
       if (s != CTM_OK) return s;
@@ -1201,7 +1204,8 @@ ctm_status backward(ctm_mlp* h, const float* gop, const float* gf, float* const*
     launch_maxabs(gop, N, h->f16b + 5, st);
     if (gf) launch_maxabs(gf, N, h->f16b + 6, st);
     ctm::f16_bwd_prep_kernel<<<1, 1024, 0, st>>>(h->f16b + 5, gf != nullptr, h->w_out, h->wpad[L - 1], T.scale, jw,
-                                                 P - 2, h->f16b, h->f16w, h->f16rec, L, h->f16bb, h->f16zb);
+                                                 P - 2, h->f16b, T.random ? 1 : 0, h->f16w, h->f16rec, L, h->f16bb,
+                                                 h->f16zb);
     h->last_launches += gf ? 3 : 2;
   }
   auto zrec = [&](int l) -> const ctm::F16Rec* { return f16 ? h->f16zrec + l : nullptr; };

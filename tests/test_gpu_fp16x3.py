@@ -74,7 +74,9 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.laplacian(X)
     assert m.last_precision() == "fp16x3"  # fp16x3 training: fixed direction sets
     m.randomized_laplacian(X, S=4, seed=1)
-    assert m.last_precision() == "fp32"  # per-point directions in grad mode run fp32
+    assert m.last_precision() == "fp16x3"  # per-point directions in grad mode too
+    m.randomized_laplacian(X, S=4, seed=1, sigma=torch.from_numpy(make_sigma(5, 5)).cuda())
+    assert m.last_precision() == "fp32"  # sigma: not covered
     m.grad_enable(False)
     m.laplacian(X)
     assert m.last_precision() == "fp16x3"

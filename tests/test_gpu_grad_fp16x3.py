@@ -8,7 +8,9 @@ import numpy as np
 import pytest
 import torch
 
-from synth import gaussian_directions, mlp_params, points, sigma as make_sigma, signed_weights, widths_for
+import oracle as O
+from synth import (gaussian_directions, mlp_params, points, sigma as make_sigma, sigma_field, signed_weights,
+                   widths_for)
 from tests.test_gpu_grad import GTOL, _check_grads, _gs, _k2
 
 pytestmark = pytest.mark.gpu
@@ -35,9 +37,9 @@ def _np64(params):
     return [W.astype(np.float64) for W, _ in params], [b.astype(np.float64) for _, b in params]
 
 
-def test_fp16x3_training_covers_the_fixed_direction_sets(ctm):
-    """Grad mode in the fp16x3 mode: the exact / weighted Laplacians and shared K=2
-    directional sums run fp16x3; per-point directions (randomized, sigma(x)) run fp32."""
+def test_fp16x3_training_covers_the_k2_operators(ctm):
+    """Grad mode in the fp16x3 mode: the exact / weighted Laplacians, K=2 directional sums and
+    the per-point directions (randomized, sigma(x)) run fp16x3; randomized with sigma runs fp32."""
     params = mlp_params([5, 64, 48, 1], 0)
     X = torch.from_numpy(points(9, 5)).cuda()
     m = _mlp(ctm, params)
@@ -46,7 +48,46 @@ def test_fp16x3_training_covers_the_fixed_direction_sets(ctm):
     m.weighted_laplacian(X, torch.from_numpy(make_sigma(5, 3, kind="rect")).cuda())
     assert m.last_precision() == "fp16x3"
     m.randomized_laplacian(X, S=4, seed=1)
+    assert m.last_precision() == "fp16x3"
+    m.randomized_laplacian(X, S=4, seed=1, sigma=torch.from_numpy(make_sigma(5, 5)).cuda())
     assert m.last_precision() == "fp32"
+    m.close()
+
+
+def test_fp16x3_per_point_direction_gradients(ctm):
+    """Per-point directions in grad mode (layer 1 on the tensor cores, B_0 = [x0; u; 0] with
+    one scale): randomized Rademacher / Gaussian (generated in-kernel), sigma(x), per-point
+    K=2 directional sums -- against the fp64 reverse-mode oracle."""
+    widths = [5, 48, 40, 1]
+    params = mlp_params(widths, 0)
+    Ws, bs = _np64(params)
+    D, N = 5, 11
+    X = points(N, D)
+    Xc = torch.from_numpy(X).cuda()
+    Xd = X.astype(np.float64)
+    gop, gf = _gs(N)
+    g_op, g_f = torch.from_numpy(gop).cuda(), torch.from_numpy(gf).cuda()
+    m = _mlp(ctm, params)
+    m.randomized_laplacian(Xc, S=6, seed=3)
+    assert m.last_precision() == "fp16x3"
+    V = O.rademacher(3, 0, N, 6, D)
+    dW, db, mag = _k2(Ws, bs, Xd, V, np.full(6, 1 / 6), gop, gf)
+    _check_grads("fp16x3_randomized", m.backward(g_op, g_f), dW, db, mag)
+    Vg = gaussian_directions(N, 5, D, seed=4)
+    m.randomized_laplacian(Xc, V=torch.from_numpy(Vg).cuda(), dist="gaussian")
+    dW, db, mag = _k2(Ws, bs, Xd, Vg.astype(np.float64), np.full(5, 1 / 5), gop, gf)
+    _check_grads("fp16x3_randomized_gaussian_V", m.backward(g_op, g_f), dW, db, mag)
+    sx = sigma_field(X, 4)
+    m.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())
+    assert m.last_precision() == "fp16x3"
+    dW, db, mag = _k2(Ws, bs, Xd, np.transpose(sx.astype(np.float64), (0, 2, 1)), np.ones(4), gop, gf)
+    _check_grads("fp16x3_pointwise", m.backward(g_op, g_f), dW, db, mag)
+    w = signed_weights(4)
+    dirs = gaussian_directions(N, 4, D, seed=8)
+    m.directional_sum(Xc, 2, torch.from_numpy(dirs).cuda(), torch.from_numpy(w).cuda())
+    assert m.last_precision() == "fp16x3"
+    dW, db, mag = _k2(Ws, bs, Xd, dirs.astype(np.float64), w.astype(np.float64), gop, gf)
+    _check_grads("fp16x3_directional_per_point", m.backward(g_op, g_f), dW, db, mag)
     m.close()
 
 
