@@ -185,11 +185,11 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
  *     tensor time and energy of BF16X3. Covers the collapsed forward
  *     operators of tanh and sin nets with at least two points per MMA tile: K=2
  *     (laplacian, weighted, randomized without sigma, sigma(x), K=2 directional sums) and
- *     K=4 with fixed directions (biharmonic, shared K=4 directional sums), and in grad
+ *     K=4 (biharmonic, stochastic biharmonic, K=4 directional sums), and in grad
  *     mode the whole differentiable path (forward, ctm_backward's adjoint layers and weight
  *     gradients) of the same K=2 operators (one scale per slot block, DESIGN.md §5 "fp16x3
- *     training"); other calls on an FP16X3 handle (randomized with a sigma matrix, per-point
- *     K=4 directions, nested, standard modes, other activations) run in CTM_PRECISION_FP32.
+ *     training"); other calls on an FP16X3 handle (randomized with a sigma matrix, nested,
+ *     standard modes, other activations) run in CTM_PRECISION_FP32.
  * Changing the precision invalidates a recorded tape (ctm_backward then fails).
  * Errors: CTM_EINVAL (NULL handle, unknown value). */
 typedef enum { CTM_PRECISION_FP32 = 0, CTM_PRECISION_BF16X3 = 1, CTM_PRECISION_FP16X3 = 2 } ctm_precision;

@@ -588,10 +588,23 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
     bp.pstride = (int64_t)buf.cap;
     bp.nplanes = h->nplanes;
     bp.act = h->act;
-    if (h->nplanes == 3)
+    if (h->cur_f16) {  // fp16x3: bounds from ||W1||_inf and max |v| (explicit V: f16b[7]; generated: 6)
+      ctm::SeedStochF16 sf{};
+      if (a.V) {
+        launch_maxabs(a.V + p0 * a.S * D, n * (int64_t)a.S * D, h->f16b + 7, st);
+        ++launches;
+        sf.vmax = h->f16b + 7;
+      }
+      sf.g1 = h->f16w + 2;
+      sf.vgen = 6.f;  // |Box-Muller draw| <= sqrt(-2 ln 2^-25) = 5.9
+      f16_act_sups(h->act, sf.s0, sf.s1, sf.s2, sf.s3, sf.s4);
+      sf.out = h->f16rec + 1;
+      ctm::seed_stoch_biharmonic_kernel<2, true><<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp, sf);
+    } else if (h->nplanes == 3) {
       ctm::seed_stoch_biharmonic_kernel<3><<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
-    else
+    } else {
       ctm::seed_stoch_biharmonic_kernel<2><<<(unsigned)blocks, threads, sizeof(float) * a.S * D, st>>>(bp);
+    }
   } else {
     ctm::SeedParams sp{};
     sp.X = a.X + p0 * D;
@@ -854,11 +867,13 @@ bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, b
   if (h->act != ctm::kActTanh && h->act != ctm::kActSin) return false;
   const bool k2op = a.op == OP_LAP || a.op == OP_WLAP || a.op == OP_RLAP || a.op == OP_WLAP_X ||
                     (a.op == OP_DSUM && a.K == 2);
-  // K=4: the fixed interpolation family and shared K=4 directional sums (the per-point K=4
-  // directions' layer 1 runs in fp32 on the CUDA cores, seed_stoch_biharmonic_kernel)
-  const bool k4op = a.op == OP_BIH || (a.op == OP_DSUM && a.K == 4 && !a.per_point);
+  // K=4: the fixed interpolation family, and (session 3) per-point K=4 directions -- the
+  // stochastic biharmonic and per-point K=4 sums, whose layer 1 stays fp32 on the CUDA cores
+  // and writes the fp16x3 planes of its output block
+  const bool k4op = a.op == OP_BIH || a.op == OP_SBIH || (a.op == OP_DSUM && a.K == 4);
   if (!(KORD == 2 ? k2op : k4op)) return false;
   if (random_k2(a)) return a.sigma == nullptr;
+  if (stoch_k4(a)) return h->L >= 3;
   const int D = h->widths[0], ld1 = h->wpad[1];
   return h->L >= 3 && ctm::seed_fixed_smem(D, R, pl.nb) <= 200 * 1024 && ld1 % ctm::kSeedFixedFeats == 0;
 }

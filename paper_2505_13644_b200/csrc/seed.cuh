@@ -491,10 +491,48 @@ struct SeedStochParams {
 
 __device__ __forceinline__ float gaussian_draw(uint64_t seed, uint64_t idx);
 
-template <int NP>
-__global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(const SeedStochParams p) {
+// fp16x3 mode of seed_stoch_biharmonic_kernel (collapsed layout only): ||W1||_inf (g1, from
+// the layer-1 weight statistics), the bound of |v| (vmax: max |V| of explicit directions, or
+// vgen for the generated normals), the activation sups, the block's record. With
+// Z = ||W1||_inf max|v| >= |z1| and Rw = sum_s |w_s|: |h1| <= s1 Z, |h2| <= s2 Z^2,
+// |h3| <= s3 Z^3, |top| <= s4 Rw Z^4, |h0| <= s0 (slot types 1, 3, 4, 2, 0).
+struct SeedStochF16 {
+  const float* g1;
+  const unsigned* vmax;
+  float vgen;
+  float s0, s1, s2, s3, s4;
+  F16Rec* out;
+};
+
+template <int NP, bool F16 = false>
+__global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(const SeedStochParams p,
+                                                                             const SeedStochF16 f = {}) {
   extern __shared__ float vsh[];  // [S, D]
   const PlaneOut o{p.out, p.pstride, p.nplanes};
+  static_assert(!F16 || NP == 2, "fp16x3: two planes");
+  float os[kF16Types], mx[kF16Types];
+#pragma unroll
+  for (int t = 0; t < kF16Types; ++t) os[t] = 1.f, mx[t] = 0.f;
+  if constexpr (F16) {
+    const float Z = f.g1[1] * (f.vmax ? __uint_as_float(*f.vmax) : f.vgen);
+    float rw = 0.f;
+    for (int s = 0; s < p.S; ++s) rw += p.w ? fabsf(p.w[s]) : 1.f;
+    os[0] = f16_scale_for(f.s0);
+    os[1] = f16_scale_for(f.s1 * Z);
+    os[3] = f16_scale_for(f.s2 * Z * Z);
+    os[4] = f16_scale_for(f.s3 * Z * Z * Z);
+    os[2] = f16_scale_for(f.s4 * rw * Z * Z * Z * Z);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int t = 0; t < kF16Types; ++t) f.out->scale[t] = os[t];
+  }
+  auto put4 = [&](size_t idx, float a, float b, float c, float d, int type) {
+    if constexpr (F16) {
+      seed_store4_f16(o, idx, a, b, c, d, os[type]);
+      mx[type] = fmaxf(mx[type], max4abs(a, b, c, d));
+    } else {
+      seed_store4<NP>(o, idx, a, b, c, d);
+    }
+  };
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
@@ -508,7 +546,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
     }
   }
   __syncthreads();
-  if (m >= p.ld) return;
+  if (m < p.ld) {
   const int P = p.standard ? 1 + 4 * p.rb : 3 * p.rb + 2;  // slots per block
   const int st = p.standard ? 4 : 3;                       // rows per sample
   float4 z0 = __ldg(reinterpret_cast<const float4*>(p.b1 + m));
@@ -529,7 +567,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
   }
   for (int b = 0; b < p.blocks; ++b) {
     const size_t row0 = ((size_t)n * p.blocks + b) * P;
-    seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    put4(row0 * p.ld + m, t[0], t[1], t[2], t[3], 0);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int s = b * p.rb; s < (b + 1) * p.rb; ++s) {
       float z[4] = {0.f, 0.f, 0.f, 0.f};
@@ -553,9 +591,9 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
         acc[i] = fmaf((p.w && s < p.S) ? p.w[s] * z2 : z2, z2, acc[i]);
       }
       const size_t r = row0 + 1 + st * (size_t)(s - b * p.rb);
-      seed_store4<NP>(o, r * p.ld + m, h1[0], h1[1], h1[2], h1[3]);
-      seed_store4<NP>(o, (r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3]);
-      seed_store4<NP>(o, (r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3]);
+      put4(r * p.ld + m, h1[0], h1[1], h1[2], h1[3], 1);
+      put4((r + 1) * p.ld + m, h2[0], h2[1], h2[2], h2[3], 3);
+      put4((r + 2) * p.ld + m, h3[0], h3[1], h3[2], h3[3], 4);
       if (p.standard) {  // h4 of this sample = s'''' z1^4   (x2 = x3 = x4 = 0)
         float h4[4];
 #pragma unroll
@@ -564,8 +602,12 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
       }
     }
     if (!p.standard)
-      seed_store4<NP>(o, (row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2],
-                  d4[3] * acc[3]);
+      put4((row0 + P - 1) * p.ld + m, d4[0] * acc[0], d4[1] * acc[1], d4[2] * acc[2], d4[3] * acc[3], 2);
+  }
+  }
+  if constexpr (F16) {  // every thread of the block reaches here (warp-uniform records)
+#pragma unroll
+    for (int t = 0; t < kF16Types; ++t) warp_max_record(mx[t], &f.out->maxabs[t]);
   }
 }
 

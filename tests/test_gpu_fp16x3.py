@@ -65,7 +65,7 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.biharmonic(X)
     assert m.last_precision() == "fp16x3"  # K=4, the interpolation family
     m.stochastic_biharmonic(X, S=3, seed=2)
-    assert m.last_precision() == "fp32"  # per-point K=4 directions: layer 1 on the CUDA cores
+    assert m.last_precision() == "fp16x3"  # per-point K=4 directions: layer 1 fp32, its output fp16x3
     m.biharmonic_nested(X)
     assert m.last_precision() == "fp32"
     m.laplacian_standard(X)
@@ -127,11 +127,18 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
         want, _, norm = O.biharmonic(onet, Xd)
         _check(m.biharmonic(Xc)[0], want, norm)
         assert m.last_precision() == "fp16x3"
-    dirs = gaussian_directions(1, 4, D, seed=9)[0]
     w4 = signed_weights(4)
-    got = m.directional_sum(Xc, 4, torch.from_numpy(dirs).cuda(), torch.from_numpy(w4).cuda())[0]
+    for per_point in (False, True):  # K=4 sums, shared and per-point directions
+        dirs = gaussian_directions(N, 4, D, seed=9) if per_point else gaussian_directions(1, 4, D, seed=9)[0]
+        got = m.directional_sum(Xc, 4, torch.from_numpy(dirs).cuda(), torch.from_numpy(w4).cuda())[0]
+        assert m.last_precision() == "fp16x3"
+        want, _, norm = O.directional_sum(onet, Xd, 4, dirs.astype(np.float64), w4.astype(np.float64))
+        _check(got, want, norm)
+    # the stochastic biharmonic (Eq. 12 stochastic, scale 1/(3S)) with explicit Gaussian V
+    Vb = gaussian_directions(N, 6, D, seed=10)
+    got = m.stochastic_biharmonic(Xc, V=torch.from_numpy(Vb).cuda())[0]
     assert m.last_precision() == "fp16x3"
-    want, _, norm = O.directional_sum(onet, Xd, 4, dirs.astype(np.float64), w4.astype(np.float64))
+    want, _, norm = O.stochastic_biharmonic(onet, Xd, Vb.astype(np.float64))
     _check(got, want, norm)
     m.close()
 
