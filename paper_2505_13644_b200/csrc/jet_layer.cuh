@@ -244,6 +244,20 @@ __device__ __forceinline__ void f16_out_scales(const F16Args& a, float rw, float
   os[3] = os[4] = 1.f;
   if (a.uniform) os[0] = os[1] = os[2] = os[3] = os[4] = fminf(os[0], fminf(os[1], os[2]));
 }
+// The nested rule (epilogue_nested) with ONE scale per block: m = G M bounds every input slot
+// value of the layer (M = the input block's max |value| over all slots, maxabs[0]), so
+// |g'| <= s1 m, |H'| <= s2 m^2 + s1 m, |L'| <= s3 D m^3 + 3 s2 D m^2 + s1 m,
+// |Q'| <= s4 D^2 m^4 + 6 s3 D^2 m^3 + 3 s2 D^2 m^2 + 4 s2 D m^2 + s1 m   (|g|^2 <= D m^2,
+// tr H <= D m, g^T H g <= D^2 m^3, |H|_F^2 <= D^2 m^2, g^T L <= D m^2), |h0| <= s0.
+__device__ __forceinline__ void f16_nest_scales(const F16Args& a, int D, float* os) {
+  const float m = a.wsc[1] * __uint_as_float(a.in->maxabs[0]);
+  const float Dm = (float)D * m, m2 = m * m;
+  const float b = fmaxf(fmaxf(a.s0, a.s1 * m), fmaxf(a.s2 * m2 + a.s1 * m,
+      fmaxf(a.s3 * Dm * m2 + 3.f * a.s2 * Dm * m + a.s1 * m,
+            a.s4 * Dm * Dm * m2 + 6.f * a.s3 * Dm * Dm * m + 3.f * a.s2 * Dm * Dm + 4.f * a.s2 * Dm * m + a.s1 * m)));
+  const float sc = f16_scale_for(b);
+  for (int t = 0; t < kF16Types; ++t) os[t] = sc;
+}
 // The adjoint of the K=2 rule (epilogue_bwd2) with G = ||W^T||_inf and the input adjoint
 // block's maxima Mb[t]: |hb_t| <= G Mb[t] =: H_t (hb = W^T zb per slot), and with Z1, Zt the
 // bounds of the saved z1, z_top, R = P - 2 directions, Rw = sum |w_r|, w = max |w_r|:
@@ -283,7 +297,7 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
                                                int bar_id, float& fpart, float& opart, F16Ctx* fc = nullptr) {
   constexpr int NPL = planes_of<FLAGS>();
   constexpr bool F16 = (FLAGS & kFlagF16) != 0;  // fp16x3: unscale what is read, scale what is stored
-  static_assert(!F16 || KORD == 2 || KORD == 4 || KORD == kBwd2, "fp16x3: K=2 and K=4 collapsed rules only");
+  static_assert(!F16 || KORD == 2 || KORD == 4 || KORD == kBwd2 || KORD == kNest, "fp16x3: K=2 and K=4 collapsed rules only");
   const int P = p.P;
   const int ld = p.ldo;
   constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
@@ -553,27 +567,40 @@ __device__ __forceinline__ void epilogue_point_small(const LayerParams& p, uint3
 //           + 4 s'' g^T L + s' Q
 // (D = 1 gives the K=4 Faa di Bruno row of the cheat sheet.) Register
 // arrays are sized kNestMaxD and indexed with compile-time indices under runtime guards.
-template <int NPL>
+// fp16x3 (F16): every accumulator column is unscaled by us (uniform over the block's slots),
+// every stored value scaled by os and its max |value| recorded in mx[0]
+template <int NPL, bool F16 = false>
 __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t tcol, int64_t row, int m, float bias,
-                                                float wo, float& fpart, float& opart) {
+                                                float wo, float& fpart, float& opart, F16Ctx* fc = nullptr) {
   const int D = p.J;
   const int ld = p.ldo;
-  const float z0 = ptx::tmem_ld1(tcol) + bias;
+  const float us = F16 ? fc->us[0] : 1.f;
+  const float z0 = ptx::tmem_ld1(tcol) * us + bias;
   float g[kNestMaxD];
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a) g[a] = (a < D) ? ptx::tmem_ld1(tcol + 1u + (uint32_t)a) : 0.f;
   ptx::tmem_ld_wait();
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a) g[a] *= us;
+  auto sto = [&](const LayerParams& pp, size_t idx, float v) {
+    if constexpr (F16) {
+      ptx::store_f16_off(pp.out + idx, pp.out + idx + pp.pstride, 0u, v * fc->os[0]);
+      fc->mx[0] = fmaxf(fc->mx[0], fabsf(v));
+    } else {
+      ctm::store_out<NPL>(pp, idx, v);
+    }
+  };
   const ActD A = act_derivs(p.act, z0);
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
   const bool store = !p.readout;
   fpart = wo * t;
-  if (store) store_out<NPL>(p, (size_t)row * ld + m, t);
+  if (store) sto(p, (size_t)row * ld + m, t);
   float gg = 0.f;
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a)
     if (a < D) {
       gg = fmaf(g[a], g[a], gg);
-      if (store) store_out<NPL>(p, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
+      if (store) sto(p, (size_t)(row + 1 + a) * ld + m, d1 * g[a]);
     }
   // Hessian slots, one packed row at a time
   float hg[kNestMaxD];
@@ -589,11 +616,13 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
       for (int b = a; b < kNestMaxD; ++b) hr[b] = (b < D) ? ptx::tmem_ld1(tcol + (uint32_t)(slot + b - a)) : 0.f;
       ptx::tmem_ld_wait();
 #pragma unroll
+      for (int b = a; b < kNestMaxD; ++b) hr[b] *= us;
+#pragma unroll
       for (int b = a; b < kNestMaxD; ++b)
         if (b < D) {
           const float h = hr[b];
           if (store)
-            store_out<NPL>(p, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
+            sto(p, (size_t)(row + slot + b - a) * ld + m, fmaf(d2 * g[a], g[b], d1 * h));
           if (b == a) {
             trH += h;
             HF = fmaf(h, h, HF);
@@ -611,8 +640,11 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
   float Lv[kNestMaxD];
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a) Lv[a] = (a < D) ? ptx::tmem_ld1(tcol + (uint32_t)(slot + a)) : 0.f;
-  const float zq = ptx::tmem_ld1(tcol + (uint32_t)(slot + D));
+  float zq = ptx::tmem_ld1(tcol + (uint32_t)(slot + D));
   ptx::tmem_ld_wait();
+  zq *= us;
+#pragma unroll
+  for (int a = 0; a < kNestMaxD; ++a) Lv[a] *= us;
   float gL = 0.f, gHg = 0.f;
 #pragma unroll
   for (int a = 0; a < kNestMaxD; ++a)
@@ -621,27 +653,32 @@ __device__ __forceinline__ void epilogue_nested(const LayerParams& p, uint32_t t
       gHg = fmaf(g[a], hg[a], gHg);
       if (store) {
         const float v = d3 * g[a] * gg + 2.f * d2 * hg[a] + d2 * g[a] * trH + d1 * Lv[a];
-        store_out<NPL>(p, (size_t)(row + slot + a) * ld + m, v);
+        sto(p, (size_t)(row + slot + a) * ld + m, v);
       }
     }
   const float q = d4 * gg * gg + 2.f * d3 * gg * trH + 4.f * d3 * gHg + 2.f * d2 * HF + d2 * trH * trH +
                   4.f * d2 * gL + d1 * zq;
   opart = wo * q;
-  if (store) store_out<NPL>(p, (size_t)(row + slot + D) * ld + m, q);
+  if (store) sto(p, (size_t)(row + slot + D) * ld + m, q);
 }
 
 // The same rule with D known at compile time (D <= 8, P <= 54): the point's P columns
 // are read with one burst of x16/x8/x4/x2/x1 loads and a single wait, and every slot
 // index is a constant, so the whole point lives in registers.
-template <int D, int NPL>
+template <int D, int NPL, bool F16 = false>
 __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t tcol, int64_t row, int m,
-                                                  float bias, float wo, float& fpart, float& opart) {
+                                                  float bias, float wo, float& fpart, float& opart,
+                                                  F16Ctx* fc = nullptr) {
   constexpr int T = D * (D + 1) / 2;
   constexpr int P = 2 + 2 * D + T;
   constexpr int oH = 1 + D, oL = 1 + D + T;
   float v[P];
   ptx::tmem_ld_cols<P>(tcol, v);
   ptx::tmem_ld_wait();
+  if constexpr (F16) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) v[i] *= fc->us[0];
+  }
   const int ld = p.ldo;
   const ActD A = act_derivs(p.act, v[0] + bias);
   const float t = A.d0, d1 = A.d1, d2 = A.d2, d3 = A.d3, d4 = A.d4;
@@ -680,7 +717,14 @@ __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t
   opart = wo * q;
   if (p.readout) return;
   uint16_t* po = p.out + (size_t)row * ld + m;
-  auto put = [&](size_t off, float v) { ptx::store_planes<NPL>(po + off, p.pstride, v); };
+  auto put = [&](size_t off, float v) {
+    if constexpr (F16) {
+      ptx::store_f16_off(po + off, po + off + p.pstride, 0u, v * fc->os[0]);
+      fc->mx[0] = fmaxf(fc->mx[0], fabsf(v));
+    } else {
+      ptx::store_planes<NPL>(po + off, p.pstride, v);
+    }
+  };
   put(0, t);
 #pragma unroll
   for (int a = 0; a < D; ++a) put((size_t)(1 + a) * ld, d1 * g[a]);
@@ -697,19 +741,20 @@ __device__ __forceinline__ void epilogue_nested_d(const LayerParams& p, uint32_t
   put((size_t)(P - 1) * ld, q);
 }
 
-template <int NPL>
+template <int NPL, bool F16 = false>
 __device__ __forceinline__ void epilogue_nested_any(const LayerParams& p, uint32_t tcol, int64_t row, int m,
-                                                    float bias, float wo, float& fpart, float& opart) {
+                                                    float bias, float wo, float& fpart, float& opart,
+                                                    F16Ctx* fc = nullptr) {
   switch (p.J) {
-    case 1: epilogue_nested_d<1, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 2: epilogue_nested_d<2, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 3: epilogue_nested_d<3, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 4: epilogue_nested_d<4, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 5: epilogue_nested_d<5, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 6: epilogue_nested_d<6, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 7: epilogue_nested_d<7, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    case 8: epilogue_nested_d<8, NPL>(p, tcol, row, m, bias, wo, fpart, opart); break;
-    default: epilogue_nested<NPL>(p, tcol, row, m, bias, wo, fpart, opart);
+    case 1: epilogue_nested_d<1, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 2: epilogue_nested_d<2, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 3: epilogue_nested_d<3, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 4: epilogue_nested_d<4, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 5: epilogue_nested_d<5, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 6: epilogue_nested_d<6, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 7: epilogue_nested_d<7, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    case 8: epilogue_nested_d<8, NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc); break;
+    default: epilogue_nested<NPL, F16>(p, tcol, row, m, bias, wo, fpart, opart, fc);
   }
 }
 
@@ -1063,6 +1108,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           f16_out_scales4(f16, rw, fcx.os);
         else if (KORD == kBwd2)
           f16_bwd_scales(f16, p.P - 2, fcx.os);
+        else if (KORD == kNest)
+          f16_nest_scales(f16, p.J, fcx.os);
         else
           f16_out_scales(f16, rw, fcx.os);
         if (blockIdx.x == 0 && threadIdx.x == 64)
@@ -1105,8 +1152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         // only warp group 0 works on it
         for (int pt = g; pt < npts; pt += EG) {
           float fpart, opart;
-          epilogue_nested_any<NPL>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo, fpart,
-                              opart);
+          epilogue_nested_any<NPL, F16>(p, tbase + (uint32_t)(pt * p.P), row0 + (int64_t)pt * p.P, m, bias, wo,
+                                        fpart, opart, fc);
           if (p.readout) {
             fpart = warp_sum(fpart);
             opart = warp_sum(opart);

@@ -127,11 +127,16 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 // features, so loads are float4 and the bf16-pair stores are 8 bytes wide. Direction
 // block b of the point gets its own slot group [h0; its directions; its partial top], with
 // zero rows for the padding of the last block.
-template <int KORD, int NP>
+template <int KORD, int NP, bool F16 = false>
 // (min blocks per SM: the register budget of the single-block kernel, which this store-bound
 // kernel needs for its occupancy: 40 registers for K=2 / standard, 48 for K=4 / nested)
+// F16 (kNest only): the fp16x3 planes of the nested block with ONE scale (every slot type),
+// from the bounds U = max|U| = f.bounds[0], C = max|csum| = f.bounds[1] (C = max |g|^2):
+// |h0| <= s0, |g| <= s1 U, |H| <= s2 U^2, |L| <= s3 U C, |Q| <= s4 C^2; the block's record
+// holds the max |value| over all slots in maxabs[0] (jet_layer.cuh f16_nest_scales)
 __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6 : 5)
-    seed_layer_kernel(const SeedParams p) {
+    seed_layer_kernel(const SeedParams p, const SeedF16 f = {}) {
+  static_assert(!F16 || (KORD == kNest && NP == 2), "fp16x3 seed_layer_kernel: the nested block");
   const PlaneOut o{p.out, p.pstride, p.nplanes};
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
@@ -249,29 +254,42 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
     // nested biharmonic, layer 1 (one block): g_a = W1[:, a] = UT[a] and H = L = Q = 0 at
     // the input, so h_a = s' g_a, H'_ab = s'' g_a g_b, L'_a = s''' g_a |g|^2,
     // Q' = s'''' |g|^4 (the epilogue rule of jet_layer.cuh with H = L = Q = 0); |g|^2 = csum.
+    float os = 1.f, mx = 0.f;
+    if constexpr (F16) {
+      const float U = __uint_as_float(f.bounds[0]), C = __uint_as_float(f.bounds[1]);
+      os = f16_scale_for(fmaxf(fmaxf(f.s0, f.s1 * U), fmaxf(f.s2 * U * U, fmaxf(f.s3 * U * C, f.s4 * C * C))));
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int t2 = 0; t2 < kF16Types; ++t2) f.out->scale[t2] = os;
+    }
+    auto putn = [&](size_t idx, float a, float b, float c, float d) {
+      if constexpr (F16) {
+        seed_store4_f16(o, idx, a, b, c, d, os);
+        mx = fmaxf(mx, max4abs(a, b, c, d));
+      } else {
+        seed_store4<NP>(o, idx, a, b, c, d);
+      }
+    };
     const size_t row0 = (size_t)n * p.P;
-    seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    putn(row0 * p.ld + m, t[0], t[1], t[2], t[3]);
     const float4 cs = ldg4(p.csum + m);
     size_t r = row0 + 1;
     for (int a = 0; a < p.R; ++a, ++r) {
       const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
-      seed_store4<NP>(o, r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
+      putn(r * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
     }
     for (int a = 0; a < p.R; ++a) {
       const float4 ua = ldg4(p.UT + (size_t)a * p.ld + m);
       for (int c = a; c < p.R; ++c, ++r) {
         const float4 uc = ldg4(p.UT + (size_t)c * p.ld + m);
-        seed_store4<NP>(o, r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y,
-                    d2[2] * ua.z * uc.z, d2[3] * ua.w * uc.w);
+        putn(r * p.ld + m, d2[0] * ua.x * uc.x, d2[1] * ua.y * uc.y, d2[2] * ua.z * uc.z, d2[3] * ua.w * uc.w);
       }
     }
     for (int a = 0; a < p.R; ++a, ++r) {
       const float4 u = ldg4(p.UT + (size_t)a * p.ld + m);
-      seed_store4<NP>(o, r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z,
-                  d3[3] * u.w * cs.w);
+      putn(r * p.ld + m, d3[0] * u.x * cs.x, d3[1] * u.y * cs.y, d3[2] * u.z * cs.z, d3[3] * u.w * cs.w);
     }
-    seed_store4<NP>(o, r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z,
-                d4[3] * cs.w * cs.w);
+    putn(r * p.ld + m, d4[0] * cs.x * cs.x, d4[1] * cs.y * cs.y, d4[2] * cs.z * cs.z, d4[3] * cs.w * cs.w);
+    if constexpr (F16) warp_max_record(mx, &f.out->maxabs[0]);
   } else {
     CTM_BLOCK_BEGIN
     auto jet = [&](const float4 u, int j) {

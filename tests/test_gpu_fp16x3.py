@@ -67,7 +67,7 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.stochastic_biharmonic(X, S=3, seed=2)
     assert m.last_precision() == "fp16x3"  # per-point K=4 directions: layer 1 fp32, its output fp16x3
     m.biharmonic_nested(X)
-    assert m.last_precision() == "fp32"
+    assert m.last_precision() == "fp16x3"  # the nested Laplacians: one scale per block
     m.laplacian_standard(X)
     assert m.last_precision() == "fp32"
     m.grad_enable()
@@ -123,9 +123,11 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
         assert m.last_precision() == "fp16x3"
         want, _, norm = O.directional_sum(onet, Xd, 2, dirs.astype(np.float64), w.astype(np.float64))
         _check(got, want, norm)
-    if D <= 7:  # K=4: the biharmonic family and a shared K=4 directional sum
+    if D <= 7:  # K=4: the biharmonic family and a shared K=4 directional sum; nested Laplacians
         want, _, norm = O.biharmonic(onet, Xd)
         _check(m.biharmonic(Xc)[0], want, norm)
+        assert m.last_precision() == "fp16x3"
+        _check(m.biharmonic_nested(Xc)[0], want, norm)
         assert m.last_precision() == "fp16x3"
     w4 = signed_weights(4)
     for per_point in (False, True):  # K=4 sums, shared and per-point directions
@@ -144,12 +146,13 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
 
 
 @pytest.mark.parametrize("op,S", [("laplacian", 0), ("weighted", 0), ("randomized", 8), ("randomized", 32),
-                                  ("randomized", 128), ("biharmonic", 0)])
+                                  ("randomized", 128), ("biharmonic", 0), ("biharmonic_nested", 0),
+                                  ("stochastic_biharmonic", 16)])
 def test_fp16x3_full_size_sampled(ctm, op, S):
     """BASELINE C1 / C2 / C3 / C4 at N = 16384 in the bench's launch configuration (the bench's
     default mode), 256 sampled points at every position inside a tile; op at the north_star
     metric and f(x) to 1e-5 max(1, |f|)."""
-    D = 5 if op == "biharmonic" else 50
+    D = 5 if "biharmonic" in op else 50
     params, onet = _nets(widths_for(D), 0)
     N = 16384
     X = points(N, D)
@@ -167,6 +170,13 @@ def test_fp16x3_full_size_sampled(ctm, op, S):
     elif op == "biharmonic":
         got, f = m.biharmonic(Xc)
         want, fwant, norm = O.biharmonic(onet, Xs)
+    elif op == "biharmonic_nested":
+        got, f = m.biharmonic_nested(Xc)
+        want, fwant, norm = O.biharmonic(onet, Xs)
+    elif op == "stochastic_biharmonic":  # explicit Gaussian directions (the oracle needs them)
+        Vb = gaussian_directions(N, S, D, seed=5)
+        got, f = m.stochastic_biharmonic(Xc, V=torch.from_numpy(Vb).cuda())
+        want, fwant, norm = O.stochastic_biharmonic(onet, Xs, Vb[idx].astype(np.float64))
     else:
         got, f = m.randomized_laplacian(Xc, S=S, seed=2)
         V = np.concatenate([O.rademacher(2, int(n), 1, S, 50) for n in idx])
