@@ -393,7 +393,8 @@ template <int KORD, int FLAGS>
 ctm_status launch_layer_kernel(ctm_mlp* h, int64_t grid, const CUtensorMap& amap, const CUtensorMap& bmap,
                                const ctm::LayerParams& lp, cudaStream_t st, const ctm::F16Args& fa = {}) {
   if constexpr (KORD == 2 || (KORD == 4 && FLAGS == 0) || (KORD == ctm::kBwd2 && FLAGS == 0) ||
-                (KORD == ctm::kNest && FLAGS == 0)) {
+                (KORD == ctm::kNest && FLAGS == 0) || (KORD == ctm::kStd2 && FLAGS == 0) ||
+                (KORD == ctm::kStd4 && FLAGS == 0)) {
     if (fa.wsc) return launch_layer_instance<KORD, FLAGS | ctm::kFlagF16>(h, grid, amap, bmap, lp, st, fa);
   }
   if (fa.wsc) return fail(CTM_EUNSUPPORTED, "fp16x3: collapsed K=2 / K=4 layers and the K=2 adjoint only");
@@ -703,7 +704,18 @@ ctm_status launch_seed(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, 
       ctm::seed_layer_kernel<ctm::kNest, 2, true><<<(unsigned)blocks, threads, 0, st>>>(sp, sf);
     } else if (KORD == ctm::kNest)
       CTM_SEED(ctm::kNest);
-    else if (KORD == ctm::kStd4)
+    else if ((KORD == ctm::kStd4 || KORD == ctm::kStd2) && h->cur_f16) {  // fp16x3: bound max|U| of this call
+      launch_maxabs(UT, (int64_t)R * ld1, h->f16b, st);
+      ++launches;
+      ctm::SeedF16 sf{};
+      sf.bounds = h->f16b;
+      f16_act_sups(h->act, sf.s0, sf.s1, sf.s2, sf.s3, sf.s4);
+      sf.out = h->f16rec + 1;
+      if (KORD == ctm::kStd4)
+        ctm::seed_layer_kernel<ctm::kStd4, 2, true><<<(unsigned)blocks, threads, 0, st>>>(sp, sf);
+      else
+        ctm::seed_layer_kernel<ctm::kStd2, 2, true><<<(unsigned)blocks, threads, 0, st>>>(sp, sf);
+    } else if (KORD == ctm::kStd4)
       CTM_SEED(ctm::kStd4);
     else
       CTM_SEED(ctm::kStd2);
@@ -813,9 +825,9 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       } else if (KORD == ctm::kNest) {
         s = launch_layer_kernel<ctm::kNest, 0>(h, grid, *am, mb, lp, st, fa);
       } else if (KORD == ctm::kStd4) {
-        s = launch_layer_kernel<ctm::kStd4, 0>(h, grid, *gl.amap, mb, lp, st);
+        s = launch_layer_kernel<ctm::kStd4, 0>(h, grid, *am, mb, lp, st, fa);
       } else {
-        s = launch_layer_kernel<ctm::kStd2, 0>(h, grid, *gl.amap, mb, lp, st);
+        s = launch_layer_kernel<ctm::kStd2, 0>(h, grid, *am, mb, lp, st, fa);
       }
       if (s != CTM_OK) return s;
     }
@@ -871,7 +883,7 @@ ctm_status prepare_tape(ctm_mlp* h, int64_t rows) {
 // operators of tanh / sin nets, random directions without sigma, >= 2 points per tile (no
 // split point), the streaming seed for fixed sets, and at least one tensor-core layer
 bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, bool grad, int R) {
-  if (h->prec != CTM_PRECISION_FP16X3 || (KORD != 2 && KORD != 4 && KORD != ctm::kNest) || pl.ppt < 2) return false;
+  if (h->prec != CTM_PRECISION_FP16X3 || pl.ppt < 2) return false;
   // grad mode (fp16x3 training): the K=2 operators (uniform block scales)
   if (grad && (KORD != 2 || h->WTp16.empty())) return false;
   if (h->act != ctm::kActTanh && h->act != ctm::kActSin) return false;
@@ -883,6 +895,12 @@ bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, b
   const bool k4op = a.op == OP_BIH || a.op == OP_SBIH || (a.op == OP_DSUM && a.K == 4);
   // the nested biharmonic (session 3): one scale per block (seed_layer_kernel<kNest, 2, true>)
   if (KORD == ctm::kNest) return a.op == OP_BIH_NEST && h->L >= 3;
+  // the standard-mode baselines (session 3): the seeds' and epilogues' standard layouts
+  if (KORD == ctm::kStd2 || KORD == ctm::kStd4) {
+    if (h->L < 3) return false;
+    if (a.op == OP_RLAP_STD) return a.sigma == nullptr;
+    return a.op == OP_LAP_STD || a.op == OP_BIH_STD || a.op == OP_SBIH_STD;
+  }
   if (!(KORD == 2 ? k2op : k4op)) return false;
   if (random_k2(a)) return a.sigma == nullptr;
   if (stoch_k4(a)) return h->L >= 3;

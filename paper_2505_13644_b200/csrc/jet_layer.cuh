@@ -244,6 +244,28 @@ __device__ __forceinline__ void f16_out_scales(const F16Args& a, float rw, float
   os[3] = os[4] = 1.f;
   if (a.uniform) os[0] = os[1] = os[2] = os[3] = os[4] = fminf(os[0], fminf(os[1], os[2]));
 }
+// The standard modes (the paper's baselines): per direction / jet, no collapse.
+// K=2 pairs: |h1| <= s1 g1, |h2_r| <= s2 g1^2 + s1 g2 (g_k = G M_k, M2 = the input's type-2
+// maximum); K=4 jets: |h1| <= s1 g1, |h2| <= s2 g1^2 + s1 g2, |h3| <= s3 g1^3 + 3 s2 g1 g2 +
+// s1 g3, |h4| <= s4 g1^4 + 6 s3 g1^2 g2 + 4 s2 g1 g3 + 3 s2 g2^2 + s1 g4 (types 1, 3, 4, 2).
+__device__ __forceinline__ void f16_std_scales(const F16Args& a, bool k4, float* os) {
+  const float G = a.wsc[1];
+  os[0] = f16_scale_for(a.s0);
+  if (!k4) {
+    const float g1 = G * __uint_as_float(a.in->maxabs[1]), g2 = G * __uint_as_float(a.in->maxabs[2]);
+    os[1] = f16_scale_for(a.s1 * g1);
+    os[2] = f16_scale_for(a.s2 * g1 * g1 + a.s1 * g2);
+    os[3] = os[4] = 1.f;
+    return;
+  }
+  const float g1 = G * __uint_as_float(a.in->maxabs[1]), g2 = G * __uint_as_float(a.in->maxabs[3]),
+              g3 = G * __uint_as_float(a.in->maxabs[4]), g4 = G * __uint_as_float(a.in->maxabs[2]);
+  os[1] = f16_scale_for(a.s1 * g1);
+  os[3] = f16_scale_for(a.s2 * g1 * g1 + a.s1 * g2);
+  os[4] = f16_scale_for(a.s3 * g1 * g1 * g1 + 3.f * a.s2 * g1 * g2 + a.s1 * g3);
+  os[2] = f16_scale_for(a.s4 * g1 * g1 * g1 * g1 + 6.f * a.s3 * g1 * g1 * g2 + 4.f * a.s2 * g1 * g3 +
+                        3.f * a.s2 * g2 * g2 + a.s1 * g4);
+}
 // The nested rule (epilogue_nested) with ONE scale per block: m = G M bounds every input slot
 // value of the layer (M = the input block's max |value| over all slots, maxabs[0]), so
 // |g'| <= s1 m, |H'| <= s2 m^2 + s1 m, |L'| <= s3 D m^3 + 3 s2 D m^2 + s1 m,
@@ -297,7 +319,8 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
                                                int bar_id, float& fpart, float& opart, F16Ctx* fc = nullptr) {
   constexpr int NPL = planes_of<FLAGS>();
   constexpr bool F16 = (FLAGS & kFlagF16) != 0;  // fp16x3: unscale what is read, scale what is stored
-  static_assert(!F16 || KORD == 2 || KORD == 4 || KORD == kBwd2 || KORD == kNest, "fp16x3: K=2 and K=4 collapsed rules only");
+  static_assert(!F16 || KORD == 2 || KORD == 4 || KORD == kBwd2 || KORD == kNest || KORD == kStd2 || KORD == kStd4,
+                "fp16x3: an instance without fp16x3 support");
   const int P = p.P;
   const int ld = p.ldo;
   constexpr bool kStd = (KORD == kStd2) || (KORD == kStd4);  // no collapsed top slot
@@ -379,12 +402,18 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
     // standard K=4 mode: per jet (h1, h2, h3, h4), the weighted h4 summed for the readout
     // (cheat-sheet rows k <= 4, per jet); 4 jets per 16 columns
     auto jet4 = [&](float z1, float z2, float z3, float z4) {
-      put(d1 * z1);
-      put(d2 * z1 * z1 + d1 * z2);
-      put(d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3);
+      if constexpr (F16) {  // fp16x3: the jet's coefficients carry the scales of types 1, 3, 4, 2
+        z1 *= fc->us[1];
+        z2 *= fc->us[3];
+        z3 *= fc->us[4];
+        z4 *= fc->us[2];
+      }
+      put(d1 * z1, 1);
+      put(d2 * z1 * z1 + d1 * z2, 3);
+      put(d3 * z1 * z1 * z1 + 3.f * d2 * z1 * z2 + d1 * z3, 4);
       const float h4 = d4 * z1 * z1 * z1 * z1 + 6.f * d3 * z1 * z1 * z2 + 4.f * d2 * z1 * z3 + 3.f * d2 * z2 * z2 +
                        d1 * z4;
-      put(h4);
+      put(h4, 2);
       acc = fmaf(jw[jj], h4, acc);
       ++jj;
     };
@@ -406,10 +435,14 @@ __device__ __forceinline__ void epilogue_point(const LayerParams& p, uint32_t tc
   } else if constexpr (KORD == kStd2) {
     // standard mode: per direction (h1_r, h2_r) with no collapse, 8 pairs per 16 columns
     auto pair = [&](float z1, float z2) {
-      put(d1 * z1);                             // h_{1,r}
+      if constexpr (F16) {  // fp16x3: first- and second-order coefficients, types 1 and 2
+        z1 *= fc->us[1];
+        z2 *= fc->us[2];
+      }
+      put(d1 * z1, 1);                          // h_{1,r}
       const float h2 = fmaf(d2 * z1, z1, d1 * z2);  // h_{2,r} = tanh'' z1^2 + tanh' z2 (Eq. 1)
       acc += h2;
-      put(h2);
+      put(h2, 2);
     };
     const int np = (me - mb) / 2;
     int j = 0;
@@ -1110,6 +1143,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
           f16_bwd_scales(f16, p.P - 2, fcx.os);
         else if (KORD == kNest)
           f16_nest_scales(f16, p.J, fcx.os);
+        else if (KORD == kStd2 || KORD == kStd4)
+          f16_std_scales(f16, KORD == kStd4, fcx.os);
         else
           f16_out_scales(f16, rw, fcx.os);
         if (blockIdx.x == 0 && threadIdx.x == 64)
@@ -1230,7 +1265,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
     if constexpr (F16) {  // this thread's output maxima per slot type into the block's record
       if (f16.out) {
 #pragma unroll
-        for (int t = 0; t < (KORD == 4 ? kF16Types : 3); ++t) {
+        for (int t = 0; t < ((KORD == 4 || KORD == kStd4) ? kF16Types : 3); ++t) {
           float v = fcx.mx[t];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -136,8 +136,37 @@ template <int KORD, int NP, bool F16 = false>
 // holds the max |value| over all slots in maxabs[0] (jet_layer.cuh f16_nest_scales)
 __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6 : 5)
     seed_layer_kernel(const SeedParams p, const SeedF16 f = {}) {
-  static_assert(!F16 || (KORD == kNest && NP == 2), "fp16x3 seed_layer_kernel: the nested block");
   const PlaneOut o{p.out, p.pstride, p.nplanes};
+  static_assert(!F16 || ((KORD == kNest || KORD == kStd2 || KORD == kStd4) && NP == 2),
+                "fp16x3 seed_layer_kernel: the nested block and the standard modes");
+  // fp16x3, standard modes: per slot type from U = max|U| = f.bounds[0]: primal s0 (type 0),
+  // h1 = s' u <= s1 U (1), h2 = s'' u^2 <= s2 U^2 (kStd2: 2, kStd4: 3), h3 <= s3 U^3 (4),
+  // h4 <= s4 U^4 (2)
+  float sos[kF16Types], smx[kF16Types];
+#pragma unroll
+  for (int t2 = 0; t2 < kF16Types; ++t2) sos[t2] = 1.f, smx[t2] = 0.f;
+  if constexpr (F16 && KORD != kNest) {
+    const float U = __uint_as_float(f.bounds[0]);
+    sos[0] = f16_scale_for(f.s0);
+    sos[1] = f16_scale_for(f.s1 * U);
+    if (KORD == kStd2) {
+      sos[2] = f16_scale_for(f.s2 * U * U);
+    } else {
+      sos[3] = f16_scale_for(f.s2 * U * U);
+      sos[4] = f16_scale_for(f.s3 * U * U * U);
+      sos[2] = f16_scale_for(f.s4 * U * U * U * U);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int t2 = 0; t2 < kF16Types; ++t2) f.out->scale[t2] = sos[t2];
+  }
+  auto put4t = [&](size_t idx, float a, float b, float c, float d, int type) {
+    if constexpr (F16 && KORD != kNest) {
+      seed_store4_f16(o, idx, a, b, c, d, sos[type]);
+      smx[type] = fmaxf(smx[type], max4abs(a, b, c, d));
+    } else {
+      seed_store4<NP>(o, idx, a, b, c, d);
+    }
+  };
   const int feats = 4 * blockDim.x;
   const int mchunks = (p.ld + feats - 1) / feats;
   const int64_t n = blockIdx.x / mchunks;
@@ -167,16 +196,15 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
     const size_t row0 = ((size_t)n * p.blocks + b) * p.P;                \
     const int r0 = b * p.rb;                                             \
     const int r1 = (r0 + p.rb < p.R) ? r0 + p.rb : p.R;                  \
-    seed_store4<NP>(o, row0 * p.ld + m, t[0], t[1], t[2], t[3]);
+    put4t(row0 * p.ld + m, t[0], t[1], t[2], t[3], 0);
 #define CTM_BLOCK_END }
   if (KORD == kStd2) {
     CTM_BLOCK_BEGIN
     // standard mode: per direction (h1_r, h2_r) = (tanh' z1, tanh'' z1^2)   (x2 = 0)
     auto pair = [&](const float4 u, int r) {
       const size_t rr = row0 + 1 + 2 * (r - r0);
-      seed_store4<NP>(o, rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w);
-      seed_store4<NP>(o, (rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y,
-                  d2[2] * u.z * u.z, d2[3] * u.w * u.w);
+      put4t(rr * p.ld + m, d1[0] * u.x, d1[1] * u.y, d1[2] * u.z, d1[3] * u.w, 1);
+      put4t((rr + 1) * p.ld + m, d2[0] * u.x * u.x, d2[1] * u.y * u.y, d2[2] * u.z * u.z, d2[3] * u.w * u.w, 2);
     };
     int r = r0;
 #ifndef CTM_SEED_BATCHS
@@ -208,9 +236,9 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
         h[3][i] = d4[i] * z2 * z2;
       }
       const size_t r = row0 + 1 + 4 * (j - r0);
+      constexpr int kType[4] = {1, 3, 4, 2};  // h1, h2, h3, h4
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        seed_store4<NP>(o, (r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3]);
+      for (int k = 0; k < 4; ++k) put4t((r + k) * p.ld + m, h[k][0], h[k][1], h[k][2], h[k][3], kType[k]);
     }
     CTM_BLOCK_END
   } else if (KORD == 2) {
@@ -329,6 +357,10 @@ __global__ void __launch_bounds__(kSeedThreads, (KORD == 2 || KORD == kStd2) ? 6
   }
 #undef CTM_BLOCK_BEGIN
 #undef CTM_BLOCK_END
+  if constexpr (F16 && KORD != kNest) {
+#pragma unroll
+    for (int t2 = 0; t2 < kF16Types; ++t2) warp_max_record(smx[t2], &f.out->maxabs[t2]);
+  }
 }
 
 // Fixed direction sets, K=2 (e_d, sigma columns) and K=4 (the biharmonic family), forward
@@ -616,7 +648,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_stoch_biharmonic_kernel(con
         float h4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) h4[i] = d4[i] * (z[i] * z[i]) * (z[i] * z[i]);
-        seed_store4<NP>(o, (r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3]);
+        put4((r + 3) * p.ld + m, h4[0], h4[1], h4[2], h4[3], 2);  // (type 2: the top's bound covers it)
       }
     }
     if (!p.standard)

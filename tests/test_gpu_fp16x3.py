@@ -69,7 +69,7 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.biharmonic_nested(X)
     assert m.last_precision() == "fp16x3"  # the nested Laplacians: one scale per block
     m.laplacian_standard(X)
-    assert m.last_precision() == "fp32"
+    assert m.last_precision() == "fp16x3"  # the standard-mode baselines too
     m.grad_enable()
     m.laplacian(X)
     assert m.last_precision() == "fp16x3"  # fp16x3 training: fixed direction sets
@@ -136,12 +136,26 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
         assert m.last_precision() == "fp16x3"
         want, _, norm = O.directional_sum(onet, Xd, 4, dirs.astype(np.float64), w4.astype(np.float64))
         _check(got, want, norm)
-    # the stochastic biharmonic (Eq. 12 stochastic, scale 1/(3S)) with explicit Gaussian V
+    # the stochastic biharmonic (Eq. 12 stochastic, scale 1/(3S)) with explicit Gaussian V,
+    # collapsed and standard
     Vb = gaussian_directions(N, 6, D, seed=10)
-    got = m.stochastic_biharmonic(Xc, V=torch.from_numpy(Vb).cuda())[0]
-    assert m.last_precision() == "fp16x3"
     want, _, norm = O.stochastic_biharmonic(onet, Xd, Vb.astype(np.float64))
-    _check(got, want, norm)
+    for std in (False, True):
+        got = m.stochastic_biharmonic(Xc, V=torch.from_numpy(Vb).cuda(), standard=std)[0]
+        assert m.last_precision() == "fp16x3"
+        _check(got, want, norm)
+    # the standard-mode baselines: exact and randomized Laplacian, biharmonic
+    want, _, norm = O.laplacian(onet, Xd)
+    _check(m.laplacian_standard(Xc)[0], want, norm)
+    assert m.last_precision() == "fp16x3"
+    V = O.rademacher(3, 0, N, 6, D)
+    want, _, norm = O.randomized_laplacian(onet, Xd, V)
+    _check(m.randomized_laplacian(Xc, S=6, seed=3, standard=True)[0], want, norm)
+    assert m.last_precision() == "fp16x3"
+    if D <= 7:
+        want, _, norm = O.biharmonic(onet, Xd)
+        _check(m.biharmonic_standard(Xc)[0], want, norm)
+        assert m.last_precision() == "fp16x3"
     m.close()
 
 
