@@ -21,7 +21,11 @@ if ! skip bench; then
   for spec in "precision fp32" "precision bf16x3" "precision fp32 --op weighted" \
               "precision fp32 --op randomized --S 8" "precision fp32 --op randomized --S 32" \
               "precision fp32 --op randomized --S 128" "precision fp32 --op biharmonic" \
-              "precision fp32 --op laplacian_train" \
+              "precision fp32 --op laplacian_train" "precision fp32 --op biharmonic_nested" \
+              "precision fp32 --op stochastic_biharmonic --S 16" "precision fp32 --op standard" \
+              "precision fp32 --op biharmonic_standard" "precision fp32 --op randomized_standard --S 8" \
+              "precision fp32 --op randomized_standard --S 32" \
+              "precision fp32 --op stochastic_biharmonic_standard --S 16" \
               "op weighted" "op standard" "op biharmonic" "op biharmonic_nested" \
               "op randomized --S 8" "op randomized --S 32" "op randomized --S 128" \
               "op stochastic_biharmonic --S 16" "op laplacian_train" "op biharmonic_standard" \
