@@ -852,10 +852,7 @@ __device__ __forceinline__ void epilogue_bwd2(const LayerParams& p, uint32_t tco
   };
   for (; s + kB <= nmid; s += kB) {
     float v[kB], z[kB];
-    if constexpr (kB == 16)
-      ptx::tmem_ld16(tcol + (uint32_t)(1 + s), v);
-    else
-      ptx::tmem_ld8(tcol + (uint32_t)(1 + s), v);
+    ptx::tmem_ld_cols<kB>(tcol + (uint32_t)(1 + s), v);
 #pragma unroll
     for (int i = 0; i < kB; ++i) {
       z[i] = zr[(uint32_t)(1 + s + i) * ldz];
