@@ -189,8 +189,8 @@ ctm_status ctm_set_activation(ctm_mlp_t mlp, ctm_activation act);
  *     mode the whole differentiable path (forward, ctm_backward's adjoint layers and weight
  *     gradients) of the same K=2 operators (one scale per slot block, DESIGN.md §5 "fp16x3
  *     training"), the nested biharmonic (one scale per block) and the standard-mode
- *     baselines; other calls on an FP16X3 handle (randomized with a sigma matrix, the exp /
- *     identity / square activations) run in CTM_PRECISION_FP32.
+ *     baselines; other calls on an FP16X3 handle (the exp / identity / square activations,
+ *     nets with one hidden layer) run in CTM_PRECISION_FP32.
  * Changing the precision invalidates a recorded tape (ctm_backward then fails).
  * Errors: CTM_EINVAL (NULL handle, unknown value). */
 typedef enum { CTM_PRECISION_FP32 = 0, CTM_PRECISION_BF16X3 = 1, CTM_PRECISION_FP16X3 = 2 } ctm_precision;

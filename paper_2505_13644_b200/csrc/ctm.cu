@@ -898,11 +898,10 @@ bool f16_covers(const ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl, b
   // the standard-mode baselines (session 3): the seeds' and epilogues' standard layouts
   if (KORD == ctm::kStd2 || KORD == ctm::kStd4) {
     if (h->L < 3) return false;
-    if (a.op == OP_RLAP_STD) return a.sigma == nullptr;
-    return a.op == OP_LAP_STD || a.op == OP_BIH_STD || a.op == OP_SBIH_STD;
+    return a.op == OP_LAP_STD || a.op == OP_RLAP_STD || a.op == OP_BIH_STD || a.op == OP_SBIH_STD;
   }
   if (!(KORD == 2 ? k2op : k4op)) return false;
-  if (random_k2(a)) return a.sigma == nullptr;
+  if (random_k2(a)) return true;
   if (stoch_k4(a)) return h->L >= 3;
   const int D = h->widths[0], ld1 = h->wpad[1];
   return h->L >= 3 && ctm::seed_fixed_smem(D, R, pl.nb) <= 200 * 1024 && ld1 % ctm::kSeedFixedFeats == 0;
@@ -1014,6 +1013,10 @@ ctm_status run(ctm_mlp* h, const CallArgs& a) {
       ++launches;
       if (a.V) {
         launch_maxabs(a.V, a.N * (int64_t)a.S * a.Rv, h->f16b + 3, st);
+        ++launches;
+      }
+      if (a.sigma) {  // u = sigma v: |u| <= Rv max|sigma| max|v| (seed_random_kernel)
+        launch_maxabs(a.sigma, (int64_t)D * a.Rv, h->f16b + 4, st);
         ++launches;
       }
       rp.f16_bounds = h->f16b + 2;

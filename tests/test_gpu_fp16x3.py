@@ -61,7 +61,7 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.randomized_laplacian(X, S=4, seed=1)
     assert m.last_precision() == "fp16x3"
     m.randomized_laplacian(X, S=4, seed=1, sigma=torch.from_numpy(make_sigma(5, 5)).cuda())
-    assert m.last_precision() == "fp32"  # sigma: not covered
+    assert m.last_precision() == "fp16x3"  # with a sigma matrix too
     m.biharmonic(X)
     assert m.last_precision() == "fp16x3"  # K=4, the interpolation family
     m.stochastic_biharmonic(X, S=3, seed=2)
@@ -76,7 +76,7 @@ def test_fp16x3_covers_the_k2_forward_operators_and_falls_back_otherwise(ctm):
     m.randomized_laplacian(X, S=4, seed=1)
     assert m.last_precision() == "fp16x3"  # per-point directions in grad mode too
     m.randomized_laplacian(X, S=4, seed=1, sigma=torch.from_numpy(make_sigma(5, 5)).cuda())
-    assert m.last_precision() == "fp32"  # sigma: not covered
+    assert m.last_precision() == "fp16x3"
     m.grad_enable(False)
     m.laplacian(X)
     assert m.last_precision() == "fp16x3"
@@ -113,6 +113,12 @@ def test_fp16x3_parity_every_covered_operator(ctm, act, widths, N):
     Vg = np.random.default_rng(2).standard_normal((N, 5, D)).astype(np.float32)
     want, _, norm = O.randomized_laplacian(onet, Xd, Vg.astype(np.float64))
     _check(m.randomized_laplacian(Xc, V=torch.from_numpy(Vg).cuda(), dist="gaussian")[0], want, norm)
+    # with a sigma matrix (Eq. 10 stochastic: u = sigma v), Rademacher v drawn in-kernel
+    sg = make_sigma(D, min(D, 4), kind="rect")
+    Vs = O.rademacher(3, 0, N, 6, sg.shape[1])
+    want, _, norm = O.randomized_laplacian(onet, Xd, Vs, sg.astype(np.float64))
+    _check(m.randomized_laplacian(Xc, S=6, seed=3, sigma=torch.from_numpy(sg).cuda())[0], want, norm)
+    assert m.last_precision() == "fp16x3"
     sx = sigma_field(X, 4)
     want, _, norm = O.weighted_laplacian_pointwise(onet, Xd, sx.astype(np.float64))
     _check(m.weighted_laplacian_pointwise(Xc, torch.from_numpy(sx).cuda())[0], want, norm)

@@ -39,7 +39,7 @@ def _np64(params):
 
 def test_fp16x3_training_covers_the_k2_operators(ctm):
     """Grad mode in the fp16x3 mode: the exact / weighted Laplacians, K=2 directional sums and
-    the per-point directions (randomized, sigma(x)) run fp16x3; randomized with sigma runs fp32."""
+    the per-point directions (randomized with or without sigma, sigma(x)) run fp16x3."""
     params = mlp_params([5, 64, 48, 1], 0)
     X = torch.from_numpy(points(9, 5)).cuda()
     m = _mlp(ctm, params)
@@ -50,7 +50,7 @@ def test_fp16x3_training_covers_the_k2_operators(ctm):
     m.randomized_laplacian(X, S=4, seed=1)
     assert m.last_precision() == "fp16x3"
     m.randomized_laplacian(X, S=4, seed=1, sigma=torch.from_numpy(make_sigma(5, 5)).cuda())
-    assert m.last_precision() == "fp32"
+    assert m.last_precision() == "fp16x3"
     m.close()
 
 
