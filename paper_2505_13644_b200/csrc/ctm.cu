@@ -167,7 +167,7 @@ struct ctm_mlp {
   size_t partial_elems = 0;
   // last plan
   int last_launches = 0, last_P = 0, last_ppt = 0, last_nmma = 0, last_nb = 1, last_rb = 0;
-  bool smem_attr_set[256] = {};  // per (KORD, FLAGS) kernel instance
+  bool smem_attr_set[512] = {};  // per (KORD, FLAGS) kernel instance
   // differentiable path (ctm_grad_enable / ctm_backward)
   bool grad = false;
   std::vector<uint16_t*> WTp;               // W_l^T bf16 planes [3][wpad[l-1], wpad[l]], l = 2..L-1
@@ -357,11 +357,11 @@ struct ProfScope {
 // cudaFuncSetAttribute is per device: tracked per handle (a handle lives on one device)
 template <int KORD, int FLAGS = 0>
 ctm_status set_layer_attr(ctm_mlp* h) {
-  static_assert(KORD < 8 && FLAGS < 32, "smem_attr_set index");
-  if (!h->smem_attr_set[KORD * 32 + FLAGS]) {
+  static_assert(KORD < 8 && FLAGS < 64, "smem_attr_set index");
+  if (!h->smem_attr_set[KORD * 64 + FLAGS]) {
     CTM_CUDA(cudaFuncSetAttribute(ctm::jet_layer_kernel<KORD, FLAGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctm::kLayerSmem));
-    h->smem_attr_set[KORD * 32 + FLAGS] = true;
+    h->smem_attr_set[KORD * 64 + FLAGS] = true;
   }
   return CTM_OK;
 }
@@ -798,6 +798,8 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
       ctm_status s;
       int flags = (lp.weighted ? ctm::kFlagWeighted : 0) | (lp.z_out ? ctm::kFlagSaveZ : 0);
       if (KORD == 2 && flags == 0 && pl.ppt >= 8) flags = ctm::kFlagWide;
+      // a 7-slot ring when the B half-tile fits 104 rows (C1 / C2: 4 points of 52 slots)
+      if (KORD == 2 && flags == 0 && pl.nmma <= 208) flags = ctm::kFlagRing7;
       ctm::F16Args fa{};
       const CUtensorMap* am = gl.amap;
       if (h->cur_f16) {  // fp16x3: this layer's weight planes, its input and output block records
@@ -814,6 +816,9 @@ ctm_status launch_layers(ctm_mlp* h, const CallArgs& a, int KORD, const Plan& pl
         switch (flags) {
           case ctm::kFlagWide:
             s = launch_layer_kernel<2, ctm::kFlagWide>(h, grid, *am, mb, lp, st, fa);
+            break;
+          case ctm::kFlagRing7:
+            s = launch_layer_kernel<2, ctm::kFlagRing7>(h, grid, *am, mb, lp, st, fa);
             break;
           case 0: s = launch_layer_kernel<2, 0>(h, grid, *am, mb, lp, st, fa); break;
           case 1: s = launch_layer_kernel<2, 1>(h, grid, *am, mb, lp, st, fa); break;

@@ -49,20 +49,19 @@ constexpr uint32_t kSwLayout = 2, kSwSBO = 1024;
 // its second phase one slot (p0 again), of the fast mode two slots.
 constexpr int kMaxN = 256;                       // MMA N cap (TMEM columns per accumulator)
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
-#ifdef CTM_EXP_RING7  // experiment: 7 slots of 29 KB (valid for MMA N <= 208 only: C1)
-constexpr int kSlots = 7;
-constexpr int kBTileBytes = 104 * kBK * 2;
-#else
 constexpr int kSlots = 6;                        // 6 x 32 KB ring
 constexpr int kBTileBytes = (kMaxN / 2) * kBK * 2;  // 16 KB: a CTA of the pair stages half of B
-#endif
 constexpr int kSlotBytes = kATileBytes + kBTileBytes;
 constexpr int kStageBytes = kSlotBytes;          // (ring bytes = kSlots * kSlotBytes)
+// kFlagRing7 instances (MMA N <= 208, e.g. C1's 4 points of 52 slots): 7 slots of 29 KB
+constexpr int kSlots7 = 7;
+constexpr int kSlotBytes7 = kATileBytes + 104 * kBK * 2;
+constexpr int kRingBytes = (kSlots * kSlotBytes > kSlots7 * kSlotBytes7) ? kSlots * kSlotBytes : kSlots7 * kSlotBytes7;
 constexpr int kMaxPtsPerTile = 128;              // P >= 2  ->  pts_per_tile <= 128
 constexpr int kMaxJets = 84;                     // K=4: 3J+2 <= 256
 constexpr int kMaxW = 2048;                      // per-direction weights in smem (all blocks of a point)
 constexpr int kLayerThreads = 320;               // warp0 TMA, warp1 MMA, warps2-9 epilogue (2 groups)
-constexpr int kLayerSmem = kSlots * kSlotBytes + 1024 /*align*/ + 256 /*barriers*/ +
+constexpr int kLayerSmem = kRingBytes + 1024 /*align*/ + 256 /*barriers*/ +
                            4 * kMaxPtsPerTile * 2 * 4 /*readout*/ + kMaxW * 4 + 2 * kBM * 4 /*xacc*/;
 constexpr uint32_t kTmemCols = 512;              // 1 CTA/SM; reads past N stay in range
 // Epilogue modes (template parameter KORD): 2 = K=2 collapsed, 4 = K=4 collapsed (weighted
@@ -184,6 +183,9 @@ constexpr int kFlagNP2 = 8;
 // (weights per layer, slot blocks per slot type), products p1*p0 + p0*p1 over the whole K,
 // then p0*p0. Implies two planes.
 constexpr int kFlagF16 = 16;
+// kFlagRing7 (plain K=2, MMA N <= 208): a 7-slot operand ring of 29 KB slots instead of 6 x 32 KB
+// (one more K block of TMA lookahead)
+constexpr int kFlagRing7 = 32;
 template <int FLAGS>
 __host__ __device__ constexpr int planes_of() {
   return (FLAGS & (kFlagNP2 | kFlagF16)) ? 2 : 3;
@@ -951,14 +953,16 @@ template <int KORD, int FLAGS = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, FLAGS>(), 1)
     jet_layer_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const LayerParams p, const F16Args f16) {
+  constexpr int NS = (FLAGS & kFlagRing7) ? kSlots7 : kSlots;        // ring slots
+  constexpr int SB = (FLAGS & kFlagRing7) ? kSlotBytes7 : kSlotBytes;  // bytes per slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kSlots * kSlotBytes);
-  uint64_t* empty_bar = full_bar + kSlots;
-  uint64_t* tmem_full_bar = empty_bar + kSlots;    // [2]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + NS * SB);
+  uint64_t* empty_bar = full_bar + NS;
+  uint64_t* tmem_full_bar = empty_bar + NS;    // [2]
   uint64_t* tmem_empty_bar = tmem_full_bar + 2;    // [2] (used in the leader)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty_bar + 2);
-  float* red = reinterpret_cast<float*>(smem + kSlots * kSlotBytes + 256);  // [4][kMaxPtsPerTile][2]
+  float* red = reinterpret_cast<float*>(smem + NS * SB + 256);  // [4][kMaxPtsPerTile][2]
   float* jw = red + 4 * kMaxPtsPerTile * 2;                                    // [kMaxJets]
   float* xacc = jw + kMaxW;                                                 // [2][128] split-point partials
 
@@ -978,7 +982,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
@@ -1011,14 +1015,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         const int32_t row0 = (int32_t)(nt * p.pts_per_tile * p.P) + (int32_t)rank * half_n;
         for_each_group(NPL, F16, p.k_iters, [&](int phase, int kb, int nslots) {
           for (int pl = 0; pl < nslots; ++pl, ++it) {
-            const uint32_t s = it % kSlots;
-            const uint32_t ph = (it / kSlots) & 1u;
+            const uint32_t s = it % NS;
+            const uint32_t ph = (it / NS) & 1u;
             {
               STAT_T0();
               ptx::mbar_wait(&empty_bar[s], ph ^ 1u);
               STAT_ADD(0);  // producer waits for a free slot
             }
-            uint8_t* st = smem + s * kSlotBytes;
+            uint8_t* st = smem + s * SB;
             if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2u * ((uint32_t)kATileBytes + b_bytes));
             const int k0 = kb * kBK;
             // fp16x3 phase 2: p0 of B with the weights' p0 * 2^11 (plane 2), the scale of the corrections
@@ -1038,7 +1042,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
       const long long tstart = clock64();
 #endif
       const uint32_t idesc = F16 ? ptx::idesc_f16(2 * kBM, (uint32_t)p.n_mma) : ptx::idesc_bf16(2 * kBM, (uint32_t)p.n_mma);
-      // K-major SW128 descriptor of slot 0's A tile (slot s: + s * kSlotBytes >> 4)
+      // K-major SW128 descriptor of slot 0's A tile (slot s: + s * SB >> 4)
       const uint64_t desc0 = ptx::smem_desc_kmajor(ptx::smem_u32(smem), kSwSBO, kSwLayout);
       uint32_t it = 0, local = 0;
       int64_t nt;
@@ -1057,16 +1061,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
         for_each_group(NPL, F16, p.k_iters, [&](int phase, int, int nslots) {
           for (int pl = 0; pl < nslots; ++pl) {
             STAT_T0();
-            ptx::mbar_wait(&full_bar[(it + pl) % kSlots], ((it + pl) / kSlots) & 1u);
+            ptx::mbar_wait(&full_bar[(it + pl) % NS], ((it + pl) / NS) & 1u);
             if (lane == 0) STAT_ADD(2);  // MMA waits for TMA
           }
           ptx::tc_fence_after();
           // descriptors of plane i of this group (A at the slot, B at +kATileBytes); the
           // start-address field is addr >> 4 in the low bits, so a K step of 32 bytes adds 2
           // (the single issuing thread must keep up with one MMA per ~100 tensor cycles)
-          constexpr uint64_t kS = kSlotBytes >> 4;
-          const uint64_t dA0 = desc0 + (it % kSlots) * kS, dA1 = desc0 + ((it + 1) % kSlots) * kS,
-                         dA2 = desc0 + ((it + 2) % kSlots) * kS;
+          constexpr uint64_t kS = SB >> 4;
+          const uint64_t dA0 = desc0 + (it % NS) * kS, dA1 = desc0 + ((it + 1) % NS) * kS,
+                         dA2 = desc0 + ((it + 2) % NS) * kS;
           constexpr uint64_t kB = kATileBytes >> 4;
           if (ptx::elect_one()) {
 #pragma unroll
@@ -1088,7 +1092,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(layer_threads<KORD, 
             acc = 1u;
           }
           for (int pl = 0; pl < nslots; ++pl)  // both CTAs' slots are free once these retire
-            ptx::mma_commit_pair(&empty_bar[(it + pl) % kSlots]);
+            ptx::mma_commit_pair(&empty_bar[(it + pl) % NS]);
           }
           __syncwarp();
           acc = 1u;
